@@ -1,0 +1,247 @@
+/*
+ * megb200.h -- C ABI of the B200 (sm_100a) low-rank MEG hot path.
+ *
+ * Drop-in boundary for the per-iteration path of the reference `specmeg`
+ * package (arXiv 2012.10469).  The reference is pure Python/numpy, so the
+ * FFI a maintainer would bind is ctypes; each entry
+ * point below names the reference function it replaces.
+ *
+ * Conventions
+ *   - All pointers marked (device) are CUDA device pointers on the current
+ *     device; (host) pointers are plain host memory.  Nothing is freed by the
+ *     library that it did not allocate.
+ *   - Tall-skinny blocks (V, U, W, Ritz vectors) are float64, row-major:
+ *     element (i, c) at ptr[i * ld + c]  (a C-contiguous numpy (n, k) array
+ *     has ld = k).
+ *   - Dense operands (M or a dense gradient G) are symmetric n x n row-major
+ *     with leading dimension ld, float64 or float32.
+ *   - Every function returns an int status; on non-zero,
+ *     megb200_last_error() describes it (thread-local).  No C++ exception
+ *     crosses the ABI.  Parameter errors are detected before any launch.
+ *   - Work is enqueued on the stream given to megb200_solver_set_stream
+ *     (default: the legacy default stream); functions that return host
+ *     results synchronise that stream.
+ */
+#ifndef MEGB200_H
+#define MEGB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MEGB200_ABI_VERSION 1
+
+/* status codes ------------------------------------------------------------ */
+enum {
+  MEGB200_OK = 0,
+  MEGB200_ERR_PARAM = 1,     /* -> specmeg.linalg.ParameterError (linalg.py:23-24)     */
+  MEGB200_ERR_LANCZOS = 2,   /* -> specmeg.linalg.LanczosError   (linalg.py:43-52)     */
+  MEGB200_ERR_CUDA = 3,      /* CUDA runtime / launch failure                           */
+  MEGB200_ERR_KEPT_MASS = 4, /* -> AssertionError "kept mass vanished" (meg.py:350)     */
+  MEGB200_ERR_NO_DEVICE = 5  /* no sm_100 device visible                                */
+};
+
+enum { MEGB200_F64 = 0, MEGB200_F32 = 1 };
+
+/* A symmetric linear operator on R^n, applied to n x k blocks:
+ *     A u = scale * Op(u) + L diag(d) L^T u + alpha u
+ * Op is a dense symmetric matrix, a CSR matrix with float64 values, or
+ * absent.  This is the device form of specmeg.linalg.SymmetricOperator
+ * (linalg.py:81-103) for the operators the hot path builds. */
+enum { MEGB200_OP_NONE = 0, MEGB200_OP_DENSE = 1, MEGB200_OP_CSR = 2 };
+
+typedef struct megb200_operator {
+  int32_t kind;          /* MEGB200_OP_*                                      */
+  int32_t dtype;         /* dense only: MEGB200_F64 | MEGB200_F32             */
+  int64_t n;
+  const void* dense;     /* (device) n x n row-major, symmetric               */
+  int64_t ld;            /* leading dimension of dense (elements)             */
+  const int32_t* rowptr; /* (device) CSR row pointers, n + 1                  */
+  const int32_t* col;    /* (device) CSR column indices, nnz                  */
+  const double* val;     /* (device) CSR values, nnz                          */
+  int64_t nnz;
+  double scale;
+  const double* L;       /* (device) n x l row-major low-rank factor, or NULL */
+  int64_t l;
+  int64_t ldl;
+  const double* d;       /* (host) l coefficients                             */
+  double alpha;
+} megb200_operator;
+
+/* The gradient a step consumes: the device form of the reference's
+ * `grad_apply` callable (meg.py:327-335).  grad f is evaluated at the
+ * iterate X_g = (1 - g_eps) Vg diag(g_lam) Vg^T + g_eps/(n - r)(I - Vg Vg^T).
+ *   DENSE       grad u = G u                        (test_meg.py:153 `g @ u`)
+ *   FROBENIUS   grad u = X_g u - M u                (1/2||X - M||_F^2)
+ *   SAMPLED     grad u = P_Omega(X_g - Mobs) u      (1/2 sum_Omega (X_ij - M_ij)^2)
+ *   STOCHASTIC  grad u = X_g u - M u + sigma (A A^T u / b - u / n)
+ *   ZERO        grad u = 0 */
+enum {
+  MEGB200_GRAD_ZERO = 0,
+  MEGB200_GRAD_DENSE = 1,
+  MEGB200_GRAD_FROBENIUS = 2,
+  MEGB200_GRAD_SAMPLED = 3,
+  MEGB200_GRAD_STOCHASTIC = 4
+};
+
+typedef struct megb200_gradient {
+  int32_t kind;          /* MEGB200_GRAD_*                                    */
+  int32_t dtype;         /* dtype of `dense`                                  */
+  int64_t n;
+  const void* dense;     /* (device) G (DENSE) or M (FROBENIUS, STOCHASTIC)   */
+  int64_t ld;
+  const int32_t* rowptr; /* (device) SAMPLED: Omega pattern (symmetric)       */
+  const int32_t* col;
+  const double* obs;     /* (device) SAMPLED: observed M_ij on Omega          */
+  int64_t nnz;
+  const double* gV;      /* (device) X_g factor, n x g_r row-major (ld g_ldv) */
+  int64_t g_r;
+  int64_t g_ldv;
+  const double* g_lam;   /* (host) g_r weights                                */
+  double g_eps;
+  const double* A;       /* (device) STOCHASTIC: n x bsz row-major (ld lda)   */
+  int64_t bsz;
+  int64_t lda;
+  double sigma;
+} megb200_gradient;
+
+/* Structured iterate (meg.py:47-92): V (device) n x r, lam (host) r, eps. */
+typedef struct megb200_iterate {
+  int64_t n;
+  int64_t r;
+  const double* V;
+  int64_t ldv;
+  const double* lam;
+  double eps;
+} megb200_iterate;
+
+/* Eigensolver options: lanczos_top_r(op, r, tol, max_iter, seed, subspace,
+ * restarts) (linalg.py:130-138) plus the block parameters of the device
+ * solver.  Zero / NULL fields take defaults. */
+typedef struct megb200_eig_opts {
+  double tol;            /* residual rule tol * max(1, max|theta|) (linalg.py:214-215); 0 -> 1e-10 */
+  int32_t max_passes;    /* budget in operator passes; 0 -> restarts * basis        */
+  int32_t restarts;      /* 0 -> 12 (linalg.py:137)                                  */
+  int32_t block;         /* block width k; 0 -> solver default                       */
+  int32_t basis;         /* Krylov basis size (svd_subspace); 0 -> solver default    */
+  int32_t keep;          /* thick-restart size; 0 -> basis / 2                       */
+  uint64_t seed;         /* svd_seed: random start / refill directions               */
+  const double* warm;    /* (device) optional warm-start block, n x warm_cols        */
+  int64_t warm_cols;
+  int64_t ld_warm;
+} megb200_eig_opts;
+
+typedef struct megb200_eig_result {
+  double* eigenvalues;    /* (host, r)   theta, non-increasing                       */
+  double* residual_norms; /* (host, r)   ||A x - theta x|| per pair                  */
+  double* eigenvectors;   /* (device)    n x r row-major, ld = ld_vec (NULL: skip)   */
+  int64_t ld_vec;
+  double* ritz_block;     /* (device)    n x block top Ritz vectors for warm start    */
+  int64_t ld_ritz;        /*             (NULL: skip)                                */
+  int32_t passes;         /* out: operator passes executed                           */
+  int32_t restarts;       /* out: thick restarts                                     */
+  double norm_est;        /* out: max(1, max|theta_all|)                             */
+  int32_t ritz_cols;      /* out: columns written to ritz_block (<= 64)              */
+} megb200_eig_result;
+
+/* Result of one MEG step (LowRankStepResult, meg.py:310-324). */
+typedef struct megb200_step_result {
+  double* V_next;         /* (device) n x r, ld = ld_next (caller-allocated)        */
+  int64_t ld_next;
+  double* lam_next;       /* (host, r)                                              */
+  double* y;              /* (host, r+1) exp(mu - mu_1) = top_eigenvalues           */
+  double* mu;             /* (host, r+1) Ritz values of log X - eta grad            */
+  double* residual_norms; /* (host, r+1)                                            */
+  double* ritz_block;     /* (device, optional) n x block warm block for next step  */
+  int64_t ld_ritz;
+  double lambda_r_plus_1; /* y[r]                                                   */
+  double b_r_plus_1;      /* sum(y)                                                 */
+  double shift;           /* mu_1                                                   */
+  double lhs_cheap;       /* certificate (meg.py:222-239)                           */
+  int32_t holds_cheap;
+  double threshold;
+  double gram_err;        /* max |V^T V - I| of V_next                              */
+  int32_t passes;
+  int32_t restarts;
+  int32_t ritz_cols;      /* columns written to ritz_block (<= 64)                  */
+} megb200_step_result;
+
+typedef struct megb200_solver megb200_solver;
+
+/* library ------------------------------------------------------------------ */
+int megb200_abi_version(void);
+const char* megb200_last_error(void);
+/* 0 if a CUDA device of compute capability 10.x is current, else an error. */
+int megb200_device_check(int* sm_count);
+
+/* solver handle: owns the device workspace for dimension n and block/basis
+ * limits (max_block <= 64, max_basis <= 112).  One stream per handle. */
+int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64_t max_lowrank,
+                          int64_t max_nnz, megb200_solver** out);
+void megb200_solver_destroy(megb200_solver* s);
+int megb200_solver_set_stream(megb200_solver* s, void* cuda_stream);
+/* bytes of device workspace held by the handle */
+int64_t megb200_solver_workspace_bytes(const megb200_solver* s);
+
+/* operator application W = A U (SymmetricOperator.apply, linalg.py:93-94;
+ * logmap_operator(...).apply, meg.py:299-305).  U, W: (device) n x k. */
+int megb200_operator_apply(megb200_solver* s, const megb200_operator* op, const double* U, int64_t ldu,
+                           int32_t k, double* W, int64_t ldw);
+
+/* logmap_operator(x, grad_apply, eta).apply (meg.py:287-307): W = (log X - eta grad) U.
+ * The low-rank factors are gathered into the handle's workspace. */
+int megb200_logmap_apply(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta,
+                         const double* U, int64_t ldu, int32_t k, double* W, int64_t ldw);
+
+/* lanczos_top_r (linalg.py:130-241): the r algebraically largest eigenpairs. */
+int megb200_top_r(megb200_solver* s, const megb200_operator* op, int32_t r, const megb200_eig_opts* opts,
+                  megb200_eig_result* out);
+
+/* lowrank_meg_step (meg.py:327-364): one low-rank MEG update + cheap certificate. */
+int megb200_lowrank_meg_step(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta,
+                             double eps_next, const megb200_eig_opts* opts, megb200_step_result* out);
+
+/* certificate_cheap arithmetic (meg.py:222-239), host-only. */
+int megb200_certificate_cheap(double lambda_r_plus_1, double b_r_plus_1, double eps, int64_t n, int64_t r,
+                              double* lhs, int32_t* holds, double* threshold);
+
+/* Objective evaluation from factors:
+ *   FROBENIUS / STOCHASTIC: 1/2 ||X - M||_F^2  (needs ||M||_F^2 and Tr M:
+ *                           pass NaN to have them computed and cached)
+ *   SAMPLED:                1/2 sum_Omega (X_ij - Mobs_ij)^2
+ * X is the gradient's (gV, g_lam, g_eps). */
+int megb200_objective_value(megb200_solver* s, const megb200_gradient* g, double m_norm2, double m_trace,
+                            double* value);
+
+/* ||M||_F^2 and Tr M of a dense symmetric operand. */
+int megb200_dense_stats(megb200_solver* s, const void* M, int32_t dtype, int64_t ld, double* norm2, double* trace);
+
+/* Dual-gap certificate (_dual_gap_core, objectives.py:332-335) for the
+ * Frobenius objective: Tr(X grad) - lambda_min(grad), grad = X - M, with
+ * lambda_min from the block solver on M - X.  Also returns lambda_min. */
+int megb200_dual_gap(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts, double m_trace,
+                     double* gap, double* lambda_min);
+
+/* Seeded synthetic inputs (oracle/inputs.py twins):
+ *   M_ij = sum_k U_ik lam_k U_jk + sigma (g_ij + g_ji) / (2 sqrt(n)),
+ *   g_ij = N(0,1) at counter i*n + j of stream `stream` (float64 or float32 output). */
+int megb200_gen_dense_target(megb200_solver* s, const double* U, int64_t r, const double* lam_host, double sigma,
+                             uint64_t seed, int32_t stream, void* M, int32_t dtype, int64_t ld);
+/* out_ij = scale * N(0,1) at counter base + i*k + j (n x k row-major, ld).  If
+ * round_f32 != 0 the values are rounded through float32. */
+int megb200_gen_gaussian(megb200_solver* s, uint64_t seed, int32_t stream, uint64_t base, int64_t n, int64_t k,
+                         double scale, int32_t round_f32, double* out, int64_t ld);
+
+/* max |V^T V - I| of an n x r block (LowRankIterate validation, meg.py:69-71). */
+int megb200_gram_error(megb200_solver* s, const double* V, int64_t ldv, int32_t r, double* err);
+
+/* counters of the last call (for benchmarks): kernels launched. */
+int64_t megb200_kernel_launches(const megb200_solver* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEGB200_H */

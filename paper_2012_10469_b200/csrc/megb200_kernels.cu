@@ -1,0 +1,1146 @@
+// sm_100a kernels of the low-rank MEG hot path.
+//
+// Streaming kernels (the operand passes) are HBM-bound: the dense operand is
+// read exactly once per pass with coalesced 16-byte streaming loads; the
+// tall-skinny block U is staged through shared memory and broadcast.  The
+// small dense work (Gram/projection reductions, Cholesky, Jacobi
+// Rayleigh-Ritz) runs in float64 with fixed reduction orders so every result
+// is bitwise reproducible run to run (SPEC.md:97 determinism).
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "megb200_internal.h"
+
+namespace megb200 {
+namespace {
+
+constexpr double kTwoPi = 6.283185307179586;
+constexpr double kInv53 = 1.0 / 9007199254740992.0;
+
+__device__ __forceinline__ double gauss_dev(uint64_t key, uint64_t ctr) {
+  const uint64_t b1 = mix64(key + (2 * ctr + 1) * kGolden);
+  const uint64_t b2 = mix64(key + (2 * ctr + 2) * kGolden);
+  const double u1 = ((double)(b1 >> 11) + 1.0) * kInv53;
+  const double u2 = (double)(b2 >> 11) * kInv53;
+  return sqrt(-2.0 * log(u1)) * cos(kTwoPi * u2);
+}
+
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// ===========================================================================
+// K1: dense streamed product, float64 operand.
+//
+// part[s][i][c] = sum_{k in slice s} M[k][i] * U[k][c]   (M symmetric: the
+// k-th row of M supplies column i, so each warp reads 512 contiguous bytes
+// of one operand row per k).  CTA = 8 warps over 64 output rows (2 per
+// lane); warps interleave over k within the slice; U chunks of KC rows are
+// staged in shared memory and read as broadcasts.
+constexpr int kApplyThreads = 256;
+constexpr int KC = 64;          // k rows per staged chunk
+constexpr int kPerWarp = KC / 8; // k rows per warp per chunk
+
+template <int BN, bool VEC>
+__global__ void __launch_bounds__(kApplyThreads, 1)
+    k_dense_apply_f64(const double* __restrict__ M, int64_t ldm, int64_t n, const double* __restrict__ U,
+                      int64_t ldu, int b, double* __restrict__ part, int64_t kslice) {
+  extern __shared__ __align__(16) double sm[];
+  double* Us = sm;              // KC x BN
+  double* red = sm + KC * BN;   // 4 x BN x 64
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row0 = (int64_t)blockIdx.x * 64;
+  const int64_t i = row0 + 2 * lane;
+  const int64_t kbeg = (int64_t)blockIdx.y * kslice;
+  const int64_t kend = min(n, kbeg + kslice);
+
+  double a0[BN], a1[BN];
+#pragma unroll
+  for (int c = 0; c < BN; ++c) a0[c] = a1[c] = 0.0;
+
+  for (int64_t kc = kbeg; kc < kend; kc += KC) {
+    double m0[kPerWarp], m1[kPerWarp];
+#pragma unroll
+    for (int j = 0; j < kPerWarp; ++j) {
+      const int64_t k = kc + warp + 8 * j;
+      m0[j] = 0.0;
+      m1[j] = 0.0;
+      if (k < kend) {
+        const double* p = M + k * ldm + i;
+        if (VEC && i + 1 < n) {
+          const double2 v = ld_stream2(p);
+          m0[j] = v.x;
+          m1[j] = v.y;
+        } else {
+          if (i < n) m0[j] = p[0];
+          if (i + 1 < n) m1[j] = p[1];
+        }
+      }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < KC * BN; idx += kApplyThreads) {
+      const int r = idx / BN, c = idx - r * BN;
+      const int64_t k = kc + r;
+      Us[idx] = (k < kend && c < b) ? U[k * ldu + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPerWarp; ++j) {
+      const double* u = Us + (warp + 8 * j) * BN;
+#pragma unroll
+      for (int c = 0; c < BN; c += 2) {
+        const double2 uu = *reinterpret_cast<const double2*>(u + c);
+        a0[c] = fma(m0[j], uu.x, a0[c]);
+        a0[c + 1] = fma(m0[j], uu.y, a0[c + 1]);
+        a1[c] = fma(m1[j], uu.x, a1[c]);
+        a1[c + 1] = fma(m1[j], uu.y, a1[c + 1]);
+      }
+    }
+  }
+  // fixed-order tree over the 8 warps: (w, w+4) -> (w, w+2) -> (0, 1)
+#pragma unroll
+  for (int half = 4; half >= 1; half >>= 1) {
+    __syncthreads();
+    if (warp >= half && warp < 2 * half) {
+      double* dst = red + (warp - half) * BN * 64;
+#pragma unroll
+      for (int c = 0; c < BN; ++c)
+        *reinterpret_cast<double2*>(dst + c * 64 + 2 * lane) = make_double2(a0[c], a1[c]);
+    }
+    __syncthreads();
+    if (warp < half) {
+      const double* src = red + warp * BN * 64;
+#pragma unroll
+      for (int c = 0; c < BN; ++c) {
+        const double2 v = *reinterpret_cast<const double2*>(src + c * 64 + 2 * lane);
+        a0[c] += v.x;
+        a1[c] += v.y;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int c = 0; c < BN; ++c) *reinterpret_cast<double2*>(red + c * 64 + 2 * lane) = make_double2(a0[c], a1[c]);
+  }
+  __syncthreads();
+  double* out = part + (int64_t)blockIdx.y * n * b;
+  const int rows = (int)min((int64_t)64, n - row0);
+  for (int idx = threadIdx.x; idx < rows * b; idx += kApplyThreads) {
+    const int r = idx / b, c = idx - r * b;
+    out[(row0 + r) * b + c] = red[c * 64 + r];
+  }
+}
+
+// K1 with a float32 operand: 4 rows per lane (16-byte streaming loads) and
+// float32 FMA into per-lane accumulators over the CTA's k-slice (bounded to
+// kF32Slice rows, so at most kF32Slice/8 terms per accumulator); the
+// cross-warp tree and the cross-slice sum run in float64.
+constexpr int kF32Slice = 4096;
+
+template <int BN, bool VEC>
+__global__ void __launch_bounds__(kApplyThreads, 1)
+    k_dense_apply_f32(const float* __restrict__ M, int64_t ldm, int64_t n, const double* __restrict__ U,
+                      int64_t ldu, int b, double* __restrict__ part, int64_t kslice) {
+  extern __shared__ __align__(16) double sm[];
+  float* Us = reinterpret_cast<float*>(sm);          // KC x BN floats
+  double* red = sm + (KC * BN + 1) / 2;              // 4 x BN x 128 doubles
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row0 = (int64_t)blockIdx.x * 128;
+  const int64_t i = row0 + 4 * lane;
+  const int64_t kbeg = (int64_t)blockIdx.y * kslice;
+  const int64_t kend = min(n, kbeg + kslice);
+
+  float s[4][BN];
+#pragma unroll
+  for (int c = 0; c < BN; ++c) s[0][c] = s[1][c] = s[2][c] = s[3][c] = 0.f;
+
+  for (int64_t kc = kbeg; kc < kend; kc += KC) {
+    float4 mv[kPerWarp];
+#pragma unroll
+    for (int j = 0; j < kPerWarp; ++j) {
+      const int64_t k = kc + warp + 8 * j;
+      mv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < kend) {
+        const float* p = M + k * ldm + i;
+        if (VEC && i + 3 < n) {
+          mv[j] = ld_stream4(p);
+        } else {
+          if (i < n) mv[j].x = p[0];
+          if (i + 1 < n) mv[j].y = p[1];
+          if (i + 2 < n) mv[j].z = p[2];
+          if (i + 3 < n) mv[j].w = p[3];
+        }
+      }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < KC * BN; idx += kApplyThreads) {
+      const int r = idx / BN, c = idx - r * BN;
+      const int64_t k = kc + r;
+      Us[idx] = (k < kend && c < b) ? __double2float_rn(U[k * ldu + c]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPerWarp; ++j) {
+      const float* u = Us + (warp + 8 * j) * BN;
+#pragma unroll
+      for (int c = 0; c < BN; c += 4) {
+        const float4 uu = *reinterpret_cast<const float4*>(u + c);
+        s[0][c] = fmaf(mv[j].x, uu.x, s[0][c]);
+        s[0][c + 1] = fmaf(mv[j].x, uu.y, s[0][c + 1]);
+        s[0][c + 2] = fmaf(mv[j].x, uu.z, s[0][c + 2]);
+        s[0][c + 3] = fmaf(mv[j].x, uu.w, s[0][c + 3]);
+        s[1][c] = fmaf(mv[j].y, uu.x, s[1][c]);
+        s[1][c + 1] = fmaf(mv[j].y, uu.y, s[1][c + 1]);
+        s[1][c + 2] = fmaf(mv[j].y, uu.z, s[1][c + 2]);
+        s[1][c + 3] = fmaf(mv[j].y, uu.w, s[1][c + 3]);
+        s[2][c] = fmaf(mv[j].z, uu.x, s[2][c]);
+        s[2][c + 1] = fmaf(mv[j].z, uu.y, s[2][c + 1]);
+        s[2][c + 2] = fmaf(mv[j].z, uu.z, s[2][c + 2]);
+        s[2][c + 3] = fmaf(mv[j].z, uu.w, s[2][c + 3]);
+        s[3][c] = fmaf(mv[j].w, uu.x, s[3][c]);
+        s[3][c + 1] = fmaf(mv[j].w, uu.y, s[3][c + 1]);
+        s[3][c + 2] = fmaf(mv[j].w, uu.z, s[3][c + 2]);
+        s[3][c + 3] = fmaf(mv[j].w, uu.w, s[3][c + 3]);
+      }
+    }
+  }
+  // float64 fixed-order tree over the 8 warps: w += w+4, then w += w+2, then 0 += 1
+  __syncthreads();
+  if (warp >= 4) {
+    double* dst = red + (warp - 4) * BN * 128;
+#pragma unroll
+    for (int c = 0; c < BN; ++c) {
+      *reinterpret_cast<double2*>(dst + c * 128 + 4 * lane) = make_double2(s[0][c], s[1][c]);
+      *reinterpret_cast<double2*>(dst + c * 128 + 4 * lane + 2) = make_double2(s[2][c], s[3][c]);
+    }
+  }
+  __syncthreads();
+  if (warp < 4) {
+    double* dst = red + warp * BN * 128;
+#pragma unroll
+    for (int c = 0; c < BN; ++c) {
+      double2 v0 = *reinterpret_cast<const double2*>(dst + c * 128 + 4 * lane);
+      double2 v1 = *reinterpret_cast<const double2*>(dst + c * 128 + 4 * lane + 2);
+      v0.x = (double)s[0][c] + v0.x;
+      v0.y = (double)s[1][c] + v0.y;
+      v1.x = (double)s[2][c] + v1.x;
+      v1.y = (double)s[3][c] + v1.y;
+      *reinterpret_cast<double2*>(dst + c * 128 + 4 * lane) = v0;
+      *reinterpret_cast<double2*>(dst + c * 128 + 4 * lane + 2) = v1;
+    }
+  }
+#pragma unroll
+  for (int half = 2; half >= 1; half >>= 1) {
+    __syncthreads();
+    if (warp < half) {
+      double* dst = red + warp * BN * 128;
+      const double* src = red + (warp + half) * BN * 128;
+      for (int idx = lane; idx < BN * 128; idx += 32) dst[idx] += src[idx];
+    }
+  }
+  __syncthreads();
+  double* out = part + (int64_t)blockIdx.y * n * b;
+  const int rows = (int)min((int64_t)128, n - row0);
+  for (int idx = threadIdx.x; idx < rows * b; idx += kApplyThreads) {
+    const int r = idx / b, c = idx - r * b;
+    out[(row0 + r) * b + c] = red[c * 128 + r];
+  }
+}
+
+// ===========================================================================
+// K2: CSR product (sampled-entry gradient), one warp per row, lanes over the
+// row's nonzeros gathering U rows; fixed xor-tree warp reduction.
+template <int BN>
+__global__ void __launch_bounds__(256) k_csr_apply(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                                   const double* __restrict__ val, int64_t n,
+                                                   const double* __restrict__ U, int64_t ldu, int b,
+                                                   double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  double acc[BN];
+#pragma unroll
+  for (int c = 0; c < BN; ++c) acc[c] = 0.0;
+  const int e0 = rowptr[row], e1 = rowptr[row + 1];
+  for (int e = e0 + lane; e < e1; e += 32) {
+    const int64_t j = col[e];
+    const double g = val[e];
+    const double* u = U + j * ldu;
+#pragma unroll
+    for (int c = 0; c < BN; ++c)
+      if (c < b) acc[c] = fma(g, __ldg(u + c), acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < BN; ++c) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+  }
+#pragma unroll
+  for (int c = 0; c < BN; ++c)
+    if (c < b && lane == (c & 31)) out[row * b + c] = acc[c];
+}
+
+// W = scale * sum_s part[s] + L E + alpha U
+__global__ void k_apply_finish(int64_t n, int b, int S, const double* __restrict__ part, double scale,
+                               const double* __restrict__ Lf, int64_t ldl, int l, const double* __restrict__ E,
+                               double alpha, const double* __restrict__ U, int64_t ldu, double* __restrict__ W,
+                               int64_t ldw) {
+  extern __shared__ double Es[];
+  for (int idx = threadIdx.x; idx < l * b; idx += blockDim.x) Es[idx] = E[idx];
+  __syncthreads();
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * b) return;
+  const int64_t i = idx / b;
+  const int c = (int)(idx - i * b);
+  double s = 0.0;
+  for (int t = 0; t < S; ++t) s += part[(int64_t)t * n * b + idx];
+  double v = scale * s + alpha * U[i * ldu + c];
+  const double* Lr = Lf + i * ldl;
+  for (int k = 0; k < l; ++k) v = fma(Lr[k], Es[k * b + c], v);
+  W[i * ldw + c] = v;
+}
+
+// ===========================================================================
+// Tall-skinny X^T Y partials: each CTA reduces a contiguous row range into
+// one p x q partial; k_reduce_partials sums the partials in CTA order.
+constexpr int kTnThreads = 512;
+constexpr int kTnRows = 16;
+
+template <int J>
+__global__ void __launch_bounds__(kTnThreads) k_tn_partial(int64_t n, const double* __restrict__ X, int64_t ldx, int p,
+                                                           const double* __restrict__ Y, int64_t ldy, int q,
+                                                           double* __restrict__ part, int64_t rows_per_cta) {
+  extern __shared__ double sm[];
+  double* Xs = sm;                 // kTnRows x p
+  double* Ys = sm + kTnRows * p;   // kTnRows x q
+  const int pq = p * q;
+  int oa[J], oc[J];
+  double acc[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int o = threadIdx.x + j * kTnThreads;
+    oa[j] = o < pq ? o / q : 0;
+    oc[j] = o < pq ? o - (o / q) * q : 0;
+    acc[j] = 0.0;
+  }
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(n, r0 + rows_per_cta);
+  for (int64_t rc = r0; rc < r1; rc += kTnRows) {
+    const int rows = (int)min((int64_t)kTnRows, r1 - rc);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kTnRows * p; idx += kTnThreads) {
+      const int r = idx / p, a = idx - r * p;
+      Xs[idx] = r < rows ? X[(rc + r) * ldx + a] : 0.0;
+    }
+    for (int idx = threadIdx.x; idx < kTnRows * q; idx += kTnThreads) {
+      const int r = idx / q, c = idx - r * q;
+      Ys[idx] = r < rows ? Y[(rc + r) * ldy + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int r = 0; r < kTnRows; ++r) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[j] = fma(Xs[r * p + oa[j]], Ys[r * q + oc[j]], acc[j]);
+    }
+  }
+  double* out = part + (int64_t)blockIdx.x * pq;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int o = threadIdx.x + j * kTnThreads;
+    if (o < pq) out[o] = acc[j];
+  }
+}
+
+// out[a * ldo + c] = rowscale[a] * sum_g part[g][a * q + c]; mode 1: sqrt
+__global__ void k_reduce_partials(const double* __restrict__ part, int G, int p, int q, double* __restrict__ out,
+                                  int64_t ldo, const double* __restrict__ rowscale, int mode) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  const int pq = p * q;
+  if (o >= pq) return;
+  double s = 0.0;
+  for (int g = 0; g < G; ++g) s += part[(int64_t)g * pq + o];
+  const int a = o / q, c = o - a * q;
+  if (rowscale) s *= rowscale[a];
+  if (mode == 1) s = sqrt(s);
+  out[(int64_t)a * ldo + c] = s;
+}
+
+// Y = beta Y + alpha X C   (C p x q in shared memory)
+__global__ void k_nn(int64_t n, const double* __restrict__ X, int64_t ldx, int p, const double* __restrict__ C,
+                     int64_t ldc, int q, double alpha, double beta, double* __restrict__ Y, int64_t ldy) {
+  extern __shared__ double Cs[];
+  for (int idx = threadIdx.x; idx < p * q; idx += blockDim.x) {
+    const int k = idx / q, c = idx - k * q;
+    Cs[idx] = C[(int64_t)k * ldc + c];
+  }
+  __syncthreads();
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * q) return;
+  const int64_t i = idx / q;
+  const int c = (int)(idx - i * q);
+  const double* xr = X + i * ldx;
+  double s = 0.0;
+  for (int k = 0; k < p; ++k) s = fma(xr[k], Cs[k * q + c], s);
+  double* y = Y + i * ldy + c;
+  *y = (beta == 0.0 ? 0.0 : beta * *y) + alpha * s;
+}
+
+// ===========================================================================
+// K4: Cholesky of a q x q Gram matrix (q <= 64) with column equilibration
+// and breakdown detection (linalg.py:193-199 rule: a direction whose norm is
+// <= thresh is replaced by a fresh random one).
+__global__ void __launch_bounds__(256) k_chol(const double* __restrict__ Gin, int q, double thresh, double* __restrict__ Rrel,
+                                              double* __restrict__ Rinv, int* __restrict__ mask,
+                                              const double* __restrict__ Rprev, double* __restrict__ Rtot,
+                                              int cols_prev) {
+  extern __shared__ double chol_sm[];
+  const int ld = q + 1;
+  double* Ab = chol_sm;            // q x (q+1)
+  double* Rb = chol_sm + q * ld;   // q x (q+1)
+  __shared__ double D[64];
+  __shared__ int bad[64];
+  const int t = threadIdx.x;
+#define A(i, j) Ab[(i) * ld + (j)]
+#define R(i, j) Rb[(i) * ld + (j)]
+  for (int idx = t; idx < q * q; idx += blockDim.x) {
+    const int i = idx / q, j = idx - i * q;
+    A(i, j) = Gin[(i <= j) ? i * q + j : j * q + i];
+    R(i, j) = 0.0;
+  }
+  __syncthreads();
+  if (t < q) {
+    const double g = A(t, t);
+    bad[t] = !(g > thresh * thresh);
+    D[t] = bad[t] ? 1.0 : sqrt(g);
+  }
+  __syncthreads();
+  for (int idx = t; idx < q * q; idx += blockDim.x) {
+    const int i = idx / q, j = idx - i * q;
+    A(i, j) = (bad[i] || bad[j]) ? (i == j ? 1.0 : 0.0) : A(i, j) / (D[i] * D[j]);
+  }
+  __syncthreads();
+  for (int j = 0; j < q; ++j) {
+    if (t == 0) {
+      const double d = A(j, j);
+      if (!bad[j] && d > 1e-20) {
+        R(j, j) = sqrt(d);
+      } else {
+        bad[j] = 1;
+        R(j, j) = 1.0;
+      }
+    }
+    __syncthreads();
+    const double rjj = R(j, j);
+    const bool bj = bad[j];
+    for (int k = j + 1 + t; k < q; k += blockDim.x) R(j, k) = bj ? 0.0 : A(j, k) / rjj;
+    __syncthreads();
+    for (int idx = t; idx < (q - j - 1) * (q - j - 1); idx += blockDim.x) {
+      const int k = j + 1 + idx / (q - j - 1), l = j + 1 + idx % (q - j - 1);
+      A(k, l) -= R(j, k) * R(j, l);
+    }
+    __syncthreads();
+  }
+  // de-equilibrate: R_true = Rs D, Rinv = D^-1 Rs^-1
+  if (t < q) {
+    const int c = t;  // column c of Rs^-1 by back substitution
+    double x[64];
+    for (int i = 0; i < 64; ++i) x[i] = 0.0;
+    x[c] = 1.0 / R(c, c);
+    for (int i = c - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int k = i + 1; k <= c; ++k) s += R(i, k) * x[k];
+      x[i] = -s / R(i, i);
+    }
+    for (int i = 0; i < q; ++i) Rinv[i * q + c] = (i <= c) ? x[i] / D[i] : 0.0;
+  }
+  __syncthreads();
+  for (int idx = t; idx < q * q; idx += blockDim.x) {
+    const int i = idx / q, j = idx - i * q;
+    Rrel[idx] = (bad[i] || j < i) ? 0.0 : R(i, j) * D[j];
+  }
+  if (t < q) mask[t] = bad[t];
+  if (Rtot) {
+    __syncthreads();
+    // Rtot (q x cols_prev) = Rrel (q x q) * Rprev (q x cols_prev)
+    for (int idx = t; idx < q * cols_prev; idx += blockDim.x) {
+      const int i = idx / cols_prev, j = idx - i * cols_prev;
+      double s = 0.0;
+      if (!bad[i])
+        for (int k = i; k < q; ++k) s += R(i, k) * D[k] * Rprev[k * cols_prev + j];
+      Rtot[idx] = s;
+    }
+  }
+}
+#undef A
+#undef R
+
+// W = W Rinv, deficient columns replaced by random normals
+__global__ void __launch_bounds__(256) k_apply_rinv(int64_t n, double* __restrict__ W, int64_t ldw, int q,
+                                                    const double* __restrict__ Rinv, const int* __restrict__ mask,
+                                                    uint64_t key, uint64_t base) {
+  extern __shared__ double rinv_sm[];
+  double* Ri = rinv_sm;           // q x q
+  double* Ws = rinv_sm + q * q;   // 32 x q
+  __shared__ int bad[64];
+  for (int idx = threadIdx.x; idx < q * q; idx += blockDim.x) Ri[idx] = Rinv[idx];
+  if (threadIdx.x < q) bad[threadIdx.x] = mask[threadIdx.x];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int rows = (int)min((int64_t)32, n - r0);
+  for (int idx = threadIdx.x; idx < rows * q; idx += blockDim.x) {
+    const int r = idx / q, c = idx - r * q;
+    Ws[idx] = W[(r0 + r) * ldw + c];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < rows * q; idx += blockDim.x) {
+    const int r = idx / q, c = idx - r * q;
+    double v;
+    if (bad[c]) {
+      v = gauss_dev(key, base + (uint64_t)(r0 + r) * q + c);
+    } else {
+      v = 0.0;
+      for (int k = 0; k <= c; ++k) v = fma(Ws[r * q + k], Ri[k * q + c], v);
+    }
+    W[(r0 + r) * ldw + c] = v;
+  }
+}
+
+// ===========================================================================
+// K6: Rayleigh-Ritz by parallel cyclic Jacobi (round-robin ordering) in one
+// CTA; H and the accumulated rotations live in shared memory (m <= 112).
+constexpr int kJacobiThreads = 1024;
+
+__global__ void __launch_bounds__(kJacobiThreads, 1)
+    k_rr_jacobi(const double* __restrict__ Hg, int64_t ldh, int m, double* __restrict__ theta,
+                double* __restrict__ Sout, const double* __restrict__ Rn, int rn_rows, int cur, int nreq,
+                double* __restrict__ est, double* __restrict__ info) {
+  extern __shared__ double sm[];
+  const int mp = (m + 1) & ~1;  // padded even size
+  double* H = sm;               // mp x mp
+  double* V = sm + mp * mp;     // mp x mp
+  __shared__ double cs[64], sn[64];
+  __shared__ int pp[64], qq[64];
+  __shared__ double red[32];
+  __shared__ int done;
+  const int t = threadIdx.x;
+  const int half = mp / 2;
+  for (int idx = t; idx < mp * mp; idx += blockDim.x) {
+    const int i = idx / mp, j = idx - i * mp;
+    double h = 0.0;
+    if (i < m && j < m) h = (i <= j) ? Hg[i * ldh + j] : Hg[j * ldh + i];
+    H[idx] = h;
+    V[idx] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  // scale for the stopping rule
+  double local = 0.0;
+  for (int idx = t; idx < mp * mp; idx += blockDim.x) local += H[idx] * H[idx];
+  for (int off = 16; off >= 1; off >>= 1) local += __shfl_xor_sync(0xffffffffu, local, off);
+  if ((t & 31) == 0) red[t >> 5] = local;
+  __syncthreads();
+  if (t == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    red[0] = s;
+  }
+  __syncthreads();
+  const double fro2 = red[0];
+  const double stop2 = fro2 * 1e-30;  // off(H) <= 1e-15 ||H||_F
+  int sweep = 0;
+  double off2 = 0.0;
+  for (sweep = 0; sweep < 40; ++sweep) {
+    for (int round = 0; round < mp - 1; ++round) {
+      if (t < half) {
+        int p, q;
+        if (t == 0) {
+          p = 0;
+          q = 1 + (round % (mp - 1));
+        } else {
+          p = 1 + (round + t) % (mp - 1);
+          q = 1 + (round - t + (mp - 1)) % (mp - 1);
+        }
+        if (p > q) {
+          const int tmp = p;
+          p = q;
+          q = tmp;
+        }
+        const double apq = H[p * mp + q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0) {
+          const double tau = (H[q * mp + q] - H[p * mp + p]) / (2.0 * apq);
+          const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + tt * tt);
+          s = tt * c;
+        }
+        pp[t] = p;
+        qq[t] = q;
+        cs[t] = c;
+        sn[t] = s;
+      }
+      __syncthreads();
+      // H <- J^T H J on all 2x2 blocks, V <- V J
+      for (int idx = t; idx < half * half; idx += blockDim.x) {
+        const int a = idx / half, bb = idx - a * half;
+        const int pa = pp[a], qa = qq[a], pb = pp[bb], qb = qq[bb];
+        const double ca = cs[a], sa = sn[a], cb = cs[bb], sb = sn[bb];
+        const double h00 = H[pa * mp + pb], h01 = H[pa * mp + qb];
+        const double h10 = H[qa * mp + pb], h11 = H[qa * mp + qb];
+        const double t00 = ca * h00 - sa * h10, t01 = ca * h01 - sa * h11;
+        const double t10 = sa * h00 + ca * h10, t11 = sa * h01 + ca * h11;
+        double n00 = t00 * cb - t01 * sb, n01 = t00 * sb + t01 * cb;
+        double n10 = t10 * cb - t11 * sb, n11 = t10 * sb + t11 * cb;
+        if (a == bb) {
+          n01 = 0.0;
+          n10 = 0.0;
+        }
+        H[pa * mp + pb] = n00;
+        H[pa * mp + qb] = n01;
+        H[qa * mp + pb] = n10;
+        H[qa * mp + qb] = n11;
+      }
+      for (int idx = t; idx < mp * half; idx += blockDim.x) {
+        const int i = idx / half, a = idx - i * half;
+        const int pa = pp[a], qa = qq[a];
+        const double ca = cs[a], sa = sn[a];
+        const double vp = V[i * mp + pa], vq = V[i * mp + qa];
+        V[i * mp + pa] = ca * vp - sa * vq;
+        V[i * mp + qa] = sa * vp + ca * vq;
+      }
+      __syncthreads();
+    }
+    // off-diagonal mass
+    double lo = 0.0;
+    for (int idx = t; idx < mp * mp; idx += blockDim.x) {
+      const int i = idx / mp, j = idx - i * mp;
+      if (i != j) lo += H[idx] * H[idx];
+    }
+    for (int off = 16; off >= 1; off >>= 1) lo += __shfl_xor_sync(0xffffffffu, lo, off);
+    __syncthreads();
+    if ((t & 31) == 0) red[t >> 5] = lo;
+    __syncthreads();
+    if (t == 0) {
+      double s = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+      red[0] = s;
+      done = (s <= stop2);
+    }
+    __syncthreads();
+    off2 = red[0];
+    if (done) break;
+    __syncthreads();
+  }
+  // sort eigenvalues non-increasing (stable by index) and write theta, S
+  for (int i = t; i < m; i += blockDim.x) {
+    const double di = H[i * mp + i];
+    int rank = 0;
+    for (int j = 0; j < m; ++j) {
+      const double dj = H[j * mp + j];
+      rank += (dj > di) || (dj == di && j < i);
+    }
+    theta[rank] = di;
+    for (int k = 0; k < m; ++k) Sout[(int64_t)k * m + rank] = V[k * mp + i];
+  }
+  __syncthreads();
+  // residual estimates est[j] = || Rn (rn_rows x cur) * S[m-cur:m, j] ||
+  if (Rn && est) {
+    for (int j = t; j < nreq; j += blockDim.x) {
+      double s2 = 0.0;
+      for (int a = 0; a < rn_rows; ++a) {
+        double v = 0.0;
+        for (int c = 0; c < cur; ++c) v = fma(Rn[a * cur + c], Sout[(int64_t)(m - cur + c) * m + j], v);
+        s2 += v * v;
+      }
+      est[j] = sqrt(s2);
+    }
+  }
+  if (t == 0 && info) {
+    info[0] = sweep + 1;
+    info[1] = sqrt(off2);
+    info[2] = sqrt(fro2);
+  }
+}
+
+// partial sums of (AX_j - theta_j X_j)^2 per CTA
+__global__ void __launch_bounds__(256) k_resid_partial(int64_t n, const double* __restrict__ X, int64_t ldx,
+                                                       const double* __restrict__ AX, int64_t ldax, int q,
+                                                       const double* __restrict__ theta, double* __restrict__ part,
+                                                       int64_t rows_per_cta) {
+  __shared__ double red[8][64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(n, r0 + rows_per_cta);
+  for (int c = 0; c < q; ++c) {
+    const double th = theta[c];
+    double s = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      const double d = AX[i * ldax + c] - th * X[i * ldx + c];
+      s = fma(d, d, s);
+    }
+    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) red[warp][c & 63] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < 8; ++w) tot += red[w][c & 63];
+      part[(int64_t)blockIdx.x * q + c] = tot;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_copy_block(int64_t n, int q, const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
+                             int64_t ldd) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * q) return;
+  const int64_t i = idx / q;
+  const int c = (int)(idx - i * q);
+  dst[i * ldd + c] = src[i * lds + c];
+}
+
+__global__ void k_fill_gaussian(int64_t n, int q, uint64_t key, uint64_t base, double scale, int round_f32,
+                                double* __restrict__ dst, int64_t ldd) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * q) return;
+  const int64_t i = idx / q;
+  const int c = (int)(idx - i * q);
+  double v = scale * gauss_dev(key, base + (uint64_t)idx);
+  if (round_f32) v = (double)__double2float_rn(v);
+  dst[i * ldd + c] = v;
+}
+
+__global__ void k_zero(double* p, int64_t count) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < count) p[idx] = 0.0;
+}
+
+// sampled gradient values: one warp per row; optional per-row sum of squares
+__global__ void __launch_bounds__(256) k_csr_values(int64_t n, const int32_t* __restrict__ rowptr,
+                                                    const int32_t* __restrict__ col, const double* __restrict__ obs,
+                                                    const double* __restrict__ V, int64_t ldv, int r,
+                                                    const double* __restrict__ coeff, double tail,
+                                                    double* __restrict__ g, double* __restrict__ sq_rows) {
+  __shared__ double cf[64];
+  if (threadIdx.x < r) cf[threadIdx.x] = coeff[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const double* vi = V + row * ldv;
+  double s2 = 0.0;
+  for (int e = rowptr[row] + lane; e < rowptr[row + 1]; e += 32) {
+    const int64_t j = col[e];
+    const double* vj = V + j * ldv;
+    double x = 0.0;
+    for (int k = 0; k < r; ++k) x = fma(vi[k] * vj[k], cf[k], x);
+    if (j == row) x += tail;
+    const double d = x - obs[e];
+    if (g) g[e] = d;
+    s2 = fma(d, d, s2);
+  }
+  if (sq_rows) {
+    for (int off = 16; off >= 1; off >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+    if (lane == 0) sq_rows[row] = s2;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_dense_stats(const T* __restrict__ M, int64_t ld, int64_t n,
+                                                     double* __restrict__ part) {
+  // part[2*blockIdx.x] = sum of squares over this CTA's rows, [2*blockIdx.x+1] = trace part
+  __shared__ double red[2][8];
+  double s = 0.0, tr = 0.0;
+  const int64_t rows_per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(n, r0 + rows_per);
+  for (int64_t i = r0; i < r1; ++i) {
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      const double v = (double)M[i * ld + j];
+      s = fma(v, v, s);
+      if (j == i) tr += v;
+    }
+  }
+  for (int off = 16; off >= 1; off >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, off);
+    tr += __shfl_xor_sync(0xffffffffu, tr, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = s;
+    red[1][threadIdx.x >> 5] = tr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_gen_dense_target(const double* __restrict__ U, int r,
+                                                          const double* __restrict__ lam, double sigma, uint64_t key,
+                                                          T* __restrict__ M, int64_t ld, int64_t n) {
+  __shared__ double lm[64];
+  if (threadIdx.x < r) lm[threadIdx.x] = lam[threadIdx.x];
+  __syncthreads();
+  const int64_t i = blockIdx.y;
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double acc = 0.0;
+  for (int k = 0; k < r; ++k) acc = fma(U[i * r + k] * U[j * r + k], lm[k], acc);
+  if (sigma != 0.0) {
+    const double g = gauss_dev(key, (uint64_t)i * n + j) + gauss_dev(key, (uint64_t)j * n + i);
+    acc += sigma * ((0.5 / sqrt((double)n)) * g);
+  }
+  M[i * ld + j] = (T)acc;
+}
+
+__global__ void k_step_epilogue(const double* __restrict__ theta, int r, int64_t n, double eps_next,
+                                double* __restrict__ out) {
+  // out layout: [0, r+1) y; [r+1, 2r+1) lam; then lam_rp1, b_rp1, shift, lhs, holds, threshold, status
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double shift = theta[0];
+  double y[65];
+  for (int k = 0; k <= r; ++k) y[k] = exp(theta[k] - shift);
+  double kept = 0.0;
+  for (int k = 0; k < r; ++k) kept += y[k];
+  double* o = out;
+  for (int k = 0; k <= r; ++k) o[k] = y[k];
+  double status = 0.0;
+  if (!(kept > 1e-290)) status = 4.0;
+  double lsum = 0.0;
+  for (int k = 0; k < r; ++k) {
+    o[r + 1 + k] = y[k] / kept;
+    lsum += o[r + 1 + k];
+  }
+  for (int k = 0; k < r; ++k) o[r + 1 + k] /= lsum;
+  const double lam_rp1 = y[r];
+  double b = 0.0;
+  for (int k = 0; k <= r; ++k) b += y[k];
+  double lhs;
+  if (!(b > 0.0) || lam_rp1 < 0.0) {
+    status = 1.0;
+    lhs = 0.0;
+  } else if (lam_rp1 == 0.0) {
+    lhs = -INFINITY;
+  } else {
+    lhs = log((double)(n - r) * lam_rp1 / (eps_next * b));
+  }
+  double* tail = o + 2 * r + 1;
+  tail[0] = lam_rp1;
+  tail[1] = b;
+  tail[2] = shift;
+  tail[3] = lhs;
+  tail[4] = (lhs <= 2.0 * eps_next) ? 1.0 : 0.0;
+  tail[5] = 2.0 * eps_next;
+  tail[6] = status;
+}
+
+__global__ void k_reduce_sum(const double* __restrict__ part, int slots, int width, double* __restrict__ out) {
+  const int c = threadIdx.x;
+  if (c >= width) return;
+  double s = 0.0;
+  for (int g = 0; g < slots; ++g) s += part[(int64_t)g * width + c];
+  out[c] = s;
+}
+
+template <int BN>
+void launch_dense_f64(const Launch& L, const double* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                      double* part, int S, int64_t kslice, bool vec) {
+  const size_t smem = (size_t)(KC * BN + 4 * BN * 64) * sizeof(double);
+  dim3 grid(cdiv(n, 64), S);
+  if (vec) {
+    static bool attr = false;
+    if (!attr) {
+      MEG_CUDA(cudaFuncSetAttribute(k_dense_apply_f64<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    k_dense_apply_f64<BN, true><<<grid, kApplyThreads, smem, L.stream>>>(M, ldm, n, U, ldu, b, part, kslice);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      MEG_CUDA(cudaFuncSetAttribute(k_dense_apply_f64<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    k_dense_apply_f64<BN, false><<<grid, kApplyThreads, smem, L.stream>>>(M, ldm, n, U, ldu, b, part, kslice);
+  }
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+template <int BN>
+void launch_dense_f32(const Launch& L, const float* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                      double* part, int S, int64_t kslice, bool vec) {
+  const size_t smem = (size_t)((KC * BN + 1) / 2 + 4 * BN * 128) * sizeof(double);
+  dim3 grid(cdiv(n, 128), S);
+  if (vec) {
+    static bool attr = false;
+    if (!attr) {
+      MEG_CUDA(cudaFuncSetAttribute(k_dense_apply_f32<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    k_dense_apply_f32<BN, true><<<grid, kApplyThreads, smem, L.stream>>>(M, ldm, n, U, ldu, b, part, kslice);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      MEG_CUDA(cudaFuncSetAttribute(k_dense_apply_f32<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    k_dense_apply_f32<BN, false><<<grid, kApplyThreads, smem, L.stream>>>(M, ldm, n, U, ldu, b, part, kslice);
+  }
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+}  // namespace
+
+// ===========================================================================
+// launch wrappers
+
+int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, int64_t n, const double* U,
+                        int64_t ldu, int b, double* part, int64_t part_cap_slices, int sm_count) {
+  const int rows = dtype == MEGB200_F64 ? 64 : 128;
+  const int tiles = cdiv(n, rows);
+  int S = std::max(1, cdiv(sm_count, tiles));
+  if (dtype != MEGB200_F64) S = std::max(S, cdiv(n, kF32Slice));
+  S = std::min<int>((int)part_cap_slices, S);
+  int64_t kslice = (int64_t)cdiv(cdiv(n, S), KC) * KC;
+  S = cdiv(n, kslice);
+  if (dtype == MEGB200_F64) {
+    const bool vec = (ldm % 2 == 0) && ((uintptr_t)M % 16 == 0);
+    const double* m = static_cast<const double*>(M);
+    if (b <= 8)
+      launch_dense_f64<8>(L, m, ldm, n, U, ldu, b, part, S, kslice, vec);
+    else if (b <= 16)
+      launch_dense_f64<16>(L, m, ldm, n, U, ldu, b, part, S, kslice, vec);
+    else if (b <= 24)
+      launch_dense_f64<24>(L, m, ldm, n, U, ldu, b, part, S, kslice, vec);
+    else
+      launch_dense_f64<32>(L, m, ldm, n, U, ldu, b, part, S, kslice, vec);
+  } else {
+    const bool vec = (ldm % 4 == 0) && ((uintptr_t)M % 16 == 0);
+    const float* m = static_cast<const float*>(M);
+    if (b <= 8)
+      launch_dense_f32<8>(L, m, ldm, n, U, ldu, b, part, S, kslice, vec);
+    else if (b <= 16)
+      launch_dense_f32<16>(L, m, ldm, n, U, ldu, b, part, S, kslice, vec);
+    else if (b <= 24)
+      launch_dense_f32<24>(L, m, ldm, n, U, ldu, b, part, S, kslice, vec);
+    else
+      launch_dense_f32<32>(L, m, ldm, n, U, ldu, b, part, S, kslice, vec);
+  }
+  return S;
+}
+
+void csr_apply_partial(const Launch& L, const int32_t* rowptr, const int32_t* col, const double* val, int64_t n,
+                       const double* U, int64_t ldu, int b, double* part) {
+  const dim3 grid(cdiv(n, 8));
+  if (b <= 8)
+    k_csr_apply<8><<<grid, 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
+  else if (b <= 16)
+    k_csr_apply<16><<<grid, 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
+  else if (b <= 24)
+    k_csr_apply<24><<<grid, 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
+  else
+    k_csr_apply<32><<<grid, 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void apply_finish(const Launch& L, int64_t n, int b, int S, const double* part, double scale, const double* Lf,
+                  int64_t ldl, int l, const double* E, double alpha, const double* U, int64_t ldu, double* W,
+                  int64_t ldw) {
+  const size_t smem = (size_t)std::max(1, l * b) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    MEG_CUDA(cudaFuncSetAttribute(k_apply_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  k_apply_finish<<<cdiv(n * b, 256), 256, smem, L.stream>>>(n, b, S, part, scale, Lf, ldl, l, E, alpha, U, ldu, W,
+                                                           ldw);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void tn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const double* Y, int64_t ldy, int q,
+        double* C, int64_t ldc, const double* rowscale, double* part, int64_t part_cap, int sm_count) {
+  const int pq = p * q;
+  int G = std::max(1, std::min(sm_count, cdiv(n, 128)));
+  while ((int64_t)G * pq > part_cap && G > 1) G = (G + 1) / 2;
+  const int64_t rows_per = (int64_t)cdiv(cdiv(n, G), kTnRows) * kTnRows;
+  G = cdiv(n, rows_per);
+  const size_t smem = (size_t)kTnRows * (p + q) * sizeof(double);
+  const int J = cdiv(pq, kTnThreads);
+  static bool attr = false;
+  if (!attr) {
+    MEG_CUDA(cudaFuncSetAttribute(k_tn_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    MEG_CUDA(cudaFuncSetAttribute(k_tn_partial<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    MEG_CUDA(cudaFuncSetAttribute(k_tn_partial<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    MEG_CUDA(cudaFuncSetAttribute(k_tn_partial<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    MEG_CUDA(cudaFuncSetAttribute(k_tn_partial<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    attr = true;
+  }
+  if (J <= 1)
+    k_tn_partial<1><<<G, kTnThreads, smem, L.stream>>>(n, X, ldx, p, Y, ldy, q, part, rows_per);
+  else if (J <= 4)
+    k_tn_partial<4><<<G, kTnThreads, smem, L.stream>>>(n, X, ldx, p, Y, ldy, q, part, rows_per);
+  else if (J <= 8)
+    k_tn_partial<8><<<G, kTnThreads, smem, L.stream>>>(n, X, ldx, p, Y, ldy, q, part, rows_per);
+  else if (J <= 16)
+    k_tn_partial<16><<<G, kTnThreads, smem, L.stream>>>(n, X, ldx, p, Y, ldy, q, part, rows_per);
+  else if (J <= 24)
+    k_tn_partial<24><<<G, kTnThreads, smem, L.stream>>>(n, X, ldx, p, Y, ldy, q, part, rows_per);
+  else
+    throw Error(MEGB200_ERR_PARAM, "tn: p*q too large");
+  MEG_LAUNCHED();
+  k_reduce_partials<<<cdiv(pq, 256), 256, 0, L.stream>>>(part, G, p, q, C, ldc, rowscale, 0);
+  MEG_LAUNCHED();
+  *L.counter += 2;
+}
+
+void nn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const double* C, int64_t ldc, int q,
+        double alpha, double beta, double* Y, int64_t ldy) {
+  const size_t smem = (size_t)std::max(1, p * q) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    MEG_CUDA(cudaFuncSetAttribute(k_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  k_nn<<<cdiv(n * q, 256), 256, smem, L.stream>>>(n, X, ldx, p, C, ldc, q, alpha, beta, Y, ldy);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void chol(const Launch& L, const double* G, int q, double thresh, double* R, double* Rinv, int* mask,
+          const double* Rprev, double* Rtot, int cols_prev) {
+  static bool attr = false;
+  if (!attr) {
+    MEG_CUDA(cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 65 * 8));
+    attr = true;
+  }
+  k_chol<<<1, 256, (size_t)2 * q * (q + 1) * sizeof(double), L.stream>>>(G, q, thresh, R, Rinv, mask, Rprev, Rtot,
+                                                                          cols_prev);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void apply_rinv(const Launch& L, int64_t n, double* W, int64_t ldw, int q, const double* Rinv, const int* mask,
+                uint64_t key, uint64_t ctr_base) {
+  static bool attr = false;
+  if (!attr) {
+    MEG_CUDA(cudaFuncSetAttribute(k_apply_rinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 64 + 32 * 64) * 8));
+    attr = true;
+  }
+  k_apply_rinv<<<cdiv(n, 32), 256, (size_t)(q * q + 32 * q) * sizeof(double), L.stream>>>(n, W, ldw, q, Rinv, mask,
+                                                                                          key, ctr_base);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void rr_jacobi(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, const double* Rn,
+               int rn_rows, int cur, int nreq, double* est, double* info) {
+  const int mp = (m + 1) & ~1;
+  const size_t smem = (size_t)2 * mp * mp * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    MEG_CUDA(cudaFuncSetAttribute(k_rr_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    attr = true;
+  }
+  k_rr_jacobi<<<1, kJacobiThreads, smem, L.stream>>>(H, ldh, m, theta, S, Rn, rn_rows, cur, nreq, est, info);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void resid_norms(const Launch& L, int64_t n, const double* X, int64_t ldx, const double* AX, int64_t ldax, int q,
+                 const double* theta, double* out, double* part, int64_t part_cap, int sm_count) {
+  int G = std::max(1, std::min(sm_count, cdiv(n, 256)));
+  while ((int64_t)G * q > part_cap && G > 1) G = (G + 1) / 2;
+  const int64_t rows_per = cdiv(n, G);
+  G = cdiv(n, rows_per);
+  k_resid_partial<<<G, 256, 0, L.stream>>>(n, X, ldx, AX, ldax, q, theta, part, rows_per);
+  MEG_LAUNCHED();
+  k_reduce_partials<<<cdiv(q, 256), 256, 0, L.stream>>>(part, G, 1, q, out, q, nullptr, 1);
+  MEG_LAUNCHED();
+  *L.counter += 2;
+}
+
+void copy_block(const Launch& L, int64_t n, int q, const double* src, int64_t lds, double* dst, int64_t ldd) {
+  if (n * q == 0) return;
+  k_copy_block<<<cdiv(n * q, 256), 256, 0, L.stream>>>(n, q, src, lds, dst, ldd);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void fill_gaussian(const Launch& L, int64_t n, int q, uint64_t key, uint64_t base, double scale, bool round_f32,
+                   double* dst, int64_t ldd) {
+  if (n * q == 0) return;
+  k_fill_gaussian<<<cdiv(n * q, 256), 256, 0, L.stream>>>(n, q, key, base, scale, round_f32 ? 1 : 0, dst, ldd);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void zero(const Launch& L, double* p, int64_t count) {
+  if (count == 0) return;
+  k_zero<<<cdiv(count, 256), 256, 0, L.stream>>>(p, count);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void csr_values(const Launch& L, int64_t n, const int32_t* rowptr, const int32_t* col, const double* obs,
+                const double* V, int64_t ldv, int r, const double* coeff, double tail, double* g, double* sq_rows,
+                int) {
+  k_csr_values<<<cdiv(n, 8), 256, 0, L.stream>>>(n, rowptr, col, obs, V, ldv, r, coeff, tail, g, sq_rows);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void dense_stats(const Launch& L, const void* M, int dtype, int64_t ld, int64_t n, double* part, int slots) {
+  if (dtype == MEGB200_F64)
+    k_dense_stats<double><<<slots, 256, 0, L.stream>>>(static_cast<const double*>(M), ld, n, part);
+  else
+    k_dense_stats<float><<<slots, 256, 0, L.stream>>>(static_cast<const float*>(M), ld, n, part);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void gen_dense_target(const Launch& L, const double* U, int64_t r, const double* lam, double sigma, uint64_t key,
+                      void* M, int dtype, int64_t ld, int64_t n) {
+  dim3 grid(cdiv(n, 256), (unsigned)n);
+  if (dtype == MEGB200_F64)
+    k_gen_dense_target<double><<<grid, 256, 0, L.stream>>>(U, (int)r, lam, sigma, key, static_cast<double*>(M), ld, n);
+  else
+    k_gen_dense_target<float><<<grid, 256, 0, L.stream>>>(U, (int)r, lam, sigma, key, static_cast<float*>(M), ld, n);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void step_epilogue(const Launch& L, const double* theta, int r, int64_t n, double eps_next, double* out) {
+  k_step_epilogue<<<1, 32, 0, L.stream>>>(theta, r, n, eps_next, out);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void reduce_sum(const Launch& L, const double* part, int slots, int width, double* out) {
+  k_reduce_sum<<<1, 64, 0, L.stream>>>(part, slots, width, out);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+}  // namespace megb200

@@ -1,0 +1,954 @@
+// Host runtime of the B200 low-rank MEG path: solver handle / workspace arena,
+// the block thick-restart Lanczos eigensolver (replaces lanczos_top_r,
+// linalg.py:130-241), the MEG step (replaces lowrank_meg_step,
+// meg.py:327-364), objective values and the dual-gap certificate, and the
+// extern "C" entry points declared in include/megb200.h.
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "megb200_internal.h"
+
+using namespace megb200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+constexpr int kMaxBlock = 64;
+constexpr int kMaxBasis = 112;  // Jacobi Rayleigh-Ritz keeps H and S in shared memory
+
+inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct megb200_solver {
+  int64_t n = 0;
+  int max_block = 0, max_basis = 0, cap = 0;
+  int64_t max_lowrank = 0, max_nnz = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+
+  char* arena = nullptr;
+  int64_t arena_bytes = 0;
+  // tall-skinny (row-major, ld = cap)
+  double *Q = nullptr, *AQ = nullptr, *T = nullptr;
+  int64_t ldq = 0;
+  double* W = nullptr;      // n x max_block
+  double* part = nullptr;   // apply partial slices
+  int64_t part_slices = 0;
+  double* red = nullptr;    // reduction partials
+  int64_t red_cap = 0;
+  double* L = nullptr;      // n x max_lowrank
+  double* E = nullptr;      // max_lowrank x max_block
+  double* dvec = nullptr;   // max_lowrank
+  double* H = nullptr;      // cap x cap
+  double* C = nullptr;      // cap x max_block
+  double* C2 = nullptr;
+  double *G = nullptr, *R1 = nullptr, *R2 = nullptr, *Rinv = nullptr, *Rn = nullptr, *Rtmp = nullptr;
+  int* mask = nullptr;
+  double *theta = nullptr, *S = nullptr, *est = nullptr, *info = nullptr, *resid = nullptr;
+  double* small = nullptr;  // misc device scalars
+  double* csr_g = nullptr;  // max_nnz
+  double* rowsq = nullptr;  // n
+  double* h_buf = nullptr;  // pinned host staging
+  int64_t h_buf_len = 0;
+  double m_norm2_cache = NAN, m_trace_cache = NAN;
+  const void* m_cache_ptr = nullptr;
+
+  Launch launch() { return Launch{stream, &launches}; }
+  void sync() { MEG_CUDA(cudaStreamSynchronize(stream)); }
+  void d2h(double* host, const double* dev, int64_t count) {
+    if (count <= 0) return;
+    MEG_CUDA(cudaMemcpyAsync(host, dev, count * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  }
+  void h2d(double* dev, const double* host, int64_t count) {
+    if (count <= 0) return;
+    MEG_CUDA(cudaMemcpyAsync(dev, host, count * sizeof(double), cudaMemcpyHostToDevice, stream));
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// operators
+
+struct OpDev {
+  int kind = MEGB200_OP_NONE;
+  int dtype = MEGB200_F64;
+  const void* dense = nullptr;
+  int64_t ld = 0;
+  const int32_t* rowptr = nullptr;
+  const int32_t* col = nullptr;
+  const double* val = nullptr;
+  double scale = 0.0;
+  const double* L = nullptr;
+  int64_t ldl = 0;
+  int l = 0;
+  const double* d_dev = nullptr;  // device coefficients (length l)
+  double alpha = 0.0;
+};
+
+void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k, double* W, int64_t ldw) {
+  Launch L = s->launch();
+  const int64_t n = s->n;
+  int S = 0;
+  if (op.kind == MEGB200_OP_DENSE && op.scale != 0.0) {
+    S = dense_apply_partial(L, op.dense, op.dtype, op.ld, n, U, ldu, k, s->part, s->part_slices, s->sm_count);
+  } else if (op.kind == MEGB200_OP_CSR && op.scale != 0.0) {
+    csr_apply_partial(L, op.rowptr, op.col, op.val, n, U, ldu, k, s->part);
+    S = 1;
+  }
+  if (op.l > 0) tn(L, n, op.L, op.ldl, op.l, U, ldu, k, s->E, k, op.d_dev, s->red, s->red_cap, s->sm_count);
+  apply_finish(L, n, k, S, s->part, op.scale, op.L, op.ldl, op.l, s->E, op.alpha, U, ldu, W, ldw);
+}
+
+// columns k > 64 are applied in chunks (re-streams the operand; not used by the configs)
+void apply_op_wide(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k, double* W, int64_t ldw) {
+  const int chunk = std::min(32, s->max_block);
+  for (int c0 = 0; c0 < k; c0 += chunk) {
+    const int kc = std::min(chunk, k - c0);
+    apply_op(s, op, U + c0, ldu, kc, W + c0, ldw);
+  }
+}
+
+OpDev op_from_public(megb200_solver* s, const megb200_operator* op) {
+  if (!op) throw Error(MEGB200_ERR_PARAM, "operator is NULL");
+  if (op->n != s->n) throw Error(MEGB200_ERR_PARAM, "operator dimension does not match the solver");
+  OpDev o;
+  o.kind = op->kind;
+  o.dtype = op->dtype;
+  o.dense = op->dense;
+  o.ld = op->ld;
+  o.rowptr = op->rowptr;
+  o.col = op->col;
+  o.val = op->val;
+  o.scale = op->scale;
+  o.alpha = op->alpha;
+  if (o.kind == MEGB200_OP_DENSE && (!o.dense || o.ld < s->n)) throw Error(MEGB200_ERR_PARAM, "dense operand missing");
+  if (o.kind == MEGB200_OP_CSR && (!o.rowptr || !o.col || !o.val)) throw Error(MEGB200_ERR_PARAM, "CSR operand missing");
+  if (op->l > 0) {
+    if (op->l > s->max_lowrank) throw Error(MEGB200_ERR_PARAM, "low-rank width exceeds the solver's max_lowrank");
+    if (!op->L || !op->d) throw Error(MEGB200_ERR_PARAM, "low-rank factor or coefficients missing");
+    o.L = op->L;
+    o.ldl = op->ldl;
+    o.l = (int)op->l;
+    s->h2d(s->dvec, op->d, op->l);
+    o.d_dev = s->dvec;
+  }
+  return o;
+}
+
+// ---------------------------------------------------------------------------
+// block orthonormalisation: W (n x q, ld ldw) against Q[:, 0:cols] with CGS2,
+// then CholQR2 with breakdown replacement.  Writes the relation factor
+// Rn (q x q): W_in - Q C = Q_new Rn  (C = first-round coefficients).
+
+struct OrthStats {
+  int deficient = 0;
+};
+
+void orthonormalize(megb200_solver* s, double* W, int64_t ldw, int q, int cols, double scale, uint64_t key,
+                    uint64_t& refill_ctr, bool want_relation) {
+  Launch L = s->launch();
+  const int64_t n = s->n;
+  for (int round = 0; round < 2 && cols > 0; ++round) {
+    tn(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, q, nullptr, s->red, s->red_cap, s->sm_count);
+    nn(L, n, s->Q, s->ldq, cols, s->C2, q, q, -1.0, 1.0, W, ldw);
+  }
+  // CholQR round 1 (breakdown -> random refill, rule of linalg.py:193-199)
+  tn(L, n, W, ldw, q, W, ldw, q, s->G, q, nullptr, s->red, s->red_cap, s->sm_count);
+  chol(L, s->G, q, 1e-13 * scale, s->R1, s->Rinv, s->mask, nullptr, nullptr, 0);
+  apply_rinv(L, n, W, ldw, q, s->Rinv, s->mask, key, refill_ctr);
+  refill_ctr += (uint64_t)n * q;
+  // re-project (refilled columns and R1^-1 amplification), CholQR round 2
+  if (cols > 0) {
+    tn(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, q, nullptr, s->red, s->red_cap, s->sm_count);
+    nn(L, n, s->Q, s->ldq, cols, s->C2, q, q, -1.0, 1.0, W, ldw);
+  }
+  tn(L, n, W, ldw, q, W, ldw, q, s->G, q, nullptr, s->red, s->red_cap, s->sm_count);
+  chol(L, s->G, q, 0.0, s->R2, s->Rinv, s->mask, want_relation ? s->R1 : nullptr, want_relation ? s->Rn : nullptr, q);
+  apply_rinv(L, n, W, ldw, q, s->Rinv, s->mask, key, refill_ctr);
+  refill_ctr += (uint64_t)n * q;
+}
+
+// ---------------------------------------------------------------------------
+// block thick-restart Lanczos (device Krylov-Schur) for the nreq algebraically
+// largest eigenpairs.
+
+struct EigRun {
+  std::vector<double> theta, resid;
+  int passes = 0, restarts = 0;
+  double norm_est = 1.0;
+  bool converged = false;
+};
+
+struct EigParams {
+  double tol = 1e-10;
+  int max_passes = 0;
+  int restarts = 12;
+  int block = 0, basis = 0, keep = 0;
+  uint64_t seed = 0;
+  const double* warm = nullptr;
+  int64_t warm_cols = 0, ld_warm = 0;
+};
+
+EigParams params_from_opts(const megb200_eig_opts* o) {
+  EigParams p;
+  if (!o) return p;
+  if (o->tol > 0) p.tol = o->tol;
+  p.max_passes = o->max_passes;
+  if (o->restarts > 0) p.restarts = o->restarts;
+  p.block = o->block;
+  p.basis = o->basis;
+  p.keep = o->keep;
+  p.seed = o->seed;
+  p.warm = o->warm;
+  p.warm_cols = o->warm ? o->warm_cols : 0;
+  p.ld_warm = o->ld_warm;
+  return p;
+}
+
+// Outputs: eigenvectors (nreq) -> vec_out, top `bw` Ritz vectors -> ritz_out.
+EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P, double* vec_out, int64_t ld_vec,
+                double* ritz_out, int64_t ld_ritz, int* ritz_cols_out) {
+  const int64_t n = s->n;
+  if (!(1 <= nreq && nreq < n)) throw Error(MEGB200_ERR_PARAM, "need 1 <= r < n, got r=" + std::to_string(nreq) + ", n=" + std::to_string(n));
+  Launch L = s->launch();
+  // ---- sizes
+  int bw = P.block > 0 ? P.block : std::min(s->max_block, nreq + 7);
+  int mmax = P.basis > 0 ? P.basis : std::max({4 * bw, 2 * nreq + 10, 30});
+  if (P.basis > 0 && P.block <= 0) bw = std::max(1, std::min(bw, P.basis / 2));
+  bw = std::max(1, std::min<int>(bw, s->max_block));
+  mmax = std::min<int>(mmax, s->max_basis);
+  mmax = std::max(mmax, std::min<int>(nreq + bw, s->max_basis));
+  bool exhaust = false;
+  if (n <= s->max_basis && n <= 64) {  // tiny problems: span R^n exactly (basis.shape[1] >= n rule, linalg.py:215)
+    bw = (int)std::min<int64_t>(n, s->max_block);
+    mmax = (int)n;
+    exhaust = true;
+  }
+  mmax = (int)std::min<int64_t>(mmax, n);
+  if (bw > mmax) bw = mmax;
+  int keep = P.keep > 0 ? P.keep : std::max(nreq, mmax / 2);
+  keep = std::min(keep, mmax - bw);
+  if (!exhaust && keep < nreq) throw Error(MEGB200_ERR_PARAM, "basis too small for the requested eigenpairs");
+  const int max_passes = P.max_passes > 0 ? P.max_passes : P.restarts * mmax;
+  const double tol = P.tol;
+  const uint64_t key_start = stream_key(P.seed, kStreamStart);
+  const uint64_t key_refill = stream_key(P.seed, kStreamRefill);
+  uint64_t refill_ctr = 0;
+
+  // ---- start block: warm columns + seeded random fill
+  const int wc = (int)std::min<int64_t>(P.warm_cols, bw);
+  if (wc > 0) copy_block(L, n, wc, P.warm, P.ld_warm, s->Q, s->ldq);
+  if (bw > wc) fill_gaussian(L, n, bw - wc, key_start, 0, 1.0, false, s->Q + wc, s->ldq);
+  orthonormalize(s, s->Q, s->ldq, bw, 0, 1.0, key_refill, refill_ctr, false);
+
+  EigRun run;
+  std::vector<double> best(nreq, INFINITY);
+  std::vector<double> hbuf;
+  int cols = 0, cur = bw;
+  double scale = 1.0;
+  zero(L, s->H, (int64_t)s->cap * s->cap);
+  for (;;) {
+    // operator pass on the current block
+    apply_op_wide(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq);
+    run.passes++;
+    // first-round projection coefficients = H[0:cols+cur, cols:cols+cur]
+    tn(L, n, s->Q, s->ldq, cols + cur, s->AQ + cols, s->ldq, cur, s->H + cols, s->cap, nullptr, s->red, s->red_cap,
+       s->sm_count);
+    const int newcols = cols + cur;
+    const int nxt = (int)std::min<int64_t>(bw, n - newcols);
+    bool have_relation = false;
+    if (nxt == cur) {
+      // W = AQ_j - Q H[:, j]  -> next block with relation factor Rn
+      copy_block(L, n, cur, s->AQ + cols, s->ldq, s->Q + newcols, s->ldq);
+      nn(L, n, s->Q, s->ldq, newcols, s->H + cols, s->cap, cur, -1.0, 1.0, s->Q + newcols, s->ldq);
+      orthonormalize(s, s->Q + newcols, s->ldq, cur, newcols, scale, key_refill, refill_ctr, true);
+      have_relation = true;
+    } else if (nxt > 0) {
+      fill_gaussian(L, n, nxt, key_refill, refill_ctr, 1.0, false, s->Q + newcols, s->ldq);
+      refill_ctr += (uint64_t)n * nxt;
+      orthonormalize(s, s->Q + newcols, s->ldq, nxt, newcols, 1.0, key_refill, refill_ctr, false);
+    }
+    cols = newcols;
+    // Rayleigh-Ritz on H[0:cols, 0:cols]
+    rr_jacobi(L, s->H, s->cap, cols, s->theta, s->S, have_relation ? s->Rn : nullptr, cur, cur, nreq, s->est,
+              s->info);
+    // host decision data: theta (cols), est (nreq)
+    const int nt = cols;
+    double* hb = s->h_buf;
+    s->d2h(hb, s->theta, nt);
+    s->d2h(hb + nt, s->est, nreq);
+    s->sync();
+    double tmax = 0.0;
+    for (int j = 0; j < nt; ++j) tmax = std::max(tmax, fabs(hb[j]));
+    scale = std::max(1.0, tmax);
+    const bool complete = (cols >= n);
+    bool est_ok = have_relation;
+    double est_max = 0.0;
+    if (have_relation) {
+      for (int j = 0; j < nreq; ++j) {
+        est_ok = est_ok && (hb[nt + j] <= tol * scale);
+        est_max = std::max(est_max, hb[nt + j]);
+      }
+      double best_max = 0.0;
+      for (double v : best) best_max = std::max(best_max, v);
+      if (est_max < best_max)
+        for (int j = 0; j < nreq; ++j) best[j] = hb[nt + j];
+    }
+    if (est_ok || complete) {
+      // explicit residuals of the top Ritz pairs from the cached images (linalg.py:209-211)
+      const int rq = std::min(cols, std::max(nreq, bw));
+      nn(L, n, s->Q, s->ldq, cols, s->S, cols, rq, 1.0, 0.0, s->T, s->ldq);
+      nn(L, n, s->AQ, s->ldq, cols, s->S, cols, nreq, 1.0, 0.0, s->T + rq, s->ldq);
+      resid_norms(L, n, s->T, s->ldq, s->T + rq, s->ldq, nreq, s->theta, s->resid, s->red, s->red_cap, s->sm_count);
+      s->d2h(hb + nt + nreq, s->resid, nreq);
+      s->sync();
+      bool ok = true;
+      double rmax = 0.0;
+      for (int j = 0; j < nreq; ++j) {
+        ok = ok && (hb[nt + nreq + j] <= tol * scale);
+        rmax = std::max(rmax, hb[nt + nreq + j]);
+      }
+      double best_max = 0.0;
+      for (double v : best) best_max = std::max(best_max, v);
+      if (rmax < best_max)
+        for (int j = 0; j < nreq; ++j) best[j] = hb[nt + nreq + j];
+      if (ok || complete) {
+        run.theta.assign(hb, hb + nreq);
+        run.resid.assign(hb + nt + nreq, hb + nt + 2 * nreq);
+        run.norm_est = scale;
+        run.converged = true;
+        if (vec_out) copy_block(L, n, nreq, s->T, s->ldq, vec_out, ld_vec);
+        if (ritz_out) copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
+        if (ritz_cols_out) *ritz_cols_out = rq;
+        return run;
+      }
+    }
+    if (run.passes >= max_passes) break;
+    if (nxt <= 0) break;  // cannot grow (complete handled above)
+    if (cols + nxt > mmax) {
+      // thick restart: keep the leading `keep` Ritz pairs, continue from the next block
+      nn(L, n, s->Q, s->ldq, cols, s->S, cols, keep, 1.0, 0.0, s->T, s->ldq);
+      copy_block(L, n, keep, s->T, s->ldq, s->Q, s->ldq);
+      nn(L, n, s->AQ, s->ldq, cols, s->S, cols, keep, 1.0, 0.0, s->T, s->ldq);
+      copy_block(L, n, keep, s->T, s->ldq, s->AQ, s->ldq);
+      copy_block(L, n, nxt, s->Q + cols, s->ldq, s->Q + keep, s->ldq);
+      // H = diag(theta_keep); the coupling rows come with the next pass
+      zero(L, s->H, (int64_t)s->cap * s->cap);
+      hbuf.assign((size_t)keep * s->cap, 0.0);
+      for (int j = 0; j < keep; ++j) hbuf[(size_t)j * s->cap + j] = hb[j];
+      s->h2d(s->H, hbuf.data(), (int64_t)keep * s->cap);
+      cols = keep;
+      run.restarts++;
+    }
+    cur = nxt;
+  }
+  run.resid = best;
+  run.theta.clear();
+  run.norm_est = scale;
+  return run;
+}
+
+std::string fmt_resid(const std::vector<double>& r) {
+  std::string out = "[";
+  char buf[32];
+  for (size_t i = 0; i < r.size(); ++i) {
+    snprintf(buf, sizeof buf, "%s%.3e", i ? " " : "", r[i]);
+    out += buf;
+  }
+  return out + "]";
+}
+
+[[noreturn]] void throw_lanczos(const EigRun& run, double tol) {
+  char buf[128];
+  snprintf(buf, sizeof buf, "residual tolerance %g not reached after %d block passes (best residuals ", tol,
+           run.passes);
+  throw Error(MEGB200_ERR_LANCZOS, std::string(buf) + fmt_resid(run.resid) + ")");
+}
+
+// ---------------------------------------------------------------------------
+// MEG step operator: A = log X - eta grad  (logmap_operator, meg.py:287-307)
+
+struct StepOperator {
+  OpDev op;
+  std::vector<double> d;  // host coefficients of the gathered low-rank factor
+};
+
+void check_iterate(megb200_solver* s, const megb200_iterate* x) {
+  if (!x) throw Error(MEGB200_ERR_PARAM, "iterate is NULL");
+  if (x->n != s->n) throw Error(MEGB200_ERR_PARAM, "iterate dimension does not match the solver");
+  if (!(1 <= x->r && x->r < x->n)) throw Error(MEGB200_ERR_PARAM, "need 1 <= r < n");
+  if (!x->V || !x->lam) throw Error(MEGB200_ERR_PARAM, "iterate factors missing");
+  if (!(x->eps > 0.0 && x->eps <= 0.75)) throw Error(MEGB200_ERR_PARAM, "eps must lie in (0, 3/4]");
+  for (int64_t k = 0; k < x->r; ++k)
+    if (!(x->lam[k] > 0.0)) throw Error(MEGB200_ERR_PARAM, "lam must be strictly positive");
+}
+
+void check_gradient(megb200_solver* s, const megb200_gradient* g) {
+  if (!g) throw Error(MEGB200_ERR_PARAM, "gradient is NULL");
+  if (g->n != s->n) throw Error(MEGB200_ERR_PARAM, "gradient dimension does not match the solver");
+  switch (g->kind) {
+    case MEGB200_GRAD_ZERO:
+      break;
+    case MEGB200_GRAD_DENSE:
+      if (!g->dense || g->ld < g->n) throw Error(MEGB200_ERR_PARAM, "dense gradient operand missing");
+      break;
+    case MEGB200_GRAD_FROBENIUS:
+    case MEGB200_GRAD_STOCHASTIC:
+      if (!g->dense || g->ld < g->n) throw Error(MEGB200_ERR_PARAM, "target matrix M missing");
+      if (!g->gV || !g->g_lam || g->g_r < 1) throw Error(MEGB200_ERR_PARAM, "gradient iterate factors missing");
+      if (g->kind == MEGB200_GRAD_STOCHASTIC && (!g->A || g->bsz < 1))
+        throw Error(MEGB200_ERR_PARAM, "stochastic minibatch missing");
+      break;
+    case MEGB200_GRAD_SAMPLED:
+      if (!g->rowptr || !g->col || !g->obs) throw Error(MEGB200_ERR_PARAM, "sampled pattern missing");
+      if (g->nnz > s->max_nnz) throw Error(MEGB200_ERR_PARAM, "nnz exceeds the solver's max_nnz");
+      if (!g->gV || !g->g_lam || g->g_r < 1) throw Error(MEGB200_ERR_PARAM, "gradient iterate factors missing");
+      break;
+    default:
+      throw Error(MEGB200_ERR_PARAM, "unknown gradient kind");
+  }
+  if (g->gV && (g->g_r >= g->n || !(g->g_eps > 0.0)) && g->kind != MEGB200_GRAD_ZERO && g->kind != MEGB200_GRAD_DENSE)
+    throw Error(MEGB200_ERR_PARAM, "invalid gradient iterate");
+}
+
+// X_g coefficients: c_k = (1 - eps) lam_k - tail, tail = eps / (n - r)
+void x_coeffs(int64_t n, int64_t r, const double* lam, double eps, std::vector<double>& c, double& tail) {
+  tail = eps / (double)(n - r);
+  c.resize(r);
+  for (int64_t k = 0; k < r; ++k) c[k] = (1.0 - eps) * lam[k] - tail;
+}
+
+StepOperator build_step_operator(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g,
+                                 double eta) {
+  Launch L = s->launch();
+  const int64_t n = s->n, r = x->r;
+  StepOperator so;
+  OpDev& op = so.op;
+  // log X = V diag(log_kept - log_tail) V^T + log_tail I
+  const double tail_x = x->eps / (double)(n - r);
+  const double log_tail = log(tail_x);
+  std::vector<double> dx(r);
+  for (int64_t k = 0; k < r; ++k) dx[k] = log((1.0 - x->eps) * x->lam[k]) - log_tail;
+  op.alpha = log_tail;
+  bool merged = false;
+  std::vector<double> cg;
+  double tail_g = 0.0;
+  if (g->kind == MEGB200_GRAD_FROBENIUS || g->kind == MEGB200_GRAD_STOCHASTIC || g->kind == MEGB200_GRAD_SAMPLED)
+    x_coeffs(n, g->g_r, g->g_lam, g->g_eps, cg, tail_g);
+  switch (g->kind) {
+    case MEGB200_GRAD_ZERO:
+      op.kind = MEGB200_OP_NONE;
+      break;
+    case MEGB200_GRAD_DENSE:
+      op.kind = MEGB200_OP_DENSE;
+      op.dtype = g->dtype;
+      op.dense = g->dense;
+      op.ld = g->ld;
+      op.scale = -eta;
+      break;
+    case MEGB200_GRAD_FROBENIUS:
+    case MEGB200_GRAD_STOCHASTIC:
+      // -eta (X_g - M) = eta M - eta Vg diag(c) Vg^T - eta tail_g I
+      op.kind = MEGB200_OP_DENSE;
+      op.dtype = g->dtype;
+      op.dense = g->dense;
+      op.ld = g->ld;
+      op.scale = eta;
+      op.alpha += -eta * tail_g;
+      merged = (g->gV == x->V && g->g_r == r && g->g_ldv == x->ldv);
+      break;
+    case MEGB200_GRAD_SAMPLED: {
+      // -eta P_Omega(X_g - Mobs): values from the factors, once per step
+      double* dcoef = s->small;
+      s->h2d(dcoef, cg.data(), (int64_t)cg.size());
+      csr_values(L, n, g->rowptr, g->col, g->obs, g->gV, g->g_ldv, (int)g->g_r, dcoef, tail_g, s->csr_g, nullptr,
+                 0);
+      op.kind = MEGB200_OP_CSR;
+      op.rowptr = g->rowptr;
+      op.col = g->col;
+      op.val = s->csr_g;
+      op.scale = -eta;
+      break;
+    }
+  }
+  // gather low-rank factors: [V_x | V_g (unless merged) | A]
+  std::vector<double>& d = so.d;
+  d = dx;
+  if (merged)
+    for (int64_t k = 0; k < r; ++k) d[k] += -eta * cg[k];
+  const bool need_g = (g->kind == MEGB200_GRAD_FROBENIUS || g->kind == MEGB200_GRAD_STOCHASTIC) && !merged;
+  const bool need_a = g->kind == MEGB200_GRAD_STOCHASTIC;
+  const int64_t l = r + (need_g ? g->g_r : 0) + (need_a ? g->bsz : 0);
+  if (l > s->max_lowrank) throw Error(MEGB200_ERR_PARAM, "low-rank width exceeds the solver's max_lowrank");
+  if (!need_g && !need_a) {
+    op.L = x->V;
+    op.ldl = x->ldv;
+  } else {
+    copy_block(L, n, (int)r, x->V, x->ldv, s->L, s->max_lowrank);
+    int64_t off = r;
+    if (need_g) {
+      copy_block(L, n, (int)g->g_r, g->gV, g->g_ldv, s->L + off, s->max_lowrank);
+      for (int64_t k = 0; k < g->g_r; ++k) d.push_back(-eta * cg[k]);
+      off += g->g_r;
+    }
+    if (need_a) {
+      copy_block(L, n, (int)g->bsz, g->A, g->lda, s->L + off, s->max_lowrank);
+      for (int64_t k = 0; k < g->bsz; ++k) d.push_back(-eta * g->sigma / (double)g->bsz);
+      op.alpha += eta * g->sigma / (double)n;
+    }
+    op.L = s->L;
+    op.ldl = s->max_lowrank;
+  }
+  op.l = (int)l;
+  s->h2d(s->dvec, d.data(), l);
+  op.d_dev = s->dvec;
+  return so;
+}
+
+// Gram error max |V^T V - I| for an n x r block (LowRankIterate validation, meg.py:69-71)
+double gram_error(megb200_solver* s, const double* V, int64_t ldv, int r) {
+  Launch L = s->launch();
+  tn(L, s->n, V, ldv, r, V, ldv, r, s->G, r, nullptr, s->red, s->red_cap, s->sm_count);
+  std::vector<double> g((size_t)r * r);
+  s->d2h(g.data(), s->G, (int64_t)r * r);
+  s->sync();
+  double e = 0.0;
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < r; ++j) e = std::max(e, fabs(g[(size_t)i * r + j] - (i == j ? 1.0 : 0.0)));
+  return e;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+
+namespace {
+int guarded_impl(const std::function<void()>& body) {
+  try {
+    body();
+    return MEGB200_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MEGB200_ERR_CUDA;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return MEGB200_ERR_CUDA;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int megb200_abi_version(void) { return MEGB200_ABI_VERSION; }
+
+const char* megb200_last_error(void) { return g_last_error.c_str(); }
+
+int megb200_device_check(int* sm_count) {
+  return guarded_impl([&] {
+    int dev = 0, count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) throw Error(MEGB200_ERR_NO_DEVICE, "no CUDA device visible");
+    MEG_CUDA(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    MEG_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+      throw Error(MEGB200_ERR_NO_DEVICE, std::string("device is not sm_100 (Blackwell): ") + prop.name);
+    if (sm_count) *sm_count = prop.multiProcessorCount;
+  });
+}
+
+int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64_t max_lowrank, int64_t max_nnz,
+                          megb200_solver** out) {
+  return guarded_impl([&] {
+    if (!out) throw Error(MEGB200_ERR_PARAM, "out is NULL");
+    if (n < 2) throw Error(MEGB200_ERR_PARAM, "need n >= 2");
+    if (max_block < 1 || max_block > kMaxBlock) throw Error(MEGB200_ERR_PARAM, "max_block must be in [1, 64]");
+    if (max_basis < 2 || max_basis > kMaxBasis) throw Error(MEGB200_ERR_PARAM, "max_basis must be in [2, 112]");
+    int sm = 148;
+    int rc = megb200_device_check(&sm);
+    if (rc != MEGB200_OK) throw Error(rc, g_last_error);
+    auto* s = new megb200_solver();
+    s->n = n;
+    s->max_block = max_block;
+    s->max_basis = max_basis;
+    s->cap = max_basis + max_block;
+    s->max_lowrank = std::max<int64_t>(1, max_lowrank);
+    s->max_nnz = std::max<int64_t>(0, max_nnz);
+    s->sm_count = sm;
+    s->ldq = s->cap;
+    // apply partial slices: enough to fill the GPU for small n; bounded memory for large n
+    const int64_t tiles = (n + 63) / 64;
+    s->part_slices = std::max<int64_t>(std::max<int64_t>(1, (2 * sm + tiles - 1) / tiles), (n + 4095) / 4096);
+    s->part_slices = std::min<int64_t>(s->part_slices, 64);
+    s->red_cap = (int64_t)sm * std::max<int64_t>((int64_t)s->cap * std::max<int>(s->cap, max_block),
+                                                 s->max_lowrank * max_block);
+    struct Item {
+      double** p;
+      int64_t count;
+    };
+    const int64_t nb = n * (int64_t)max_block;
+    std::vector<Item> items = {
+        {&s->Q, n * s->ldq},
+        {&s->AQ, n * s->ldq},
+        {&s->T, n * s->ldq},
+        {&s->W, nb},
+        {&s->part, s->part_slices * nb},
+        {&s->red, s->red_cap},
+        {&s->L, n * s->max_lowrank},
+        {&s->E, s->max_lowrank * max_block},
+        {&s->dvec, s->max_lowrank},
+        {&s->H, (int64_t)s->cap * s->cap},
+        {&s->C, (int64_t)s->cap * max_block},
+        {&s->C2, (int64_t)s->cap * max_block},
+        {&s->G, (int64_t)s->cap * s->cap},
+        {&s->R1, (int64_t)max_block * max_block},
+        {&s->R2, (int64_t)max_block * max_block},
+        {&s->Rinv, (int64_t)max_block * max_block},
+        {&s->Rn, (int64_t)max_block * max_block},
+        {&s->Rtmp, (int64_t)max_block * max_block},
+        {&s->theta, s->cap},
+        {&s->S, (int64_t)s->cap * s->cap},
+        {&s->est, s->cap},
+        {&s->info, 16},
+        {&s->resid, s->cap},
+        {&s->small, 4096},
+        {&s->csr_g, std::max<int64_t>(1, s->max_nnz)},
+        {&s->rowsq, n},
+    };
+    int64_t total = 0;
+    for (auto& it : items) total += align_up(it.count * (int64_t)sizeof(double), 256);
+    total += align_up(kMaxBlock * sizeof(int), 256);
+    cudaError_t e = cudaMalloc(&s->arena, total);
+    if (e != cudaSuccess) {
+      delete s;
+      throw Error(MEGB200_ERR_CUDA, std::string("workspace allocation failed: ") + cudaGetErrorString(e));
+    }
+    s->arena_bytes = total;
+    int64_t off = 0;
+    for (auto& it : items) {
+      *it.p = reinterpret_cast<double*>(s->arena + off);
+      off += align_up(it.count * (int64_t)sizeof(double), 256);
+    }
+    s->mask = reinterpret_cast<int*>(s->arena + off);
+    s->h_buf_len = 4 * (int64_t)s->cap + 4096;
+    e = cudaMallocHost(&s->h_buf, s->h_buf_len * sizeof(double));
+    if (e != cudaSuccess) {
+      cudaFree(s->arena);
+      delete s;
+      throw Error(MEGB200_ERR_CUDA, "pinned staging allocation failed");
+    }
+    *out = s;
+  });
+}
+
+void megb200_solver_destroy(megb200_solver* s) {
+  if (!s) return;
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  cudaFree(s->arena);
+  cudaFreeHost(s->h_buf);
+  delete s;
+}
+
+int megb200_solver_set_stream(megb200_solver* s, void* stream) {
+  return guarded_impl([&] {
+    if (!s) throw Error(MEGB200_ERR_PARAM, "solver is NULL");
+    s->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+int64_t megb200_solver_workspace_bytes(const megb200_solver* s) { return s ? s->arena_bytes : 0; }
+
+int64_t megb200_kernel_launches(const megb200_solver* s) { return s ? s->launches : 0; }
+
+int megb200_operator_apply(megb200_solver* s, const megb200_operator* op, const double* U, int64_t ldu, int32_t k,
+                           double* W, int64_t ldw) {
+  return guarded_impl([&] {
+    if (!s) throw Error(MEGB200_ERR_PARAM, "solver is NULL");
+    if (!U || !W || k < 1) throw Error(MEGB200_ERR_PARAM, "invalid block");
+    OpDev o = op_from_public(s, op);
+    apply_op_wide(s, o, U, ldu, k, W, ldw);
+  });
+}
+
+int megb200_logmap_apply(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta,
+                         const double* U, int64_t ldu, int32_t k, double* W, int64_t ldw) {
+  return guarded_impl([&] {
+    if (!s) throw Error(MEGB200_ERR_PARAM, "solver is NULL");
+    check_iterate(s, x);
+    check_gradient(s, g);
+    if (!U || !W || k < 1) throw Error(MEGB200_ERR_PARAM, "invalid block");
+    StepOperator so = build_step_operator(s, x, g, eta);
+    apply_op_wide(s, so.op, U, ldu, k, W, ldw);
+  });
+}
+
+int megb200_top_r(megb200_solver* s, const megb200_operator* op, int32_t r, const megb200_eig_opts* opts,
+                  megb200_eig_result* out) {
+  return guarded_impl([&] {
+    if (!s || !out) throw Error(MEGB200_ERR_PARAM, "solver/result is NULL");
+    if (!(1 <= r && r < s->n))
+      throw Error(MEGB200_ERR_PARAM, "need 1 <= r < n, got r=" + std::to_string(r) + ", n=" + std::to_string(s->n));
+    OpDev o = op_from_public(s, op);
+    EigParams P = params_from_opts(opts);
+    int rc = 0;
+    EigRun run = top_eigs(s, o, r, P, out->eigenvectors, out->ld_vec, out->ritz_block, out->ld_ritz, &rc);
+    out->ritz_cols = out->ritz_block ? rc : 0;
+    out->passes = run.passes;
+    out->restarts = run.restarts;
+    out->norm_est = run.norm_est;
+    if (out->residual_norms)
+      for (int j = 0; j < r; ++j) out->residual_norms[j] = run.resid[j];
+    if (!run.converged) throw_lanczos(run, P.tol);
+    if (out->eigenvalues)
+      for (int j = 0; j < r; ++j) out->eigenvalues[j] = run.theta[j];
+    s->sync();
+  });
+}
+
+int megb200_certificate_cheap(double lam_rp1, double b_rp1, double eps, int64_t n, int64_t r, double* lhs,
+                              int32_t* holds, double* threshold) {
+  return guarded_impl([&] {
+    if (!(b_rp1 > 0.0)) throw Error(MEGB200_ERR_PARAM, "partial trace must be positive");
+    if (lam_rp1 < 0.0) throw Error(MEGB200_ERR_PARAM, "lambda_(r+1) must be non-negative");
+    const double v = lam_rp1 == 0.0 ? -INFINITY : log((double)(n - r) * lam_rp1 / (eps * b_rp1));
+    if (lhs) *lhs = v;
+    if (holds) *holds = v <= 2.0 * eps;
+    if (threshold) *threshold = 2.0 * eps;
+  });
+}
+
+int megb200_lowrank_meg_step(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta,
+                             double eps_next, const megb200_eig_opts* opts, megb200_step_result* out) {
+  return guarded_impl([&] {
+    if (!s || !out) throw Error(MEGB200_ERR_PARAM, "solver/result is NULL");
+    if (!(eps_next > 0.0 && eps_next <= 0.75))
+      throw Error(MEGB200_ERR_PARAM, "eps_next must lie in (0, 3/4], got " + std::to_string(eps_next));
+    check_iterate(s, x);
+    check_gradient(s, g);
+    if (!out->V_next || !out->lam_next || !out->y) throw Error(MEGB200_ERR_PARAM, "step outputs missing");
+    const int r = (int)x->r, nreq = r + 1;
+    if (nreq >= s->n) throw Error(MEGB200_ERR_PARAM, "need r + 1 < n");
+    Launch L = s->launch();
+    StepOperator so = build_step_operator(s, x, g, eta);
+    EigParams P = params_from_opts(opts);
+    // warm start: caller's Ritz block if given, else the iterate's own factor V
+    if (!P.warm) {
+      P.warm = x->V;
+      P.warm_cols = r;
+      P.ld_warm = x->ldv;
+    }
+    int rc = 0;
+    EigRun run = top_eigs(s, so.op, nreq, P, nullptr, 0, out->ritz_block, out->ld_ritz, &rc);
+    out->ritz_cols = out->ritz_block ? rc : 0;
+    out->passes = run.passes;
+    out->restarts = run.restarts;
+    if (out->residual_norms)
+      for (int j = 0; j < nreq; ++j) out->residual_norms[j] = run.resid[j];
+    if (!run.converged) throw_lanczos(run, P.tol);
+    // next iterate: V = top r Ritz vectors (still in T), lam / certificate by the epilogue kernel
+    copy_block(L, s->n, r, s->T, s->ldq, out->V_next, out->ld_next);
+    step_epilogue(L, s->theta, r, s->n, eps_next, s->small);
+    const int olen = 2 * r + 1 + 7;
+    double* hb = s->h_buf;
+    s->d2h(hb, s->small, olen);
+    s->sync();
+    const double status = hb[2 * r + 1 + 6];
+    if (status == 4.0) throw Error(MEGB200_ERR_KEPT_MASS, "kept mass vanished despite max-shift");
+    if (status == 1.0) throw Error(MEGB200_ERR_PARAM, "certificate inputs invalid (partial trace <= 0 or lambda < 0)");
+    for (int k = 0; k < nreq; ++k) out->y[k] = hb[k];
+    for (int k = 0; k < r; ++k) out->lam_next[k] = hb[nreq + k];
+    if (out->mu)
+      for (int k = 0; k < nreq; ++k) out->mu[k] = run.theta[k];
+    const double* t = hb + 2 * r + 1;
+    out->lambda_r_plus_1 = t[0];
+    out->b_r_plus_1 = t[1];
+    out->shift = t[2];
+    out->lhs_cheap = t[3];
+    out->holds_cheap = t[4] != 0.0;
+    out->threshold = t[5];
+    out->gram_err = gram_error(s, out->V_next, out->ld_next, r);
+  });
+}
+
+int megb200_dense_stats(megb200_solver* s, const void* M, int32_t dtype, int64_t ld, double* norm2, double* trace) {
+  return guarded_impl([&] {
+    if (!s || !M) throw Error(MEGB200_ERR_PARAM, "solver/operand is NULL");
+    Launch L = s->launch();
+    const int slots = std::min<int>(s->sm_count * 2, 1024);
+    dense_stats(L, M, dtype, ld, s->n, s->red, slots);
+    reduce_sum(L, s->red, slots, 2, s->small);
+    double h[2];
+    s->d2h(h, s->small, 2);
+    s->sync();
+    if (norm2) *norm2 = h[0];
+    if (trace) *trace = h[1];
+  });
+}
+
+int megb200_objective_value(megb200_solver* s, const megb200_gradient* g, double m_norm2, double m_trace,
+                            double* value) {
+  return guarded_impl([&] {
+    if (!s || !value) throw Error(MEGB200_ERR_PARAM, "solver/value is NULL");
+    check_gradient(s, g);
+    Launch L = s->launch();
+    const int64_t n = s->n, r = g->g_r;
+    std::vector<double> c;
+    double tail = 0.0;
+    x_coeffs(n, r, g->g_lam, g->g_eps, c, tail);
+    if (g->kind == MEGB200_GRAD_SAMPLED) {
+      s->h2d(s->small, c.data(), r);
+      csr_values(L, n, g->rowptr, g->col, g->obs, g->gV, g->g_ldv, (int)r, s->small, tail, nullptr, s->rowsq, 0);
+      // sum of per-row squares in fixed order: tn of a column vector with ones is avoided; reuse reduce over slots
+      const int slots = (int)std::min<int64_t>(n, 1024);
+      // rows -> slots partial sums via tn-like two-level reduction: treat rowsq as (n x 1) and use tn with a ones column
+      std::vector<double> ones((size_t)n, 1.0);
+      double* d_ones = s->T;  // n doubles of scratch (ld ldq) -> use contiguous column view of T
+      s->h2d(d_ones, ones.data(), n);
+      tn(L, n, s->rowsq, 1, 1, d_ones, 1, 1, s->small + 64, 1, nullptr, s->red, s->red_cap, s->sm_count);
+      (void)slots;
+      double h = 0.0;
+      s->d2h(&h, s->small + 64, 1);
+      s->sync();
+      *value = 0.5 * h;
+      return;
+    }
+    if (g->kind != MEGB200_GRAD_FROBENIUS && g->kind != MEGB200_GRAD_STOCHASTIC)
+      throw Error(MEGB200_ERR_PARAM, "objective value needs a Frobenius or sampled gradient descriptor");
+    if (isnan(m_norm2) || isnan(m_trace)) {
+      if (s->m_cache_ptr != g->dense) {
+        double a = 0, b = 0;
+        int rc = megb200_dense_stats(s, g->dense, g->dtype, g->ld, &a, &b);
+        if (rc != MEGB200_OK) throw Error(rc, g_last_error);
+        s->m_norm2_cache = a;
+        s->m_trace_cache = b;
+        s->m_cache_ptr = g->dense;
+      }
+      if (isnan(m_norm2)) m_norm2 = s->m_norm2_cache;
+      if (isnan(m_trace)) m_trace = s->m_trace_cache;
+    }
+    // M V -> T[:, 0:r]; diag(V^T M V)
+    OpDev op;
+    op.kind = MEGB200_OP_DENSE;
+    op.dtype = g->dtype;
+    op.dense = g->dense;
+    op.ld = g->ld;
+    op.scale = 1.0;
+    apply_op_wide(s, op, g->gV, g->g_ldv, (int)r, s->T, s->ldq);
+    tn(L, n, g->gV, g->g_ldv, (int)r, s->T, s->ldq, (int)r, s->G, r, nullptr, s->red, s->red_cap, s->sm_count);
+    std::vector<double> vmv((size_t)r * r);
+    s->d2h(vmv.data(), s->G, r * r);
+    s->sync();
+    double x2 = tail * tail * (double)(n - r), inner = tail * m_trace;
+    for (int64_t k = 0; k < r; ++k) {
+      const double kept = (1.0 - g->g_eps) * g->g_lam[k];
+      x2 += kept * kept;
+      inner += c[k] * vmv[(size_t)k * r + k];
+    }
+    *value = 0.5 * (x2 - 2.0 * inner + m_norm2);
+  });
+}
+
+int megb200_dual_gap(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts, double m_trace,
+                     double* gap, double* lambda_min) {
+  return guarded_impl([&] {
+    if (!s) throw Error(MEGB200_ERR_PARAM, "solver is NULL");
+    check_gradient(s, g);
+    if (g->kind != MEGB200_GRAD_FROBENIUS && g->kind != MEGB200_GRAD_STOCHASTIC)
+      throw Error(MEGB200_ERR_PARAM, "dual gap needs a Frobenius gradient descriptor");
+    const int64_t n = s->n, r = g->g_r;
+    std::vector<double> c;
+    double tail = 0.0;
+    x_coeffs(n, r, g->g_lam, g->g_eps, c, tail);
+    // -grad = M - X = M - Vg diag(c) Vg^T - tail I; its top eigenvalue is -lambda_min(grad)
+    OpDev op;
+    op.kind = MEGB200_OP_DENSE;
+    op.dtype = g->dtype;
+    op.dense = g->dense;
+    op.ld = g->ld;
+    op.scale = 1.0;
+    op.L = g->gV;
+    op.ldl = g->g_ldv;
+    op.l = (int)r;
+    std::vector<double> d(r);
+    for (int64_t k = 0; k < r; ++k) d[k] = -c[k];
+    s->h2d(s->dvec, d.data(), r);
+    op.d_dev = s->dvec;
+    op.alpha = -tail;
+    EigParams P = params_from_opts(opts);
+    EigRun run = top_eigs(s, op, 1, P, nullptr, 0, nullptr, 0, nullptr);
+    if (!run.converged) throw_lanczos(run, P.tol);
+    const double lmin = -run.theta[0];
+    // Tr(X grad) = ||X||^2 - <X, M>
+    if (isnan(m_trace)) {
+      double a = 0, b = 0;
+      int rc = megb200_dense_stats(s, g->dense, g->dtype, g->ld, &a, &b);
+      if (rc != MEGB200_OK) throw Error(rc, g_last_error);
+      m_trace = b;
+    }
+    Launch L = s->launch();
+    OpDev mop;
+    mop.kind = MEGB200_OP_DENSE;
+    mop.dtype = g->dtype;
+    mop.dense = g->dense;
+    mop.ld = g->ld;
+    mop.scale = 1.0;
+    apply_op_wide(s, mop, g->gV, g->g_ldv, (int)r, s->T, s->ldq);
+    tn(L, n, g->gV, g->g_ldv, (int)r, s->T, s->ldq, (int)r, s->G, r, nullptr, s->red, s->red_cap, s->sm_count);
+    std::vector<double> vmv((size_t)r * r);
+    s->d2h(vmv.data(), s->G, r * r);
+    s->sync();
+    double x2 = tail * tail * (double)(n - r), inner = tail * m_trace;
+    for (int64_t k = 0; k < r; ++k) {
+      const double kept = (1.0 - g->g_eps) * g->g_lam[k];
+      x2 += kept * kept;
+      inner += c[k] * vmv[(size_t)k * r + k];
+    }
+    if (gap) *gap = (x2 - inner) - lmin;
+    if (lambda_min) *lambda_min = lmin;
+  });
+}
+
+int megb200_gen_dense_target(megb200_solver* s, const double* U, int64_t r, const double* lam_host, double sigma,
+                             uint64_t seed, int32_t stream, void* M, int32_t dtype, int64_t ld) {
+  return guarded_impl([&] {
+    if (!s || !U || !M || !lam_host) throw Error(MEGB200_ERR_PARAM, "null argument");
+    if (r < 0 || r > 64) throw Error(MEGB200_ERR_PARAM, "r must be in [0, 64]");
+    s->h2d(s->small, lam_host, r);
+    gen_dense_target(s->launch(), U, r, s->small, sigma, stream_key(seed, (uint64_t)stream), M, dtype, ld, s->n);
+    s->sync();
+  });
+}
+
+int megb200_gram_error(megb200_solver* s, const double* V, int64_t ldv, int32_t r, double* err) {
+  return guarded_impl([&] {
+    if (!s || !V || !err) throw Error(MEGB200_ERR_PARAM, "null argument");
+    if (r < 1 || r > s->cap) throw Error(MEGB200_ERR_PARAM, "r out of range");
+    *err = gram_error(s, V, ldv, r);
+  });
+}
+
+int megb200_gen_gaussian(megb200_solver* s, uint64_t seed, int32_t stream, uint64_t base, int64_t n, int64_t k,
+                         double scale, int32_t round_f32, double* out, int64_t ld) {
+  return guarded_impl([&] {
+    if (!s || !out) throw Error(MEGB200_ERR_PARAM, "null argument");
+    fill_gaussian(s->launch(), n, (int)k, stream_key(seed, (uint64_t)stream), base, scale, round_f32 != 0, out, ld);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,248 @@
+"""Device gradient descriptors: the B200 form of the reference's `grad_apply` boundary.
+
+The reference step takes any callable u -> grad f(X) u (meg.py:327-335; the
+test objective `frobenius_objective`, test_meg.py:28-35, is used as
+`lambda u: g @ u` at :153).  The device solver cannot call Python per
+application, so gradients are descriptors whose data live in HBM:
+
+    DenseGradient(G)                  grad u = G u           (a fixed dense gradient)
+    FrobeniusObjective(M)             f = 1/2 ||X - M||_F^2,  grad u = X u - M u
+    SampledObjective(Omega, Mobs)     f = 1/2 sum_Omega (X_ij - Mobs_ij)^2, grad = P_Omega(X - Mobs)
+    StochasticFrobeniusObjective(M)   grad estimate X - M + sigma((1/b) A_t A_t^T - I/n)
+    ZeroGradient(n)
+
+`objective.grad_operator(x)` binds the gradient to an iterate X (factors
+stay on device; X u is evaluated from them, never densified).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from . import _lib, runtime
+from .errors import ParameterError
+
+# residual-rule floor for float32 operands: the fp32 product's rounding noise
+# (~1e-8 relative to ||A||) sits above the fp64 default tol of 1e-10
+F32_TOL_FLOOR = 1e-7
+
+
+class GradientOperator:
+    """A gradient evaluated at a bound iterate (device descriptor, see module doc)."""
+
+    def __init__(self, kind: int, n: int, *, dense=None, csr=None, obs=None, x=None, A=None, sigma: float = 0.0,
+                 owner=None):
+        self.kind = kind
+        self.n = int(n)
+        self.dense = dense
+        self.csr = csr
+        self.obs = obs
+        self.x = x
+        self.A = A
+        self.sigma = float(sigma)
+        self.owner = owner
+
+    @property
+    def tol_floor(self) -> float:
+        if self.dense is not None and self.dense.dtype == torch.float32:
+            return F32_TOL_FLOOR
+        return 0.0
+
+    @property
+    def nnz(self) -> int:
+        return int(self.csr[1].numel()) if self.csr is not None else 0
+
+    @property
+    def lowrank_width(self) -> int:
+        w = 0
+        if self.x is not None:
+            w += self.x.r
+        if self.A is not None:
+            w += self.A.shape[1]
+        return w
+
+    def struct(self, keep: list) -> _lib.Gradient:
+        g = _lib.Gradient()
+        g.kind = self.kind
+        g.n = self.n
+        if self.dense is not None:
+            g.dtype = runtime.dtype_code(self.dense)
+            g.dense = self.dense.data_ptr()
+            g.ld = self.dense.stride(0)
+        if self.csr is not None:
+            rp, cl = self.csr
+            g.rowptr, g.col = rp.data_ptr(), cl.data_ptr()
+            g.nnz = cl.numel()
+            g.obs = self.obs.data_ptr()
+        if self.x is not None:
+            lam = runtime.host_f64(self.x.lam)
+            keep.append(lam)
+            g.gV = self.x.V_device.data_ptr()
+            g.g_r = self.x.r
+            g.g_ldv = self.x.V_device.stride(0)
+            g.g_lam = _lib.dptr(lam)
+            g.g_eps = float(self.x.eps)
+        if self.A is not None:
+            g.A = self.A.data_ptr()
+            g.bsz = self.A.shape[1]
+            g.lda = self.A.stride(0)
+            g.sigma = self.sigma
+        return g
+
+    def solver(self):
+        return runtime.solver_for(self.n, max_nnz=self.nnz,
+                                  max_lowrank=max(runtime.MAX_LOWRANK, 2 * self.lowrank_width + 8))
+
+    def __call__(self, u):  # pragma: no cover - guard against reference-style use
+        raise TypeError("device gradient descriptors are consumed by lowrank_meg_step; they are not host callables")
+
+
+class ZeroGradient(GradientOperator):
+    def __init__(self, n: int):
+        super().__init__(_lib.GRAD_ZERO, n)
+
+
+class DenseGradient(GradientOperator):
+    """grad u = G u for a fixed dense symmetric G (symmetrised on upload, linalg.py:96-99)."""
+
+    def __init__(self, g, dtype: str = "f64"):
+        t = runtime.as_device_operand(g, "f64")
+        t = 0.5 * (t + t.T)
+        if dtype == "f32":
+            t = t.to(torch.float32)
+        super().__init__(_lib.GRAD_DENSE, t.shape[0], dense=t.contiguous())
+
+
+class FrobeniusObjective:
+    """f(X) = 1/2 ||X - M||_F^2 with M resident in HBM (f64 or f32)."""
+
+    def __init__(self, m, dtype: str = "f64", symmetrize: bool = True):
+        t = runtime.as_device_operand(m, "f64") if not (isinstance(m, torch.Tensor) and m.is_cuda) else m
+        if symmetrize:
+            t = 0.5 * (t.to(torch.float64) + t.to(torch.float64).T)
+        t = t.to(torch.float64 if dtype == "f64" else torch.float32).contiguous()
+        self.m = t
+        self.n = t.shape[0]
+        self.dtype = dtype
+        s = runtime.solver_for(self.n)
+        a, b = C.c_double(), C.c_double()
+        runtime.check(s.lib.megb200_dense_stats(s.handle, t.data_ptr(), runtime.dtype_code(t), t.stride(0),
+                                                C.byref(a), C.byref(b)))
+        self.m_norm2 = a.value
+        self.m_trace = b.value
+
+    @classmethod
+    def from_device(cls, m: torch.Tensor, dtype: str) -> "FrobeniusObjective":
+        """Wrap a device matrix already symmetric (e.g. from the device generator) without copying."""
+        obj = cls.__new__(cls)
+        obj.m = m
+        obj.n = m.shape[0]
+        obj.dtype = dtype
+        s = runtime.solver_for(obj.n)
+        a, b = C.c_double(), C.c_double()
+        runtime.check(s.lib.megb200_dense_stats(s.handle, m.data_ptr(), runtime.dtype_code(m), m.stride(0),
+                                                C.byref(a), C.byref(b)))
+        obj.m_norm2 = a.value
+        obj.m_trace = b.value
+        return obj
+
+    def grad_operator(self, x, t: int = 0) -> GradientOperator:
+        return GradientOperator(_lib.GRAD_FROBENIUS, self.n, dense=self.m, x=x, owner=self)
+
+    def value(self, x) -> float:
+        """1/2 ||X - M||_F^2 from the factors: one pass M V."""
+        g = self.grad_operator(x)
+        s = g.solver()
+        keep: list = []
+        gs = g.struct(keep)
+        v = C.c_double()
+        runtime.check(s.lib.megb200_objective_value(s.handle, C.byref(gs), self.m_norm2, self.m_trace, C.byref(v)))
+        return v.value
+
+    def dual_gap(self, x, tol: float = 1e-10, seed: int = 0, block: int | None = None,
+                 subspace: int | None = None) -> tuple[float, float]:
+        """Tr(X grad) - lambda_min(grad), grad = X - M (_dual_gap_core, objectives.py:332-335).
+
+        Returns (gap, lambda_min).  lambda_min comes from the block solver on
+        M - X (the top eigenpair of -grad, as the reference computes it).
+        """
+        from .linalg import _eig_opts
+
+        g = self.grad_operator(x)
+        s = g.solver()
+        keep: list = []
+        gs = g.struct(keep)
+        tol = max(tol, g.tol_floor)
+        opts = _eig_opts(tol, None, seed, subspace, 12, block)
+        gap, lmin = C.c_double(), C.c_double()
+        runtime.check(s.lib.megb200_dual_gap(s.handle, C.byref(gs), C.byref(opts), self.m_trace, C.byref(gap),
+                                             C.byref(lmin)), residual_norms=[])
+        return gap.value, lmin.value
+
+
+class SampledObjective:
+    """f(X) = 1/2 sum_{(i,j) in Omega} (X_ij - Mobs_ij)^2 with a symmetric CSR pattern Omega."""
+
+    def __init__(self, n: int, rowptr, col, obs):
+        dev = runtime.device()
+        self.n = int(n)
+        self.rowptr = torch.as_tensor(np.asarray(rowptr, dtype=np.int32)).to(dev)
+        self.col = torch.as_tensor(np.asarray(col, dtype=np.int32)).to(dev)
+        self.obs = runtime.as_device_f64(obs)
+        if self.rowptr.numel() != self.n + 1 or self.col.numel() != self.obs.numel():
+            raise ParameterError("inconsistent CSR arrays")
+
+    def grad_operator(self, x, t: int = 0) -> GradientOperator:
+        return GradientOperator(_lib.GRAD_SAMPLED, self.n, csr=(self.rowptr, self.col), obs=self.obs, x=x, owner=self)
+
+    def value(self, x) -> float:
+        g = self.grad_operator(x)
+        s = g.solver()
+        keep: list = []
+        gs = g.struct(keep)
+        v = C.c_double()
+        runtime.check(s.lib.megb200_objective_value(s.handle, C.byref(gs), math.nan, math.nan, C.byref(v)))
+        return v.value
+
+
+class StochasticFrobeniusObjective(FrobeniusObjective):
+    """grad estimate = X - M + sigma((1/b) A_t A_t^T - I/n), A_t ~ N(0, I/n)^{n x b}.
+
+    A_t is generated on device by the counter-based generator (stream 5,
+    counter (t n + i) b + j), the twin of oracle/inputs.minibatch, so no
+    per-iteration upload is needed.
+    """
+
+    def __init__(self, m, batch: int = 64, sigma: float = 0.05, seed: int = 0, dtype: str = "f32"):
+        super().__init__(m, dtype=dtype)
+        self._init_stochastic(batch, sigma, seed)
+
+    def _init_stochastic(self, batch, sigma, seed):
+        self.batch = int(batch)
+        self.sigma = float(sigma)
+        self.seed = int(seed)
+        self._a = torch.empty((self.n, self.batch), dtype=torch.float64, device=runtime.device())
+        self._a_t = None
+
+    @classmethod
+    def from_device(cls, m: torch.Tensor, dtype: str, batch: int = 64, sigma: float = 0.05, seed: int = 0):
+        obj = FrobeniusObjective.from_device.__func__(cls, m, dtype)
+        obj._init_stochastic(batch, sigma, seed)
+        return obj
+
+    def minibatch(self, t: int) -> torch.Tensor:
+        if self._a_t != t:
+            s = runtime.solver_for(self.n)
+            runtime.check(s.lib.megb200_gen_gaussian(
+                s.handle, self.seed, 5, int(t) * self.n * self.batch, self.n, self.batch, 1.0 / math.sqrt(self.n),
+                1 if self.dtype == "f32" else 0, self._a.data_ptr(), self._a.stride(0)))
+            self._a_t = t
+        return self._a
+
+    def grad_operator(self, x, t: int = 0) -> GradientOperator:
+        return GradientOperator(_lib.GRAD_STOCHASTIC, self.n, dense=self.m, x=x, A=self.minibatch(t),
+                                sigma=self.sigma, owner=self)

@@ -1,0 +1,233 @@
+"""Parity of the B200 path (through the C ABI) with the oracle and the reference goldens.
+
+Every test here needs a CUDA device; tolerances are the north_star's:
+1e-9 relative for float64 operands, 1e-4 relative for float32 operands.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import cpu_meg as om
+from oracle import inputs, objectives
+from tests.gpu_helpers import f_scale, random_lowrank_iterate_np, run_gpu
+from tests.parity import TOL, compare_trajectory, load_golden, normwise
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import paper_2012_10469_b200 as pkg
+
+    return pkg
+
+
+def random_symmetric(n, rng, scale=1.0):
+    return om.symmetrize(rng.standard_normal((n, n))) * scale
+
+
+# ---------------------------------------------------------------------------
+# lanczos_top_r known answers on the device solver (test_linalg.py:61-140)
+
+
+def test_top_r_diagonal(pb):
+    top = pb.lanczos_top_r(pb.SymmetricOperator.from_dense(np.diag([5.0, 4, 3, 2, 1])), r=2, seed=1)
+    assert np.allclose(top.eigenvalues, [5.0, 4.0], atol=1e-10)
+    assert np.allclose(np.abs(top.eigenvectors), np.eye(5)[:, :2], atol=1e-8)
+
+
+def test_top_r_algebraic_not_magnitude(pb):
+    top = pb.lanczos_top_r(pb.SymmetricOperator.from_dense(-np.diag(np.arange(1.0, 13))), r=1, seed=5)
+    assert np.allclose(top.eigenvalues, [-1.0], atol=1e-10)
+    assert np.allclose(np.abs(top.eigenvectors[:, 0]), np.eye(12)[:, 0], atol=1e-7)
+
+
+def test_top_r_repeated(pb):
+    top = pb.lanczos_top_r(pb.SymmetricOperator.from_dense(np.diag([2.0, 2, 2, 1, 0])), r=3, seed=11)
+    assert np.allclose(top.eigenvalues, [2.0, 2.0, 2.0], atol=1e-9)
+
+
+def test_top_r_errors(pb):
+    with pytest.raises(pb.ParameterError):
+        pb.lanczos_top_r(pb.SymmetricOperator.from_dense(np.eye(4)), r=4)
+    with pytest.raises(pb.ParameterError):
+        pb.lanczos_top_r(pb.SymmetricOperator.from_dense(np.eye(4)), r=0)
+    op = pb.SymmetricOperator.from_dense(random_symmetric(60, np.random.default_rng(2)))
+    with pytest.raises(pb.LanczosError) as err:
+        pb.lanczos_top_r(op, r=3, tol=1e-16, subspace=6, max_iter=8, restarts=1)
+    assert err.value.residual_norms.shape == (3,)
+
+
+@pytest.mark.parametrize("n,r,seed,aseed", [(100, 5, 3, 7), (200, 8, 2, 17), (1000, 12, 0, 5)])
+def test_top_r_matches_dense(pb, n, r, seed, aseed):
+    a = random_symmetric(n, np.random.default_rng(aseed))
+    w, v = om.full_eigh(a)
+    top = pb.lanczos_top_r(pb.SymmetricOperator.from_dense(a), r=r, seed=seed, subspace=96)
+    scale = max(1.0, np.abs(w).max())
+    assert np.max(np.abs(top.eigenvalues - w[:r])) <= 1e-8 * scale
+    ov = v[:, :r].T @ top.eigenvectors
+    assert np.max(np.arccos(np.clip(np.linalg.svd(ov, compute_uv=False), -1, 1))) <= 1e-6
+    assert np.max(np.abs(top.eigenvectors.T @ top.eigenvectors - np.eye(r))) <= 1e-10
+
+
+def test_top_r_deterministic(pb):
+    op = pb.SymmetricOperator.from_dense(random_symmetric(300, np.random.default_rng(4)))
+    t1, t2 = pb.lanczos_top_r(op, r=3, seed=9), pb.lanczos_top_r(op, r=3, seed=9)
+    assert np.array_equal(t1.eigenvalues, t2.eigenvalues)
+    assert np.array_equal(t1.eigenvectors, t2.eigenvectors)
+
+
+def test_operator_apply_f32_and_csr(pb):
+    rng = np.random.default_rng(3)
+    n = 777
+    a = random_symmetric(n, rng)
+    u = rng.standard_normal((n, 19))
+    a32 = a.astype(np.float32).astype(np.float64)
+    got = pb.SymmetricOperator.from_dense(a, dtype="f32").apply(u)
+    assert normwise(got, a32 @ u) <= 2e-6
+    import scipy.sparse as sp
+
+    mask = rng.random((n, n)) < 0.03
+    mask = np.triu(mask) | np.triu(mask).T
+    g = sp.csr_matrix(np.where(mask, a, 0.0))
+    op = pb.SymmetricOperator.from_csr(n, g.indptr, g.indices, g.data, scale=-0.5)
+    assert normwise(op.apply(u), -0.5 * (g @ u)) <= 1e-14
+
+
+# ---------------------------------------------------------------------------
+# step, operator, certificates (test_meg.py)
+
+
+def test_step_diagonal_oracle(pb):
+    """test_meg.py:127-131."""
+    x = pb.LowRankIterate(3, 1, np.eye(3)[:, :1], np.array([1.0]), 0.5)
+    res = pb.lowrank_meg_step(x, pb.ZeroGradient(3), eta=1.0, eps_next=0.1, svd_seed=0)
+    assert np.allclose(res.iterate.densify(), np.diag([0.9, 0.05, 0.05]), atol=1e-10)
+
+
+def test_eps_next_validation(pb):
+    q, lam, eps = random_lowrank_iterate_np(8, 2, np.random.default_rng(10))
+    x = pb.LowRankIterate(8, 2, q, lam, eps)
+    with pytest.raises(pb.ParameterError):
+        pb.lowrank_meg_step(x, pb.ZeroGradient(8), eta=1.0, eps_next=0.8)
+    with pytest.raises(TypeError):
+        pb.lowrank_meg_step(x, lambda u: u, eta=1.0, eps_next=0.1)
+
+
+def test_iterate_validation(pb):
+    with pytest.raises(pb.ParameterError):
+        pb.LowRankIterate(5, 2, np.ones((5, 2)), np.array([0.5, 0.5]), 0.1)  # not orthonormal
+    with pytest.raises(pb.ParameterError):
+        pb.LowRankIterate(5, 2, np.eye(5)[:, :2], np.array([0.3, 0.7]), 0.1)  # not sorted
+
+
+def test_logmap_matches_dense_log(pb):
+    """test_meg.py:98-108 on the device operator."""
+    rng = np.random.default_rng(4)
+    q, lam, eps = random_lowrank_iterate_np(40, 3, rng)
+    g = om.symmetrize(rng.standard_normal((40, 40)))
+    x = pb.LowRankIterate(40, 3, q, lam, eps)
+    op = pb.logmap_operator(x, pb.DenseGradient(g), eta=0.3)
+    w, v = np.linalg.eigh(x.densify())
+    assert np.max(np.abs(op.to_dense() - ((v * np.log(w)) @ v.T - 0.3 * g))) <= 1e-8
+
+
+def test_logmap_frobenius_matches_oracle(pb):
+    """The factored Frobenius gradient operator equals the oracle's logmap of the dense driver."""
+    rng = np.random.default_rng(5)
+    n, r = 300, 6
+    q, lam, eps = random_lowrank_iterate_np(n, r, rng)
+    m = om.symmetrize(rng.standard_normal((n, n))) * 0.1
+    xo = om.LowRankIterate(n, r, q, lam, eps)
+    x = pb.LowRankIterate(n, r, q, lam, eps)
+    u = rng.standard_normal((n, 7))
+    ref = om.logmap_operator(xo, lambda v: xo.apply(v) - m @ v, 0.7).apply(u)
+    got = pb.logmap_operator(x, pb.FrobeniusObjective(m).grad_operator(x), 0.7).apply(u)
+    assert normwise(got, ref) <= 1e-13
+
+
+def test_dense_shadow_equivalence_fifty_steps(pb):
+    """test_meg.py:144-156 on the device path: 50 steps vs the dense shadow at 1e-7."""
+    rng = np.random.default_rng(8)
+    n, r = 60, 5
+    d = om.symmetrize(rng.standard_normal((n, n))) * 0.3
+    q, lam, _ = random_lowrank_iterate_np(n, r, rng)
+    x = pb.LowRankIterate(n, r, q, lam, 0.3)
+    for t in range(50):
+        eps_next = 0.6 / (t + 11) ** 2
+        g = om.symmetrize(x.densify() - d)
+        res = pb.lowrank_meg_step(x, pb.DenseGradient(g), eta=0.5, eps_next=eps_next, svd_seed=t)
+        shadow, _, _ = om.shadow_lowrank_step(x.densify(), g, 0.5, eps_next, r)
+        assert np.max(np.abs(res.iterate.densify() - shadow)) <= 1e-7
+        x = res.iterate
+
+
+def test_trace_one_and_floor(pb):
+    """test_meg.py:133-142."""
+    rng = np.random.default_rng(7)
+    n = 30
+    q, lam, eps = random_lowrank_iterate_np(n, 4, rng)
+    x = pb.LowRankIterate(n, 4, q, lam, eps)
+    g = pb.DenseGradient(om.symmetrize(rng.standard_normal((n, n))))
+    for t in range(5):
+        x = pb.lowrank_meg_step(x, g, eta=0.2, eps_next=0.1 / (t + 1), svd_seed=t).iterate
+        assert abs(np.trace(x.densify()) - 1.0) <= 1e-12
+        assert x.eigenvalues_full()[-1] >= x.eps / (n - x.r) - 1e-12
+
+
+def test_certificate_arithmetic(pb):
+    rec = pb.certificate_cheap(0.3, 0.8, 0.5, 3, 1)
+    assert rec.lhs_cheap == pytest.approx(math.log(1.5), abs=1e-12) and rec.holds_cheap and rec.threshold == 1.0
+
+
+# ---------------------------------------------------------------------------
+# trajectories vs the reference goldens
+
+
+SMALL = [
+    ("cfg1_full", "cfg1", None),
+    ("cfg2_n1024", "cfg2", 1024),
+    ("cfg3_n2048", "cfg3", 2048),
+    ("cfg4_n2048", "cfg4", 2048),
+    ("cfg5_n2048", "cfg5", 2048),
+]
+
+
+@pytest.mark.parametrize("name,cfg_name,n", SMALL)
+def test_trajectory_matches_reference(pb, name, cfg_name, n):
+    ref = load_golden(name)
+    iters = int(ref["iters"])
+    cfg = inputs.CONFIGS[cfg_name]
+    if n is not None:
+        cfg = cfg.scaled(n, iters)
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    probe_at = [int(k.split("_")[1]) for k in ref if k.startswith("probe_")]
+    got, _, _ = run_gpu(cfg, host, x0, iters, probe_at=probe_at, block=cfg.block)
+    compare_trajectory(got, ref, tol=TOL[cfg.dtype], f_scale=f_scale(host))
+
+
+@pytest.mark.parametrize("name,cfg_name", [("cfg2_prefix", "cfg2"), ("cfg3_prefix", "cfg3"), ("cfg4_prefix", "cfg4")])
+def test_full_size_prefix_matches_reference(pb, name, cfg_name):
+    ref = load_golden(name)
+    iters = int(ref["iters"])
+    cfg = inputs.CONFIGS[cfg_name]
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    probe_at = [int(k.split("_")[1]) for k in ref if k.startswith("probe_")]
+    got, _, _ = run_gpu(cfg, host, x0, iters, probe_at=probe_at, block=cfg.block)
+    compare_trajectory(got, ref, tol=TOL[cfg.dtype], f_scale=f_scale(host))
+
+
+def test_dual_gap_matches_reference(pb):
+    """_dual_gap_core (objectives.py:332-335) at the final config-5 (n=2048) iterate."""
+    ref = load_golden("cfg5_n2048")
+    iters = int(ref["iters"])
+    cfg = inputs.CONFIGS["cfg5"].scaled(2048, iters)
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    _, x, gobj = run_gpu(cfg, host, x0, iters, block=cfg.block)
+    gap, lmin = gobj.dev.dual_gap(x, block=32)
+    assert abs(gap - float(ref["dual_gap_final"])) <= 1e-4 * max(1.0, abs(float(ref["dual_gap_final"])))

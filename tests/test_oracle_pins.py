@@ -1,0 +1,194 @@
+"""Pin the CPU oracle (oracle/cpu_meg.py) before trusting it.
+
+1. Every known-answer / property test the reference suite holds for the hot
+   path, restated against the oracle (reference test file:line cited).
+2. The golden trajectories produced by the unmodified reference
+   (tests/golden/make_golden.py) reproduced by the oracle on the same seeded
+   inputs.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import cpu_meg as om
+from oracle import inputs, objectives
+from tests.parity import compare_trajectory, load_golden
+
+
+def random_symmetric(n, rng, scale=1.0):
+    return om.symmetrize(rng.standard_normal((n, n))) * scale
+
+
+def random_lowrank_iterate(n, r, rng, eps=None):
+    """test_entropy.py:28-35 fixture, restated."""
+    q, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    lam = np.sort(rng.dirichlet(np.ones(r) * 3))[::-1]
+    lam = np.maximum(lam, 1e-6)
+    lam /= lam.sum()
+    lam = np.sort(lam)[::-1]
+    if eps is None:
+        eps = float(rng.uniform(0.01, 0.5))
+    return om.LowRankIterate(n=n, r=r, V=q, lam=lam, eps=eps)
+
+
+# ---------------------------------------------------------------------------
+# Lanczos known answers (test_linalg.py:61-140)
+
+
+def test_lanczos_diagonal_top2():
+    top = om.lanczos_top_r(om.SymmetricOperator.from_dense(np.diag([5.0, 4, 3, 2, 1])), r=2, seed=1)
+    assert np.allclose(top.eigenvalues, [5.0, 4.0], atol=1e-10)
+    assert np.allclose(np.abs(top.eigenvectors), np.eye(5)[:, :2], atol=1e-8)
+
+
+def test_lanczos_algebraic_not_magnitude():
+    op = om.SymmetricOperator.from_dense(-np.diag(np.arange(1.0, 13)))
+    top = om.lanczos_top_r(op, r=1, seed=5)
+    assert np.allclose(top.eigenvalues, [-1.0], atol=1e-10)
+
+
+def test_lanczos_repeated_eigenvalues():
+    top = om.lanczos_top_r(om.SymmetricOperator.from_dense(np.diag([2.0, 2, 2, 1, 0])), r=3, seed=11)
+    assert np.allclose(top.eigenvalues, [2.0, 2.0, 2.0], atol=1e-9)
+
+
+def test_lanczos_parameter_error_and_failure():
+    with pytest.raises(om.ParameterError):
+        om.lanczos_top_r(om.SymmetricOperator.from_dense(np.eye(4)), r=4)
+    rng = np.random.default_rng(2)
+    op = om.SymmetricOperator.from_dense(random_symmetric(60, rng))
+    with pytest.raises(om.LanczosError) as err:
+        om.lanczos_top_r(op, r=3, tol=1e-16, subspace=6, max_iter=8, restarts=1)
+    assert err.value.residual_norms.shape == (3,)
+
+
+@pytest.mark.parametrize("n,r,seed,aseed", [(100, 5, 3, 7), (200, 8, 2, 17)])
+def test_lanczos_matches_dense(n, r, seed, aseed):
+    a = random_symmetric(n, np.random.default_rng(aseed))
+    w, v = om.full_eigh(a)
+    top = om.lanczos_top_r(om.SymmetricOperator.from_dense(a), r=r, seed=seed)
+    assert np.max(np.abs(top.eigenvalues - w[:r])) <= 1e-8 * max(1.0, np.abs(w).max())
+    ov = v[:, :r].T @ top.eigenvectors
+    assert np.max(np.arccos(np.clip(np.linalg.svd(ov, compute_uv=False), -1, 1))) <= 1e-6
+
+
+def test_lanczos_deterministic():
+    op = om.SymmetricOperator.from_dense(random_symmetric(40, np.random.default_rng(4)))
+    t1, t2 = om.lanczos_top_r(op, r=3, seed=9), om.lanczos_top_r(op, r=3, seed=9)
+    assert np.array_equal(t1.eigenvectors, t2.eigenvectors)
+
+
+# ---------------------------------------------------------------------------
+# step / operator / certificate known answers (test_meg.py)
+
+
+def test_step_diagonal_oracle():
+    """test_meg.py:127-131."""
+    x = om.LowRankIterate(n=3, r=1, V=np.eye(3)[:, :1], lam=np.array([1.0]), eps=0.5)
+    res = om.lowrank_meg_step(x, lambda u: np.zeros_like(u), eta=1.0, eps_next=0.1, svd_seed=0)
+    assert np.allclose(res.iterate.densify(), np.diag([0.9, 0.05, 0.05]), atol=1e-10)
+
+
+def test_logmap_matches_dense_log():
+    """test_meg.py:98-108."""
+    rng = np.random.default_rng(4)
+    x = random_lowrank_iterate(40, 3, rng)
+    g = om.symmetrize(rng.standard_normal((40, 40)))
+    op = om.logmap_operator(x, lambda u: g @ u, eta=0.3)
+    w, v = np.linalg.eigh(x.densify())
+    assert np.max(np.abs(op.to_dense() - ((v * np.log(w)) @ v.T - 0.3 * g))) <= 1e-8
+
+
+def test_dense_shadow_equivalence_fifty_steps():
+    """test_meg.py:144-156: 50 low-rank steps vs the dense shadow, 1e-7."""
+    rng = np.random.default_rng(8)
+    n, r = 60, 5
+    d = om.symmetrize(rng.standard_normal((n, n))) * 0.3
+    x = random_lowrank_iterate(n, r, rng, eps=0.3)
+    for t in range(50):
+        eps_next = 0.6 / (t + 11) ** 2
+        g = om.symmetrize(x.densify() - d)
+        res = om.lowrank_meg_step(x, lambda u, g=g: g @ u, eta=0.5, eps_next=eps_next, svd_seed=t)
+        shadow, _, _ = om.shadow_lowrank_step(x.densify(), g, 0.5, eps_next, r)
+        assert np.max(np.abs(res.iterate.densify() - shadow)) <= 1e-7
+        x = res.iterate
+
+
+def test_certificate_arithmetic():
+    """test_meg.py:190-217."""
+    rec = om.certificate_cheap(0.3, 0.8, 0.5, 3, 1)
+    assert rec.lhs_cheap == pytest.approx(math.log(1.5), abs=1e-12) and rec.holds_cheap and rec.threshold == 1.0
+    assert om.certificate_cheap(0.0, 0.5, 0.1, 5, 1).lhs_cheap == -math.inf
+    full = om.certificate_full(np.array([0.5, 0.3, 0.2]), 0.5, 3, 1)
+    assert full.lhs_full == pytest.approx(math.log(1.2), abs=1e-12)
+    for n in (2, 5, 50):
+        assert om.certificate_full(np.full(n, 1.0 / n), 0.5, n, 1).lhs_full == pytest.approx(
+            math.log(2 * (n - 1) / n), abs=1e-12
+        )
+    with pytest.raises(om.ParameterError):
+        om.certificate_cheap(0.1, 0.0, 0.1, 5, 1)
+
+
+def test_warm_start_and_schedules():
+    """test_meg.py:263-289, 341-377."""
+    x1 = om.warm_start_wrap(np.eye(2)[:, :1], np.array([1.0]), eps0=0.1)
+    assert np.allclose(x1.densify(), np.diag([0.95, 0.05]), atol=1e-14)
+    assert om.EpsilonSchedule.experiment(10.0).eval(0) == pytest.approx(0.6 / 121.0, rel=1e-12)
+    assert om.EpsilonSchedule.cubic_det(100.0, 0.5, 0.0).eval(0) == 0.75
+    assert inputs.CONFIGS["cfg2"].eps(0) == pytest.approx(0.6 / 121.0, rel=1e-15)
+
+
+def test_project_simplex():
+    """test_linalg.py:158-187."""
+    assert np.allclose(om.project_simplex(np.array([0.2, 0.3])), [0.45, 0.55], atol=1e-12)
+    assert np.allclose(om.project_simplex(np.array([2.0, -1.0])), [1.0, 0.0], atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# golden trajectories from the reference itself
+
+
+def f_scale(obj):
+    if hasattr(obj, "m_norm2"):
+        return 0.5 * obj.m_norm2
+    return 0.5 * float(obj.inst.obs @ obj.inst.obs)
+
+
+GOLDEN_SMALL = [
+    ("cfg1_full", "cfg1", None),
+    ("cfg2_n1024", "cfg2", 1024),
+    ("cfg3_n2048", "cfg3", 2048),
+    ("cfg4_n2048", "cfg4", 2048),
+    ("cfg5_n2048", "cfg5", 2048),
+]
+
+
+@pytest.mark.parametrize("name,cfg_name,n", GOLDEN_SMALL)
+def test_oracle_reproduces_reference_trajectory(name, cfg_name, n):
+    ref = load_golden(name)
+    iters = int(ref["iters"])
+    cfg = inputs.CONFIGS[cfg_name]
+    if n is not None:
+        cfg = cfg.scaled(n, iters)
+    obj = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, obj)
+    z = objectives.probes(cfg.n)
+    assert np.max(np.abs(objectives.x_apply(x0, z) - ref["x0_probe"])) <= 1e-12
+    probe_at = [int(k.split("_")[1]) for k in ref if k.startswith("probe_")]
+    got, _ = objectives.run_trajectory(om, cfg, obj, x0, iters, probe_at=probe_at)
+    # converged-quantity parity between two valid solvers: <= ~1e-11
+    compare_trajectory(got, ref, tol=1e-10, f_scale=f_scale(obj))
+
+
+def test_generator_is_counter_based():
+    """Same counters -> same draws regardless of the chunking used to request them."""
+    key = inputs.stream_key(0, 2)
+    a = inputs.gaussian(key, np.arange(1000, dtype=np.uint64))
+    b = np.concatenate([inputs.gaussian(key, np.arange(i, i + 100, dtype=np.uint64)) for i in range(0, 1000, 100)])
+    assert np.array_equal(a, b)
+    assert abs(a.mean()) < 0.1 and abs(a.std() - 1.0) < 0.1
+    cfg = inputs.CONFIGS["cfg2"].scaled(64)
+    m = inputs.dense_target(cfg)
+    assert np.array_equal(m, m.T)
