@@ -231,7 +231,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   mmax = std::min<int>(mmax, s->max_basis);
   mmax = std::max(mmax, std::min<int>(nreq + bw, s->max_basis));
   bool exhaust = false;
-  if (n <= s->max_basis && n <= 64) {  // tiny problems: span R^n exactly (basis.shape[1] >= n rule, linalg.py:215)
+  if (n <= s->max_basis && n <= 64 && (P.basis <= 0 || P.basis >= n)) {  // tiny problems: span R^n exactly (basis.shape[1] >= n rule, linalg.py:215)
     bw = (int)std::min<int64_t>(n, s->max_block);
     mmax = (int)n;
     exhaust = true;
