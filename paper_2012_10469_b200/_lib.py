@@ -109,6 +109,8 @@ SIGNATURES = [
      [C.c_void_p, C.c_uint64, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int32, C.c_void_p,
       C.c_int64]),
     ("megb200_gram_error", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, c_double_p]),
+    ("megb200_profile_enable", C.c_int, [C.c_void_p, C.c_int32]),
+    ("megb200_profile_read", C.c_int, [C.c_void_p, c_double_p, C.POINTER(C.c_int64), c_double_p]),
     ("megb200_kernel_launches", C.c_int64, [C.c_void_p]),
 ]
 

@@ -105,5 +105,22 @@ void gen_dense_target(const Launch& L, const double* U, int64_t r, const double*
 // threshold, kept-mass flag
 void step_epilogue(const Launch& L, const double* theta, int r, int64_t n, double eps_next, double* out);
 void reduce_sum(const Launch& L, const double* part, int slots, int width, double* out);
+// H[0:cap, 0:cap] = 0 except H[j][j] = theta[j] for j < k
+void set_diag(const Launch& L, double* H, int cap, int k, const double* theta);
+
+// cooperative tall-skinny kernels (megb200_coop.cu): one launch each
+void coop_tn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const double* Y, int64_t ldy, int q,
+             double* C, int64_t ldc, const double* rowscale, double scale, double* part, int sm_count);
+void coop_cgs(const Launch& L, int64_t n, const double* Q, int64_t ldq, int cols, double* W, int64_t ldw, int q,
+              double* Cws, double* part, int sm_count);
+void coop_cholqr(const Launch& L, int64_t n, double* W, int64_t ldw, int q, double thresh, double* Gws, double* Rrel,
+                 double* Rinv, int* mask, const double* Rprev, double* Rtot, uint64_t key, uint64_t base, double* part,
+                 int sm_count);
+void coop_ritz(const Launch& L, int64_t n, const double* Q, const double* AQ, int64_t ldq, int cols, const double* S,
+               int ldS, int rq, int nreq, const double* theta, double* T, int64_t ldt, double* resid, double* part,
+               int sm_count);
+void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, double scale, const double* Lf,
+                 int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
+                 int64_t ldw, double* Ews, double* part, int sm_count);
 
 }  // namespace megb200

@@ -7,11 +7,15 @@
 // Rayleigh-Ritz) runs in float64 with fixed reduction orders so every result
 // is bitwise reproducible run to run (SPEC.md:97 determinism).
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
 #include <algorithm>
+
+#include <string>
 
 #include "megb200_internal.h"
 
@@ -260,6 +264,207 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
   for (int idx = threadIdx.x; idx < rows * b; idx += kApplyThreads) {
     const int r = idx / b, c = idx - r * b;
     out[(row0 + r) * b + c] = red[c * 128 + r];
+  }
+}
+
+// ===========================================================================
+// K1 (pipelined): warp-specialised streamed pass.  One producer warp moves
+// k-row segments of the operand tile and the matching rows of U into a ring
+// of NST shared-memory stages with cp.async.bulk (the TMA engine, SASS
+// UBLKCP), signalling an mbarrier per stage with the byte count; eight
+// consumer warps wait on the stage, run the FMA block and release it.
+// The grid is persistent: CTA c processes items c, c + grid, ... of the
+// (k-slice, row-tile) work list, so the pipeline never drains between items.
+namespace pipe {
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  uint64_t st;
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(st) : "r"(su32(b)), "r"(bytes) : "memory");
+  (void)st;
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  uint64_t st;
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 %0, [%1];" : "=l"(st) : "r"(su32(b)) : "memory");
+  (void)st;
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(su32(b)), "r"(parity) : "memory");
+  }
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(su32(dst)), "l"(map), "r"(x), "r"(y), "r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(b)) : "memory");
+}
+}  // namespace pipe
+
+constexpr int kPipeKC = 32;      // k rows per stage
+constexpr int kPipeStages = 5;   // ring depth
+constexpr int kPipeConsumers = 8;
+constexpr int kPipeThreads = 32 * (kPipeConsumers + 1);
+
+template <typename T>
+struct PipeShape {
+  static constexpr int RPL = sizeof(T) == 8 ? 2 : 4;  // output rows per lane (16-byte smem reads)
+  static constexpr int BM = 32 * RPL;                 // output rows per item
+};
+
+template <typename T, int BN>
+constexpr size_t pipe_smem_bytes() {
+  return (size_t)kPipeStages * kPipeKC * PipeShape<T>::BM * sizeof(T) + (size_t)kPipeStages * kPipeKC * BN * 8 +
+         (size_t)4 * BN * PipeShape<T>::BM * sizeof(T) + 2 * kPipeStages * 8;
+}
+
+template <typename T, int BN>
+__global__ void __launch_bounds__(kPipeThreads, 1)
+    k_dense_pass(const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmU, int64_t n, int b,
+                 double* __restrict__ part, int tiles, int64_t kslice, int items) {
+  constexpr int RPL = PipeShape<T>::RPL, BM = PipeShape<T>::BM;
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* Ms = reinterpret_cast<T*>(smem);
+  double* Us = reinterpret_cast<double*>(smem + (size_t)kPipeStages * kPipeKC * BM * sizeof(T));
+  T* red = reinterpret_cast<T*>(Us + (size_t)kPipeStages * kPipeKC * BN);
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + (size_t)4 * BN * BM);
+  uint64_t* empty = full + kPipeStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kPipeStages; ++st) {
+      pipe::bar_init(full + st, 1);
+      pipe::bar_init(empty + st, kPipeConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmM) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
+  }
+  __syncthreads();
+
+  if (warp == kPipeConsumers) {
+    // ---------------- producer warp: one elected lane issues two 2D TMA tiles per stage
+    if (lane == 0) {
+      const uint32_t stage_bytes = (uint32_t)(kPipeKC * BM * sizeof(T) + kPipeKC * b * 8);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int slice = item / tiles, tile = item - slice * tiles;
+        const int64_t kbeg = (int64_t)slice * kslice, kend = min(n, kbeg + kslice);
+        for (int64_t kc = kbeg; kc < kend; kc += kPipeKC) {
+          pipe::bar_wait(empty + st, ph ^ 1u);
+          pipe::bar_arrive_tx(full + st, stage_bytes);
+          pipe::tma_2d(Ms + (size_t)st * kPipeKC * BM, &tmM, tile * BM, (int)kc, full + st);
+          pipe::tma_2d(Us + (size_t)st * kPipeKC * BN, &tmU, 0, (int)kc, full + st);
+          if (++st == kPipeStages) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps
+  int st = 0;
+  uint32_t ph = 0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int slice = item / tiles, tile = item - slice * tiles;
+    const int64_t i0 = (int64_t)tile * BM;
+    const int64_t kbeg = (int64_t)slice * kslice, kend = min(n, kbeg + kslice);
+    T acc[RPL][BN];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q)
+#pragma unroll
+      for (int c = 0; c < BN; ++c) acc[q][c] = (T)0;
+    for (int64_t kc = kbeg; kc < kend; kc += kPipeKC) {
+      const int nk = (int)min((int64_t)kPipeKC, kend - kc);
+      pipe::bar_wait(full + st, ph);
+      auto body = [&](int kk) {
+        const T* mrow = Ms + ((size_t)st * kPipeKC + kk) * BM + RPL * lane;
+        const double* urow = Us + (size_t)st * kPipeKC * BN + (size_t)kk * b;
+        T mv[RPL];
+        if constexpr (RPL == 2) {
+          const double2 v = *reinterpret_cast<const double2*>(mrow);
+          mv[0] = v.x;
+          mv[1] = v.y;
+        } else {
+          const float4 v = *reinterpret_cast<const float4*>(mrow);
+          mv[0] = v.x;
+          mv[1] = v.y;
+          mv[2] = v.z;
+          mv[3] = v.w;
+        }
+#pragma unroll
+        for (int c = 0; c < BN; c += 2) {
+          const double2 uu = *reinterpret_cast<const double2*>(urow + c);
+          const T u0 = (T)uu.x, u1 = (T)uu.y;
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) {
+            acc[q][c] = fma(mv[q], u0, acc[q][c]);
+            acc[q][c + 1] = fma(mv[q], u1, acc[q][c + 1]);
+          }
+        }
+      };
+      if (nk == kPipeKC) {
+#pragma unroll
+        for (int j = 0; j < kPipeKC / kPipeConsumers; ++j) body(warp + kPipeConsumers * j);
+      } else {
+        for (int j = 0; j < kPipeKC / kPipeConsumers; ++j)
+          if (warp + kPipeConsumers * j < nk) body(warp + kPipeConsumers * j);
+      }
+      __syncwarp();
+      if (lane == 0) pipe::bar_arrive(empty + st);
+      if (++st == kPipeStages) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+    // fixed-order tree over the consumer warps: w += w+4, w += w+2, 0 += 1
+#pragma unroll
+    for (int half = 4; half >= 1; half >>= 1) {
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kPipeConsumers) : "memory");
+      if (warp >= half && warp < 2 * half) {
+        T* dst = red + (size_t)(warp - half) * BN * BM;
+#pragma unroll
+        for (int c = 0; c < BN; ++c)
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) dst[c * BM + RPL * lane + q] = acc[q][c];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kPipeConsumers) : "memory");
+      if (warp < half) {
+        const T* src = red + (size_t)warp * BN * BM;
+#pragma unroll
+        for (int c = 0; c < BN; ++c)
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) acc[q][c] += src[c * BM + RPL * lane + q];
+      }
+    }
+    if (warp == 0) {
+#pragma unroll
+      for (int c = 0; c < BN; ++c)
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) red[c * BM + RPL * lane + q] = acc[q][c];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kPipeConsumers) : "memory");
+    double* out = part + (int64_t)slice * n * b;
+    const int rows = (int)min((int64_t)BM, n - i0);
+    for (int idx = threadIdx.x; idx < rows * b; idx += 32 * kPipeConsumers) {
+      const int r = idx / b, c = idx - r * b;
+      out[(i0 + r) * b + c] = (double)red[c * BM + r];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kPipeConsumers) : "memory");
   }
 }
 
@@ -853,6 +1058,13 @@ __global__ void k_step_epilogue(const double* __restrict__ theta, int r, int64_t
   tail[6] = status;
 }
 
+__global__ void k_set_diag(double* __restrict__ H, int cap, int k, const double* __restrict__ theta) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= cap * cap) return;
+  const int i = idx / cap, j = idx - i * cap;
+  H[idx] = (i == j && i < k) ? theta[i] : 0.0;
+}
+
 __global__ void k_reduce_sum(const double* __restrict__ part, int slots, int width, double* __restrict__ out) {
   const int c = threadIdx.x;
   if (c >= width) return;
@@ -914,8 +1126,109 @@ void launch_dense_f32(const Launch& L, const float* M, int64_t ldm, int64_t n, c
 // ===========================================================================
 // launch wrappers
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    MEG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw Error(MEGB200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2D row-major tensor map: inner dimension `cols` (contiguous), outer `rows`, leading dimension `ld`
+CUtensorMap make_map(const void* base, CUtensorMapDataType dt, size_t es, int64_t cols, int64_t rows, int64_t ld,
+                     uint32_t box_cols, uint32_t box_rows) {
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(MEGB200_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return map;
+}
+
+template <typename T, int BN>
+void launch_pipe(const Launch& L, const T* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                 double* part, int tiles, int64_t kslice, int items, int grid) {
+  constexpr size_t smem = pipe_smem_bytes<T, BN>();
+  static bool attr = false;
+  if (!attr) {
+    MEG_CUDA(cudaFuncSetAttribute(k_dense_pass<T, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const CUtensorMap tmM = make_map(M, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                   sizeof(T), n, n, ldm, PipeShape<T>::BM, kPipeKC);
+  const CUtensorMap tmU = make_map(U, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, b, n, ldu, (uint32_t)b, kPipeKC);
+  k_dense_pass<T, BN><<<grid, kPipeThreads, smem, L.stream>>>(tmM, tmU, n, b, part, tiles, kslice, items);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+template <typename T>
+void dispatch_pipe(const Launch& L, const T* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                   double* part, int tiles, int64_t kslice, int items, int grid) {
+  switch ((b + 1) / 2) {
+#define MEG_PIPE_CASE(h) \
+  case h:                \
+    launch_pipe<T, 2 * h>(L, M, ldm, n, U, ldu, b, part, tiles, kslice, items, grid); \
+    break;
+    MEG_PIPE_CASE(1) MEG_PIPE_CASE(2) MEG_PIPE_CASE(3) MEG_PIPE_CASE(4) MEG_PIPE_CASE(5) MEG_PIPE_CASE(6)
+    MEG_PIPE_CASE(7) MEG_PIPE_CASE(8) MEG_PIPE_CASE(9) MEG_PIPE_CASE(10) MEG_PIPE_CASE(11) MEG_PIPE_CASE(12)
+    MEG_PIPE_CASE(13) MEG_PIPE_CASE(14) MEG_PIPE_CASE(15) MEG_PIPE_CASE(16)
+#undef MEG_PIPE_CASE
+    default:
+      throw Error(MEGB200_ERR_PARAM, "pipelined pass supports b <= 32");
+  }
+}
+
+// Choose the number of k-slices S so that tiles * S fills whole waves of one
+// CTA per SM (static round-robin of the persistent grid), preferring small S.
+int choose_slices(int tiles, int64_t n, int sm_count, int s_min, int s_max) {
+  int best = s_min;
+  double best_eff = -1.0;
+  for (int S = s_min; S <= s_max; ++S) {
+    if ((int64_t)S * kPipeKC * 2 > n && S > s_min) break;
+    const int items = tiles * S;
+    const int waves = cdiv(items, sm_count);
+    const double eff = (double)items / ((double)waves * sm_count);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = S;
+    }
+  }
+  return best;
+}
+
 int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, int64_t n, const double* U,
                         int64_t ldu, int b, double* part, int64_t part_cap_slices, int sm_count) {
+  {
+    const size_t es = dtype == MEGB200_F64 ? 8 : 4;
+    const bool aligned = b % 2 == 0 && b <= 32 && ldu % 2 == 0 && ((uintptr_t)U % 16 == 0) &&
+                         (ldm * es) % 16 == 0 && ((uintptr_t)M % 16 == 0) && (n * es) % 16 == 0;
+    if (aligned) {
+      const int BM = dtype == MEGB200_F64 ? 64 : 128;
+      const int tiles = cdiv(n, BM);
+      int s_min = dtype == MEGB200_F64 ? 1 : std::max(1, cdiv(n, kF32Slice));
+      int s_max = std::max(s_min, (int)std::min<int64_t>(part_cap_slices, 16));
+      s_min = std::min(s_min, (int)part_cap_slices);
+      int S = choose_slices(tiles, n, sm_count, s_min, s_max);
+      int64_t kslice = (int64_t)cdiv(cdiv(n, S), kPipeKC) * kPipeKC;
+      S = cdiv(n, kslice);
+      const int items = tiles * S;
+      const int grid = std::min(items, sm_count);
+      if (dtype == MEGB200_F64)
+        dispatch_pipe<double>(L, static_cast<const double*>(M), ldm, n, U, ldu, b, part, tiles, kslice, items, grid);
+      else
+        dispatch_pipe<float>(L, static_cast<const float*>(M), ldm, n, U, ldu, b, part, tiles, kslice, items, grid);
+      return S;
+    }
+  }
   const int rows = dtype == MEGB200_F64 ? 64 : 128;
   const int tiles = cdiv(n, rows);
   int S = std::max(1, cdiv(sm_count, tiles));
@@ -1063,7 +1376,8 @@ void rr_jacobi(const Launch& L, const double* H, int64_t ldh, int m, double* the
     MEG_CUDA(cudaFuncSetAttribute(k_rr_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
     attr = true;
   }
-  k_rr_jacobi<<<1, kJacobiThreads, smem, L.stream>>>(H, ldh, m, theta, S, Rn, rn_rows, cur, nreq, est, info);
+  const int threads = m <= 24 ? 64 : m <= 48 ? 256 : m <= 80 ? 512 : kJacobiThreads;
+  k_rr_jacobi<<<1, threads, smem, L.stream>>>(H, ldh, m, theta, S, Rn, rn_rows, cur, nreq, est, info);
   MEG_LAUNCHED();
   ++*L.counter;
 }
@@ -1133,6 +1447,12 @@ void gen_dense_target(const Launch& L, const double* U, int64_t r, const double*
 
 void step_epilogue(const Launch& L, const double* theta, int r, int64_t n, double eps_next, double* out) {
   k_step_epilogue<<<1, 32, 0, L.stream>>>(theta, r, n, eps_next, out);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void set_diag(const Launch& L, double* H, int cap, int k, const double* theta) {
+  k_set_diag<<<cdiv((int64_t)cap * cap, 256), 256, 0, L.stream>>>(H, cap, k, theta);
   MEG_LAUNCHED();
   ++*L.counter;
 }

@@ -63,6 +63,21 @@ struct megb200_solver {
   int64_t h_buf_len = 0;
   double m_norm2_cache = NAN, m_trace_cache = NAN;
   const void* m_cache_ptr = nullptr;
+  // live pass profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_pending;
+  int ev_next = 0;
+  double prof_bytes = 0.0;
+  int64_t prof_passes = 0;
+  cudaEvent_t next_event() {
+    if (ev_next == (int)ev_pool.size()) {
+      cudaEvent_t e;
+      MEG_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_next++];
+  }
 
   Launch launch() { return Launch{stream, &launches}; }
   void sync() { MEG_CUDA(cudaStreamSynchronize(stream)); }
@@ -89,6 +104,7 @@ struct OpDev {
   const int32_t* rowptr = nullptr;
   const int32_t* col = nullptr;
   const double* val = nullptr;
+  int64_t nnz = 0;
   double scale = 0.0;
   const double* L = nullptr;
   int64_t ldl = 0;
@@ -101,14 +117,31 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
   Launch L = s->launch();
   const int64_t n = s->n;
   int S = 0;
+  const bool streamed = (op.kind == MEGB200_OP_DENSE || op.kind == MEGB200_OP_CSR) && op.scale != 0.0;
+  int ev0 = -1;
+  if (s->prof && streamed) {
+    ev0 = s->ev_next;
+    MEG_CUDA(cudaEventRecord(s->next_event(), s->stream));
+  }
   if (op.kind == MEGB200_OP_DENSE && op.scale != 0.0) {
     S = dense_apply_partial(L, op.dense, op.dtype, op.ld, n, U, ldu, k, s->part, s->part_slices, s->sm_count);
   } else if (op.kind == MEGB200_OP_CSR && op.scale != 0.0) {
     csr_apply_partial(L, op.rowptr, op.col, op.val, n, U, ldu, k, s->part);
     S = 1;
   }
-  if (op.l > 0) tn(L, n, op.L, op.ldl, op.l, U, ldu, k, s->E, k, op.d_dev, s->red, s->red_cap, s->sm_count);
-  apply_finish(L, n, k, S, s->part, op.scale, op.L, op.ldl, op.l, s->E, op.alpha, U, ldu, W, ldw);
+  coop_finish(L, n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
+              s->sm_count);
+  if (ev0 >= 0) {
+    const int ev1 = s->ev_next;
+    MEG_CUDA(cudaEventRecord(s->next_event(), s->stream));
+    s->ev_pending.emplace_back(ev0, ev1);
+    const double es = op.kind == MEGB200_OP_DENSE ? (op.dtype == MEGB200_F64 ? 8.0 : 4.0) : 0.0;
+    double b = 2.0 * (double)n * k * 8.0;  // read U, write W (float64)
+    if (op.kind == MEGB200_OP_DENSE) b += (double)n * (double)n * es;
+    if (op.kind == MEGB200_OP_CSR) b += (double)op.nnz * 12.0 + (double)(n + 1) * 4.0;
+    s->prof_bytes += b;
+    s->prof_passes++;
+  }
 }
 
 // columns k > 64 are applied in chunks (re-streams the operand; not used by the configs)
@@ -131,6 +164,7 @@ OpDev op_from_public(megb200_solver* s, const megb200_operator* op) {
   o.rowptr = op->rowptr;
   o.col = op->col;
   o.val = op->val;
+  o.nnz = op->nnz;
   o.scale = op->scale;
   o.alpha = op->alpha;
   if (o.kind == MEGB200_OP_DENSE && (!o.dense || o.ld < s->n)) throw Error(MEGB200_ERR_PARAM, "dense operand missing");
@@ -148,35 +182,23 @@ OpDev op_from_public(megb200_solver* s, const megb200_operator* op) {
 }
 
 // ---------------------------------------------------------------------------
-// block orthonormalisation: W (n x q, ld ldw) against Q[:, 0:cols] with CGS2,
-// then CholQR2 with breakdown replacement.  Writes the relation factor
-// Rn (q x q): W_in - Q C = Q_new Rn  (C = first-round coefficients).
-
-struct OrthStats {
-  int deficient = 0;
-};
+// block orthonormalisation: W (n x q, ld ldw) against Q[:, 0:cols] with two
+// cooperative CGS rounds, then two cooperative CholQR rounds (breakdown ->
+// seeded random refill, the rule of linalg.py:193-199).  With want_relation
+// the relation factor Rn = R2 R1 (W_in - Q C = W_out Rn) is formed.
 
 void orthonormalize(megb200_solver* s, double* W, int64_t ldw, int q, int cols, double scale, uint64_t key,
-                    uint64_t& refill_ctr, bool want_relation) {
+                    uint64_t& refill_ctr, bool want_relation, int cgs_rounds = 2) {
   Launch L = s->launch();
   const int64_t n = s->n;
-  for (int round = 0; round < 2 && cols > 0; ++round) {
-    tn(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, q, nullptr, s->red, s->red_cap, s->sm_count);
-    nn(L, n, s->Q, s->ldq, cols, s->C2, q, q, -1.0, 1.0, W, ldw);
-  }
-  // CholQR round 1 (breakdown -> random refill, rule of linalg.py:193-199)
-  tn(L, n, W, ldw, q, W, ldw, q, s->G, q, nullptr, s->red, s->red_cap, s->sm_count);
-  chol(L, s->G, q, 1e-13 * scale, s->R1, s->Rinv, s->mask, nullptr, nullptr, 0);
-  apply_rinv(L, n, W, ldw, q, s->Rinv, s->mask, key, refill_ctr);
+  for (int round = 0; round < cgs_rounds && cols > 0; ++round)
+    coop_cgs(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, s->red, s->sm_count);
+  coop_cholqr(L, n, W, ldw, q, 1e-13 * scale, s->G, s->R1, s->Rinv, s->mask, nullptr, nullptr, key, refill_ctr,
+              s->red, s->sm_count);
   refill_ctr += (uint64_t)n * q;
-  // re-project (refilled columns and R1^-1 amplification), CholQR round 2
-  if (cols > 0) {
-    tn(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, q, nullptr, s->red, s->red_cap, s->sm_count);
-    nn(L, n, s->Q, s->ldq, cols, s->C2, q, q, -1.0, 1.0, W, ldw);
-  }
-  tn(L, n, W, ldw, q, W, ldw, q, s->G, q, nullptr, s->red, s->red_cap, s->sm_count);
-  chol(L, s->G, q, 0.0, s->R2, s->Rinv, s->mask, want_relation ? s->R1 : nullptr, want_relation ? s->Rn : nullptr, q);
-  apply_rinv(L, n, W, ldw, q, s->Rinv, s->mask, key, refill_ctr);
+  if (cols > 0) coop_cgs(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, s->red, s->sm_count);
+  coop_cholqr(L, n, W, ldw, q, 0.0, s->G, s->R2, s->Rinv, s->mask, want_relation ? s->R1 : nullptr,
+              want_relation ? s->Rn : nullptr, key, refill_ctr, s->red, s->sm_count);
   refill_ctr += (uint64_t)n * q;
 }
 
@@ -255,88 +277,60 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
 
   EigRun run;
   std::vector<double> best(nreq, INFINITY);
-  std::vector<double> hbuf;
   int cols = 0, cur = bw;
   double scale = 1.0;
-  zero(L, s->H, (int64_t)s->cap * s->cap);
   for (;;) {
-    // operator pass on the current block
+    // operator pass on the current block, then its column of H = Q^T A Q
     apply_op_wide(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq);
     run.passes++;
-    // first-round projection coefficients = H[0:cols+cur, cols:cols+cur]
-    tn(L, n, s->Q, s->ldq, cols + cur, s->AQ + cols, s->ldq, cur, s->H + cols, s->cap, nullptr, s->red, s->red_cap,
-       s->sm_count);
+    coop_tn(L, n, s->Q, s->ldq, cols + cur, s->AQ + cols, s->ldq, cur, s->H + cols, s->cap, nullptr, 1.0, s->red,
+            s->sm_count);
     const int newcols = cols + cur;
-    const int nxt = (int)std::min<int64_t>(bw, n - newcols);
-    bool have_relation = false;
-    if (nxt == cur) {
-      // W = AQ_j - Q H[:, j]  -> next block with relation factor Rn
-      copy_block(L, n, cur, s->AQ + cols, s->ldq, s->Q + newcols, s->ldq);
-      nn(L, n, s->Q, s->ldq, newcols, s->H + cols, s->cap, cur, -1.0, 1.0, s->Q + newcols, s->ldq);
-      orthonormalize(s, s->Q + newcols, s->ldq, cur, newcols, scale, key_refill, refill_ctr, true);
-      have_relation = true;
-    } else if (nxt > 0) {
-      fill_gaussian(L, n, nxt, key_refill, refill_ctr, 1.0, false, s->Q + newcols, s->ldq);
-      refill_ctr += (uint64_t)n * nxt;
-      orthonormalize(s, s->Q + newcols, s->ldq, nxt, newcols, 1.0, key_refill, refill_ctr, false);
-    }
-    cols = newcols;
-    // Rayleigh-Ritz on H[0:cols, 0:cols]
-    rr_jacobi(L, s->H, s->cap, cols, s->theta, s->S, have_relation ? s->Rn : nullptr, cur, cur, nreq, s->est,
-              s->info);
-    // host decision data: theta (cols), est (nreq)
-    const int nt = cols;
+    // Rayleigh-Ritz on H[0:newcols, 0:newcols]; explicit Ritz residuals from the
+    // cached images (linalg.py:205-211) in one cooperative launch
+    rr_jacobi(L, s->H, s->cap, newcols, s->theta, s->S, nullptr, 0, 0, nreq, nullptr, s->info);
+    const int rq = std::min(newcols, std::max(nreq, bw));
+    coop_ritz(L, n, s->Q, s->AQ, s->ldq, newcols, s->S, newcols, rq, nreq, s->theta, s->T, s->ldq, s->resid, s->red,
+              s->sm_count);
     double* hb = s->h_buf;
-    s->d2h(hb, s->theta, nt);
-    s->d2h(hb + nt, s->est, nreq);
+    s->d2h(hb, s->theta, newcols);
+    s->d2h(hb + newcols, s->resid, nreq);
     s->sync();
     double tmax = 0.0;
-    for (int j = 0; j < nt; ++j) tmax = std::max(tmax, fabs(hb[j]));
-    scale = std::max(1.0, tmax);
-    const bool complete = (cols >= n);
-    bool est_ok = have_relation;
-    double est_max = 0.0;
-    if (have_relation) {
-      for (int j = 0; j < nreq; ++j) {
-        est_ok = est_ok && (hb[nt + j] <= tol * scale);
-        est_max = std::max(est_max, hb[nt + j]);
-      }
-      double best_max = 0.0;
-      for (double v : best) best_max = std::max(best_max, v);
-      if (est_max < best_max)
-        for (int j = 0; j < nreq; ++j) best[j] = hb[nt + j];
+    for (int j = 0; j < newcols; ++j) tmax = std::max(tmax, fabs(hb[j]));
+    scale = std::max(1.0, tmax);  // norm estimate max(1, max|theta_all|) (linalg.py:214)
+    const bool complete = (newcols >= n);
+    bool ok = true;
+    double rmax = 0.0, best_max = 0.0;
+    for (int j = 0; j < nreq; ++j) {
+      ok = ok && (hb[newcols + j] <= tol * scale);
+      rmax = std::max(rmax, hb[newcols + j]);
     }
-    if (est_ok || complete) {
-      // explicit residuals of the top Ritz pairs from the cached images (linalg.py:209-211)
-      const int rq = std::min(cols, std::max(nreq, bw));
-      nn(L, n, s->Q, s->ldq, cols, s->S, cols, rq, 1.0, 0.0, s->T, s->ldq);
-      nn(L, n, s->AQ, s->ldq, cols, s->S, cols, nreq, 1.0, 0.0, s->T + rq, s->ldq);
-      resid_norms(L, n, s->T, s->ldq, s->T + rq, s->ldq, nreq, s->theta, s->resid, s->red, s->red_cap, s->sm_count);
-      s->d2h(hb + nt + nreq, s->resid, nreq);
-      s->sync();
-      bool ok = true;
-      double rmax = 0.0;
-      for (int j = 0; j < nreq; ++j) {
-        ok = ok && (hb[nt + nreq + j] <= tol * scale);
-        rmax = std::max(rmax, hb[nt + nreq + j]);
-      }
-      double best_max = 0.0;
-      for (double v : best) best_max = std::max(best_max, v);
-      if (rmax < best_max)
-        for (int j = 0; j < nreq; ++j) best[j] = hb[nt + nreq + j];
-      if (ok || complete) {
-        run.theta.assign(hb, hb + nreq);
-        run.resid.assign(hb + nt + nreq, hb + nt + 2 * nreq);
-        run.norm_est = scale;
-        run.converged = true;
-        if (vec_out) copy_block(L, n, nreq, s->T, s->ldq, vec_out, ld_vec);
-        if (ritz_out) copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
-        if (ritz_cols_out) *ritz_cols_out = rq;
-        return run;
-      }
+    for (double v : best) best_max = std::max(best_max, v);
+    if (rmax < best_max)
+      for (int j = 0; j < nreq; ++j) best[j] = hb[newcols + j];
+    if (ok || complete) {
+      run.theta.assign(hb, hb + nreq);
+      run.resid.assign(hb + newcols, hb + newcols + nreq);
+      run.norm_est = scale;
+      run.converged = true;
+      if (vec_out) copy_block(L, n, nreq, s->T, s->ldq, vec_out, ld_vec);
+      if (ritz_out) copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
+      if (ritz_cols_out) *ritz_cols_out = rq;
+      return run;
     }
     if (run.passes >= max_passes) break;
-    if (nxt <= 0) break;  // cannot grow (complete handled above)
+    const int nxt = (int)std::min<int64_t>(bw, n - newcols);
+    if (nxt <= 0) break;
+    // next Krylov block: the image block orthogonalised against the basis
+    if (nxt == cur) {
+      copy_block(L, n, cur, s->AQ + cols, s->ldq, s->Q + newcols, s->ldq);
+    } else {
+      fill_gaussian(L, n, nxt, key_refill, refill_ctr, 1.0, false, s->Q + newcols, s->ldq);
+      refill_ctr += (uint64_t)n * nxt;
+    }
+    orthonormalize(s, s->Q + newcols, s->ldq, nxt, newcols, scale, key_refill, refill_ctr, false);
+    cols = newcols;
     if (cols + nxt > mmax) {
       // thick restart: keep the leading `keep` Ritz pairs, continue from the next block
       nn(L, n, s->Q, s->ldq, cols, s->S, cols, keep, 1.0, 0.0, s->T, s->ldq);
@@ -344,11 +338,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       nn(L, n, s->AQ, s->ldq, cols, s->S, cols, keep, 1.0, 0.0, s->T, s->ldq);
       copy_block(L, n, keep, s->T, s->ldq, s->AQ, s->ldq);
       copy_block(L, n, nxt, s->Q + cols, s->ldq, s->Q + keep, s->ldq);
-      // H = diag(theta_keep); the coupling rows come with the next pass
-      zero(L, s->H, (int64_t)s->cap * s->cap);
-      hbuf.assign((size_t)keep * s->cap, 0.0);
-      for (int j = 0; j < keep; ++j) hbuf[(size_t)j * s->cap + j] = hb[j];
-      s->h2d(s->H, hbuf.data(), (int64_t)keep * s->cap);
+      set_diag(L, s->H, s->cap, keep, s->theta);  // H = diag(theta_keep); couplings arrive with the next pass
       cols = keep;
       run.restarts++;
     }
@@ -479,6 +469,7 @@ StepOperator build_step_operator(megb200_solver* s, const megb200_iterate* x, co
       op.rowptr = g->rowptr;
       op.col = g->col;
       op.val = s->csr_g;
+      op.nnz = g->nnz;
       op.scale = -eta;
       break;
     }
@@ -520,7 +511,7 @@ StepOperator build_step_operator(megb200_solver* s, const megb200_iterate* x, co
 // Gram error max |V^T V - I| for an n x r block (LowRankIterate validation, meg.py:69-71)
 double gram_error(megb200_solver* s, const double* V, int64_t ldv, int r) {
   Launch L = s->launch();
-  tn(L, s->n, V, ldv, r, V, ldv, r, s->G, r, nullptr, s->red, s->red_cap, s->sm_count);
+  coop_tn(L, s->n, V, ldv, r, V, ldv, r, s->G, r, nullptr, 1.0, s->red, s->sm_count);
   std::vector<double> g((size_t)r * r);
   s->d2h(g.data(), s->G, (int64_t)r * r);
   s->sync();
@@ -592,10 +583,8 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
     s->max_nnz = std::max<int64_t>(0, max_nnz);
     s->sm_count = sm;
     s->ldq = s->cap;
-    // apply partial slices: enough to fill the GPU for small n; bounded memory for large n
-    const int64_t tiles = (n + 63) / 64;
-    s->part_slices = std::max<int64_t>(std::max<int64_t>(1, (2 * sm + tiles - 1) / tiles), (n + 4095) / 4096);
-    s->part_slices = std::min<int64_t>(s->part_slices, 64);
+    // apply partial slices: up to 16 (wave balancing of the persistent pass), <= 256 MiB
+    s->part_slices = std::max<int64_t>(1, std::min<int64_t>(16, (256ll << 20) / (n * (int64_t)max_block * 8)));
     s->red_cap = (int64_t)sm * std::max<int64_t>((int64_t)s->cap * std::max<int>(s->cap, max_block),
                                                  s->max_lowrank * max_block);
     struct Item {
@@ -660,6 +649,7 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
 void megb200_solver_destroy(megb200_solver* s) {
   if (!s) return;
   if (s->stream) cudaStreamSynchronize(s->stream);
+  for (auto e : s->ev_pool) cudaEventDestroy(e);
   cudaFree(s->arena);
   cudaFreeHost(s->h_buf);
   delete s;
@@ -932,6 +922,33 @@ int megb200_gen_dense_target(megb200_solver* s, const double* U, int64_t r, cons
     s->h2d(s->small, lam_host, r);
     gen_dense_target(s->launch(), U, r, s->small, sigma, stream_key(seed, (uint64_t)stream), M, dtype, ld, s->n);
     s->sync();
+  });
+}
+
+int megb200_profile_enable(megb200_solver* s, int32_t enable) {
+  return guarded_impl([&] {
+    if (!s) throw Error(MEGB200_ERR_PARAM, "solver is NULL");
+    s->prof = enable != 0;
+  });
+}
+
+int megb200_profile_read(megb200_solver* s, double* pass_ms, int64_t* passes, double* bytes) {
+  return guarded_impl([&] {
+    if (!s) throw Error(MEGB200_ERR_PARAM, "solver is NULL");
+    s->sync();
+    double total = 0.0;
+    for (auto& pr : s->ev_pending) {
+      float ms = 0.f;
+      MEG_CUDA(cudaEventElapsedTime(&ms, s->ev_pool[pr.first], s->ev_pool[pr.second]));
+      total += ms;
+    }
+    if (pass_ms) *pass_ms = total;
+    if (passes) *passes = s->prof_passes;
+    if (bytes) *bytes = s->prof_bytes;
+    s->ev_pending.clear();
+    s->ev_next = 0;
+    s->prof_bytes = 0.0;
+    s->prof_passes = 0;
   });
 }
 

@@ -1,0 +1,55 @@
+"""Device generator for the synthetic BASELINE inputs (twin of oracle/inputs.py).
+
+The counter-based Gaussian (splitmix64 finaliser + Box-Muller, csrc
+megb200_internal.h) is evaluated on the device, so an n = 32768 target is
+produced in HBM without host generation or upload.  The planted factor's QR
+runs once on the host (n x r, setup only), like the oracle.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from . import _lib, runtime
+from .configs import Workload
+
+
+def planted_factor(w: Workload) -> np.ndarray:
+    """Orthonormal n x r: QR of the stream-1 Gaussian block (counter i*r + j)."""
+    s = runtime.solver_for(w.n)
+    g = torch.empty((w.n, w.r), dtype=torch.float64, device=runtime.device())
+    runtime.check(s.lib.megb200_gen_gaussian(s.handle, w.seed, 1, 0, w.n, w.r, 1.0, 0, g.data_ptr(), g.stride(0)))
+    q, _ = np.linalg.qr(g.cpu().numpy())
+    return np.ascontiguousarray(q)
+
+
+def dense_target(w: Workload, U: np.ndarray | None = None) -> torch.Tensor:
+    """M = U diag(Lambda) U^T + sigma sym(G) generated in HBM (f64, or rounded to f32)."""
+    U = planted_factor(w) if U is None else U
+    s = runtime.solver_for(w.n)
+    ud = runtime.as_device_f64(U)
+    lam = np.ascontiguousarray(np.asarray(w.spectrum, dtype=np.float64))
+    tdt = torch.float64 if w.dtype == "f64" else torch.float32
+    m = torch.empty((w.n, w.n), dtype=tdt, device=runtime.device())
+    runtime.check(s.lib.megb200_gen_dense_target(s.handle, ud.data_ptr(), w.r, _lib.dptr(lam), float(w.noise),
+                                                 w.seed, 2, m.data_ptr(), runtime.dtype_code(m), m.stride(0)))
+    return m
+
+
+def initial_iterate(w: Workload, op_dense: torch.Tensor, tol: float = 1e-10):
+    """Warm start of SURVEY.md 8d step 4: top-r eigenpairs of M (device solver, basis 64),
+    simplex-projected weights floored at 1e-12, warm_start_wrap with eps0 = schedule(0)."""
+    from .linalg import SymmetricOperator, lanczos_top_r, project_simplex
+    from .meg import warm_start_wrap
+
+    top = lanczos_top_r(SymmetricOperator(w.n, dense=op_dense), w.r, tol=tol, seed=w.seed, subspace=64,
+                        return_device=True)
+    lam = project_simplex(top.eigenvalues, 1.0)
+    lam = lam / lam.sum()
+    lam = np.maximum(lam, 1e-12)
+    lam = lam / lam.sum()
+    return warm_start_wrap(top.eigenvectors, lam, w.eps(0))

@@ -1,0 +1,57 @@
+"""Where does a steady-state MEG step spend its time?  Host phases vs device time (cfg2)."""
+
+import ctypes as C
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2012_10469_b200 as pb  # noqa: E402
+from paper_2012_10469_b200 import configs, inputs, meg, runtime  # noqa: E402
+
+w = configs.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "cfg2"]
+m = inputs.dense_target(w)
+obj = pb.FrobeniusObjective.from_device(m, w.dtype)
+x = inputs.initial_iterate(w, m)
+for t in range(5):
+    x = pb.lowrank_meg_step(x, obj.grad_operator(x), 1.0, w.eps(t + 1), svd_seed=t, svd_subspace=w.subspace,
+                            block=w.block).iterate
+torch.cuda.synchronize()
+
+# monkeypatch the native call to time it
+s = runtime.solver_for(w.n)
+lib = s.lib
+orig = lib.megb200_lowrank_meg_step
+acc = {"native": 0.0}
+
+
+def timed(*a):
+    t0 = time.perf_counter()
+    rc = orig(*a)
+    acc["native"] += time.perf_counter() - t0
+    return rc
+
+
+class Shim:
+    def __getattr__(self, k):
+        return timed if k == "megb200_lowrank_meg_step" else getattr(lib, k)
+
+
+s.lib = Shim()
+K = 200
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+t0 = time.perf_counter()
+e0.record()
+for t in range(5, 5 + K):
+    x = pb.lowrank_meg_step(x, obj.grad_operator(x), 1.0, w.eps(t + 1), svd_seed=t, svd_subspace=w.subspace,
+                            block=w.block).iterate
+e1.record()
+torch.cuda.synchronize()
+host = (time.perf_counter() - t0) / K
+print(f"per step: host total {host*1e6:.1f} us, inside native call {acc['native']/K*1e6:.1f} us, "
+      f"python outside {(host - acc['native']/K)*1e6:.1f} us, device span {e0.elapsed_time(e1)/K*1e3:.1f} us, "
+      f"launches/step {s.launches}")
