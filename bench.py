@@ -285,7 +285,7 @@ def run_device_arm(args, world, rank, local):
     # ---- end to end through the public API with host buffers
     K2 = args.e2e_steps or K
     Vh = x.V.copy()
-    lam, eps, warm = x.lam.copy(), x.eps, x.warm_block
+    lam, eps, warm, werr = x.lam.copy(), x.eps, x.warm_block, x.warm_orth_err
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K2)]
     h2d = w.n * w.r * 8 + w.r * 8
     d2h = w.n * w.r * 8 + (4 * w.r + 3) * 8 + 8 * 8
@@ -294,11 +294,11 @@ def run_device_arm(args, world, rank, local):
     for i in range(K2):
         flush.zero_()
         ev2[i][0].record()
-        xi = pb.LowRankIterate(w.n, w.r, Vh, lam, eps, warm_block=warm)
+        xi = pb.LowRankIterate(w.n, w.r, Vh, lam, eps, warm_block=warm, warm_orth_err=werr)
         res = step(xi, t)
         Vh = res.iterate.V  # device -> host read of the step's result
         ev2[i][1].record()
-        lam, eps, warm = res.iterate.lam, res.iterate.eps, res.iterate.warm_block
+        lam, eps, warm, werr = res.iterate.lam, res.iterate.eps, res.iterate.warm_block, res.iterate.warm_orth_err
         t += 1
     torch.cuda.synchronize()
     e2e_s = sum(a.elapsed_time(b) for a, b in ev2) / 1e3

@@ -132,6 +132,7 @@ typedef struct megb200_eig_opts {
   const double* warm;    /* (device) optional warm-start block, n x warm_cols        */
   int64_t warm_cols;
   int64_t ld_warm;
+  int32_t warm_orthonormal; /* warm block verified orthonormal (<= 1e-13): skip its CholQR */
 } megb200_eig_opts;
 
 typedef struct megb200_eig_result {
@@ -167,6 +168,7 @@ typedef struct megb200_step_result {
   int32_t passes;
   int32_t restarts;
   int32_t ritz_cols;      /* columns written to ritz_block (<= 64)                  */
+  double ritz_orth_err;   /* max |B^T B - I| of the returned Ritz block B           */
 } megb200_step_result;
 
 typedef struct megb200_solver megb200_solver;
@@ -245,6 +247,11 @@ int megb200_gram_error(megb200_solver* s, const double* V, int64_t ldv, int32_t 
  * and resets the counters. */
 int megb200_profile_enable(megb200_solver* s, int32_t enable);
 int megb200_profile_read(megb200_solver* s, double* pass_ms, int64_t* passes, double* bytes);
+
+/* Phase tracer (diagnostics): CUDA events at solver phase boundaries; the
+ * report lists the average device time per phase tag. */
+int megb200_trace_enable(megb200_solver* s, int32_t enable);
+int megb200_trace_report(megb200_solver* s, char* buf, int64_t len);
 
 /* counters of the last call (for benchmarks): kernels launched. */
 int64_t megb200_kernel_launches(const megb200_solver* s);

@@ -55,6 +55,7 @@ class EigOpts(C.Structure):
         ("tol", C.c_double), ("max_passes", C.c_int32), ("restarts", C.c_int32),
         ("block", C.c_int32), ("basis", C.c_int32), ("keep", C.c_int32),
         ("seed", C.c_uint64), ("warm", C.c_void_p), ("warm_cols", C.c_int64), ("ld_warm", C.c_int64),
+        ("warm_orthonormal", C.c_int32),
     ]
 
 
@@ -75,6 +76,7 @@ class StepResult(C.Structure):
         ("lambda_r_plus_1", C.c_double), ("b_r_plus_1", C.c_double), ("shift", C.c_double),
         ("lhs_cheap", C.c_double), ("holds_cheap", C.c_int32), ("threshold", C.c_double),
         ("gram_err", C.c_double), ("passes", C.c_int32), ("restarts", C.c_int32), ("ritz_cols", C.c_int32),
+        ("ritz_orth_err", C.c_double),
     ]
 
 
@@ -111,6 +113,8 @@ SIGNATURES = [
     ("megb200_gram_error", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, c_double_p]),
     ("megb200_profile_enable", C.c_int, [C.c_void_p, C.c_int32]),
     ("megb200_profile_read", C.c_int, [C.c_void_p, c_double_p, C.POINTER(C.c_int64), c_double_p]),
+    ("megb200_trace_enable", C.c_int, [C.c_void_p, C.c_int32]),
+    ("megb200_trace_report", C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     ("megb200_kernel_launches", C.c_int64, [C.c_void_p]),
 ]
 

@@ -16,10 +16,27 @@
 #include <algorithm>
 
 #include "megb200_internal.h"
+#include "megb200_jacobi.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace megb200 {
+
+// Optional phase timestamps (compile with -DMEG_PHASE_TIMING): CTA 0 thread 0
+// records %globaltimer at phase boundaries of the cooperative kernels.
+__device__ unsigned long long g_phase_ns[64];
+__device__ __forceinline__ void phase_mark(int slot) {
+#ifdef MEG_PHASE_TIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_phase_ns[slot] = t;
+  }
+#else
+  (void)slot;
+#endif
+}
+
 namespace {
 
 constexpr int kCT = 256;     // threads per CTA
@@ -85,92 +102,117 @@ __device__ __forceinline__ void store_partial(double* __restrict__ part, int pq,
   }
 }
 
-// distributed final reduction: CTA g handles outputs o = g*kCT + tid + k*G*kCT
+// Distributed final reduction, one warp per output: lanes load partials
+// g = lane, lane + 32, ... in parallel (independent L2 loads) and combine with a
+// fixed xor-shuffle tree, so the result is reproducible and the latency is one
+// round trip instead of G dependent ones.
+__device__ __forceinline__ double warp_sum_partials(const double* __restrict__ part, int G, int64_t stride, int o) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int g = lane; g < G; g += 32) s += part[(int64_t)g * stride + o];
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
+}
+
 __device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int pq, int q,
                                                 double* __restrict__ C, int64_t ldc,
                                                 const double* __restrict__ rowscale, double scale) {
   const int G = gridDim.x;
-  for (int o = blockIdx.x * kCT + threadIdx.x; o < pq; o += G * kCT) {
-    double s = 0.0;
-    for (int g = 0; g < G; ++g) s += part[(int64_t)g * pq + o];
-    const int a = o / q, c = o - a * q;
-    if (rowscale) s *= rowscale[a];
-    C[(int64_t)a * ldc + c] = scale * s;
+  const int wpb = kCT / 32;
+  const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
+  for (int o = gw; o < pq; o += G * wpb) {
+    double s = warp_sum_partials(part, G, pq, o);
+    if ((threadIdx.x & 31) == 0) {
+      const int a = o / q, c = o - a * q;
+      if (rowscale) s *= rowscale[a];
+      C[(int64_t)a * ldc + c] = scale * s;
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
-// Cholesky of a q x q SPD Gram (q <= 64) in one warp, column-equilibrated,
-// breakdown (pivot <= thresh^2 absolute or 1e-20 relative) -> flagged column.
-// Writes Rrel (zero rows for flagged columns), Rinv, mask; optionally
-// Rtot = Rrel * Rprev.
-__device__ void warp_cholesky(const double* __restrict__ Gg, int q, double thresh, double* sm,
-                              double* __restrict__ Rrel, double* __restrict__ Rinv, int* __restrict__ mask,
-                              const double* __restrict__ Rprev, double* __restrict__ Rtot) {
-  const int lane = threadIdx.x & 31;
+// Cholesky of a q x q SPD Gram (q <= 64) by one CTA (all threads),
+// column-equilibrated, with breakdown detection (pivot <= thresh^2 absolute or
+// 1e-20 relative -> flagged column).  Writes Rrel (zero rows for flagged
+// columns), Rinv (by a row-parallel backward sweep, reciprocal multiplies
+// only), mask; optionally Rtot = Rrel * Rprev.
+__device__ void block_cholesky(const double* __restrict__ Gg, int q, double thresh, double* sm,
+                               double* __restrict__ Rrel, double* __restrict__ Rinv, int* __restrict__ mask,
+                               const double* __restrict__ Rprev, double* __restrict__ Rtot) {
+  const int t = threadIdx.x, nth = blockDim.x;
   const int ld = q + 1;
-  double* A = sm;            // q x ld
-  double* R = sm + q * ld;   // q x ld
-  double* D = R + q * ld;    // q
-  int* bad = reinterpret_cast<int*>(D + q);
-  for (int idx = lane; idx < q * q; idx += 32) {
+  double* A = sm;             // q x ld   (factorised in place: upper triangle -> Rs)
+  double* X = sm + q * ld;    // q x ld   (Rs^-1)
+  double* D = X + q * ld;     // q
+  double* rd = D + q;         // q  (1 / Rs_ii)
+  int* bad = reinterpret_cast<int*>(rd + q);
+  for (int idx = t; idx < q * q; idx += nth) {
     const int i = idx / q, j = idx - i * q;
     A[i * ld + j] = Gg[(i <= j) ? i * q + j : j * q + i];
-    R[i * ld + j] = 0.0;
+    X[i * ld + j] = 0.0;
   }
-  __syncwarp();
-  for (int t = lane; t < q; t += 32) {
-    const double g = A[t * ld + t];
-    bad[t] = !(g > thresh * thresh);
-    D[t] = bad[t] ? 1.0 : sqrt(g);
+  __syncthreads();
+  for (int i = t; i < q; i += nth) {
+    const double g = A[i * ld + i];
+    bad[i] = !(g > thresh * thresh);
+    D[i] = bad[i] ? 1.0 : sqrt(g);
   }
-  __syncwarp();
-  for (int idx = lane; idx < q * q; idx += 32) {
+  __syncthreads();
+  for (int idx = t; idx < q * q; idx += nth) {
     const int i = idx / q, j = idx - i * q;
     A[i * ld + j] = (bad[i] || bad[j]) ? (i == j ? 1.0 : 0.0) : A[i * ld + j] / (D[i] * D[j]);
   }
-  __syncwarp();
+  __syncthreads();
+  // right-looking factorisation: column j pivot by thread 0, row scale + trailing update in parallel
   for (int j = 0; j < q; ++j) {
-    const double d = A[j * ld + j];
-    const bool bj = bad[j] || !(d > 1e-20);
-    const double rjj = bj ? 1.0 : sqrt(d);
-    __syncwarp();
-    if (lane == 0) {
+    if (t == 0) {
+      const double d = A[j * ld + j];
+      const bool bj = bad[j] || !(d > 1e-20);
       bad[j] = bj;
-      R[j * ld + j] = rjj;
+      const double r = bj ? 1.0 : sqrt(d);
+      A[j * ld + j] = r;
+      rd[j] = 1.0 / r;
     }
-    for (int k = j + 1 + lane; k < q; k += 32) R[j * ld + k] = bj ? 0.0 : A[j * ld + k] / rjj;
-    __syncwarp();
+    __syncthreads();
+    const double ir = rd[j];
+    const bool bj = bad[j];
+    for (int k = j + 1 + t; k < q; k += nth) A[j * ld + k] = bj ? 0.0 : A[j * ld + k] * ir;
+    __syncthreads();
     const int m = q - j - 1;
-    for (int idx = lane; idx < m * m; idx += 32) {
+    for (int idx = t; idx < m * m; idx += nth) {
       const int k = j + 1 + idx / m, l = j + 1 + idx % m;
-      A[k * ld + l] -= R[j * ld + k] * R[j * ld + l];
+      if (l >= k) A[k * ld + l] -= A[j * ld + k] * A[j * ld + l];
     }
-    __syncwarp();
+    __syncthreads();
   }
-  // Rinv = D^-1 Rs^-1 : lane c owns column c (q <= 64 -> two passes)
-  for (int c = lane; c < q; c += 32) {
-    double x[64];
-    x[c] = 1.0 / R[c * ld + c];
-    for (int i = c - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int k = i + 1; k <= c; ++k) s += R[i * ld + k] * x[k];
-      x[i] = -s / R[i * ld + i];
+  // Rs^-1 by rows from the bottom: X[i][c] = -rd_i * sum_{k=i+1..c} Rs[i][k] X[k][c], X[i][i] = rd_i
+  for (int i = q - 1; i >= 0; --i) {
+    for (int c = i + t; c < q; c += nth) {
+      double v;
+      if (c == i) {
+        v = rd[i];
+      } else {
+        double s = 0.0;
+        for (int k = i + 1; k <= c; ++k) s = fma(A[i * ld + k], X[k * ld + c], s);
+        v = -s * rd[i];
+      }
+      X[i * ld + c] = v;
     }
-    for (int i = 0; i < q; ++i) Rinv[i * q + c] = (i <= c) ? x[i] / D[i] : 0.0;
+    __syncthreads();
   }
-  for (int idx = lane; idx < q * q; idx += 32) {
+  for (int idx = t; idx < q * q; idx += nth) {
     const int i = idx / q, j = idx - i * q;
-    Rrel[idx] = (bad[i] || j < i) ? 0.0 : R[i * ld + j] * D[j];
+    Rinv[idx] = (i <= j) ? X[i * ld + j] / D[i] : 0.0;
+    Rrel[idx] = (bad[i] || j < i) ? 0.0 : A[i * ld + j] * D[j];
   }
-  for (int t = lane; t < q; t += 32) mask[t] = bad[t];
-  __syncwarp();
+  for (int i = t; i < q; i += nth) mask[i] = bad[i];
   if (Rtot) {
-    for (int idx = lane; idx < q * q; idx += 32) {
+    for (int idx = t; idx < q * q; idx += nth) {
       const int i = idx / q, j = idx - i * q;
       double s = 0.0;
       if (!bad[i])
-        for (int k = i; k < q; ++k) s += R[i * ld + k] * D[k] * Rprev[k * q + j];
+        for (int k = i; k < q; ++k) s += A[i * ld + k] * D[k] * Rprev[k * q + j];
       Rtot[idx] = s;
     }
   }
@@ -226,24 +268,30 @@ __global__ void __launch_bounds__(kCT) k_coop_cgs(int64_t n, const double* __res
 // One CholQR round: G = W^T W, R = chol(G) (CTA 0, one warp), W = W R^-1 with
 // breakdown columns replaced by seeded random normals.
 template <int J>
-__global__ void __launch_bounds__(kCT) k_coop_cholqr(int64_t n, double* __restrict__ W, int64_t ldw, int q,
+__global__ void __launch_bounds__(kCT) k_coop_cholqr(int64_t n, const double* __restrict__ Wsrc, int64_t lds, double* __restrict__ W, int64_t ldw, int q,
                                                       double thresh, double* __restrict__ Gws,
                                                       double* __restrict__ Rrel, double* __restrict__ Rinv,
                                                       int* __restrict__ mask, const double* __restrict__ Rprev,
                                                       double* __restrict__ Rtot, uint64_t key, uint64_t base,
                                                       double* __restrict__ part) {
   extern __shared__ double sm[];
+  phase_mark(0);
   int64_t r0, r1;
   cta_rows(n, r0, r1);
   double acc[J];
-  xty_rows<J>(r0, r1, W, ldw, q, W, ldw, q, sm, acc);
+  xty_rows<J>(r0, r1, Wsrc, lds, q, Wsrc, lds, q, sm, acc);
   store_partial<J>(part, q * q, acc);
+  phase_mark(1);
   cg::grid_group grid = cg::this_grid();
   grid.sync();
+  phase_mark(2);
   reduce_partials(part, q * q, q, Gws, q, nullptr, 1.0);
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x < 32) warp_cholesky(Gws, q, thresh, sm, Rrel, Rinv, mask, Rprev, Rtot);
+  phase_mark(3);
+  if (blockIdx.x == 0) block_cholesky(Gws, q, thresh, sm, Rrel, Rinv, mask, Rprev, Rtot);
+  phase_mark(4);
   grid.sync();
+  phase_mark(5);
   double* Ri = sm;
   int* bad = reinterpret_cast<int*>(sm + q * q);
   for (int idx = threadIdx.x; idx < q * q; idx += kCT) Ri[idx] = Rinv[idx];
@@ -256,7 +304,7 @@ __global__ void __launch_bounds__(kCT) k_coop_cholqr(int64_t n, double* __restri
     __syncthreads();
     for (int idx = threadIdx.x; idx < rows * q; idx += kCT) {
       const int r = idx / q, c = idx - r * q;
-      Ws[idx] = W[(rc + r) * ldw + c];
+      Ws[idx] = Wsrc[(rc + r) * lds + c];
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < rows * q; idx += kCT) {
@@ -271,73 +319,21 @@ __global__ void __launch_bounds__(kCT) k_coop_cholqr(int64_t n, double* __restri
       W[(rc + r) * ldw + c] = v;
     }
   }
-}
-
-// Ritz vectors and residuals: T[:, 0:rq] = Q S[:, 0:rq]; AX = AQ S[:, 0:nreq];
-// resid[j] = ||AX_j - theta_j X_j|| (j < nreq).  S is cols x ldS row-major.
-// Thread t owns column c = t % rq of rows t / rq, t / rq + rpt, ... so each
-// thread accumulates one column's squared residual in a register.
-__global__ void __launch_bounds__(kCT) k_coop_ritz(int64_t n, const double* __restrict__ Q,
-                                                   const double* __restrict__ AQ, int64_t ldq, int cols,
-                                                   const double* __restrict__ S, int ldS, int rq, int nreq,
-                                                   const double* __restrict__ theta, double* __restrict__ T,
-                                                   int64_t ldt, double* __restrict__ resid,
-                                                   double* __restrict__ part) {
-  extern __shared__ double sm[];
-  double* Ss = sm;               // cols x rq
-  double* red = sm + cols * rq;  // kCT
-  for (int idx = threadIdx.x; idx < cols * rq; idx += kCT) {
-    const int k = idx / rq, c = idx - k * rq;
-    Ss[idx] = S[k * ldS + c];
-  }
-  __syncthreads();
-  int64_t r0, r1;
-  cta_rows(n, r0, r1);
-  const int rpt = kCT / rq;  // rows in flight per sweep
-  const int c = threadIdx.x % rq;
-  const int rofs = threadIdx.x / rq;
-  double sq = 0.0;
-  if (rofs < rpt) {
-    const double th = c < nreq ? theta[c] : 0.0;
-    for (int64_t r = r0 + rofs; r < r1; r += rpt) {
-      const double* qr = Q + r * ldq;
-      double x = 0.0;
-      for (int k = 0; k < cols; ++k) x = fma(qr[k], Ss[k * rq + c], x);
-      T[r * ldt + c] = x;
-      if (c < nreq) {
-        const double* ar = AQ + r * ldq;
-        double ax = 0.0;
-        for (int k = 0; k < cols; ++k) ax = fma(ar[k], Ss[k * rq + c], ax);
-        const double d = ax - th * x;
-        sq = fma(d, d, sq);
-      }
-    }
-  }
-  red[threadIdx.x] = sq;
-  __syncthreads();
-  if (threadIdx.x < nreq) {
-    double s = 0.0;
-    for (int t = threadIdx.x; t < rpt * rq; t += rq) s += red[t];
-    part[(int64_t)blockIdx.x * nreq + threadIdx.x] = s;
-  }
-  cg::this_grid().sync();
-  if (blockIdx.x == 0 && threadIdx.x < nreq) {
-    double s = 0.0;
-    for (int g = 0; g < (int)gridDim.x; ++g) s += part[(int64_t)g * nreq + threadIdx.x];
-    resid[threadIdx.x] = sqrt(s);
-  }
+  phase_mark(6);
 }
 
 // Operator epilogue: E = diag(d) L^T U (reduced across the grid), then
 // W = scale * sum_s part[s] + L E + alpha U.
-template <int J>
+template <int J, int J2>
 __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, const double* __restrict__ spart,
                                                       double scale, const double* __restrict__ Lf, int64_t ldl, int l,
                                                       const double* __restrict__ d, double alpha,
                                                       const double* __restrict__ U, int64_t ldu,
                                                       double* __restrict__ W, int64_t ldw, double* __restrict__ Ews,
-                                                      double* __restrict__ part) {
+                                                      double* __restrict__ part, const double* __restrict__ Qh,
+                                                      int64_t ldq, int hp, double* __restrict__ Hout, int64_t ldh) {
   extern __shared__ double sm[];
+  phase_mark(20);
   int64_t r0, r1;
   cta_rows(n, r0, r1);
   if (l > 0) {
@@ -346,22 +342,42 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
     store_partial<J>(part, l * b, acc);
     cg::grid_group grid = cg::this_grid();
     grid.sync();
+    phase_mark(21);
     reduce_partials(part, l * b, b, Ews, b, d, 1.0);
     grid.sync();
   }
+  phase_mark(22);
   double* Es = sm;
   for (int idx = threadIdx.x; idx < l * b; idx += kCT) Es[idx] = Ews[idx];
   __syncthreads();
   for (int64_t idx = threadIdx.x; idx < (r1 - r0) * b; idx += kCT) {
     const int64_t i = r0 + idx / b;
     const int c = (int)(idx % b);
+    double pv[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) pv[t] = t < S ? spart[(int64_t)t * n * b + i * b + c] : 0.0;
     double s = 0.0;
-    for (int t = 0; t < S; ++t) s += spart[(int64_t)t * n * b + i * b + c];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) s += pv[t];
     double v = scale * s + alpha * U[i * ldu + c];
     const double* Lr = Lf + i * ldl;
     for (int k = 0; k < l; ++k) v = fma(Lr[k], Es[k * b + c], v);
     W[i * ldw + c] = v;
   }
+  phase_mark(23);
+  if (Hout) {
+    // H[0:hp, :] = Q[:, 0:hp]^T W over this CTA's rows (W just written), reduced across the grid
+    __syncthreads();
+    double acc2[J2];
+    xty_rows<J2>(r0, r1, Qh, ldq, hp, W, ldw, b, sm, acc2);
+    store_partial<J2>(part, hp * b, acc2);  // E partials were consumed before the previous grid.sync
+    cg::grid_group grid = cg::this_grid();
+    phase_mark(24);
+    grid.sync();
+    phase_mark(25);
+    reduce_partials(part, hp * b, b, Hout, ldh, nullptr, 1.0);
+  }
+  phase_mark(26);
 }
 
 int coop_grid(int64_t n, int sm_count) {
@@ -438,11 +454,11 @@ void coop_cgs(const Launch& L, int64_t n, const double* Q, int64_t ldq, int cols
 #undef MEG_CGS
 }
 
-void coop_cholqr(const Launch& L, int64_t n, double* W, int64_t ldw, int q, double thresh, double* Gws, double* Rrel,
-                 double* Rinv, int* mask, const double* Rprev, double* Rtot, uint64_t key, uint64_t base, double* part,
-                 int sm_count) {
+void coop_cholqr(const Launch& L, int64_t n, const double* Wsrc, int64_t lds, double* W, int64_t ldw, int q,
+                 double thresh, double* Gws, double* Rrel, double* Rinv, int* mask, const double* Rprev, double* Rtot,
+                 uint64_t key, uint64_t base, double* part, int sm_count) {
   const int G = coop_grid(n, sm_count);
-  const size_t chol_smem = (size_t)(2 * q * (q + 1) + q + 1) * sizeof(double) + 64 * sizeof(int);
+  const size_t chol_smem = (size_t)(2 * q * (q + 1) + 2 * q + 1) * sizeof(double) + 64 * sizeof(int);
   const size_t smem = std::max({(size_t)kRC * 2 * q * sizeof(double), chol_smem,
                                 (size_t)(q * q + 64 + kRC * q) * sizeof(double)});
   const int J = pick_j(q * q);
@@ -450,42 +466,198 @@ void coop_cholqr(const Launch& L, int64_t n, double* W, int64_t ldw, int q, doub
   {                                                                                                          \
     static bool a = false;                                                                                   \
     if (!a) { raise_smem(k_coop_cholqr<jj>, kCoopSmem); a = true; }                                          \
-    coop_launch(L, k_coop_cholqr<jj>, G, smem, n, W, ldw, q, thresh, Gws, Rrel, Rinv, mask, Rprev, Rtot, key, \
+    coop_launch(L, k_coop_cholqr<jj>, G, smem, n, Wsrc, lds, W, ldw, q, thresh, Gws, Rrel, Rinv, mask, Rprev, Rtot, key, \
                 base, part);                                                                                 \
   }
   MEG_J_DISPATCH(J, MEG_CQR)
 #undef MEG_CQR
 }
 
-void coop_ritz(const Launch& L, int64_t n, const double* Q, const double* AQ, int64_t ldq, int cols, const double* S,
-               int ldS, int rq, int nreq, const double* theta, double* T, int64_t ldt, double* resid, double* part,
-               int sm_count) {
-  if (nreq > 64 || rq > 64) throw Error(MEGB200_ERR_PARAM, "ritz: at most 64 vectors");
-  const int G = coop_grid(n, sm_count);
-  const size_t smem = (size_t)(cols * rq + kCT) * sizeof(double);
-  static bool a = false;
-  if (!a) {
-    raise_smem(k_coop_ritz, kCoopSmem);
-    a = true;
-  }
-  coop_launch(L, k_coop_ritz, G, smem, n, Q, AQ, ldq, cols, S, ldS, rq, nreq, theta, T, ldt, resid, part);
-}
-
 void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, double scale, const double* Lf,
                  int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
-                 int64_t ldw, double* Ews, double* part, int sm_count) {
+                 int64_t ldw, double* Ews, double* part, int sm_count, const double* Qh, int64_t ldq, int hp,
+                 double* Hout, int64_t ldh) {
   const int G = coop_grid(n, sm_count);
-  const size_t smem = std::max((size_t)kRC * (l + b), (size_t)std::max(1, l * b)) * sizeof(double);
+  const size_t smem = std::max({(size_t)kRC * (l + b), (size_t)std::max(1, l * b), (size_t)kRC * (hp + b)}) *
+                      sizeof(double);
   const int J = pick_j(std::max(1, l * b));
-#define MEG_FIN(jj)                                                                                            \
-  {                                                                                                            \
-    static bool a = false;                                                                                     \
-    if (!a) { raise_smem(k_coop_finish<jj>, kCoopSmem); a = true; }                                            \
-    coop_launch(L, k_coop_finish<jj>, G, smem, n, b, S, spart, scale, Lf, ldl, l, d, alpha, U, ldu, W, ldw, Ews, \
-                part);                                                                                         \
+  const int J2 = Hout ? pick_j(hp * b) : 1;
+#define MEG_FIN2(jj, j2)                                                                                        \
+  {                                                                                                             \
+    static bool a = false;                                                                                      \
+    if (!a) { raise_smem(k_coop_finish<jj, j2>, kCoopSmem); a = true; }                                         \
+    coop_launch(L, k_coop_finish<jj, j2>, G, smem, n, b, S, spart, scale, Lf, ldl, l, d, alpha, U, ldu, W, ldw,  \
+                Ews, part, Qh, ldq, hp, Hout, ldh);                                                             \
+  }
+#define MEG_FIN(jj)                                            \
+  switch (J2) {                                                \
+    case 1: MEG_FIN2(jj, 1); break;                            \
+    case 2: MEG_FIN2(jj, 2); break;                            \
+    case 4: MEG_FIN2(jj, 4); break;                            \
+    case 8: MEG_FIN2(jj, 8); break;                            \
+    case 16: MEG_FIN2(jj, 16); break;                          \
+    default: MEG_FIN2(jj, 24); break;                          \
   }
   MEG_J_DISPATCH(J, MEG_FIN)
 #undef MEG_FIN
+#undef MEG_FIN2
+}
+
+// ===========================================================================
+// Rayleigh-Ritz + Ritz vectors + residuals (+ optional V_next Gram and MEG
+// step epilogue) in one cooperative launch: CTA 0 runs the Jacobi
+// eigensolver while the grid waits, then every CTA forms its rows of the
+// Ritz block and the squared residuals.
+template <int JG>
+__global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H, int64_t ldh, int m,
+                                                   double* __restrict__ theta, double* __restrict__ S,
+                                                   double* __restrict__ info, int64_t n, const double* __restrict__ Q,
+                                                   const double* __restrict__ AQ, int64_t ldq, int rq, int nreq,
+                                                   double* __restrict__ T, int64_t ldt, double* __restrict__ resid,
+                                                   double* __restrict__ part, int gr, double* __restrict__ Gout,
+                                                   double eps_next, double* __restrict__ epi) {
+  extern __shared__ double sm[];
+  cg::grid_group grid = cg::this_grid();
+  phase_mark(10);
+  if (blockIdx.x == 0) block_jacobi(H, ldh, m, theta, S, sm, info);
+  phase_mark(11);
+  grid.sync();
+  phase_mark(12);
+  const int cols = m;
+  double* Ss = sm;
+  double* red = sm + cols * rq;
+  for (int idx = threadIdx.x; idx < cols * rq; idx += kCT) {
+    const int k = idx / rq, c = idx - k * rq;
+    Ss[idx] = S[k * m + c];
+  }
+  __syncthreads();
+  int64_t r0, r1;
+  cta_rows(n, r0, r1);
+  const int rpt = kCT / rq;
+  const int c = threadIdx.x % rq;
+  const int rofs = threadIdx.x / rq;
+  double sq = 0.0;
+  if (rofs < rpt) {
+    const double th = c < nreq ? theta[c] : 0.0;
+    for (int64_t r = r0 + rofs; r < r1; r += rpt) {
+      const double* qr = Q + r * ldq;
+      double x = 0.0;
+      for (int k = 0; k < cols; ++k) x = fma(qr[k], Ss[k * rq + c], x);
+      T[r * ldt + c] = x;
+      if (c < nreq) {
+        const double* ar = AQ + r * ldq;
+        double ax = 0.0;
+        for (int k = 0; k < cols; ++k) ax = fma(ar[k], Ss[k * rq + c], ax);
+        const double d = ax - th * x;
+        sq = fma(d, d, sq);
+      }
+    }
+  }
+  red[threadIdx.x] = sq;
+  __syncthreads();
+  double* rpart = part;                                   // G x nreq
+  double* gpart = part + (int64_t)gridDim.x * nreq;       // G x gr*gr
+  if (threadIdx.x < nreq) {
+    double s2 = 0.0;
+    for (int t = threadIdx.x; t < rpt * rq; t += rq) s2 += red[t];
+    rpart[(int64_t)blockIdx.x * nreq + threadIdx.x] = s2;
+  }
+  if (gr > 0) {
+    __syncthreads();
+    double acc[JG];
+    xty_rows<JG>(r0, r1, T, ldt, gr, T, ldt, gr, sm + cols * rq + kCT, acc);
+    double* out = gpart + (int64_t)blockIdx.x * gr * gr;
+#pragma unroll
+    for (int j = 0; j < JG; ++j) {
+      const int o = threadIdx.x + j * kCT;
+      if (o < gr * gr) out[o] = acc[j];
+    }
+  }
+  phase_mark(13);
+  grid.sync();
+  phase_mark(14);
+  {
+    // warp-per-output grid reduction of the residual squares and the Gram
+    const int wpb = kCT / 32;
+    const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
+    const int nout = nreq + gr * gr;
+    for (int o = gw; o < nout; o += gridDim.x * wpb) {
+      const double v = o < nreq ? warp_sum_partials(rpart, gridDim.x, nreq, o)
+                                : warp_sum_partials(gpart, gridDim.x, gr * gr, o - nreq);
+      if ((threadIdx.x & 31) == 0) {
+        if (o < nreq)
+          resid[o] = sqrt(v);
+        else
+          Gout[o - nreq] = v;
+      }
+    }
+  }
+  phase_mark(15);
+  if (blockIdx.x == 0) {
+    if (epi && threadIdx.x == 0) {
+      // step epilogue (meg.py:347-356): y = exp(mu - mu_1), lam, lambda_{r+1}, b_{r+1}, cheap certificate
+      const int r = nreq - 1;
+      const double shift = theta[0];
+      double kept = 0.0, b = 0.0, lsum = 0.0;
+      for (int k = 0; k <= r; ++k) {
+        const double y = exp(theta[k] - shift);
+        epi[k] = y;
+        if (k < r) kept += y;
+        b += y;
+      }
+      double status = !(kept > 1e-290) ? 4.0 : 0.0;
+      for (int k = 0; k < r; ++k) {
+        epi[r + 1 + k] = epi[k] / kept;
+        lsum += epi[r + 1 + k];
+      }
+      for (int k = 0; k < r; ++k) epi[r + 1 + k] /= lsum;
+      const double lam_rp1 = epi[r];
+      double lhs;
+      if (!(b > 0.0) || lam_rp1 < 0.0) {
+        status = 1.0;
+        lhs = 0.0;
+      } else if (lam_rp1 == 0.0) {
+        lhs = -INFINITY;
+      } else {
+        lhs = log((double)(n - r) * lam_rp1 / (eps_next * b));
+      }
+      double* tail = epi + 2 * r + 1;
+      tail[0] = lam_rp1;
+      tail[1] = b;
+      tail[2] = shift;
+      tail[3] = lhs;
+      tail[4] = (lhs <= 2.0 * eps_next) ? 1.0 : 0.0;
+      tail[5] = 2.0 * eps_next;
+      tail[6] = status;
+    }
+  }
+}
+
+void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,
+             const double* Q, const double* AQ, int64_t ldq, int rq, int nreq, double* T, int64_t ldt, double* resid,
+             double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi) {
+  if (nreq > 64 || rq > 64) throw Error(MEGB200_ERR_PARAM, "rr: at most 64 Ritz vectors");
+  const int G = coop_grid(n, sm_count);
+  const size_t smem = std::max((size_t)jacobi_smem_doubles(m),
+                               (size_t)(m * rq + kCT + kRC * 2 * std::max(gr, 1))) * sizeof(double);
+  const int JG = pick_j(std::max(1, gr * gr));
+#define MEG_RR(jj)                                                                                              \
+  {                                                                                                             \
+    static bool a = false;                                                                                      \
+    if (!a) { raise_smem(k_coop_rr<jj>, 215 * 1024); a = true; }                                                \
+    coop_launch(L, k_coop_rr<jj>, G, smem, H, ldh, m, theta, S, info, n, Q, AQ, ldq, rq, nreq, T, ldt, resid,    \
+                part, gr, Gout, eps_next, epi);                                                                 \
+  }
+  MEG_J_DISPATCH(JG, MEG_RR)
+#undef MEG_RR
 }
 
 }  // namespace megb200
+
+// Diagnostics: copy the phase timestamps of the last cooperative launches (-DMEG_PHASE_TIMING builds).
+extern "C" int megb200_debug_phase_ns(unsigned long long* out, int count) {
+  if (!out || count < 1 || count > 64) return MEGB200_ERR_PARAM;
+  return cudaMemcpyFromSymbol(out, megb200::g_phase_ns, sizeof(unsigned long long) * count) == cudaSuccess
+             ? MEGB200_OK
+             : MEGB200_ERR_CUDA;
+}

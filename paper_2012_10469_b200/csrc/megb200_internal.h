@@ -113,14 +113,16 @@ void coop_tn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, co
              double* C, int64_t ldc, const double* rowscale, double scale, double* part, int sm_count);
 void coop_cgs(const Launch& L, int64_t n, const double* Q, int64_t ldq, int cols, double* W, int64_t ldw, int q,
               double* Cws, double* part, int sm_count);
-void coop_cholqr(const Launch& L, int64_t n, double* W, int64_t ldw, int q, double thresh, double* Gws, double* Rrel,
-                 double* Rinv, int* mask, const double* Rprev, double* Rtot, uint64_t key, uint64_t base, double* part,
-                 int sm_count);
-void coop_ritz(const Launch& L, int64_t n, const double* Q, const double* AQ, int64_t ldq, int cols, const double* S,
-               int ldS, int rq, int nreq, const double* theta, double* T, int64_t ldt, double* resid, double* part,
-               int sm_count);
+void coop_cholqr(const Launch& L, int64_t n, const double* Wsrc, int64_t lds, double* W, int64_t ldw, int q,
+                 double thresh, double* Gws, double* Rrel, double* Rinv, int* mask, const double* Rprev, double* Rtot,
+                 uint64_t key, uint64_t base, double* part, int sm_count);
 void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, double scale, const double* Lf,
                  int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
-                 int64_t ldw, double* Ews, double* part, int sm_count);
+                 int64_t ldw, double* Ews, double* part, int sm_count, const double* Qh = nullptr, int64_t ldq = 0,
+                 int hp = 0, double* Hout = nullptr, int64_t ldh = 0);
+// Jacobi RR + Ritz block + residuals (+ Gram of the first gr Ritz vectors, + MEG epilogue into epi)
+void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,
+             const double* Q, const double* AQ, int64_t ldq, int rq, int nreq, double* T, int64_t ldt, double* resid,
+             double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi);
 
 }  // namespace megb200

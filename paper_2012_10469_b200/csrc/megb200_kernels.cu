@@ -18,6 +18,7 @@
 #include <string>
 
 #include "megb200_internal.h"
+#include "megb200_jacobi.cuh"
 
 namespace megb200 {
 namespace {
@@ -735,135 +736,11 @@ __global__ void __launch_bounds__(kJacobiThreads, 1)
                 double* __restrict__ Sout, const double* __restrict__ Rn, int rn_rows, int cur, int nreq,
                 double* __restrict__ est, double* __restrict__ info) {
   extern __shared__ double sm[];
-  const int mp = (m + 1) & ~1;  // padded even size
-  double* H = sm;               // mp x mp
-  double* V = sm + mp * mp;     // mp x mp
-  __shared__ double cs[64], sn[64];
-  __shared__ int pp[64], qq[64];
-  __shared__ double red[32];
-  __shared__ int done;
-  const int t = threadIdx.x;
-  const int half = mp / 2;
-  for (int idx = t; idx < mp * mp; idx += blockDim.x) {
-    const int i = idx / mp, j = idx - i * mp;
-    double h = 0.0;
-    if (i < m && j < m) h = (i <= j) ? Hg[i * ldh + j] : Hg[j * ldh + i];
-    H[idx] = h;
-    V[idx] = (i == j) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  // scale for the stopping rule
-  double local = 0.0;
-  for (int idx = t; idx < mp * mp; idx += blockDim.x) local += H[idx] * H[idx];
-  for (int off = 16; off >= 1; off >>= 1) local += __shfl_xor_sync(0xffffffffu, local, off);
-  if ((t & 31) == 0) red[t >> 5] = local;
-  __syncthreads();
-  if (t == 0) {
-    double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    red[0] = s;
-  }
-  __syncthreads();
-  const double fro2 = red[0];
-  const double stop2 = fro2 * 1e-30;  // off(H) <= 1e-15 ||H||_F
-  int sweep = 0;
-  double off2 = 0.0;
-  for (sweep = 0; sweep < 40; ++sweep) {
-    for (int round = 0; round < mp - 1; ++round) {
-      if (t < half) {
-        int p, q;
-        if (t == 0) {
-          p = 0;
-          q = 1 + (round % (mp - 1));
-        } else {
-          p = 1 + (round + t) % (mp - 1);
-          q = 1 + (round - t + (mp - 1)) % (mp - 1);
-        }
-        if (p > q) {
-          const int tmp = p;
-          p = q;
-          q = tmp;
-        }
-        const double apq = H[p * mp + q];
-        double c = 1.0, s = 0.0;
-        if (apq != 0.0) {
-          const double tau = (H[q * mp + q] - H[p * mp + p]) / (2.0 * apq);
-          const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + tt * tt);
-          s = tt * c;
-        }
-        pp[t] = p;
-        qq[t] = q;
-        cs[t] = c;
-        sn[t] = s;
-      }
-      __syncthreads();
-      // H <- J^T H J on all 2x2 blocks, V <- V J
-      for (int idx = t; idx < half * half; idx += blockDim.x) {
-        const int a = idx / half, bb = idx - a * half;
-        const int pa = pp[a], qa = qq[a], pb = pp[bb], qb = qq[bb];
-        const double ca = cs[a], sa = sn[a], cb = cs[bb], sb = sn[bb];
-        const double h00 = H[pa * mp + pb], h01 = H[pa * mp + qb];
-        const double h10 = H[qa * mp + pb], h11 = H[qa * mp + qb];
-        const double t00 = ca * h00 - sa * h10, t01 = ca * h01 - sa * h11;
-        const double t10 = sa * h00 + ca * h10, t11 = sa * h01 + ca * h11;
-        double n00 = t00 * cb - t01 * sb, n01 = t00 * sb + t01 * cb;
-        double n10 = t10 * cb - t11 * sb, n11 = t10 * sb + t11 * cb;
-        if (a == bb) {
-          n01 = 0.0;
-          n10 = 0.0;
-        }
-        H[pa * mp + pb] = n00;
-        H[pa * mp + qb] = n01;
-        H[qa * mp + pb] = n10;
-        H[qa * mp + qb] = n11;
-      }
-      for (int idx = t; idx < mp * half; idx += blockDim.x) {
-        const int i = idx / half, a = idx - i * half;
-        const int pa = pp[a], qa = qq[a];
-        const double ca = cs[a], sa = sn[a];
-        const double vp = V[i * mp + pa], vq = V[i * mp + qa];
-        V[i * mp + pa] = ca * vp - sa * vq;
-        V[i * mp + qa] = sa * vp + ca * vq;
-      }
-      __syncthreads();
-    }
-    // off-diagonal mass
-    double lo = 0.0;
-    for (int idx = t; idx < mp * mp; idx += blockDim.x) {
-      const int i = idx / mp, j = idx - i * mp;
-      if (i != j) lo += H[idx] * H[idx];
-    }
-    for (int off = 16; off >= 1; off >>= 1) lo += __shfl_xor_sync(0xffffffffu, lo, off);
-    __syncthreads();
-    if ((t & 31) == 0) red[t >> 5] = lo;
-    __syncthreads();
-    if (t == 0) {
-      double s = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-      red[0] = s;
-      done = (s <= stop2);
-    }
-    __syncthreads();
-    off2 = red[0];
-    if (done) break;
-    __syncthreads();
-  }
-  // sort eigenvalues non-increasing (stable by index) and write theta, S
-  for (int i = t; i < m; i += blockDim.x) {
-    const double di = H[i * mp + i];
-    int rank = 0;
-    for (int j = 0; j < m; ++j) {
-      const double dj = H[j * mp + j];
-      rank += (dj > di) || (dj == di && j < i);
-    }
-    theta[rank] = di;
-    for (int k = 0; k < m; ++k) Sout[(int64_t)k * m + rank] = V[k * mp + i];
-  }
+  block_jacobi(Hg, ldh, m, theta, Sout, sm, info);
   __syncthreads();
   // residual estimates est[j] = || Rn (rn_rows x cur) * S[m-cur:m, j] ||
   if (Rn && est) {
-    for (int j = t; j < nreq; j += blockDim.x) {
+    for (int j = threadIdx.x; j < nreq; j += blockDim.x) {
       double s2 = 0.0;
       for (int a = 0; a < rn_rows; ++a) {
         double v = 0.0;
@@ -872,11 +749,6 @@ __global__ void __launch_bounds__(kJacobiThreads, 1)
       }
       est[j] = sqrt(s2);
     }
-  }
-  if (t == 0 && info) {
-    info[0] = sweep + 1;
-    info[1] = sqrt(off2);
-    info[2] = sqrt(fro2);
   }
 }
 
@@ -1369,11 +1241,10 @@ void apply_rinv(const Launch& L, int64_t n, double* W, int64_t ldw, int q, const
 
 void rr_jacobi(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, const double* Rn,
                int rn_rows, int cur, int nreq, double* est, double* info) {
-  const int mp = (m + 1) & ~1;
-  const size_t smem = (size_t)2 * mp * mp * sizeof(double);
+  const size_t smem = (size_t)jacobi_smem_doubles(m) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    MEG_CUDA(cudaFuncSetAttribute(k_rr_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    MEG_CUDA(cudaFuncSetAttribute(k_rr_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 215 * 1024));
     attr = true;
   }
   const int threads = m <= 24 ? 64 : m <= 48 ? 256 : m <= 80 ? 512 : kJacobiThreads;

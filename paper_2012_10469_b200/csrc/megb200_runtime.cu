@@ -57,6 +57,10 @@ struct megb200_solver {
   int* mask = nullptr;
   double *theta = nullptr, *S = nullptr, *est = nullptr, *info = nullptr, *resid = nullptr;
   double* small = nullptr;  // misc device scalars
+  // per-pass result pack, read back with ONE device-to-host copy:
+  // [theta (cap) | resid (64) | step epilogue (136) | Ritz-block Gram (<= 64 x 64)]
+  double* pack = nullptr;
+  int64_t pack_resid = 0, pack_epi = 0, pack_gram = 0;
   double* csr_g = nullptr;  // max_nnz
   double* rowsq = nullptr;  // n
   double* h_buf = nullptr;  // pinned host staging
@@ -70,6 +74,43 @@ struct megb200_solver {
   int ev_next = 0;
   double prof_bytes = 0.0;
   int64_t prof_passes = 0;
+  // phase tracer: (tag, event) marks; segment time is attributed to the tag of its end mark
+  bool trace = false;
+  std::vector<std::pair<const char*, cudaEvent_t>> marks;
+  std::vector<cudaEvent_t> trace_pool;
+  size_t trace_next = 0;
+  std::vector<std::pair<std::string, std::pair<double, int64_t>>> trace_acc;
+  void mark(const char* tag) {
+    if (!trace) return;
+    if (trace_next == trace_pool.size()) {
+      cudaEvent_t e;
+      MEG_CUDA(cudaEventCreate(&e));
+      trace_pool.push_back(e);
+    }
+    cudaEvent_t e = trace_pool[trace_next++];
+    MEG_CUDA(cudaEventRecord(e, stream));
+    marks.emplace_back(tag, e);
+  }
+  void trace_collect() {
+    if (marks.size() >= 2) {
+      MEG_CUDA(cudaEventSynchronize(marks.back().second));
+      for (size_t i = 1; i < marks.size(); ++i) {
+        float ms = 0.f;
+        MEG_CUDA(cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second));
+        const std::string tag = marks[i].first;
+        bool found = false;
+        for (auto& kv : trace_acc)
+          if (kv.first == tag) {
+            kv.second.first += ms;
+            kv.second.second += 1;
+            found = true;
+          }
+        if (!found) trace_acc.push_back({tag, {ms, 1}});
+      }
+    }
+    marks.clear();
+    trace_next = 0;
+  }
   cudaEvent_t next_event() {
     if (ev_next == (int)ev_pool.size()) {
       cudaEvent_t e;
@@ -113,7 +154,8 @@ struct OpDev {
   double alpha = 0.0;
 };
 
-void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k, double* W, int64_t ldw) {
+void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k, double* W, int64_t ldw,
+              int hp = 0, double* Hout = nullptr) {
   Launch L = s->launch();
   const int64_t n = s->n;
   int S = 0;
@@ -130,7 +172,7 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
     S = 1;
   }
   coop_finish(L, n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
-              s->sm_count);
+              s->sm_count, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap);
   if (ev0 >= 0) {
     const int ev1 = s->ev_next;
     MEG_CUDA(cudaEventRecord(s->next_event(), s->stream));
@@ -193,11 +235,11 @@ void orthonormalize(megb200_solver* s, double* W, int64_t ldw, int q, int cols, 
   const int64_t n = s->n;
   for (int round = 0; round < cgs_rounds && cols > 0; ++round)
     coop_cgs(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, s->red, s->sm_count);
-  coop_cholqr(L, n, W, ldw, q, 1e-13 * scale, s->G, s->R1, s->Rinv, s->mask, nullptr, nullptr, key, refill_ctr,
-              s->red, s->sm_count);
+  coop_cholqr(L, n, W, ldw, W, ldw, q, 1e-13 * scale, s->G, s->R1, s->Rinv, s->mask, nullptr, nullptr, key,
+              refill_ctr, s->red, s->sm_count);
   refill_ctr += (uint64_t)n * q;
   if (cols > 0) coop_cgs(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, s->red, s->sm_count);
-  coop_cholqr(L, n, W, ldw, q, 0.0, s->G, s->R2, s->Rinv, s->mask, want_relation ? s->R1 : nullptr,
+  coop_cholqr(L, n, W, ldw, W, ldw, q, 0.0, s->G, s->R2, s->Rinv, s->mask, want_relation ? s->R1 : nullptr,
               want_relation ? s->Rn : nullptr, key, refill_ctr, s->red, s->sm_count);
   refill_ctr += (uint64_t)n * q;
 }
@@ -221,6 +263,7 @@ struct EigParams {
   uint64_t seed = 0;
   const double* warm = nullptr;
   int64_t warm_cols = 0, ld_warm = 0;
+  bool warm_orthonormal = false;
 };
 
 EigParams params_from_opts(const megb200_eig_opts* o) {
@@ -236,12 +279,22 @@ EigParams params_from_opts(const megb200_eig_opts* o) {
   p.warm = o->warm;
   p.warm_cols = o->warm ? o->warm_cols : 0;
   p.ld_warm = o->ld_warm;
+  p.warm_orthonormal = o->warm && o->warm_orthonormal != 0;
   return p;
 }
 
+// Speculative per-pass MEG epilogue: computed with the Rayleigh-Ritz launch and
+// read back with the convergence data, so a converged step costs one sync.
+struct EpiSpec {
+  int r = 0;             // > 0: run the step epilogue for r kept pairs (nreq = r + 1)
+  double eps_next = 0.0;
+  int gr = 0;                // out: order of the returned Ritz-block Gram
+  std::vector<double> host;  // out: epilogue block (2r + 8 doubles) + Gram (gr x gr)
+};
+
 // Outputs: eigenvectors (nreq) -> vec_out, top `bw` Ritz vectors -> ritz_out.
 EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P, double* vec_out, int64_t ld_vec,
-                double* ritz_out, int64_t ld_ritz, int* ritz_cols_out) {
+                double* ritz_out, int64_t ld_ritz, int* ritz_cols_out, EpiSpec* epi = nullptr) {
   const int64_t n = s->n;
   if (!(1 <= nreq && nreq < n)) throw Error(MEGB200_ERR_PARAM, "need 1 <= r < n, got r=" + std::to_string(nreq) + ", n=" + std::to_string(n));
   Launch L = s->launch();
@@ -269,33 +322,61 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   const uint64_t key_refill = stream_key(P.seed, kStreamRefill);
   uint64_t refill_ctr = 0;
 
+  s->mark("begin");
   // ---- start block: warm columns + seeded random fill
   const int wc = (int)std::min<int64_t>(P.warm_cols, bw);
   if (wc > 0) copy_block(L, n, wc, P.warm, P.ld_warm, s->Q, s->ldq);
   if (bw > wc) fill_gaussian(L, n, bw - wc, key_start, 0, 1.0, false, s->Q + wc, s->ldq);
-  orthonormalize(s, s->Q, s->ldq, bw, 0, 1.0, key_refill, refill_ctr, false);
+  if (wc == bw && P.warm_orthonormal) {
+    // verified-orthonormal warm Ritz block (its Gram came back with the previous step): use as is
+  } else if (wc == bw) {
+    // a warm Ritz block needs one CholQR round
+    coop_cholqr(L, n, s->Q, s->ldq, s->Q, s->ldq, bw, 1e-13, s->G, s->R1, s->Rinv, s->mask, nullptr, nullptr,
+                key_refill, refill_ctr, s->red, s->sm_count);
+    refill_ctr += (uint64_t)n * bw;
+  } else {
+    orthonormalize(s, s->Q, s->ldq, bw, 0, 1.0, key_refill, refill_ctr, false);
+  }
 
+  s->mark("start_block");
   EigRun run;
   std::vector<double> best(nreq, INFINITY);
   int cols = 0, cur = bw;
   double scale = 1.0;
   for (;;) {
     // operator pass on the current block, then its column of H = Q^T A Q
-    apply_op_wide(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq);
-    run.passes++;
-    coop_tn(L, n, s->Q, s->ldq, cols + cur, s->AQ + cols, s->ldq, cur, s->H + cols, s->cap, nullptr, 1.0, s->red,
-            s->sm_count);
-    const int newcols = cols + cur;
-    // Rayleigh-Ritz on H[0:newcols, 0:newcols]; explicit Ritz residuals from the
-    // cached images (linalg.py:205-211) in one cooperative launch
-    rr_jacobi(L, s->H, s->cap, newcols, s->theta, s->S, nullptr, 0, 0, nreq, nullptr, s->info);
-    const int rq = std::min(newcols, std::max(nreq, bw));
-    coop_ritz(L, n, s->Q, s->AQ, s->ldq, newcols, s->S, newcols, rq, nreq, s->theta, s->T, s->ldq, s->resid, s->red,
+    if (cur <= 32) {
+      // pass + epilogue; the epilogue launch also reduces the H column Q^T (A Q_j)
+      apply_op(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq, cols + cur, s->H + cols);
+    } else {
+      apply_op_wide(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq);
+      coop_tn(L, n, s->Q, s->ldq, cols + cur, s->AQ + cols, s->ldq, cur, s->H + cols, s->cap, nullptr, 1.0, s->red,
               s->sm_count);
-    double* hb = s->h_buf;
-    s->d2h(hb, s->theta, newcols);
-    s->d2h(hb + newcols, s->resid, nreq);
+    }
+    run.passes++;
+    s->mark("pass+finish");
+    const int newcols = cols + cur;
+    // Rayleigh-Ritz on H[0:newcols, 0:newcols] + explicit Ritz residuals from the
+    // cached images (linalg.py:205-211) (+ speculative step epilogue) in one launch
+    const int rq = std::min(newcols, std::max(nreq, bw));
+    const int gr = epi ? rq : 0;  // Gram of the whole Ritz block (V_next = its first r columns)
+    coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, n, s->Q, s->AQ, s->ldq, rq, nreq, s->T, s->ldq,
+            s->resid, s->red, s->sm_count, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
+            epi ? s->pack + s->pack_epi : nullptr);
+    // one read-back: theta | resid | epilogue | Gram
+    double* pk = s->h_buf;
+    s->d2h(pk, s->pack, s->pack_gram + (int64_t)gr * gr);
+    const int epi_len = epi ? 2 * epi->r + 8 : 0;
+    double* hb = pk + s->pack_gram + (int64_t)gr * gr;  // scratch: compact copy in the old layout
+    s->mark("rr+ritz");
     s->sync();
+    s->mark("host_decide");
+    std::copy(pk, pk + newcols, hb);
+    std::copy(pk + s->pack_resid, pk + s->pack_resid + nreq, hb + newcols);
+    if (epi) {
+      std::copy(pk + s->pack_epi, pk + s->pack_epi + epi_len, hb + newcols + nreq);
+      std::copy(pk + s->pack_gram, pk + s->pack_gram + (int64_t)gr * gr, hb + newcols + nreq + epi_len);
+    }
     double tmax = 0.0;
     for (int j = 0; j < newcols; ++j) tmax = std::max(tmax, fabs(hb[j]));
     scale = std::max(1.0, tmax);  // norm estimate max(1, max|theta_all|) (linalg.py:214)
@@ -314,6 +395,10 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       run.resid.assign(hb + newcols, hb + newcols + nreq);
       run.norm_est = scale;
       run.converged = true;
+      if (epi) {
+        epi->host.assign(hb + newcols + nreq, hb + newcols + nreq + epi_len + gr * gr);
+        epi->gr = gr;
+      }
       if (vec_out) copy_block(L, n, nreq, s->T, s->ldq, vec_out, ld_vec);
       if (ritz_out) copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
       if (ritz_cols_out) *ritz_cols_out = rq;
@@ -330,6 +415,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       refill_ctr += (uint64_t)n * nxt;
     }
     orthonormalize(s, s->Q + newcols, s->ldq, nxt, newcols, scale, key_refill, refill_ctr, false);
+    s->mark("orth_next");
     cols = newcols;
     if (cols + nxt > mmax) {
       // thick restart: keep the leading `keep` Ritz pairs, continue from the next block
@@ -339,6 +425,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       copy_block(L, n, keep, s->T, s->ldq, s->AQ, s->ldq);
       copy_block(L, n, nxt, s->Q + cols, s->ldq, s->Q + keep, s->ldq);
       set_diag(L, s->H, s->cap, keep, s->theta);  // H = diag(theta_keep); couplings arrive with the next pass
+      s->mark("restart");
       cols = keep;
       run.restarts++;
     }
@@ -617,6 +704,7 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
         {&s->info, 16},
         {&s->resid, s->cap},
         {&s->small, 4096},
+        {&s->pack, s->cap + 64 + 136 + 64 * 64},
         {&s->csr_g, std::max<int64_t>(1, s->max_nnz)},
         {&s->rowsq, n},
     };
@@ -635,7 +723,12 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
       off += align_up(it.count * (int64_t)sizeof(double), 256);
     }
     s->mask = reinterpret_cast<int*>(s->arena + off);
-    s->h_buf_len = 4 * (int64_t)s->cap + 4096;
+    s->pack_resid = s->cap;
+    s->pack_epi = s->cap + 64;
+    s->pack_gram = s->cap + 64 + 136;
+    s->theta = s->pack;  // theta lives at the head of the pack
+    s->resid = s->pack + s->pack_resid;
+    s->h_buf_len = 2 * ((int64_t)s->cap + 64 + 136 + 64 * 64) + 64;
     e = cudaMallocHost(&s->h_buf, s->h_buf_len * sizeof(double));
     if (e != cudaSuccess) {
       cudaFree(s->arena);
@@ -744,20 +837,19 @@ int megb200_lowrank_meg_step(megb200_solver* s, const megb200_iterate* x, const 
       P.ld_warm = x->ldv;
     }
     int rc = 0;
-    EigRun run = top_eigs(s, so.op, nreq, P, nullptr, 0, out->ritz_block, out->ld_ritz, &rc);
+    EpiSpec epi;
+    epi.r = r;
+    epi.eps_next = eps_next;
+    EigRun run = top_eigs(s, so.op, nreq, P, nullptr, 0, out->ritz_block, out->ld_ritz, &rc, &epi);
     out->ritz_cols = out->ritz_block ? rc : 0;
     out->passes = run.passes;
     out->restarts = run.restarts;
     if (out->residual_norms)
       for (int j = 0; j < nreq; ++j) out->residual_norms[j] = run.resid[j];
     if (!run.converged) throw_lanczos(run, P.tol);
-    // next iterate: V = top r Ritz vectors (still in T), lam / certificate by the epilogue kernel
+    // next iterate: V = top r Ritz vectors (in T); lam / certificate came from the fused epilogue
     copy_block(L, s->n, r, s->T, s->ldq, out->V_next, out->ld_next);
-    step_epilogue(L, s->theta, r, s->n, eps_next, s->small);
-    const int olen = 2 * r + 1 + 7;
-    double* hb = s->h_buf;
-    s->d2h(hb, s->small, olen);
-    s->sync();
+    const double* hb = epi.host.data();
     const double status = hb[2 * r + 1 + 6];
     if (status == 4.0) throw Error(MEGB200_ERR_KEPT_MASS, "kept mass vanished despite max-shift");
     if (status == 1.0) throw Error(MEGB200_ERR_PARAM, "certificate inputs invalid (partial trace <= 0 or lambda < 0)");
@@ -772,7 +864,19 @@ int megb200_lowrank_meg_step(megb200_solver* s, const megb200_iterate* x, const 
     out->lhs_cheap = t[3];
     out->holds_cheap = t[4] != 0.0;
     out->threshold = t[5];
-    out->gram_err = gram_error(s, out->V_next, out->ld_next, r);
+    const double* g = hb + 2 * r + 8;
+    const int gr = epi.gr;
+    double ge = 0.0, gall = 0.0;
+    for (int i = 0; i < gr; ++i)
+      for (int j = 0; j < gr; ++j) {
+        const double e = fabs(g[i * gr + j] - (i == j ? 1.0 : 0.0));
+        gall = std::max(gall, e);
+        if (i < r && j < r) ge = std::max(ge, e);
+      }
+    out->gram_err = ge;
+    out->ritz_orth_err = gall;
+    s->mark("epilogue");
+    s->trace_collect();
   });
 }
 
@@ -949,6 +1053,30 @@ int megb200_profile_read(megb200_solver* s, double* pass_ms, int64_t* passes, do
     s->ev_next = 0;
     s->prof_bytes = 0.0;
     s->prof_passes = 0;
+  });
+}
+
+int megb200_trace_enable(megb200_solver* s, int32_t enable) {
+  return guarded_impl([&] {
+    if (!s) throw Error(MEGB200_ERR_PARAM, "solver is NULL");
+    s->trace = enable != 0;
+    s->marks.clear();
+    s->trace_next = 0;
+    s->trace_acc.clear();
+  });
+}
+
+int megb200_trace_report(megb200_solver* s, char* buf, int64_t len) {
+  return guarded_impl([&] {
+    if (!s || !buf || len < 1) throw Error(MEGB200_ERR_PARAM, "null argument");
+    std::string out;
+    char line[160];
+    for (auto& kv : s->trace_acc) {
+      snprintf(line, sizeof line, "%-14s %10.2f us avg  x%lld\n", kv.first.c_str(),
+               1e3 * kv.second.first / std::max<int64_t>(1, kv.second.second), (long long)kv.second.second);
+      out += line;
+    }
+    snprintf(buf, (size_t)len, "%s", out.c_str());
   });
 }
 

@@ -142,7 +142,8 @@ class SymmetricOperator:
         return symmetrize(self.apply(np.eye(self.dim)))
 
 
-def _eig_opts(tol, max_iter, seed, subspace, restarts, block=None, keep=None, warm=None) -> _lib.EigOpts:
+def _eig_opts(tol, max_iter, seed, subspace, restarts, block=None, keep=None, warm=None,
+              warm_orthonormal=False) -> _lib.EigOpts:
     o = _lib.EigOpts()
     o.tol = float(tol)
     o.max_passes = int(max_iter) if max_iter is not None else 0
@@ -155,6 +156,7 @@ def _eig_opts(tol, max_iter, seed, subspace, restarts, block=None, keep=None, wa
         o.warm = warm.data_ptr()
         o.warm_cols = warm.shape[1]
         o.ld_warm = warm.stride(0)
+        o.warm_orthonormal = 1 if warm_orthonormal else 0
     return o
 
 

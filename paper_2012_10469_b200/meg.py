@@ -40,9 +40,10 @@ class LowRankIterate:
     Validation matches meg.py:62-77 (the V^T V check runs on the device).
     """
 
-    __slots__ = ("n", "r", "lam", "eps", "_vd", "_vh", "warm_block")
+    __slots__ = ("n", "r", "lam", "eps", "_vd", "_vh", "warm_block", "warm_orth_err")
 
-    def __init__(self, n: int, r: int, V, lam, eps: float, *, warm_block=None, _gram_err: float | None = None):
+    def __init__(self, n: int, r: int, V, lam, eps: float, *, warm_block=None, warm_orth_err: float = 1.0,
+                 _gram_err: float | None = None):
         n, r = int(n), int(r)
         if not 1 <= r < n:
             raise ParameterError(f"need 1 <= r < n, got r={r}, n={n}")
@@ -60,6 +61,7 @@ class LowRankIterate:
         object.__setattr__(self, "lam", lam)
         object.__setattr__(self, "eps", float(eps))
         object.__setattr__(self, "warm_block", warm_block)
+        object.__setattr__(self, "warm_orth_err", float(warm_orth_err))
         if _gram_err is None:
             s = runtime.solver_for(n)
             err = C.c_double()
@@ -352,7 +354,8 @@ def lowrank_meg_step(
     hold: list = []
     xs, gs = x.struct(hold), g.struct(hold)
     warm = x.warm_block if isinstance(x.warm_block, torch.Tensor) and x.warm_block.shape[0] == n else None
-    opts = _eig_opts(max(svd_tol, g.tol_floor), max_passes, svd_seed, svd_subspace, 12, block, keep, warm)
+    opts = _eig_opts(max(svd_tol, g.tol_floor), max_passes, svd_seed, svd_subspace, 12, block, keep, warm,
+                     warm_orthonormal=warm is not None and x.warm_orth_err <= 1e-13)
     v_next = torch.empty((n, r), dtype=torch.float64, device=dev)
     ritz = torch.empty((n, runtime.MAX_BLOCK), dtype=torch.float64, device=dev)
     lam = np.zeros(r)
@@ -372,7 +375,7 @@ def lowrank_meg_step(
                                         C.byref(opts), C.byref(out))
     runtime.check(rc, residual_norms=res.copy())
     nxt = LowRankIterate(n, r, v_next, lam, eps_next, warm_block=ritz[:, : out.ritz_cols],
-                         _gram_err=out.gram_err)
+                         warm_orth_err=out.ritz_orth_err, _gram_err=out.gram_err)
     cert = CertificateRecord(iteration=None, lhs_cheap=out.lhs_cheap, holds_cheap=bool(out.holds_cheap),
                              threshold=out.threshold)
     return LowRankStepResult(
