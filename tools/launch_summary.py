@@ -15,7 +15,7 @@ for r in rows[hi + 1:]:
     if len(r) <= vi:
         continue
     v = float(r[vi].replace(",", ""))
-    v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+    v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
     m = re.search(r"(k_\w+|vectorized_elementwise_kernel|\w+_kernel)", r[ki])
     name = m.group(1) if m else r[ki][:40]
     t = re.search(r"k_\w+<([^>]*)>", r[ki])
