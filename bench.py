@@ -320,7 +320,7 @@ def run_device_arm(args, world, rank, local):
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-        "kernel": "streamed operator pass (k_dense_apply_f64 + k_apply_finish)",
+        "kernel": "streamed operator pass k_dense_pass_mma (TMA + DMMA), timed alone by events inside the library",
         "bytes_per_pass": (pb_bytes.value / pc.value) if pc.value else None,
         "pass_ms": (pm.value / pc.value) if pc.value else None, "passes": int(pc.value), "peak_source": peak_src,
         "share_of_step": (pm.value / 1e3) / total_s if total_s else None,

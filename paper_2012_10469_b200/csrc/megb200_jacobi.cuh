@@ -172,4 +172,146 @@ __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, 
   }
 }
 
+// Single-warp variant for m <= 32: warp-synchronous rounds (only __syncwarp),
+// the round-robin schedule tabulated once in shared memory, and each lane's
+// 2x2-block and rotation work lists fixed for the whole solve.  Same numerics
+// and outputs as block_jacobi; call with the whole warp (lanes 0..31).
+__host__ __device__ constexpr int warp_jacobi_smem_doubles(int m) {
+  return 2 * jacobi_pad(m) * jacobi_pad(m) + 32 * 16 + 64;
+}
+
+__device__ inline void warp_jacobi(const double* __restrict__ Hg, int64_t ldh, int m, double* __restrict__ theta,
+                                   double* __restrict__ Sout, double* sm, double* __restrict__ info) {
+  const int lane = threadIdx.x & 31;
+  const int mp = jacobi_pad(m);
+  const int half = mp / 2;
+  double* H = sm;
+  double* V = H + mp * mp;
+  short2* sched = reinterpret_cast<short2*>(V + mp * mp);  // (mp-1) x half pairs (<= 31 x 16)
+  double* cs = reinterpret_cast<double*>(sched + 32 * 16);
+  double* sn = cs + 16;
+  int* pp = reinterpret_cast<int*>(sn + 16);
+  int* qq = pp + 16;
+  for (int idx = lane; idx < mp * mp; idx += 32) {
+    const int i = idx / mp, j = idx - i * mp;
+    double h = 0.0;
+    if (i < m && j < m) h = (i <= j) ? Hg[i * ldh + j] : Hg[j * ldh + i];
+    H[idx] = h;
+    V[idx] = (i == j) ? 1.0 : 0.0;
+  }
+  for (int idx = lane; idx < (mp - 1) * half; idx += 32) {
+    const int round = idx / half, k = idx - round * half;
+    int p, q;
+    if (k == 0) {
+      p = 0;
+      q = 1 + round;
+    } else {
+      p = 1 + (round + k) % (mp - 1);
+      q = 1 + (round - k + (mp - 1)) % (mp - 1);
+    }
+    sched[idx] = make_short2((short)min(p, q), (short)max(p, q));
+  }
+  __syncwarp();
+  auto warp_sum = [&](double v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+  };
+  double fl = 0.0, ol = 0.0;
+  for (int idx = lane; idx < mp * mp; idx += 32) {
+    const double h = H[idx];
+    fl += h * h;
+    if (idx / mp != idx % mp) ol += h * h;
+  }
+  const double fro2 = warp_sum(fl);
+  const double stop2 = fro2 * 1e-30;
+  double off2 = warp_sum(ol), prev = INFINITY;
+  const int nblk = half * half, nv = mp * half;
+  int sweep = 0;
+  for (sweep = 0; sweep < 40 && !(off2 <= stop2); ++sweep) {
+    for (int round = 0; round < mp - 1; ++round) {
+      if (lane < half) {
+        const short2 pq = sched[round * half + lane];
+        const int p = pq.x, q = pq.y;
+        const double apq = H[p * mp + q];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0) {
+          const float tau = (float)(H[q * mp + q] - H[p * mp + p]) * (0.5f / (float)apq);
+          const float at = fabsf(tau);
+          float tt = at > 1e15f ? 0.5f / at : 1.0f / (at + sqrtf(1.0f + tau * tau));
+          if (tau < 0.f) tt = -tt;
+          const float cf = rsqrtf(1.0f + tt * tt);
+          c = (double)cf;
+          s = (double)tt * (double)cf;
+#pragma unroll
+          for (int it = 0; it < 2; ++it) {
+            const double g = 1.5 - 0.5 * (c * c + s * s);
+            c *= g;
+            s *= g;
+          }
+        }
+        pp[lane] = p;
+        qq[lane] = q;
+        cs[lane] = c;
+        sn[lane] = s;
+      }
+      __syncwarp();
+      for (int b = lane; b < nblk; b += 32) {
+        const int a = b / half, bb = b - a * half;
+        const int pa = pp[a], qa = qq[a], pb = pp[bb], qb = qq[bb];
+        const double ca = cs[a], sa = sn[a], cb = cs[bb], sb = sn[bb];
+        const double h00 = H[pa * mp + pb], h01 = H[pa * mp + qb];
+        const double h10 = H[qa * mp + pb], h11 = H[qa * mp + qb];
+        const double t00 = ca * h00 - sa * h10, t01 = ca * h01 - sa * h11;
+        const double t10 = sa * h00 + ca * h10, t11 = sa * h01 + ca * h11;
+        double n00 = t00 * cb - t01 * sb, n01 = t00 * sb + t01 * cb;
+        double n10 = t10 * cb - t11 * sb, n11 = t10 * sb + t11 * cb;
+        if (a == bb) {
+          const double avg = 0.5 * (n01 + n10);
+          n01 = avg;
+          n10 = avg;
+        }
+        H[pa * mp + pb] = n00;
+        H[pa * mp + qb] = n01;
+        H[qa * mp + pb] = n10;
+        H[qa * mp + qb] = n11;
+      }
+      for (int v = lane; v < nv; v += 32) {
+        const int i = v / half, a = v - i * half;
+        const int pa = pp[a], qa = qq[a];
+        const double ca = cs[a], sa = sn[a];
+        const double vp = V[i * mp + pa], vq = V[i * mp + qa];
+        V[i * mp + pa] = ca * vp - sa * vq;
+        V[i * mp + qa] = sa * vp + ca * vq;
+      }
+      __syncwarp();
+    }
+    double lo = 0.0;
+    for (int idx = lane; idx < mp * mp; idx += 32)
+      if (idx / mp != idx % mp) lo += H[idx] * H[idx];
+    off2 = warp_sum(lo);
+    const bool stag = (off2 > 0.25 * prev && off2 <= fro2 * 1e-26);
+    prev = off2;
+    if (stag) {
+      ++sweep;
+      break;
+    }
+  }
+  for (int i = lane; i < m; i += 32) {
+    const double di = H[i * mp + i];
+    int rank = 0;
+    for (int j = 0; j < m; ++j) {
+      const double dj = H[j * mp + j];
+      rank += (dj > di) || (dj == di && j < i);
+    }
+    theta[rank] = di;
+    for (int k = 0; k < m; ++k) Sout[(int64_t)k * m + rank] = V[k * mp + i];
+  }
+  if (lane == 0 && info) {
+    info[0] = sweep;
+    info[1] = sqrt(off2);
+    info[2] = sqrt(fro2);
+  }
+}
+
 }  // namespace megb200

@@ -470,6 +470,143 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
 }
 
 // ===========================================================================
+// K1 (float64, tensor path): same TMA/mbarrier producer as k_dense_pass, but
+// the consumers run the FP64 tensor-core MMA (mma.sync.m8n8k4.f64, SASS
+// DMMA.8x8x4): 256 FMAs per instruction instead of 32, so the FP64 pipe is fed
+// without the issue/latency stalls of the DFMA loop.  Item = 128 output rows
+// x one k-slice; consumer warp w owns rows [16w, 16w+16) (two 8-row m-tiles)
+// x NT 8-column n-tiles over the whole k-slice, so no cross-warp reduction.
+// U is staged as KC x (8 NT) with the columns beyond b zero-filled by TMA.
+constexpr int kMmaRows = 128;
+
+template <int NT>
+constexpr size_t mma_smem_bytes() {
+  return 1024 + (size_t)kPipeStages * kPipeKC * kMmaRows * 8 + (size_t)kPipeStages * kPipeKC * 8 * NT * 8 +
+         2 * kPipeStages * 8;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kPipeThreads, 1)
+    k_dense_pass_mma(const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmU, int64_t n,
+                     int b, double* __restrict__ part, int tiles, int64_t kslice, int items) {
+  // Operand stage = 8 TMA boxes of 16 (i) x 32 (k) doubles with the 128-byte
+  // swizzle (16-byte chunk index XOR row & 7), 4 KiB each; consumer warp w
+  // reads box w.  Each 8-row k group feeds two MMAs with k permuted as
+  // {0,1,4,5} / {2,3,6,7}: with the swizzle (operand) and the 192-byte U row
+  // stride, both fragment loads hit the 2-wavefront minimum (no bank conflicts).
+  constexpr int BNP = 8 * NT;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* base = smem + ((1024 - ((uintptr_t)smem & 1023)) & 1023);
+  double* Ms = reinterpret_cast<double*>(base);                      // stages x 8 boxes x 512 doubles
+  double* Us = Ms + (size_t)kPipeStages * kPipeKC * kMmaRows;         // stages x KC x BNP
+  uint64_t* full = reinterpret_cast<uint64_t*>(Us + (size_t)kPipeStages * kPipeKC * BNP);
+  uint64_t* empty = full + kPipeStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kPipeStages; ++st) {
+      pipe::bar_init(full + st, 1);
+      pipe::bar_init(empty + st, kPipeConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmM) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
+  }
+  __syncthreads();
+  if (warp == kPipeConsumers) {
+    if (lane == 0) {
+      const uint32_t stage_bytes = (uint32_t)(kPipeKC * kMmaRows * 8 + kPipeKC * BNP * 8);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int slice = item / tiles, tile = item - slice * tiles;
+        const int64_t kbeg = (int64_t)slice * kslice, kend = min(n, kbeg + kslice);
+        for (int64_t kc = kbeg; kc < kend; kc += kPipeKC) {
+          pipe::bar_wait(empty + st, ph ^ 1u);
+          pipe::bar_arrive_tx(full + st, stage_bytes);
+          double* mst = Ms + (size_t)st * kPipeKC * kMmaRows;
+#pragma unroll
+          for (int bx = 0; bx < kMmaRows / 16; ++bx)
+            pipe::tma_2d(mst + bx * 16 * kPipeKC, &tmM, tile * kMmaRows + 16 * bx, (int)kc, full + st);
+          pipe::tma_2d(Us + (size_t)st * kPipeKC * BNP, &tmU, 0, (int)kc, full + st);
+          if (++st == kPipeStages) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
+  const int kperm = (tq & 1) + 4 * (tq >> 1);  // {0,1,4,5}; +2 for the second MMA of a k group
+  int st = 0;
+  uint32_t ph = 0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int slice = item / tiles, tile = item - slice * tiles;
+    const int64_t i0 = (int64_t)tile * kMmaRows;
+    const int64_t kbeg = (int64_t)slice * kslice, kend = min(n, kbeg + kslice);
+    double acc[2][NT][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    for (int64_t kc = kbeg; kc < kend; kc += kPipeKC) {
+      const int nk = (int)min((int64_t)kPipeKC, kend - kc);  // rows past kend belong to the next slice
+      pipe::bar_wait(full + st, ph);
+      const char* box = reinterpret_cast<const char*>(Ms + (size_t)st * kPipeKC * kMmaRows) + warp * 4096;
+      const double* us = Us + (size_t)st * kPipeKC * BNP;
+      auto mma_k = [&](int k) {  // one m8n8k4 step over k rows {k + kperm}
+        const int kk = k + kperm;
+        const bool valid = kk < nk;
+        const int sw = kk & 7;
+        const double a0 = valid ? *reinterpret_cast<const double*>(box + kk * 128 + (((g >> 1) ^ sw) << 4) +
+                                                                    ((g & 1) << 3))
+                                : 0.0;
+        const double a1 = valid ? *reinterpret_cast<const double*>(box + kk * 128 + ((((8 + g) >> 1) ^ sw) << 4) +
+                                                                    ((g & 1) << 3))
+                                : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double bv = valid ? us[kk * BNP + nt * 8 + g] : 0.0;
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[0][nt][0]), "+d"(acc[0][nt][1]) : "d"(a0), "d"(bv));
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[1][nt][0]), "+d"(acc[1][nt][1]) : "d"(a1), "d"(bv));
+        }
+      };
+#pragma unroll
+      for (int k8 = 0; k8 < kPipeKC; k8 += 8) {
+        if (k8 < nk) {
+          mma_k(k8);
+          mma_k(k8 + 2);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) pipe::bar_arrive(empty + st);
+      if (++st == kPipeStages) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+    // C fragment: row g, columns 2*tq, 2*tq+1 of each 8x8 tile
+    double* out = part + (int64_t)slice * n * b;
+    const int rbase = warp * 16;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int64_t row = i0 + rbase + mt * 8 + g;
+      if (row < n) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = nt * 8 + 2 * tq;
+          if (c < b) out[row * b + c] = acc[mt][nt][0];
+          if (c + 1 < b) out[row * b + c + 1] = acc[mt][nt][1];
+        }
+      }
+    }
+  }
+}
+
+// ===========================================================================
 // K2: CSR product (sampled-entry gradient), one warp per row, lanes over the
 // row's nonzeros gathering U rows; fixed xor-tree warp reduction.
 template <int BN>
@@ -1012,14 +1149,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2D row-major tensor map: inner dimension `cols` (contiguous), outer `rows`, leading dimension `ld`
 CUtensorMap make_map(const void* base, CUtensorMapDataType dt, size_t es, int64_t cols, int64_t rows, int64_t ld,
-                     uint32_t box_cols, uint32_t box_rows) {
+                     uint32_t box_cols, uint32_t box_rows,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   CUtensorMap map;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(MEGB200_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return map;
@@ -1059,6 +1197,23 @@ void dispatch_pipe(const Launch& L, const T* M, int64_t ldm, int64_t n, const do
   }
 }
 
+template <int NT>
+void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                     double* part, int tiles, int64_t kslice, int items, int grid) {
+  constexpr size_t smem = mma_smem_bytes<NT>();
+  static bool attr = false;
+  if (!attr) {
+    MEG_CUDA(cudaFuncSetAttribute(k_dense_pass_mma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const CUtensorMap tmM =
+      make_map(M, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, n, n, ldm, 16, kPipeKC, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap tmU = make_map(U, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, b, n, ldu, (uint32_t)(8 * NT), kPipeKC);
+  k_dense_pass_mma<NT><<<grid, kPipeThreads, smem, L.stream>>>(tmM, tmU, n, b, part, tiles, kslice, items);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
 // Choose the number of k-slices S so that tiles * S fills whole waves of one
 // CTA per SM (static round-robin of the persistent grid), preferring small S.
 int choose_slices(int tiles, int64_t n, int sm_count, int s_min, int s_max) {
@@ -1083,6 +1238,23 @@ int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, 
     const size_t es = dtype == MEGB200_F64 ? 8 : 4;
     const bool aligned = b % 2 == 0 && b <= 32 && ldu % 2 == 0 && ((uintptr_t)U % 16 == 0) &&
                          (ldm * es) % 16 == 0 && ((uintptr_t)M % 16 == 0) && (n * es) % 16 == 0;
+    if (aligned && dtype == MEGB200_F64 && getenv("MEGB200_NO_DMMA") == nullptr) {
+      const int tiles = cdiv(n, kMmaRows);
+      const int s_max = std::max(1, (int)std::min<int64_t>(part_cap_slices, 16));
+      int S = choose_slices(tiles, n, sm_count, 1, s_max);
+      int64_t kslice = (int64_t)cdiv(cdiv(n, S), kPipeKC) * kPipeKC;
+      S = cdiv(n, kslice);
+      const int items = tiles * S;
+      const int grid = std::min(items, sm_count);
+      const double* m = static_cast<const double*>(M);
+      switch ((b + 7) / 8) {
+        case 1: launch_pipe_mma<1>(L, m, ldm, n, U, ldu, b, part, tiles, kslice, items, grid); break;
+        case 2: launch_pipe_mma<2>(L, m, ldm, n, U, ldu, b, part, tiles, kslice, items, grid); break;
+        case 3: launch_pipe_mma<3>(L, m, ldm, n, U, ldu, b, part, tiles, kslice, items, grid); break;
+        default: launch_pipe_mma<4>(L, m, ldm, n, U, ldu, b, part, tiles, kslice, items, grid); break;
+      }
+      return S;
+    }
     if (aligned) {
       const int BM = dtype == MEGB200_F64 ? 64 : 128;
       const int tiles = cdiv(n, BM);

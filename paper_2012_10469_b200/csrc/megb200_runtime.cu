@@ -160,6 +160,7 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
   const int64_t n = s->n;
   int S = 0;
   const bool streamed = (op.kind == MEGB200_OP_DENSE || op.kind == MEGB200_OP_CSR) && op.scale != 0.0;
+  // live profiling brackets the streamed operand kernel only (the roofline's dominant kernel)
   int ev0 = -1;
   if (s->prof && streamed) {
     ev0 = s->ev_next;
@@ -171,8 +172,6 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
     csr_apply_partial(L, op.rowptr, op.col, op.val, n, U, ldu, k, s->part);
     S = 1;
   }
-  coop_finish(L, n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
-              s->sm_count, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap);
   if (ev0 >= 0) {
     const int ev1 = s->ev_next;
     MEG_CUDA(cudaEventRecord(s->next_event(), s->stream));
@@ -184,6 +183,8 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
     s->prof_bytes += b;
     s->prof_passes++;
   }
+  coop_finish(L, n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
+              s->sm_count, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap);
 }
 
 // columns k > 64 are applied in chunks (re-streams the operand; not used by the configs)
@@ -312,9 +313,12 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
     exhaust = true;
   }
   mmax = (int)std::min<int64_t>(mmax, n);
+  // even block widths and column offsets keep every block 16-byte aligned for the TMA pass
+  if (!exhaust && (bw & 1) && bw < s->max_block && bw + 1 + nreq <= mmax) bw += 1;
   if (bw > mmax) bw = mmax;
   int keep = P.keep > 0 ? P.keep : std::max(nreq, mmax / 2);
   keep = std::min(keep, mmax - bw);
+  if (!exhaust && (keep & 1) && (bw & 1) == 0) keep = (keep + 1 <= mmax - bw) ? keep + 1 : (keep - 1 >= nreq ? keep - 1 : keep);
   if (!exhaust && keep < nreq) throw Error(MEGB200_ERR_PARAM, "basis too small for the requested eigenpairs");
   const int max_passes = P.max_passes > 0 ? P.max_passes : P.restarts * mmax;
   const double tol = P.tol;
