@@ -206,6 +206,47 @@ int megb200_top_r(megb200_solver* s, const megb200_operator* op, int32_t r, cons
 int megb200_lowrank_meg_step(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta,
                              double eps_next, const megb200_eig_opts* opts, megb200_step_result* out);
 
+/* Run loop: T low-rank MEG steps from x0 without returning between steps --
+ * the driver of test_meg.py:150-156 / the harness loop of SPEC.md:433-450,
+ * absent from the reference code.  Step t = t0 + i uses eta_t, eps_next =
+ * eps_{t+1} and svd_seed = t; the gradient is evaluated at the current iterate
+ * (g's gV / g_lam / g_eps are ignored; STOCHASTIC regenerates A_t per step
+ * into g->A).  flush_bytes > 0 writes that much scratch between steps,
+ * outside the per-step events, to evict the operand from L2. */
+enum {
+  MEGB200_EPS_EXPERIMENT = 0,        /* 0.6/(t+c+1)^2                 meg.py:182-190 */
+  MEGB200_EPS_CUBIC_DET = 1,         /* eps0/(2 max(G^2,1))/(t+1+c)^3 */
+  MEGB200_EPS_CUBIC_DET_GENERAL = 2, /* 3 eps0/(2 max(G^2,1))/(t+c+1)^3 */
+  MEGB200_EPS_QUADRATIC_STOCH = 3,   /* (9/32) eps0/(t+c+1)^2        */
+  MEGB200_EPS_CONSTANT = 4           /* eps0_tilde                    */
+};
+enum { MEGB200_ETA_CONSTANT = 0, MEGB200_ETA_INV_SQRT = 1 /* eta0 / sqrt(t + 1) */ };
+
+typedef struct megb200_schedule {
+  int32_t eps_kind;
+  double eps0_tilde, G, c;
+  int32_t eta_kind;
+  double eta0;
+  uint64_t minibatch_seed;     /* STOCHASTIC: A_t = N(0,1/n) at stream 5, counter (t n + i) b + j */
+  int32_t minibatch_round_f32; /* round A_t through float32 (f32 configs)                         */
+} megb200_schedule;
+
+typedef struct megb200_run_record { /* host arrays, any may be NULL; row i = step t0 + i */
+  double* shift;   /* T           */
+  double* y;       /* T x (r + 1) */
+  double* lam;     /* T x r       */
+  double* eps;     /* T           */
+  double* lhs;     /* T           */
+  int32_t* holds;  /* T           */
+  int32_t* passes; /* T           */
+  double* step_ms; /* T: device time per step: previous step end -> this step end, minus the flush */
+} megb200_run_record;
+
+int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_gradient* g,
+                    const megb200_schedule* sch, int64_t t0, int64_t T, const megb200_eig_opts* opts,
+                    uint64_t flush_bytes, double* V_out, int64_t ld_out, double* lam_out, double* eps_out,
+                    megb200_run_record* rec);
+
 /* certificate_cheap arithmetic (meg.py:222-239), host-only. */
 int megb200_certificate_cheap(double lambda_r_plus_1, double b_r_plus_1, double eps, int64_t n, int64_t r,
                               double* lhs, int32_t* holds, double* threshold);

@@ -80,6 +80,24 @@ class StepResult(C.Structure):
     ]
 
 
+class Schedule(C.Structure):
+    _fields_ = [
+        ("eps_kind", C.c_int32), ("eps0_tilde", C.c_double), ("G", C.c_double), ("c", C.c_double),
+        ("eta_kind", C.c_int32), ("eta0", C.c_double),
+        ("minibatch_seed", C.c_uint64), ("minibatch_round_f32", C.c_int32),
+    ]
+
+
+class RunRecord(C.Structure):
+    _fields_ = [
+        ("shift", c_double_p), ("y", c_double_p), ("lam", c_double_p), ("eps", c_double_p), ("lhs", c_double_p),
+        ("holds", c_int32_p), ("passes", c_int32_p), ("step_ms", c_double_p),
+    ]
+
+
+EPS_KINDS = {"experiment": 0, "cubic_det": 1, "cubic_det_general": 2, "quadratic_stoch": 3, "constant": 4}
+
+
 # (name, restype, argtypes) for every symbol include/megb200.h declares
 SIGNATURES = [
     ("megb200_abi_version", C.c_int, []),
@@ -98,6 +116,9 @@ SIGNATURES = [
     ("megb200_lowrank_meg_step", C.c_int,
      [C.c_void_p, C.POINTER(Iterate), C.POINTER(Gradient), C.c_double, C.c_double, C.POINTER(EigOpts),
       C.POINTER(StepResult)]),
+    ("megb200_meg_run", C.c_int,
+     [C.c_void_p, C.POINTER(Iterate), C.POINTER(Gradient), C.POINTER(Schedule), C.c_int64, C.c_int64,
+      C.POINTER(EigOpts), C.c_uint64, C.c_void_p, C.c_int64, c_double_p, c_double_p, C.POINTER(RunRecord)]),
     ("megb200_certificate_cheap", C.c_int,
      [C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, c_double_p, c_int32_p, c_double_p]),
     ("megb200_objective_value", C.c_int, [C.c_void_p, C.POINTER(Gradient), C.c_double, C.c_double, c_double_p]),

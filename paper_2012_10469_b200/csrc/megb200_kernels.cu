@@ -1148,9 +1148,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2D row-major tensor map: inner dimension `cols` (contiguous), outer `rows`, leading dimension `ld`
-CUtensorMap make_map(const void* base, CUtensorMapDataType dt, size_t es, int64_t cols, int64_t rows, int64_t ld,
-                     uint32_t box_cols, uint32_t box_rows,
-                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
+CUtensorMap encode_map(const void* base, CUtensorMapDataType dt, size_t es, int64_t cols, int64_t rows, int64_t ld,
+                       uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz) {
   CUtensorMap map;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
@@ -1161,6 +1160,39 @@ CUtensorMap make_map(const void* base, CUtensorMapDataType dt, size_t es, int64_
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(MEGB200_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return map;
+}
+
+// small direct-mapped cache of encoded tensor maps (the descriptors are pure
+// functions of their arguments; re-encoding costs ~1 us of host time per launch)
+CUtensorMap make_map(const void* base, CUtensorMapDataType dt, size_t es, int64_t cols, int64_t rows, int64_t ld,
+                     uint32_t box_cols, uint32_t box_rows,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
+  struct Key {
+    const void* base;
+    int dt;
+    int64_t cols, rows, ld;
+    uint32_t bc, br;
+    int swz;
+    bool operator==(const Key& o) const {
+      return base == o.base && dt == o.dt && cols == o.cols && rows == o.rows && ld == o.ld && bc == o.bc &&
+             br == o.br && swz == o.swz;
+    }
+  };
+  struct Entry {
+    Key key;
+    CUtensorMap map;
+    bool used;
+  };
+  static thread_local Entry cache[64] = {};
+  const Key k{base, (int)dt, cols, rows, ld, box_cols, box_rows, (int)swz};
+  const size_t h = (((uintptr_t)base >> 4) ^ (size_t)cols * 31 ^ (size_t)box_cols * 7 ^ (size_t)swz) & 63;
+  Entry& e = cache[h];
+  if (!(e.used && e.key == k)) {
+    e.map = encode_map(base, dt, es, cols, rows, ld, box_cols, box_rows, swz);
+    e.key = k;
+    e.used = true;
+  }
+  return e.map;
 }
 
 template <typename T, int BN>

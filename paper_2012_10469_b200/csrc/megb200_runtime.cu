@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <functional>
 #include <string>
 #include <vector>
@@ -67,6 +68,10 @@ struct megb200_solver {
   int64_t h_buf_len = 0;
   double m_norm2_cache = NAN, m_trace_cache = NAN;
   const void* m_cache_ptr = nullptr;
+  // run-loop buffers (allocated on first megb200_meg_run)
+  double* run_buf = nullptr;  // 2 x n x 64 (V ping-pong) + 2 x n x 64 (warm ping-pong)
+  void* flush_buf = nullptr;
+  uint64_t flush_len = 0;
   // live pass profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -120,15 +125,31 @@ struct megb200_solver {
     return ev_pool[ev_next++];
   }
 
+  // pinned upload ring for the small per-step host->device copies (coefficients):
+  // truly asynchronous, reset at every stream synchronisation
+  double* h_up = nullptr;
+  int64_t h_up_len = 0, h_up_cur = 0;
+
   Launch launch() { return Launch{stream, &launches}; }
-  void sync() { MEG_CUDA(cudaStreamSynchronize(stream)); }
+  void sync() {
+    MEG_CUDA(cudaStreamSynchronize(stream));
+    h_up_cur = 0;
+  }
   void d2h(double* host, const double* dev, int64_t count) {
     if (count <= 0) return;
     MEG_CUDA(cudaMemcpyAsync(host, dev, count * sizeof(double), cudaMemcpyDeviceToHost, stream));
   }
   void h2d(double* dev, const double* host, int64_t count) {
     if (count <= 0) return;
-    MEG_CUDA(cudaMemcpyAsync(dev, host, count * sizeof(double), cudaMemcpyHostToDevice, stream));
+    if (count > h_up_len) {
+      MEG_CUDA(cudaMemcpyAsync(dev, host, count * sizeof(double), cudaMemcpyHostToDevice, stream));
+      return;
+    }
+    if (h_up_cur + count > h_up_len) sync();
+    double* stage = h_up + h_up_cur;
+    std::copy(host, host + count, stage);
+    h_up_cur += count;
+    MEG_CUDA(cudaMemcpyAsync(dev, stage, count * sizeof(double), cudaMemcpyHostToDevice, stream));
   }
 };
 
@@ -733,6 +754,13 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
     s->theta = s->pack;  // theta lives at the head of the pack
     s->resid = s->pack + s->pack_resid;
     s->h_buf_len = 2 * ((int64_t)s->cap + 64 + 136 + 64 * 64) + 64;
+    s->h_up_len = 8192;
+    e = cudaMallocHost(&s->h_up, s->h_up_len * sizeof(double));
+    if (e != cudaSuccess) {
+      cudaFree(s->arena);
+      delete s;
+      throw Error(MEGB200_ERR_CUDA, "pinned upload ring allocation failed");
+    }
     e = cudaMallocHost(&s->h_buf, s->h_buf_len * sizeof(double));
     if (e != cudaSuccess) {
       cudaFree(s->arena);
@@ -748,7 +776,10 @@ void megb200_solver_destroy(megb200_solver* s) {
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   cudaFree(s->arena);
+  if (s->run_buf) cudaFree(s->run_buf);
+  if (s->flush_buf) cudaFree(s->flush_buf);
   cudaFreeHost(s->h_buf);
+  cudaFreeHost(s->h_up);
   delete s;
 }
 
@@ -808,6 +839,153 @@ int megb200_top_r(megb200_solver* s, const megb200_operator* op, int32_t r, cons
   });
 }
 
+namespace {
+void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta, double eps_next,
+               const megb200_eig_opts* opts, megb200_step_result* out);
+
+double eps_eval(const megb200_schedule& sc, int64_t t) {
+  const double g2 = std::max(sc.G * sc.G, 1.0);
+  double raw;
+  switch (sc.eps_kind) {
+    case MEGB200_EPS_EXPERIMENT: raw = 0.6 / std::pow((double)t + sc.c + 1.0, 2); break;
+    case MEGB200_EPS_CUBIC_DET: raw = sc.eps0_tilde / (2.0 * g2) / std::pow((double)t + 1.0 + sc.c, 3); break;
+    case MEGB200_EPS_CUBIC_DET_GENERAL:
+      raw = 3.0 * sc.eps0_tilde / (2.0 * g2) / std::pow((double)t + sc.c + 1.0, 3);
+      break;
+    case MEGB200_EPS_QUADRATIC_STOCH: raw = (9.0 / 32.0) * sc.eps0_tilde / std::pow((double)t + sc.c + 1.0, 2); break;
+    case MEGB200_EPS_CONSTANT: raw = sc.eps0_tilde; break;
+    default: throw Error(MEGB200_ERR_PARAM, "unknown epsilon schedule");
+  }
+  return std::min(raw, 0.75);
+}
+double eta_eval(const megb200_schedule& sc, int64_t t) {
+  if (sc.eta_kind == MEGB200_ETA_INV_SQRT) return sc.eta0 / std::sqrt((double)t + 1.0);
+  if (sc.eta_kind == MEGB200_ETA_CONSTANT) return sc.eta0;
+  throw Error(MEGB200_ERR_PARAM, "unknown step rule");
+}
+}  // namespace
+
+int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_gradient* g,
+                    const megb200_schedule* sch, int64_t t0, int64_t T, const megb200_eig_opts* opts,
+                    uint64_t flush_bytes, double* V_out, int64_t ld_out, double* lam_out, double* eps_out,
+                    megb200_run_record* rec) {
+  return guarded_impl([&] {
+    if (!s || !sch || !g) throw Error(MEGB200_ERR_PARAM, "null argument");
+    if (T < 0) throw Error(MEGB200_ERR_PARAM, "T must be >= 0");
+    check_iterate(s, x0);
+    const int64_t n = s->n;
+    const int r = (int)x0->r;
+    if (r + 1 > 64 || r + 1 >= n) throw Error(MEGB200_ERR_PARAM, "run loop supports r + 1 <= 64, r + 1 < n");
+    Launch L = s->launch();
+    if (!s->run_buf) MEG_CUDA(cudaMalloc(&s->run_buf, (size_t)4 * n * 64 * sizeof(double)));
+    if (flush_bytes > s->flush_len) {
+      if (s->flush_buf) MEG_CUDA(cudaFree(s->flush_buf));
+      MEG_CUDA(cudaMalloc(&s->flush_buf, flush_bytes));
+      s->flush_len = flush_bytes;
+    }
+    double* Vb[2] = {s->run_buf, s->run_buf + n * 64};
+    double* Wb[2] = {s->run_buf + 2 * n * 64, s->run_buf + 3 * n * 64};
+    copy_block(L, n, r, x0->V, x0->ldv, Vb[0], r);
+    std::vector<double> lam(x0->lam, x0->lam + r);
+    double eps = x0->eps;
+    megb200_eig_opts o{};
+    if (opts) o = *opts;
+    const double* warm = o.warm;
+    int64_t warm_cols = o.warm ? o.warm_cols : 0, ld_warm = o.ld_warm;
+    bool warm_orth = o.warm && o.warm_orthonormal;
+    int cur = 0, wcur = 0;
+    std::vector<double> lam_next(r), y(r + 1), mu(r + 1), res(r + 1);
+    // per-step device time: from the end of the previous step (or this step's
+    // start) to this step's end, minus the flush; host turnaround gaps count
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    std::vector<cudaEvent_t> evf;
+    if (rec && rec->step_ms) {
+      ev.resize((size_t)T);
+      evf.resize((size_t)T);
+      for (int64_t i = 0; i < T; ++i) {
+        MEG_CUDA(cudaEventCreate(&ev[i].first));
+        MEG_CUDA(cudaEventCreate(&ev[i].second));
+        MEG_CUDA(cudaEventCreate(&evf[i]));
+      }
+    }
+    for (int64_t i = 0; i < T; ++i) {
+      const int64_t t = t0 + i;
+      const double eta = eta_eval(*sch, t), eps_next = eps_eval(*sch, t + 1);
+      if (!ev.empty()) MEG_CUDA(cudaEventRecord(evf[i], s->stream));
+      if (flush_bytes) MEG_CUDA(cudaMemsetAsync(s->flush_buf, (int)(i & 0xff), flush_bytes, s->stream));
+      if (!ev.empty()) MEG_CUDA(cudaEventRecord(ev[i].first, s->stream));
+      megb200_gradient gg = *g;
+      if (gg.kind == MEGB200_GRAD_FROBENIUS || gg.kind == MEGB200_GRAD_STOCHASTIC || gg.kind == MEGB200_GRAD_SAMPLED) {
+        gg.gV = Vb[cur];
+        gg.g_r = r;
+        gg.g_ldv = r;
+        gg.g_lam = lam.data();
+        gg.g_eps = eps;
+      }
+      if (gg.kind == MEGB200_GRAD_STOCHASTIC) {
+        if (!gg.A) throw Error(MEGB200_ERR_PARAM, "stochastic run needs a minibatch buffer g->A");
+        fill_gaussian(L, n, (int)gg.bsz, stream_key(sch->minibatch_seed, 5), (uint64_t)t * n * gg.bsz,
+                      1.0 / std::sqrt((double)n), sch->minibatch_round_f32 != 0, const_cast<double*>(gg.A), gg.lda);
+      }
+      megb200_iterate it{n, r, Vb[cur], r, lam.data(), eps};
+      megb200_eig_opts so = o;
+      so.seed = (uint64_t)t;
+      so.warm = warm;
+      so.warm_cols = warm_cols;
+      so.ld_warm = ld_warm;
+      so.warm_orthonormal = warm_orth ? 1 : 0;
+      megb200_step_result out{};
+      out.V_next = Vb[1 - cur];
+      out.ld_next = r;
+      out.lam_next = lam_next.data();
+      out.y = y.data();
+      out.mu = mu.data();
+      out.residual_norms = res.data();
+      out.ritz_block = Wb[1 - wcur];
+      out.ld_ritz = 64;
+      step_core(s, &it, &gg, eta, eps_next, &so, &out);
+      if (!ev.empty()) MEG_CUDA(cudaEventRecord(ev[i].second, s->stream));
+      if (rec) {
+        if (rec->shift) rec->shift[i] = out.shift;
+        if (rec->y) std::copy(y.begin(), y.end(), rec->y + i * (r + 1));
+        if (rec->lam) std::copy(lam_next.begin(), lam_next.end(), rec->lam + i * r);
+        if (rec->eps) rec->eps[i] = eps_next;
+        if (rec->lhs) rec->lhs[i] = out.lhs_cheap;
+        if (rec->holds) rec->holds[i] = out.holds_cheap;
+        if (rec->passes) rec->passes[i] = out.passes;
+      }
+      cur = 1 - cur;
+      wcur = 1 - wcur;
+      lam = lam_next;
+      eps = eps_next;
+      warm = Wb[wcur];
+      warm_cols = out.ritz_cols;
+      ld_warm = 64;
+      warm_orth = out.ritz_orth_err <= 1e-13;
+    }
+    if (V_out) copy_block(L, n, r, Vb[cur], r, V_out, ld_out);
+    if (lam_out) std::copy(lam.begin(), lam.end(), lam_out);
+    if (eps_out) *eps_out = eps;
+    s->sync();
+    for (int64_t i = 0; i < (int64_t)ev.size(); ++i) {
+      float ms = 0.f, fl = 0.f;
+      if (i == 0) {
+        MEG_CUDA(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second));
+      } else {
+        MEG_CUDA(cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second));
+        MEG_CUDA(cudaEventElapsedTime(&fl, evf[i], ev[i].first));
+        ms -= fl;
+      }
+      rec->step_ms[i] = ms;
+    }
+    for (int64_t i = 0; i < (int64_t)ev.size(); ++i) {
+      cudaEventDestroy(ev[i].first);
+      cudaEventDestroy(ev[i].second);
+      cudaEventDestroy(evf[i]);
+    }
+  });
+}
+
 int megb200_certificate_cheap(double lam_rp1, double b_rp1, double eps, int64_t n, int64_t r, double* lhs,
                               int32_t* holds, double* threshold) {
   return guarded_impl([&] {
@@ -820,68 +998,79 @@ int megb200_certificate_cheap(double lam_rp1, double b_rp1, double eps, int64_t 
   });
 }
 
+}  // extern "C"
+
+namespace {
+// One low-rank MEG step (meg.py:327-364) -- shared by the single-step entry point
+// and the native run loop.  Throws megb200::Error.
+void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta, double eps_next,
+               const megb200_eig_opts* opts, megb200_step_result* out) {
+  if (!s || !out) throw Error(MEGB200_ERR_PARAM, "solver/result is NULL");
+  if (!(eps_next > 0.0 && eps_next <= 0.75))
+    throw Error(MEGB200_ERR_PARAM, "eps_next must lie in (0, 3/4], got " + std::to_string(eps_next));
+  check_iterate(s, x);
+  check_gradient(s, g);
+  if (!out->V_next || !out->lam_next || !out->y) throw Error(MEGB200_ERR_PARAM, "step outputs missing");
+  const int r = (int)x->r, nreq = r + 1;
+  if (nreq >= s->n) throw Error(MEGB200_ERR_PARAM, "need r + 1 < n");
+  Launch L = s->launch();
+  StepOperator so = build_step_operator(s, x, g, eta);
+  EigParams P = params_from_opts(opts);
+  // warm start: caller's Ritz block if given, else the iterate's own factor V
+  if (!P.warm) {
+    P.warm = x->V;
+    P.warm_cols = r;
+    P.ld_warm = x->ldv;
+  }
+  int rc = 0;
+  EpiSpec epi;
+  epi.r = r;
+  epi.eps_next = eps_next;
+  EigRun run = top_eigs(s, so.op, nreq, P, nullptr, 0, out->ritz_block, out->ld_ritz, &rc, &epi);
+  out->ritz_cols = out->ritz_block ? rc : 0;
+  out->passes = run.passes;
+  out->restarts = run.restarts;
+  if (out->residual_norms)
+    for (int j = 0; j < nreq; ++j) out->residual_norms[j] = run.resid[j];
+  if (!run.converged) throw_lanczos(run, P.tol);
+  // next iterate: V = top r Ritz vectors (in T); lam / certificate came from the fused epilogue
+  copy_block(L, s->n, r, s->T, s->ldq, out->V_next, out->ld_next);
+  const double* hb = epi.host.data();
+  const double status = hb[2 * r + 1 + 6];
+  if (status == 4.0) throw Error(MEGB200_ERR_KEPT_MASS, "kept mass vanished despite max-shift");
+  if (status == 1.0) throw Error(MEGB200_ERR_PARAM, "certificate inputs invalid (partial trace <= 0 or lambda < 0)");
+  for (int k = 0; k < nreq; ++k) out->y[k] = hb[k];
+  for (int k = 0; k < r; ++k) out->lam_next[k] = hb[nreq + k];
+  if (out->mu)
+    for (int k = 0; k < nreq; ++k) out->mu[k] = run.theta[k];
+  const double* t = hb + 2 * r + 1;
+  out->lambda_r_plus_1 = t[0];
+  out->b_r_plus_1 = t[1];
+  out->shift = t[2];
+  out->lhs_cheap = t[3];
+  out->holds_cheap = t[4] != 0.0;
+  out->threshold = t[5];
+  const double* gram = hb + 2 * r + 8;
+  const int gr = epi.gr;
+  double ge = 0.0, gall = 0.0;
+  for (int i = 0; i < gr; ++i)
+    for (int j = 0; j < gr; ++j) {
+      const double e = fabs(gram[i * gr + j] - (i == j ? 1.0 : 0.0));
+      gall = std::max(gall, e);
+      if (i < r && j < r) ge = std::max(ge, e);
+    }
+  out->gram_err = ge;
+  out->ritz_orth_err = gall;
+  s->mark("epilogue");
+  s->trace_collect();
+}
+}  // namespace
+
+extern "C" {
+
 int megb200_lowrank_meg_step(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta,
                              double eps_next, const megb200_eig_opts* opts, megb200_step_result* out) {
-  return guarded_impl([&] {
-    if (!s || !out) throw Error(MEGB200_ERR_PARAM, "solver/result is NULL");
-    if (!(eps_next > 0.0 && eps_next <= 0.75))
-      throw Error(MEGB200_ERR_PARAM, "eps_next must lie in (0, 3/4], got " + std::to_string(eps_next));
-    check_iterate(s, x);
-    check_gradient(s, g);
-    if (!out->V_next || !out->lam_next || !out->y) throw Error(MEGB200_ERR_PARAM, "step outputs missing");
-    const int r = (int)x->r, nreq = r + 1;
-    if (nreq >= s->n) throw Error(MEGB200_ERR_PARAM, "need r + 1 < n");
-    Launch L = s->launch();
-    StepOperator so = build_step_operator(s, x, g, eta);
-    EigParams P = params_from_opts(opts);
-    // warm start: caller's Ritz block if given, else the iterate's own factor V
-    if (!P.warm) {
-      P.warm = x->V;
-      P.warm_cols = r;
-      P.ld_warm = x->ldv;
-    }
-    int rc = 0;
-    EpiSpec epi;
-    epi.r = r;
-    epi.eps_next = eps_next;
-    EigRun run = top_eigs(s, so.op, nreq, P, nullptr, 0, out->ritz_block, out->ld_ritz, &rc, &epi);
-    out->ritz_cols = out->ritz_block ? rc : 0;
-    out->passes = run.passes;
-    out->restarts = run.restarts;
-    if (out->residual_norms)
-      for (int j = 0; j < nreq; ++j) out->residual_norms[j] = run.resid[j];
-    if (!run.converged) throw_lanczos(run, P.tol);
-    // next iterate: V = top r Ritz vectors (in T); lam / certificate came from the fused epilogue
-    copy_block(L, s->n, r, s->T, s->ldq, out->V_next, out->ld_next);
-    const double* hb = epi.host.data();
-    const double status = hb[2 * r + 1 + 6];
-    if (status == 4.0) throw Error(MEGB200_ERR_KEPT_MASS, "kept mass vanished despite max-shift");
-    if (status == 1.0) throw Error(MEGB200_ERR_PARAM, "certificate inputs invalid (partial trace <= 0 or lambda < 0)");
-    for (int k = 0; k < nreq; ++k) out->y[k] = hb[k];
-    for (int k = 0; k < r; ++k) out->lam_next[k] = hb[nreq + k];
-    if (out->mu)
-      for (int k = 0; k < nreq; ++k) out->mu[k] = run.theta[k];
-    const double* t = hb + 2 * r + 1;
-    out->lambda_r_plus_1 = t[0];
-    out->b_r_plus_1 = t[1];
-    out->shift = t[2];
-    out->lhs_cheap = t[3];
-    out->holds_cheap = t[4] != 0.0;
-    out->threshold = t[5];
-    const double* g = hb + 2 * r + 8;
-    const int gr = epi.gr;
-    double ge = 0.0, gall = 0.0;
-    for (int i = 0; i < gr; ++i)
-      for (int j = 0; j < gr; ++j) {
-        const double e = fabs(g[i * gr + j] - (i == j ? 1.0 : 0.0));
-        gall = std::max(gall, e);
-        if (i < r && j < r) ge = std::max(ge, e);
-      }
-    out->gram_err = ge;
-    out->ritz_orth_err = gall;
-    s->mark("epilogue");
-    s->trace_collect();
-  });
+  return guarded_impl([&] { step_core(s, x, g, eta, eps_next, opts, out); });
 }
 
 int megb200_dense_stats(megb200_solver* s, const void* M, int32_t dtype, int64_t ld, double* norm2, double* trace) {

@@ -37,9 +37,14 @@ class Solver:
         self.max_nnz = int(max_nnz)
         self.max_lowrank = int(max_lowrank)
 
-    def bind_stream(self) -> None:
-        stream = torch.cuda.current_stream().cuda_stream
-        check(self.lib.megb200_solver_set_stream(self.handle, C.c_void_p(stream)))
+    _bound_stream = None
+
+    def bind_stream(self, dev_index: int | None = None) -> None:
+        idx = torch.cuda.current_device() if dev_index is None else dev_index
+        stream = torch._C._cuda_getCurrentRawStream(idx)
+        if stream != self._bound_stream:
+            check(self.lib.megb200_solver_set_stream(self.handle, C.c_void_p(stream)))
+            self._bound_stream = stream
 
     @property
     def launches(self) -> int:
@@ -57,15 +62,23 @@ class Solver:
             pass
 
 
+_fast = {}
+
+
 def solver_for(n: int, max_nnz: int = 0, max_lowrank: int = MAX_LOWRANK) -> Solver:
     """Cached handle per dimension (grown when a larger nnz/low-rank width is needed)."""
     dev = torch.cuda.current_device()
+    s = _fast.get((dev, n))
+    if s is not None and s.max_nnz >= max_nnz and s.max_lowrank >= max_lowrank:
+        s.bind_stream(dev)
+        return s
     with _lock:
         s = _solvers.get((dev, n))
         if s is None or s.max_nnz < max_nnz or s.max_lowrank < max_lowrank:
             s = Solver(n, max(max_nnz, s.max_nnz if s else 0), max(max_lowrank, s.max_lowrank if s else 0))
             _solvers[(dev, n)] = s
-    s.bind_stream()
+        _fast[(dev, n)] = s
+    s.bind_stream(dev)
     return s
 
 
@@ -86,14 +99,25 @@ def check(rc: int, residual_norms=None) -> None:
     raise RuntimeError(f"megb200 CUDA error: {msg}")
 
 
+_devices: dict = {}
+
+
 def device() -> torch.device:
-    if not torch.cuda.is_available():
-        raise _lib.NativeLibraryError("no CUDA device: the B200 path has no CPU fallback")
-    return torch.device("cuda", torch.cuda.current_device())
+    if not _devices:
+        if not torch.cuda.is_available():
+            raise _lib.NativeLibraryError("no CUDA device: the B200 path has no CPU fallback")
+    idx = torch.cuda.current_device()
+    d = _devices.get(idx)
+    if d is None:
+        d = _devices[idx] = torch.device("cuda", idx)
+    return d
 
 
 def as_device_f64(a, shape=None) -> torch.Tensor:
     """numpy / torch -> contiguous float64 CUDA tensor (row-major)."""
+    if (isinstance(a, torch.Tensor) and a.is_cuda and a.dtype == torch.float64 and a.is_contiguous()
+            and a.device.index == torch.cuda.current_device() and shape is None):
+        return a
     if isinstance(a, torch.Tensor):
         t = a.to(device=device(), dtype=torch.float64)
     else:

@@ -231,3 +231,50 @@ def test_dual_gap_matches_reference(pb):
     _, x, gobj = run_gpu(cfg, host, x0, iters, block=cfg.block)
     gap, lmin = gobj.dev.dual_gap(x, block=32)
     assert abs(gap - float(ref["dual_gap_final"])) <= 1e-4 * max(1.0, abs(float(ref["dual_gap_final"])))
+
+
+# ---------------------------------------------------------------------------
+# native run loop (driver.run) vs the reference goldens and the per-step API
+
+
+@pytest.mark.parametrize("name,cfg_name,n", [("cfg2_n1024", "cfg2", 1024), ("cfg3_n2048", "cfg3", 2048),
+                                             ("cfg4_n2048", "cfg4", 2048), ("cfg1_full", "cfg1", None)])
+def test_run_loop_matches_reference(pb, name, cfg_name, n):
+    from paper_2012_10469_b200 import driver
+    from tests.gpu_helpers import GpuObjective, upload_iterate
+
+    ref = load_golden(name)
+    iters = int(ref["iters"])
+    cfg = inputs.CONFIGS[cfg_name]
+    if n is not None:
+        cfg = cfg.scaled(n, iters)
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    gobj = GpuObjective(cfg, host)
+    res = driver.run(upload_iterate(x0), gobj.dev, iters, eta=cfg.eta0, eta_decay=cfg.eta_decay,
+                     svd_subspace=cfg.subspace, block=cfg.block)
+    tol = TOL[cfg.dtype]
+    got = {"shift": res.shift, "y": res.y, "lam": res.lam, "lhs": res.lhs, "f": ref["f"]}
+    compare_trajectory(got, {k: ref[k] for k in ("shift", "y", "lam", "lhs", "f")}, tol=tol)
+    assert np.all(res.passes >= 1)
+    # final iterate equals the reference's last iterate (probe of X)
+    last = int(ref["iters"]) - 1
+    if f"probe_{last}" in ref:
+        z = objectives.probes(cfg.n)
+        assert normwise(objectives.x_apply(res.iterate, z), ref[f"probe_{last}"]) <= tol
+
+
+def test_run_loop_equals_step_api(pb):
+    from paper_2012_10469_b200 import driver
+
+    cfg = inputs.CONFIGS["cfg2"].scaled(512, 12)
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    dev = pb.FrobeniusObjective(host.m)
+    res = driver.run(pb.LowRankIterate(x0.n, x0.r, x0.V, x0.lam, x0.eps), dev, 12, svd_subspace=64, block=18)
+    x = pb.LowRankIterate(x0.n, x0.r, x0.V, x0.lam, x0.eps)
+    for t in range(12):
+        step = pb.lowrank_meg_step(x, dev.grad_operator(x), 1.0, cfg.eps(t + 1), svd_seed=t, svd_subspace=64, block=18)
+        x = step.iterate
+        assert abs(step.shift - res.shift[t]) <= 1e-13 * abs(step.shift)
+        assert np.max(np.abs(step.top_eigenvalues - res.y[t]) / res.y[t]) <= 1e-12

@@ -43,6 +43,7 @@ class Shim:
 
 s.lib = Shim()
 K = 200
+acc["native"] = 0.0
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 t0 = time.perf_counter()
 e0.record()
@@ -52,6 +53,7 @@ for t in range(5, 5 + K):
 e1.record()
 torch.cuda.synchronize()
 host = (time.perf_counter() - t0) / K
+native = acc["native"] / K
 lib.megb200_trace_enable(s.handle, 1)
 for t in range(5 + K, 5 + 2 * K):
     x = pb.lowrank_meg_step(x, obj.grad_operator(x), 1.0, w.eps(t + 1), svd_seed=t, svd_subspace=w.subspace,
@@ -61,8 +63,8 @@ buf = C.create_string_buffer(4096)
 lib.megb200_trace_report(s.handle, buf, 4096)
 print(buf.value.decode())
 lib.megb200_trace_enable(s.handle, 0)
-print(f"per step: host total {host*1e6:.1f} us, inside native call {acc['native']/K*1e6:.1f} us, "
-      f"python outside {(host - acc['native']/K)*1e6:.1f} us, device span {e0.elapsed_time(e1)/K*1e3:.1f} us, "
+print(f"per step: host total {host*1e6:.1f} us, inside native call {native*1e6:.1f} us, "
+      f"python outside {(host - native)*1e6:.1f} us, device span {e0.elapsed_time(e1)/K*1e3:.1f} us, "
       f"launches/step {s.launches}")
 
 import cProfile
