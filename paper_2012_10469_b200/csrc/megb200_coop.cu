@@ -519,7 +519,9 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
   extern __shared__ double sm[];
   cg::grid_group grid = cg::this_grid();
   phase_mark(10);
-  if (blockIdx.x == 0) block_jacobi(H, ldh, m, theta, S, sm, info);
+  // small Rayleigh-Ritz problems are solved here by CTA 0; large ones (m > 48)
+  // arrive pre-solved from k_rr_jacobi (1024 threads) -- flagged by info == nullptr
+  if (blockIdx.x == 0 && info) block_jacobi(H, ldh, m, theta, S, sm, info);
   phase_mark(11);
   grid.sync();
   phase_mark(12);
@@ -638,14 +640,17 @@ void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta
              double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi) {
   if (nreq > 64 || rq > 64) throw Error(MEGB200_ERR_PARAM, "rr: at most 64 Ritz vectors");
   const int G = coop_grid(n, sm_count);
-  const size_t smem = std::max((size_t)jacobi_smem_doubles(m),
+  const bool fused = m <= 48;
+  if (!fused) rr_jacobi(L, H, ldh, m, theta, S, nullptr, 0, 0, nreq, nullptr, info);
+  const size_t smem = std::max(fused ? (size_t)jacobi_smem_doubles(m) : (size_t)0,
                                (size_t)(m * rq + kCT + kRC * 2 * std::max(gr, 1))) * sizeof(double);
+  double* info_arg = fused ? info : nullptr;
   const int JG = pick_j(std::max(1, gr * gr));
 #define MEG_RR(jj)                                                                                              \
   {                                                                                                             \
     static bool a = false;                                                                                      \
     if (!a) { raise_smem(k_coop_rr<jj>, 215 * 1024); a = true; }                                                \
-    coop_launch(L, k_coop_rr<jj>, G, smem, H, ldh, m, theta, S, info, n, Q, AQ, ldq, rq, nreq, T, ldt, resid,    \
+    coop_launch(L, k_coop_rr<jj>, G, smem, H, ldh, m, theta, S, info_arg, n, Q, AQ, ldq, rq, nreq, T, ldt, resid, \
                 part, gr, Gout, eps_next, epi);                                                                 \
   }
   MEG_J_DISPATCH(JG, MEG_RR)

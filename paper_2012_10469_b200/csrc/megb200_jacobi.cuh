@@ -111,17 +111,18 @@ __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, 
         sn[rot_pair] = s;
       }
       __syncthreads();
-      for (int idx = t; idx < half * half; idx += nth) {
-        const int a = idx / half, bb = idx - a * half;
-        const int pa = pp[a], qa = qq[a], pb = pp[bb], qb = qq[bb];
-        const double ca = cs[a], sa = sn[a], cb = cs[bb], sb = sn[bb];
+      // two independent items per iteration (ILP: both items' loads issue before either's math)
+      auto hblock = [&](int idx) {
+        const int aa = idx / half, bb = idx - aa * half;
+        const int pa = pp[aa], qa = qq[aa], pb = pp[bb], qb = qq[bb];
+        const double ca = cs[aa], sa = sn[aa], cb = cs[bb], sb = sn[bb];
         const double h00 = H[pa * mp + pb], h01 = H[pa * mp + qb];
         const double h10 = H[qa * mp + pb], h11 = H[qa * mp + qb];
         const double t00 = ca * h00 - sa * h10, t01 = ca * h01 - sa * h11;
         const double t10 = sa * h00 + ca * h10, t11 = sa * h01 + ca * h11;
         double n00 = t00 * cb - t01 * sb, n01 = t00 * sb + t01 * cb;
         double n10 = t10 * cb - t11 * sb, n11 = t10 * sb + t11 * cb;
-        if (a == bb) {
+        if (aa == bb) {
           const double avg = 0.5 * (n01 + n10);
           n01 = avg;
           n10 = avg;
@@ -130,14 +131,23 @@ __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, 
         H[pa * mp + qb] = n01;
         H[qa * mp + pb] = n10;
         H[qa * mp + qb] = n11;
-      }
-      for (int idx = t; idx < mp * half; idx += nth) {
-        const int i = idx / half, a = idx - i * half;
-        const int pa = pp[a], qa = qq[a];
-        const double ca = cs[a], sa = sn[a];
+      };
+      auto vrot = [&](int idx) {
+        const int i = idx / half, aa = idx - i * half;
+        const int pa = pp[aa], qa = qq[aa];
+        const double ca = cs[aa], sa = sn[aa];
         const double vp = V[i * mp + pa], vq = V[i * mp + qa];
         V[i * mp + pa] = ca * vp - sa * vq;
         V[i * mp + qa] = sa * vp + ca * vq;
+      };
+      const int nhb = half * half, nvr = mp * half;
+      for (int idx = t; idx < nhb; idx += 2 * nth) {
+        hblock(idx);
+        if (idx + nth < nhb) hblock(idx + nth);
+      }
+      for (int idx = t; idx < nvr; idx += 2 * nth) {
+        vrot(idx);
+        if (idx + nth < nvr) vrot(idx + nth);
       }
       __syncthreads();
     }

@@ -1451,7 +1451,7 @@ void rr_jacobi(const Launch& L, const double* H, int64_t ldh, int m, double* the
     MEG_CUDA(cudaFuncSetAttribute(k_rr_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 215 * 1024));
     attr = true;
   }
-  const int threads = m <= 24 ? 64 : m <= 48 ? 256 : m <= 80 ? 512 : kJacobiThreads;
+  const int threads = m <= 24 ? 64 : m <= 48 ? 256 : kJacobiThreads;
   k_rr_jacobi<<<1, threads, smem, L.stream>>>(H, ldh, m, theta, S, Rn, rn_rows, cur, nreq, est, info);
   MEG_LAUNCHED();
   ++*L.counter;

@@ -322,8 +322,11 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   Launch L = s->launch();
   // ---- sizes
   int bw = P.block > 0 ? P.block : std::min(s->max_block, nreq + 7);
-  int mmax = P.basis > 0 ? P.basis : std::max({4 * bw, 2 * nreq + 10, 30});
+  // basis: the reference's `subspace` (basis size of its single-vector Lanczos)
+  // is honoured as a lower bound; a block method needs several blocks per cycle,
+  // so the default is 6 blocks (<= 112, the Rayleigh-Ritz limit)
   if (P.basis > 0 && P.block <= 0) bw = std::max(1, std::min(bw, P.basis / 2));
+  int mmax = std::max({P.basis > 0 ? P.basis : 0, 6 * bw, 2 * nreq + 10, 30});
   bw = std::max(1, std::min<int>(bw, s->max_block));
   mmax = std::min<int>(mmax, s->max_basis);
   mmax = std::max(mmax, std::min<int>(nreq + bw, s->max_basis));
@@ -381,56 +384,62 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
     run.passes++;
     s->mark("pass+finish");
     const int newcols = cols + cur;
-    // Rayleigh-Ritz on H[0:newcols, 0:newcols] + explicit Ritz residuals from the
-    // cached images (linalg.py:205-211) (+ speculative step epilogue) in one launch
-    const int rq = std::min(newcols, std::max(nreq, bw));
-    const int gr = epi ? rq : 0;  // Gram of the whole Ritz block (V_next = its first r columns)
-    coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, n, s->Q, s->AQ, s->ldq, rq, nreq, s->T, s->ldq,
-            s->resid, s->red, s->sm_count, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
-            epi ? s->pack + s->pack_epi : nullptr);
-    // one read-back: theta | resid | epilogue | Gram
-    double* pk = s->h_buf;
-    s->d2h(pk, s->pack, s->pack_gram + (int64_t)gr * gr);
-    const int epi_len = epi ? 2 * epi->r + 8 : 0;
-    double* hb = pk + s->pack_gram + (int64_t)gr * gr;  // scratch: compact copy in the old layout
-    s->mark("rr+ritz");
-    s->sync();
-    s->mark("host_decide");
-    std::copy(pk, pk + newcols, hb);
-    std::copy(pk + s->pack_resid, pk + s->pack_resid + nreq, hb + newcols);
-    if (epi) {
-      std::copy(pk + s->pack_epi, pk + s->pack_epi + epi_len, hb + newcols + nreq);
-      std::copy(pk + s->pack_gram, pk + s->pack_gram + (int64_t)gr * gr, hb + newcols + nreq + epi_len);
-    }
-    double tmax = 0.0;
-    for (int j = 0; j < newcols; ++j) tmax = std::max(tmax, fabs(hb[j]));
-    scale = std::max(1.0, tmax);  // norm estimate max(1, max|theta_all|) (linalg.py:214)
-    const bool complete = (newcols >= n);
-    bool ok = true;
-    double rmax = 0.0, best_max = 0.0;
-    for (int j = 0; j < nreq; ++j) {
-      ok = ok && (hb[newcols + j] <= tol * scale);
-      rmax = std::max(rmax, hb[newcols + j]);
-    }
-    for (double v : best) best_max = std::max(best_max, v);
-    if (rmax < best_max)
-      for (int j = 0; j < nreq; ++j) best[j] = hb[newcols + j];
-    if (ok || complete) {
-      run.theta.assign(hb, hb + nreq);
-      run.resid.assign(hb + newcols, hb + newcols + nreq);
-      run.norm_est = scale;
-      run.converged = true;
-      if (epi) {
-        epi->host.assign(hb + newcols + nreq, hb + newcols + nreq + epi_len + gr * gr);
-        epi->gr = gr;
-      }
-      if (vec_out) copy_block(L, n, nreq, s->T, s->ldq, vec_out, ld_vec);
-      if (ritz_out) copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
-      if (ritz_cols_out) *ritz_cols_out = rq;
-      return run;
-    }
-    if (run.passes >= max_passes) break;
     const int nxt = (int)std::min<int64_t>(bw, n - newcols);
+    const bool full = (nxt <= 0) || (newcols + nxt > mmax);
+    // Rayleigh-Ritz only where its result is used: the first pass of a solve
+    // (warm-started steps converge there), a full basis (restart), the budget end
+    const bool do_rr = (cols == 0) || full || (run.passes >= max_passes);
+    if (do_rr) {
+      // Rayleigh-Ritz on H[0:newcols, 0:newcols] + explicit Ritz residuals from the
+      // cached images (linalg.py:205-211) (+ speculative step epilogue) in one launch
+      const int rq = std::min(newcols, std::max(nreq, bw));
+      const int gr = epi ? rq : 0;  // Gram of the whole Ritz block (V_next = its first r columns)
+      coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, n, s->Q, s->AQ, s->ldq, rq, nreq, s->T, s->ldq,
+              s->resid, s->red, s->sm_count, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
+              epi ? s->pack + s->pack_epi : nullptr);
+      // one read-back: theta | resid | epilogue | Gram
+      double* pk = s->h_buf;
+      s->d2h(pk, s->pack, s->pack_gram + (int64_t)gr * gr);
+      const int epi_len = epi ? 2 * epi->r + 8 : 0;
+      double* hb = pk + s->pack_gram + (int64_t)gr * gr;  // scratch: compact copy in the old layout
+      s->mark("rr+ritz");
+      s->sync();
+      s->mark("host_decide");
+      std::copy(pk, pk + newcols, hb);
+      std::copy(pk + s->pack_resid, pk + s->pack_resid + nreq, hb + newcols);
+      if (epi) {
+        std::copy(pk + s->pack_epi, pk + s->pack_epi + epi_len, hb + newcols + nreq);
+        std::copy(pk + s->pack_gram, pk + s->pack_gram + (int64_t)gr * gr, hb + newcols + nreq + epi_len);
+      }
+      double tmax = 0.0;
+      for (int j = 0; j < newcols; ++j) tmax = std::max(tmax, fabs(hb[j]));
+      scale = std::max(1.0, tmax);  // norm estimate max(1, max|theta_all|) (linalg.py:214)
+      const bool complete = (newcols >= n);
+      bool ok = true;
+      double rmax = 0.0, best_max = 0.0;
+      for (int j = 0; j < nreq; ++j) {
+        ok = ok && (hb[newcols + j] <= tol * scale);
+        rmax = std::max(rmax, hb[newcols + j]);
+      }
+      for (double v : best) best_max = std::max(best_max, v);
+      if (rmax < best_max)
+        for (int j = 0; j < nreq; ++j) best[j] = hb[newcols + j];
+      if (ok || complete) {
+        run.theta.assign(hb, hb + nreq);
+        run.resid.assign(hb + newcols, hb + newcols + nreq);
+        run.norm_est = scale;
+        run.converged = true;
+        if (epi) {
+          epi->host.assign(hb + newcols + nreq, hb + newcols + nreq + epi_len + gr * gr);
+          epi->gr = gr;
+        }
+        if (vec_out) copy_block(L, n, nreq, s->T, s->ldq, vec_out, ld_vec);
+        if (ritz_out) copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
+        if (ritz_cols_out) *ritz_cols_out = rq;
+        return run;
+      }
+      if (run.passes >= max_passes) break;
+    }
     if (nxt <= 0) break;
     // next Krylov block: the image block orthogonalised against the basis
     if (nxt == cur) {
@@ -442,7 +451,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
     orthonormalize(s, s->Q + newcols, s->ldq, nxt, newcols, scale, key_refill, refill_ctr, false);
     s->mark("orth_next");
     cols = newcols;
-    if (cols + nxt > mmax) {
+    if (full) {
       // thick restart: keep the leading `keep` Ritz pairs, continue from the next block
       nn(L, n, s->Q, s->ldq, cols, s->S, cols, keep, 1.0, 0.0, s->T, s->ldq);
       copy_block(L, n, keep, s->T, s->ldq, s->Q, s->ldq);
