@@ -240,6 +240,13 @@ typedef struct megb200_run_record { /* host arrays, any may be NULL; row i = ste
   int32_t* holds;  /* T           */
   int32_t* passes; /* T           */
   double* step_ms; /* T: device time per step: previous step end -> this step end, minus the flush */
+  /* final warm Ritz block (device, n x ritz_cap, leading dim ld_ritz) so a later run or step
+   * continues warm: ritz_cols and ritz_orth_err are written when ritz_block is set */
+  double* ritz_block;
+  int64_t ld_ritz;
+  int64_t ritz_cap;
+  int64_t ritz_cols;
+  double ritz_orth_err;
 } megb200_run_record;
 
 int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_gradient* g,

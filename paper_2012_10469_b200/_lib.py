@@ -92,6 +92,8 @@ class RunRecord(C.Structure):
     _fields_ = [
         ("shift", c_double_p), ("y", c_double_p), ("lam", c_double_p), ("eps", c_double_p), ("lhs", c_double_p),
         ("holds", c_int32_p), ("passes", c_int32_p), ("step_ms", c_double_p),
+        ("ritz_block", C.c_void_p), ("ld_ritz", C.c_int64), ("ritz_cap", C.c_int64), ("ritz_cols", C.c_int64),
+        ("ritz_orth_err", C.c_double),
     ]
 
 

@@ -41,6 +41,7 @@ namespace {
 
 constexpr int kCT = 256;     // threads per CTA
 constexpr int kRC = 32;      // rows staged per chunk
+constexpr int kMaxLowrank = 160;  // widest low-rank factor of an operator (solver max_lowrank)
 constexpr double kInv53c = 1.0 / 9007199254740992.0;
 
 __device__ __forceinline__ double gauss_c(uint64_t key, uint64_t ctr) {
@@ -331,11 +332,27 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
                                                       const double* __restrict__ U, int64_t ldu,
                                                       double* __restrict__ W, int64_t ldw, double* __restrict__ Ews,
                                                       double* __restrict__ part, const double* __restrict__ Qh,
-                                                      int64_t ldq, int hp, double* __restrict__ Hout, int64_t ldh) {
+                                                      int64_t ldq, int hp, double* __restrict__ Hout, int64_t ldh,
+                                                      LamCoef lc) {
   extern __shared__ double sm[];
+  __shared__ double dsh[kMaxLowrank];
   phase_mark(20);
   int64_t r0, r1;
   cta_rows(n, r0, r1);
+  if (lc.lam) {
+    // coefficients from device-resident kept weights (first lr), the rest as given
+    for (int k = threadIdx.x; k < l; k += kCT) {
+      double v;
+      if (k < lc.lr) {
+        const double kept = lc.c1 * lc.lam[k];
+        v = (log(kept) - lc.log_tail) + (-lc.eta * (kept - lc.tail_g));
+      } else {
+        v = d[k];
+      }
+      dsh[k] = v;
+    }
+    d = dsh;  // read after the grid.sync below
+  }
   if (l > 0) {
     double acc[J];
     xty_rows<J>(r0, r1, Lf, ldl, l, U, ldu, b, sm, acc);
@@ -476,7 +493,8 @@ void coop_cholqr(const Launch& L, int64_t n, const double* Wsrc, int64_t lds, do
 void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, double scale, const double* Lf,
                  int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
                  int64_t ldw, double* Ews, double* part, int sm_count, const double* Qh, int64_t ldq, int hp,
-                 double* Hout, int64_t ldh) {
+                 double* Hout, int64_t ldh, LamCoef lc) {
+  if (lc.lam && (l > kMaxLowrank || lc.lr > l)) throw Error(MEGB200_ERR_PARAM, "finish: coefficient width out of range");
   const int G = coop_grid(n, sm_count);
   const size_t smem = std::max({(size_t)kRC * (l + b), (size_t)std::max(1, l * b), (size_t)kRC * (hp + b)}) *
                       sizeof(double);
@@ -487,7 +505,7 @@ void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, 
     static bool a = false;                                                                                      \
     if (!a) { raise_smem(k_coop_finish<jj, j2>, kCoopSmem); a = true; }                                         \
     coop_launch(L, k_coop_finish<jj, j2>, G, smem, n, b, S, spart, scale, Lf, ldl, l, d, alpha, U, ldu, W, ldw,  \
-                Ews, part, Qh, ldq, hp, Hout, ldh);                                                             \
+                Ews, part, Qh, ldq, hp, Hout, ldh, lc);                                                         \
   }
 #define MEG_FIN(jj)                                            \
   switch (J2) {                                                \

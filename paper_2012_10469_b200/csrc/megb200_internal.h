@@ -116,10 +116,18 @@ void coop_cgs(const Launch& L, int64_t n, const double* Q, int64_t ldq, int cols
 void coop_cholqr(const Launch& L, int64_t n, const double* Wsrc, int64_t lds, double* W, int64_t ldw, int q,
                  double thresh, double* Gws, double* Rrel, double* Rinv, int* mask, const double* Rprev, double* Rtot,
                  uint64_t key, uint64_t base, double* part, int sm_count);
+// Log-map coefficients of a factored iterate computed on the device (so a step
+// can consume the kept weights lam another launch left in device memory):
+// d[k] = log(c1 lam[k]) - log_tail - eta (c1 lam[k] - tail_g) for k < lr.
+struct LamCoef {
+  const double* lam = nullptr;
+  int lr = 0;
+  double c1 = 0.0, log_tail = 0.0, eta = 0.0, tail_g = 0.0;
+};
 void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, double scale, const double* Lf,
                  int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
                  int64_t ldw, double* Ews, double* part, int sm_count, const double* Qh = nullptr, int64_t ldq = 0,
-                 int hp = 0, double* Hout = nullptr, int64_t ldh = 0);
+                 int hp = 0, double* Hout = nullptr, int64_t ldh = 0, LamCoef lc = LamCoef());
 // Jacobi RR + Ritz block + residuals (+ Gram of the first gr Ritz vectors, + MEG epilogue into epi)
 void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,
              const double* Q, const double* AQ, int64_t ldq, int rq, int nreq, double* T, int64_t ldt, double* resid,

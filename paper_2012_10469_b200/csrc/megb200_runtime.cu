@@ -51,6 +51,7 @@ struct megb200_solver {
   double* L = nullptr;      // n x max_lowrank
   double* E = nullptr;      // max_lowrank x max_block
   double* dvec = nullptr;   // max_lowrank
+  double* dlam = nullptr;   // 64: kept weights of the current iterate (device copy)
   double* H = nullptr;      // cap x cap
   double* C = nullptr;      // cap x max_block
   double* C2 = nullptr;
@@ -61,7 +62,7 @@ struct megb200_solver {
   // per-pass result pack, read back with ONE device-to-host copy:
   // [theta (cap) | resid (64) | step epilogue (136) | Ritz-block Gram (<= 64 x 64)]
   double* pack = nullptr;
-  int64_t pack_resid = 0, pack_epi = 0, pack_gram = 0;
+  int64_t pack_resid = 0, pack_epi = 0, pack_gram = 0, pack_len = 0;
   double* csr_g = nullptr;  // max_nnz
   double* rowsq = nullptr;  // n
   double* h_buf = nullptr;  // pinned host staging
@@ -85,6 +86,16 @@ struct megb200_solver {
   std::vector<cudaEvent_t> trace_pool;
   size_t trace_next = 0;
   std::vector<std::pair<std::string, std::pair<double, int64_t>>> trace_acc;
+  std::vector<std::pair<std::string, std::pair<double, int64_t>>> trace_stat;  // (name, (sum, count))
+  void stat(const std::string& name, double v) {
+    for (auto& kv : trace_stat)
+      if (kv.first == name) {
+        kv.second.first += v;
+        kv.second.second += 1;
+        return;
+      }
+    trace_stat.push_back({name, {v, 1}});
+  }
   void mark(const char* tag) {
     if (!trace) return;
     if (trace_next == trace_pool.size()) {
@@ -172,6 +183,7 @@ struct OpDev {
   int64_t ldl = 0;
   int l = 0;
   const double* d_dev = nullptr;  // device coefficients (length l)
+  LamCoef lc;                     // or the first lc.lr of them from device-resident kept weights
   double alpha = 0.0;
 };
 
@@ -205,7 +217,7 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
     s->prof_passes++;
   }
   coop_finish(L, n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
-              s->sm_count, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap);
+              s->sm_count, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap, op.lc);
 }
 
 // columns k > 64 are applied in chunks (re-streams the operand; not used by the configs)
@@ -314,13 +326,15 @@ struct EpiSpec {
   std::vector<double> host;  // out: epilogue block (2r + 8 doubles) + Gram (gr x gr)
 };
 
-// Outputs: eigenvectors (nreq) -> vec_out, top `bw` Ritz vectors -> ritz_out.
-EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P, double* vec_out, int64_t ld_vec,
-                double* ritz_out, int64_t ld_ritz, int* ritz_cols_out, EpiSpec* epi = nullptr) {
+// Block sizes of a solve: block width bw, basis limit mmax, thick-restart keep.
+struct EigShape {
+  int bw = 1, mmax = 1, keep = 1, max_passes = 1;
+  bool exhaust = false;
+};
+
+EigShape eig_shape(const megb200_solver* s, int nreq, const EigParams& P) {
   const int64_t n = s->n;
   if (!(1 <= nreq && nreq < n)) throw Error(MEGB200_ERR_PARAM, "need 1 <= r < n, got r=" + std::to_string(nreq) + ", n=" + std::to_string(n));
-  Launch L = s->launch();
-  // ---- sizes
   int bw = P.block > 0 ? P.block : std::min(s->max_block, nreq + 7);
   // basis: the reference's `subspace` (basis size of its single-vector Lanczos)
   // is honoured as a lower bound; a block method needs several blocks per cycle,
@@ -344,7 +358,72 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   keep = std::min(keep, mmax - bw);
   if (!exhaust && (keep & 1) && (bw & 1) == 0) keep = (keep + 1 <= mmax - bw) ? keep + 1 : (keep - 1 >= nreq ? keep - 1 : keep);
   if (!exhaust && keep < nreq) throw Error(MEGB200_ERR_PARAM, "basis too small for the requested eigenpairs");
-  const int max_passes = P.max_passes > 0 ? P.max_passes : P.restarts * mmax;
+  EigShape sh;
+  sh.bw = bw;
+  sh.mmax = mmax;
+  sh.keep = keep;
+  sh.exhaust = exhaust;
+  sh.max_passes = P.max_passes > 0 ? P.max_passes : P.restarts * mmax;
+  return sh;
+}
+
+// One operator pass on the block Q[:, cols:cols+cur] into AQ, and its column of H = Q^T A Q.
+void block_pass(megb200_solver* s, const OpDev& op, int cols, int cur) {
+  Launch L = s->launch();
+  if (cur <= 32) {
+    // pass + epilogue; the epilogue launch also reduces the H column Q^T (A Q_j)
+    apply_op(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq, cols + cur, s->H + cols);
+  } else {
+    apply_op_wide(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq);
+    coop_tn(L, s->n, s->Q, s->ldq, cols + cur, s->AQ + cols, s->ldq, cur, s->H + cols, s->cap, nullptr, 1.0, s->red,
+            s->sm_count);
+  }
+}
+
+// Rayleigh-Ritz on H[0:newcols, 0:newcols] + Ritz block T + explicit residuals
+// from the cached images (linalg.py:205-211) (+ speculative step epilogue and
+// the Ritz-block Gram) in one launch, then one asynchronous read-back of the
+// pack [theta | resid | epilogue | Gram] into dst (pinned).  Returns the Gram order.
+int rr_readback(megb200_solver* s, int newcols, int nreq, int bw, const EpiSpec* epi, double* dst) {
+  Launch L = s->launch();
+  const int rq = std::min(newcols, std::max(nreq, bw));
+  const int gr = epi ? rq : 0;  // Gram of the whole Ritz block (V_next = its first r columns)
+  coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, s->n, s->Q, s->AQ, s->ldq, rq, nreq, s->T, s->ldq,
+          s->resid, s->red, s->sm_count, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
+          epi ? s->pack + s->pack_epi : nullptr);
+  s->d2h(dst, s->pack, s->pack_gram + (int64_t)gr * gr);
+  return gr;
+}
+
+// Convergence decision on a read-back pack (linalg.py:212-216): every wanted
+// residual <= tol * max(1, max |theta|), or the basis spans R^n.
+struct RRDecision {
+  bool ok = false;
+  double scale = 1.0, rmax = 0.0;
+};
+
+RRDecision rr_decide(const megb200_solver* s, const double* pk, int newcols, int nreq, double tol) {
+  RRDecision d;
+  double tmax = 0.0;
+  for (int j = 0; j < newcols; ++j) tmax = std::max(tmax, fabs(pk[j]));
+  d.scale = std::max(1.0, tmax);  // norm estimate max(1, max|theta_all|) (linalg.py:214)
+  bool ok = true;
+  for (int j = 0; j < nreq; ++j) {
+    const double rj = pk[s->pack_resid + j];
+    ok = ok && (rj <= tol * d.scale);
+    d.rmax = std::max(d.rmax, rj);
+  }
+  d.ok = ok || (newcols >= s->n);
+  return d;
+}
+
+// Outputs: eigenvectors (nreq) -> vec_out, top `bw` Ritz vectors -> ritz_out.
+EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P, double* vec_out, int64_t ld_vec,
+                double* ritz_out, int64_t ld_ritz, int* ritz_cols_out, EpiSpec* epi = nullptr) {
+  const int64_t n = s->n;
+  Launch L = s->launch();
+  const EigShape sh = eig_shape(s, nreq, P);
+  const int bw = sh.bw, mmax = sh.mmax, keep = sh.keep, max_passes = sh.max_passes;
   const double tol = P.tol;
   const uint64_t key_start = stream_key(P.seed, kStreamStart);
   const uint64_t key_refill = stream_key(P.seed, kStreamRefill);
@@ -373,14 +452,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   double scale = 1.0;
   for (;;) {
     // operator pass on the current block, then its column of H = Q^T A Q
-    if (cur <= 32) {
-      // pass + epilogue; the epilogue launch also reduces the H column Q^T (A Q_j)
-      apply_op(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq, cols + cur, s->H + cols);
-    } else {
-      apply_op_wide(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq);
-      coop_tn(L, n, s->Q, s->ldq, cols + cur, s->AQ + cols, s->ldq, cur, s->H + cols, s->cap, nullptr, 1.0, s->red,
-              s->sm_count);
-    }
+    block_pass(s, op, cols, cur);
     run.passes++;
     s->mark("pass+finish");
     const int newcols = cols + cur;
@@ -390,47 +462,32 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
     // (warm-started steps converge there), a full basis (restart), the budget end
     const bool do_rr = (cols == 0) || full || (run.passes >= max_passes);
     if (do_rr) {
-      // Rayleigh-Ritz on H[0:newcols, 0:newcols] + explicit Ritz residuals from the
-      // cached images (linalg.py:205-211) (+ speculative step epilogue) in one launch
-      const int rq = std::min(newcols, std::max(nreq, bw));
-      const int gr = epi ? rq : 0;  // Gram of the whole Ritz block (V_next = its first r columns)
-      coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, n, s->Q, s->AQ, s->ldq, rq, nreq, s->T, s->ldq,
-              s->resid, s->red, s->sm_count, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
-              epi ? s->pack + s->pack_epi : nullptr);
-      // one read-back: theta | resid | epilogue | Gram
       double* pk = s->h_buf;
-      s->d2h(pk, s->pack, s->pack_gram + (int64_t)gr * gr);
-      const int epi_len = epi ? 2 * epi->r + 8 : 0;
-      double* hb = pk + s->pack_gram + (int64_t)gr * gr;  // scratch: compact copy in the old layout
+      const int gr = rr_readback(s, newcols, nreq, bw, epi, pk);
+      const int rq = std::min(newcols, std::max(nreq, bw));
       s->mark("rr+ritz");
       s->sync();
       s->mark("host_decide");
-      std::copy(pk, pk + newcols, hb);
-      std::copy(pk + s->pack_resid, pk + s->pack_resid + nreq, hb + newcols);
-      if (epi) {
-        std::copy(pk + s->pack_epi, pk + s->pack_epi + epi_len, hb + newcols + nreq);
-        std::copy(pk + s->pack_gram, pk + s->pack_gram + (int64_t)gr * gr, hb + newcols + nreq + epi_len);
+      if (s->trace) {  // diagnostics only: Jacobi sweeps of this Rayleigh-Ritz solve
+        double inf[3];
+        MEG_CUDA(cudaMemcpy(inf, s->info, sizeof inf, cudaMemcpyDeviceToHost));
+        s->stat("jacobi_sweeps m=" + std::to_string(newcols), inf[0]);
       }
-      double tmax = 0.0;
-      for (int j = 0; j < newcols; ++j) tmax = std::max(tmax, fabs(hb[j]));
-      scale = std::max(1.0, tmax);  // norm estimate max(1, max|theta_all|) (linalg.py:214)
-      const bool complete = (newcols >= n);
-      bool ok = true;
-      double rmax = 0.0, best_max = 0.0;
-      for (int j = 0; j < nreq; ++j) {
-        ok = ok && (hb[newcols + j] <= tol * scale);
-        rmax = std::max(rmax, hb[newcols + j]);
-      }
+      const RRDecision dec = rr_decide(s, pk, newcols, nreq, tol);
+      scale = dec.scale;
+      double best_max = 0.0;
       for (double v : best) best_max = std::max(best_max, v);
-      if (rmax < best_max)
-        for (int j = 0; j < nreq; ++j) best[j] = hb[newcols + j];
-      if (ok || complete) {
-        run.theta.assign(hb, hb + nreq);
-        run.resid.assign(hb + newcols, hb + newcols + nreq);
+      if (dec.rmax < best_max)
+        for (int j = 0; j < nreq; ++j) best[j] = pk[s->pack_resid + j];
+      if (dec.ok) {
+        run.theta.assign(pk, pk + nreq);
+        run.resid.assign(pk + s->pack_resid, pk + s->pack_resid + nreq);
         run.norm_est = scale;
         run.converged = true;
         if (epi) {
-          epi->host.assign(hb + newcols + nreq, hb + newcols + nreq + epi_len + gr * gr);
+          const int epi_len = 2 * epi->r + 8;
+          epi->host.assign(pk + s->pack_epi, pk + s->pack_epi + epi_len);
+          epi->host.insert(epi->host.end(), pk + s->pack_gram, pk + s->pack_gram + (int64_t)gr * gr);
           epi->gr = gr;
         }
         if (vec_out) copy_block(L, n, nreq, s->T, s->ldq, vec_out, ld_vec);
@@ -541,11 +598,48 @@ void x_coeffs(int64_t n, int64_t r, const double* lam, double eps, std::vector<d
   for (int64_t k = 0; k < r; ++k) c[k] = (1.0 - eps) * lam[k] - tail;
 }
 
+// The step operator of a Frobenius objective whose gradient iterate is the
+// iterate itself: eta M + V diag(d) V^T + alpha I with
+// d = log((1-eps) lam) - log tail - eta ((1-eps) lam - tail), alpha = log tail - eta tail,
+// tail = eps / (n - r) (meg.py:287-307 + objectives.py X_g).  The kept weights
+// lam are read on the device (lam_dev), so the operator of step t+1 can be
+// enqueued before step t's results reach the host.
+OpDev frob_merged_op(const megb200_gradient* g, const double* V, int64_t ldv, int64_t n, int r, double eps, double eta,
+                     const double* lam_dev) {
+  OpDev op;
+  op.kind = MEGB200_OP_DENSE;
+  op.dtype = g->dtype;
+  op.dense = g->dense;
+  op.ld = g->ld;
+  op.scale = eta;
+  const double tail = eps / (double)(n - r);
+  const double log_tail = log(tail);
+  op.alpha = log_tail;
+  op.alpha += -eta * tail;
+  op.L = V;
+  op.ldl = ldv;
+  op.l = r;
+  op.d_dev = nullptr;
+  op.lc.lam = lam_dev;
+  op.lc.lr = r;
+  op.lc.c1 = 1.0 - eps;
+  op.lc.log_tail = log_tail;
+  op.lc.eta = eta;
+  op.lc.tail_g = tail;
+  return op;
+}
+
 StepOperator build_step_operator(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g,
                                  double eta) {
   Launch L = s->launch();
   const int64_t n = s->n, r = x->r;
   StepOperator so;
+  if (g->kind == MEGB200_GRAD_FROBENIUS && g->gV == x->V && g->g_r == r && g->g_ldv == x->ldv && g->g_eps == x->eps &&
+      r <= 64 && std::equal(x->lam, x->lam + r, g->g_lam)) {
+    s->h2d(s->dlam, x->lam, r);
+    so.op = frob_merged_op(g, x->V, x->ldv, n, (int)r, x->eps, eta, s->dlam);
+    return so;
+  }
   OpDev& op = so.op;
   // log X = V diag(log_kept - log_tail) V^T + log_tail I
   const double tail_x = x->eps / (double)(n - r);
@@ -723,6 +817,7 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
         {&s->L, n * s->max_lowrank},
         {&s->E, s->max_lowrank * max_block},
         {&s->dvec, s->max_lowrank},
+        {&s->dlam, 64},
         {&s->H, (int64_t)s->cap * s->cap},
         {&s->C, (int64_t)s->cap * max_block},
         {&s->C2, (int64_t)s->cap * max_block},
@@ -762,7 +857,9 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
     s->pack_gram = s->cap + 64 + 136;
     s->theta = s->pack;  // theta lives at the head of the pack
     s->resid = s->pack + s->pack_resid;
-    s->h_buf_len = 2 * ((int64_t)s->cap + 64 + 136 + 64 * 64) + 64;
+    // [pack copy | scratch | pipelined read-back slot 0 | slot 1]
+    s->pack_len = (int64_t)s->cap + 64 + 136 + 64 * 64;
+    s->h_buf_len = 4 * s->pack_len + 64;
     s->h_up_len = 8192;
     e = cudaMallocHost(&s->h_up, s->h_up_len * sizeof(double));
     if (e != cudaSuccess) {
@@ -852,6 +949,92 @@ namespace {
 void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta, double eps_next,
                const megb200_eig_opts* opts, megb200_step_result* out);
 
+// Step outputs from a converged solve's read-back: epilogue block
+// [y (r+1) | lam (r) | lam_{r+1}, b_{r+1}, shift, lhs, holds, threshold, status]
+// and the Gram of the gr-column Ritz block (V_next = its first r columns).
+void fill_step_result(const double* hb, const double* gram, int gr, int r, const double* theta,
+                      megb200_step_result* out) {
+  const int nreq = r + 1;
+  const double status = hb[2 * r + 1 + 6];
+  if (status == 4.0) throw Error(MEGB200_ERR_KEPT_MASS, "kept mass vanished despite max-shift");
+  if (status == 1.0) throw Error(MEGB200_ERR_PARAM, "certificate inputs invalid (partial trace <= 0 or lambda < 0)");
+  for (int k = 0; k < nreq; ++k) out->y[k] = hb[k];
+  for (int k = 0; k < r; ++k) out->lam_next[k] = hb[nreq + k];
+  if (out->mu)
+    for (int k = 0; k < nreq; ++k) out->mu[k] = theta[k];
+  const double* t = hb + 2 * r + 1;
+  out->lambda_r_plus_1 = t[0];
+  out->b_r_plus_1 = t[1];
+  out->shift = t[2];
+  out->lhs_cheap = t[3];
+  out->holds_cheap = t[4] != 0.0;
+  out->threshold = t[5];
+  double ge = 0.0, gall = 0.0;
+  for (int i = 0; i < gr; ++i)
+    for (int j = 0; j < gr; ++j) {
+      const double e = fabs(gram[i * gr + j] - (i == j ? 1.0 : 0.0));
+      gall = std::max(gall, e);
+      if (i < r && j < r) ge = std::max(ge, e);
+    }
+  out->gram_err = ge;
+  out->ritz_orth_err = gall;
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined warm steps.  A step whose start block is a verified-orthonormal
+// Ritz block of exactly bw columns runs, in top_eigs, as: copy the block into
+// Q, one pass, Rayleigh-Ritz + epilogue, read-back, and (when that converged)
+// copies of the Ritz block and V_next.  fast_step_enqueue issues exactly that
+// sequence without waiting for the read-back; fast_step_confirm then applies
+// top_eigs' convergence rule to it.  When it holds, the enqueued work is the
+// work step_core would have done (same kernels, same operands), so results are
+// bit-identical; when it does not, the caller drains the stream and re-runs the
+// step through step_core.
+struct FastStep {
+  int r = 0, nreq = 0, bw = 0, gr = 0;
+  double tol = 0.0;
+  double* dst = nullptr;  // pinned read-back slot
+  cudaEvent_t done = nullptr;
+};
+
+void fast_step_enqueue(megb200_solver* s, const OpDev& op, int r, const EigShape& sh, double tol, const double* warm,
+                       int64_t ld_warm, double eps_next, double* ritz_out, int64_t ld_ritz, double* V_next,
+                       int64_t ld_next, double* dst, cudaEvent_t done, FastStep& fs) {
+  Launch L = s->launch();
+  const int64_t n = s->n;
+  fs.r = r;
+  fs.nreq = r + 1;
+  fs.bw = sh.bw;
+  fs.tol = tol;
+  fs.dst = dst;
+  fs.done = done;
+  copy_block(L, n, sh.bw, warm, ld_warm, s->Q, s->ldq);
+  block_pass(s, op, 0, sh.bw);
+  EpiSpec epi;
+  epi.r = r;
+  epi.eps_next = eps_next;
+  fs.gr = rr_readback(s, sh.bw, fs.nreq, sh.bw, &epi, dst);
+  MEG_CUDA(cudaEventRecord(done, s->stream));
+  const int rq = std::min(sh.bw, std::max(fs.nreq, sh.bw));
+  copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
+  copy_block(L, n, r, s->T, s->ldq, V_next, ld_next);
+}
+
+bool fast_step_confirm(megb200_solver* s, const FastStep& fs, megb200_step_result* out) {
+  MEG_CUDA(cudaEventSynchronize(fs.done));
+  const double* pk = fs.dst;
+  const RRDecision dec = rr_decide(s, pk, fs.bw, fs.nreq, fs.tol);
+  if (!dec.ok) return false;
+  out->passes = 1;
+  out->restarts = 0;
+  out->ritz_cols = std::min(fs.bw, std::max(fs.nreq, fs.bw));
+  if (out->residual_norms)
+    for (int j = 0; j < fs.nreq; ++j) out->residual_norms[j] = pk[s->pack_resid + j];
+  fill_step_result(pk + s->pack_epi, pk + s->pack_gram, fs.gr, fs.r, pk, out);
+  return true;
+}
+
+
 double eps_eval(const megb200_schedule& sc, int64_t t) {
   const double g2 = std::max(sc.G * sc.G, 1.0);
   double raw;
@@ -886,26 +1069,40 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
     const int r = (int)x0->r;
     if (r + 1 > 64 || r + 1 >= n) throw Error(MEGB200_ERR_PARAM, "run loop supports r + 1 <= 64, r + 1 < n");
     Launch L = s->launch();
-    if (!s->run_buf) MEG_CUDA(cudaMalloc(&s->run_buf, (size_t)4 * n * 64 * sizeof(double)));
+    // three slots of (V, Ritz block): step i reads slot i % 3 and writes slot (i + 1) % 3, so a
+    // speculatively enqueued step i + 1 never overwrites the inputs of a step i that must re-run
+    if (!s->run_buf) MEG_CUDA(cudaMalloc(&s->run_buf, (size_t)6 * n * 64 * sizeof(double)));
     if (flush_bytes > s->flush_len) {
       if (s->flush_buf) MEG_CUDA(cudaFree(s->flush_buf));
       MEG_CUDA(cudaMalloc(&s->flush_buf, flush_bytes));
       s->flush_len = flush_bytes;
     }
-    double* Vb[2] = {s->run_buf, s->run_buf + n * 64};
-    double* Wb[2] = {s->run_buf + 2 * n * 64, s->run_buf + 3 * n * 64};
+    double* Vb[3];
+    double* Wb[3];
+    for (int k = 0; k < 3; ++k) {
+      Vb[k] = s->run_buf + (int64_t)k * n * 64;
+      Wb[k] = s->run_buf + (int64_t)(3 + k) * n * 64;
+    }
     copy_block(L, n, r, x0->V, x0->ldv, Vb[0], r);
     std::vector<double> lam(x0->lam, x0->lam + r);
     double eps = x0->eps;
     megb200_eig_opts o{};
     if (opts) o = *opts;
+    const EigParams P0 = params_from_opts(&o);
+    const EigShape sh = eig_shape(s, r + 1, P0);
+    // warm block of the current step: caller's block for step 0 (slot-free), then slot i % 3
     const double* warm = o.warm;
     int64_t warm_cols = o.warm ? o.warm_cols : 0, ld_warm = o.ld_warm;
     bool warm_orth = o.warm && o.warm_orthonormal;
-    int cur = 0, wcur = 0;
+    double last_orth = INFINITY;
+    // pipelining: Frobenius steps (operator coefficients computable on the device), not under the tracer
+    const char* nopipe = getenv("MEGB200_NO_PIPELINE");
+    const bool pipe = g->kind == MEGB200_GRAD_FROBENIUS && !s->trace && !(nopipe && nopipe[0] == '1') &&
+                      !sh.exhaust && sh.max_passes >= 1;
     std::vector<double> lam_next(r), y(r + 1), mu(r + 1), res(r + 1);
     // per-step device time: from the end of the previous step (or this step's
-    // start) to this step's end, minus the flush; host turnaround gaps count
+    // start) to this step's end, minus the flush; host turnaround gaps and
+    // discarded speculative work count
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
     std::vector<cudaEvent_t> evf;
     if (rec && rec->step_ms) {
@@ -917,43 +1114,38 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
         MEG_CUDA(cudaEventCreate(&evf[i]));
       }
     }
-    for (int64_t i = 0; i < T; ++i) {
-      const int64_t t = t0 + i;
-      const double eta = eta_eval(*sch, t), eps_next = eps_eval(*sch, t + 1);
+    cudaEvent_t done[2];
+    for (auto& e : done) MEG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct EvGuard {
+      cudaEvent_t* e;
+      ~EvGuard() {
+        cudaEventDestroy(e[0]);
+        cudaEventDestroy(e[1]);
+      }
+    } guard{done};
+    double* hspec[2] = {s->h_buf + 2 * s->pack_len, s->h_buf + 3 * s->pack_len};
+
+    auto begin_step = [&](int64_t i) {
       if (!ev.empty()) MEG_CUDA(cudaEventRecord(evf[i], s->stream));
       if (flush_bytes) MEG_CUDA(cudaMemsetAsync(s->flush_buf, (int)(i & 0xff), flush_bytes, s->stream));
       if (!ev.empty()) MEG_CUDA(cudaEventRecord(ev[i].first, s->stream));
-      megb200_gradient gg = *g;
-      if (gg.kind == MEGB200_GRAD_FROBENIUS || gg.kind == MEGB200_GRAD_STOCHASTIC || gg.kind == MEGB200_GRAD_SAMPLED) {
-        gg.gV = Vb[cur];
-        gg.g_r = r;
-        gg.g_ldv = r;
-        gg.g_lam = lam.data();
-        gg.g_eps = eps;
-      }
-      if (gg.kind == MEGB200_GRAD_STOCHASTIC) {
-        if (!gg.A) throw Error(MEGB200_ERR_PARAM, "stochastic run needs a minibatch buffer g->A");
-        fill_gaussian(L, n, (int)gg.bsz, stream_key(sch->minibatch_seed, 5), (uint64_t)t * n * gg.bsz,
-                      1.0 / std::sqrt((double)n), sch->minibatch_round_f32 != 0, const_cast<double*>(gg.A), gg.lda);
-      }
-      megb200_iterate it{n, r, Vb[cur], r, lam.data(), eps};
-      megb200_eig_opts so = o;
-      so.seed = (uint64_t)t;
-      so.warm = warm;
-      so.warm_cols = warm_cols;
-      so.ld_warm = ld_warm;
-      so.warm_orthonormal = warm_orth ? 1 : 0;
-      megb200_step_result out{};
-      out.V_next = Vb[1 - cur];
+    };
+    auto end_step = [&](int64_t i) {
+      if (!ev.empty()) MEG_CUDA(cudaEventRecord(ev[i].second, s->stream));
+    };
+    auto result_for = [&](int64_t i, megb200_step_result& out) {
+      out = megb200_step_result{};
+      out.V_next = Vb[(i + 1) % 3];
       out.ld_next = r;
       out.lam_next = lam_next.data();
       out.y = y.data();
       out.mu = mu.data();
       out.residual_norms = res.data();
-      out.ritz_block = Wb[1 - wcur];
+      out.ritz_block = Wb[(i + 1) % 3];
       out.ld_ritz = 64;
-      step_core(s, &it, &gg, eta, eps_next, &so, &out);
-      if (!ev.empty()) MEG_CUDA(cudaEventRecord(ev[i].second, s->stream));
+    };
+    // commit step i: records, then the iterate / warm block move to slot (i + 1) % 3
+    auto commit = [&](int64_t i, const megb200_step_result& out, double eps_next) {
       if (rec) {
         if (rec->shift) rec->shift[i] = out.shift;
         if (rec->y) std::copy(y.begin(), y.end(), rec->y + i * (r + 1));
@@ -963,34 +1155,131 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
         if (rec->holds) rec->holds[i] = out.holds_cheap;
         if (rec->passes) rec->passes[i] = out.passes;
       }
-      cur = 1 - cur;
-      wcur = 1 - wcur;
       lam = lam_next;
       eps = eps_next;
-      warm = Wb[wcur];
+      warm = Wb[(i + 1) % 3];
       warm_cols = out.ritz_cols;
       ld_warm = 64;
       warm_orth = out.ritz_orth_err <= 1e-13;
+      last_orth = out.ritz_orth_err;
+    };
+    auto gradient_for = [&](int64_t i, const double* V) {
+      megb200_gradient gg = *g;
+      if (gg.kind == MEGB200_GRAD_FROBENIUS || gg.kind == MEGB200_GRAD_STOCHASTIC || gg.kind == MEGB200_GRAD_SAMPLED) {
+        gg.gV = V;
+        gg.g_r = r;
+        gg.g_ldv = r;
+        gg.g_lam = lam.data();
+        gg.g_eps = eps;
+      }
+      if (gg.kind == MEGB200_GRAD_STOCHASTIC) {
+        if (!gg.A) throw Error(MEGB200_ERR_PARAM, "stochastic run needs a minibatch buffer g->A");
+        fill_gaussian(L, n, (int)gg.bsz, stream_key(sch->minibatch_seed, 5), (uint64_t)(t0 + i) * n * gg.bsz,
+                      1.0 / std::sqrt((double)n), sch->minibatch_round_f32 != 0, const_cast<double*>(gg.A), gg.lda);
+      }
+      return gg;
+    };
+    // full (synchronous) step through step_core
+    auto full_step = [&](int64_t i) {
+      const int64_t t = t0 + i;
+      const double eta = eta_eval(*sch, t), eps_next = eps_eval(*sch, t + 1);
+      const double* V = Vb[i % 3];
+      megb200_gradient gg = gradient_for(i, V);
+      megb200_iterate it{n, r, V, r, lam.data(), eps};
+      megb200_eig_opts so = o;
+      so.seed = (uint64_t)t;
+      so.warm = warm;
+      so.warm_cols = warm_cols;
+      so.ld_warm = ld_warm;
+      so.warm_orthonormal = warm_orth ? 1 : 0;
+      megb200_step_result out;
+      result_for(i, out);
+      step_core(s, &it, &gg, eta, eps_next, &so, &out);
+      end_step(i);
+      commit(i, out, eps_next);
+    };
+    auto fast_ok = [&]() { return pipe && warm && warm_cols == sh.bw && warm_orth; };
+    FastStep fs[2];
+    int64_t i = 0;
+    bool pending = false;  // step i is enqueued as a fast step (fs[i & 1]) and not yet confirmed
+    while (i < T) {
+      if (!pending) {
+        begin_step(i);
+        if (!fast_ok()) {
+          full_step(i);
+          ++i;
+          continue;
+        }
+        // first fast step of a chain: coefficients from the host kept weights
+        const int64_t t = t0 + i;
+        const double* V = Vb[i % 3];
+        megb200_gradient gg = gradient_for(i, V);
+        megb200_iterate it{n, r, V, r, lam.data(), eps};
+        check_gradient(s, &gg);
+        StepOperator so = build_step_operator(s, &it, &gg, eta_eval(*sch, t));
+        fast_step_enqueue(s, so.op, r, sh, P0.tol, warm, ld_warm, eps_eval(*sch, t + 1), Wb[(i + 1) % 3], 64,
+                          Vb[(i + 1) % 3], r, hspec[i & 1], done[i & 1], fs[i & 1]);
+        end_step(i);
+        pending = true;
+      }
+      // speculate step i + 1 on step i's device outputs (V, Ritz block, kept weights in the pack)
+      bool spec = false;
+      if (i + 1 < T) {
+        const int64_t t1 = t0 + i + 1;
+        const double eps1 = eps_eval(*sch, t0 + i + 1);  // eps of iterate i + 1 = eps_next of step i
+        begin_step(i + 1);
+        const double* V1 = Vb[(i + 1) % 3];
+        const OpDev op1 = frob_merged_op(g, V1, r, n, r, eps1, eta_eval(*sch, t1), s->pack + s->pack_epi + (r + 1));
+        fast_step_enqueue(s, op1, r, sh, P0.tol, Wb[(i + 1) % 3], 64, eps_eval(*sch, t1 + 1), Wb[(i + 2) % 3], 64,
+                          Vb[(i + 2) % 3], r, hspec[(i + 1) & 1], done[(i + 1) & 1], fs[(i + 1) & 1]);
+        end_step(i + 1);
+        spec = true;
+      }
+      megb200_step_result out;
+      result_for(i, out);
+      const double eps_next = eps_eval(*sch, t0 + i + 1);
+      if (fast_step_confirm(s, fs[i & 1], &out)) {
+        commit(i, out, eps_next);
+        ++i;
+        bool lam_pos = true;
+        for (double v : lam) lam_pos = lam_pos && v > 0.0;
+        // the speculation assumed an orthonormal bw-column warm block and valid kept weights
+        pending = spec && fast_ok() && lam_pos;
+        if (spec && !pending) s->sync();  // discard the speculative step; it re-runs from its inputs
+        continue;
+      }
+      // step i did not converge in its first pass: drop the work enqueued after
+      // it and run it through the full solver from its (intact) inputs
+      s->sync();
+      full_step(i);
+      ++i;
+      pending = false;
     }
-    if (V_out) copy_block(L, n, r, Vb[cur], r, V_out, ld_out);
+    if (V_out) copy_block(L, n, r, Vb[T % 3], r, V_out, ld_out);
+    if (rec && rec->ritz_block) {
+      const int64_t wc = (T > 0) ? std::min<int64_t>(warm_cols, rec->ritz_cap) : 0;
+      if (T > 0 && wc > 0) copy_block(L, n, (int)wc, warm, ld_warm, rec->ritz_block, rec->ld_ritz);
+      rec->ritz_cols = wc;
+      rec->ritz_orth_err = (T > 0 && wc == warm_cols) ? last_orth : INFINITY;
+    }
     if (lam_out) std::copy(lam.begin(), lam.end(), lam_out);
     if (eps_out) *eps_out = eps;
     s->sync();
-    for (int64_t i = 0; i < (int64_t)ev.size(); ++i) {
+    for (int64_t k = 0; k < (int64_t)ev.size(); ++k) {
       float ms = 0.f, fl = 0.f;
-      if (i == 0) {
-        MEG_CUDA(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second));
+      if (k == 0) {
+        MEG_CUDA(cudaEventElapsedTime(&ms, ev[k].first, ev[k].second));
       } else {
-        MEG_CUDA(cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second));
-        MEG_CUDA(cudaEventElapsedTime(&fl, evf[i], ev[i].first));
+        MEG_CUDA(cudaEventElapsedTime(&ms, ev[k - 1].second, ev[k].second));
+        MEG_CUDA(cudaEventElapsedTime(&fl, evf[k], ev[k].first));
         ms -= fl;
       }
-      rec->step_ms[i] = ms;
+      rec->step_ms[k] = ms;
     }
-    for (int64_t i = 0; i < (int64_t)ev.size(); ++i) {
-      cudaEventDestroy(ev[i].first);
-      cudaEventDestroy(ev[i].second);
-      cudaEventDestroy(evf[i]);
+    for (int64_t k = 0; k < (int64_t)ev.size(); ++k) {
+      cudaEventDestroy(ev[k].first);
+      cudaEventDestroy(ev[k].second);
+      cudaEventDestroy(evf[k]);
     }
   });
 }
@@ -1044,32 +1333,7 @@ void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradie
   if (!run.converged) throw_lanczos(run, P.tol);
   // next iterate: V = top r Ritz vectors (in T); lam / certificate came from the fused epilogue
   copy_block(L, s->n, r, s->T, s->ldq, out->V_next, out->ld_next);
-  const double* hb = epi.host.data();
-  const double status = hb[2 * r + 1 + 6];
-  if (status == 4.0) throw Error(MEGB200_ERR_KEPT_MASS, "kept mass vanished despite max-shift");
-  if (status == 1.0) throw Error(MEGB200_ERR_PARAM, "certificate inputs invalid (partial trace <= 0 or lambda < 0)");
-  for (int k = 0; k < nreq; ++k) out->y[k] = hb[k];
-  for (int k = 0; k < r; ++k) out->lam_next[k] = hb[nreq + k];
-  if (out->mu)
-    for (int k = 0; k < nreq; ++k) out->mu[k] = run.theta[k];
-  const double* t = hb + 2 * r + 1;
-  out->lambda_r_plus_1 = t[0];
-  out->b_r_plus_1 = t[1];
-  out->shift = t[2];
-  out->lhs_cheap = t[3];
-  out->holds_cheap = t[4] != 0.0;
-  out->threshold = t[5];
-  const double* gram = hb + 2 * r + 8;
-  const int gr = epi.gr;
-  double ge = 0.0, gall = 0.0;
-  for (int i = 0; i < gr; ++i)
-    for (int j = 0; j < gr; ++j) {
-      const double e = fabs(gram[i * gr + j] - (i == j ? 1.0 : 0.0));
-      gall = std::max(gall, e);
-      if (i < r && j < r) ge = std::max(ge, e);
-    }
-  out->gram_err = ge;
-  out->ritz_orth_err = gall;
+  fill_step_result(epi.host.data(), epi.host.data() + 2 * r + 8, epi.gr, r, run.theta.data(), out);
   s->mark("epilogue");
   s->trace_collect();
 }
@@ -1265,6 +1529,7 @@ int megb200_trace_enable(megb200_solver* s, int32_t enable) {
     s->marks.clear();
     s->trace_next = 0;
     s->trace_acc.clear();
+    s->trace_stat.clear();
   });
 }
 
@@ -1276,6 +1541,11 @@ int megb200_trace_report(megb200_solver* s, char* buf, int64_t len) {
     for (auto& kv : s->trace_acc) {
       snprintf(line, sizeof line, "%-14s %10.2f us avg  x%lld\n", kv.first.c_str(),
                1e3 * kv.second.first / std::max<int64_t>(1, kv.second.second), (long long)kv.second.second);
+      out += line;
+    }
+    for (auto& kv : s->trace_stat) {
+      snprintf(line, sizeof line, "%-22s %8.2f avg  x%lld\n", kv.first.c_str(),
+               kv.second.first / std::max<int64_t>(1, kv.second.second), (long long)kv.second.second);
       out += line;
     }
     snprintf(buf, (size_t)len, "%s", out.c_str());

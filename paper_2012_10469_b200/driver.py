@@ -94,10 +94,16 @@ def run(
     rec.holds = holds.ctypes.data_as(_lib.c_int32_p)
     rec.passes = passes.ctypes.data_as(_lib.c_int32_p)
     v_out = torch.empty((n, r), dtype=torch.float64, device=runtime.device())
+    ritz = torch.empty((n, runtime.MAX_BLOCK), dtype=torch.float64, device=runtime.device())
+    rec.ritz_block = ritz.data_ptr()
+    rec.ld_ritz = ritz.stride(0)
+    rec.ritz_cap = ritz.shape[1]
     lam_out = np.zeros(r)
     eps_out = C.c_double()
     runtime.check(s.lib.megb200_meg_run(s.handle, C.byref(xs), C.byref(gs), C.byref(sc), int(t0), T, C.byref(opts),
                                         int(flush_bytes), v_out.data_ptr(), r, _lib.dptr(lam_out),
                                         C.byref(eps_out), C.byref(rec)))
-    x = LowRankIterate(n, r, v_out, lam_out, eps_out.value) if T > 0 else x0
+    # the final iterate carries the warm Ritz block, so a later run or step continues warm
+    x = (LowRankIterate(n, r, v_out, lam_out, eps_out.value, warm_block=ritz[:, : rec.ritz_cols],
+                        warm_orth_err=rec.ritz_orth_err) if T > 0 else x0)
     return RunResult(iterate=x, holds=holds.astype(bool), passes=passes, **out)

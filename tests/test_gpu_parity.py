@@ -278,3 +278,62 @@ def test_run_loop_equals_step_api(pb):
         x = step.iterate
         assert abs(step.shift - res.shift[t]) <= 1e-13 * abs(step.shift)
         assert np.max(np.abs(step.top_eigenvalues - res.y[t]) / res.y[t]) <= 1e-12
+
+
+def _run_arrays(res):
+    return {k: np.asarray(getattr(res, k)) for k in ("shift", "y", "lam", "eps", "lhs", "holds")}
+
+
+@pytest.mark.parametrize("poor_warm", [False, True])
+def test_pipelined_run_bit_identical(pb, monkeypatch, poor_warm):
+    """The pipelined run loop (step t+1 enqueued before step t is confirmed) gives
+    bit-identical results to the synchronous loop.  poor_warm starts from an
+    orthonormal but random warm block, so the first fast step misses the
+    tolerance: the speculative step is discarded and the step re-runs."""
+    import torch
+
+    from paper_2012_10469_b200 import driver
+
+    cfg = inputs.CONFIGS["cfg2"].scaled(1024, 16)
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    dev = pb.FrobeniusObjective(host.m)
+    warm = None
+    if poor_warm:
+        q, _ = np.linalg.qr(np.random.default_rng(5).standard_normal((x0.n, 18)))
+        warm = torch.from_numpy(q).cuda()
+
+    def go():
+        x = pb.LowRankIterate(x0.n, x0.r, x0.V, x0.lam, x0.eps, warm_block=warm, warm_orth_err=0.0)
+        return driver.run(x, dev, 16, svd_subspace=64, block=18)
+
+    monkeypatch.setenv("MEGB200_NO_PIPELINE", "1")
+    ref = go()
+    monkeypatch.setenv("MEGB200_NO_PIPELINE", "0")
+    got = go()
+    a, b = _run_arrays(ref), _run_arrays(got)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+    assert np.array_equal(ref.passes, got.passes)
+    if poor_warm:
+        assert got.passes[0] > 1, "the first step did not exercise the re-run path"
+    assert np.array_equal(ref.iterate.V, got.iterate.V)
+    assert np.array_equal(ref.iterate.lam, got.iterate.lam)
+
+
+def test_run_chaining_continues_warm(pb):
+    """run(T1) then run(T2) from its iterate (which carries the Ritz block) equals run(T1 + T2)."""
+    from paper_2012_10469_b200 import driver
+
+    cfg = inputs.CONFIGS["cfg2"].scaled(768, 10)
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    dev = pb.FrobeniusObjective(host.m)
+    whole = driver.run(pb.LowRankIterate(x0.n, x0.r, x0.V, x0.lam, x0.eps), dev, 10, svd_subspace=64, block=18)
+    first = driver.run(pb.LowRankIterate(x0.n, x0.r, x0.V, x0.lam, x0.eps), dev, 4, svd_subspace=64, block=18)
+    assert first.iterate.warm_block is not None and first.iterate.warm_block.shape[1] == 18
+    second = driver.run(first.iterate, dev, 6, t0=4, svd_subspace=64, block=18)
+    assert np.all(second.passes[:1] == whole.passes[4:5])
+    assert np.array_equal(np.concatenate([first.shift, second.shift]), whole.shift)
+    assert np.array_equal(np.concatenate([first.lam, second.lam]), whole.lam)
+    assert np.array_equal(second.iterate.V, whole.iterate.V)
