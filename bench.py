@@ -285,7 +285,10 @@ def run_device_arm(args, world, rank, local):
         x = step(x, t).iterate
         t += 1
     torch.cuda.synchronize()
-    Vh = x.V.copy()
+    # the caller's iterate lives in pinned host memory: each step uploads it and reads the next one back
+    Vh = torch.empty((w.n, w.r), dtype=torch.float64).pin_memory()
+    Vh.copy_(x.V_device)
+    Vn = torch.empty_like(Vh).pin_memory()
     lam, eps, warm, werr = x.lam.copy(), x.eps, x.warm_block, x.warm_orth_err
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K2)]
     h2d = w.n * w.r * 8 + w.r * 8
@@ -297,8 +300,9 @@ def run_device_arm(args, world, rank, local):
         ev2[i][0].record()
         xi = pb.LowRankIterate(w.n, w.r, Vh, lam, eps, warm_block=warm, warm_orth_err=werr)
         res = step(xi, t)
-        Vh = res.iterate.V  # device -> host read of the step's result
+        Vn.copy_(res.iterate.V_device, non_blocking=True)  # device -> pinned host read of the step's result
         ev2[i][1].record()
+        Vh, Vn = Vn, Vh
         lam, eps, warm, werr = res.iterate.lam, res.iterate.eps, res.iterate.warm_block, res.iterate.warm_orth_err
         t += 1
     torch.cuda.synchronize()

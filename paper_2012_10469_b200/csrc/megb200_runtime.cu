@@ -324,6 +324,8 @@ struct EpiSpec {
   double eps_next = 0.0;
   int gr = 0;                // out: order of the returned Ritz-block Gram
   std::vector<double> host;  // out: epilogue block (2r + 8 doubles) + Gram (gr x gr)
+  double* v_next = nullptr;  // in: V_next = first r Ritz vectors, written with the outputs
+  int64_t ld_next = 0;
 };
 
 // Block sizes of a solve: block width bw, basis limit mmax, thick-restart keep.
@@ -465,6 +467,11 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       double* pk = s->h_buf;
       const int gr = rr_readback(s, newcols, nreq, bw, epi, pk);
       const int rq = std::min(newcols, std::max(nreq, bw));
+      // outputs written speculatively before the wait: if this Rayleigh-Ritz
+      // converged nothing is left to launch after it (otherwise they are rewritten)
+      if (vec_out) copy_block(L, n, nreq, s->T, s->ldq, vec_out, ld_vec);
+      if (ritz_out) copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
+      if (epi && epi->v_next) copy_block(L, n, epi->r, s->T, s->ldq, epi->v_next, epi->ld_next);
       s->mark("rr+ritz");
       s->sync();
       s->mark("host_decide");
@@ -490,8 +497,6 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
           epi->host.insert(epi->host.end(), pk + s->pack_gram, pk + s->pack_gram + (int64_t)gr * gr);
           epi->gr = gr;
         }
-        if (vec_out) copy_block(L, n, nreq, s->T, s->ldq, vec_out, ld_vec);
-        if (ritz_out) copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
         if (ritz_cols_out) *ritz_cols_out = rq;
         return run;
       }
@@ -1324,15 +1329,37 @@ void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradie
   EpiSpec epi;
   epi.r = r;
   epi.eps_next = eps_next;
-  EigRun run = top_eigs(s, so.op, nreq, P, nullptr, 0, out->ritz_block, out->ld_ritz, &rc, &epi);
+  // outputs are written before convergence is known unless they alias an operand of the solve
+  // (an in-place V_next / Ritz block is then written after it)
+  const int64_t n = s->n;
+  auto overlaps = [n](const double* a, int64_t lda, int cols, const double* b, int64_t ldb, int bcols) {
+    if (!a || !b) return false;
+    const double* a1 = a + (n - 1) * lda + cols;
+    const double* b1 = b + (n - 1) * ldb + bcols;
+    return a < b1 && b < a1;
+  };
+  const bool v_alias = overlaps(out->V_next, out->ld_next, r, x->V, x->ldv, r) ||
+                       overlaps(out->V_next, out->ld_next, r, g->gV, g->g_ldv, (int)g->g_r);
+  const int ritz_cap = std::max(nreq, (int)s->max_block);
+  const bool w_alias = overlaps(out->ritz_block, out->ld_ritz, ritz_cap, x->V, x->ldv, r) ||
+                       overlaps(out->ritz_block, out->ld_ritz, ritz_cap, g->gV, g->g_ldv, (int)g->g_r);
+  if (!v_alias) {
+    epi.v_next = out->V_next;
+    epi.ld_next = out->ld_next;
+  }
+  double* ritz_dst = w_alias ? s->W : out->ritz_block;
+  const int64_t ld_ritz_dst = w_alias ? (int64_t)s->max_block : out->ld_ritz;
+  EigRun run = top_eigs(s, so.op, nreq, P, nullptr, 0, out->ritz_block ? ritz_dst : nullptr, ld_ritz_dst, &rc, &epi);
   out->ritz_cols = out->ritz_block ? rc : 0;
   out->passes = run.passes;
   out->restarts = run.restarts;
   if (out->residual_norms)
     for (int j = 0; j < nreq; ++j) out->residual_norms[j] = run.resid[j];
   if (!run.converged) throw_lanczos(run, P.tol);
-  // next iterate: V = top r Ritz vectors (in T); lam / certificate came from the fused epilogue
-  copy_block(L, s->n, r, s->T, s->ldq, out->V_next, out->ld_next);
+  // next iterate: V = top r Ritz vectors (written by top_eigs unless aliased); lam / certificate
+  // came from the fused epilogue
+  if (v_alias) copy_block(L, n, r, s->T, s->ldq, out->V_next, out->ld_next);
+  if (w_alias && out->ritz_block) copy_block(L, n, out->ritz_cols, s->W, s->max_block, out->ritz_block, out->ld_ritz);
   fill_step_result(epi.host.data(), epi.host.data() + 2 * r + 8, epi.gr, r, run.theta.data(), out);
   s->mark("epilogue");
   s->trace_collect();
