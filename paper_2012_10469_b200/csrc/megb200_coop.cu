@@ -16,7 +16,6 @@
 #include <algorithm>
 
 #include "megb200_internal.h"
-#include "megb200_jacobi.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -36,6 +35,13 @@ __device__ __forceinline__ void phase_mark(int slot) {
   (void)slot;
 #endif
 }
+
+}  // namespace megb200
+
+#define JACOBI_MARK(slot) phase_mark(slot)
+#include "megb200_jacobi.cuh"
+
+namespace megb200 {
 
 namespace {
 
@@ -365,21 +371,36 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
   }
   phase_mark(22);
   double* Es = sm;
+  double* Ls = sm + l * b;  // this chunk's rows of L (kRC x l)
   for (int idx = threadIdx.x; idx < l * b; idx += kCT) Es[idx] = Ews[idx];
-  __syncthreads();
-  for (int64_t idx = threadIdx.x; idx < (r1 - r0) * b; idx += kCT) {
-    const int64_t i = r0 + idx / b;
-    const int c = (int)(idx % b);
-    double pv[16];
+  for (int64_t rc = r0; rc < r1; rc += kRC) {
+    const int rows = (int)min((int64_t)kRC, r1 - rc);
+    __syncthreads();
+    // stage the chunk's L rows (independent coalesced loads) so the L E products read shared memory
+    for (int idx = threadIdx.x; idx < rows * l; idx += kCT) {
+      const int r = idx / l, k = idx - r * l;
+      Ls[idx] = Lf[(rc + r) * ldl + k];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < rows * b; idx += kCT) {
+      const int rr = idx / b, c = idx - rr * b;
+      const int64_t i = rc + rr;
+      double pv[16];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) pv[t] = t < S ? spart[(int64_t)t * n * b + i * b + c] : 0.0;
-    double s = 0.0;
+      for (int t = 0; t < 16; ++t) pv[t] = t < S ? spart[(int64_t)t * n * b + i * b + c] : 0.0;
+      double s = 0.0;
 #pragma unroll
-    for (int t = 0; t < 16; ++t) s += pv[t];
-    double v = scale * s + alpha * U[i * ldu + c];
-    const double* Lr = Lf + i * ldl;
-    for (int k = 0; k < l; ++k) v = fma(Lr[k], Es[k * b + c], v);
-    W[i * ldw + c] = v;
+      for (int t = 0; t < 16; ++t) s += pv[t];
+      const double* Lr = Ls + rr * l;
+      double v0 = scale * s + alpha * U[i * ldu + c], v1 = 0.0;
+      int k = 0;
+      for (; k + 1 < l; k += 2) {
+        v0 = fma(Lr[k], Es[k * b + c], v0);
+        v1 = fma(Lr[k + 1], Es[(k + 1) * b + c], v1);
+      }
+      if (k < l) v0 = fma(Lr[k], Es[k * b + c], v0);
+      W[i * ldw + c] = v0 + v1;
+    }
   }
   phase_mark(23);
   if (Hout) {
@@ -496,8 +517,8 @@ void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, 
                  double* Hout, int64_t ldh, LamCoef lc) {
   if (lc.lam && (l > kMaxLowrank || lc.lr > l)) throw Error(MEGB200_ERR_PARAM, "finish: coefficient width out of range");
   const int G = coop_grid(n, sm_count);
-  const size_t smem = std::max({(size_t)kRC * (l + b), (size_t)std::max(1, l * b), (size_t)kRC * (hp + b)}) *
-                      sizeof(double);
+  const size_t smem = std::max({(size_t)kRC * (l + b), (size_t)std::max(1, l * b) + (size_t)kRC * l,
+                                (size_t)kRC * (hp + b)}) * sizeof(double);
   const int J = pick_j(std::max(1, l * b));
   const int J2 = Hout ? pick_j(hp * b) : 1;
 #define MEG_FIN2(jj, j2)                                                                                        \
@@ -545,31 +566,54 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
   phase_mark(12);
   const int cols = m;
   double* Ss = sm;
-  double* red = sm + cols * rq;
+  double* Qs = sm + cols * rq;    // chunk rows of Q (kRC x cols)
+  double* As = Qs + kRC * cols;   // chunk rows of AQ
+  double* red = As + kRC * cols;  // kCT
   for (int idx = threadIdx.x; idx < cols * rq; idx += kCT) {
     const int k = idx / rq, c = idx - k * rq;
     Ss[idx] = S[k * m + c];
   }
-  __syncthreads();
   int64_t r0, r1;
   cta_rows(n, r0, r1);
   const int rpt = kCT / rq;
   const int c = threadIdx.x % rq;
   const int rofs = threadIdx.x / rq;
+  const double th = (rofs < rpt && c < nreq) ? theta[c] : 0.0;
   double sq = 0.0;
-  if (rofs < rpt) {
-    const double th = c < nreq ? theta[c] : 0.0;
-    for (int64_t r = r0 + rofs; r < r1; r += rpt) {
-      const double* qr = Q + r * ldq;
-      double x = 0.0;
-      for (int k = 0; k < cols; ++k) x = fma(qr[k], Ss[k * rq + c], x);
-      T[r * ldt + c] = x;
-      if (c < nreq) {
-        const double* ar = AQ + r * ldq;
-        double ax = 0.0;
-        for (int k = 0; k < cols; ++k) ax = fma(ar[k], Ss[k * rq + c], ax);
-        const double d = ax - th * x;
-        sq = fma(d, d, sq);
+  for (int64_t rc = r0; rc < r1; rc += kRC) {
+    const int rows = (int)min((int64_t)kRC, r1 - rc);
+    __syncthreads();
+    // stage the chunk's rows of Q and AQ with independent coalesced loads
+    for (int idx = threadIdx.x; idx < rows * cols; idx += kCT) {
+      const int r = idx / cols, k = idx - r * cols;
+      Qs[idx] = Q[(rc + r) * ldq + k];
+      As[idx] = AQ[(rc + r) * ldq + k];
+    }
+    __syncthreads();
+    if (rofs < rpt) {
+      for (int rr = rofs; rr < rows; rr += rpt) {
+        const double* qr = Qs + rr * cols;
+        double x0 = 0.0, x1 = 0.0;
+        int k = 0;
+        for (; k + 1 < cols; k += 2) {
+          x0 = fma(qr[k], Ss[k * rq + c], x0);
+          x1 = fma(qr[k + 1], Ss[(k + 1) * rq + c], x1);
+        }
+        if (k < cols) x0 = fma(qr[k], Ss[k * rq + c], x0);
+        const double x = x0 + x1;
+        T[(rc + rr) * ldt + c] = x;
+        if (c < nreq) {
+          const double* ar = As + rr * cols;
+          double a0 = 0.0, a1 = 0.0;
+          k = 0;
+          for (; k + 1 < cols; k += 2) {
+            a0 = fma(ar[k], Ss[k * rq + c], a0);
+            a1 = fma(ar[k + 1], Ss[(k + 1) * rq + c], a1);
+          }
+          if (k < cols) a0 = fma(ar[k], Ss[k * rq + c], a0);
+          const double d = (a0 + a1) - th * x;
+          sq = fma(d, d, sq);
+        }
       }
     }
   }
@@ -585,7 +629,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
   if (gr > 0) {
     __syncthreads();
     double acc[JG];
-    xty_rows<JG>(r0, r1, T, ldt, gr, T, ldt, gr, sm + cols * rq + kCT, acc);
+    xty_rows<JG>(r0, r1, T, ldt, gr, T, ldt, gr, red + kCT, acc);
     double* out = gpart + (int64_t)blockIdx.x * gr * gr;
 #pragma unroll
     for (int j = 0; j < JG; ++j) {
@@ -661,7 +705,7 @@ void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta
   const bool fused = m <= 48;
   if (!fused) rr_jacobi(L, H, ldh, m, theta, S, nullptr, 0, 0, nreq, nullptr, info);
   const size_t smem = std::max(fused ? (size_t)jacobi_smem_doubles(m) : (size_t)0,
-                               (size_t)(m * rq + kCT + kRC * 2 * std::max(gr, 1))) * sizeof(double);
+                               (size_t)(m * rq + 2 * kRC * m + kCT + kRC * 2 * std::max(gr, 1))) * sizeof(double);
   double* info_arg = fused ? info : nullptr;
   const int JG = pick_j(std::max(1, gr * gr));
 #define MEG_RR(jj)                                                                                              \

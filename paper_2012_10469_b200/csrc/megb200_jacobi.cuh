@@ -5,17 +5,50 @@
 // a round costs two __syncthreads; sweeps stop when off(H) <= 1e-15 ||H||_F or
 // stagnates.  Output: theta non-increasing (stable by index), S (m x m
 // row-major, column j = eigenvector j).
+//
+// Near-diagonal pre-step (m <= 64, off(H) <= 1e-3 ||H||_F -- the Rayleigh-Ritz
+// matrix of a warm-started step): all pair rotations at once to first order,
+// Y = I + X with X_ij = h_ij / (h_jj - h_ii) (pairs with |h_ij| > 0.1 |gap|
+// are left to the sweeps), orthonormalised by one Newton-Schulz step
+// S = Y (3I - Y^T Y) / 2 (orthogonal to O(|X|^4)), and H <- S^T H S, V <- V S.
+// Each pre-step takes off(H) to O(off^2 / gap); up to three run while they
+// keep converging, after which the sweeps (same rule, same outputs) usually
+// have nothing left to do, so a warm step's Rayleigh-Ritz costs a few
+// parallel m x m products instead of a sweep of m - 1 serialised rounds.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
+#ifndef JACOBI_MARK
+#define JACOBI_MARK(slot)
+#endif
+
 namespace megb200 {
 
 __host__ __device__ constexpr int jacobi_pad(int m) { return (m + 1) & ~1; }
 // shared-memory doubles needed by block_jacobi for size m
-__host__ __device__ constexpr int jacobi_smem_doubles(int m) { return 2 * jacobi_pad(m) * jacobi_pad(m) + 64 * 4 + 40; }
+__host__ __device__ constexpr int jacobi_base_doubles(int m) { return 2 * jacobi_pad(m) * jacobi_pad(m) + 64 * 4 + 40; }
+constexpr int kJacobiPreMax = 64;  // largest m with the near-diagonal pre-step (third m x m buffer)
+__host__ __device__ constexpr int jacobi_smem_doubles(int m) {
+  return jacobi_base_doubles(m) + (m <= kJacobiPreMax ? 3 * jacobi_pad(m) * jacobi_pad(m) : 0);
+}
+
+// sum_k A[ia + k * sa] * B[ib + k * sb] for k < len, four independent accumulators
+// (short dependent chains: these products are latency-bound on one SM)
+__device__ __forceinline__ double jdot(const double* A, int ia, int sa, const double* B, int ib, int sb, int len) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int k = 0;
+  for (; k + 3 < len; k += 4) {
+    a0 = fma(A[ia + k * sa], B[ib + k * sb], a0);
+    a1 = fma(A[ia + (k + 1) * sa], B[ib + (k + 1) * sb], a1);
+    a2 = fma(A[ia + (k + 2) * sa], B[ib + (k + 2) * sb], a2);
+    a3 = fma(A[ia + (k + 3) * sa], B[ib + (k + 3) * sb], a3);
+  }
+  for (; k < len; ++k) a0 = fma(A[ia + k * sa], B[ib + k * sb], a0);
+  return (a0 + a1) + (a2 + a3);
+}
 
 __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, int m, double* __restrict__ theta,
                                     double* __restrict__ Sout, double* sm, double* __restrict__ info) {
@@ -39,6 +72,7 @@ __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, 
     V[idx] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
+  JACOBI_MARK(40);
   auto block_sum = [&](double v) -> double {
     for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     __syncthreads();
@@ -61,6 +95,76 @@ __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, 
   const double fro2 = block_sum(local);
   const double stop2 = fro2 * 1e-30;  // off(H) <= 1e-15 ||H||_F
   double off2 = block_sum(loff), prev = INFINITY;
+  JACOBI_MARK(41);
+  double* Vs = V;  // accumulated rotations (pointer rotates through the scratch buffers)
+  for (int pre = 0; pre < 3 && m <= kJacobiPreMax && !(off2 <= stop2) && off2 <= 1e-6 * fro2 && off2 < 0.25 * prev;
+       ++pre) {
+    const int mm = mp * mp;
+    double* Y = sm + jacobi_base_doubles(m);
+    double* Tm = Y + mm;
+    double* Z = Tm + mm;
+    if (Vs != V) {  // Vs occupies one of the scratch buffers: use V's home as scratch instead
+      if (Vs == Y) Y = V;
+      else if (Vs == Tm) Tm = V;
+      else Z = V;
+    }
+    // Y = I + X
+#pragma unroll 1
+    for (int idx = t; idx < mm; idx += nth) {
+      const int i = idx / mp, j = idx - i * mp;
+      double y = 1.0;
+      if (i != j) {
+        const double h = H[idx], d = H[j * mp + j] - H[i * mp + i];
+        y = (h != 0.0 && fabs(h) <= 0.1 * fabs(d)) ? h / d : 0.0;
+      }
+      Y[idx] = y;
+    }
+    __syncthreads();
+    // Tm = (3I - Y^T Y) / 2
+#pragma unroll 1
+    for (int idx = t; idx < mm; idx += nth) {
+      const int i = idx / mp, j = idx - i * mp;
+      Tm[idx] = 0.5 * ((i == j ? 3.0 : 0.0) - jdot(Y, i, mp, Y, j, mp, mp));
+    }
+    __syncthreads();
+    // Z = S = Y Tm
+#pragma unroll 1
+    for (int idx = t; idx < mm; idx += nth) {
+      const int i = idx / mp, j = idx - i * mp;
+      Z[idx] = jdot(Y, i * mp, 1, Tm, j, mp, mp);
+    }
+    __syncthreads();
+    // Tm = H S;  Y = Vs S (the new accumulated rotations)
+#pragma unroll 1
+    for (int idx = t; idx < mm; idx += nth) {
+      const int i = idx / mp, j = idx - i * mp;
+      Tm[idx] = jdot(H, i * mp, 1, Z, j, mp, mp);
+      Y[idx] = jdot(Vs, i * mp, 1, Z, j, mp, mp);
+    }
+    __syncthreads();
+    Vs = Y;
+    // H <- S^T (H S), symmetric by construction (upper triangle mirrored)
+    double lo2 = 0.0;
+#pragma unroll 1
+    for (int idx = t; idx < mm; idx += nth) {
+      const int i = idx / mp, j = idx - i * mp;
+      if (i <= j) {
+        const double a = jdot(Z, i, mp, Tm, j, mp, mp);
+        H[i * mp + j] = a;
+        H[j * mp + i] = a;
+        if (i != j) lo2 += 2.0 * a * a;
+      }
+    }
+    prev = off2;
+    off2 = block_sum(lo2);  // its barriers also publish H
+    JACOBI_MARK(42 + pre);
+  }
+  if (Vs != V) {
+    for (int idx = t; idx < mp * mp; idx += nth) V[idx] = Vs[idx];
+    __syncthreads();
+  }
+  JACOBI_MARK(45);
+  prev = INFINITY;
   int sweep = 0;
   // fixed thread -> work mapping for the whole solve (no divisions in the rounds)
   const int rot_pair = t < half ? t : -1;
@@ -165,6 +269,7 @@ __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, 
       break;
     }
   }
+  JACOBI_MARK(46);
   for (int i = t; i < m; i += nth) {
     const double di = H[i * mp + i];
     int rank = 0;
@@ -180,6 +285,7 @@ __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, 
     info[1] = sqrt(off2);
     info[2] = sqrt(fro2);
   }
+  JACOBI_MARK(47);
 }
 
 // Single-warp variant for m <= 32: warp-synchronous rounds (only __syncwarp),

@@ -479,6 +479,24 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
         double inf[3];
         MEG_CUDA(cudaMemcpy(inf, s->info, sizeof inf, cudaMemcpyDeviceToHost));
         s->stat("jacobi_sweeps m=" + std::to_string(newcols), inf[0]);
+        // shape of the Rayleigh-Ritz matrix: off(H)/||H||, worst coupling/gap ratio
+        if (newcols <= 64) {
+          std::vector<double> h((size_t)newcols * s->cap);
+          MEG_CUDA(cudaMemcpy(h.data(), s->H, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+          double f2 = 0.0, o2 = 0.0, worst = 0.0;
+          for (int i = 0; i < newcols; ++i)
+            for (int j = 0; j < newcols; ++j) {
+              const double v = (i <= j) ? h[(size_t)i * s->cap + j] : h[(size_t)j * s->cap + i];
+              f2 += v * v;
+              if (i != j) {
+                o2 += v * v;
+                const double gap = fabs(h[(size_t)i * s->cap + i] - h[(size_t)j * s->cap + j]);
+                worst = std::max(worst, fabs(v) / std::max(gap, 1e-300));
+              }
+            }
+          s->stat("rr_off_rel_log10 m=" + std::to_string(newcols), 0.5 * log10(std::max(o2, 1e-300) / f2));
+          s->stat("rr_coupling/gap_max_log10", log10(std::max(worst, 1e-300)));
+        }
       }
       const RRDecision dec = rr_decide(s, pk, newcols, nreq, tol);
       scale = dec.scale;

@@ -28,7 +28,9 @@ buf = (C.c_ulonglong * 64)()
 names = {1: "chol: gram partial", 2: "chol: sync1", 3: "chol: reduce+sync2", 4: "chol: cholesky(CTA0)",
          5: "chol: sync3", 6: "chol: apply Rinv", 11: "rr: jacobi(CTA0)", 12: "rr: sync1", 13: "rr: ritz+partials",
          14: "rr: sync2", 15: "rr: reduce", 21: "fin: LtU partial+sync", 22: "fin: reduce E+sync",
-         23: "fin: rows W", 24: "fin: QtW partial", 25: "fin: sync", 26: "fin: reduce H"}
+         23: "fin: rows W", 24: "fin: QtW partial", 25: "fin: sync", 26: "fin: reduce H",
+         40: "jac: load H", 41: "jac: norms", 42: "jac: pre 1", 43: "jac: pre 2", 44: "jac: pre 3",
+         45: "jac: (pre end)", 46: "jac: sweeps", 47: "jac: sort+store"}
 acc = {k: 0.0 for k in names}
 K = 0
 for t in range(80):
@@ -40,8 +42,9 @@ for t in range(80):
         K += 1
         v = list(buf)
         for k in names:
-            base = 0 if k < 10 else (10 if k < 20 else 20)
+            base = 0 if k < 10 else (10 if k < 20 else (20 if k < 40 else 10))
             prev = k - 1 if k - 1 >= base else base
             acc[k] += (v[k] - v[prev]) / 1e3
 for k, nm in names.items():
     print(f"{nm:24s} {acc[k] / K:9.2f} us")
+print("(jac rows are cumulative from the rr kernel start; pre rows are 0 when not run)")
