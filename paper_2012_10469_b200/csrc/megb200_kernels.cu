@@ -479,22 +479,42 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
 // U is staged as KC x (8 NT) with the columns beyond b zero-filled by TMA.
 constexpr int kMmaRows = 128;
 
-template <int NT>
+// U tile width in shared memory: >= the 8 NT + TAIL columns read, and = 2 (mod 8) so
+// the B-fragment rows k, k+2, k+4, k+6 of a k group fall in disjoint bank quarters
+template <int NT, int TAIL>
+__host__ __device__ constexpr int mma_bnp() {
+  return ((8 * NT + TAIL - 2 + 7) / 8) * 8 + 2;
+}
+
+template <int NT, int TAIL>
 constexpr size_t mma_smem_bytes() {
-  return 1024 + (size_t)kPipeStages * kPipeKC * kMmaRows * 8 + (size_t)kPipeStages * kPipeKC * 8 * NT * 8 +
+  return 1024 + (size_t)kPipeStages * kPipeKC * kMmaRows * 8 + (size_t)kPipeStages * kPipeKC * mma_bnp<NT, TAIL>() * 8 +
          2 * kPipeStages * 8;
 }
 
-template <int NT>
+// Columns [0, 8 NT) of the block go through DMMA (tensor pipe); the TAIL (< 8)
+// columns after them through DFMA on the FP64 pipe, which runs concurrently --
+// so k = 18 costs 2 DMMA n-tiles + 2 DFMA columns instead of 3 padded n-tiles.
+template <int NT, int TAIL>
 __global__ void __launch_bounds__(kPipeThreads, 1)
     k_dense_pass_mma(const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmU, int64_t n,
-                     int b, double* __restrict__ part, int tiles, int64_t kslice, int items) {
+                     int b, double* __restrict__ part, int tiles, int kch, int smax) {
+  // Stream-K: the (row tile, 32-row k chunk) space, tile-major, is cut into
+  // gridDim.x contiguous ranges of equal length (+-1 chunk), so every CTA
+  // streams the same number of operand bytes.  A CTA flushes one partial per
+  // tile segment it covers, into slot (its index - the index of the first CTA
+  // on that tile); the CTA that closes a tile zero-fills the tile's unused
+  // slots, so the epilogue sums exactly smax slots per row.
+  const int64_t utot = (int64_t)tiles * kch;
+  const int64_t ua = (int64_t)blockIdx.x * utot / gridDim.x, ub = (int64_t)(blockIdx.x + 1) * utot / gridDim.x;
   // Operand stage = 8 TMA boxes of 16 (i) x 32 (k) doubles with the 128-byte
   // swizzle (16-byte chunk index XOR row & 7), 4 KiB each; consumer warp w
-  // reads box w.  Each 8-row k group feeds two MMAs with k permuted as
-  // {0,1,4,5} / {2,3,6,7}: with the swizzle (operand) and the 192-byte U row
-  // stride, both fragment loads hit the 2-wavefront minimum (no bank conflicts).
-  constexpr int BNP = 8 * NT;
+  // reads box w.  Each 8-row k group feeds two MMAs, lane quad tq taking k rows
+  // {2 tq} / {2 tq + 1}: under the swizzle the four rows of a half-warp land in
+  // disjoint chunk pairs (A), and with a U row stride of 2 (mod 8) doubles in
+  // disjoint bank quarters (B) -- both fragment loads at the 2-wavefront minimum.
+  constexpr int BNP = mma_bnp<NT, TAIL>();
+  constexpr int TL = TAIL > 0 ? TAIL : 1;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* base = smem + ((1024 - ((uintptr_t)smem & 1023)) & 1023);
   double* Ms = reinterpret_cast<double*>(base);                      // stages x 8 boxes x 512 doubles
@@ -517,10 +537,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
       const uint32_t stage_bytes = (uint32_t)(kPipeKC * kMmaRows * 8 + kPipeKC * BNP * 8);
       int st = 0;
       uint32_t ph = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const int slice = item / tiles, tile = item - slice * tiles;
-        const int64_t kbeg = (int64_t)slice * kslice, kend = min(n, kbeg + kslice);
-        for (int64_t kc = kbeg; kc < kend; kc += kPipeKC) {
+      for (int64_t u = ua; u < ub; ++u) {
+        const int tile = (int)(u / kch);
+        const int64_t kc = (u - (int64_t)tile * kch) * kPipeKC;
+        {
           pipe::bar_wait(empty + st, ph ^ 1u);
           pipe::bar_arrive_tx(full + st, stage_bytes);
           double* mst = Ms + (size_t)st * kPipeKC * kMmaRows;
@@ -538,24 +558,37 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
     return;
   }
   const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
-  const int kperm = (tq & 1) + 4 * (tq >> 1);  // {0,1,4,5}; +2 for the second MMA of a k group
+  const int kperm = 2 * tq;  // {0,2,4,6}; +1 for the second MMA of a k group
   int st = 0;
   uint32_t ph = 0;
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
-    const int slice = item / tiles, tile = item - slice * tiles;
+  for (int64_t u = ua; u < ub;) {
+    const int tile = (int)(u / kch);
     const int64_t i0 = (int64_t)tile * kMmaRows;
-    const int64_t kbeg = (int64_t)slice * kslice, kend = min(n, kbeg + kslice);
-    double acc[2][NT][2];
+    const int64_t uend = min(ub, (int64_t)(tile + 1) * kch);
+    const bool closes = uend == (int64_t)(tile + 1) * kch;
+    // first CTA on this tile: the largest c with c * utot / G <= tile * kch
+    const int64_t x = (int64_t)tile * kch;
+    const int cfirst = (int)(((x + 1) * gridDim.x + utot - 1) / utot) - 1;
+    const int slot = (int)blockIdx.x - cfirst;
+    // two accumulator sets (even / odd k steps): dependent DMMAs on one accumulator
+    // are 2 * 2 * NT instructions apart, which covers the DMMA latency
+    double acc[2][2][NT][2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int ps = 0; ps < 2; ++ps)
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    for (int64_t kc = kbeg; kc < kend; kc += kPipeKC) {
-      const int nk = (int)min((int64_t)kPipeKC, kend - kc);  // rows past kend belong to the next slice
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[ps][mt][nt][0] = acc[ps][mt][nt][1] = 0.0;
+    double tl[2][TL];  // DFMA tail: rows g / 8+g, this lane's k subset
+#pragma unroll
+    for (int tc = 0; tc < TL; ++tc) tl[0][tc] = tl[1][tc] = 0.0;
+    for (; u < uend; ++u) {
+      const int64_t kc = (u - (int64_t)tile * kch) * kPipeKC;
+      const int nk = (int)min((int64_t)kPipeKC, n - kc);  // the last chunk of a row may be short
       pipe::bar_wait(full + st, ph);
       const char* box = reinterpret_cast<const char*>(Ms + (size_t)st * kPipeKC * kMmaRows) + warp * 4096;
       const double* us = Us + (size_t)st * kPipeKC * BNP;
-      auto mma_k = [&](int k) {  // one m8n8k4 step over k rows {k + kperm}
+      auto mma_k = [&](int k, double (&ac)[2][NT][2]) {  // one m8n8k4 step over k rows {k + kperm}
         const int kk = k + kperm;
         const bool valid = kk < nk;
         const int sw = kk & 7;
@@ -568,17 +601,23 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const double bv = valid ? us[kk * BNP + nt * 8 + g] : 0.0;
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(acc[0][nt][0]), "+d"(acc[0][nt][1]) : "d"(a0), "d"(bv));
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(acc[1][nt][0]), "+d"(acc[1][nt][1]) : "d"(a1), "d"(bv));
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(ac[0][nt][0]), "+d"(ac[0][nt][1]) : "d"(a0), "d"(bv));
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(ac[1][nt][0]), "+d"(ac[1][nt][1]) : "d"(a1), "d"(bv));
+        }
+#pragma unroll
+        for (int tc = 0; tc < TAIL; ++tc) {
+          const double bt = valid ? us[kk * BNP + 8 * NT + tc] : 0.0;
+          tl[0][tc] = fma(a0, bt, tl[0][tc]);
+          tl[1][tc] = fma(a1, bt, tl[1][tc]);
         }
       };
 #pragma unroll
       for (int k8 = 0; k8 < kPipeKC; k8 += 8) {
         if (k8 < nk) {
-          mma_k(k8);
-          mma_k(k8 + 2);
+          mma_k(k8, acc[0]);
+          mma_k(k8 + 1, acc[1]);
         }
       }
       __syncwarp();
@@ -589,7 +628,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
       }
     }
     // C fragment: row g, columns 2*tq, 2*tq+1 of each 8x8 tile
-    double* out = part + (int64_t)slice * n * b;
+    double* out = part + (int64_t)slot * n * b;
     const int rbase = warp * 16;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
@@ -598,8 +637,30 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int c = nt * 8 + 2 * tq;
-          if (c < b) out[row * b + c] = acc[mt][nt][0];
-          if (c + 1 < b) out[row * b + c + 1] = acc[mt][nt][1];
+          if (c < b) out[row * b + c] = acc[0][mt][nt][0] + acc[1][mt][nt][0];
+          if (c + 1 < b) out[row * b + c + 1] = acc[0][mt][nt][1] + acc[1][mt][nt][1];
+        }
+      }
+    }
+    // DFMA tail: sum the four k-subset lanes (tq) of each row, fixed xor order
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+      for (int tc = 0; tc < TAIL; ++tc) {
+        double v = tl[mt][tc];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        const int64_t row = i0 + rbase + mt * 8 + g;
+        if (tq == 0 && row < n) out[row * b + 8 * NT + tc] = v;
+      }
+    }
+    if (closes) {
+      // zero the tile's slots no CTA covers (rows of this warp)
+      for (int sl = slot + 1; sl < smax; ++sl) {
+        double* z = part + (int64_t)sl * n * b;
+        for (int idx = lane; idx < 16 * b; idx += 32) {
+          const int64_t row = i0 + rbase + idx / b;
+          if (row < n) z[row * b + idx % b] = 0.0;
         }
       }
     }
@@ -1229,19 +1290,21 @@ void dispatch_pipe(const Launch& L, const T* M, int64_t ldm, int64_t n, const do
   }
 }
 
-template <int NT>
+template <int NT, int TAIL>
 void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
-                     double* part, int tiles, int64_t kslice, int items, int grid) {
-  constexpr size_t smem = mma_smem_bytes<NT>();
+                     double* part, int tiles, int kch, int smax, int grid) {
+  constexpr size_t smem = mma_smem_bytes<NT, TAIL>();
   static bool attr = false;
   if (!attr) {
-    MEG_CUDA(cudaFuncSetAttribute(k_dense_pass_mma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MEG_CUDA(cudaFuncSetAttribute(k_dense_pass_mma<NT, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     attr = true;
   }
   const CUtensorMap tmM =
       make_map(M, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, n, n, ldm, 16, kPipeKC, CU_TENSOR_MAP_SWIZZLE_128B);
-  const CUtensorMap tmU = make_map(U, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, b, n, ldu, (uint32_t)(8 * NT), kPipeKC);
-  k_dense_pass_mma<NT><<<grid, kPipeThreads, smem, L.stream>>>(tmM, tmU, n, b, part, tiles, kslice, items);
+  const CUtensorMap tmU =
+      make_map(U, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, b, n, ldu, (uint32_t)mma_bnp<NT, TAIL>(), kPipeKC);
+  k_dense_pass_mma<NT, TAIL><<<grid, kPipeThreads, smem, L.stream>>>(tmM, tmU, n, b, part, tiles, kch, smax);
   MEG_LAUNCHED();
   ++*L.counter;
 }
@@ -1271,21 +1334,43 @@ int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, 
     const bool aligned = b % 2 == 0 && b <= 32 && ldu % 2 == 0 && ((uintptr_t)U % 16 == 0) &&
                          (ldm * es) % 16 == 0 && ((uintptr_t)M % 16 == 0) && (n * es) % 16 == 0;
     if (aligned && dtype == MEGB200_F64 && getenv("MEGB200_NO_DMMA") == nullptr) {
+      // stream-K over (row tile, k chunk): one CTA per SM, equal chunk counts; the grid
+      // shrinks until every tile is covered by at most part_cap_slices CTAs
       const int tiles = cdiv(n, kMmaRows);
-      const int s_max = std::max(1, (int)std::min<int64_t>(part_cap_slices, 16));
-      int S = choose_slices(tiles, n, sm_count, 1, s_max);
-      int64_t kslice = (int64_t)cdiv(cdiv(n, S), kPipeKC) * kPipeKC;
-      S = cdiv(n, kslice);
-      const int items = tiles * S;
-      const int grid = std::min(items, sm_count);
-      const double* m = static_cast<const double*>(M);
-      switch ((b + 7) / 8) {
-        case 1: launch_pipe_mma<1>(L, m, ldm, n, U, ldu, b, part, tiles, kslice, items, grid); break;
-        case 2: launch_pipe_mma<2>(L, m, ldm, n, U, ldu, b, part, tiles, kslice, items, grid); break;
-        case 3: launch_pipe_mma<3>(L, m, ldm, n, U, ldu, b, part, tiles, kslice, items, grid); break;
-        default: launch_pipe_mma<4>(L, m, ldm, n, U, ldu, b, part, tiles, kslice, items, grid); break;
+      const int kch = cdiv(n, kPipeKC);
+      const int64_t utot = (int64_t)tiles * kch;
+      const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(part_cap_slices, 16));
+      int grid = (int)std::min<int64_t>(sm_count, utot);
+      int smax = 1;
+      for (;;) {
+        auto cfirst = [&](int64_t x) { return (int)(((x + 1) * grid + utot - 1) / utot) - 1; };
+        smax = 1;
+        for (int t = 0; t < tiles; ++t)
+          smax = std::max(smax, cfirst((int64_t)(t + 1) * kch - 1) - cfirst((int64_t)t * kch) + 1);
+        if (smax <= cap || grid == 1) break;
+        grid = std::max(1, grid * cap / (smax + 1));
       }
-      return S;
+      const double* m = static_cast<const double*>(M);
+      // DMMA n-tiles for the multiple-of-8 head of the block, DFMA for the (even) rest
+#define MEG_MMA(nt, tail) launch_pipe_mma<nt, tail>(L, m, ldm, n, U, ldu, b, part, tiles, kch, smax, grid)
+      switch (b < 8 ? 0 : b) {
+        case 0: MEG_MMA(1, 0); break;
+        case 8: MEG_MMA(1, 0); break;
+        case 10: MEG_MMA(1, 2); break;
+        case 12: MEG_MMA(1, 4); break;
+        case 14: MEG_MMA(1, 6); break;
+        case 16: MEG_MMA(2, 0); break;
+        case 18: MEG_MMA(2, 2); break;
+        case 20: MEG_MMA(2, 4); break;
+        case 22: MEG_MMA(2, 6); break;
+        case 24: MEG_MMA(3, 0); break;
+        case 26: MEG_MMA(3, 2); break;
+        case 28: MEG_MMA(3, 4); break;
+        case 30: MEG_MMA(3, 6); break;
+        default: MEG_MMA(4, 0); break;
+      }
+#undef MEG_MMA
+      return smax;
     }
     if (aligned) {
       const int BM = dtype == MEGB200_F64 ? 64 : 128;
