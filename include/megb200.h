@@ -288,12 +288,12 @@ int megb200_gen_gaussian(megb200_solver* s, uint64_t seed, int32_t stream, uint6
 /* max |V^T V - I| of an n x r block (LowRankIterate validation, meg.py:69-71). */
 int megb200_gram_error(megb200_solver* s, const double* V, int64_t ldv, int32_t r, double* err);
 
-/* Live pass profiling (bench.py roofline): when enabled, every streamed operator
- * pass (dense or CSR product + epilogue) is bracketed by CUDA events on the
- * solver stream.  read() synchronises, returns the summed pass time (ms), the
- * number of passes and their algorithmic bytes (operand + U read + W write),
- * and resets the counters. */
-int megb200_profile_enable(megb200_solver* s, int32_t enable);
+/* Live pass profiling (bench.py roofline): when enabled, every k-th streamed
+ * operand pass kernel (dense or CSR product) is bracketed by CUDA events on the
+ * solver stream.  read() synchronises, returns the summed time (ms) of the
+ * bracketed passes, their number and their algorithmic bytes (operand + U read
+ * + partial write), and resets the counters. */
+int megb200_profile_enable(megb200_solver* s, int32_t enable); /* enable = k > 0: every k-th pass; 0: off */
 int megb200_profile_read(megb200_solver* s, double* pass_ms, int64_t* passes, double* bytes);
 
 /* Phase tracer (diagnostics): CUDA events at solver phase boundaries; the

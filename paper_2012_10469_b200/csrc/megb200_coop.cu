@@ -554,7 +554,8 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
                                                    const double* __restrict__ AQ, int64_t ldq, int rq, int nreq,
                                                    double* __restrict__ T, int64_t ldt, double* __restrict__ resid,
                                                    double* __restrict__ part, int gr, double* __restrict__ Gout,
-                                                   double eps_next, double* __restrict__ epi) {
+                                                   double eps_next, double* __restrict__ epi,
+                                                   double* __restrict__ V2, int64_t ld2, int r2) {
   extern __shared__ double sm[];
   cg::grid_group grid = cg::this_grid();
   phase_mark(10);
@@ -602,6 +603,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
         if (k < cols) x0 = fma(qr[k], Ss[k * rq + c], x0);
         const double x = x0 + x1;
         T[(rc + rr) * ldt + c] = x;
+        if (c < r2) V2[(rc + rr) * ld2 + c] = x;
         if (c < nreq) {
           const double* ar = As + rr * cols;
           double a0 = 0.0, a1 = 0.0;
@@ -699,7 +701,9 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
 
 void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,
              const double* Q, const double* AQ, int64_t ldq, int rq, int nreq, double* T, int64_t ldt, double* resid,
-             double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi) {
+             double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi, double* V2, int64_t ld2,
+             int r2) {
+  if (!V2) r2 = 0;
   if (nreq > 64 || rq > 64) throw Error(MEGB200_ERR_PARAM, "rr: at most 64 Ritz vectors");
   const int G = coop_grid(n, sm_count);
   const bool fused = m <= 48;
@@ -713,7 +717,7 @@ void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta
     static bool a = false;                                                                                      \
     if (!a) { raise_smem(k_coop_rr<jj>, 215 * 1024); a = true; }                                                \
     coop_launch(L, k_coop_rr<jj>, G, smem, H, ldh, m, theta, S, info_arg, n, Q, AQ, ldq, rq, nreq, T, ldt, resid, \
-                part, gr, Gout, eps_next, epi);                                                                 \
+                part, gr, Gout, eps_next, epi, V2, ld2, r2);                                                    \
   }
   MEG_J_DISPATCH(JG, MEG_RR)
 #undef MEG_RR

@@ -128,9 +128,11 @@ void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, 
                  int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
                  int64_t ldw, double* Ews, double* part, int sm_count, const double* Qh = nullptr, int64_t ldq = 0,
                  int hp = 0, double* Hout = nullptr, int64_t ldh = 0, LamCoef lc = LamCoef());
-// Jacobi RR + Ritz block + residuals (+ Gram of the first gr Ritz vectors, + MEG epilogue into epi)
+// Jacobi RR + Ritz block + residuals (+ Gram of the first gr Ritz vectors, + MEG epilogue into epi);
+// the first r2 Ritz vectors are also written to V2
 void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,
              const double* Q, const double* AQ, int64_t ldq, int rq, int nreq, double* T, int64_t ldt, double* resid,
-             double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi);
+             double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi, double* V2 = nullptr,
+             int64_t ld2 = 0, int r2 = 0);
 
 }  // namespace megb200

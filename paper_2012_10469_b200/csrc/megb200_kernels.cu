@@ -307,6 +307,20 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int x,
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       ::"r"(su32(dst)), "l"(map), "r"(x), "r"(y), "r"(su32(b)) : "memory");
 }
+// streaming variant: the operand is read once per pass, so its lines are marked
+// evict-first in L2 (they must not displace the small, reused blocks)
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_2d_stream(void* dst, const CUtensorMap* map, int x, int y, uint64_t* b,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(su32(dst)), "l"(map), "r"(x), "r"(y), "r"(su32(b)), "l"(policy) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(b)) : "memory");
@@ -356,6 +370,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
   if (warp == kPipeConsumers) {
     // ---------------- producer warp: one elected lane issues two 2D TMA tiles per stage
     if (lane == 0) {
+      const uint64_t pol = pipe::evict_first_policy();
       const uint32_t stage_bytes = (uint32_t)(kPipeKC * BM * sizeof(T) + kPipeKC * b * 8);
       int st = 0;
       uint32_t ph = 0;
@@ -365,7 +380,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
         for (int64_t kc = kbeg; kc < kend; kc += kPipeKC) {
           pipe::bar_wait(empty + st, ph ^ 1u);
           pipe::bar_arrive_tx(full + st, stage_bytes);
-          pipe::tma_2d(Ms + (size_t)st * kPipeKC * BM, &tmM, tile * BM, (int)kc, full + st);
+          pipe::tma_2d_stream(Ms + (size_t)st * kPipeKC * BM, &tmM, tile * BM, (int)kc, full + st, pol);
           pipe::tma_2d(Us + (size_t)st * kPipeKC * BN, &tmU, 0, (int)kc, full + st);
           if (++st == kPipeStages) {
             st = 0;
@@ -532,9 +547,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
   }
   __syncthreads();
+  // launched programmatically dependent on the previous kernel: everything above
+  // overlapped its tail; U and the partial buffer are touched only after it completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == kPipeConsumers) {
     if (lane == 0) {
       const uint32_t stage_bytes = (uint32_t)(kPipeKC * kMmaRows * 8 + kPipeKC * BNP * 8);
+      const uint64_t pol = pipe::evict_first_policy();
       int st = 0;
       uint32_t ph = 0;
       for (int64_t u = ua; u < ub; ++u) {
@@ -546,7 +565,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
           double* mst = Ms + (size_t)st * kPipeKC * kMmaRows;
 #pragma unroll
           for (int bx = 0; bx < kMmaRows / 16; ++bx)
-            pipe::tma_2d(mst + bx * 16 * kPipeKC, &tmM, tile * kMmaRows + 16 * bx, (int)kc, full + st);
+            pipe::tma_2d_stream(mst + bx * 16 * kPipeKC, &tmM, tile * kMmaRows + 16 * bx, (int)kc, full + st, pol);
           pipe::tma_2d(Us + (size_t)st * kPipeKC * BNP, &tmU, 0, (int)kc, full + st);
           if (++st == kPipeStages) {
             st = 0;
@@ -980,6 +999,9 @@ __global__ void __launch_bounds__(256) k_resid_partial(int64_t n, const double* 
 
 __global__ void k_copy_block(int64_t n, int q, const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
                              int64_t ldd) {
+  // let a programmatically dependent launch (the operand pass) start its prologue now;
+  // it waits for this grid's completion before touching memory
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * q) return;
   const int64_t i = idx / q;
@@ -1304,7 +1326,19 @@ void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, c
       make_map(M, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, n, n, ldm, 16, kPipeKC, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap tmU =
       make_map(U, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, b, n, ldu, (uint32_t)mma_bnp<NT, TAIL>(), kPipeKC);
-  k_dense_pass_mma<NT, TAIL><<<grid, kPipeThreads, smem, L.stream>>>(tmM, tmU, n, b, part, tiles, kch, smax);
+  // programmatic dependent launch: the CTA prologue (shared memory, mbarriers,
+  // tensor-map prefetch) overlaps the preceding kernel
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kPipeThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = L.stream;
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL>, tmM, tmU, n, b, part, tiles, kch, smax));
   MEG_LAUNCHED();
   ++*L.counter;
 }

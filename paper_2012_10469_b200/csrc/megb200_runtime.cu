@@ -74,7 +74,8 @@ struct megb200_solver {
   void* flush_buf = nullptr;
   uint64_t flush_len = 0;
   // live pass profiling
-  bool prof = false;
+  int prof = 0;              // profile every prof-th streamed pass (0 = off)
+  int64_t prof_seen = 0;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, int>> ev_pending;
   int ev_next = 0;
@@ -195,7 +196,7 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
   const bool streamed = (op.kind == MEGB200_OP_DENSE || op.kind == MEGB200_OP_CSR) && op.scale != 0.0;
   // live profiling brackets the streamed operand kernel only (the roofline's dominant kernel)
   int ev0 = -1;
-  if (s->prof && streamed) {
+  if (s->prof > 0 && streamed && (s->prof_seen++ % s->prof) == 0) {
     ev0 = s->ev_next;
     MEG_CUDA(cudaEventRecord(s->next_event(), s->stream));
   }
@@ -386,13 +387,18 @@ void block_pass(megb200_solver* s, const OpDev& op, int cols, int cur) {
 // from the cached images (linalg.py:205-211) (+ speculative step epilogue and
 // the Ritz-block Gram) in one launch, then one asynchronous read-back of the
 // pack [theta | resid | epilogue | Gram] into dst (pinned).  Returns the Gram order.
-int rr_readback(megb200_solver* s, int newcols, int nreq, int bw, const EpiSpec* epi, double* dst) {
+int rr_readback(megb200_solver* s, int newcols, int nreq, int bw, const EpiSpec* epi, double* dst,
+                double* tdst = nullptr, int64_t ldt = 0, double* v2 = nullptr, int64_t ld2 = 0, int r2 = 0) {
   Launch L = s->launch();
   const int rq = std::min(newcols, std::max(nreq, bw));
   const int gr = epi ? rq : 0;  // Gram of the whole Ritz block (V_next = its first r columns)
-  coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, s->n, s->Q, s->AQ, s->ldq, rq, nreq, s->T, s->ldq,
+  if (!tdst) {
+    tdst = s->T;
+    ldt = s->ldq;
+  }
+  coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, s->n, s->Q, s->AQ, s->ldq, rq, nreq, tdst, ldt,
           s->resid, s->red, s->sm_count, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
-          epi ? s->pack + s->pack_epi : nullptr);
+          epi ? s->pack + s->pack_epi : nullptr, v2, ld2, r2);
   s->d2h(dst, s->pack, s->pack_gram + (int64_t)gr * gr);
   return gr;
 }
@@ -465,13 +471,13 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
     const bool do_rr = (cols == 0) || full || (run.passes >= max_passes);
     if (do_rr) {
       double* pk = s->h_buf;
-      const int gr = rr_readback(s, newcols, nreq, bw, epi, pk);
-      const int rq = std::min(newcols, std::max(nreq, bw));
-      // outputs written speculatively before the wait: if this Rayleigh-Ritz
+      // outputs written by the Rayleigh-Ritz launch itself, before the wait: if it
       // converged nothing is left to launch after it (otherwise they are rewritten)
-      if (vec_out) copy_block(L, n, nreq, s->T, s->ldq, vec_out, ld_vec);
-      if (ritz_out) copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
-      if (epi && epi->v_next) copy_block(L, n, epi->r, s->T, s->ldq, epi->v_next, epi->ld_next);
+      double* v2 = vec_out ? vec_out : (epi ? epi->v_next : nullptr);
+      const int64_t ld2 = vec_out ? ld_vec : (epi ? epi->ld_next : 0);
+      const int r2 = vec_out ? nreq : (epi ? epi->r : 0);
+      const int gr = rr_readback(s, newcols, nreq, bw, epi, pk, ritz_out, ld_ritz, v2, ld2, r2);
+      const int rq = std::min(newcols, std::max(nreq, bw));
       s->mark("rr+ritz");
       s->sync();
       s->mark("host_decide");
@@ -1036,11 +1042,8 @@ void fast_step_enqueue(megb200_solver* s, const OpDev& op, int r, const EigShape
   EpiSpec epi;
   epi.r = r;
   epi.eps_next = eps_next;
-  fs.gr = rr_readback(s, sh.bw, fs.nreq, sh.bw, &epi, dst);
+  fs.gr = rr_readback(s, sh.bw, fs.nreq, sh.bw, &epi, dst, ritz_out, ld_ritz, V_next, ld_next, r);
   MEG_CUDA(cudaEventRecord(done, s->stream));
-  const int rq = std::min(sh.bw, std::max(fs.nreq, sh.bw));
-  copy_block(L, n, rq, s->T, s->ldq, ritz_out, ld_ritz);
-  copy_block(L, n, r, s->T, s->ldq, V_next, ld_next);
 }
 
 bool fast_step_confirm(megb200_solver* s, const FastStep& fs, megb200_step_result* out) {
@@ -1543,7 +1546,9 @@ int megb200_gen_dense_target(megb200_solver* s, const double* U, int64_t r, cons
 int megb200_profile_enable(megb200_solver* s, int32_t enable) {
   return guarded_impl([&] {
     if (!s) throw Error(MEGB200_ERR_PARAM, "solver is NULL");
-    s->prof = enable != 0;
+    if (enable < 0) throw Error(MEGB200_ERR_PARAM, "profile stride must be >= 0");
+    s->prof = enable;
+    s->prof_seen = 0;
   });
 }
 

@@ -67,8 +67,11 @@ def run(
     svd_subspace: int | None = None,
     block: int | None = None,
     flush_bytes: int = 0,
+    timing: bool = True,
 ) -> RunResult:
-    """Run T MEG steps from x0 on `objective` (Frobenius, sampled or stochastic)."""
+    """Run T MEG steps from x0 on `objective` (Frobenius, sampled or stochastic).
+
+    timing=False skips the per-step CUDA events (step_ms is then all zeros)."""
     if not isinstance(objective, (FrobeniusObjective, SampledObjective)):
         raise TypeError("run() needs a device objective (FrobeniusObjective, StochasticFrobeniusObjective, "
                         "SampledObjective)")
@@ -90,6 +93,8 @@ def run(
     passes = np.zeros(T, dtype=np.int32)
     rec = _lib.RunRecord()
     for k in ("shift", "eps", "lhs", "step_ms", "y", "lam"):
+        if k == "step_ms" and not timing:
+            continue
         setattr(rec, k, _lib.dptr(out[k]))
     rec.holds = holds.ctypes.data_as(_lib.c_int32_p)
     rec.passes = passes.ctypes.data_as(_lib.c_int32_p)
