@@ -1,6 +1,7 @@
 // Internal declarations shared by the kernel and runtime translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -61,7 +62,14 @@ struct Launch {
 // Streamed operator product: part[s] (S x n x b, dense row-major ld b) =
 // Op restricted to k-slice s times U.  Returns the number of k-slices S used.
 int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, int64_t n, const double* U,
-                        int64_t ldu, int b, double* part, int64_t part_cap_slices, int sm_count);
+                        int64_t ldu, int b, double* part, int64_t part_cap_slices, int sm_count, float* uscratch = nullptr);
+// 2D row-major tensor map (cached): inner dimension `cols`, outer `rows`, leading dimension `ld` elements
+CUtensorMap make_map(const void* base, CUtensorMapDataType dt, size_t es, int64_t cols, int64_t rows, int64_t ld,
+                     uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE);
+// tcgen05 split-TF32 pass for float32 operands (megb200_umma.cu); uscratch: 64 x n floats
+bool umma_pass_supported(int64_t n, int b, int64_t ldm, const void* M);
+int dense_pass_umma(const Launch& L, const float* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                    double* part, int64_t part_cap_slices, int sm_count, float* uscratch);
 void csr_apply_partial(const Launch& L, const int32_t* rowptr, const int32_t* col, const double* val, int64_t n,
                        const double* U, int64_t ldu, int b, double* part);
 // W = scale * sum_s part[s] + L E + alpha U   (E = l x b, dense ld b, device)

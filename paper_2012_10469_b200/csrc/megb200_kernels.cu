@@ -1248,8 +1248,7 @@ CUtensorMap encode_map(const void* base, CUtensorMapDataType dt, size_t es, int6
 // small direct-mapped cache of encoded tensor maps (the descriptors are pure
 // functions of their arguments; re-encoding costs ~1 us of host time per launch)
 CUtensorMap make_map(const void* base, CUtensorMapDataType dt, size_t es, int64_t cols, int64_t rows, int64_t ld,
-                     uint32_t box_cols, uint32_t box_rows,
-                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
+                     uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz) {
   struct Key {
     const void* base;
     int dt;
@@ -1362,7 +1361,10 @@ int choose_slices(int tiles, int64_t n, int sm_count, int s_min, int s_max) {
 }
 
 int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, int64_t n, const double* U,
-                        int64_t ldu, int b, double* part, int64_t part_cap_slices, int sm_count) {
+                        int64_t ldu, int b, double* part, int64_t part_cap_slices, int sm_count, float* uscratch) {
+  if (dtype == MEGB200_F32 && uscratch && umma_pass_supported(n, b, ldm, M))
+    return dense_pass_umma(L, static_cast<const float*>(M), ldm, n, U, ldu, b, part, part_cap_slices, sm_count,
+                           uscratch);
   {
     const size_t es = dtype == MEGB200_F64 ? 8 : 4;
     const bool aligned = b % 2 == 0 && b <= 32 && ldu % 2 == 0 && ((uintptr_t)U % 16 == 0) &&

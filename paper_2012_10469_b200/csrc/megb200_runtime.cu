@@ -52,6 +52,7 @@ struct megb200_solver {
   double* E = nullptr;      // max_lowrank x max_block
   double* dvec = nullptr;   // max_lowrank
   double* dlam = nullptr;   // 64: kept weights of the current iterate (device copy)
+  double* uT = nullptr;     // float32 operand-pass scratch (64 x n floats)
   double* H = nullptr;      // cap x cap
   double* C = nullptr;      // cap x max_block
   double* C2 = nullptr;
@@ -201,7 +202,8 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
     MEG_CUDA(cudaEventRecord(s->next_event(), s->stream));
   }
   if (op.kind == MEGB200_OP_DENSE && op.scale != 0.0) {
-    S = dense_apply_partial(L, op.dense, op.dtype, op.ld, n, U, ldu, k, s->part, s->part_slices, s->sm_count);
+    S = dense_apply_partial(L, op.dense, op.dtype, op.ld, n, U, ldu, k, s->part, s->part_slices, s->sm_count,
+                            reinterpret_cast<float*>(s->uT));
   } else if (op.kind == MEGB200_OP_CSR && op.scale != 0.0) {
     csr_apply_partial(L, op.rowptr, op.col, op.val, n, U, ldu, k, s->part);
     S = 1;
@@ -847,6 +849,7 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
         {&s->E, s->max_lowrank * max_block},
         {&s->dvec, s->max_lowrank},
         {&s->dlam, 64},
+        {&s->uT, 32 * n},  // 64 x n float32: [Uh | Ul]^T of the tcgen05 pass
         {&s->H, (int64_t)s->cap * s->cap},
         {&s->C, (int64_t)s->cap * max_block},
         {&s->C2, (int64_t)s->cap * max_block},
