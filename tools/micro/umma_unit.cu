@@ -165,5 +165,25 @@ int main() {
       printf("  K-major/SW128 k-step %d: mismatches %d maxerr %g\n", ks, bad, maxe);
     }
   }
+  // ---- tf32 conversion of raw fp32 operands: truncation or rounding?  A = 1 + 3*2^-12 (0.75 tf32 ulp), B = 1
+  {
+    for (int i = 0; i < 128 * 32; ++i) hA[i] = 0;
+    for (int i = 0; i < 32 * 32; ++i) hB[i] = 0;
+    const float va = 1.0f + 3.0f / 4096.0f, vb = 1.0f;
+    hA[(0 / 8) * 64 + (0 / 4) * 32 + (0 % 8) * 4 + 0] = va;   // a[0][0] (K-major, no swizzle layout of mode 1)
+    hB[(0 / 8) * 64 + (0 / 4) * 32 + (0 % 8) * 4 + 0] = vb;   // b[0][0]
+    cudaMemcpy(dA, hA, sizeof hA, cudaMemcpyHostToDevice); cudaMemcpy(dB, hB, sizeof hB, cudaMemcpyHostToDevice);
+    kunit<<<1, 128>>>(1, dA, dB, dO, idK, LBO1, SBO1, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpy(hO, dO, sizeof hO, cudaMemcpyDeviceToHost);
+    printf("tf32 conversion: a=1+3*2^-12 -> D = %.9f (truncate: 1.0, round: %.9f)\n", hO[0], 1.0 + 1.0 / 1024.0);
+    const float vn = -(1.0f + 3.0f / 4096.0f);
+    hA[0] = vn;
+    cudaMemcpy(dA, hA, sizeof hA, cudaMemcpyHostToDevice);
+    kunit<<<1, 128>>>(1, dA, dB, dO, idK, LBO1, SBO1, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpy(hO, dO, sizeof hO, cudaMemcpyDeviceToHost);
+    printf("negative: D = %.9f\n", hO[0]);
+  }
   return 0;
 }
