@@ -1,15 +1,14 @@
 // K1 (float32 operands): streamed operand pass on the 5th-generation tensor
 // cores.  W_s[i, c] = sum_{k in segment s} M[k, i] U[k, c] for a 128-row tile
 // of i, with M float32 (cfg 4/5) and U float64, computed as split TF32
-// TF32: M = Mh + Ml, U = Uh + Ul with Mh = trunc_TF32(M) (the tensor core's own
-// conversion of the raw tile), Uh = U rounded to TF32, and
+// TF32: M = Mh + Ml, U = Uh + Ul with Mh, Uh rounded to TF32, and
 //   W = Mh Uh + Mh Ul + Ml Uh + Ml Ul
 // accumulated in float32 in tensor memory over sub-segments of kSub k chunks,
 // each drained into float64 registers (so the float32 accumulation error does
 // not grow with n).
 //
-// Roles (192 threads): warps 0-3 derive Ml from each landed M tile (second
-// buffer) and drain the accumulators (tcgen05.ld of the accumulator
+// Roles (192 threads): warps 0-3 split each landed M tile into Mh (in place)
+// and Ml (second buffer) and drain the accumulators (tcgen05.ld of the accumulator
 // -> float64 partial rows); warp 4 lane 0 is the TMA producer; warp 5 lane 0
 // issues tcgen05.mma (kind::tf32, M=128, N=32, K=8, both operands K-major,
 // 128-byte swizzle) and commits stage releases / accumulator-ready to mbarriers.
@@ -261,19 +260,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t uend = min(send, u + kSub);
         for (; u < uend; ++u) {
           mbar_wait(full + st, ph);
-          // The tensor core reads float32 operands as TF32 by truncation (measured), so the landed
-          // tile serves unchanged as Mh = trunc(M); only Ml = M - trunc(M) (exact) is written.
-          // Elementwise, so the swizzled layout carries over.
-          const float4* a = reinterpret_cast<const float4*>(base + (size_t)st * kStageBytes);
+          // Mh = M rounded to TF32 (in place), Ml = M - Mh (exact): elementwise, so the swizzled
+          // layout carries over.  (The tensor core's own float32 -> TF32 conversion truncates;
+          // using the raw tile as Mh doubles the Ml representation error and costs the float32
+          // configs their residual floor, so Mh is rounded explicitly.)
+          float4* a = reinterpret_cast<float4*>(base + (size_t)st * kStageBytes);
           float4* al = reinterpret_cast<float4*>(base + (size_t)st * kStageBytes + kABytes);
 #pragma unroll 4
           for (int v = t; v < kABytes / 16; v += 32 * kSplitWarps) {
             const float4 x = a[v];
-            float4 l;
-            l.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-            l.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-            l.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-            l.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+            float4 h, l;
+            h.x = __uint_as_float((__float_as_uint(x.x) + 0x1000u) & 0xFFFFE000u);
+            h.y = __uint_as_float((__float_as_uint(x.y) + 0x1000u) & 0xFFFFE000u);
+            h.z = __uint_as_float((__float_as_uint(x.z) + 0x1000u) & 0xFFFFE000u);
+            h.w = __uint_as_float((__float_as_uint(x.w) + 0x1000u) & 0xFFFFE000u);
+            l.x = x.x - h.x;
+            l.y = x.y - h.y;
+            l.z = x.z - h.z;
+            l.w = x.w - h.w;
+            a[v] = h;
             al[v] = l;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
