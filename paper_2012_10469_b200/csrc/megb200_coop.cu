@@ -83,15 +83,18 @@ __device__ __forceinline__ void xty_rows(int64_t r0, int64_t r1, const double* _
   for (int64_t rc = r0; rc < r1; rc += kRC) {
     const int rows = (int)min((int64_t)kRC, r1 - rc);
     __syncthreads();
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < rows * p; idx += kCT) {
       const int r = idx / p, a = idx - r * p;
       Xs[idx] = X[(rc + r) * ldx + a];
     }
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < rows * q; idx += kCT) {
       const int r = idx / q, c = idx - r * q;
       Ys[idx] = Y[(rc + r) * ldy + c];
     }
     __syncthreads();
+    #pragma unroll 1
     for (int r = 0; r < rows; ++r) {
 #pragma unroll
       for (int j = 0; j < J; ++j) acc[j] = fma(Xs[r * p + oa[j]], Ys[r * q + oc[j]], acc[j]);
@@ -115,8 +118,15 @@ __device__ __forceinline__ void store_partial(double* __restrict__ part, int pq,
 // round trip instead of G dependent ones.
 __device__ __forceinline__ double warp_sum_partials(const double* __restrict__ part, int G, int64_t stride, int o) {
   const int lane = threadIdx.x & 31;
-  double s = 0.0;
-  for (int g = lane; g < G; g += 32) s += part[(int64_t)g * stride + o];
+  double v[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {  // G <= 160 in one round of independent loads
+    const int g = lane + 32 * k;
+    v[k] = g < G ? part[(int64_t)g * stride + o] : 0.0;
+  }
+  double s = (v[0] + v[1]) + (v[2] + v[3]) + v[4];
+#pragma unroll 1
+  for (int g = lane + 160; g < G; g += 32) s += part[(int64_t)g * stride + o];
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   return s;
@@ -128,6 +138,7 @@ __device__ __forceinline__ void reduce_partials(const double* __restrict__ part,
   const int G = gridDim.x;
   const int wpb = kCT / 32;
   const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
+  #pragma unroll 1
   for (int o = gw; o < pq; o += G * wpb) {
     double s = warp_sum_partials(part, G, pq, o);
     if ((threadIdx.x & 31) == 0) {
@@ -260,13 +271,16 @@ __global__ void __launch_bounds__(kCT) k_coop_cgs(int64_t n, const double* __res
   grid.sync();
   // W[r, c] -= sum_k Q[r, k] C[k, c]   (C in shared memory)
   double* Cs = sm;
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < cols * q; idx += kCT) Cs[idx] = Cws[idx];
   __syncthreads();
+  #pragma unroll 1
   for (int64_t idx = threadIdx.x; idx < (r1 - r0) * q; idx += kCT) {
     const int64_t r = r0 + idx / q;
     const int c = (int)(idx % q);
     const double* qr = Q + r * ldq;
     double s = 0.0;
+    #pragma unroll 1
     for (int k = 0; k < cols; ++k) s = fma(qr[k], Cs[k * q + c], s);
     W[r * ldw + c] -= s;
   }
@@ -301,7 +315,9 @@ __global__ void __launch_bounds__(kCT) k_coop_cholqr(int64_t n, const double* __
   phase_mark(5);
   double* Ri = sm;
   int* bad = reinterpret_cast<int*>(sm + q * q);
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < q * q; idx += kCT) Ri[idx] = Rinv[idx];
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < q; idx += kCT) bad[idx] = mask[idx];
   __syncthreads();
   // rows of this CTA: W[r, :] <- W[r, :] Rinv  (row staged in registers through shared memory)
@@ -309,11 +325,13 @@ __global__ void __launch_bounds__(kCT) k_coop_cholqr(int64_t n, const double* __
   for (int64_t rc = r0; rc < r1; rc += kRC) {
     const int rows = (int)min((int64_t)kRC, r1 - rc);
     __syncthreads();
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < rows * q; idx += kCT) {
       const int r = idx / q, c = idx - r * q;
       Ws[idx] = Wsrc[(rc + r) * lds + c];
     }
     __syncthreads();
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < rows * q; idx += kCT) {
       const int r = idx / q, c = idx - r * q;
       double v;
@@ -321,6 +339,7 @@ __global__ void __launch_bounds__(kCT) k_coop_cholqr(int64_t n, const double* __
         v = gauss_c(key, base + (uint64_t)(rc + r) * q + c);
       } else {
         v = 0.0;
+        #pragma unroll 1
         for (int k = 0; k <= c; ++k) v = fma(Ws[r * q + k], Ri[k * q + c], v);
       }
       W[(rc + r) * ldw + c] = v;
@@ -347,6 +366,7 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
   cta_rows(n, r0, r1);
   if (lc.lam) {
     // coefficients from device-resident kept weights (first lr), the rest as given
+    #pragma unroll 1
     for (int k = threadIdx.x; k < l; k += kCT) {
       double v;
       if (k < lc.lr) {
@@ -372,16 +392,19 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
   phase_mark(22);
   double* Es = sm;
   double* Ls = sm + l * b;  // this chunk's rows of L (kRC x l)
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < l * b; idx += kCT) Es[idx] = Ews[idx];
   for (int64_t rc = r0; rc < r1; rc += kRC) {
     const int rows = (int)min((int64_t)kRC, r1 - rc);
     __syncthreads();
     // stage the chunk's L rows (independent coalesced loads) so the L E products read shared memory
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < rows * l; idx += kCT) {
       const int r = idx / l, k = idx - r * l;
       Ls[idx] = Lf[(rc + r) * ldl + k];
     }
     __syncthreads();
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < rows * b; idx += kCT) {
       const int rr = idx / b, c = idx - rr * b;
       const int64_t i = rc + rr;
@@ -394,6 +417,7 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
       const double* Lr = Ls + rr * l;
       double v0 = scale * s + alpha * U[i * ldu + c], v1 = 0.0;
       int k = 0;
+      #pragma unroll 1
       for (; k + 1 < l; k += 2) {
         v0 = fma(Lr[k], Es[k * b + c], v0);
         v1 = fma(Lr[k + 1], Es[(k + 1) * b + c], v1);
@@ -570,6 +594,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
   double* Qs = sm + cols * rq;    // chunk rows of Q (kRC x cols)
   double* As = Qs + kRC * cols;   // chunk rows of AQ
   double* red = As + kRC * cols;  // kCT
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < cols * rq; idx += kCT) {
     const int k = idx / rq, c = idx - k * rq;
     Ss[idx] = S[k * m + c];
@@ -585,6 +610,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
     const int rows = (int)min((int64_t)kRC, r1 - rc);
     __syncthreads();
     // stage the chunk's rows of Q and AQ with independent coalesced loads
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < rows * cols; idx += kCT) {
       const int r = idx / cols, k = idx - r * cols;
       Qs[idx] = Q[(rc + r) * ldq + k];
@@ -592,10 +618,12 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
     }
     __syncthreads();
     if (rofs < rpt) {
+      #pragma unroll 1
       for (int rr = rofs; rr < rows; rr += rpt) {
         const double* qr = Qs + rr * cols;
         double x0 = 0.0, x1 = 0.0;
         int k = 0;
+        #pragma unroll 1
         for (; k + 1 < cols; k += 2) {
           x0 = fma(qr[k], Ss[k * rq + c], x0);
           x1 = fma(qr[k + 1], Ss[(k + 1) * rq + c], x1);
@@ -608,6 +636,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
           const double* ar = As + rr * cols;
           double a0 = 0.0, a1 = 0.0;
           k = 0;
+          #pragma unroll 1
           for (; k + 1 < cols; k += 2) {
             a0 = fma(ar[k], Ss[k * rq + c], a0);
             a1 = fma(ar[k + 1], Ss[(k + 1) * rq + c], a1);
@@ -625,6 +654,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
   double* gpart = part + (int64_t)gridDim.x * nreq;       // G x gr*gr
   if (threadIdx.x < nreq) {
     double s2 = 0.0;
+    #pragma unroll 1
     for (int t = threadIdx.x; t < rpt * rq; t += rq) s2 += red[t];
     rpart[(int64_t)blockIdx.x * nreq + threadIdx.x] = s2;
   }
@@ -647,6 +677,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
     const int wpb = kCT / 32;
     const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
     const int nout = nreq + gr * gr;
+    #pragma unroll 1
     for (int o = gw; o < nout; o += gridDim.x * wpb) {
       const double v = o < nreq ? warp_sum_partials(rpart, gridDim.x, nreq, o)
                                 : warp_sum_partials(gpart, gridDim.x, gr * gr, o - nreq);
@@ -659,24 +690,40 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
     }
   }
   phase_mark(15);
-  if (blockIdx.x == 0) {
-    if (epi && threadIdx.x == 0) {
-      // step epilogue (meg.py:347-356): y = exp(mu - mu_1), lam, lambda_{r+1}, b_{r+1}, cheap certificate
-      const int r = nreq - 1;
-      const double shift = theta[0];
-      double kept = 0.0, b = 0.0, lsum = 0.0;
-      for (int k = 0; k <= r; ++k) {
-        const double y = exp(theta[k] - shift);
-        epi[k] = y;
-        if (k < r) kept += y;
-        b += y;
-      }
+  if (blockIdx.x == 0 && threadIdx.x < 32 && epi) {
+    // step epilogue (meg.py:347-356) by one warp, lane k (and k + 32) owning pair k:
+    // y = exp(mu - mu_1), lam = y[:r] / sum renormalised, lambda_{r+1}, b_{r+1}, cheap certificate
+    const int lane = threadIdx.x;
+    const int r = nreq - 1;
+    const double shift = theta[0];
+    double y[2], lam[2];
+    double kept = 0.0, b = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = lane + 32 * h;
+      y[h] = k <= r ? exp(theta[k] - shift) : 0.0;
+      if (k <= r) epi[k] = y[h];
+      kept += k < r ? y[h] : 0.0;
+      b += y[h];
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      kept += __shfl_xor_sync(0xffffffffu, kept, off);
+      b += __shfl_xor_sync(0xffffffffu, b, off);
+    }
+    double lsum = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      lam[h] = (lane + 32 * h) < r ? y[h] / kept : 0.0;
+      lsum += lam[h];
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (lane + 32 * h < r) epi[r + 1 + lane + 32 * h] = lam[h] / lsum;
+    if (lane == 0) {
       double status = !(kept > 1e-290) ? 4.0 : 0.0;
-      for (int k = 0; k < r; ++k) {
-        epi[r + 1 + k] = epi[k] / kept;
-        lsum += epi[r + 1 + k];
-      }
-      for (int k = 0; k < r; ++k) epi[r + 1 + k] /= lsum;
       const double lam_rp1 = epi[r];
       double lhs;
       if (!(b > 0.0) || lam_rp1 < 0.0) {

@@ -40,12 +40,14 @@ __host__ __device__ constexpr int jacobi_smem_doubles(int m) {
 __device__ __forceinline__ double jdot(const double* A, int ia, int sa, const double* B, int ib, int sb, int len) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   int k = 0;
+#pragma unroll 1
   for (; k + 3 < len; k += 4) {
     a0 = fma(A[ia + k * sa], B[ib + k * sb], a0);
     a1 = fma(A[ia + (k + 1) * sa], B[ib + (k + 1) * sb], a1);
     a2 = fma(A[ia + (k + 2) * sa], B[ib + (k + 2) * sb], a2);
     a3 = fma(A[ia + (k + 3) * sa], B[ib + (k + 3) * sb], a3);
   }
+#pragma unroll 1
   for (; k < len; ++k) a0 = fma(A[ia + k * sa], B[ib + k * sb], a0);
   return (a0 + a1) + (a2 + a3);
 }
@@ -80,6 +82,7 @@ __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, 
     __syncthreads();
     if (t == 0) {
       double s = 0.0;
+#pragma unroll 1
       for (int w = 0; w < (nth >> 5); ++w) s += red[w];
       red[0] = s;
     }

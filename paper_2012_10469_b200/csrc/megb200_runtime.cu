@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <functional>
 #include <string>
@@ -398,9 +399,11 @@ int rr_readback(megb200_solver* s, int newcols, int nreq, int bw, const EpiSpec*
     tdst = s->T;
     ldt = s->ldq;
   }
-  coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, s->n, s->Q, s->AQ, s->ldq, rq, nreq, tdst, ldt,
-          s->resid, s->red, s->sm_count, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
-          epi ? s->pack + s->pack_epi : nullptr, v2, ld2, r2);
+  static const bool twice = getenv("MEGB200_DEBUG_RR_TWICE") != nullptr;  // diagnostics: warm i-cache timing
+  for (int rep = 0; rep < (twice ? 2 : 1); ++rep)
+    coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, s->n, s->Q, s->AQ, s->ldq, rq, nreq, tdst, ldt,
+            s->resid, s->red, s->sm_count, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
+            epi ? s->pack + s->pack_epi : nullptr, v2, ld2, r2);
   s->d2h(dst, s->pack, s->pack_gram + (int64_t)gr * gr);
   return gr;
 }
@@ -1229,6 +1232,8 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
     };
     auto fast_ok = [&]() { return pipe && warm && warm_cols == sh.bw && warm_orth; };
     FastStep fs[2];
+    double host_enq = 0.0, host_wait = 0.0;  // diagnostics (MEGB200_HOST_TIMING)
+    int64_t host_n = 0;
     int64_t i = 0;
     bool pending = false;  // step i is enqueued as a fast step (fs[i & 1]) and not yet confirmed
     while (i < T) {
@@ -1256,6 +1261,7 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
       if (i + 1 < T) {
         const int64_t t1 = t0 + i + 1;
         const double eps1 = eps_eval(*sch, t0 + i + 1);  // eps of iterate i + 1 = eps_next of step i
+        const auto h0 = std::chrono::steady_clock::now();
         begin_step(i + 1);
         const double* V1 = Vb[(i + 1) % 3];
         const OpDev op1 = frob_merged_op(g, V1, r, n, r, eps1, eta_eval(*sch, t1), s->pack + s->pack_epi + (r + 1));
@@ -1263,11 +1269,16 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
                           Vb[(i + 2) % 3], r, hspec[(i + 1) & 1], done[(i + 1) & 1], fs[(i + 1) & 1]);
         end_step(i + 1);
         spec = true;
+        host_enq += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
+        ++host_n;
       }
       megb200_step_result out;
       result_for(i, out);
       const double eps_next = eps_eval(*sch, t0 + i + 1);
-      if (fast_step_confirm(s, fs[i & 1], &out)) {
+      const auto h1 = std::chrono::steady_clock::now();
+      const bool conf = fast_step_confirm(s, fs[i & 1], &out);
+      host_wait += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h1).count();
+      if (conf) {
         commit(i, out, eps_next);
         ++i;
         bool lam_pos = true;
@@ -1284,6 +1295,9 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
       ++i;
       pending = false;
     }
+    if (getenv("MEGB200_HOST_TIMING") && host_n > 0)
+      fprintf(stderr, "meg_run host: enqueue %.1f us/step, confirm wait %.1f us/step (%lld speculative steps)\n",
+              host_enq / host_n, host_wait / host_n, (long long)host_n);
     if (V_out) copy_block(L, n, r, Vb[T % 3], r, V_out, ld_out);
     if (rec && rec->ritz_block) {
       const int64_t wc = (T > 0) ? std::min<int64_t>(warm_cols, rec->ritz_cap) : 0;
