@@ -79,5 +79,12 @@ int main(int argc, char** argv) {
     float ms; cudaEventElapsedTime(&ms, a, z);
     printf("flags %d (1=no mma 2=no split 4=3 products): avg %.1f us  (%.0f GB/s operand)\n", flags, ms * 1000 / 20, (double)n * n * 4 / (ms / 20 * 1e-3) / 1e9);
   }
+#ifdef UMMA_PROFILE
+  long long hp[8]; cudaMemcpyFromSymbol(hp, umma::g_uprof, sizeof hp);
+  printf("split warp 0 per stage (cycles): wait abuf %.0f | wait full %.0f | load+split %.0f | st+wait+arrive %.0f (%lld stages)\n",
+         (double)hp[0] / hp[4], (double)hp[1] / hp[4], (double)hp[2] / hp[4], (double)hp[3] / hp[4], hp[4]);
+  printf("MMA warp: wait split %.0f cycles per stage | drain wait acc_full %.0f cycles per drain (%lld drains)\n",
+         (double)hp[5] / hp[4], (double)hp[6] / hp[7], hp[7]);
+#endif
   return 0;
 }

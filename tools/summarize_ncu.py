@@ -11,6 +11,11 @@ KEYS = [
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active %"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe active %"),
+    ("SM_C.TriageCompute.smsp__pipe_tensor_subpipe_dmma_cycles_active.avg", "DMMA subpipe active cycles / SMSP"),
+    ("TPC.TriageCompute.sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg", "HMMA (tf32) subpipe active cycles / SM"),
+    ("sm__cycles_active.avg", "SM active cycles (avg)"),
+    ("sm__cycles_active.max", "SM active cycles (max)"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared-memory bank conflicts"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__grid_size", "grid"),
