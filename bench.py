@@ -303,11 +303,11 @@ def run_device_arm(args, world, rank, local):
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
     for i in range(K2):
-        xi = pb.LowRankIterate(w.n, w.r, Vh, lam, eps, warm_block=warm, warm_orth_err=werr)
-        res = step(xi, t)
-        Vn.copy_(res.iterate.V_device, non_blocking=True)  # device -> pinned host read of the step's result
+        # one reference-facing call with host buffers: upload + validate V, step, read V_next back
+        res = pb.lowrank_meg_step_host(Vh, lam, eps, obj, w.eta(t), w.eps(t + 1), svd_seed=t,
+                                       svd_subspace=w.subspace, block=w.block, warm=warm, warm_orth_err=werr, out=Vn)
         Vh, Vn = Vn, Vh
-        lam, eps, warm, werr = res.iterate.lam, res.iterate.eps, res.iterate.warm_block, res.iterate.warm_orth_err
+        lam, eps, warm, werr = res.lam, res.eps, res.warm_block, res.warm_orth_err
         t += 1
     f1.record()
     torch.cuda.synchronize()
@@ -363,8 +363,8 @@ def run_device_arm(args, world, rank, local):
             "cold_start_passes": cold_passes,
             "host_ms_per_step": 1e3 * host_s / K,
             "timing": "device: native run loop megb200_meg_run (pipelined), one CUDA-event pair around the K steps "
-                      "on the solver stream; e2e: per-step lowrank_meg_step through the Python API, V from/to "
-                      "pinned host memory every step",
+                      "on the solver stream; e2e: per-step lowrank_meg_step_host (C-ABI megb200_lowrank_meg_step_host): "
+                      "V uploaded from pinned host memory, validated, stepped and V_next read back every step",
         }
         print(json.dumps(line), flush=True)
     if world > 1:

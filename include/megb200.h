@@ -206,6 +206,16 @@ int megb200_top_r(megb200_solver* s, const megb200_operator* op, int32_t r, cons
 int megb200_lowrank_meg_step(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta,
                              double eps_next, const megb200_eig_opts* opts, megb200_step_result* out);
 
+/* The step for a caller whose iterate factor lives in HOST memory: x->V and
+ * V_next_host are host pointers (pinned memory makes the copies asynchronous).
+ * In one call the factor is uploaded, validated (V^T V = I to 1e-10,
+ * meg.py:69-71, before the step: MEGB200_ERR_PARAM otherwise), stepped, and
+ * V_next read back.  A Frobenius / stochastic / sampled gradient with gV == NULL
+ * is evaluated at the uploaded iterate.  out->V_next is not used. */
+int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_host, const megb200_gradient* g,
+                                  double eta, double eps_next, const megb200_eig_opts* opts, double* V_next_host,
+                                  int64_t ld_next_host, megb200_step_result* out);
+
 /* Run loop: T low-rank MEG steps from x0 without returning between steps --
  * the driver of test_meg.py:150-156 / the harness loop of SPEC.md:433-450,
  * absent from the reference code.  Step t = t0 + i uses eta_t, eps_next =

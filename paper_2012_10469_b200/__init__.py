@@ -14,6 +14,7 @@ from .meg import (
     EpsilonSchedule,
     LogmapOperator,
     LowRankIterate,
+    HostStepResult,
     LowRankStepResult,
     StepConfig,
     certificate_cheap,
@@ -21,6 +22,7 @@ from .meg import (
     eps_schedule_eval,
     logmap_operator,
     lowrank_meg_step,
+    lowrank_meg_step_host,
     merge_certificates,
     step_eval,
     warm_start_wrap,
@@ -35,9 +37,9 @@ from .objectives import (
 )
 
 __all__ = [
-    "CertificateRecord", "DenseGradient", "EighError", "EpsilonSchedule", "FrobeniusObjective", "GradientOperator",
+    "CertificateRecord", "DenseGradient", "HostStepResult", "EighError", "EpsilonSchedule", "FrobeniusObjective", "GradientOperator",
     "LanczosError", "LogmapOperator", "LowRankIterate", "LowRankStepResult", "ParameterError", "RankDeficiencyError",
     "SampledObjective", "StepConfig", "StochasticFrobeniusObjective", "SymmetricOperator", "TopREigen",
     "ZeroGradient", "certificate_cheap", "certificate_full", "eps_schedule_eval", "lanczos_top_r", "logmap_operator",
-    "lowrank_meg_step", "merge_certificates", "project_simplex", "step_eval", "symmetrize", "warm_start_wrap",
+    "lowrank_meg_step", "lowrank_meg_step_host", "merge_certificates", "project_simplex", "step_eval", "symmetrize", "warm_start_wrap",
 ]

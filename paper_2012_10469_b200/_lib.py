@@ -118,6 +118,9 @@ SIGNATURES = [
     ("megb200_lowrank_meg_step", C.c_int,
      [C.c_void_p, C.POINTER(Iterate), C.POINTER(Gradient), C.c_double, C.c_double, C.POINTER(EigOpts),
       C.POINTER(StepResult)]),
+    ("megb200_lowrank_meg_step_host", C.c_int,
+     [C.c_void_p, C.POINTER(Iterate), C.POINTER(Gradient), C.c_double, C.c_double, C.POINTER(EigOpts),
+      C.c_void_p, C.c_int64, C.POINTER(StepResult)]),
     ("megb200_meg_run", C.c_int,
      [C.c_void_p, C.POINTER(Iterate), C.POINTER(Gradient), C.POINTER(Schedule), C.c_int64, C.c_int64,
       C.POINTER(EigOpts), C.c_uint64, C.c_void_p, C.c_int64, c_double_p, c_double_p, C.POINTER(RunRecord)]),

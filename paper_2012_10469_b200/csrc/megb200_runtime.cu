@@ -54,6 +54,7 @@ struct megb200_solver {
   double* dvec = nullptr;   // max_lowrank
   double* dlam = nullptr;   // 64: kept weights of the current iterate (device copy)
   double* uT = nullptr;     // float32 operand-pass scratch (64 x n floats)
+  double* host_io = nullptr;  // 2 x n x 64: device copies of a host caller's V / V_next
   double* H = nullptr;      // cap x cap
   double* C = nullptr;      // cap x max_block
   double* C2 = nullptr;
@@ -330,6 +331,9 @@ struct EpiSpec {
   std::vector<double> host;  // out: epilogue block (2r + 8 doubles) + Gram (gr x gr)
   double* v_next = nullptr;  // in: V_next = first r Ritz vectors, written with the outputs
   int64_t ld_next = 0;
+  double* v_host = nullptr;  // in: host copy of V_next read back with the pack (host-buffer step)
+  int64_t ld_host = 0;
+  bool v_host_done = false;  // out: v_host holds the converged V_next
 };
 
 // Block sizes of a solve: block width bw, basis limit mmax, thick-restart keep.
@@ -483,6 +487,10 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       const int r2 = vec_out ? nreq : (epi ? epi->r : 0);
       const int gr = rr_readback(s, newcols, nreq, bw, epi, pk, ritz_out, ld_ritz, v2, ld2, r2);
       const int rq = std::min(newcols, std::max(nreq, bw));
+      // host-buffer step: V_next travels back with the pack (one wait when this RR converges)
+      if (epi && epi->v_host && epi->v_next && epi->ld_next == epi->r && epi->ld_host == epi->r)
+        MEG_CUDA(cudaMemcpyAsync(epi->v_host, epi->v_next, (size_t)n * epi->r * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s->stream));
       s->mark("rr+ritz");
       s->sync();
       s->mark("host_decide");
@@ -521,6 +529,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
         run.norm_est = scale;
         run.converged = true;
         if (epi) {
+          epi->v_host_done = epi->v_host && epi->v_next && epi->ld_next == epi->r && epi->ld_host == epi->r;
           const int epi_len = 2 * epi->r + 8;
           epi->host.assign(pk + s->pack_epi, pk + s->pack_epi + epi_len);
           epi->host.insert(epi->host.end(), pk + s->pack_gram, pk + s->pack_gram + (int64_t)gr * gr);
@@ -894,7 +903,7 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
     s->resid = s->pack + s->pack_resid;
     // [pack copy | scratch | pipelined read-back slot 0 | slot 1]
     s->pack_len = (int64_t)s->cap + 64 + 136 + 64 * 64;
-    s->h_buf_len = 4 * s->pack_len + 64;
+    s->h_buf_len = 5 * s->pack_len + 64;
     s->h_up_len = 8192;
     e = cudaMallocHost(&s->h_up, s->h_up_len * sizeof(double));
     if (e != cudaSuccess) {
@@ -919,6 +928,7 @@ void megb200_solver_destroy(megb200_solver* s) {
   cudaFree(s->arena);
   if (s->run_buf) cudaFree(s->run_buf);
   if (s->flush_buf) cudaFree(s->flush_buf);
+  if (s->host_io) cudaFree(s->host_io);
   cudaFreeHost(s->h_buf);
   cudaFreeHost(s->h_up);
   delete s;
@@ -982,7 +992,8 @@ int megb200_top_r(megb200_solver* s, const megb200_operator* op, int32_t r, cons
 
 namespace {
 void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta, double eps_next,
-               const megb200_eig_opts* opts, megb200_step_result* out);
+               const megb200_eig_opts* opts, megb200_step_result* out, double* v_host = nullptr,
+               int64_t ld_host = 0, bool* v_host_done = nullptr);
 
 // Step outputs from a converged solve's read-back: epilogue block
 // [y (r+1) | lam (r) | lam_{r+1}, b_{r+1}, shift, lhs, holds, threshold, status]
@@ -1345,7 +1356,8 @@ namespace {
 // One low-rank MEG step (meg.py:327-364) -- shared by the single-step entry point
 // and the native run loop.  Throws megb200::Error.
 void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta, double eps_next,
-               const megb200_eig_opts* opts, megb200_step_result* out) {
+               const megb200_eig_opts* opts, megb200_step_result* out, double* v_host, int64_t ld_host,
+               bool* v_host_done) {
   if (!s || !out) throw Error(MEGB200_ERR_PARAM, "solver/result is NULL");
   if (!(eps_next > 0.0 && eps_next <= 0.75))
     throw Error(MEGB200_ERR_PARAM, "eps_next must lie in (0, 3/4], got " + std::to_string(eps_next));
@@ -1384,6 +1396,8 @@ void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradie
   if (!v_alias) {
     epi.v_next = out->V_next;
     epi.ld_next = out->ld_next;
+    epi.v_host = v_host;
+    epi.ld_host = ld_host;
   }
   double* ritz_dst = w_alias ? s->W : out->ritz_block;
   const int64_t ld_ritz_dst = w_alias ? (int64_t)s->max_block : out->ld_ritz;
@@ -1397,6 +1411,7 @@ void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradie
   // next iterate: V = top r Ritz vectors (written by top_eigs unless aliased); lam / certificate
   // came from the fused epilogue
   if (v_alias) copy_block(L, n, r, s->T, s->ldq, out->V_next, out->ld_next);
+  if (v_host_done) *v_host_done = epi.v_host_done;
   if (w_alias && out->ritz_block) copy_block(L, n, out->ritz_cols, s->W, s->max_block, out->ritz_block, out->ld_ritz);
   fill_step_result(epi.host.data(), epi.host.data() + 2 * r + 8, epi.gr, r, run.theta.data(), out);
   s->mark("epilogue");
@@ -1409,6 +1424,81 @@ extern "C" {
 int megb200_lowrank_meg_step(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta,
                              double eps_next, const megb200_eig_opts* opts, megb200_step_result* out) {
   return guarded_impl([&] { step_core(s, x, g, eta, eps_next, opts, out); });
+}
+
+int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_host, const megb200_gradient* g,
+                                  double eta, double eps_next, const megb200_eig_opts* opts, double* V_next_host,
+                                  int64_t ld_next_host, megb200_step_result* out) {
+  return guarded_impl([&] {
+    if (!s || !x_host || !g || !out || !V_next_host) throw Error(MEGB200_ERR_PARAM, "null argument");
+    const int64_t n = s->n, r = x_host->r;
+    if (x_host->n != n) throw Error(MEGB200_ERR_PARAM, "iterate dimension does not match the solver");
+    if (!(1 <= r && r < n) || r > 64) throw Error(MEGB200_ERR_PARAM, "need 1 <= r < n and r <= 64");
+    if (!x_host->V || x_host->ldv < r || ld_next_host < r) throw Error(MEGB200_ERR_PARAM, "host factor missing");
+    Launch L = s->launch();
+    if (!s->host_io) MEG_CUDA(cudaMalloc(&s->host_io, (size_t)2 * n * 64 * sizeof(double)));
+    double* Vd = s->host_io;
+    double* Vn = s->host_io + n * 64;
+    // contiguous factors move as one block (a pitched copy of 8r-byte rows is n tiny DMA rows)
+    if (x_host->ldv == r)
+      MEG_CUDA(cudaMemcpyAsync(Vd, x_host->V, (size_t)n * r * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    else
+      MEG_CUDA(cudaMemcpy2DAsync(Vd, r * sizeof(double), x_host->V, x_host->ldv * sizeof(double), r * sizeof(double),
+                                 n, cudaMemcpyHostToDevice, s->stream));
+    // LowRankIterate validation (meg.py:69-71): V^T V is formed now and read back with the
+    // step's first wait; a failed check discards the step and raises before any result
+    coop_tn(L, n, Vd, r, (int)r, Vd, r, (int)r, s->G, (int)r, nullptr, 1.0, s->red, s->sm_count);
+    double* gram_dst = s->h_buf + 4 * s->pack_len;  // pinned slot (pack_len >= 64 x 64 doubles)
+    s->d2h(gram_dst, s->G, r * r);
+    auto gram_check = [&]() {
+      double ge = 0.0;
+      for (int i = 0; i < (int)r; ++i)
+        for (int j = 0; j < (int)r; ++j) ge = std::max(ge, fabs(gram_dst[i * r + j] - (i == j ? 1.0 : 0.0)));
+      if (!(ge <= 1e-10)) {
+        char buf[96];
+        snprintf(buf, sizeof buf, "V columns not orthonormal (error %.3e)", ge);
+        throw Error(MEGB200_ERR_PARAM, buf);
+      }
+    };
+    megb200_iterate it = *x_host;
+    it.V = Vd;
+    it.ldv = r;
+    megb200_gradient gg = *g;
+    if ((gg.kind == MEGB200_GRAD_FROBENIUS || gg.kind == MEGB200_GRAD_STOCHASTIC || gg.kind == MEGB200_GRAD_SAMPLED) &&
+        !gg.gV) {
+      gg.gV = Vd;
+      gg.g_r = r;
+      gg.g_ldv = r;
+      gg.g_lam = x_host->lam;
+      gg.g_eps = x_host->eps;
+    }
+    megb200_step_result o = *out;
+    o.V_next = Vn;
+    o.ld_next = r;
+    bool v_done = false;
+    try {
+      step_core(s, &it, &gg, eta, eps_next, opts, &o, ld_next_host == r ? V_next_host : nullptr, r, &v_done);
+    } catch (const Error&) {
+      s->sync();
+      gram_check();  // an invalid factor takes precedence over what the step made of it
+      throw;
+    }
+    s->sync();
+    gram_check();
+    if (!v_done) {
+      if (ld_next_host == r)
+        MEG_CUDA(cudaMemcpyAsync(V_next_host, Vn, (size_t)n * r * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+      else
+        MEG_CUDA(cudaMemcpy2DAsync(V_next_host, ld_next_host * sizeof(double), Vn, r * sizeof(double),
+                                   r * sizeof(double), n, cudaMemcpyDeviceToHost, s->stream));
+      s->sync();
+    }
+    double* keep_v = out->V_next;
+    const int64_t keep_ld = out->ld_next;
+    *out = o;
+    out->V_next = keep_v;
+    out->ld_next = keep_ld;
+  });
 }
 
 int megb200_dense_stats(megb200_solver* s, const void* M, int32_t dtype, int64_t ld, double* norm2, double* trace) {

@@ -409,3 +409,98 @@ def warm_start_wrap(V0, lam0, eps0: float) -> LowRankIterate:
     eps_p = eps0 * (n - r) / n
     lam = ((1.0 - eps0) * lam0 + eps0 / n) / (1.0 - eps_p)
     return LowRankIterate(n=n, r=r, V=V0, lam=lam / lam.sum(), eps=eps_p)
+
+
+@dataclass(frozen=True)
+class HostStepResult:
+    """Result of `lowrank_meg_step_host`: the next factor in host memory plus the
+    step's scalars (same meaning as LowRankStepResult's fields)."""
+
+    V: object  # host array / pinned tensor, n x r
+    lam: np.ndarray
+    eps: float
+    cert: CertificateRecord
+    lambda_r_plus_1: float
+    b_r_plus_1: float
+    shift: float
+    top_eigenvalues: np.ndarray
+    residual_norms: np.ndarray
+    passes: int
+    warm_block: object  # device Ritz block for the next step
+    warm_orth_err: float
+
+
+def lowrank_meg_step_host(
+    V,
+    lam,
+    eps: float,
+    objective,
+    eta: float,
+    eps_next: float,
+    svd_tol: float = 1e-10,
+    svd_seed: int = 0,
+    svd_subspace: int | None = None,
+    *,
+    t: int = 0,
+    block: int | None = None,
+    warm=None,
+    warm_orth_err: float = 1.0,
+    out=None,
+) -> HostStepResult:
+    """One MEG step for a caller that keeps the iterate factor V (n x r) in host
+    memory: one native call uploads V, validates it like LowRankIterate
+    (meg.py:62-77; ParameterError before the step), runs the step and writes
+    V_next to `out` (a host array or pinned CPU tensor; allocated if None).
+
+    `objective` is a device objective (its gradient is taken at the uploaded
+    iterate) or a gradient descriptor; `warm` is the device Ritz block returned
+    by the previous call (optional)."""
+    if not 0 < eps_next <= 0.75:
+        raise ParameterError(f"eps_next must lie in (0, 3/4], got {eps_next}")
+    if not 0 < eps <= 0.75:
+        raise ParameterError(f"eps must lie in (0, 3/4], got {eps}")
+    n, r = int(V.shape[0]), int(V.shape[1])
+    lam = np.ascontiguousarray(np.asarray(lam, dtype=np.float64).ravel())
+    if lam.shape != (r,):
+        raise ParameterError(f"lam must have {r} entries")
+    if abs(lam.sum() - 1.0) > 1e-10:
+        raise ParameterError(f"lam must sum to 1, got {lam.sum()!r}")
+    if np.any(np.diff(lam) > 0) or not lam[-1] > 0:
+        raise ParameterError("lam must be sorted non-increasing and strictly positive")
+    g = objective.grad_operator(None, t) if hasattr(objective, "grad_operator") else objective
+    if not isinstance(g, GradientOperator):
+        raise TypeError("objective must be a device objective or gradient descriptor")
+    s = g.solver()
+    hold: list = []
+    gs = g.struct(hold)
+    it = _lib.Iterate()
+    it.n, it.r, it.eps = n, r, float(eps)
+    it.lam = _lib.dptr(lam)
+    if isinstance(V, torch.Tensor):
+        if V.is_cuda or V.dtype != torch.float64 or not V.is_contiguous():
+            raise ParameterError("V must be a contiguous float64 host tensor")
+        it.V, it.ldv = V.data_ptr(), V.stride(0)
+    else:
+        V = np.ascontiguousarray(V, dtype=np.float64)
+        it.V, it.ldv = V.ctypes.data, V.strides[0] // 8
+    if out is None:
+        out = np.empty((n, r))
+    out_ptr = out.data_ptr() if isinstance(out, torch.Tensor) else out.ctypes.data
+    ld_out = out.stride(0) if isinstance(out, torch.Tensor) else out.strides[0] // 8
+    warm_t = warm if isinstance(warm, torch.Tensor) and warm.shape[0] == n else None
+    opts = _eig_opts(max(svd_tol, g.tol_floor), None, svd_seed, svd_subspace, 12, block, None, warm_t,
+                     warm_orthonormal=warm_t is not None and warm_orth_err <= 1e-13)
+    ritz = torch.empty((n, runtime.MAX_BLOCK), dtype=torch.float64, device=runtime.device())
+    lam_next, y, mu, res = np.zeros(r), np.zeros(r + 1), np.zeros(r + 1), np.zeros(r + 1)
+    o = _lib.StepResult()
+    o.lam_next, o.y, o.mu, o.residual_norms = _lib.dptr(lam_next), _lib.dptr(y), _lib.dptr(mu), _lib.dptr(res)
+    o.ritz_block = ritz.data_ptr()
+    o.ld_ritz = ritz.stride(0)
+    rc = s.lib.megb200_lowrank_meg_step_host(s.handle, C.byref(it), C.byref(gs), float(eta), float(eps_next),
+                                             C.byref(opts), C.c_void_p(out_ptr), int(ld_out), C.byref(o))
+    runtime.check(rc, residual_norms=res.copy())
+    cert = CertificateRecord(iteration=None, lhs_cheap=o.lhs_cheap, holds_cheap=bool(o.holds_cheap),
+                             threshold=o.threshold)
+    return HostStepResult(V=out, lam=lam_next, eps=float(eps_next), cert=cert, lambda_r_plus_1=o.lambda_r_plus_1,
+                          b_r_plus_1=o.b_r_plus_1, shift=o.shift, top_eigenvalues=y, residual_norms=res,
+                          passes=int(o.passes), warm_block=ritz[:, : o.ritz_cols], warm_orth_err=o.ritz_orth_err)

@@ -337,3 +337,31 @@ def test_run_chaining_continues_warm(pb):
     assert np.array_equal(np.concatenate([first.shift, second.shift]), whole.shift)
     assert np.array_equal(np.concatenate([first.lam, second.lam]), whole.lam)
     assert np.array_equal(second.iterate.V, whole.iterate.V)
+
+
+def test_host_buffer_step_matches_device_step(pb):
+    """lowrank_meg_step_host (host V in/out, one native call) equals the device-tensor step,
+    and rejects a non-orthonormal V with ParameterError before stepping (meg.py:69-71)."""
+    import torch
+
+    cfg = inputs.CONFIGS["cfg2"].scaled(1024, 6)
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    dev = pb.FrobeniusObjective(host.m)
+    x = pb.LowRankIterate(x0.n, x0.r, x0.V, x0.lam, x0.eps)
+    Vh = torch.from_numpy(np.ascontiguousarray(x0.V)).pin_memory()
+    lam, eps, warm, werr = x0.lam.copy(), x0.eps, None, 1.0
+    for t in range(6):
+        ref = pb.lowrank_meg_step(x, dev.grad_operator(x), 1.0, cfg.eps(t + 1), svd_seed=t, svd_subspace=64, block=18)
+        got = pb.lowrank_meg_step_host(Vh, lam, eps, dev, 1.0, cfg.eps(t + 1), svd_seed=t, svd_subspace=64, block=18,
+                                       warm=warm, warm_orth_err=werr, out=torch.empty_like(Vh).pin_memory())
+        assert np.array_equal(got.top_eigenvalues, ref.top_eigenvalues)
+        assert np.array_equal(got.lam, ref.iterate.lam)
+        assert got.shift == ref.shift and got.cert.lhs_cheap == ref.cert.lhs_cheap
+        assert np.array_equal(got.V.numpy(), ref.iterate.V)
+        x = ref.iterate
+        Vh, lam, eps, warm, werr = got.V, got.lam, got.eps, got.warm_block, got.warm_orth_err
+    bad = Vh.clone()
+    bad[:, 0] *= 1.5
+    with pytest.raises(pb.ParameterError):
+        pb.lowrank_meg_step_host(bad, lam, eps, dev, 1.0, 0.01)
