@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
                                                       double* __restrict__ W, int64_t ldw, double* __restrict__ Ews,
                                                       double* __restrict__ part, const double* __restrict__ Qh,
                                                       int64_t ldq, int hp, double* __restrict__ Hout, int64_t ldh,
-                                                      LamCoef lc) {
+                                                      LamCoef lc, const double* __restrict__ Eg, int64_t ldg) {
   extern __shared__ double sm[];
   __shared__ double dsh[kMaxLowrank];
   phase_mark(20);
@@ -377,9 +377,11 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
       }
       dsh[k] = v;
     }
-    d = dsh;  // read after the grid.sync below
+    d = dsh;  // read after the barrier below
   }
-  if (l > 0) {
+  if (Eg) {
+    __syncthreads();  // E = diag(d) L^T U from the caller's L^T U (no grid reduction)
+  } else if (l > 0) {
     double acc[J];
     xty_rows<J>(r0, r1, Lf, ldl, l, U, ldu, b, sm, acc);
     store_partial<J>(part, l * b, acc);
@@ -393,7 +395,10 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
   double* Es = sm;
   double* Ls = sm + l * b;  // this chunk's rows of L (kRC x l)
   #pragma unroll 1
-  for (int idx = threadIdx.x; idx < l * b; idx += kCT) Es[idx] = Ews[idx];
+  for (int idx = threadIdx.x; idx < l * b; idx += kCT) {
+    const int k = idx / b, c = idx - k * b;
+    Es[idx] = Eg ? d[k] * Eg[k * ldg + c] : Ews[idx];
+  }
   for (int64_t rc = r0; rc < r1; rc += kRC) {
     const int rows = (int)min((int64_t)kRC, r1 - rc);
     __syncthreads();
@@ -538,7 +543,7 @@ void coop_cholqr(const Launch& L, int64_t n, const double* Wsrc, int64_t lds, do
 void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, double scale, const double* Lf,
                  int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
                  int64_t ldw, double* Ews, double* part, int sm_count, const double* Qh, int64_t ldq, int hp,
-                 double* Hout, int64_t ldh, LamCoef lc) {
+                 double* Hout, int64_t ldh, LamCoef lc, const double* Eg, int64_t ldg) {
   if (lc.lam && (l > kMaxLowrank || lc.lr > l)) throw Error(MEGB200_ERR_PARAM, "finish: coefficient width out of range");
   const int G = coop_grid(n, sm_count);
   const size_t smem = std::max({(size_t)kRC * (l + b), (size_t)std::max(1, l * b) + (size_t)kRC * l,
@@ -550,7 +555,7 @@ void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, 
     static bool a = false;                                                                                      \
     if (!a) { raise_smem(k_coop_finish<jj, j2>, kCoopSmem); a = true; }                                         \
     coop_launch(L, k_coop_finish<jj, j2>, G, smem, n, b, S, spart, scale, Lf, ldl, l, d, alpha, U, ldu, W, ldw,  \
-                Ews, part, Qh, ldq, hp, Hout, ldh, lc);                                                         \
+                Ews, part, Qh, ldq, hp, Hout, ldh, lc, Eg, ldg);                                                \
   }
 #define MEG_FIN(jj)                                            \
   switch (J2) {                                                \

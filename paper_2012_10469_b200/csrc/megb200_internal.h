@@ -135,7 +135,8 @@ struct LamCoef {
 void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, double scale, const double* Lf,
                  int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
                  int64_t ldw, double* Ews, double* part, int sm_count, const double* Qh = nullptr, int64_t ldq = 0,
-                 int hp = 0, double* Hout = nullptr, int64_t ldh = 0, LamCoef lc = LamCoef());
+                 int hp = 0, double* Hout = nullptr, int64_t ldh = 0, LamCoef lc = LamCoef(),
+                 const double* Eg = nullptr, int64_t ldg = 0);  // Eg: precomputed L^T U (skips its reduction)
 // Jacobi RR + Ritz block + residuals (+ Gram of the first gr Ritz vectors, + MEG epilogue into epi);
 // the first r2 Ritz vectors are also written to V2
 void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,

@@ -189,6 +189,8 @@ struct OpDev {
   const double* d_dev = nullptr;  // device coefficients (length l)
   LamCoef lc;                     // or the first lc.lr of them from device-resident kept weights
   double alpha = 0.0;
+  const double* Eg = nullptr;     // device L^T U when the caller already has it (else reduced per pass)
+  int64_t ldg = 0;
 };
 
 void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k, double* W, int64_t ldw,
@@ -222,7 +224,7 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
     s->prof_passes++;
   }
   coop_finish(L, n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
-              s->sm_count, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap, op.lc);
+              s->sm_count, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap, op.lc, op.Eg, op.ldg);
 }
 
 // columns k > 64 are applied in chunks (re-streams the operand; not used by the configs)
@@ -1275,7 +1277,11 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
         const auto h0 = std::chrono::steady_clock::now();
         begin_step(i + 1);
         const double* V1 = Vb[(i + 1) % 3];
-        const OpDev op1 = frob_merged_op(g, V1, r, n, r, eps1, eta_eval(*sch, t1), s->pack + s->pack_epi + (r + 1));
+        OpDev op1 = frob_merged_op(g, V1, r, n, r, eps1, eta_eval(*sch, t1), s->pack + s->pack_epi + (r + 1));
+        // L^T U = V_{t+1}^T W_{t+1} is block [0:r, 0:bw] of the Ritz-block Gram step t's
+        // Rayleigh-Ritz launch just reduced (same rows, same order: bit-identical to reducing it again)
+        op1.Eg = s->pack + s->pack_gram;
+        op1.ldg = sh.bw;
         fast_step_enqueue(s, op1, r, sh, P0.tol, Wb[(i + 1) % 3], 64, eps_eval(*sch, t1 + 1), Wb[(i + 2) % 3], 64,
                           Vb[(i + 2) % 3], r, hspec[(i + 1) & 1], done[(i + 1) & 1], fs[(i + 1) & 1]);
         end_step(i + 1);
