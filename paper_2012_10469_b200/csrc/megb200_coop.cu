@@ -590,22 +590,33 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
   phase_mark(10);
   // small Rayleigh-Ritz problems are solved here by CTA 0; large ones (m > 48)
   // arrive pre-solved from k_rr_jacobi (1024 threads) -- flagged by info == nullptr
-  if (blockIdx.x == 0 && info) block_jacobi(H, ldh, m, theta, S, sm, info);
-  phase_mark(11);
-  grid.sync();
-  phase_mark(12);
   const int cols = m;
   double* Ss = sm;
   double* Qs = sm + cols * rq;    // chunk rows of Q (kRC x cols)
   double* As = Qs + kRC * cols;   // chunk rows of AQ
   double* red = As + kRC * cols;  // kCT
+  int64_t r0, r1;
+  cta_rows(n, r0, r1);
+  // a CTA whose rows fit one chunk stages them while CTA 0 solves the Rayleigh-Ritz problem
+  const bool prestaged = (r1 - r0) <= kRC && (blockIdx.x != 0 || !info);
+  if (prestaged) {
+    const int rows = (int)(r1 - r0);
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < rows * cols; idx += kCT) {
+      const int r = idx / cols, k = idx - r * cols;
+      Qs[idx] = Q[(r0 + r) * ldq + k];
+      As[idx] = AQ[(r0 + r) * ldq + k];
+    }
+  }
+  if (blockIdx.x == 0 && info) block_jacobi(H, ldh, m, theta, S, sm, info);
+  phase_mark(11);
+  grid.sync();
+  phase_mark(12);
   #pragma unroll 1
   for (int idx = threadIdx.x; idx < cols * rq; idx += kCT) {
     const int k = idx / rq, c = idx - k * rq;
     Ss[idx] = S[k * m + c];
   }
-  int64_t r0, r1;
-  cta_rows(n, r0, r1);
   const int rpt = kCT / rq;
   const int c = threadIdx.x % rq;
   const int rofs = threadIdx.x / rq;
@@ -614,14 +625,16 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
   for (int64_t rc = r0; rc < r1; rc += kRC) {
     const int rows = (int)min((int64_t)kRC, r1 - rc);
     __syncthreads();
-    // stage the chunk's rows of Q and AQ with independent coalesced loads
-    #pragma unroll 1
-    for (int idx = threadIdx.x; idx < rows * cols; idx += kCT) {
-      const int r = idx / cols, k = idx - r * cols;
-      Qs[idx] = Q[(rc + r) * ldq + k];
-      As[idx] = AQ[(rc + r) * ldq + k];
+    if (!prestaged) {
+      // stage the chunk's rows of Q and AQ with independent coalesced loads
+#pragma unroll 1
+      for (int idx = threadIdx.x; idx < rows * cols; idx += kCT) {
+        const int r = idx / cols, k = idx - r * cols;
+        Qs[idx] = Q[(rc + r) * ldq + k];
+        As[idx] = AQ[(rc + r) * ldq + k];
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (rofs < rpt) {
       #pragma unroll 1
       for (int rr = rofs; rr < rows; rr += rpt) {

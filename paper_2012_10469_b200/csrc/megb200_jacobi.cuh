@@ -112,6 +112,7 @@ __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, 
       else Z = V;
     }
     // Y = I + X
+    double xmax = 0.0;
 #pragma unroll 1
     for (int idx = t; idx < mm; idx += nth) {
       const int i = idx / mp, j = idx - i * mp;
@@ -119,22 +120,35 @@ __device__ inline void block_jacobi(const double* __restrict__ Hg, int64_t ldh, 
       if (i != j) {
         const double h = H[idx], d = H[j * mp + j] - H[i * mp + i];
         y = (h != 0.0 && fabs(h) <= 0.1 * fabs(d)) ? h / d : 0.0;
+        xmax = fmax(xmax, fabs(y));
       }
       Y[idx] = y;
     }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, off));
+    if ((t & 31) == 0) red[32 + (t >> 5)] = xmax;
     __syncthreads();
-    // Tm = (3I - Y^T Y) / 2
+    xmax = 0.0;
 #pragma unroll 1
-    for (int idx = t; idx < mm; idx += nth) {
-      const int i = idx / mp, j = idx - i * mp;
-      Tm[idx] = 0.5 * ((i == j ? 3.0 : 0.0) - jdot(Y, i, mp, Y, j, mp, mp));
-    }
-    __syncthreads();
-    // Z = S = Y Tm
+    for (int w = 0; w < (nth >> 5); ++w) xmax = fmax(xmax, red[32 + w]);
+    if (xmax < 1e-8) {
+      // Y^T Y = I + O(|X|^2) < 1e-16 off the identity: the Newton-Schulz step would not change S
 #pragma unroll 1
-    for (int idx = t; idx < mm; idx += nth) {
-      const int i = idx / mp, j = idx - i * mp;
-      Z[idx] = jdot(Y, i * mp, 1, Tm, j, mp, mp);
+      for (int idx = t; idx < mm; idx += nth) Z[idx] = Y[idx];
+    } else {
+      // Tm = (3I - Y^T Y) / 2
+#pragma unroll 1
+      for (int idx = t; idx < mm; idx += nth) {
+        const int i = idx / mp, j = idx - i * mp;
+        Tm[idx] = 0.5 * ((i == j ? 3.0 : 0.0) - jdot(Y, i, mp, Y, j, mp, mp));
+      }
+      __syncthreads();
+      // Z = S = Y Tm
+#pragma unroll 1
+      for (int idx = t; idx < mm; idx += nth) {
+        const int i = idx / mp, j = idx - i * mp;
+        Z[idx] = jdot(Y, i * mp, 1, Tm, j, mp, mp);
+      }
     }
     __syncthreads();
     // Tm = H S;  Y = Vs S (the new accumulated rotations)

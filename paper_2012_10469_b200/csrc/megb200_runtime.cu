@@ -352,7 +352,11 @@ EigShape eig_shape(const megb200_solver* s, int nreq, const EigParams& P) {
   // is honoured as a lower bound; a block method needs several blocks per cycle,
   // so the default is 6 blocks (<= 112, the Rayleigh-Ritz limit)
   if (P.basis > 0 && P.block <= 0) bw = std::max(1, std::min(bw, P.basis / 2));
-  int mmax = std::max({P.basis > 0 ? P.basis : 0, 6 * bw, 2 * nreq + 10, 30});
+  static const int blocks_per_basis = [] {  // diagnostics override (MEGB200_BASIS_BLOCKS), default 6
+    const char* e = getenv("MEGB200_BASIS_BLOCKS");
+    return e ? std::max(2, atoi(e)) : 6;
+  }();
+  int mmax = std::max({P.basis > 0 ? P.basis : 0, blocks_per_basis * bw, 2 * nreq + 10, 30});
   bw = std::max(1, std::min<int>(bw, s->max_block));
   mmax = std::min<int>(mmax, s->max_basis);
   mmax = std::max(mmax, std::min<int>(nreq + bw, s->max_basis));

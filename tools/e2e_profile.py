@@ -39,11 +39,10 @@ lam, eps, warm, werr = x.lam.copy(), x.eps, x.warm_block, x.warm_orth_err
 def loop(K):
     global Vh, Vn, lam, eps, warm, werr, t
     for _ in range(K):
-        xi = pb.LowRankIterate(w.n, w.r, Vh, lam, eps, warm_block=warm, warm_orth_err=werr)
-        res = step(xi, t)
-        Vn.copy_(res.iterate.V_device, non_blocking=True)
+        res = pb.lowrank_meg_step_host(Vh, lam, eps, obj, w.eta(t), w.eps(t + 1), svd_seed=t,
+                                       svd_subspace=w.subspace, block=w.block, warm=warm, warm_orth_err=werr, out=Vn)
         Vh, Vn = Vn, Vh
-        lam, eps, warm, werr = res.iterate.lam, res.iterate.eps, res.iterate.warm_block, res.iterate.warm_orth_err
+        lam, eps, warm, werr = res.lam, res.eps, res.warm_block, res.warm_orth_err
         t += 1
 
 
