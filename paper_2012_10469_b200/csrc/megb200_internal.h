@@ -144,4 +144,51 @@ void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta
              double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi, double* V2 = nullptr,
              int64_t ld2 = 0, int r2 = 0);
 
+// First pass of a solve fused with its finish and Rayleigh-Ritz (megb200_step.cu):
+// W = scale * sum_s part[s] + L E + alpha U, H = U^T W, Jacobi RR, Ritz block T,
+// residuals, Gram of T, step epilogue, result pack (device + optional host slot),
+// in one launch.  Cross-CTA reductions by last-CTA tickets in fixed CTA order.
+constexpr int kFusedMaxL = 64;
+constexpr int kFusedStride = 2048;  // doubles per CTA partial (>= l*b, b*b, nreq + gr*gr)
+constexpr int kFusedFlags = 96;    // sync[0..95]: tickets of the three reductions, then release flags
+struct FusedPassArgs {
+  int64_t n = 0;
+  int b = 0, R = 0;
+  const double* part = nullptr;  // S x n x b pass partials
+  int S = 0;
+  double scale = 0.0, alpha = 0.0;
+  const double* L = nullptr;
+  int64_t ldl = 0;
+  int l = 0;
+  const double* d = nullptr;  // host-provided coefficients (device), or from lc
+  LamCoef lc;
+  const double* Eg = nullptr;  // precomputed L^T U (l x b, ld ldg) or null
+  int64_t ldg = 0;
+  const double* U = nullptr;
+  int64_t ldu = 0;
+  double* W = nullptr;
+  int64_t ldw = 0;
+  double* H = nullptr;
+  int64_t ldh = 0;
+  double *theta = nullptr, *Sout = nullptr, *info = nullptr;
+  double* T = nullptr;
+  int64_t ldt = 0;
+  double* V2 = nullptr;
+  int64_t ld2 = 0;
+  int r2 = 0;
+  double *resid = nullptr, *gram = nullptr;
+  int gr = 0, nreq = 0, rq = 0;
+  double* epi = nullptr;
+  double eps_next = 0.0;
+  double *part0 = nullptr, *part1 = nullptr, *part2 = nullptr, *Ews = nullptr;
+  unsigned* sync = nullptr;  // tickets [0..95] (32 per reduction), flags [96..97]
+  unsigned epoch = 0;
+  const double* pack = nullptr;  // device result pack, copied to host_pack[0:pack_count] at the end
+  double* host_pack = nullptr;
+  int pack_count = 0;
+  unsigned long long* stamps = nullptr;  // diagnostics: phase timestamps (or null)
+};
+bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count);
+void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count);
+
 }  // namespace megb200

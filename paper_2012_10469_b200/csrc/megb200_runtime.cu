@@ -69,7 +69,10 @@ struct megb200_solver {
   double* csr_g = nullptr;  // max_nnz
   double* rowsq = nullptr;  // n
   double* h_buf = nullptr;  // pinned host staging
+  double* h_buf_dev = nullptr;  // its device alias (mapped pinned memory), or null
   int64_t h_buf_len = 0;
+  unsigned* fsync = nullptr;  // tickets / flags of the fused first-pass kernel (zeroed)
+  unsigned epoch = 0;
   double m_norm2_cache = NAN, m_trace_cache = NAN;
   const void* m_cache_ptr = nullptr;
   // run-loop buffers (allocated on first megb200_meg_run)
@@ -193,8 +196,8 @@ struct OpDev {
   int64_t ldg = 0;
 };
 
-void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k, double* W, int64_t ldw,
-              int hp = 0, double* Hout = nullptr) {
+// Streamed operand pass alone: partial slices of Op U into s->part; returns the slice count.
+int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k) {
   Launch L = s->launch();
   const int64_t n = s->n;
   int S = 0;
@@ -223,7 +226,14 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
     s->prof_bytes += b;
     s->prof_passes++;
   }
-  coop_finish(L, n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
+  return S;
+}
+
+void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k, double* W, int64_t ldw,
+              int hp = 0, double* Hout = nullptr) {
+  Launch L = s->launch();
+  const int S = pass_launch(s, op, U, ldu, k);
+  coop_finish(L, s->n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
               s->sm_count, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap, op.lc, op.Eg, op.ldg);
 }
 
@@ -418,6 +428,77 @@ int rr_readback(megb200_solver* s, int newcols, int nreq, int bw, const EpiSpec*
   return gr;
 }
 
+// The first pass of a solve through the fused kernel (megb200_step.cu): pass, then
+// finish + H + Rayleigh-Ritz + Ritz block + residuals + Gram (+ epilogue) in one
+// launch whose result pack lands in dst (pinned; written by the kernel itself when
+// the staging buffer is mapped).  Same outputs as block_pass + rr_readback.
+// per reduction: G partials + ceil(G / 8) group partials + the result, kFusedStride doubles each
+constexpr int64_t kFusedPart1 = (148 + 19 + 1) * (int64_t)kFusedStride;  // offsets in s->red
+constexpr int64_t kFusedPart2 = 2 * kFusedPart1;
+constexpr int64_t kFusedRed = 3 * kFusedPart1;
+
+bool fused_ok(const megb200_solver* s, const OpDev& op, int bw, int nreq) {
+  static const bool off = getenv("MEGB200_NO_FUSED") != nullptr;  // diagnostics: the two-kernel path
+  return !off && s->sm_count <= 148 && s->red_cap >= kFusedRed && op.l <= kFusedMaxL && op.l <= s->max_lowrank &&
+         nreq <= bw && fused_pass_supported(s->n, bw, op.l, nreq, s->sm_count);
+}
+
+int fused_pass(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int bw, int nreq, const EpiSpec* epi,
+               double* tdst, int64_t ldt, double* v2, int64_t ld2, int r2, double* dst) {
+  Launch L = s->launch();
+  const int S = pass_launch(s, op, U, ldu, bw);
+  FusedPassArgs a;
+  a.n = s->n;
+  a.b = bw;
+  a.part = s->part;
+  a.S = S;
+  a.scale = op.scale;
+  a.alpha = op.alpha;
+  a.L = op.L;
+  a.ldl = op.ldl;
+  a.l = op.L ? op.l : 0;
+  a.d = op.d_dev;
+  a.lc = op.lc;
+  a.Eg = op.Eg;
+  a.ldg = op.ldg;
+  a.U = U;
+  a.ldu = ldu;
+  a.W = s->AQ;
+  a.ldw = s->ldq;
+  a.H = s->H;
+  a.ldh = s->cap;
+  a.theta = s->theta;
+  a.Sout = s->S;
+  a.info = s->info;
+  a.T = tdst ? tdst : s->T;
+  a.ldt = tdst ? ldt : s->ldq;
+  a.V2 = v2;
+  a.ld2 = ld2;
+  a.r2 = v2 ? r2 : 0;
+  a.resid = s->resid;
+  a.rq = bw;
+  a.gr = epi ? bw : 0;
+  a.gram = s->pack + s->pack_gram;
+  a.nreq = nreq;
+  a.epi = epi ? s->pack + s->pack_epi : nullptr;
+  a.eps_next = epi ? epi->eps_next : 0.0;
+  a.part0 = s->red;
+  a.part1 = s->red + kFusedPart1;
+  a.part2 = s->red + kFusedPart2;
+  a.Ews = s->E;
+  a.sync = s->fsync;
+  if (++s->epoch == 0) ++s->epoch;
+  a.epoch = s->epoch;
+  a.pack = s->pack;
+  a.pack_count = (int)(s->pack_gram + (int64_t)a.gr * a.gr);
+  a.host_pack = s->h_buf_dev ? s->h_buf_dev + (dst - s->h_buf) : nullptr;
+  static const bool stamps = getenv("MEGB200_FUSED_STAMPS") != nullptr;
+  if (stamps) a.stamps = reinterpret_cast<unsigned long long*>(s->fsync + 128);
+  fused_first_pass(L, a, s->sm_count);
+  if (!a.host_pack) s->d2h(dst, s->pack, a.pack_count);
+  return a.gr;
+}
+
 // Convergence decision on a read-back pack (linalg.py:212-216): every wanted
 // residual <= tol * max(1, max |theta|), or the basis spans R^n.
 struct RRDecision {
@@ -474,8 +555,10 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   int cols = 0, cur = bw;
   double scale = 1.0;
   for (;;) {
-    // operator pass on the current block, then its column of H = Q^T A Q
-    block_pass(s, op, cols, cur);
+    // operator pass on the current block, then its column of H = Q^T A Q; the first pass
+    // of a solve runs fused with its Rayleigh-Ritz (one launch after the pass)
+    const bool fuse = cols == 0 && cur == bw && fused_ok(s, op, bw, nreq);
+    if (!fuse) block_pass(s, op, cols, cur);
     run.passes++;
     s->mark("pass+finish");
     const int newcols = cols + cur;
@@ -491,7 +574,8 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       double* v2 = vec_out ? vec_out : (epi ? epi->v_next : nullptr);
       const int64_t ld2 = vec_out ? ld_vec : (epi ? epi->ld_next : 0);
       const int r2 = vec_out ? nreq : (epi ? epi->r : 0);
-      const int gr = rr_readback(s, newcols, nreq, bw, epi, pk, ritz_out, ld_ritz, v2, ld2, r2);
+      const int gr = fuse ? fused_pass(s, op, s->Q, s->ldq, bw, nreq, epi, ritz_out, ld_ritz, v2, ld2, r2, pk)
+                          : rr_readback(s, newcols, nreq, bw, epi, pk, ritz_out, ld_ritz, v2, ld2, r2);
       const int rq = std::min(newcols, std::max(nreq, bw));
       // host-buffer step: V_next travels back with the pack (one wait when this RR converges)
       if (epi && epi->v_host && epi->v_next && epi->ld_next == epi->r && epi->ld_host == epi->r)
@@ -923,6 +1007,19 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
       delete s;
       throw Error(MEGB200_ERR_CUDA, "pinned staging allocation failed");
     }
+    // device alias of the pinned staging buffer: the fused first-pass kernel writes its result pack there
+    void* hd = nullptr;
+    if (cudaHostGetDevicePointer(&hd, s->h_buf, 0) == cudaSuccess && getenv("MEGB200_NO_ZEROCOPY") == nullptr)
+      s->h_buf_dev = static_cast<double*>(hd);
+    cudaGetLastError();
+    e = cudaMalloc(&s->fsync, 128 * sizeof(unsigned) + 64 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(s->fsync, 0, 128 * sizeof(unsigned) + 64 * sizeof(unsigned long long));
+    if (e != cudaSuccess) {
+      cudaFree(s->arena);
+      cudaFreeHost(s->h_buf);
+      delete s;
+      throw Error(MEGB200_ERR_CUDA, "sync flag allocation failed");
+    }
     *out = s;
   });
 }
@@ -937,6 +1034,7 @@ void megb200_solver_destroy(megb200_solver* s) {
   if (s->host_io) cudaFree(s->host_io);
   cudaFreeHost(s->h_buf);
   cudaFreeHost(s->h_up);
+  if (s->fsync) cudaFree(s->fsync);
   delete s;
 }
 
@@ -1060,12 +1158,17 @@ void fast_step_enqueue(megb200_solver* s, const OpDev& op, int r, const EigShape
   fs.tol = tol;
   fs.dst = dst;
   fs.done = done;
-  copy_block(L, n, sh.bw, warm, ld_warm, s->Q, s->ldq);
-  block_pass(s, op, 0, sh.bw);
   EpiSpec epi;
   epi.r = r;
   epi.eps_next = eps_next;
-  fs.gr = rr_readback(s, sh.bw, fs.nreq, sh.bw, &epi, dst, ritz_out, ld_ritz, V_next, ld_next, r);
+  if (fused_ok(s, op, sh.bw, fs.nreq)) {
+    // the fused first pass reads the warm block in place (no copy into the basis)
+    fs.gr = fused_pass(s, op, warm, ld_warm, sh.bw, fs.nreq, &epi, ritz_out, ld_ritz, V_next, ld_next, r, dst);
+  } else {
+    copy_block(L, n, sh.bw, warm, ld_warm, s->Q, s->ldq);
+    block_pass(s, op, 0, sh.bw);
+    fs.gr = rr_readback(s, sh.bw, fs.nreq, sh.bw, &epi, dst, ritz_out, ld_ritz, V_next, ld_next, r);
+  }
   MEG_CUDA(cudaEventRecord(done, s->stream));
 }
 
@@ -1657,6 +1760,15 @@ int megb200_gen_dense_target(megb200_solver* s, const double* U, int64_t r, cons
     s->h2d(s->small, lam_host, r);
     gen_dense_target(s->launch(), U, r, s->small, sigma, stream_key(seed, (uint64_t)stream), M, dtype, ld, s->n);
     s->sync();
+  });
+}
+
+// Diagnostics (not part of the ABI header): phase timestamps of the last fused first pass
+// (solver run with MEGB200_FUSED_STAMPS=1).
+int megb200_debug_fused_ns(megb200_solver* s, unsigned long long* out, int32_t count) {
+  return guarded_impl([&] {
+    if (!s || !out || count < 1 || count > 64) throw Error(MEGB200_ERR_PARAM, "bad arguments");
+    MEG_CUDA(cudaMemcpy(out, s->fsync + 128, count * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   });
 }
 

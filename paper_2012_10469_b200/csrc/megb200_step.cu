@@ -1,0 +1,459 @@
+// First-pass finish + Rayleigh-Ritz + Ritz block + residuals + step epilogue
+// in ONE launch (the steady-state MEG step is: operand pass, this kernel).
+//
+// Replaces, for the first pass of a solve (block of bw <= 32 columns), the pair
+// k_coop_finish + k_coop_rr and their three grid barriers.  G <= #SMs CTAs of
+// 256 threads each own a contiguous row range, staged once in shared memory;
+// the cross-CTA steps use "last CTA" tickets instead of grid barriers: every
+// CTA writes its partial, the CTA that arrives last reduces all partials in a
+// FIXED CTA order (warp xor-trees: bitwise reproducible whichever CTA is last),
+// runs the serial part and publishes it with a release flag the others spin on
+// (all CTAs are co-resident: G <= #SMs, one CTA per SM at most).
+//
+//   phase 0  (only without a precomputed L^T U)  E = diag(d) L^T U
+//   phase 1  W = scale * sum_s part[s] + L E + alpha U   (rows, -> AQ)
+//            H = U^T W (upper triangle) -> last CTA: Jacobi Rayleigh-Ritz
+//            (linalg.py:205-211) + step epilogue (meg.py:347-356)
+//   phase 2  T = U S (Ritz block, V_next), residuals ||W s_j - theta_j T_j||
+//            (linalg.py:212-216), Gram of T -> last CTA: reduce, write the
+//            result pack to device memory and to the caller's pinned host slot.
+//
+// The phase-0 partial of L^T U and the phase-2 Gram partial use the same
+// per-row fma order and the same cross-CTA tree, so a pipelined step that takes
+// E from the previous step's Ritz-block Gram is bit-identical to one that
+// reduces L^T U again (L = V_next = first r Ritz vectors, U = the Ritz block).
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "megb200_internal.h"
+
+#define JACOBI_MARK(slot)
+#include "megb200_jacobi.cuh"
+
+namespace megb200 {
+namespace {
+
+constexpr int kFT = 256;  // threads per CTA
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// sum_{j < cnt} part[(g0 + j) * stride + o] in index order by ONE thread: the loads are
+// issued eight at a time before they are added, neighbouring threads take neighbouring o
+__device__ __forceinline__ double ordered_sum(const double* part, int g0, int cnt, int64_t stride, int o) {
+  double s = 0.0;
+  for (int j0 = 0; j0 < cnt; j0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = j0 + j < cnt ? __ldcg(part + (int64_t)(g0 + j0 + j) * stride + o) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
+  }
+  return s;
+}
+
+// Every thread's partial-sum stores are fenced, then one atomic ticket per CTA;
+// returns true (in all threads) in the CTA that arrived last of `expected`, which
+// re-arms the ticket.
+__device__ __forceinline__ bool arrive_last(unsigned* ticket, unsigned expected, int* s_flag) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(ticket, 1u);
+    const bool last = (t == expected - 1);
+    if (last) atomicExch(ticket, 0u);
+    *s_flag = last;
+  }
+  __syncthreads();
+  const bool last = *s_flag != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+// Two-level fixed-order reduction of the per-CTA partials part[g * stride + o], o < count:
+// groups of kGroup consecutive CTAs (the last CTA of a group sums its group in CTA order
+// into gpart), then the last group finisher sums the group partials in group order into
+// res.  Returns true in the one CTA that wrote res (whichever CTAs arrive last, the
+// association -- hence every bit of res -- is the same).  tick: 1 + #groups tickets.
+constexpr int kGroup = 8;
+__device__ __forceinline__ bool tree_reduce(const double* part, double* gpart, double* res, int count,
+                                            int64_t stride, unsigned* tick, int* s_flag) {
+  const int G = gridDim.x, NG = (G + kGroup - 1) / kGroup, grp = blockIdx.x / kGroup;
+  const int g0 = grp * kGroup, gn = min(kGroup, G - g0);
+  if (!arrive_last(tick + 1 + grp, (unsigned)gn, s_flag)) return false;
+  for (int o = threadIdx.x; o < count; o += kFT) gpart[grp * stride + o] = ordered_sum(part, g0, gn, stride, o);
+  if (!arrive_last(tick, (unsigned)NG, s_flag)) return false;
+  for (int o = threadIdx.x; o < count; o += kFT) res[o] = ordered_sum(gpart, 0, NG, stride, o);
+  __threadfence_block();
+  __syncthreads();
+  return true;
+}
+
+__device__ __forceinline__ void publish(unsigned* flag, unsigned epoch) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release_u32(flag, epoch);
+}
+
+__device__ __forceinline__ void wait_published(const unsigned* flag, unsigned epoch) {
+  if (threadIdx.x == 0)
+    while (ld_acquire_u32(flag) != epoch) {
+    }
+  __syncthreads();
+}
+
+// acc = sum over the CTA's rows of X[r, a] * Y[r, c]: even and odd rows in two chains,
+// added at the end (shared by the L^T U partial and the Gram partial: same products,
+// same order)
+__device__ __forceinline__ double rows_dot(const double* X, int ldx, int a, const double* Y, int ldy, int c,
+                                           int rows) {
+  double e = 0.0, o = 0.0;
+  int r = 0;
+#pragma unroll 2
+  for (; r + 1 < rows; r += 2) {
+    e = fma(X[r * ldx + a], Y[r * ldy + c], e);
+    o = fma(X[(r + 1) * ldx + a], Y[(r + 1) * ldy + c], o);
+  }
+  if (r < rows) e = fma(X[r * ldx + a], Y[r * ldy + c], e);
+  return e + o;
+}
+
+// diagnostics: %globaltimer at phase boundaries (a.stamps, MEGB200_FUSED_STAMPS=1)
+__device__ __forceinline__ void stamp(unsigned long long* st, int slot) {
+  if (st && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    st[slot] = v;
+  }
+}
+
+// dst[r * w + c] = src[(r0 + r) * ld + c] for r < rows, c < w: eight independent loads in
+// flight per thread before the shared-memory stores
+__device__ __forceinline__ void stage_rows(double* dst, const double* __restrict__ src, int64_t ld, int64_t r0,
+                                           int rows, int w) {
+  const int total = rows * w;
+  for (int base = threadIdx.x; base < total; base += 8 * kFT) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int idx = base + j * kFT;
+      const int r = idx / w, c = idx - r * w;
+      v[j] = idx < total ? src[(r0 + r) * ld + c] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int idx = base + j * kFT;
+      if (idx < total) dst[idx] = v[j];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs a) {
+  // programmatic dependent launch after the operand pass: nothing is read before it completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  unsigned long long* st0 = blockIdx.x == 0 ? a.stamps : nullptr;
+  stamp(st0, 0);
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double dsh[kFusedMaxL];
+  __shared__ double thsh[64];
+  __shared__ int s_flag;
+  const int t = threadIdx.x, g = blockIdx.x, G = gridDim.x;
+  const int b = a.b, l = a.l, rq = a.rq, R = a.R;
+  const int64_t r0 = min(a.n, (int64_t)g * R);
+  const int rows = (int)(min(a.n, r0 + (int64_t)R) - r0);
+  double* Us = sm;            // R x b
+  double* Ws = Us + R * b;    // R x b
+  double* Ss = Ws + R * b;    // b x rq
+  double* red = Ss + b * rq;  // kFT
+  double* Ls = red + kFT;     // R x l      } phases 0-1
+  double* Es = Ls + R * l;    // l x b      }
+  double* jac = Es + l * b;   // Jacobi scratch (the last CTA of phase 1)
+  double* Ts = Ls;            // R x rq: phase 2 (reuses the phase 0-1 region)
+
+  // log-map coefficients: from the device-resident kept weights (lc) or as given
+  for (int k = t; k < l; k += kFT) {
+    double v;
+    if (a.lc.lam && k < a.lc.lr) {
+      const double kept = a.lc.c1 * a.lc.lam[k];
+      v = (log(kept) - a.lc.log_tail) + (-a.lc.eta * (kept - a.lc.tail_g));
+    } else {
+      v = a.d[k];
+    }
+    dsh[k] = v;
+  }
+  stage_rows(Us, a.U, a.ldu, r0, rows, b);
+  if (l > 0) stage_rows(Ls, a.L, a.ldl, r0, rows, l);
+  __syncthreads();
+  stamp(st0, 1);
+
+  // ---- phase 0: E = diag(d) L^T U
+  if (l > 0) {
+    if (a.Eg) {
+      for (int idx = t; idx < l * b; idx += kFT) {
+        const int k = idx / b, c = idx - k * b;
+        Es[idx] = dsh[k] * a.Eg[k * a.ldg + c];
+      }
+    } else {
+      double* p0 = a.part0 + (int64_t)g * kFusedStride;
+      for (int o = t; o < l * b; o += kFT) {
+        const int k = o / b, c = o - k * b;
+        p0[o] = rows_dot(Ls, l, k, Us, b, c, rows);
+      }
+      if (tree_reduce(a.part0, a.part0 + (int64_t)G * kFusedStride, a.Ews, l * b, kFusedStride, a.sync,
+                      &s_flag))
+        publish(a.sync + kFusedFlags, a.epoch);
+      else
+        wait_published(a.sync + kFusedFlags, a.epoch);
+      for (int idx = t; idx < l * b; idx += kFT) Es[idx] = dsh[idx / b] * __ldcg(a.Ews + idx);
+    }
+  }
+  __syncthreads();
+
+  stamp(st0, 2);
+  // ---- phase 1: W rows, H = U^T W
+  {
+    const int64_t slice = a.n * b;
+    for (int idx = t; idx < rows * b; idx += kFT) {
+      const int rr = idx / b, c = idx - rr * b;
+      const int64_t i = r0 + rr;
+      const double* pp = a.part + i * b + c;
+      double pv[16];  // all slices' loads in flight before the (ordered) sum
+#pragma unroll
+      for (int tt = 0; tt < 16; ++tt) pv[tt] = tt < a.S ? pp[tt * slice] : 0.0;
+      double s = 0.0;
+#pragma unroll
+      for (int tt = 0; tt < 16; ++tt) s += pv[tt];
+      for (int tt = 16; tt < a.S; ++tt) s += pp[tt * slice];
+      const double* Lr = Ls + rr * l;
+      double v0 = a.scale * s + a.alpha * Us[idx], v1 = 0.0;
+      int k = 0;
+      for (; k + 1 < l; k += 2) {
+        v0 = fma(Lr[k], Es[k * b + c], v0);
+        v1 = fma(Lr[k + 1], Es[(k + 1) * b + c], v1);
+      }
+      if (k < l) v0 = fma(Lr[k], Es[k * b + c], v0);
+      const double wv = v0 + v1;
+      Ws[idx] = wv;
+      a.W[i * a.ldw + c] = wv;
+    }
+    __syncthreads();
+    double* p1 = a.part1 + (int64_t)g * kFusedStride;
+    for (int o = t; o < b * b; o += kFT) {
+      const int ia = o / b, c = o - ia * b;
+      p1[o] = ia <= c ? rows_dot(Us, b, ia, Ws, b, c, rows) : 0.0;
+    }
+  }
+  stamp(st0, 3);
+  double* hres = a.part1 + (int64_t)(G + (G + kGroup - 1) / kGroup) * kFusedStride;
+  if (tree_reduce(a.part1, a.part1 + (int64_t)G * kFusedStride, hres, b * b, kFusedStride, a.sync + 32,
+                  &s_flag)) {
+    stamp(a.stamps, 4);
+    for (int o = t; o < b * b; o += kFT) {
+      const int ia = o / b, c = o - ia * b;
+      if (ia <= c) a.H[ia * a.ldh + c] = hres[o];
+    }
+    __threadfence_block();
+    __syncthreads();
+    stamp(a.stamps, 5);
+    block_jacobi(a.H, a.ldh, b, a.theta, a.Sout, jac, a.info);
+    __syncthreads();
+    stamp(a.stamps, 6);
+    if (a.epi && t < 32) {
+      // step epilogue (meg.py:347-356), lane k (and k + 32) owning pair k:
+      // y = exp(mu - mu_1), lam = y[:r] / sum renormalised, lambda_{r+1}, b_{r+1}, cheap certificate
+      const int lane = t;
+      const int r = a.nreq - 1;
+      const double* theta = a.theta;
+      double* epi = a.epi;
+      const double shift = theta[0];
+      double y[2], lam[2];
+      double kept = 0.0, bsum = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = lane + 32 * h;
+        y[h] = k <= r ? exp(theta[k] - shift) : 0.0;
+        if (k <= r) epi[k] = y[h];
+        kept += k < r ? y[h] : 0.0;
+        bsum += y[h];
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        kept += __shfl_xor_sync(0xffffffffu, kept, off);
+        bsum += __shfl_xor_sync(0xffffffffu, bsum, off);
+      }
+      double lsum = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        lam[h] = (lane + 32 * h) < r ? y[h] / kept : 0.0;
+        lsum += lam[h];
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (lane + 32 * h < r) epi[r + 1 + lane + 32 * h] = lam[h] / lsum;
+      __syncwarp();
+      if (lane == 0) {
+        double status = !(kept > 1e-290) ? 4.0 : 0.0;
+        const double lam_rp1 = epi[r];
+        double lhs;
+        if (!(bsum > 0.0) || lam_rp1 < 0.0) {
+          status = 1.0;
+          lhs = 0.0;
+        } else if (lam_rp1 == 0.0) {
+          lhs = -INFINITY;
+        } else {
+          lhs = log((double)(a.n - r) * lam_rp1 / (a.eps_next * bsum));
+        }
+        double* tail = epi + 2 * r + 1;
+        tail[0] = lam_rp1;
+        tail[1] = bsum;
+        tail[2] = shift;
+        tail[3] = lhs;
+        tail[4] = (lhs <= 2.0 * a.eps_next) ? 1.0 : 0.0;
+        tail[5] = 2.0 * a.eps_next;
+        tail[6] = status;
+      }
+    }
+    publish(a.sync + kFusedFlags + 1, a.epoch);
+    stamp(a.stamps, 7);
+  } else {
+    wait_published(a.sync + kFusedFlags + 1, a.epoch);
+  }
+  stamp(st0, 8);
+
+  // ---- phase 2: Ritz block, residuals, Gram
+  for (int idx = t; idx < b * rq; idx += kFT) {
+    const int k = idx / rq, c = idx - k * rq;
+    Ss[idx] = __ldcg(a.Sout + k * b + c);
+  }
+  for (int c = t; c < rq; c += kFT) thsh[c] = __ldcg(a.theta + c);
+  __syncthreads();
+  const int rpt = kFT / rq;
+  const int c = t % rq;
+  const int rofs = t / rq;
+  double sq = 0.0;
+  if (rofs < rpt) {
+    const double th = c < a.nreq ? thsh[c] : 0.0;
+    for (int rr = rofs; rr < rows; rr += rpt) {
+      const double* ur = Us + rr * b;
+      double x0 = 0.0, x1 = 0.0;
+      int k = 0;
+      for (; k + 1 < b; k += 2) {
+        x0 = fma(ur[k], Ss[k * rq + c], x0);
+        x1 = fma(ur[k + 1], Ss[(k + 1) * rq + c], x1);
+      }
+      if (k < b) x0 = fma(ur[k], Ss[k * rq + c], x0);
+      const double x = x0 + x1;
+      const int64_t i = r0 + rr;
+      a.T[i * a.ldt + c] = x;
+      Ts[rr * rq + c] = x;
+      if (c < a.r2) a.V2[i * a.ld2 + c] = x;
+      if (c < a.nreq) {
+        const double* wr = Ws + rr * b;
+        double y0 = 0.0, y1 = 0.0;
+        k = 0;
+        for (; k + 1 < b; k += 2) {
+          y0 = fma(wr[k], Ss[k * rq + c], y0);
+          y1 = fma(wr[k + 1], Ss[(k + 1) * rq + c], y1);
+        }
+        if (k < b) y0 = fma(wr[k], Ss[k * rq + c], y0);
+        const double d = (y0 + y1) - th * x;
+        sq = fma(d, d, sq);
+      }
+    }
+  }
+  red[t] = sq;
+  __syncthreads();  // also publishes Ts
+  const int pw = a.nreq + a.gr * a.gr;
+  double* p2 = a.part2 + (int64_t)g * kFusedStride;
+  if (t < a.nreq) {
+    double s2 = 0.0;
+    for (int j = t; j < rpt * rq; j += rq) s2 += red[j];
+    p2[t] = s2;
+  }
+  if (a.gr > 0) {
+    // same product order as the phase-0 partial
+    for (int o = t; o < a.gr * a.gr; o += kFT) {
+      const int ia = o / a.gr, cc = o - ia * a.gr;
+      p2[a.nreq + o] = rows_dot(Ts, rq, ia, Ts, rq, cc, rows);
+    }
+  }
+  stamp(st0, 9);
+  double* res2 = a.part2 + (int64_t)(G + (G + kGroup - 1) / kGroup) * kFusedStride;
+  if (tree_reduce(a.part2, a.part2 + (int64_t)G * kFusedStride, res2, pw, kFusedStride, a.sync + 64, &s_flag)) {
+    stamp(a.stamps, 10);
+    for (int o = t; o < pw; o += kFT) {
+      const double v = res2[o];
+      if (o < a.nreq)
+        a.resid[o] = sqrt(v);
+      else
+        a.gram[o - a.nreq] = v;
+    }
+    __threadfence_block();
+    __syncthreads();
+    stamp(a.stamps, 11);
+    if (a.host_pack) {
+      // the result pack straight into the caller's pinned host slot (no separate read-back copy)
+      for (int idx = t; idx < a.pack_count; idx += kFT) a.host_pack[idx] = __ldcg(a.pack + idx);
+    }
+    stamp(a.stamps, 12);
+  }
+}
+
+}  // namespace
+
+int fused_pass_rows(int64_t n, int sm_count) {
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count, (n + 15) / 16));
+  return (int)((n + G - 1) / G);
+}
+
+size_t fused_pass_smem(int64_t n, int b, int l, int rq, int sm_count) {
+  const int R = fused_pass_rows(n, sm_count);
+  const size_t tail = std::max((size_t)R * l + (size_t)l * b + jacobi_smem_doubles(b), (size_t)R * rq);
+  return ((size_t)2 * R * b + (size_t)b * rq + kFT + tail) * sizeof(double);
+}
+
+bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count) {
+  return b >= 2 && b <= 32 && nreq <= b && l >= 0 && l <= kFusedMaxL && n >= b &&
+         fused_pass_smem(n, b, l, b, sm_count) <= (size_t)200 * 1024;
+}
+
+void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count) {
+  a.R = fused_pass_rows(a.n, sm_count);
+  const int G = (int)((a.n + a.R - 1) / a.R);
+  const size_t smem = fused_pass_smem(a.n, a.b, a.l, a.rq, sm_count);
+  if (!(a.b >= 2 && a.b <= 32 && a.rq <= a.b && a.nreq <= a.rq && a.gr <= a.rq && a.l <= kFusedMaxL) ||
+      smem > (size_t)200 * 1024)
+    throw Error(MEGB200_ERR_PARAM, "fused first pass: unsupported shape");
+  static bool attr = false;
+  if (!attr) {
+    MEG_CUDA(cudaFuncSetAttribute(k_fused_first_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kFT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = L.stream;
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  MEG_CUDA(cudaLaunchKernelEx(&cfg, k_fused_first_pass, a));
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+}  // namespace megb200
