@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -37,7 +38,6 @@
 namespace megb200 {
 namespace {
 
-constexpr int kFT = 256;  // threads per CTA
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -86,14 +86,15 @@ __device__ __forceinline__ bool arrive_last(unsigned* ticket, unsigned expected,
 // res.  Returns true in the one CTA that wrote res (whichever CTAs arrive last, the
 // association -- hence every bit of res -- is the same).  tick: 1 + #groups tickets.
 constexpr int kGroup = 8;
+template <int NT>
 __device__ __forceinline__ bool tree_reduce(const double* part, double* gpart, double* res, int count,
                                             int64_t stride, unsigned* tick, int* s_flag) {
   const int G = gridDim.x, NG = (G + kGroup - 1) / kGroup, grp = blockIdx.x / kGroup;
   const int g0 = grp * kGroup, gn = min(kGroup, G - g0);
   if (!arrive_last(tick + 1 + grp, (unsigned)gn, s_flag)) return false;
-  for (int o = threadIdx.x; o < count; o += kFT) gpart[grp * stride + o] = ordered_sum(part, g0, gn, stride, o);
+  for (int o = threadIdx.x; o < count; o += NT) gpart[grp * stride + o] = ordered_sum(part, g0, gn, stride, o);
   if (!arrive_last(tick, (unsigned)NG, s_flag)) return false;
-  for (int o = threadIdx.x; o < count; o += kFT) res[o] = ordered_sum(gpart, 0, NG, stride, o);
+  for (int o = threadIdx.x; o < count; o += NT) res[o] = ordered_sum(gpart, 0, NG, stride, o);
   __threadfence_block();
   __syncthreads();
   return true;
@@ -139,26 +140,175 @@ __device__ __forceinline__ void stamp(unsigned long long* st, int slot) {
 
 // dst[r * w + c] = src[(r0 + r) * ld + c] for r < rows, c < w: eight independent loads in
 // flight per thread before the shared-memory stores
+template <int NT>
 __device__ __forceinline__ void stage_rows(double* dst, const double* __restrict__ src, int64_t ld, int64_t r0,
                                            int rows, int w) {
   const int total = rows * w;
-  for (int base = threadIdx.x; base < total; base += 8 * kFT) {
+  for (int base = threadIdx.x; base < total; base += 8 * NT) {
     double v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int idx = base + j * kFT;
+      const int idx = base + j * NT;
       const int r = idx / w, c = idx - r * w;
       v[j] = idx < total ? src[(r0 + r) * ld + c] : 0.0;
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int idx = base + j * kFT;
+      const int idx = base + j * NT;
       if (idx < total) dst[idx] = v[j];
     }
   }
 }
 
-__global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs a) {
+// Near-diagonal Rayleigh-Ritz for m <= 32 (the warm-started first pass) by the whole
+// CTA with few barriers: up to three first-order Jacobi pre-steps, the scheme of
+// block_jacobi (megb200_jacobi.cuh): Y = I + X, X_ij = h_ij / (h_jj - h_ii) (pairs with
+// |h_ij| > 0.1 |gap| excluded), one Newton-Schulz step Z = Y (3I - Y^T Y) / 2 when
+// |X| >= 1e-8, H <- Z^T H Z, V <- V Z.  Same stopping rule (off(H) <= 1e-15 ||H||_F).
+// Returns false, having written nothing, when the rule is not met (H not near-diagonal
+// or the pre-steps stagnate): the caller then runs the sweeping block_jacobi.
+// Outputs: theta (non-increasing, stable by index) to theta_g and ths (shared), S to Sout
+// (m x m row-major, column j = eigenvector j).  sm: 5 m^2 + 128 doubles.
+template <int NT>
+__device__ bool rr_small_neardiag(const double* __restrict__ Hg, int64_t ldh, int m, double* __restrict__ theta_g,
+                                  double* __restrict__ Sout, double* sm, double* ths, double* __restrict__ info) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int mm = m * m;
+  double* H = sm;
+  double* V = H + mm;
+  double* Y = V + mm;
+  double* Tm = Y + mm;
+  double* Z = Tm + mm;
+  double* wred = Z + mm;          // 3 x 32 warp partials
+  int* rk = reinterpret_cast<int*>(wred + 96);  // ranks (m ints)
+  auto warp_sum = [](double v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+  };
+  double f = 0.0, o = 0.0;
+  for (int idx = t; idx < mm; idx += NT) {
+    const int i = idx / m, j = idx - i * m;
+    const double h = i <= j ? Hg[i * ldh + j] : Hg[j * ldh + i];
+    H[idx] = h;
+    V[idx] = i == j ? 1.0 : 0.0;
+    f += h * h;
+    if (i != j) o += h * h;
+  }
+  f = warp_sum(f);
+  o = warp_sum(o);
+  if (lane == 0) {
+    wred[w] = f;
+    wred[32 + w] = o;
+  }
+  __syncthreads();
+  double fro2 = 0.0, off2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < NT / 32; ++k) {
+    fro2 += wred[k];
+    off2 += wred[32 + k];
+  }
+  const double stop2 = fro2 * 1e-30;
+  bool done = off2 <= stop2;
+  if (!done && !(off2 <= 1e-6 * fro2)) return false;
+  for (int pre = 0; pre < 3 && !done; ++pre) {
+    // Y = I + X
+    double xm = 0.0;
+    for (int idx = t; idx < mm; idx += NT) {
+      const int i = idx / m, j = idx - i * m;
+      double y = 1.0;
+      if (i != j) {
+        const double h = H[idx], d = H[j * m + j] - H[i * m + i];
+        y = (h != 0.0 && fabs(h) <= 0.1 * fabs(d)) ? h / d : 0.0;
+        xm = fmax(xm, fabs(y));
+      }
+      Y[idx] = y;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) xm = fmax(xm, __shfl_xor_sync(0xffffffffu, xm, off));
+    if (lane == 0) wred[64 + w] = xm;
+    __syncthreads();
+    double xmax = 0.0;
+#pragma unroll
+    for (int k = 0; k < NT / 32; ++k) xmax = fmax(xmax, wred[64 + k]);
+    double* Zp = Y;
+    if (xmax >= 1e-8) {
+      // Newton-Schulz: Tm = (3I - Y^T Y) / 2, Z = Y Tm
+      for (int idx = t; idx < mm; idx += NT) {
+        const int i = idx / m, j = idx - i * m;
+        Tm[idx] = 0.5 * ((i == j ? 3.0 : 0.0) - jdot(Y, i, m, Y, j, m, m));
+      }
+      __syncthreads();
+      for (int idx = t; idx < mm; idx += NT) {
+        const int i = idx / m, j = idx - i * m;
+        Z[idx] = jdot(Y, i * m, 1, Tm, j, m, m);
+      }
+      __syncthreads();
+      Zp = Z;
+    }
+    double* Vn = (Zp == Y) ? Z : Y;
+    // Tm = H Zp, Vn = V Zp
+    for (int idx = t; idx < mm; idx += NT) {
+      const int i = idx / m, j = idx - i * m;
+      Tm[idx] = jdot(H, i * m, 1, Zp, j, m, m);
+      Vn[idx] = jdot(V, i * m, 1, Zp, j, m, m);
+    }
+    __syncthreads();
+    // H <- Zp^T Tm (upper triangle, mirrored)
+    double lo = 0.0;
+    for (int idx = t; idx < mm; idx += NT) {
+      const int i = idx / m, j = idx - i * m;
+      if (i <= j) {
+        const double v = jdot(Zp, i, m, Tm, j, m, m);
+        H[i * m + j] = v;
+        H[j * m + i] = v;
+        if (i != j) lo += 2.0 * v * v;
+      }
+    }
+    lo = warp_sum(lo);
+    if (lane == 0) wred[32 + w] = lo;
+    // V <- Vn (pointer swap: the old V buffer becomes scratch)
+    double* oldV = V;
+    V = Vn;
+    if (Vn == Y) Y = oldV;
+    else Z = oldV;
+    __syncthreads();
+    const double prev = off2;
+    off2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < NT / 32; ++k) off2 += wred[32 + k];
+    done = off2 <= stop2;
+    if (!done && !(off2 < 0.25 * prev)) return false;
+  }
+  if (!done) return false;
+  // theta non-increasing, stable by index; S columns follow
+  for (int i = t; i < m; i += NT) {
+    const double di = H[i * m + i];
+    int rank = 0;
+    for (int j = 0; j < m; ++j) {
+      const double dj = H[j * m + j];
+      rank += (dj > di) || (dj == di && j < i);
+    }
+    rk[i] = rank;
+    ths[rank] = di;
+    theta_g[rank] = di;
+  }
+  __syncthreads();
+  for (int idx = t; idx < mm; idx += NT) {
+    const int k = idx / m, i = idx - k * m;
+    Sout[k * m + rk[i]] = V[idx];
+  }
+  if (t == 0 && info) {
+    info[0] = 0.0;
+    info[1] = sqrt(off2);
+    info[2] = sqrt(fro2);
+  }
+  __syncthreads();
+  return true;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs a) {
   // programmatic dependent launch after the operand pass: nothing is read before it completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
   unsigned long long* st0 = blockIdx.x == 0 ? a.stamps : nullptr;
@@ -174,14 +324,15 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs
   double* Us = sm;            // R x b
   double* Ws = Us + R * b;    // R x b
   double* Ss = Ws + R * b;    // b x rq
-  double* red = Ss + b * rq;  // kFT
-  double* Ls = red + kFT;     // R x l      } phases 0-1
+  double* red = Ss + b * rq;  // NT
+  double* Hs = red + NT;     // b x b: the reduced H (last CTA of phase 1)
+  double* Ls = Hs + b * b;    // R x l      } phases 0-1
   double* Es = Ls + R * l;    // l x b      }
   double* jac = Es + l * b;   // Jacobi scratch (the last CTA of phase 1)
   double* Ts = Ls;            // R x rq: phase 2 (reuses the phase 0-1 region)
 
   // log-map coefficients: from the device-resident kept weights (lc) or as given
-  for (int k = t; k < l; k += kFT) {
+  for (int k = t; k < l; k += NT) {
     double v;
     if (a.lc.lam && k < a.lc.lr) {
       const double kept = a.lc.c1 * a.lc.lam[k];
@@ -191,30 +342,30 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs
     }
     dsh[k] = v;
   }
-  stage_rows(Us, a.U, a.ldu, r0, rows, b);
-  if (l > 0) stage_rows(Ls, a.L, a.ldl, r0, rows, l);
+  stage_rows<NT>(Us, a.U, a.ldu, r0, rows, b);
+  if (l > 0) stage_rows<NT>(Ls, a.L, a.ldl, r0, rows, l);
   __syncthreads();
   stamp(st0, 1);
 
   // ---- phase 0: E = diag(d) L^T U
   if (l > 0) {
     if (a.Eg) {
-      for (int idx = t; idx < l * b; idx += kFT) {
+      for (int idx = t; idx < l * b; idx += NT) {
         const int k = idx / b, c = idx - k * b;
         Es[idx] = dsh[k] * a.Eg[k * a.ldg + c];
       }
     } else {
       double* p0 = a.part0 + (int64_t)g * kFusedStride;
-      for (int o = t; o < l * b; o += kFT) {
+      for (int o = t; o < l * b; o += NT) {
         const int k = o / b, c = o - k * b;
         p0[o] = rows_dot(Ls, l, k, Us, b, c, rows);
       }
-      if (tree_reduce(a.part0, a.part0 + (int64_t)G * kFusedStride, a.Ews, l * b, kFusedStride, a.sync,
+      if (tree_reduce<NT>(a.part0, a.part0 + (int64_t)G * kFusedStride, a.Ews, l * b, kFusedStride, a.sync,
                       &s_flag))
         publish(a.sync + kFusedFlags, a.epoch);
       else
         wait_published(a.sync + kFusedFlags, a.epoch);
-      for (int idx = t; idx < l * b; idx += kFT) Es[idx] = dsh[idx / b] * __ldcg(a.Ews + idx);
+      for (int idx = t; idx < l * b; idx += NT) Es[idx] = dsh[idx / b] * __ldcg(a.Ews + idx);
     }
   }
   __syncthreads();
@@ -223,7 +374,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs
   // ---- phase 1: W rows, H = U^T W
   {
     const int64_t slice = a.n * b;
-    for (int idx = t; idx < rows * b; idx += kFT) {
+    for (int idx = t; idx < rows * b; idx += NT) {
       const int rr = idx / b, c = idx - rr * b;
       const int64_t i = r0 + rr;
       const double* pp = a.part + i * b + c;
@@ -248,32 +399,36 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs
     }
     __syncthreads();
     double* p1 = a.part1 + (int64_t)g * kFusedStride;
-    for (int o = t; o < b * b; o += kFT) {
+    for (int o = t; o < b * b; o += NT) {
       const int ia = o / b, c = o - ia * b;
       p1[o] = ia <= c ? rows_dot(Us, b, ia, Ws, b, c, rows) : 0.0;
     }
   }
   stamp(st0, 3);
-  double* hres = a.part1 + (int64_t)(G + (G + kGroup - 1) / kGroup) * kFusedStride;
-  if (tree_reduce(a.part1, a.part1 + (int64_t)G * kFusedStride, hres, b * b, kFusedStride, a.sync + 32,
-                  &s_flag)) {
+  if (tree_reduce<NT>(a.part1, a.part1 + (int64_t)G * kFusedStride, Hs, b * b, kFusedStride, a.sync + 32, &s_flag)) {
     stamp(a.stamps, 4);
-    for (int o = t; o < b * b; o += kFT) {
-      const int ia = o / b, c = o - ia * b;
-      if (ia <= c) a.H[ia * a.ldh + c] = hres[o];
-    }
-    __threadfence_block();
-    __syncthreads();
     stamp(a.stamps, 5);
-    block_jacobi(a.H, a.ldh, b, a.theta, a.Sout, jac, a.info);
-    __syncthreads();
+    if (!rr_small_neardiag<NT>(Hs, b, b, a.theta, a.Sout, jac, thsh, a.info)) {
+      __syncthreads();
+      block_jacobi(Hs, b, b, a.theta, a.Sout, jac, a.info);
+      __syncthreads();
+      for (int c = t; c < b; c += NT) thsh[c] = a.theta[c];
+      __syncthreads();
+    }
     stamp(a.stamps, 6);
+    // the other CTAs need theta and S only; H (for a continued solve) and the step
+    // epilogue are written after the release, off the critical path
+    publish(a.sync + kFusedFlags + 1, a.epoch);
+    for (int o = t; o < b * b; o += NT) {
+      const int ia = o / b, c = o - ia * b;
+      if (ia <= c) a.H[ia * a.ldh + c] = Hs[o];
+    }
     if (a.epi && t < 32) {
       // step epilogue (meg.py:347-356), lane k (and k + 32) owning pair k:
       // y = exp(mu - mu_1), lam = y[:r] / sum renormalised, lambda_{r+1}, b_{r+1}, cheap certificate
       const int lane = t;
       const int r = a.nreq - 1;
-      const double* theta = a.theta;
+      const double* theta = thsh;
       double* epi = a.epi;
       const double shift = theta[0];
       double y[2], lam[2];
@@ -302,10 +457,10 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs
 #pragma unroll
       for (int h = 0; h < 2; ++h)
         if (lane + 32 * h < r) epi[r + 1 + lane + 32 * h] = lam[h] / lsum;
-      __syncwarp();
+      // y_{r+1} from the lane that owns pair r
+      const double lam_rp1 = __shfl_sync(0xffffffffu, (r >> 5) ? y[1] : y[0], r & 31);
       if (lane == 0) {
         double status = !(kept > 1e-290) ? 4.0 : 0.0;
-        const double lam_rp1 = epi[r];
         double lhs;
         if (!(bsum > 0.0) || lam_rp1 < 0.0) {
           status = 1.0;
@@ -325,7 +480,6 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs
         tail[6] = status;
       }
     }
-    publish(a.sync + kFusedFlags + 1, a.epoch);
     stamp(a.stamps, 7);
   } else {
     wait_published(a.sync + kFusedFlags + 1, a.epoch);
@@ -333,13 +487,13 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs
   stamp(st0, 8);
 
   // ---- phase 2: Ritz block, residuals, Gram
-  for (int idx = t; idx < b * rq; idx += kFT) {
+  for (int idx = t; idx < b * rq; idx += NT) {
     const int k = idx / rq, c = idx - k * rq;
     Ss[idx] = __ldcg(a.Sout + k * b + c);
   }
-  for (int c = t; c < rq; c += kFT) thsh[c] = __ldcg(a.theta + c);
+  for (int c = t; c < rq; c += NT) thsh[c] = __ldcg(a.theta + c);
   __syncthreads();
-  const int rpt = kFT / rq;
+  const int rpt = NT / rq;
   const int c = t % rq;
   const int rofs = t / rq;
   double sq = 0.0;
@@ -384,16 +538,16 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs
   }
   if (a.gr > 0) {
     // same product order as the phase-0 partial
-    for (int o = t; o < a.gr * a.gr; o += kFT) {
+    for (int o = t; o < a.gr * a.gr; o += NT) {
       const int ia = o / a.gr, cc = o - ia * a.gr;
       p2[a.nreq + o] = rows_dot(Ts, rq, ia, Ts, rq, cc, rows);
     }
   }
   stamp(st0, 9);
   double* res2 = a.part2 + (int64_t)(G + (G + kGroup - 1) / kGroup) * kFusedStride;
-  if (tree_reduce(a.part2, a.part2 + (int64_t)G * kFusedStride, res2, pw, kFusedStride, a.sync + 64, &s_flag)) {
+  if (tree_reduce<NT>(a.part2, a.part2 + (int64_t)G * kFusedStride, res2, pw, kFusedStride, a.sync + 64, &s_flag)) {
     stamp(a.stamps, 10);
-    for (int o = t; o < pw; o += kFT) {
+    for (int o = t; o < pw; o += NT) {
       const double v = res2[o];
       if (o < a.nreq)
         a.resid[o] = sqrt(v);
@@ -405,7 +559,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs
     stamp(a.stamps, 11);
     if (a.host_pack) {
       // the result pack straight into the caller's pinned host slot (no separate read-back copy)
-      for (int idx = t; idx < a.pack_count; idx += kFT) a.host_pack[idx] = __ldcg(a.pack + idx);
+      for (int idx = t; idx < a.pack_count; idx += NT) a.host_pack[idx] = __ldcg(a.pack + idx);
     }
     stamp(a.stamps, 12);
   }
@@ -413,15 +567,31 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_first_pass(const FusedPassArgs
 
 }  // namespace
 
+// launch shape: threads per CTA and target rows per CTA (diagnostics overrides
+// MEGB200_FUSED_NT = 256 | 512 | 1024, MEGB200_FUSED_ROWS)
+int fused_nt() {
+  static const int nt = [] {
+    const char* e = getenv("MEGB200_FUSED_NT");
+    const int v = e ? atoi(e) : 512;
+    return (v == 512 || v == 1024) ? v : 256;
+  }();
+  return nt;
+}
+
 int fused_pass_rows(int64_t n, int sm_count) {
-  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count, (n + 15) / 16));
+  static const int target = [] {
+    const char* e = getenv("MEGB200_FUSED_ROWS");
+    return e ? std::max(1, atoi(e)) : 32;
+  }();
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count, (n + target - 1) / target));
   return (int)((n + G - 1) / G);
 }
 
 size_t fused_pass_smem(int64_t n, int b, int l, int rq, int sm_count) {
   const int R = fused_pass_rows(n, sm_count);
-  const size_t tail = std::max((size_t)R * l + (size_t)l * b + jacobi_smem_doubles(b), (size_t)R * rq);
-  return ((size_t)2 * R * b + (size_t)b * rq + kFT + tail) * sizeof(double);
+  const size_t jac = std::max((size_t)jacobi_smem_doubles(b), (size_t)5 * b * b + 128);
+  const size_t tail = std::max((size_t)R * l + (size_t)l * b + jac, (size_t)R * rq);
+  return ((size_t)2 * R * b + (size_t)b * rq + fused_nt() + (size_t)b * b + tail) * sizeof(double);
 }
 
 bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count) {
@@ -429,21 +599,16 @@ bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count) {
          fused_pass_smem(n, b, l, b, sm_count) <= (size_t)200 * 1024;
 }
 
-void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count) {
-  a.R = fused_pass_rows(a.n, sm_count);
-  const int G = (int)((a.n + a.R - 1) / a.R);
-  const size_t smem = fused_pass_smem(a.n, a.b, a.l, a.rq, sm_count);
-  if (!(a.b >= 2 && a.b <= 32 && a.rq <= a.b && a.nreq <= a.rq && a.gr <= a.rq && a.l <= kFusedMaxL) ||
-      smem > (size_t)200 * 1024)
-    throw Error(MEGB200_ERR_PARAM, "fused first pass: unsupported shape");
+template <int NT>
+void launch_fused(const Launch& L, const FusedPassArgs& a, int G, size_t smem) {
   static bool attr = false;
   if (!attr) {
-    MEG_CUDA(cudaFuncSetAttribute(k_fused_first_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    MEG_CUDA(cudaFuncSetAttribute(k_fused_first_pass<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G);
-  cfg.blockDim = dim3(kFT);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = L.stream;
   cudaLaunchAttribute pdl[1];
@@ -451,9 +616,23 @@ void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count) {
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  MEG_CUDA(cudaLaunchKernelEx(&cfg, k_fused_first_pass, a));
+  MEG_CUDA(cudaLaunchKernelEx(&cfg, k_fused_first_pass<NT>, a));
   MEG_LAUNCHED();
   ++*L.counter;
+}
+
+void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count) {
+  a.R = fused_pass_rows(a.n, sm_count);
+  const int G = (int)((a.n + a.R - 1) / a.R);
+  const size_t smem = fused_pass_smem(a.n, a.b, a.l, a.rq, sm_count);
+  if (!(a.b >= 2 && a.b <= 32 && a.rq <= a.b && a.nreq <= a.rq && a.gr <= a.rq && a.l <= kFusedMaxL) ||
+      smem > (size_t)200 * 1024 || G > sm_count)
+    throw Error(MEGB200_ERR_PARAM, "fused first pass: unsupported shape");
+  switch (fused_nt()) {
+    case 1024: launch_fused<1024>(L, a, G, smem); break;
+    case 512: launch_fused<512>(L, a, G, smem); break;
+    default: launch_fused<256>(L, a, G, smem); break;
+  }
 }
 
 }  // namespace megb200
