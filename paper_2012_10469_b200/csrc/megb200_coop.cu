@@ -767,12 +767,12 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
 void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,
              const double* Q, const double* AQ, int64_t ldq, int rq, int nreq, double* T, int64_t ldt, double* resid,
              double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi, double* V2, int64_t ld2,
-             int r2) {
+             int r2, int nvec) {
   if (!V2) r2 = 0;
   if (nreq > 64 || rq > 64) throw Error(MEGB200_ERR_PARAM, "rr: at most 64 Ritz vectors");
   const int G = coop_grid(n, sm_count);
   const bool fused = m <= 48;
-  if (!fused) rr_jacobi(L, H, ldh, m, theta, S, nullptr, 0, 0, nreq, nullptr, info);
+  if (!fused) rr_wide(L, H, ldh, m, theta, S, info, nvec > 0 ? std::max(nvec, rq) : 0);
   const size_t smem = std::max(fused ? (size_t)jacobi_smem_doubles(m) : (size_t)0,
                                (size_t)(m * rq + 2 * kRC * m + kCT + kRC * 2 * std::max(gr, 1))) * sizeof(double);
   double* info_arg = fused ? info : nullptr;

@@ -95,6 +95,12 @@ void apply_rinv(const Launch& L, int64_t n, double* W, int64_t ldw, int q, const
 // row-major (column j = eigenvector j).  est[j] = ||Rn * S[m-cur:m, j]|| for j < nreq.
 void rr_jacobi(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, const double* Rn,
                int rn_rows, int cur, int nreq, double* est, double* info);
+// Wide Rayleigh-Ritz (m <= 112, one CTA): Householder tridiagonalisation + multisection +
+// twisted-factorisation eigenvectors, verified, with a cyclic-Jacobi fallback (megb200_rr.cu)
+// (only the top nvec eigenpairs and the smallest eigenvalue are computed when nvec < m; the
+// other theta entries are reported as the smallest, the other S columns as zero)
+void rr_wide(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info,
+             int nvec = 0);
 // explicit residuals  ||AX_j - theta_j X_j||^2 partial sums, reduced into out[j] (sqrt applied)
 void resid_norms(const Launch& L, int64_t n, const double* X, int64_t ldx, const double* AX, int64_t ldax,
                  int q, const double* theta, double* out, double* part, int64_t part_cap, int sm_count);
@@ -142,7 +148,7 @@ void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, 
 void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,
              const double* Q, const double* AQ, int64_t ldq, int rq, int nreq, double* T, int64_t ldt, double* resid,
              double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi, double* V2 = nullptr,
-             int64_t ld2 = 0, int r2 = 0);
+             int64_t ld2 = 0, int r2 = 0, int nvec = 0);
 
 // First pass of a solve fused with its finish and Rayleigh-Ritz (megb200_step.cu):
 // W = scale * sum_s part[s] + L E + alpha U, H = U^T W, Jacobi RR, Ritz block T,

@@ -1,0 +1,506 @@
+// Wide Rayleigh-Ritz (m = 49..112, the restarted block Krylov basis of the
+// multi-pass solves, linalg.py:205-211) by one CTA of 1024 threads:
+//
+//   1. Householder tridiagonalisation H = Q T Q^T (LAPACK dsytd2 'L' scheme:
+//      per column one norm, one symmetric matvec, one rank-2 update);
+//   2. all eigenvalues of T by multisection on Sturm counts (eight lanes per
+//      eigenvalue, nine-way split per round, 18 rounds: width <= 1e-17 ||T||),
+//      the k-th lane group owning the k-th largest eigenvalue (so theta comes out
+//      non-increasing);
+//   3. eigenvectors of T from twisted factorisations T - lambda I = L+ D+ L+^T =
+//      U- D- U-^T (twist at the smallest |gamma_k|, the MRRR "getvec" step), one
+//      thread per eigenvalue, O(m) each;
+//   4. S = Q Y by the stored reflectors, applied in reverse;
+//   5. one to three Newton-Schulz steps S <- S (3I - S^T S) / 2 (clustered
+//      eigenvalues leave the twisted vectors slightly non-orthogonal), row-wise in
+//      place;
+//   6. verification against the original H: every column residual
+//      ||H s_k - theta_k s_k|| <= 1e-12 ||H||_F and S orthonormal; otherwise the
+//      same CTA runs the cyclic Jacobi solver (block_jacobi) from H instead.
+//
+// Cost: O(m) barriers-deep (tridiagonalisation and back-transform), versus the
+// ~ (m - 1) x sweeps rounds of cyclic Jacobi (8-10 sweeps of 100+ rounds at these
+// sizes, milliseconds).
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "megb200_internal.h"
+
+#define JACOBI_MARK(slot)
+#include "megb200_jacobi.cuh"
+
+namespace megb200 {
+namespace {
+
+constexpr int kRT = 1024;           // threads
+constexpr int kNW = kRT / 32;       // warps
+constexpr int kLanesPerEig = 8;     // multisection lanes per eigenvalue
+constexpr int kBisectRounds = 18;   // 9^18 > 1e17
+
+// diagnostics: %globaltimer at the phase boundaries of the last wide solve (thread 0)
+__device__ unsigned long long g_rr_ns[16];
+__device__ __forceinline__ void rr_mark(int slot) {
+  if (threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    g_rr_ns[slot] = v;
+  }
+}
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+__device__ __forceinline__ double wmax(double v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+  return v;
+}
+
+// number of eigenvalues of T (d, e2 = e^2) below x (Sturm count, LAPACK dlaneg-style pivot guard)
+// 1/q from the MUFU float64 reciprocal approximation refined by two Newton steps (full
+// precision; the Sturm recurrence is throughput-bound on float64 division)
+__device__ __forceinline__ double fast_rcp(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  double e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int m, double x, double pivmin) {
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  int c = q < 0.0;
+  for (int i = 1; i < m; ++i) {
+    q = (d[i] - x) - e2[i - 1] * fast_rcp(q);
+    if (fabs(q) < pivmin) q = -pivmin;
+    c += q < 0.0;
+  }
+  return c;
+}
+
+// C(i, j) = sum_k Aop(i, k) Bop(k, j) for i, j < m, Aop(i, k) = A[i * ai + k * ak],
+// Bop(k, j) = B[k * bk + j * bj]; 4 x 4 register tiles whose rows / columns are strided by
+// the tile count (neighbouring lanes take neighbouring columns: conflict-free, broadcast rows)
+template <typename F>
+__device__ __forceinline__ void gemm_t4(const double* A, int ai, int ak, const double* B, int bk, int bj, int mr,
+                                        int mc, int kd, F&& out) {
+  const int nr = (mr + 3) / 4, nc = (mc + 3) / 4;
+  for (int tt = threadIdx.x; tt < nr * nc; tt += kRT) {
+    const int it = tt / nc, jt = tt - it * nc;
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+    for (int k = 0; k < kd; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = it + r * nr < mr ? A[(it + r * nr) * ai + k * ak] : 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = jt + c * nc < mc ? B[k * bk + (jt + c * nc) * bj] : 0.0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (it + r * nr < mr && jt + c * nc < mc) out(it + r * nr, jt + c * nc, acc[r][c]);
+  }
+}
+
+// Returns true with theta (non-increasing) and S (m x m row-major, column k =
+// eigenvector k) written; false (nothing written) when the verification fails.
+__device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, int nvec, double* __restrict__ theta_g,
+                           double* __restrict__ Sout, double* sm, double* __restrict__ info) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int la = m + 1;
+  double* A = sm;              // m x la: H, then the reflectors below the subdiagonal
+  double* Z = A + m * la;      // m x m: eigenvectors of T, then S
+  double* d = Z + m * m;       // m
+  double* e = d + m;           // m
+  double* e2 = e + m;          // m
+  double* tau = e2 + m;        // m
+  double* v = tau + m;         // m
+  double* p = v + m;           // m
+  double* lam = p + m;         // m
+  double* wp = lam + m;        // kNW x 8 partials
+  double* sc = wp + 8 * kNW;   // scalars
+  // ---- load H (upper triangle given), ||H||_F^2
+  double f = 0.0;
+  for (int idx = t; idx < m * m; idx += kRT) {
+    const int i = idx / m, j = idx - i * m;
+    const double h = i <= j ? Hg[i * ldh + j] : Hg[j * ldh + i];
+    A[i * la + j] = h;
+    f += h * h;
+  }
+  f = wsum(f);
+  if (lane == 0) wp[w] = f;
+  __syncthreads();
+  double fro2 = 0.0;
+  for (int k = 0; k < kNW; ++k) fro2 += wp[k];
+  rr_mark(0);
+  // ---- 1. tridiagonalisation
+  for (int j = 0; j < m - 2; ++j) {
+    const int L = m - j - 1;
+    if (w == 0) {
+      double s = 0.0;
+      for (int i = lane + 1; i < L; i += 32) {
+        const double x = A[(j + 1 + i) * la + j];
+        s += x * x;
+      }
+      s = wsum(s);
+      const double alpha = A[(j + 1) * la + j];
+      double tj = 0.0, beta = alpha, scale = 0.0;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tj = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      for (int i = lane; i < L; i += 32) {
+        const double vi = i == 0 ? 1.0 : A[(j + 1 + i) * la + j] * scale;
+        v[i] = vi;
+        if (i > 0) A[(j + 1 + i) * la + j] = vi;  // reflector kept for the back-transform
+      }
+      if (lane == 0) {
+        tau[j] = tj;
+        e[j] = beta;
+        d[j] = A[j * la + j];
+        sc[0] = tj;
+      }
+    }
+    __syncthreads();
+    const double tj = sc[0];
+    if (tj == 0.0) {  // uniform; the barrier keeps warp 0's next write of sc[0] behind every read
+      __syncthreads();
+      continue;
+    }
+    // p = tau A22 v (warp per row), partial p^T v
+    double pv = 0.0;
+    for (int i = w; i < L; i += kNW) {
+      const double* row = A + (j + 1 + i) * la + (j + 1);
+      double s = 0.0;
+      for (int k = lane; k < L; k += 32) s = fma(row[k], v[k], s);
+      s = wsum(s);
+      const double pi = tj * s;
+      if (lane == 0) p[i] = pi;
+      pv = fma(pi, v[i], pv);
+    }
+    if (lane == 0) wp[w] = pv;
+    __syncthreads();
+    double K = 0.0;
+    for (int k = 0; k < kNW; ++k) K += wp[k];
+    K *= 0.5 * tj;
+    // w = p - K v (in place over p)
+    for (int i = t; i < L; i += kRT) p[i] = p[i] - K * v[i];
+    __syncthreads();
+    // A22 -= v w^T + w v^T: eight threads per row, each row's (v_i, w_i) held in registers
+    for (int rr = t >> 3; rr < L; rr += kRT >> 3) {
+      const double vi = v[rr], wi = p[rr];
+      double* row = A + (j + 1 + rr) * la + (j + 1);
+      for (int k = t & 7; k < L; k += 8) row[k] -= fma(vi, p[k], wi * v[k]);
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    if (m >= 2) {
+      d[m - 2] = A[(m - 2) * la + (m - 2)];
+      e[m - 2] = A[(m - 1) * la + (m - 2)];
+      tau[m - 2] = 0.0;
+    }
+    d[m - 1] = A[(m - 1) * la + (m - 1)];
+    tau[m - 1] = 0.0;
+    e[m - 1] = 0.0;
+  }
+  __syncthreads();
+  rr_mark(1);
+  // Gershgorin interval, pivot guard
+  if (w == 0) {
+    double lo = INFINITY, hi = -INFINITY, em = 0.0;
+    for (int i = lane; i < m; i += 32) {
+      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < m - 1 ? fabs(e[i]) : 0.0);
+      lo = fmin(lo, d[i] - r);
+      hi = fmax(hi, d[i] + r);
+      if (i < m - 1) em = fmax(em, e[i] * e[i]);
+    }
+    lo = -wmax(-lo);
+    hi = wmax(hi);
+    em = wmax(em);
+    if (lane == 0) {
+      const double span = fmax(hi - lo, 1e-300);
+      sc[1] = lo - 1e-14 * span;
+      sc[2] = hi + 1e-14 * span;
+      sc[3] = 1e-290 * fmax(1.0, em);
+    }
+  }
+  for (int i = t; i < m - 1; i += kRT) e2[i] = e[i] * e[i];
+  __syncthreads();
+  const double pivmin = sc[3];
+  // ---- 2. eigenvalues by multisection: group k owns the k-th largest (index m-1-k ascending),
+  //      the eight lanes of a group split its interval nine ways per round; only the top nvec
+  //      and the smallest are computed (the Ritz values a restart keeps, and the norm estimate)
+  {
+    const int grp = t / kLanesPerEig, sub = t % kLanesPerEig;
+    const int ngrp = kRT / kLanesPerEig;
+    const int neig = nvec < m ? nvec + 1 : m;
+    for (int k0 = 0; k0 < neig; k0 += ngrp) {
+      const int kk = k0 + grp;
+      const bool act = kk < neig;
+      const int k = (act && kk == nvec && nvec < m) ? m - 1 : kk;  // the extra group: the smallest
+      const int idx = m - 1 - (act ? k : 0);
+      double lo = sc[1], hi = sc[2];
+      for (int round = 0; round < kBisectRounds; ++round) {
+        const double x = lo + (hi - lo) * (double)(sub + 1) / (double)(kLanesPerEig + 1);
+        const int c = act ? sturm_count(d, e2, m, x, pivmin) : 0;
+        const unsigned below = __ballot_sync(0xffffffffu, c <= idx);
+        const unsigned mine = (below >> ((lane / kLanesPerEig) * kLanesPerEig)) & ((1u << kLanesPerEig) - 1u);
+        const int ones = __popc(mine);  // counts are monotone in x: lanes 0..ones-1 are below
+        const double step = (hi - lo) / (double)(kLanesPerEig + 1);
+        const double nlo = ones > 0 ? lo + step * ones : lo;
+        const double nhi = ones < kLanesPerEig ? lo + step * (ones + 1) : hi;
+        lo = nlo;
+        hi = nhi;
+      }
+      if (act && sub == 0) lam[k] = 0.5 * (lo + hi);
+    }
+  }
+  __syncthreads();
+  // Ritz values not computed (between the top nvec and the smallest) are reported as the smallest
+  for (int k = nvec + t; k < m - 1; k += kRT) lam[k] = lam[m - 1];
+  __syncthreads();
+  rr_mark(2);
+  // ---- 3. eigenvectors of T by twisted factorisations (thread k <-> eigenvalue k, column k of Z)
+  for (int k = t; k < nvec; k += kRT) {
+    const double lk = lam[k];
+    // forward: D+_i, stored in Z[i][k]
+    double dp = d[0] - lk;
+    for (int i = 0; i < m - 1; ++i) {
+      if (fabs(dp) < pivmin) dp = -pivmin;
+      Z[i * m + k] = dp;
+      dp = (d[i + 1] - lk) - e2[i] / dp;
+    }
+    if (fabs(dp) < pivmin) dp = -pivmin;
+    Z[(m - 1) * m + k] = dp;
+    // backward: D-_{i+1}, gamma_i = D+_i - e_i^2 / D-_{i+1}; twist r = argmin |gamma|
+    double dm = d[m - 1] - lk;
+    if (fabs(dm) < pivmin) dm = -pivmin;
+    int r = m - 1;
+    double gbest = fabs(Z[(m - 1) * m + k]);
+    for (int i = m - 2; i >= 0; --i) {
+      const double g = Z[i * m + k] - e2[i] / dm;
+      if (fabs(g) < gbest) {
+        gbest = fabs(g);
+        r = i;
+      }
+      dm = (d[i] - lk) - e2[i] / dm;
+      if (fabs(dm) < pivmin) dm = -pivmin;
+    }
+    // U-_i = e_i / D-_{i+1} for i >= r, stored over D+_i (i >= r no longer needed)
+    dm = d[m - 1] - lk;
+    if (fabs(dm) < pivmin) dm = -pivmin;
+    for (int i = m - 2; i >= r; --i) {
+      Z[i * m + k] = e[i] / dm;
+      dm = (d[i] - lk) - e2[i] / dm;
+      if (fabs(dm) < pivmin) dm = -pivmin;
+    }
+    // z_r = 1; upward z_{i+1} = -U-_i z_i; downward z_i = -(e_i / D+_i) z_{i+1}
+    double nrm = 1.0;
+    double cur = 1.0;
+    double u = Z[r * m + k];
+    Z[r * m + k] = 1.0;
+    for (int i = r; i < m - 1; ++i) {
+      const double nxt = -u * cur;
+      u = Z[(i + 1) * m + k];
+      Z[(i + 1) * m + k] = nxt;
+      nrm = fma(nxt, nxt, nrm);
+      cur = nxt;
+    }
+    cur = 1.0;
+    for (int i = r - 1; i >= 0; --i) {
+      const double nxt = -(e[i] / Z[i * m + k]) * cur;
+      Z[i * m + k] = nxt;
+      nrm = fma(nxt, nxt, nrm);
+      cur = nxt;
+    }
+    const double s = 1.0 / sqrt(nrm);
+    for (int i = 0; i < m; ++i) Z[i * m + k] *= s;
+  }
+  __syncthreads();
+  rr_mark(3);
+  // ---- 4. S = Q Z: reflectors j = m-3 .. 0 applied to rows j+1.. of Z
+  {
+    const int nch = kRT / nvec >= 8 ? 8 : (kRT / nvec >= 4 ? 4 : 1);  // row chunks per column dot
+    for (int j = m - 3; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;  // uniform (tau is never rewritten here)
+      const int L = m - j - 1;
+      // u_c = v^T Z[j+1.., c] in nch row chunks, partials in sc[8 + c * nch + ch]
+      if (t < nvec * nch) {
+        const int c = t / nch, ch = t - c * nch;
+        const int i0 = (L * ch) / nch, i1 = (L * (ch + 1)) / nch;
+        double s = 0.0;
+        for (int i = i0; i < i1; ++i) {
+          const double vi = i == 0 ? 1.0 : A[(j + 1 + i) * la + j];
+          s = fma(vi, Z[(j + 1 + i) * m + c], s);
+        }
+        sc[8 + c * nch + ch] = s;
+      }
+      __syncthreads();
+      for (int c = t; c < nvec; c += kRT) {
+        double u = 0.0;
+        for (int ch = 0; ch < nch; ++ch) u += sc[8 + c * nch + ch];
+        p[c] = tj * u;
+      }
+      __syncthreads();
+      for (int rr = t >> 3; rr < L; rr += kRT >> 3) {
+        const double vi = rr == 0 ? 1.0 : A[(j + 1 + rr) * la + j];
+        double* zr = Z + (j + 1 + rr) * m;
+        for (int c = t & 7; c < nvec; c += 8) zr[c] -= vi * p[c];
+      }
+      __syncthreads();
+    }
+  }
+  rr_mark(4);
+  // ---- 5. Newton-Schulz: G = S^T S in A (reflectors no longer needed), S <- S (3I - G) / 2 by rows
+  double delta = 0.0;
+  for (int it = 0; it < 3; ++it) {
+    double gm = 0.0;
+    gemm_t4(Z, 1, m, Z, m, 1, nvec, nvec, m, [&](int i, int c, double g) {
+      A[i * la + c] = g;
+      gm = fmax(gm, fabs(g - (i == c ? 1.0 : 0.0)));
+    });
+    gm = wmax(gm);
+    if (lane == 0) wp[w] = gm;
+    __syncthreads();
+    delta = 0.0;
+    for (int k = 0; k < kNW; ++k) delta = fmax(delta, wp[k]);
+    __syncthreads();
+    if (!(delta < 0.25)) return false;  // uniform: twisted vectors too far from orthogonal
+    if (delta <= 1e-15) break;
+    // M = (3I - G) / 2 in place, then S <- S M by rows: four rows per warp, in place
+    for (int idx = t; idx < nvec * nvec; idx += kRT) {
+      const int i = idx / nvec, c = idx - i * nvec;
+      A[i * la + c] = 0.5 * ((i == c ? 3.0 : 0.0) - A[i * la + c]);
+    }
+    __syncthreads();
+    for (int i0 = 4 * w; i0 < m; i0 += 4 * kNW) {
+      double out[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[r][q] = 0.0;
+      for (int k = 0; k < nvec; ++k) {
+        double zr[4], mk[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) zr[r] = i0 + r < m ? Z[(i0 + r) * m + k] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mk[q] = lane + 32 * q < nvec ? A[k * la + lane + 32 * q] : 0.0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) out[r][q] = fma(zr[r], mk[q], out[r][q]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i0 + r < m && lane + 32 * q < nvec) Z[(i0 + r) * m + lane + 32 * q] = out[r][q];
+    }
+    __syncthreads();
+  }
+  rr_mark(5);
+  // ---- 6. verification from the original H: column residuals ||H s_k - theta_k s_k||^2
+  for (int idx = t; idx < m * m; idx += kRT) {
+    const int i = idx / m, j = idx - i * m;
+    A[i * la + j] = i <= j ? Hg[i * ldh + j] : Hg[j * ldh + i];
+  }
+  __syncthreads();
+  double rmax = 0.0;
+  gemm_t4(A, la, 1, Z, m, 1, m, nvec, m,
+          [&](int i, int c, double hs) { rmax = fmax(rmax, fabs(hs - lam[c] * Z[i * m + c])); });
+  rmax = wmax(rmax);
+  if (lane == 0) wp[w] = rmax;
+  __syncthreads();
+  double res = 0.0;
+  for (int k = 0; k < kNW; ++k) res = fmax(res, wp[k]);
+  const double hn = sqrt(fro2);
+  if (!(res <= 1e-12 * fmax(hn, 1e-300) && delta < 1e-10)) return false;
+  rr_mark(6);
+  for (int k = t; k < m; k += kRT) theta_g[k] = lam[k];
+  for (int idx = t; idx < m * m; idx += kRT) Sout[idx] = (idx % m) < nvec ? Z[idx] : 0.0;
+  if (t == 0 && info) {
+    info[0] = -1.0;  // marks the tridiagonal solver (no Jacobi sweeps)
+    info[1] = res;
+    info[2] = hn;
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(kRT, 1) k_rr_wide(const double* __restrict__ Hg, int64_t ldh, int m,
+                                                    double* __restrict__ theta, double* __restrict__ Sout,
+                                                    double* __restrict__ info, int nvec, int force_jacobi) {
+  extern __shared__ double sm[];
+  if (!force_jacobi && rr_tridiag(Hg, ldh, m, nvec, theta, Sout, sm, info)) return;
+  __syncthreads();
+  block_jacobi(Hg, ldh, m, theta, Sout, sm, info);
+}
+
+}  // namespace
+
+size_t rr_wide_smem(int m) {
+  const size_t tri = (size_t)m * (m + 1) + (size_t)m * m + 8 * (size_t)m + 8 * kNW + 8 + 8 * 112;
+  return std::max(tri, (size_t)jacobi_smem_doubles(m)) * sizeof(double);
+}
+
+void rr_wide(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int nvec) {
+  nvec = (nvec <= 0 || nvec > m) ? m : nvec;
+  static const bool force_env = getenv("MEGB200_RR_JACOBI") != nullptr;  // diagnostics: cyclic Jacobi only
+  const bool force = force_env || getenv("MEGB200_RR_JACOBI_ONCE") != nullptr;
+  const size_t smem = rr_wide_smem(m);
+  static bool attr = false;
+  if (!attr) {
+    MEG_CUDA(cudaFuncSetAttribute(k_rr_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  if (smem > 227 * 1024) throw Error(MEGB200_ERR_PARAM, "wide Rayleigh-Ritz: basis too large");
+  k_rr_wide<<<1, kRT, smem, L.stream>>>(H, ldh, m, theta, S, info, nvec, force ? 1 : 0);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+}  // namespace megb200
+
+// Diagnostics: one wide solve on a device matrix H (m x m, ld ldh), force_jacobi selects the fallback
+extern "C" int megb200_debug_rr_solve(const double* H, int64_t ldh, int32_t m, double* theta, double* S, double* info,
+                                      int32_t force_jacobi) {
+  try {
+    int64_t cnt = 0;
+    megb200::Launch L{nullptr, &cnt};
+    if (force_jacobi > 0) setenv("MEGB200_RR_JACOBI_ONCE", "1", 1);
+    megb200::rr_wide(L, H, ldh, m, theta, S, info, force_jacobi < 0 ? -force_jacobi : 0);
+    unsetenv("MEGB200_RR_JACOBI_ONCE");
+    return MEGB200_OK;
+  } catch (...) {
+    return MEGB200_ERR_CUDA;
+  }
+}
+
+// Diagnostics: phase timestamps of the last wide Rayleigh-Ritz solve (tridiagonal path)
+extern "C" int megb200_debug_rr_ns(unsigned long long* out, int count) {
+  if (!out || count < 1 || count > 16) return MEGB200_ERR_PARAM;
+  return cudaMemcpyFromSymbol(out, megb200::g_rr_ns, sizeof(unsigned long long) * count) == cudaSuccess
+             ? MEGB200_OK
+             : MEGB200_ERR_CUDA;
+}

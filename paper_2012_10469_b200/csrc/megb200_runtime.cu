@@ -73,6 +73,7 @@ struct megb200_solver {
   int64_t h_buf_len = 0;
   unsigned* fsync = nullptr;  // tickets / flags of the fused first-pass kernel (zeroed)
   unsigned epoch = 0;
+  int rr_nvec = 0;  // Ritz pairs a wide Rayleigh-Ritz must return (0: all); set by top_eigs
   double m_norm2_cache = NAN, m_trace_cache = NAN;
   const void* m_cache_ptr = nullptr;
   // run-loop buffers (allocated on first megb200_meg_run)
@@ -423,7 +424,7 @@ int rr_readback(megb200_solver* s, int newcols, int nreq, int bw, const EpiSpec*
   for (int rep = 0; rep < (twice ? 2 : 1); ++rep)
     coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, s->n, s->Q, s->AQ, s->ldq, rq, nreq, tdst, ldt,
             s->resid, s->red, s->sm_count, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
-            epi ? s->pack + s->pack_epi : nullptr, v2, ld2, r2);
+            epi ? s->pack + s->pack_epi : nullptr, v2, ld2, r2, s->rr_nvec);
   s->d2h(dst, s->pack, s->pack_gram + (int64_t)gr * gr);
   return gr;
 }
@@ -528,6 +529,12 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   Launch L = s->launch();
   const EigShape sh = eig_shape(s, nreq, P);
   const int bw = sh.bw, mmax = sh.mmax, keep = sh.keep, max_passes = sh.max_passes;
+  // a wide Rayleigh-Ritz needs the Ritz pairs a thick restart keeps (and the Ritz block)
+  s->rr_nvec = sh.exhaust ? 0 : std::max(keep, nreq);
+  struct NvecReset {
+    megb200_solver* s;
+    ~NvecReset() { s->rr_nvec = 0; }
+  } nvec_reset{s};
   const double tol = P.tol;
   const uint64_t key_start = stream_key(P.seed, kStreamStart);
   const uint64_t key_refill = stream_key(P.seed, kStreamRefill);
