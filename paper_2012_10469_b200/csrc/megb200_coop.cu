@@ -447,6 +447,135 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
   phase_mark(26);
 }
 
+
+// ===========================================================================
+// Whole block orthonormalisation in one cooperative launch (the sequence of
+// orthonormalize(): CGS, CGS, CholQR (breakdown threshold), CGS, CholQR), the
+// CTA's rows of the basis Q and of the block W staged ONCE in shared memory.
+// Each CGS / Gram reduction is one grid barrier + a fixed-order warp reduction
+// + one grid barrier; the q x q Cholesky and R^-1 run in CTA 0 (block_cholesky).
+// Same rules as k_coop_cgs / k_coop_cholqr:
+// column equilibration, breakdown pivots (<= thresh^2 absolute, 1e-20 relative)
+// flagged and refilled with the seeded normals of the same counters.
+
+__global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* __restrict__ Q, int64_t ldq, int cols,
+                                                     double* __restrict__ W, int64_t ldw, int q, double thresh1,
+                                                     uint64_t key, uint64_t base, double* __restrict__ part,
+                                                     double* __restrict__ Cws, double* __restrict__ Gws,
+                                                     double* __restrict__ Rinv, int* __restrict__ mask,
+                                                     double* __restrict__ Rrel, int cgs_rounds) {
+  extern __shared__ double sm[];
+  phase_mark(50);
+  cg::grid_group grid = cg::this_grid();
+  int64_t r0, r1;
+  cta_rows(n, r0, r1);
+  const int rows = (int)(r1 - r0);
+  const int R = (int)((n + gridDim.x - 1) / gridDim.x);
+  double* Qs = sm;               // R x cols
+  double* Ws = Qs + R * cols;    // R x q
+  double* W2 = Ws + R * q;       // R x q
+  double* Cs = W2 + R * q;       // cols x q, later R^-1 (q x q)
+  int* bad = reinterpret_cast<int*>(Cs + max(cols * q, q * q));
+  double* chol_sm = Cs + max(cols * q, q * q) + 32;  // CTA 0: Cholesky scratch
+  const int t = threadIdx.x;
+  for (int idx = t; idx < rows * cols; idx += kCT) {
+    const int r = idx / cols, k = idx - r * cols;
+    Qs[idx] = Q[(r0 + r) * ldq + k];
+  }
+  for (int idx = t; idx < rows * q; idx += kCT) {
+    const int r = idx / q, c = idx - r * q;
+    Ws[idx] = W[(r0 + r) * ldw + c];
+  }
+  __syncthreads();
+  phase_mark(51);
+  int pm = 52;
+  const int wpb = kCT / 32;
+  const int gw = blockIdx.x * wpb + (t >> 5);
+  auto cgs = [&]() {
+    const int pq = cols * q;
+    for (int o = t; o < pq; o += kCT) {
+      const int a = o / q, c = o - a * q;
+      double acc = 0.0;
+      for (int r = 0; r < rows; ++r) acc = fma(Qs[r * cols + a], Ws[r * q + c], acc);
+      part[(int64_t)blockIdx.x * pq + o] = acc;
+    }
+    phase_mark(pm++);
+    grid.sync();
+    for (int o = gw; o < pq; o += gridDim.x * wpb) {
+      const double v = warp_sum_partials(part, gridDim.x, pq, o);
+      if ((t & 31) == 0) Cws[o] = v;
+    }
+    grid.sync();
+    phase_mark(pm++);
+    for (int o = t; o < pq; o += kCT) Cs[o] = Cws[o];
+    __syncthreads();
+    for (int idx = t; idx < rows * q; idx += kCT) {
+      const int r = idx / q, c = idx - r * q;
+      const double* qr = Qs + r * cols;
+      double s0 = 0.0, s1 = 0.0;
+      int k = 0;
+      for (; k + 1 < cols; k += 2) {
+        s0 = fma(qr[k], Cs[k * q + c], s0);
+        s1 = fma(qr[k + 1], Cs[(k + 1) * q + c], s1);
+      }
+      if (k < cols) s0 = fma(qr[k], Cs[k * q + c], s0);
+      Ws[idx] -= s0 + s1;
+    }
+    __syncthreads();
+    phase_mark(pm++);
+  };
+  auto cholqr = [&](double thresh, uint64_t bs) {
+    const int qq = q * q;
+    for (int o = t; o < qq; o += kCT) {
+      const int a = o / q, c = o - a * q;
+      double acc = 0.0;
+      for (int r = 0; r < rows; ++r) acc = fma(Ws[r * q + a], Ws[r * q + c], acc);
+      part[(int64_t)blockIdx.x * qq + o] = acc;
+    }
+    phase_mark(pm++);
+    grid.sync();
+    for (int o = gw; o < qq; o += gridDim.x * wpb) {
+      const double v = warp_sum_partials(part, gridDim.x, qq, o);
+      if ((t & 31) == 0) Gws[o] = v;
+    }
+    grid.sync();
+    phase_mark(pm++);
+    if (blockIdx.x == 0) block_cholesky(Gws, q, thresh, chol_sm, Rrel, Rinv, mask, nullptr, nullptr);
+    __syncthreads();
+    phase_mark(pm++);
+    grid.sync();
+    double* Ri = Cs;  // q x q (C is consumed)
+    for (int o = t; o < qq; o += kCT) Ri[o] = Rinv[o];
+    for (int c = t; c < q; c += kCT) bad[c] = mask[c];
+    __syncthreads();
+    for (int idx = t; idx < rows * q; idx += kCT) {
+      const int r = idx / q, c = idx - r * q;
+      double v;
+      if (bad[c]) {
+        v = gauss_c(key, bs + (uint64_t)(r0 + r) * q + c);
+      } else {
+        v = 0.0;
+        for (int k = 0; k <= c; ++k) v = fma(Ws[r * q + k], Ri[k * q + c], v);
+      }
+      W2[idx] = v;
+    }
+    __syncthreads();
+    for (int idx = t; idx < rows * q; idx += kCT) Ws[idx] = W2[idx];
+    __syncthreads();
+    phase_mark(pm++);
+  };
+  for (int round = 0; round < cgs_rounds && cols > 0; ++round) cgs();
+  cholqr(thresh1, base);
+  if (cols > 0) cgs();
+  cholqr(0.0, base + (uint64_t)n * q);
+  for (int idx = t; idx < rows * q; idx += kCT) {
+    const int r = idx / q, c = idx - r * q;
+    W[(r0 + r) * ldw + c] = Ws[idx];
+  }
+  phase_mark(pm < 63 ? pm : 63);
+  if (threadIdx.x == 0 && blockIdx.x == 0) g_phase_ns[49] = pm;
+}
+
 int coop_grid(int64_t n, int sm_count) {
   const int64_t want = (n + kRC - 1) / kRC;
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, sm_count));
@@ -538,6 +667,27 @@ void coop_cholqr(const Launch& L, int64_t n, const double* Wsrc, int64_t lds, do
   }
   MEG_J_DISPATCH(J, MEG_CQR)
 #undef MEG_CQR
+}
+
+
+bool coop_orth(const Launch& L, int64_t n, const double* Q, int64_t ldq, int cols, double* W, int64_t ldw, int q,
+               double thresh1, uint64_t key, uint64_t base, double* part, double* Cws, double* Gws, double* Rinv,
+               int* mask, double* Rrel, int sm_count, int cgs_rounds) {
+  static const bool off = getenv("MEGB200_NO_ORTH_FUSED") != nullptr;  // diagnostics: the five-launch path
+  const int G = coop_grid(n, sm_count);
+  const int R = (int)((n + G - 1) / G);
+  const size_t chol_smem = (size_t)(2 * q * (q + 1) + 2 * q + 1) + 64;
+  const size_t smem =
+      ((size_t)R * cols + 2 * (size_t)R * q + (size_t)std::max(cols * q, q * q) + 32 + chol_smem) * sizeof(double);
+  if (off || q > 32 || q < 1 || smem > 200 * 1024) return false;
+  static bool a = false;
+  if (!a) {
+    raise_smem(k_coop_orth, 200 * 1024);
+    a = true;
+  }
+  coop_launch(L, k_coop_orth, G, smem, n, Q, ldq, cols, W, ldw, q, thresh1, key, base, part, Cws, Gws, Rinv, mask,
+              Rrel, cgs_rounds);
+  return true;
 }
 
 void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, double scale, const double* Lf,

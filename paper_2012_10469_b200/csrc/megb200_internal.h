@@ -130,6 +130,12 @@ void coop_cgs(const Launch& L, int64_t n, const double* Q, int64_t ldq, int cols
 void coop_cholqr(const Launch& L, int64_t n, const double* Wsrc, int64_t lds, double* W, int64_t ldw, int q,
                  double thresh, double* Gws, double* Rrel, double* Rinv, int* mask, const double* Rprev, double* Rtot,
                  uint64_t key, uint64_t base, double* part, int sm_count);
+// The whole orthonormalize() sequence (CGS x cgs_rounds, CholQR(thresh1), CGS, CholQR(0)) of
+// W (n x q) against Q[:, 0:cols] in one cooperative launch; false when the shape does not fit
+// (q > 32 or the staged rows exceed shared memory): the caller then runs the separate launches.
+bool coop_orth(const Launch& L, int64_t n, const double* Q, int64_t ldq, int cols, double* W, int64_t ldw, int q,
+               double thresh1, uint64_t key, uint64_t base, double* part, double* Cws, double* Gws, double* Rinv,
+               int* mask, double* Rrel, int sm_count, int cgs_rounds);
 // Log-map coefficients of a factored iterate computed on the device (so a step
 // can consume the kept weights lam another launch left in device memory):
 // d[k] = log(c1 lam[k]) - log_tail - eta (c1 lam[k] - tail_g) for k < lr.

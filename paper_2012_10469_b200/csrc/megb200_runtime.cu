@@ -285,6 +285,11 @@ void orthonormalize(megb200_solver* s, double* W, int64_t ldw, int q, int cols, 
                     uint64_t& refill_ctr, bool want_relation, int cgs_rounds = 2) {
   Launch L = s->launch();
   const int64_t n = s->n;
+  if (!want_relation && coop_orth(L, n, s->Q, s->ldq, cols, W, ldw, q, 1e-13 * scale, key, refill_ctr, s->red, s->C2,
+                                  s->G, s->Rinv, s->mask, s->Rtmp, s->sm_count, cgs_rounds)) {
+    refill_ctr += 2 * (uint64_t)n * q;
+    return;
+  }
   for (int round = 0; round < cgs_rounds && cols > 0; ++round)
     coop_cgs(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, s->red, s->sm_count);
   coop_cholqr(L, n, W, ldw, W, ldw, q, 1e-13 * scale, s->G, s->R1, s->Rinv, s->mask, nullptr, nullptr, key,
