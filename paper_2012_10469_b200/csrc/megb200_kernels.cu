@@ -687,36 +687,53 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
 }
 
 // ===========================================================================
-// K2: CSR product (sampled-entry gradient), one warp per row, lanes over the
-// row's nonzeros gathering U rows; fixed xor-tree warp reduction.
-template <int BN>
+// K2: CSR product (sampled-entry gradient), one warp per row.  The warp loads 32
+// (col, val) pairs with one coalesced access, then walks them two at a time: each
+// half-warp takes one nonzero and reads that U row with consecutive lanes
+// (columns hl and hl + 16), so a gathered row costs ~b*8/32 sectors instead of
+// one sector per column.  Sixteen steps are unrolled so their row loads are in
+// flight together.  Fixed order: nonzeros in index order per half, halves
+// combined at the end (bitwise reproducible).
 __global__ void __launch_bounds__(256) k_csr_apply(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                                    const double* __restrict__ val, int64_t n,
                                                    const double* __restrict__ U, int64_t ldu, int b,
                                                    double* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= n) return;
-  double acc[BN];
-#pragma unroll
-  for (int c = 0; c < BN; ++c) acc[c] = 0.0;
+  double a0 = 0.0, a1 = 0.0;
   const int e0 = rowptr[row], e1 = rowptr[row + 1];
-  for (int e = e0 + lane; e < e1; e += 32) {
-    const int64_t j = col[e];
-    const double g = val[e];
-    const double* u = U + j * ldu;
+  const bool c0 = hl < b, c1 = hl + 16 < b;
+  for (int base = e0; base < e1; base += 32) {
+    const int e = base + lane;
+    int j = 0;
+    double g = 0.0;
+    if (e < e1) {
+      j = __ldg(col + e);
+      g = __ldg(val + e);
+    }
+    double u0[16], u1[16], gg[16];
 #pragma unroll
-    for (int c = 0; c < BN; ++c)
-      if (c < b) acc[c] = fma(g, __ldg(u + c), acc[c]);
+    for (int s2 = 0; s2 < 16; ++s2) {
+      const int src = 2 * s2 + half;
+      const int jj = __shfl_sync(0xffffffffu, j, src);
+      gg[s2] = __shfl_sync(0xffffffffu, g, src);
+      const double* u = U + (int64_t)jj * ldu;
+      u0[s2] = c0 ? __ldg(u + hl) : 0.0;
+      u1[s2] = c1 ? __ldg(u + hl + 16) : 0.0;
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < 16; ++s2) {
+      a0 = fma(gg[s2], u0[s2], a0);
+      a1 = fma(gg[s2], u1[s2], a1);
+    }
   }
-#pragma unroll
-  for (int c = 0; c < BN; ++c) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+  a0 += __shfl_xor_sync(0xffffffffu, a0, 16);
+  a1 += __shfl_xor_sync(0xffffffffu, a1, 16);
+  if (half == 0) {
+    if (c0) out[row * b + hl] = a0;
+    if (c1) out[row * b + hl + 16] = a1;
   }
-#pragma unroll
-  for (int c = 0; c < BN; ++c)
-    if (c < b && lane == (c & 31)) out[row * b + c] = acc[c];
 }
 
 // W = scale * sum_s part[s] + L E + alpha U
@@ -1461,15 +1478,8 @@ int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, 
 
 void csr_apply_partial(const Launch& L, const int32_t* rowptr, const int32_t* col, const double* val, int64_t n,
                        const double* U, int64_t ldu, int b, double* part) {
-  const dim3 grid(cdiv(n, 8));
-  if (b <= 8)
-    k_csr_apply<8><<<grid, 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
-  else if (b <= 16)
-    k_csr_apply<16><<<grid, 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
-  else if (b <= 24)
-    k_csr_apply<24><<<grid, 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
-  else
-    k_csr_apply<32><<<grid, 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
+  if (b > 32) throw Error(MEGB200_ERR_PARAM, "CSR pass supports b <= 32");
+  k_csr_apply<<<cdiv(n, 8), 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
   MEG_LAUNCHED();
   ++*L.counter;
 }
