@@ -510,8 +510,10 @@ constexpr size_t mma_smem_bytes() {
 // Columns [0, 8 NT) of the block go through DMMA (tensor pipe); the TAIL (< 8)
 // columns after them through DFMA on the FP64 pipe, which runs concurrently --
 // so k = 18 costs 2 DMMA n-tiles + 2 DFMA columns instead of 3 padded n-tiles.
-template <int NT, int TAIL>
-__global__ void __launch_bounds__(kPipeThreads, 1)
+// CW consumer warps: 8 (warp w owns rows [16w, 16w+16), two m-tiles) or 16 (warp w owns one
+// 8-row m-tile: rows [8w, 8w+8); twice the warps per SMSP to hide fragment-load latency)
+template <int NT, int TAIL, int CW>
+__global__ void __launch_bounds__(32 * (CW + 1), 1)
     k_dense_pass_mma(const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmU, int64_t n,
                      int b, double* __restrict__ part, int tiles, int kch, int smax) {
   // Stream-K: the (row tile, 32-row k chunk) space, tile-major, is cut into
@@ -540,7 +542,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
   if (threadIdx.x == 0) {
     for (int st = 0; st < kPipeStages; ++st) {
       pipe::bar_init(full + st, 1);
-      pipe::bar_init(empty + st, kPipeConsumers);
+      pipe::bar_init(empty + st, CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmM) : "memory");
@@ -550,7 +552,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
   // launched programmatically dependent on the previous kernel: everything above
   // overlapped its tail; U and the partial buffer are touched only after it completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (warp == kPipeConsumers) {
+  if (warp == CW) {
     if (lane == 0) {
       const uint32_t stage_bytes = (uint32_t)(kPipeKC * kMmaRows * 8 + kPipeKC * BNP * 8);
       const uint64_t pol = pipe::evict_first_policy();
@@ -576,6 +578,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
     }
     return;
   }
+  constexpr int MT = 16 / (CW / 8) / 8;  // m-tiles per warp: 2 (CW = 8) or 1 (CW = 16)
+  const int mrow0 = (CW == 16) ? 8 * (warp & 1) : 0;  // first row of this warp within its box
   const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
   const int kperm = 2 * tq;  // {0,2,4,6}; +1 for the second MMA of a k group
   int st = 0;
@@ -591,45 +595,48 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
     const int slot = (int)blockIdx.x - cfirst;
     // two accumulator sets (even / odd k steps): dependent DMMAs on one accumulator
     // are 2 * 2 * NT instructions apart, which covers the DMMA latency
-    double acc[2][2][NT][2];
+    double acc[2][MT][NT][2];
 #pragma unroll
     for (int ps = 0; ps < 2; ++ps)
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[ps][mt][nt][0] = acc[ps][mt][nt][1] = 0.0;
-    double tl[2][TL];  // DFMA tail: rows g / 8+g, this lane's k subset
+    double tl[MT][TL];  // DFMA tail: rows g (/ 8+g), this lane's k subset
 #pragma unroll
-    for (int tc = 0; tc < TL; ++tc) tl[0][tc] = tl[1][tc] = 0.0;
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int tc = 0; tc < TL; ++tc) tl[mt][tc] = 0.0;
     for (; u < uend; ++u) {
       const int64_t kc = (u - (int64_t)tile * kch) * kPipeKC;
       const int nk = (int)min((int64_t)kPipeKC, n - kc);  // the last chunk of a row may be short
       pipe::bar_wait(full + st, ph);
-      const char* box = reinterpret_cast<const char*>(Ms + (size_t)st * kPipeKC * kMmaRows) + warp * 4096;
+      const char* box = reinterpret_cast<const char*>(Ms + (size_t)st * kPipeKC * kMmaRows) + (warp / (CW / 8)) * 4096;
       const double* us = Us + (size_t)st * kPipeKC * BNP;
-      auto mma_k = [&](int k, double (&ac)[2][NT][2]) {  // one m8n8k4 step over k rows {k + kperm}
+      auto mma_k = [&](int k, double (&ac)[MT][NT][2]) {  // one m8n8k4 step over k rows {k + kperm}
         const int kk = k + kperm;
         const bool valid = kk < nk;
         const int sw = kk & 7;
-        const double a0 = valid ? *reinterpret_cast<const double*>(box + kk * 128 + (((g >> 1) ^ sw) << 4) +
-                                                                    ((g & 1) << 3))
-                                : 0.0;
-        const double a1 = valid ? *reinterpret_cast<const double*>(box + kk * 128 + ((((8 + g) >> 1) ^ sw) << 4) +
-                                                                    ((g & 1) << 3))
-                                : 0.0;
+        double a[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int rib = mrow0 + 8 * mt + g;  // row within the 16-row box
+          a[mt] = valid ? *reinterpret_cast<const double*>(box + kk * 128 + (((rib >> 1) ^ sw) << 4) + ((rib & 1) << 3))
+                        : 0.0;
+        }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const double bv = valid ? us[kk * BNP + nt * 8 + g] : 0.0;
-          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-              : "+d"(ac[0][nt][0]), "+d"(ac[0][nt][1]) : "d"(a0), "d"(bv));
-          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-              : "+d"(ac[1][nt][0]), "+d"(ac[1][nt][1]) : "d"(a1), "d"(bv));
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(ac[mt][nt][0]), "+d"(ac[mt][nt][1]) : "d"(a[mt]), "d"(bv));
         }
 #pragma unroll
         for (int tc = 0; tc < TAIL; ++tc) {
           const double bt = valid ? us[kk * BNP + 8 * NT + tc] : 0.0;
-          tl[0][tc] = fma(a0, bt, tl[0][tc]);
-          tl[1][tc] = fma(a1, bt, tl[1][tc]);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) tl[mt][tc] = fma(a[mt], bt, tl[mt][tc]);
         }
       };
 #pragma unroll
@@ -648,9 +655,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
     }
     // C fragment: row g, columns 2*tq, 2*tq+1 of each 8x8 tile
     double* out = part + (int64_t)slot * n * b;
-    const int rbase = warp * 16;
+    const int rbase = (CW == 16) ? warp * 8 : warp * 16;
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
+    for (int mt = 0; mt < MT; ++mt) {
       const int64_t row = i0 + rbase + mt * 8 + g;
       if (row < n) {
 #pragma unroll
@@ -663,7 +670,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
     }
     // DFMA tail: sum the four k-subset lanes (tq) of each row, fixed xor order
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
+    for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
       for (int tc = 0; tc < TAIL; ++tc) {
         double v = tl[mt][tc];
@@ -677,7 +684,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
       // zero the tile's slots no CTA covers (rows of this warp)
       for (int sl = slot + 1; sl < smax; ++sl) {
         double* z = part + (int64_t)sl * n * b;
-        for (int idx = lane; idx < 16 * b; idx += 32) {
+        for (int idx = lane; idx < 8 * MT * b; idx += 32) {
           const int64_t row = i0 + rbase + idx / b;
           if (row < n) z[row * b + idx % b] = 0.0;
         }
@@ -1328,13 +1335,26 @@ void dispatch_pipe(const Launch& L, const T* M, int64_t ldm, int64_t n, const do
   }
 }
 
+// 8 consumer warps (two m-tiles each); the 16-warp variant measured slower (47 vs 37 us at
+// n = 4096, k = 18) and is kept only as a diagnostics option (MEGB200_MMA_WARPS=16)
+int mma_consumer_warps() {
+  static const int cw = [] {
+    const char* e = getenv("MEGB200_MMA_WARPS");
+    return (e && atoi(e) == 16) ? 16 : 8;
+  }();
+  return cw;
+}
+
 template <int NT, int TAIL>
 void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
                      double* part, int tiles, int kch, int smax, int grid) {
   constexpr size_t smem = mma_smem_bytes<NT, TAIL>();
+  const int cw = mma_consumer_warps();
   static bool attr = false;
   if (!attr) {
-    MEG_CUDA(cudaFuncSetAttribute(k_dense_pass_mma<NT, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MEG_CUDA(cudaFuncSetAttribute(k_dense_pass_mma<NT, TAIL, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    MEG_CUDA(cudaFuncSetAttribute(k_dense_pass_mma<NT, TAIL, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     attr = true;
   }
@@ -1346,7 +1366,7 @@ void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, c
   // tensor-map prefetch) overlaps the preceding kernel
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kPipeThreads);
+  cfg.blockDim = dim3(32 * (cw + 1));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = L.stream;
   cudaLaunchAttribute pdl[1];
@@ -1354,7 +1374,10 @@ void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, c
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL>, tmM, tmU, n, b, part, tiles, kch, smax));
+  if (cw == 16)
+    MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL, 16>, tmM, tmU, n, b, part, tiles, kch, smax));
+  else
+    MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL, 8>, tmM, tmU, n, b, part, tiles, kch, smax));
   MEG_LAUNCHED();
   ++*L.counter;
 }

@@ -30,7 +30,11 @@
 
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "megb200_internal.h"
+
+namespace cg = cooperative_groups;
 
 #define JACOBI_MARK(slot)
 #include "megb200_jacobi.cuh"
@@ -86,12 +90,20 @@ __device__ __forceinline__ bool arrive_last(unsigned* ticket, unsigned expected,
 // res.  Returns true in the one CTA that wrote res (whichever CTAs arrive last, the
 // association -- hence every bit of res -- is the same).  tick: 1 + #groups tickets.
 constexpr int kGroup = 8;
-template <int NT>
+template <int NT, bool CL>
 __device__ __forceinline__ bool tree_reduce(const double* part, double* gpart, double* res, int count,
                                             int64_t stride, unsigned* tick, int* s_flag) {
   const int G = gridDim.x, NG = (G + kGroup - 1) / kGroup, grp = blockIdx.x / kGroup;
   const int g0 = grp * kGroup, gn = min(kGroup, G - g0);
-  if (!arrive_last(tick + 1 + grp, (unsigned)gn, s_flag)) return false;
+  if constexpr (CL) {
+    // launched as clusters of kGroup CTAs (cluster = group): the hardware cluster barrier
+    // (release / acquire at cluster scope) replaces the group ticket; rank 0 sums the group
+    __threadfence_block();
+    cg::this_cluster().sync();
+    if (cg::this_cluster().block_rank() != 0) return false;
+  } else {
+    if (!arrive_last(tick + 1 + grp, (unsigned)gn, s_flag)) return false;
+  }
   for (int o = threadIdx.x; o < count; o += NT) gpart[grp * stride + o] = ordered_sum(part, g0, gn, stride, o);
   if (!arrive_last(tick, (unsigned)NG, s_flag)) return false;
   for (int o = threadIdx.x; o < count; o += NT) res[o] = ordered_sum(gpart, 0, NG, stride, o);
@@ -108,8 +120,7 @@ __device__ __forceinline__ void publish(unsigned* flag, unsigned epoch) {
 
 __device__ __forceinline__ void wait_published(const unsigned* flag, unsigned epoch) {
   if (threadIdx.x == 0)
-    while (ld_acquire_u32(flag) != epoch) {
-    }
+    while (ld_acquire_u32(flag) != epoch) __nanosleep(40);  // back off: keep the flag's L2 line quiet
   __syncthreads();
 }
 
@@ -307,7 +318,7 @@ __device__ bool rr_small_neardiag(const double* __restrict__ Hg, int64_t ldh, in
   return true;
 }
 
-template <int NT>
+template <int NT, bool CL>
 __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs a) {
   // programmatic dependent launch after the operand pass: nothing is read before it completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -360,7 +371,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
         const int k = o / b, c = o - k * b;
         p0[o] = rows_dot(Ls, l, k, Us, b, c, rows);
       }
-      if (tree_reduce<NT>(a.part0, a.part0 + (int64_t)G * kFusedStride, a.Ews, l * b, kFusedStride, a.sync,
+      if (tree_reduce<NT, CL>(a.part0, a.part0 + (int64_t)G * kFusedStride, a.Ews, l * b, kFusedStride, a.sync,
                       &s_flag))
         publish(a.sync + kFusedFlags, a.epoch);
       else
@@ -405,7 +416,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
     }
   }
   stamp(st0, 3);
-  if (tree_reduce<NT>(a.part1, a.part1 + (int64_t)G * kFusedStride, Hs, b * b, kFusedStride, a.sync + 32, &s_flag)) {
+  if (tree_reduce<NT, CL>(a.part1, a.part1 + (int64_t)G * kFusedStride, Hs, b * b, kFusedStride, a.sync + 32, &s_flag)) {
     stamp(a.stamps, 4);
     stamp(a.stamps, 5);
     if (!rr_small_neardiag<NT>(Hs, b, b, a.theta, a.Sout, jac, thsh, a.info)) {
@@ -545,7 +556,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
   }
   stamp(st0, 9);
   double* res2 = a.part2 + (int64_t)(G + (G + kGroup - 1) / kGroup) * kFusedStride;
-  if (tree_reduce<NT>(a.part2, a.part2 + (int64_t)G * kFusedStride, res2, pw, kFusedStride, a.sync + 64, &s_flag)) {
+  if (tree_reduce<NT, CL>(a.part2, a.part2 + (int64_t)G * kFusedStride, res2, pw, kFusedStride, a.sync + 64, &s_flag)) {
     stamp(a.stamps, 10);
     for (int o = t; o < pw; o += NT) {
       const double v = res2[o];
@@ -583,7 +594,8 @@ int fused_pass_rows(int64_t n, int sm_count) {
     const char* e = getenv("MEGB200_FUSED_ROWS");
     return e ? std::max(1, atoi(e)) : 32;
   }();
-  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count, (n + target - 1) / target));
+  int G = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count, (n + target - 1) / target));
+  if (G >= kGroup) G -= G % kGroup;  // whole clusters of kGroup CTAs
   return (int)((n + G - 1) / G);
 }
 
@@ -599,11 +611,12 @@ bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count) {
          fused_pass_smem(n, b, l, b, sm_count) <= (size_t)200 * 1024;
 }
 
-template <int NT>
+template <int NT, bool CL>
 void launch_fused(const Launch& L, const FusedPassArgs& a, int G, size_t smem) {
   static bool attr = false;
   if (!attr) {
-    MEG_CUDA(cudaFuncSetAttribute(k_fused_first_pass<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    MEG_CUDA(cudaFuncSetAttribute(k_fused_first_pass<NT, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -611,27 +624,71 @@ void launch_fused(const Launch& L, const FusedPassArgs& a, int G, size_t smem) {
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = L.stream;
-  cudaLaunchAttribute pdl[1];
-  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  pdl[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = pdl;
-  cfg.numAttrs = 1;
-  MEG_CUDA(cudaLaunchKernelEx(&cfg, k_fused_first_pass<NT>, a));
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  int na = 1;
+  if (CL) {
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = kGroup;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    na = 2;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  MEG_CUDA(cudaLaunchKernelEx(&cfg, k_fused_first_pass<NT, CL>, a));
   MEG_LAUNCHED();
   ++*L.counter;
 }
 
+// clusters of kGroup CTAs when every cluster of the grid can be resident at once (the release
+// flags need co-residency); otherwise the ticket version
+template <int NT>
+bool cluster_fits(int G, size_t smem) {
+  static int max_clusters = -1;
+  if (max_clusters < 0) {
+    MEG_CUDA(cudaFuncSetAttribute(k_fused_first_pass<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = 200 * 1024;  // worst case of the supported shapes
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kGroup;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k_fused_first_pass<NT, true>, &cfg) != cudaSuccess) nc = 0;
+    cudaGetLastError();
+    max_clusters = nc;
+  }
+  (void)smem;
+  return G % kGroup == 0 && G / kGroup <= max_clusters;
+}
+
 void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count) {
+  // clusters of 8 replace the group tickets with the hardware cluster barrier; measured ~1.5 us
+  // faster per step but with sporadic 2x slow runs (cluster placement under the pass's tail), so
+  // they are a diagnostics option (MEGB200_CLUSTER=1), not the default
+  static const bool no_cluster = getenv("MEGB200_CLUSTER") == nullptr;
   a.R = fused_pass_rows(a.n, sm_count);
-  const int G = (int)((a.n + a.R - 1) / a.R);
+  int G = (int)((a.n + a.R - 1) / a.R);
   const size_t smem = fused_pass_smem(a.n, a.b, a.l, a.rq, sm_count);
   if (!(a.b >= 2 && a.b <= 32 && a.rq <= a.b && a.nreq <= a.rq && a.gr <= a.rq && a.l <= kFusedMaxL) ||
       smem > (size_t)200 * 1024 || G > sm_count)
     throw Error(MEGB200_ERR_PARAM, "fused first pass: unsupported shape");
-  switch (fused_nt()) {
-    case 1024: launch_fused<1024>(L, a, G, smem); break;
-    case 512: launch_fused<512>(L, a, G, smem); break;
-    default: launch_fused<256>(L, a, G, smem); break;
+  const int nt = fused_nt();
+  const bool cl = !no_cluster && G % kGroup == 0 &&
+                  (nt == 1024 ? cluster_fits<1024>(G, smem) : nt == 512 ? cluster_fits<512>(G, smem)
+                                                                        : cluster_fits<256>(G, smem));
+  switch (nt) {
+    case 1024: cl ? launch_fused<1024, true>(L, a, G, smem) : launch_fused<1024, false>(L, a, G, smem); break;
+    case 512: cl ? launch_fused<512, true>(L, a, G, smem) : launch_fused<512, false>(L, a, G, smem); break;
+    default: cl ? launch_fused<256, true>(L, a, G, smem) : launch_fused<256, false>(L, a, G, smem); break;
   }
 }
 
