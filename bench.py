@@ -48,6 +48,8 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline sampling")
+    ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi clock sampling interval (ms)")
+    ap.add_argument("--prof-stride", type=int, default=8, help="bracket every N-th pass with events (0: off)")
     return ap.parse_args()
 
 
@@ -105,8 +107,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, interval_ms: int = 50):
         self.gpu = gpu_index
+        self.interval = max(1, int(interval_ms))
         self.proc = None
         self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
 
@@ -115,7 +118,7 @@ class ClockSampler:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=self.fh, stderr=subprocess.DEVNULL)
+                 "-lms", str(self.interval)], stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
@@ -254,11 +257,11 @@ def run_device_arm(args, world, rank, local):
     import ctypes as C
 
     K = args.steps
-    prof_stride = 8  # roofline: every 8th pass kernel bracketed by events (keeps the perturbation small)
+    prof_stride = args.prof_stride  # roofline: every 8th pass kernel bracketed by events (small perturbation)
     lib.megb200_profile_enable(solver.handle, prof_stride)
     pm, pc, pb_bytes = C.c_double(), C.c_int64(), C.c_double()
     lib.megb200_profile_read(solver.handle, C.byref(pm), C.byref(pc), C.byref(pb_bytes))  # reset
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local, args.clock_ms)
     sampler.start()
     time.sleep(0.3)  # let nvidia-smi attach before the timed region
     barrier(world)

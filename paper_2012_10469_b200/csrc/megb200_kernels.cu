@@ -639,11 +639,45 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1)
           for (int mt = 0; mt < MT; ++mt) tl[mt][tc] = fma(a[mt], bt, tl[mt][tc]);
         }
       };
+      // full chunks (all but possibly the last k chunk of a row): no bounds predicates; the
+      // swizzled fragment addresses are per-lane bases plus immediates
+      auto mma_full = [&](int k, double (&ac)[MT][NT][2]) {
+        const int kk = k + kperm;
+        const int sw = kk & 7;
+        double a[MT];
 #pragma unroll
-      for (int k8 = 0; k8 < kPipeKC; k8 += 8) {
-        if (k8 < nk) {
-          mma_k(k8, acc[0]);
-          mma_k(k8 + 1, acc[1]);
+        for (int mt = 0; mt < MT; ++mt) {
+          const int rib = mrow0 + 8 * mt + g;
+          a[mt] = *reinterpret_cast<const double*>(box + kk * 128 + (((rib >> 1) ^ sw) << 4) + ((rib & 1) << 3));
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double bv = us[kk * BNP + nt * 8 + g];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(ac[mt][nt][0]), "+d"(ac[mt][nt][1]) : "d"(a[mt]), "d"(bv));
+        }
+#pragma unroll
+        for (int tc = 0; tc < TAIL; ++tc) {
+          const double bt = us[kk * BNP + 8 * NT + tc];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) tl[mt][tc] = fma(a[mt], bt, tl[mt][tc]);
+        }
+      };
+      if (nk == kPipeKC) {
+#pragma unroll
+        for (int k8 = 0; k8 < kPipeKC; k8 += 8) {
+          mma_full(k8, acc[0]);
+          mma_full(k8 + 1, acc[1]);
+        }
+      } else {
+#pragma unroll
+        for (int k8 = 0; k8 < kPipeKC; k8 += 8) {
+          if (k8 < nk) {
+            mma_k(k8, acc[0]);
+            mma_k(k8 + 1, acc[1]);
+          }
         }
       }
       __syncwarp();
