@@ -199,6 +199,8 @@ struct FusedPassArgs {
   double* host_pack = nullptr;
   int pack_count = 0;
   unsigned long long* stamps = nullptr;  // diagnostics: phase timestamps (or null)
+  double* vgram = nullptr;  // optional out: Gram of the first nvg columns of L (phase 0 only)
+  int nvg = 0;
 };
 bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count);
 void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count);

@@ -73,6 +73,9 @@ struct megb200_solver {
   int64_t h_buf_len = 0;
   unsigned* fsync = nullptr;  // tickets / flags of the fused first-pass kernel (zeroed)
   unsigned epoch = 0;
+  int want_vgram = 0;      // host-buffer step: fused phase 0 also reduces the factor Gram (r x r)
+  bool vgram_done = false;
+  int64_t pack_vgram = 0;  // its offset in the result pack
   int rr_nvec = 0;  // Ritz pairs a wide Rayleigh-Ritz must return (0: all); set by top_eigs
   double m_norm2_cache = NAN, m_trace_cache = NAN;
   const void* m_cache_ptr = nullptr;
@@ -497,6 +500,14 @@ int fused_pass(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu,
   a.epoch = s->epoch;
   a.pack = s->pack;
   a.pack_count = (int)(s->pack_gram + (int64_t)a.gr * a.gr);
+  if (s->want_vgram > 0 && !op.Eg && a.L && a.l >= s->want_vgram && s->want_vgram <= 32 &&
+      a.l * bw + s->want_vgram * s->want_vgram <= kFusedStride) {
+    a.vgram = s->pack + s->pack_vgram;
+    a.nvg = s->want_vgram;
+    a.pack_count = (int)(s->pack_vgram + (int64_t)a.nvg * a.nvg);
+    s->vgram_done = true;
+  }
+  s->want_vgram = 0;
   a.host_pack = s->h_buf_dev ? s->h_buf_dev + (dst - s->h_buf) : nullptr;
   static const bool stamps = getenv("MEGB200_FUSED_STAMPS") != nullptr;
   if (stamps) a.stamps = reinterpret_cast<unsigned long long*>(s->fsync + 128);
@@ -1001,6 +1012,7 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
     s->pack_resid = s->cap;
     s->pack_epi = s->cap + 64;
     s->pack_gram = s->cap + 64 + 136;
+    s->pack_vgram = s->pack_gram + 32 * 32;  // after the fused kernel's Ritz-block Gram (<= 32 x 32)
     s->theta = s->pack;  // theta lives at the head of the pack
     s->resid = s->pack + s->pack_resid;
     // [pack copy | scratch | pipelined read-back slot 0 | slot 1]
@@ -1570,12 +1582,23 @@ int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_ho
     else
       MEG_CUDA(cudaMemcpy2DAsync(Vd, r * sizeof(double), x_host->V, x_host->ldv * sizeof(double), r * sizeof(double),
                                  n, cudaMemcpyHostToDevice, s->stream));
-    // LowRankIterate validation (meg.py:69-71): V^T V is formed now and read back with the
-    // step's first wait; a failed check discards the step and raises before any result
-    coop_tn(L, n, Vd, r, (int)r, Vd, r, (int)r, s->G, (int)r, nullptr, 1.0, s->red, s->sm_count);
+    // LowRankIterate validation (meg.py:69-71): V^T V is reduced by the fused first pass (with
+    // L^T U) and arrives in the result pack; a failed check discards the step and raises before
+    // any result.  Steps that do not take the fused path form it separately after the solve.
     double* gram_dst = s->h_buf + 4 * s->pack_len;  // pinned slot (pack_len >= 64 x 64 doubles)
-    s->d2h(gram_dst, s->G, r * r);
+    s->want_vgram = (int)r;
+    s->vgram_done = false;
+    auto gram_fetch = [&]() {
+      if (s->vgram_done) {
+        std::copy(s->h_buf + s->pack_vgram, s->h_buf + s->pack_vgram + r * r, gram_dst);
+      } else {
+        coop_tn(L, n, Vd, r, (int)r, Vd, r, (int)r, s->G, (int)r, nullptr, 1.0, s->red, s->sm_count);
+        s->d2h(gram_dst, s->G, r * r);
+        s->sync();
+      }
+    };
     auto gram_check = [&]() {
+      gram_fetch();
       double ge = 0.0;
       for (int i = 0; i < (int)r; ++i)
         for (int j = 0; j < (int)r; ++j) ge = std::max(ge, fabs(gram_dst[i * r + j] - (i == j ? 1.0 : 0.0)));
@@ -1601,13 +1624,25 @@ int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_ho
     o.V_next = Vn;
     o.ld_next = r;
     bool v_done = false;
+    // a mapped pinned destination takes V_next straight from the kernels (no read-back copy)
+    double* vn_mapped = nullptr;
+    if (ld_next_host == r && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&vn_mapped), V_next_host, 0) != cudaSuccess) {
+      cudaGetLastError();
+      vn_mapped = nullptr;
+    }
+    if (vn_mapped) o.V_next = vn_mapped;
     try {
-      step_core(s, &it, &gg, eta, eps_next, opts, &o, ld_next_host == r ? V_next_host : nullptr, r, &v_done);
+      step_core(s, &it, &gg, eta, eps_next, opts, &o, (ld_next_host == r && !vn_mapped) ? V_next_host : nullptr, r,
+                &v_done);
+      if (vn_mapped) v_done = true;
     } catch (const Error&) {
+      s->want_vgram = 0;
       s->sync();
       gram_check();  // an invalid factor takes precedence over what the step made of it
       throw;
     }
+    s->want_vgram = 0;
     s->sync();
     gram_check();
     if (!v_done) {

@@ -371,11 +371,19 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
         const int k = o / b, c = o - k * b;
         p0[o] = rows_dot(Ls, l, k, Us, b, c, rows);
       }
-      if (tree_reduce<NT, CL>(a.part0, a.part0 + (int64_t)G * kFusedStride, a.Ews, l * b, kFusedStride, a.sync,
-                      &s_flag))
+      // optional: the Gram of the first nvg factor columns (LowRankIterate validation, meg.py:69-71)
+      const int nvg = a.vgram ? a.nvg : 0;
+      for (int o = t; o < nvg * nvg; o += NT) {
+        const int k = o / nvg, c = o - k * nvg;
+        p0[l * b + o] = rows_dot(Ls, l, k, Ls, l, c, rows);
+      }
+      if (tree_reduce<NT, CL>(a.part0, a.part0 + (int64_t)G * kFusedStride, a.Ews, l * b + nvg * nvg, kFusedStride,
+                              a.sync, &s_flag)) {
+        for (int o = t; o < nvg * nvg; o += NT) a.vgram[o] = a.Ews[l * b + o];
         publish(a.sync + kFusedFlags, a.epoch);
-      else
+      } else {
         wait_published(a.sync + kFusedFlags, a.epoch);
+      }
       for (int idx = t; idx < l * b; idx += NT) Es[idx] = dsh[idx / b] * __ldcg(a.Ews + idx);
     }
   }
