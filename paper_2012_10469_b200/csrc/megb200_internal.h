@@ -201,6 +201,7 @@ struct FusedPassArgs {
   unsigned long long* stamps = nullptr;  // diagnostics: phase timestamps (or null)
   double* vgram = nullptr;  // optional out: Gram of the first nvg columns of L (phase 0 only)
   int nvg = 0;
+  bool stage_l = true;  // set by fused_first_pass: L rows staged in shared memory
 };
 bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count);
 void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count);

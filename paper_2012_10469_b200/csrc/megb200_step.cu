@@ -337,8 +337,11 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
   double* Ss = Ws + R * b;    // b x rq
   double* red = Ss + b * rq;  // NT
   double* Hs = red + NT;     // b x b: the reduced H (last CTA of phase 1)
-  double* Ls = Hs + b * b;    // R x l      } phases 0-1
-  double* Es = Ls + R * l;    // l x b      }
+  double* Ls = Hs + b * b;    // R x l      } phases 0-1 (L rows staged unless shared memory is short,
+  const bool stL = a.stage_l;  //           } then read from global: cfg5-sized row ranges)
+  double* Es = stL ? Ls + R * l : Ls;  // l x b
+  const double* Lb = stL ? Ls : a.L + r0 * a.ldl;
+  const int ldL = stL ? l : (int)a.ldl;
   double* jac = Es + l * b;   // Jacobi scratch (the last CTA of phase 1)
   double* Ts = Ls;            // R x rq: phase 2 (reuses the phase 0-1 region)
 
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
     dsh[k] = v;
   }
   stage_rows<NT>(Us, a.U, a.ldu, r0, rows, b);
-  if (l > 0) stage_rows<NT>(Ls, a.L, a.ldl, r0, rows, l);
+  if (l > 0 && stL) stage_rows<NT>(Ls, a.L, a.ldl, r0, rows, l);
   __syncthreads();
   stamp(st0, 1);
 
@@ -369,13 +372,13 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
       double* p0 = a.part0 + (int64_t)g * kFusedStride;
       for (int o = t; o < l * b; o += NT) {
         const int k = o / b, c = o - k * b;
-        p0[o] = rows_dot(Ls, l, k, Us, b, c, rows);
+        p0[o] = rows_dot(Lb, ldL, k, Us, b, c, rows);
       }
       // optional: the Gram of the first nvg factor columns (LowRankIterate validation, meg.py:69-71)
       const int nvg = a.vgram ? a.nvg : 0;
       for (int o = t; o < nvg * nvg; o += NT) {
         const int k = o / nvg, c = o - k * nvg;
-        p0[l * b + o] = rows_dot(Ls, l, k, Ls, l, c, rows);
+        p0[l * b + o] = rows_dot(Lb, ldL, k, Lb, ldL, c, rows);
       }
       if (tree_reduce<NT, CL>(a.part0, a.part0 + (int64_t)G * kFusedStride, a.Ews, l * b + nvg * nvg, kFusedStride,
                               a.sync, &s_flag)) {
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
 #pragma unroll
       for (int tt = 0; tt < 16; ++tt) s += pv[tt];
       for (int tt = 16; tt < a.S; ++tt) s += pp[tt * slice];
-      const double* Lr = Ls + rr * l;
+      const double* Lr = Lb + rr * ldL;
       double v0 = a.scale * s + a.alpha * Us[idx], v1 = 0.0;
       int k = 0;
       for (; k + 1 < l; k += 2) {
@@ -607,16 +610,23 @@ int fused_pass_rows(int64_t n, int sm_count) {
   return (int)((n + G - 1) / G);
 }
 
-size_t fused_pass_smem(int64_t n, int b, int l, int rq, int sm_count) {
+constexpr size_t kFusedSmemMax = 200 * 1024;
+
+// shared memory of the fused kernel; L rows are staged when they fit (stage_l), else read from global
+size_t fused_pass_smem(int64_t n, int b, int l, int rq, int sm_count, bool* stage_l = nullptr) {
   const int R = fused_pass_rows(n, sm_count);
   const size_t jac = std::max((size_t)jacobi_smem_doubles(b), (size_t)5 * b * b + 128);
-  const size_t tail = std::max((size_t)R * l + (size_t)l * b + jac, (size_t)R * rq);
-  return ((size_t)2 * R * b + (size_t)b * rq + fused_nt() + (size_t)b * b + tail) * sizeof(double);
+  const size_t head = (size_t)2 * R * b + (size_t)b * rq + fused_nt() + (size_t)b * b;
+  const size_t with_l = (head + std::max((size_t)R * l + (size_t)l * b + jac, (size_t)R * rq)) * sizeof(double);
+  const size_t without = (head + std::max((size_t)l * b + jac, (size_t)R * rq)) * sizeof(double);
+  const bool st = with_l <= kFusedSmemMax;
+  if (stage_l) *stage_l = st;
+  return st ? with_l : without;
 }
 
 bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count) {
   return b >= 2 && b <= 32 && nreq <= b && l >= 0 && l <= kFusedMaxL && n >= b &&
-         fused_pass_smem(n, b, l, b, sm_count) <= (size_t)200 * 1024;
+         fused_pass_smem(n, b, l, b, sm_count) <= kFusedSmemMax;
 }
 
 template <int NT, bool CL>
@@ -685,9 +695,11 @@ void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count) {
   static const bool no_cluster = getenv("MEGB200_CLUSTER") == nullptr;
   a.R = fused_pass_rows(a.n, sm_count);
   int G = (int)((a.n + a.R - 1) / a.R);
-  const size_t smem = fused_pass_smem(a.n, a.b, a.l, a.rq, sm_count);
+  bool stage_l = true;
+  const size_t smem = fused_pass_smem(a.n, a.b, a.l, a.rq, sm_count, &stage_l);
+  a.stage_l = stage_l;
   if (!(a.b >= 2 && a.b <= 32 && a.rq <= a.b && a.nreq <= a.rq && a.gr <= a.rq && a.l <= kFusedMaxL) ||
-      smem > (size_t)200 * 1024 || G > sm_count)
+      smem > kFusedSmemMax || G > sm_count)
     throw Error(MEGB200_ERR_PARAM, "fused first pass: unsupported shape");
   const int nt = fused_nt();
   const bool cl = !no_cluster && G % kGroup == 0 &&
