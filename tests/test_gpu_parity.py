@@ -365,3 +365,47 @@ def test_host_buffer_step_matches_device_step(pb):
     bad[:, 0] *= 1.5
     with pytest.raises(pb.ParameterError):
         pb.lowrank_meg_step_host(bad, lam, eps, dev, 1.0, 0.01)
+
+
+@pytest.mark.parametrize("m", [56, 96, 112])
+@pytest.mark.parametrize("spectrum", ["separated", "clustered", "repeated"])
+def test_wide_rayleigh_ritz(pb, m, spectrum):
+    """The wide Rayleigh-Ritz solver (k_rr_wide: tridiagonalisation + multisection + twisted
+    eigenvectors, verified, cyclic-Jacobi fallback) against numpy.linalg.eigh on restarted-basis-like
+    spectra: theta non-increasing, eigenvalues to 1e-12 ||H||, the returned columns orthonormal and
+    eigenvectors to 1e-12 ||H|| (linalg.py:205-211 semantics), for all pairs and for a top-nvec solve."""
+    import ctypes as C
+
+    import torch
+    from paper_2012_10469_b200 import runtime
+
+    rng = np.random.default_rng(m + len(spectrum))
+    top = -1.0 - 0.4 * np.arange(10)
+    if spectrum == "separated":
+        ev = np.concatenate([top, -13.6 - 3.0 * rng.random(m - 10)])
+    elif spectrum == "clustered":  # the bulk edge of the MEG operator: gaps ~1e-5 and below
+        ev = np.concatenate([top, -13.6 - 0.028 * rng.random(m - 20), -13.6 - 1e-7 * rng.random(10)])
+    else:  # exact multiplicities
+        ev = np.concatenate([top, np.repeat([-13.6, -13.7, -14.0], (m - 10) // 3 + 1)[: m - 10]])
+    q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    h = (q * ev) @ q.T
+    h = 0.5 * (h + h.T)
+    lib = runtime.solver_for(4096).lib
+    f = lib.megb200_debug_rr_solve
+    f.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]
+    dev = runtime.device()
+    H = torch.tensor(h, dtype=torch.float64, device=dev)
+    ref = np.sort(np.linalg.eigvalsh(h))[::-1]
+    hn = np.linalg.norm(h)
+    for nvec in (m, m // 3 + 2):
+        th = torch.empty(m, dtype=torch.float64, device=dev)
+        S = torch.empty((m, m), dtype=torch.float64, device=dev)
+        info = torch.empty(4, dtype=torch.float64, device=dev)
+        assert f(H.data_ptr(), m, m, th.data_ptr(), S.data_ptr(), info.data_ptr(), 0 if nvec == m else -nvec) == 0
+        torch.cuda.synchronize()
+        thv, sv = th.cpu().numpy(), S.cpu().numpy()[:, :nvec]
+        assert np.all(np.diff(thv) <= 0)
+        assert np.max(np.abs(thv[:nvec] - ref[:nvec])) <= 1e-12 * hn
+        assert abs(thv[-1] - ref[-1]) <= 1e-12 * hn  # the smallest (norm estimate) is always exact
+        assert np.max(np.abs(sv.T @ sv - np.eye(nvec))) <= 1e-13
+        assert np.max(np.abs(h @ sv - sv * thv[:nvec])) <= 1e-12 * hn
