@@ -338,35 +338,108 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
   }
   __syncthreads();
   rr_mark(3);
-  // ---- 4. S = Q Z: reflectors j = m-3 .. 0 applied to rows j+1.. of Z
+  // ---- 4. S = Q Z, the reflectors applied in blocks of kWY (compact WY: H_j0 ... H_j0+P-1 =
+  //      I - V T V^T, T upper triangular from tau and V^T V): per block one pass of dots
+  //      W1 = V^T Z (a warp per column, lanes over rows, shuffle trees), T and W2 = T W1, one
+  //      rank-P update -- four barriers per block instead of three per reflector
   {
-    const int nch = kRT / nvec >= 8 ? 8 : (kRT / nvec >= 4 ? 4 : 1);  // row chunks per column dot
-    for (int j = m - 3; j >= 0; --j) {
-      const double tj = tau[j];
-      if (tj == 0.0) continue;  // uniform (tau is never rewritten here)
-      const int L = m - j - 1;
-      // u_c = v^T Z[j+1.., c] in nch row chunks, partials in sc[8 + c * nch + ch]
-      if (t < nvec * nch) {
-        const int c = t / nch, ch = t - c * nch;
-        const int i0 = (L * ch) / nch, i1 = (L * (ch + 1)) / nch;
-        double s = 0.0;
-        for (int i = i0; i < i1; ++i) {
-          const double vi = i == 0 ? 1.0 : A[(j + 1 + i) * la + j];
-          s = fma(vi, Z[(j + 1 + i) * m + c], s);
+    constexpr int kWY = 8;
+    double* W1 = sc + 8;   // kWY x nvec (<= 8 x 112)
+    double* Gv = wp;       // kWY x kWY Gram of the block's reflectors
+    double* Tm = wp + 64;  // kWY x kWY
+    const int nr = m - 2;  // reflectors 0 .. m-3
+    for (int j1 = nr; j1 > 0; j1 -= kWY) {
+      const int j0 = j1 - kWY > 0 ? j1 - kWY : 0;
+      const int P = j1 - j0;
+      const int L0 = m - j0 - 1;  // rows j0+1 .. m-1; reflector j0+q is 1 at local row q, 0 above
+      // V[row][q] (local row, block column q)
+      auto vat = [&](int row, int q) -> double {
+        return row < q ? 0.0 : (row == q ? 1.0 : A[(j0 + 1 + row) * la + j0 + q]);
+      };
+      // W1[q][c] = sum_rows V[row][q] Z[j0+1+row][c]: warp per column c
+      for (int c = w; c < nvec; c += kNW) {
+        double acc[kWY];
+#pragma unroll
+        for (int q = 0; q < kWY; ++q) acc[q] = 0.0;
+        for (int row = lane; row < L0; row += 32) {
+          const double z = Z[(j0 + 1 + row) * m + c];
+#pragma unroll
+          for (int q = 0; q < kWY; ++q)
+            if (q < P) acc[q] = fma(vat(row, q), z, acc[q]);
         }
-        sc[8 + c * nch + ch] = s;
+#pragma unroll
+        for (int q = 0; q < kWY; ++q) {
+          const double v = wsum(acc[q]);
+          if (lane == 0 && q < P) W1[q * nvec + c] = v;
+        }
+      }
+      // Gv = V^T V: warp q' < P computes row q' (lanes over rows)
+      if (w < P) {
+        double acc[kWY];
+#pragma unroll
+        for (int q = 0; q < kWY; ++q) acc[q] = 0.0;
+        for (int row = lane; row < L0; row += 32) {
+          const double a = vat(row, w);
+#pragma unroll
+          for (int q = 0; q < kWY; ++q)
+            if (q < P) acc[q] = fma(a, vat(row, q), acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < kWY; ++q) {
+          const double v = wsum(acc[q]);
+          if (lane == 0 && q < P) Gv[w * kWY + q] = v;
+        }
       }
       __syncthreads();
+      // T (forward, columnwise): T_ii = tau_i, T[0:i, i] = -tau_i T[0:i, 0:i] Gv[0:i, i]; lane r owns row r
+      if (w == 0) {
+        double trow[kWY];
+#pragma unroll
+        for (int q = 0; q < kWY; ++q) trow[q] = 0.0;
+#pragma unroll
+        for (int i = 0; i < kWY; ++i) {
+          if (i < P) {
+            const double ti = tau[j0 + i];
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < kWY; ++q)
+              if (q < i) acc = fma(trow[q], Gv[q * kWY + i], acc);
+            if (lane == i) trow[i] = ti;
+            else if (lane < i) trow[i] = -ti * acc;
+          }
+        }
+        if (lane < P)
+#pragma unroll
+          for (int q = 0; q < kWY; ++q) Tm[lane * kWY + q] = trow[q];
+      }
+      __syncthreads();
+      // W2 = T W1 in place (rows ascending: row p reads rows q >= p only)
       for (int c = t; c < nvec; c += kRT) {
-        double u = 0.0;
-        for (int ch = 0; ch < nch; ++ch) u += sc[8 + c * nch + ch];
-        p[c] = tj * u;
+#pragma unroll
+        for (int pr = 0; pr < kWY; ++pr) {
+          if (pr < P) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < kWY; ++q)
+              if (q >= pr && q < P) acc = fma(Tm[pr * kWY + q], W1[q * nvec + c], acc);
+            W1[pr * nvec + c] = acc;
+          }
+        }
       }
       __syncthreads();
-      for (int rr = t >> 3; rr < L; rr += kRT >> 3) {
-        const double vi = rr == 0 ? 1.0 : A[(j + 1 + rr) * la + j];
-        double* zr = Z + (j + 1 + rr) * m;
-        for (int c = t & 7; c < nvec; c += 8) zr[c] -= vi * p[c];
+      // Z -= V W2 (eight threads per row)
+      for (int rr = t >> 3; rr < L0; rr += kRT >> 3) {
+        double vr[kWY];
+#pragma unroll
+        for (int q = 0; q < kWY; ++q) vr[q] = q < P ? vat(rr, q) : 0.0;
+        double* zr = Z + (j0 + 1 + rr) * m;
+        for (int c = t & 7; c < nvec; c += 8) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 0; q < kWY; ++q)
+            if (q < P) acc = fma(vr[q], W1[q * nvec + c], acc);
+          zr[c] -= acc;
+        }
       }
       __syncthreads();
     }
