@@ -49,7 +49,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline sampling")
     ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi clock sampling interval (ms)")
-    ap.add_argument("--prof-stride", type=int, default=8, help="bracket every N-th pass with events (0: off)")
+    ap.add_argument("--prof-stride", type=int, default=16, help="bracket every N-th pass with events (0: off)")
     return ap.parse_args()
 
 
@@ -263,7 +263,7 @@ def run_device_arm(args, world, rank, local):
     import ctypes as C
 
     K = args.steps
-    prof_stride = args.prof_stride  # roofline: every 8th pass kernel bracketed by events (small perturbation)
+    prof_stride = args.prof_stride  # roofline: every 16th pass kernel bracketed by events (small perturbation)
     lib.megb200_profile_enable(solver.handle, prof_stride)
     pm, pc, pb_bytes = C.c_double(), C.c_int64(), C.c_double()
     lib.megb200_profile_read(solver.handle, C.byref(pm), C.byref(pc), C.byref(pb_bytes))  # reset
@@ -351,7 +351,7 @@ def run_device_arm(args, world, rank, local):
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-        "kernel": "streamed operator pass k_dense_pass_mma (TMA + DMMA/DFMA), every 8th launch of the timed region "
+        "kernel": "streamed operator pass k_dense_pass_mma (TMA + DMMA/DFMA), every --prof-stride-th (16th) launch of the timed region "
                   "bracketed by CUDA events on the solver stream (includes its launch latency)",
         "bytes_per_pass": (pb_bytes.value / pc.value) if pc.value else None,
         "pass_ms": (pm.value / pc.value) if pc.value else None, "passes": int(pc.value), "peak_source": peak_src,
