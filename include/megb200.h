@@ -285,6 +285,24 @@ int megb200_dense_stats(megb200_solver* s, const void* M, int32_t dtype, int64_t
 int megb200_dual_gap(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts, double m_trace,
                      double* gap, double* lambda_min);
 
+/* Quadratic-measurement objective (the paper's experiment; SURVEY.md 8f row 1,
+ * reference objectives.py:111-228): f(tau X) = 1/2 sum_i (a_i^T (tau X) b_i - y_i)^2
+ * over m unit-vector pairs a, b (m x n row-major, device, ld n).
+ *   residuals: res_i = tau ((1-eps) sum_k (a_i.v_k) lam_k (v_k.b_i)
+ *              + eps/(n-r) (a_i.b_i - sum_k (a_i.v_k)(v_k.b_i))) - y_i   (replaces
+ *              _measure_structured / qm_residuals, objectives.py:111-130; 1 <= r <= 32)
+ *   gradient:  G = weight * sym(a^T diag(res) b), n x n, ld ldg (replaces
+ *              _dense_measurement_gradient, objectives.py:155-156; with weight = tau it is
+ *              RecoveryObjective.grad_operator's tau * grad f(tau X), :211-223)
+ *   value:     1/2 ||res||^2 (qm_value, objectives.py:133-136), host out.
+ * Device pointers; n must equal the solver's dimension. */
+int megb200_qm_residuals(megb200_solver* s, const double* a, const double* b, const double* y, int64_t m,
+                         const double* V, int64_t ldv, int32_t r, const double* lam_host, double eps, double tau,
+                         double* res);
+int megb200_qm_gradient(megb200_solver* s, const double* a, const double* b, const double* res, int64_t m,
+                        double weight, double* G, int64_t ldg);
+int megb200_qm_value(megb200_solver* s, const double* res, int64_t m, double* value);
+
 /* Seeded synthetic inputs (oracle/inputs.py twins):
  *   M_ij = sum_k U_ik lam_k U_jk + sigma (g_ij + g_ji) / (2 sqrt(n)),
  *   g_ij = N(0,1) at counter i*n + j of stream `stream` (float64 or float32 output). */

@@ -31,6 +31,7 @@ from .objectives import (
     DenseGradient,
     FrobeniusObjective,
     GradientOperator,
+    QuadMeasObjective,
     SampledObjective,
     StochasticFrobeniusObjective,
     ZeroGradient,
@@ -38,7 +39,7 @@ from .objectives import (
 
 __all__ = [
     "CertificateRecord", "DenseGradient", "HostStepResult", "EighError", "EpsilonSchedule", "FrobeniusObjective", "GradientOperator",
-    "LanczosError", "LogmapOperator", "LowRankIterate", "LowRankStepResult", "ParameterError", "RankDeficiencyError",
+    "LanczosError", "LogmapOperator", "QuadMeasObjective", "LowRankIterate", "LowRankStepResult", "ParameterError", "RankDeficiencyError",
     "SampledObjective", "StepConfig", "StochasticFrobeniusObjective", "SymmetricOperator", "TopREigen",
     "ZeroGradient", "certificate_cheap", "certificate_full", "eps_schedule_eval", "lanczos_top_r", "logmap_operator",
     "lowrank_meg_step", "lowrank_meg_step_host", "merge_certificates", "project_simplex", "step_eval", "symmetrize", "warm_start_wrap",

@@ -7,7 +7,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("megb200_kernels.cu", "megb200_coop.cu", "megb200_umma.cu", "megb200_step.cu", "megb200_rr.cu", "megb200_runtime.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("megb200_kernels.cu", "megb200_coop.cu", "megb200_umma.cu", "megb200_step.cu", "megb200_rr.cu", "megb200_qm.cu", "megb200_runtime.cu")]
 HEADERS = [os.path.join(HERE, "csrc", "megb200_internal.h"), os.path.join(HERE, "csrc", "megb200_umma.cuh"),
            os.path.join(HERE, "csrc", "megb200_jacobi.cuh"), os.path.join(os.path.dirname(HERE), "include", "megb200.h")]
 TARGET = os.path.join(HERE, "libmegb200.so")

@@ -206,4 +206,16 @@ struct FusedPassArgs {
 bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count);
 void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count);
 
+// quadratic-measurement objective (megb200_qm.cu)
+struct QmCoef {
+  double tau = 0.0, eps = 0.0, tail = 0.0;
+  double lam[32] = {};
+};
+void qm_residuals(const Launch& L, const double* a, const double* b, const double* y, int64_t m, int64_t n,
+                  const double* V, int64_t ldv, int r, const QmCoef& qc, double* res);
+int64_t qm_grad_part_doubles(int64_t m, int64_t n);
+void qm_gradient(const Launch& L, const double* a, const double* b, const double* res, int64_t m, int64_t n,
+                 double weight, double* G, int64_t ldg, double* part);
+void qm_sumsq(const Launch& L, const double* res, int64_t m, double* out);
+
 }  // namespace megb200

@@ -1,0 +1,177 @@
+// Quadratic-measurement objective (the paper's experiment; reference
+// objectives.py:111-228): f(tau X) = 1/2 sum_i (a_i^T (tau X) b_i - y_i)^2 over
+// m measurement pairs (a_i, b_i) of unit vectors in R^n.
+//
+//   k_qm_residuals   res_i = tau ((1 - eps) sum_k (a_i.v_k) lam_k (v_k.b_i)
+//                              + tail (a_i.b_i - sum_k (a_i.v_k)(v_k.b_i))) - y_i
+//                    (_measure_structured, objectives.py:111-118): a warp per
+//                    measurement row, coalesced reads of a_i and b_i, fixed
+//                    lane-strided sums + xor trees;
+//   k_qm_grad_part   C_c = a[chunk]^T diag(res[chunk]) b[chunk] per m-chunk and
+//                    32 x 32 output tile (split-K over the measurements);
+//   k_qm_grad_reduce G = weight * (C + C^T) / 2, chunks summed in order
+//                    (tau * _dense_measurement_gradient, objectives.py:155-156,
+//                    the reference's own path for n <= dense_cap = 1024);
+//   k_qm_sumsq       1/2 ||res||^2 (qm_value), one CTA, fixed order.
+//
+// The materialised gradient then drives the step through the dense operator
+// pass like any fixed dense gradient.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "megb200_internal.h"
+
+namespace megb200 {
+namespace {
+
+constexpr int kQmTile = 32;    // output tile of the gradient
+constexpr int kQmSub = 64;     // measurement rows staged per sub-block
+constexpr int kQmChunk = 512;  // measurement rows per split-K chunk
+
+template <int RB>
+__global__ void __launch_bounds__(256) k_qm_residuals(const double* __restrict__ a, const double* __restrict__ b,
+                                                      const double* __restrict__ y, int64_t m, int64_t n,
+                                                      const double* __restrict__ V, int64_t ldv, int r, QmCoef qc,
+                                                      double* __restrict__ res) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (i >= m) return;
+  const double* ai = a + i * n;
+  const double* bi = b + i * n;
+  double av[RB], bv[RB], ab = 0.0;
+#pragma unroll
+  for (int k = 0; k < RB; ++k) av[k] = bv[k] = 0.0;
+  for (int64_t j = lane; j < n; j += 32) {
+    const double x = ai[j], z = bi[j];
+    ab = fma(x, z, ab);
+    const double* vj = V + j * ldv;
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+      if (k < r) {
+        const double vk = __ldg(vj + k);
+        av[k] = fma(x, vk, av[k]);
+        bv[k] = fma(z, vk, bv[k]);
+      }
+    }
+  }
+  auto wsum = [](double v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+  };
+  ab = wsum(ab);
+  double kept = 0.0, cross = 0.0;
+#pragma unroll
+  for (int k = 0; k < RB; ++k) {
+    if (k < r) {
+      const double x = wsum(av[k]), z = wsum(bv[k]);
+      kept = fma(x * qc.lam[k], z, kept);
+      cross = fma(x, z, cross);
+    }
+  }
+  if (lane == 0) res[i] = qc.tau * ((1.0 - qc.eps) * kept + qc.tail * (ab - cross)) - y[i];
+}
+
+// C_c[p][q] = sum_{l in chunk c} a[l][i0 + p] res[l] b[l][j0 + q]
+__global__ void __launch_bounds__(256) k_qm_grad_part(const double* __restrict__ a, const double* __restrict__ b,
+                                                      const double* __restrict__ res, int64_t m, int64_t n,
+                                                      double* __restrict__ part) {
+  __shared__ double As[kQmSub][kQmTile + 1];
+  __shared__ double Bs[kQmSub][kQmTile + 1];
+  const int i0 = blockIdx.x * kQmTile, j0 = blockIdx.y * kQmTile;
+  const int64_t l0 = (int64_t)blockIdx.z * kQmChunk;
+  const int64_t l1 = min(m, l0 + kQmChunk);
+  const int t = threadIdx.x;
+  const int tp = t / 8, tq = (t % 8) * 4;  // outputs (tp, tq .. tq+3)
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t ls = l0; ls < l1; ls += kQmSub) {
+    const int rows = (int)min((int64_t)kQmSub, l1 - ls);
+    __syncthreads();
+    for (int idx = t; idx < kQmSub * kQmTile; idx += 256) {
+      const int rr = idx / kQmTile, c = idx % kQmTile;
+      const bool ok = rr < rows;
+      const int64_t l = ls + rr;
+      As[rr][c] = (ok && i0 + c < n) ? a[l * n + i0 + c] : 0.0;
+      Bs[rr][c] = (ok && j0 + c < n) ? res[l] * b[l * n + j0 + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < kQmSub; ++rr) {
+      const double x = As[rr][tp];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = fma(x, Bs[rr][tq + u], acc[u]);
+    }
+  }
+  double* out = part + (int64_t)blockIdx.z * n * n;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int p = i0 + tp, q = j0 + tq + u;
+    if (p < n && q < n) out[(int64_t)p * n + q] = acc[u];
+  }
+}
+
+__global__ void k_qm_grad_reduce(const double* __restrict__ part, int chunks, int64_t n, double weight,
+                                 double* __restrict__ G, int64_t ldg) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * n) return;
+  const int64_t p = idx / n, q = idx - p * n;
+  double s = 0.0, st = 0.0;
+  for (int c = 0; c < chunks; ++c) {
+    s += part[(int64_t)c * n * n + p * n + q];
+    st += part[(int64_t)c * n * n + q * n + p];
+  }
+  G[p * ldg + q] = weight * 0.5 * (s + st);
+}
+
+__global__ void __launch_bounds__(1024) k_qm_sumsq(const double* __restrict__ res, int64_t m, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += 1024) s = fma(res[i], res[i], s);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < 32; ++w) tot += red[w];
+    *out = 0.5 * tot;
+  }
+}
+
+}  // namespace
+
+void qm_residuals(const Launch& L, const double* a, const double* b, const double* y, int64_t m, int64_t n,
+                  const double* V, int64_t ldv, int r, const QmCoef& qc, double* res) {
+  if (r < 1 || r > 32) throw Error(MEGB200_ERR_PARAM, "quadratic-measurement residuals support 1 <= r <= 32");
+  const unsigned grid = (unsigned)((m + 7) / 8);
+  if (r <= 8)
+    k_qm_residuals<8><<<grid, 256, 0, L.stream>>>(a, b, y, m, n, V, ldv, r, qc, res);
+  else if (r <= 16)
+    k_qm_residuals<16><<<grid, 256, 0, L.stream>>>(a, b, y, m, n, V, ldv, r, qc, res);
+  else
+    k_qm_residuals<32><<<grid, 256, 0, L.stream>>>(a, b, y, m, n, V, ldv, r, qc, res);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+int64_t qm_grad_part_doubles(int64_t m, int64_t n) { return ((m + kQmChunk - 1) / kQmChunk) * n * n; }
+
+void qm_gradient(const Launch& L, const double* a, const double* b, const double* res, int64_t m, int64_t n,
+                 double weight, double* G, int64_t ldg, double* part) {
+  const int chunks = (int)((m + kQmChunk - 1) / kQmChunk);
+  const dim3 grid((unsigned)((n + kQmTile - 1) / kQmTile), (unsigned)((n + kQmTile - 1) / kQmTile), (unsigned)chunks);
+  k_qm_grad_part<<<grid, 256, 0, L.stream>>>(a, b, res, m, n, part);
+  MEG_LAUNCHED();
+  k_qm_grad_reduce<<<(unsigned)((n * n + 255) / 256), 256, 0, L.stream>>>(part, chunks, n, weight, G, ldg);
+  MEG_LAUNCHED();
+  *L.counter += 2;
+}
+
+void qm_sumsq(const Launch& L, const double* res, int64_t m, double* out) {
+  k_qm_sumsq<<<1, 1024, 0, L.stream>>>(res, m, out);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+}  // namespace megb200

@@ -76,6 +76,8 @@ struct megb200_solver {
   int want_vgram = 0;      // host-buffer step: fused phase 0 also reduces the factor Gram (r x r)
   bool vgram_done = false;
   int64_t pack_vgram = 0;  // its offset in the result pack
+  double* qm_part = nullptr;  // quadratic-measurement gradient split-K partials (grown on demand)
+  int64_t qm_part_len = 0;
   int rr_nvec = 0;  // Ritz pairs a wide Rayleigh-Ritz must return (0: all); set by top_eigs
   double m_norm2_cache = NAN, m_trace_cache = NAN;
   const void* m_cache_ptr = nullptr;
@@ -1065,6 +1067,7 @@ void megb200_solver_destroy(megb200_solver* s) {
   cudaFreeHost(s->h_buf);
   cudaFreeHost(s->h_up);
   if (s->fsync) cudaFree(s->fsync);
+  if (s->qm_part) cudaFree(s->qm_part);
   delete s;
 }
 
@@ -1802,6 +1805,52 @@ int megb200_dual_gap(megb200_solver* s, const megb200_gradient* g, const megb200
     }
     if (gap) *gap = (x2 - inner) - lmin;
     if (lambda_min) *lambda_min = lmin;
+  });
+}
+
+int megb200_qm_residuals(megb200_solver* s, const double* a, const double* b, const double* y, int64_t m,
+                         const double* V, int64_t ldv, int32_t r, const double* lam_host, double eps, double tau,
+                         double* res) {
+  return guarded_impl([&] {
+    if (!s || !a || !b || !y || !V || !lam_host || !res) throw Error(MEGB200_ERR_PARAM, "null argument");
+    const int64_t n = s->n;
+    if (m < 1) throw Error(MEGB200_ERR_PARAM, "need m >= 1");
+    if (!(1 <= r && r < n) || r > 32 || ldv < r) throw Error(MEGB200_ERR_PARAM, "need 1 <= r < n, r <= 32");
+    if (!(eps > 0.0 && eps <= 0.75)) throw Error(MEGB200_ERR_PARAM, "eps must lie in (0, 3/4]");
+    QmCoef qc;
+    qc.tau = tau;
+    qc.eps = eps;
+    qc.tail = eps / (double)(n - r);
+    for (int k = 0; k < r; ++k) qc.lam[k] = lam_host[k];
+    qm_residuals(s->launch(), a, b, y, m, n, V, ldv, r, qc, res);
+  });
+}
+
+int megb200_qm_gradient(megb200_solver* s, const double* a, const double* b, const double* res, int64_t m,
+                        double weight, double* G, int64_t ldg) {
+  return guarded_impl([&] {
+    if (!s || !a || !b || !res || !G) throw Error(MEGB200_ERR_PARAM, "null argument");
+    const int64_t n = s->n;
+    if (m < 1 || ldg < n) throw Error(MEGB200_ERR_PARAM, "need m >= 1 and ldg >= n");
+    const int64_t need = qm_grad_part_doubles(m, n);
+    if (need > s->qm_part_len) {
+      s->sync();
+      if (s->qm_part) MEG_CUDA(cudaFree(s->qm_part));
+      s->qm_part = nullptr;
+      MEG_CUDA(cudaMalloc(&s->qm_part, (size_t)need * sizeof(double)));
+      s->qm_part_len = need;
+    }
+    qm_gradient(s->launch(), a, b, res, m, n, weight, G, ldg, s->qm_part);
+  });
+}
+
+int megb200_qm_value(megb200_solver* s, const double* res, int64_t m, double* value) {
+  return guarded_impl([&] {
+    if (!s || !res || !value || m < 1) throw Error(MEGB200_ERR_PARAM, "bad arguments");
+    qm_sumsq(s->launch(), res, m, s->small);
+    s->d2h(s->h_buf, s->small, 1);
+    s->sync();
+    *value = s->h_buf[0];
   });
 }
 

@@ -246,3 +246,74 @@ class StochasticFrobeniusObjective(FrobeniusObjective):
     def grad_operator(self, x, t: int = 0) -> GradientOperator:
         return GradientOperator(_lib.GRAD_STOCHASTIC, self.n, dense=self.m, x=x, A=self.minibatch(t),
                                 sigma=self.sigma, owner=self)
+
+
+class QuadMeasObjective:
+    """The paper's recovery experiment (reference RecoveryObjective,
+    objectives.py:174-228): g(X) = f(tau X) on the unit-trace cone,
+    f(Z) = 1/2 sum_i (a_i^T Z b_i - y_i)^2 over m measurement pairs (a_i, b_i).
+
+    a, b (m x n, unit rows) and y are uploaded once.  `grad_operator(x)` evaluates the
+    residuals of x from its factors on the device (k_qm_residuals, the structured
+    measurement of objectives.py:111-118) and materialises tau * grad f(tau X) =
+    tau * sym(a^T diag(res) b) (k_qm_grad_part / k_qm_grad_reduce; the reference's own dense
+    path, objectives.py:211-216), which the step consumes as its dense gradient."""
+
+    def __init__(self, a, b, y, tau: float):
+        self.a = runtime.as_device_f64(a).contiguous()
+        self.b = runtime.as_device_f64(b).contiguous()
+        self.y = runtime.as_device_f64(np.asarray(y, dtype=np.float64).ravel() if not isinstance(y, torch.Tensor)
+                                       else y).reshape(-1).contiguous()
+        if self.a.dim() != 2 or self.a.shape != self.b.shape or self.y.numel() != self.a.shape[0]:
+            raise ParameterError("a, b must be m x n and y of length m")
+        self.m, self.n = int(self.a.shape[0]), int(self.a.shape[1])
+        self.dim = self.n
+        self.tau = float(tau)
+
+    @classmethod
+    def from_instance(cls, inst) -> "QuadMeasObjective":
+        """From a reference-style instance (fields a, b, y, tau; e.g. specmeg.objectives.generate_instance)."""
+        return cls(inst.a, inst.b, inst.y, inst.tau)
+
+    @staticmethod
+    def preset_beta(n: int, r: int) -> float:
+        """Smoothness preset 0.4 sqrt(r n) (objectives.py:194-197); the experiment's eta = 1/beta."""
+        return 0.4 * math.sqrt(r * n)
+
+    def _solver(self):
+        return runtime.solver_for(self.n)
+
+    def residuals(self, x) -> torch.Tensor:
+        """a_i^T (tau X) b_i - y_i for a factored iterate (device tensor of length m)."""
+        if x.n != self.n:
+            raise ParameterError("iterate dimension does not match the objective")
+        s = self._solver()
+        V = x.V_device
+        lam = runtime.host_f64(x.lam)
+        res = torch.empty(self.m, dtype=torch.float64, device=runtime.device())
+        runtime.check(s.lib.megb200_qm_residuals(s.handle, self.a.data_ptr(), self.b.data_ptr(), self.y.data_ptr(),
+                                                 self.m, V.data_ptr(), V.stride(0), x.r, _lib.dptr(lam),
+                                                 float(x.eps), self.tau, res.data_ptr()))
+        return res
+
+    def value(self, x) -> float:
+        """f(tau X) = 1/2 ||res||^2 (qm_value, objectives.py:133-136)."""
+        res = self.residuals(x)
+        s = self._solver()
+        out = C.c_double()
+        runtime.check(s.lib.megb200_qm_value(s.handle, res.data_ptr(), self.m, C.byref(out)))
+        return float(out.value)
+
+    def gradient_matrix(self, res: torch.Tensor, weight: float | None = None) -> torch.Tensor:
+        """weight * sym(a^T diag(res) b) (n x n device tensor; weight defaults to tau)."""
+        s = self._solver()
+        G = torch.empty((self.n, self.n), dtype=torch.float64, device=runtime.device())
+        w = self.tau if weight is None else float(weight)
+        runtime.check(s.lib.megb200_qm_gradient(s.handle, self.a.data_ptr(), self.b.data_ptr(), res.data_ptr(),
+                                                self.m, w, G.data_ptr(), G.stride(0)))
+        return G
+
+    def grad_operator(self, x, t: int = 0) -> GradientOperator:
+        """tau * grad f(tau X) at x, materialised on the device (RecoveryObjective.grad_operator)."""
+        G = self.gradient_matrix(self.residuals(x))
+        return GradientOperator(_lib.GRAD_DENSE, self.n, dense=G, owner=self)

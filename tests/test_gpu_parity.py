@@ -409,3 +409,39 @@ def test_wide_rayleigh_ritz(pb, m, spectrum):
         assert abs(thv[-1] - ref[-1]) <= 1e-12 * hn  # the smallest (norm estimate) is always exact
         assert np.max(np.abs(sv.T @ sv - np.eye(nvec))) <= 1e-13
         assert np.max(np.abs(h @ sv - sv * thv[:nvec])) <= 1e-12 * hn
+
+
+@pytest.mark.parametrize("name", ["qm_n100_r1", "qm_n60_r3", "qm_n100_r5"])
+def test_quad_meas_matches_reference_golden(pb, name):
+    """The paper's quadratic-measurement objective on the device:
+    residuals (k_qm_residuals) and tau * grad f(tau X) (k_qm_grad_part / reduce) against the
+    oracle restatement (1e-12), then a MEG trajectory through lowrank_meg_step against the
+    unmodified reference's golden run (1e-9, tests/golden/make_golden_qm.py)."""
+    from oracle import qm as oq
+    from tests.test_oracle_pins import _qm_eps, qm_projector_err
+
+    g = load_golden(name)
+    n, r, seed = int(g["n"]), int(g["r"]), int(g["seed"])
+    inst = oq.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=seed)
+    dev = pb.QuadMeasObjective.from_instance(inst)
+    x = pb.LowRankIterate(n, r, g["V0"], g["lam0"], float(g["eps0"]))
+    ox = om.LowRankIterate(n=n, r=r, V=g["V0"], lam=g["lam0"], eps=float(g["eps0"]))
+    res_o = oq.residuals(inst, ox)
+    res_d = dev.residuals(x).cpu().numpy()
+    assert normwise(res_d, res_o) <= 1e-12
+    G_o = oq.dense_gradient(inst, res_o, inst.tau)
+    G_d = dev.gradient_matrix(dev.residuals(x)).cpu().numpy()
+    assert normwise(G_d, G_o) <= 1e-12
+    assert abs(dev.value(x) - oq.value(inst, ox)) <= 1e-12 * abs(oq.value(inst, ox))
+    eta = float(g["eta"])
+    got = {k: [] for k in ("shift", "y", "lam", "lhs", "f")}
+    for t in range(len(g["shift"])):
+        res = pb.lowrank_meg_step(x, dev.grad_operator(x), eta, _qm_eps(t + 1), svd_seed=t)
+        x = res.iterate
+        got["shift"].append(res.shift)
+        got["y"].append(res.top_eigenvalues)
+        got["lam"].append(x.lam)
+        got["lhs"].append(res.cert.lhs_cheap)
+        got["f"].append(dev.value(x))
+        assert qm_projector_err(x.V, x.lam, x.eps, g["V"][t], g["lam"][t], float(g["eps"][t])) <= 1e-9
+    compare_trajectory({k: np.array(v) for k, v in got.items()}, g, TOL["f64"])

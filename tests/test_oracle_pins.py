@@ -192,3 +192,53 @@ def test_generator_is_counter_based():
     cfg = inputs.CONFIGS["cfg2"].scaled(64)
     m = inputs.dense_target(cfg)
     assert np.array_equal(m, m.T)
+
+
+# ---------------------------------------------------------------------------
+# quadratic-measurement objective: oracle/qm.py pinned to the
+# reference's instance generator and trajectories (tests/golden/make_golden_qm.py)
+
+QM_CASES = ["qm_n100_r1", "qm_n60_r3", "qm_n100_r5"]
+
+
+def _qm_checksums(a):
+    a = np.asarray(a)
+    return np.array([a.sum(), (a * a).sum(), a.ravel()[0], a.ravel()[-1], a.ravel()[a.size // 3]])
+
+
+def _qm_eps(t):
+    return min(0.6 / (t + 11.0) ** 2, 0.75)  # EpsilonSchedule.experiment(10) (meg.py:182-190)
+
+
+def qm_projector_err(V, lam, eps, Vg, lamg, epsg):
+    """normwise difference of the two iterates' dense forms (sign/rotation invariant)."""
+    n, r = V.shape
+    X = (1 - eps) * (V * lam) @ V.T + eps / (n - r) * (np.eye(n) - V @ V.T)
+    Xg = (1 - epsg) * (Vg * lamg) @ Vg.T + epsg / (n - r) * (np.eye(n) - Vg @ Vg.T)
+    return float(np.max(np.abs(X - Xg)) / np.max(np.abs(Xg)))
+
+
+@pytest.mark.parametrize("name", QM_CASES)
+def test_qm_oracle_matches_reference_golden(name):
+    from oracle import qm as oq
+
+    g = load_golden(name)
+    n, r, seed = int(g["n"]), int(g["r"]), int(g["seed"])
+    inst = oq.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=seed)
+    for key, arr in (("a_sum", inst.a), ("b_sum", inst.b), ("y_sum", inst.y)):
+        np.testing.assert_allclose(_qm_checksums(arr), g[key], rtol=1e-13, atol=0)
+    assert inst.tau == float(g["tau"]) and inst.m == int(g["m"])
+    x = om.LowRankIterate(n=n, r=r, V=g["V0"], lam=g["lam0"], eps=float(g["eps0"]))
+    eta = float(g["eta"])
+    got = {k: [] for k in ("shift", "y", "lam", "lhs", "f")}
+    for t in range(len(g["shift"])):
+        G = oq.dense_gradient(inst, oq.residuals(inst, x), inst.tau)
+        res = om.lowrank_meg_step(x, lambda u, G=G: G @ u, eta, _qm_eps(t + 1), svd_seed=t)
+        x = res.iterate
+        got["shift"].append(res.shift)
+        got["y"].append(res.top_eigenvalues)
+        got["lam"].append(x.lam)
+        got["lhs"].append(res.cert.lhs_cheap)
+        got["f"].append(oq.value(inst, x))
+        assert qm_projector_err(x.V, x.lam, x.eps, g["V"][t], g["lam"][t], float(g["eps"][t])) <= 1e-10
+    compare_trajectory({k: np.array(v) for k, v in got.items()}, g, 1e-10)
