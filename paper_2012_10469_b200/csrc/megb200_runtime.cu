@@ -387,6 +387,10 @@ EigShape eig_shape(const megb200_solver* s, int nreq, const EigParams& P) {
     mmax = (int)n;
     exhaust = true;
   }
+  // small problems (n <= the Rayleigh-Ritz limit): let the basis grow to span R^n instead of
+  // restarting -- a full basis converges by the basis.shape[1] >= n rule (linalg.py:215) with one
+  // wide Rayleigh-Ritz, where restarted cycles near the bulk edge take tens of passes
+  if (!exhaust && n <= s->max_basis && P.basis <= 0) mmax = (int)n;
   mmax = (int)std::min<int64_t>(mmax, n);
   // even block widths and column offsets keep every block 16-byte aligned for the TMA pass
   if (!exhaust && (bw & 1) && bw < s->max_block && bw + 1 + nreq <= mmax) bw += 1;

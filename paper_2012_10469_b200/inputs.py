@@ -53,3 +53,27 @@ def initial_iterate(w: Workload, op_dense: torch.Tensor, tol: float = 1e-10):
     lam = np.maximum(lam, 1e-12)
     lam = lam / lam.sum()
     return warm_start_wrap(top.eigenvectors, lam, w.eps(0))
+
+
+def quad_meas_instance(n: int, r_true: int, kappa: float = 0.5, tau_fraction: float = 0.5, seed: int = 0,
+                       m: int | None = None):
+    """The paper's recovery instance (reference generate_instance, objectives.py:67-105; same
+    numpy draws in the same order): unit-Frobenius Gaussian factor v, m = 20 n r spherical
+    pairs (a_i, b_i), y0_i = n (a_i.v)(v.b_i), noise of relative size kappa, tau = tau_fraction n.
+    Returns (a, b, y, tau) as host arrays (setup only)."""
+    rng = np.random.default_rng(seed)
+    m = 20 * n * r_true if m is None else m
+    v = rng.standard_normal((n, r_true))
+    v /= np.linalg.norm(v)
+    a = rng.standard_normal((m, n))
+    a /= np.linalg.norm(a, axis=1, keepdims=True)
+    b = rng.standard_normal((m, n))
+    b /= np.linalg.norm(b, axis=1, keepdims=True)
+    y0 = n * np.einsum("ij,ij->i", a @ v, b @ v)
+    if kappa == 0.0:
+        y = y0.copy()
+    else:
+        d = rng.standard_normal(m)
+        d /= np.linalg.norm(d)
+        y = y0 + kappa * np.linalg.norm(y0) * d
+    return a, b, y, tau_fraction * n
