@@ -302,6 +302,11 @@ int megb200_qm_residuals(megb200_solver* s, const double* a, const double* b, co
 int megb200_qm_gradient(megb200_solver* s, const double* a, const double* b, const double* res, int64_t m,
                         double weight, double* G, int64_t ldg);
 int megb200_qm_value(megb200_solver* s, const double* res, int64_t m, double* value);
+/* Mini-batch estimate (StochasticOracle.grad_operator, objectives.py:235-273): G = weight *
+ * sym(a[idx]^T diag(res[idx]) b[idx]) over the L measurement indices idx (device int64, repeats
+ * allowed; the caller folds tau * m / L into weight). */
+int megb200_qm_gradient_batch(megb200_solver* s, const double* a, const double* b, const double* res,
+                              const int64_t* idx, int64_t L, double weight, double* G, int64_t ldg);
 
 /* Seeded synthetic inputs (oracle/inputs.py twins):
  *   M_ij = sum_k U_ik lam_k U_jk + sigma (g_ij + g_ji) / (2 sqrt(n)),

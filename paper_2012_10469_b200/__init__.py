@@ -32,6 +32,7 @@ from .objectives import (
     FrobeniusObjective,
     GradientOperator,
     QuadMeasObjective,
+    QuadMeasStochasticOracle,
     SampledObjective,
     StochasticFrobeniusObjective,
     ZeroGradient,
@@ -39,7 +40,7 @@ from .objectives import (
 
 __all__ = [
     "CertificateRecord", "DenseGradient", "HostStepResult", "EighError", "EpsilonSchedule", "FrobeniusObjective", "GradientOperator",
-    "LanczosError", "LogmapOperator", "QuadMeasObjective", "LowRankIterate", "LowRankStepResult", "ParameterError", "RankDeficiencyError",
+    "LanczosError", "LogmapOperator", "QuadMeasObjective", "QuadMeasStochasticOracle", "LowRankIterate", "LowRankStepResult", "ParameterError", "RankDeficiencyError",
     "SampledObjective", "StepConfig", "StochasticFrobeniusObjective", "SymmetricOperator", "TopREigen",
     "ZeroGradient", "certificate_cheap", "certificate_full", "eps_schedule_eval", "lanczos_top_r", "logmap_operator",
     "lowrank_meg_step", "lowrank_meg_step_host", "merge_certificates", "project_simplex", "step_eval", "symmetrize", "warm_start_wrap",

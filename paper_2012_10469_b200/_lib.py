@@ -136,6 +136,8 @@ SIGNATURES = [
     ("megb200_qm_gradient", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_int64]),
     ("megb200_qm_value", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, c_double_p]),
+    ("megb200_qm_gradient_batch", C.c_int,
+     [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_int64]),
     ("megb200_gen_dense_target", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_int64, c_double_p, C.c_double, C.c_uint64, C.c_int32, C.c_void_p, C.c_int32,
       C.c_int64]),

@@ -215,7 +215,7 @@ void qm_residuals(const Launch& L, const double* a, const double* b, const doubl
                   const double* V, int64_t ldv, int r, const QmCoef& qc, double* res);
 int64_t qm_grad_part_doubles(int64_t m, int64_t n);
 void qm_gradient(const Launch& L, const double* a, const double* b, const double* res, int64_t m, int64_t n,
-                 double weight, double* G, int64_t ldg, double* part);
+                 double weight, double* G, int64_t ldg, double* part, const int64_t* idx = nullptr);
 void qm_sumsq(const Launch& L, const double* res, int64_t m, double* out);
 
 }  // namespace megb200

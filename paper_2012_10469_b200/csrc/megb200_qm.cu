@@ -8,7 +8,8 @@
 //                    measurement row, coalesced reads of a_i and b_i, fixed
 //                    lane-strided sums + xor trees;
 //   k_qm_grad_part   C_c = a[chunk]^T diag(res[chunk]) b[chunk] per m-chunk and
-//                    32 x 32 output tile (split-K over the measurements);
+//                    32 x 32 output tile (split-K over the measurements, or over a
+//                    mini-batch of measurement indices: StochasticOracle, :235-283);
 //   k_qm_grad_reduce G = weight * (C + C^T) / 2, chunks summed in order
 //                    (tau * _dense_measurement_gradient, objectives.py:155-156,
 //                    the reference's own path for n <= dense_cap = 1024);
@@ -74,9 +75,10 @@ __global__ void __launch_bounds__(256) k_qm_residuals(const double* __restrict__
 }
 
 // C_c[p][q] = sum_{l in chunk c} a[l][i0 + p] res[l] b[l][j0 + q]
+// rows are the measurements idx[0 .. m) when idx is given (a mini-batch, with repeats), else 0 .. m
 __global__ void __launch_bounds__(256) k_qm_grad_part(const double* __restrict__ a, const double* __restrict__ b,
                                                       const double* __restrict__ res, int64_t m, int64_t n,
-                                                      double* __restrict__ part) {
+                                                      const int64_t* __restrict__ idx, double* __restrict__ part) {
   __shared__ double As[kQmSub][kQmTile + 1];
   __shared__ double Bs[kQmSub][kQmTile + 1];
   const int i0 = blockIdx.x * kQmTile, j0 = blockIdx.y * kQmTile;
@@ -88,10 +90,10 @@ __global__ void __launch_bounds__(256) k_qm_grad_part(const double* __restrict__
   for (int64_t ls = l0; ls < l1; ls += kQmSub) {
     const int rows = (int)min((int64_t)kQmSub, l1 - ls);
     __syncthreads();
-    for (int idx = t; idx < kQmSub * kQmTile; idx += 256) {
-      const int rr = idx / kQmTile, c = idx % kQmTile;
+    for (int e = t; e < kQmSub * kQmTile; e += 256) {
+      const int rr = e / kQmTile, c = e % kQmTile;
       const bool ok = rr < rows;
-      const int64_t l = ls + rr;
+      const int64_t l = ok ? (idx ? idx[ls + rr] : ls + rr) : 0;
       As[rr][c] = (ok && i0 + c < n) ? a[l * n + i0 + c] : 0.0;
       Bs[rr][c] = (ok && j0 + c < n) ? res[l] * b[l * n + j0 + c] : 0.0;
     }
@@ -158,10 +160,10 @@ void qm_residuals(const Launch& L, const double* a, const double* b, const doubl
 int64_t qm_grad_part_doubles(int64_t m, int64_t n) { return ((m + kQmChunk - 1) / kQmChunk) * n * n; }
 
 void qm_gradient(const Launch& L, const double* a, const double* b, const double* res, int64_t m, int64_t n,
-                 double weight, double* G, int64_t ldg, double* part) {
+                 double weight, double* G, int64_t ldg, double* part, const int64_t* idx) {
   const int chunks = (int)((m + kQmChunk - 1) / kQmChunk);
   const dim3 grid((unsigned)((n + kQmTile - 1) / kQmTile), (unsigned)((n + kQmTile - 1) / kQmTile), (unsigned)chunks);
-  k_qm_grad_part<<<grid, 256, 0, L.stream>>>(a, b, res, m, n, part);
+  k_qm_grad_part<<<grid, 256, 0, L.stream>>>(a, b, res, m, n, idx, part);
   MEG_LAUNCHED();
   k_qm_grad_reduce<<<(unsigned)((n * n + 255) / 256), 256, 0, L.stream>>>(part, chunks, n, weight, G, ldg);
   MEG_LAUNCHED();

@@ -1848,6 +1848,24 @@ int megb200_qm_gradient(megb200_solver* s, const double* a, const double* b, con
   });
 }
 
+int megb200_qm_gradient_batch(megb200_solver* s, const double* a, const double* b, const double* res,
+                              const int64_t* idx, int64_t L, double weight, double* G, int64_t ldg) {
+  return guarded_impl([&] {
+    if (!s || !a || !b || !res || !idx || !G) throw Error(MEGB200_ERR_PARAM, "null argument");
+    const int64_t n = s->n;
+    if (L < 1 || ldg < n) throw Error(MEGB200_ERR_PARAM, "need L >= 1 and ldg >= n");
+    const int64_t need = qm_grad_part_doubles(L, n);
+    if (need > s->qm_part_len) {
+      s->sync();
+      if (s->qm_part) MEG_CUDA(cudaFree(s->qm_part));
+      s->qm_part = nullptr;
+      MEG_CUDA(cudaMalloc(&s->qm_part, (size_t)need * sizeof(double)));
+      s->qm_part_len = need;
+    }
+    qm_gradient(s->launch(), a, b, res, L, n, weight, G, ldg, s->qm_part, idx);
+  });
+}
+
 int megb200_qm_value(megb200_solver* s, const double* res, int64_t m, double* value) {
   return guarded_impl([&] {
     if (!s || !res || !value || m < 1) throw Error(MEGB200_ERR_PARAM, "bad arguments");

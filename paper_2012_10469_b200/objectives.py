@@ -317,3 +317,36 @@ class QuadMeasObjective:
         """tau * grad f(tau X) at x, materialised on the device (RecoveryObjective.grad_operator)."""
         G = self.gradient_matrix(self.residuals(x))
         return GradientOperator(_lib.GRAD_DENSE, self.n, dense=G, owner=self)
+
+
+class QuadMeasStochasticOracle:
+    """Mini-batch gradient estimator over the measurements (reference StochasticOracle,
+    objectives.py:235-273): batches of L indices drawn uniformly with replacement by the host
+    generator numpy default_rng(seed) (the reference's draws, in the same order), uploaded, and
+    reduced on the device as tau (m / L) sym(a[B]^T diag(res[B]) b[B]); L == m uses every index
+    once (the deterministic gradient)."""
+
+    def __init__(self, objective: QuadMeasObjective, L: int, seed: int = 0):
+        if L < 1:
+            raise ParameterError(f"mini-batch size must be >= 1, got {L}")
+        self.objective = objective
+        self.L = int(L)
+        self.rng = np.random.default_rng(seed)
+
+    def sample_batch(self) -> np.ndarray:
+        if self.L == self.objective.m:
+            return np.arange(self.objective.m)
+        return self.rng.integers(0, self.objective.m, size=self.L)
+
+    def grad_operator(self, x, batch) -> GradientOperator:
+        obj = self.objective
+        res = obj.residuals(x)
+        idx = torch.as_tensor(np.ascontiguousarray(np.asarray(batch, dtype=np.int64))).to(runtime.device())
+        if idx.numel() < 1:
+            raise ParameterError("batch must contain at least one index")
+        s = obj._solver()
+        G = torch.empty((obj.n, obj.n), dtype=torch.float64, device=runtime.device())
+        w = obj.tau * obj.m / idx.numel()
+        runtime.check(s.lib.megb200_qm_gradient_batch(s.handle, obj.a.data_ptr(), obj.b.data_ptr(), res.data_ptr(),
+                                                      idx.data_ptr(), idx.numel(), w, G.data_ptr(), G.stride(0)))
+        return GradientOperator(_lib.GRAD_DENSE, obj.n, dense=G, owner=(obj, idx))

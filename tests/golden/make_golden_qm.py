@@ -29,6 +29,8 @@ from specmeg import objectives as ref_obj  # noqa: E402
 from oracle import qm as oq  # noqa: E402  (start iterate only)
 
 CASES = {"qm_n100_r1": (100, 1, 0), "qm_n60_r3": (60, 3, 1), "qm_n100_r5": (100, 5, 2)}
+# mini-batch runs (StochasticOracle, objectives.py:235-273): name -> (n, r, seed, L, oracle seed)
+STOCH = {"qms_n100_r5_L1000": (100, 5, 3, 1000, 7), "qms_n60_r3_L3600": (60, 3, 4, 3600, 8)}
 T = 15
 
 
@@ -63,6 +65,32 @@ def main():
             a_sum=checksums(inst.a), b_sum=checksums(inst.b), y_sum=checksums(inst.y),
             V0=x0o.V, lam0=x0o.lam, eps0=x0o.eps, **{k: np.array(v) for k, v in rec.items()})
         print(name, "m =", inst.m, "f:", rec["f"][0], "->", rec["f"][-1])
+    for name, (n, r, seed, L, oseed) in STOCH.items():
+        inst = ref_obj.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=seed)
+        beta = ref_obj.RecoveryObjective.preset_beta(n, r)
+        obj = ref_obj.RecoveryObjective(inst, smoothness_hint=beta)
+        oracle = ref_obj.StochasticOracle(obj, L, seed=oseed)
+        eta = 1.0 / beta
+        x0o = oq.start_iterate(n, r, seed, sched.eval(0))
+        x = ref_meg.LowRankIterate(n=n, r=r, V=x0o.V, lam=x0o.lam, eps=x0o.eps)
+        rec = {k: [] for k in ("shift", "y", "lam", "eps", "lhs", "f", "V")}
+        for t in range(T):
+            batch = oracle.sample_batch()
+            op = oracle.grad_operator(x, batch)
+            res = ref_meg.lowrank_meg_step(x, op.apply, eta, sched.eval(t + 1), svd_seed=t)
+            x = res.iterate
+            rec["shift"].append(res.shift)
+            rec["y"].append(res.top_eigenvalues)
+            rec["lam"].append(x.lam)
+            rec["eps"].append(x.eps)
+            rec["lhs"].append(res.cert.lhs_cheap)
+            rec["f"].append(obj.value(x))
+            rec["V"].append(x.V)
+        np.savez_compressed(
+            os.path.join(out_dir, name + ".npz"), n=n, r=r, seed=seed, L=L, oracle_seed=oseed, eta=eta,
+            tau=inst.tau, m=inst.m, V0=x0o.V, lam0=x0o.lam, eps0=x0o.eps,
+            **{k: np.array(v) for k, v in rec.items()})
+        print(name, "m =", inst.m, "L =", L, "f:", rec["f"][0], "->", rec["f"][-1])
 
 
 if __name__ == "__main__":

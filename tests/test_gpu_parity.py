@@ -445,3 +445,34 @@ def test_quad_meas_matches_reference_golden(pb, name):
         got["f"].append(dev.value(x))
         assert qm_projector_err(x.V, x.lam, x.eps, g["V"][t], g["lam"][t], float(g["eps"][t])) <= 1e-9
     compare_trajectory({k: np.array(v) for k, v in got.items()}, g, TOL["f64"])
+
+
+@pytest.mark.parametrize("name", ["qms_n100_r5_L1000", "qms_n60_r3_L3600"])
+def test_quad_meas_stochastic_matches_reference_golden(pb, name):
+    """Mini-batch quadratic-measurement MEG (QuadMeasStochasticOracle: host draws of the
+    reference's generator, device batch gradient k_qm_grad_part over gathered rows) against the
+    unmodified reference's StochasticOracle run (1e-9); the batch estimate itself against the
+    oracle to 1e-12."""
+    from oracle import qm as oq
+    from tests.test_oracle_pins import _qm_eps, qm_projector_err
+
+    g = load_golden(name)
+    n, r, seed, L = int(g["n"]), int(g["r"]), int(g["seed"]), int(g["L"])
+    inst = oq.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=seed)
+    dev = pb.QuadMeasObjective.from_instance(inst)
+    sto = pb.QuadMeasStochasticOracle(dev, L, seed=int(g["oracle_seed"]))
+    osto = oq.StochasticOracle(inst, L, seed=12345)
+    x = pb.LowRankIterate(n, r, g["V0"], g["lam0"], float(g["eps0"]))
+    ox = om.LowRankIterate(n=n, r=r, V=g["V0"], lam=g["lam0"], eps=float(g["eps0"]))
+    probe = np.random.default_rng(5).integers(0, inst.m, size=L)
+    assert normwise(sto.grad_operator(x, probe).dense.cpu().numpy(), osto.gradient(ox, probe)) <= 1e-12
+    got = {k: [] for k in ("shift", "y", "lam", "lhs", "f")}
+    for t in range(len(g["shift"])):
+        res = pb.lowrank_meg_step(x, sto.grad_operator(x, sto.sample_batch()), float(g["eta"]), _qm_eps(t + 1),
+                                  svd_seed=t)
+        x = res.iterate
+        for k, v in (("shift", res.shift), ("y", res.top_eigenvalues), ("lam", x.lam), ("lhs", res.cert.lhs_cheap),
+                     ("f", dev.value(x))):
+            got[k].append(v)
+        assert qm_projector_err(x.V, x.lam, x.eps, g["V"][t], g["lam"][t], float(g["eps"][t])) <= 1e-9
+    compare_trajectory({k: np.array(v) for k, v in got.items()}, g, TOL["f64"])

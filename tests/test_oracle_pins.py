@@ -242,3 +242,26 @@ def test_qm_oracle_matches_reference_golden(name):
         got["f"].append(oq.value(inst, x))
         assert qm_projector_err(x.V, x.lam, x.eps, g["V"][t], g["lam"][t], float(g["eps"][t])) <= 1e-10
     compare_trajectory({k: np.array(v) for k, v in got.items()}, g, 1e-10)
+
+
+@pytest.mark.parametrize("name", ["qms_n100_r5_L1000", "qms_n60_r3_L3600"])
+def test_qm_stochastic_oracle_matches_reference_golden(name):
+    """Mini-batch runs (StochasticOracle, objectives.py:235-273): the oracle's batches and
+    estimates reproduce the reference trajectory."""
+    from oracle import qm as oq
+
+    g = load_golden(name)
+    n, r, seed, L = int(g["n"]), int(g["r"]), int(g["seed"]), int(g["L"])
+    inst = oq.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=seed)
+    sto = oq.StochasticOracle(inst, L, seed=int(g["oracle_seed"]))
+    x = om.LowRankIterate(n=n, r=r, V=g["V0"], lam=g["lam0"], eps=float(g["eps0"]))
+    got = {k: [] for k in ("shift", "y", "lam", "lhs", "f")}
+    for t in range(len(g["shift"])):
+        G = sto.gradient(x, sto.sample_batch())
+        res = om.lowrank_meg_step(x, lambda u, G=G: G @ u, float(g["eta"]), _qm_eps(t + 1), svd_seed=t)
+        x = res.iterate
+        for k, v in (("shift", res.shift), ("y", res.top_eigenvalues), ("lam", x.lam), ("lhs", res.cert.lhs_cheap),
+                     ("f", oq.value(inst, x))):
+            got[k].append(v)
+        assert qm_projector_err(x.V, x.lam, x.eps, g["V"][t], g["lam"][t], float(g["eps"][t])) <= 1e-10
+    compare_trajectory({k: np.array(v) for k, v in got.items()}, g, 1e-10)
