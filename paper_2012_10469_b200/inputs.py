@@ -77,3 +77,48 @@ def quad_meas_instance(n: int, r_true: int, kappa: float = 0.5, tau_fraction: fl
         d /= np.linalg.norm(d)
         y = y0 + kappa * np.linalg.norm(y0) * d
     return a, b, y, tau_fraction * n
+
+
+# ---------------------------------------------------------------------------
+# "SPECMEG-QMI v1" instance container (reference objectives.py:371-417):
+# magic line, sorted-key JSON header line, then raw little-endian float64 arrays
+# V_factor (n x r_true), a (m x n), b (m x n), y0 (m), y (m).  Byte-compatible with the
+# reference's save_instance / load_instance, so device runs ingest reference instances exactly.
+
+QMI_MAGIC = b"SPECMEG-QMI v1\n"
+
+
+def save_quad_meas(path: str, *, n: int, r_true: int, m: int, kappa: float, tau: float, seed: int, V_factor, a, b,
+                   y0, y) -> None:
+    import json
+
+    header = {"n": int(n), "r_true": int(r_true), "m": int(m), "kappa": kappa, "tau": tau, "seed": seed}
+    with open(path, "wb") as fh:
+        fh.write(QMI_MAGIC)
+        fh.write((json.dumps(header, sort_keys=True) + "\n").encode("ascii"))
+        for arr in (V_factor, a, b, y0, y):
+            fh.write(np.ascontiguousarray(arr, dtype="<f8").tobytes())
+
+
+def load_quad_meas(path: str) -> dict:
+    """Read a container: dict with n, r_true, m, kappa, tau, seed, V_factor, a, b, y0, y.
+    ValueError on a wrong magic line or a truncated payload (the reference's checks)."""
+    import json
+
+    with open(path, "rb") as fh:
+        magic = fh.readline()
+        if magic != QMI_MAGIC:
+            raise ValueError(f"{path}: not a SPECMEG-QMI v1 container (magic {magic!r})")
+        header = json.loads(fh.readline().decode("ascii"))
+        blob = fh.read()
+    n, r_true, m = header["n"], header["r_true"], header["m"]
+    sizes = [n * r_true, m * n, m * n, m, m]
+    if len(blob) != 8 * sum(sizes):
+        raise ValueError(f"{path}: truncated container ({len(blob)} payload bytes)")
+    parts, off = [], 0
+    for size in sizes:
+        parts.append(np.frombuffer(blob, dtype="<f8", count=size, offset=8 * off).copy())
+        off += size
+    v, a, b, y0, y = parts
+    return dict(n=n, r_true=r_true, m=m, kappa=header["kappa"], tau=header["tau"], seed=header["seed"],
+                V_factor=v.reshape(n, r_true), a=a.reshape(m, n), b=b.reshape(m, n), y0=y0, y=y)

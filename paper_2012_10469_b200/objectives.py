@@ -275,6 +275,14 @@ class QuadMeasObjective:
         """From a reference-style instance (fields a, b, y, tau; e.g. specmeg.objectives.generate_instance)."""
         return cls(inst.a, inst.b, inst.y, inst.tau)
 
+    @classmethod
+    def from_container(cls, path: str) -> "QuadMeasObjective":
+        """From a "SPECMEG-QMI v1" file (the reference's save_instance format)."""
+        from .inputs import load_quad_meas
+
+        d = load_quad_meas(path)
+        return cls(d["a"], d["b"], d["y"], d["tau"])
+
     @staticmethod
     def preset_beta(n: int, r: int) -> float:
         """Smoothness preset 0.4 sqrt(r n) (objectives.py:194-197); the experiment's eta = 1/beta."""

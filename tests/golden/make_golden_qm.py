@@ -93,5 +93,13 @@ def main():
         print(name, "m =", inst.m, "L =", L, "f:", rec["f"][0], "->", rec["f"][-1])
 
 
+def container_fixture():
+    """A small container written by the reference's own save_instance (format pin)."""
+    out_dir = os.path.dirname(os.path.abspath(__file__))
+    inst = ref_obj.generate_instance(8, 1, kappa=0.5, tau_fraction=0.5, seed=11)
+    ref_obj.save_instance(inst, os.path.join(out_dir, "qmi_n8_r1_seed11.bin"))
+
+
 if __name__ == "__main__":
     main()
+    container_fixture()
