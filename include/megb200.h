@@ -295,6 +295,7 @@ int megb200_dual_gap(megb200_solver* s, const megb200_gradient* g, const megb200
  *              _dense_measurement_gradient, objectives.py:155-156; with weight = tau it is
  *              RecoveryObjective.grad_operator's tau * grad f(tau X), :211-223)
  *   value:     1/2 ||res||^2 (qm_value, objectives.py:133-136), host out.
+ * eps = 0 evaluates X = V diag(lam) V^T for any V (spectral_init's probe, objectives.py:293-316).
  * Device pointers; n must equal the solver's dimension. */
 int megb200_qm_residuals(megb200_solver* s, const double* a, const double* b, const double* y, int64_t m,
                          const double* V, int64_t ldv, int32_t r, const double* lam_host, double eps, double tau,

@@ -1820,7 +1820,8 @@ int megb200_qm_residuals(megb200_solver* s, const double* a, const double* b, co
     const int64_t n = s->n;
     if (m < 1) throw Error(MEGB200_ERR_PARAM, "need m >= 1");
     if (!(1 <= r && r < n) || r > 32 || ldv < r) throw Error(MEGB200_ERR_PARAM, "need 1 <= r < n, r <= 32");
-    if (!(eps > 0.0 && eps <= 0.75)) throw Error(MEGB200_ERR_PARAM, "eps must lie in (0, 3/4]");
+    // eps = 0 evaluates the plain low-rank X = V diag(lam) V^T (any V: the spectral-init probe)
+    if (!(eps >= 0.0 && eps <= 0.75)) throw Error(MEGB200_ERR_PARAM, "eps must lie in [0, 3/4]");
     QmCoef qc;
     qc.tau = tau;
     qc.eps = eps;

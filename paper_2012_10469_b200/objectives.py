@@ -295,14 +295,50 @@ class QuadMeasObjective:
         """a_i^T (tau X) b_i - y_i for a factored iterate (device tensor of length m)."""
         if x.n != self.n:
             raise ParameterError("iterate dimension does not match the objective")
+        return self._residuals(x.V_device, x.lam, float(x.eps))
+
+    def _residuals(self, V, lam, eps: float) -> torch.Tensor:
         s = self._solver()
-        V = x.V_device
-        lam = runtime.host_f64(x.lam)
+        V = runtime.as_device_f64(V).contiguous()
+        lam = runtime.host_f64(lam)
         res = torch.empty(self.m, dtype=torch.float64, device=runtime.device())
         runtime.check(s.lib.megb200_qm_residuals(s.handle, self.a.data_ptr(), self.b.data_ptr(), self.y.data_ptr(),
-                                                 self.m, V.data_ptr(), V.stride(0), x.r, _lib.dptr(lam),
-                                                 float(x.eps), self.tau, res.data_ptr()))
+                                                 self.m, V.data_ptr(), V.stride(0), int(V.shape[1]), _lib.dptr(lam),
+                                                 float(eps), self.tau, res.data_ptr()))
         return res
+
+    def spectral_init(self, r: int, seed: int = 0, tol: float = 1e-10):
+        """Start factor (reference spectral_init, objectives.py:293-316): a Gaussian probe u (n x r,
+        unit Frobenius norm, host default_rng(seed)), the residuals of tau u u^T on the device, the
+        top-r eigenpairs of -grad f(tau u u^T) by the block solver, and the simplex-projected
+        negated eigenvalues (init_weights_from_top_eigs, :319-323).  Returns (V, weights)."""
+        from .linalg import SymmetricOperator, lanczos_top_r, project_simplex
+
+        if not 1 <= r < self.n:
+            raise ParameterError(f"need 1 <= r < n, got r={r}, n={self.n}")
+        rng = np.random.default_rng(seed)
+        u = rng.standard_normal((self.n, r))
+        u /= np.linalg.norm(u)
+        res = self._residuals(u, np.ones(r), 0.0)
+        G = self.gradient_matrix(res, weight=1.0)
+        top = lanczos_top_r(SymmetricOperator(self.n, dense=G, scale=-1.0), r, tol=tol, seed=seed)
+        w = project_simplex(-np.asarray(top.eigenvalues, dtype=float), self.tau)
+        w = w / w.sum()
+        w = np.maximum(w, 1e-12)
+        return top.eigenvectors, w / w.sum()
+
+    def dual_gap(self, x, seed: int = 0, tol: float = 1e-10) -> float:
+        """Linear-optimisation gap of tau X (reference dual_gap / _dual_gap_core,
+        objectives.py:326-341): Tr(tau X grad) - tau v^T grad v, v the bottom eigenvector of grad f(tau X)
+        (top of its negation, block solver on the device), Tr(tau X grad) = res . (res + y)."""
+        from .linalg import SymmetricOperator, lanczos_top_r
+
+        res = self.residuals(x)
+        G = self.gradient_matrix(res, weight=1.0)
+        top = lanczos_top_r(SymmetricOperator(self.n, dense=G, scale=-1.0), 1, tol=tol, seed=seed)
+        r_h = res.cpu().numpy()
+        trace_term = float(r_h @ (r_h + self.y.cpu().numpy()))
+        return trace_term + self.tau * float(top.eigenvalues[0])
 
     def value(self, x) -> float:
         """f(tau X) = 1/2 ||res||^2 (qm_value, objectives.py:133-136)."""

@@ -60,9 +60,12 @@ def main():
             rec["lhs"].append(res.cert.lhs_cheap)
             rec["f"].append(obj.value(x))
             rec["V"].append(x.V)
+        V_si, w_si = ref_obj.spectral_init(inst, r, seed=seed)
+        gap = ref_obj.dual_gap(inst, x, seed=seed)
         np.savez_compressed(
             os.path.join(out_dir, name + ".npz"), n=n, r=r, seed=seed, eta=eta, tau=inst.tau, m=inst.m,
             a_sum=checksums(inst.a), b_sum=checksums(inst.b), y_sum=checksums(inst.y),
+            si_V=V_si, si_w=w_si, gap_final=gap,
             V0=x0o.V, lam0=x0o.lam, eps0=x0o.eps, **{k: np.array(v) for k, v in rec.items()})
         print(name, "m =", inst.m, "f:", rec["f"][0], "->", rec["f"][-1])
     for name, (n, r, seed, L, oseed) in STOCH.items():

@@ -476,3 +476,21 @@ def test_quad_meas_stochastic_matches_reference_golden(pb, name):
             got[k].append(v)
         assert qm_projector_err(x.V, x.lam, x.eps, g["V"][t], g["lam"][t], float(g["eps"][t])) <= 1e-9
     compare_trajectory({k: np.array(v) for k, v in got.items()}, g, TOL["f64"])
+
+
+@pytest.mark.parametrize("name", ["qm_n100_r1", "qm_n60_r3", "qm_n100_r5"])
+def test_quad_meas_spectral_init_and_dual_gap(pb, name):
+    """QuadMeasObjective.spectral_init (probe residuals with eps = 0, gradient, block solver on
+    -grad, simplex weights) and dual_gap against the unmodified reference (1e-9)."""
+    from oracle import qm as oq
+
+    g = load_golden(name)
+    n, r, seed = int(g["n"]), int(g["r"]), int(g["seed"])
+    inst = oq.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=seed)
+    dev = pb.QuadMeasObjective.from_instance(inst)
+    V, w = dev.spectral_init(r, seed=seed)
+    P, Pg = (V * w) @ V.T, (g["si_V"] * g["si_w"]) @ g["si_V"].T
+    assert np.max(np.abs(P - Pg)) <= 1e-9 * np.max(np.abs(Pg))
+    assert np.max(np.abs(w - g["si_w"])) <= 1e-9
+    x = pb.LowRankIterate(n, r, g["V"][-1], g["lam"][-1], float(g["eps"][-1]))
+    assert abs(dev.dual_gap(x, seed=seed) - float(g["gap_final"])) <= 1e-9 * abs(float(g["gap_final"]))

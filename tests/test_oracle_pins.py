@@ -265,3 +265,19 @@ def test_qm_stochastic_oracle_matches_reference_golden(name):
             got[k].append(v)
         assert qm_projector_err(x.V, x.lam, x.eps, g["V"][t], g["lam"][t], float(g["eps"][t])) <= 1e-10
     compare_trajectory({k: np.array(v) for k, v in got.items()}, g, 1e-10)
+
+
+@pytest.mark.parametrize("name", QM_CASES)
+def test_qm_spectral_init_and_dual_gap_oracle(name):
+    """spectral_init (objectives.py:293-323) and dual_gap (:326-341) restated, against the reference."""
+    from oracle import qm as oq
+
+    g = load_golden(name)
+    n, r, seed = int(g["n"]), int(g["r"]), int(g["seed"])
+    inst = oq.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=seed)
+    V, w = oq.spectral_init(inst, r, seed=seed)
+    P, Pg = (V * w) @ V.T, (g["si_V"] * g["si_w"]) @ g["si_V"].T
+    assert np.max(np.abs(P - Pg)) <= 1e-10 * np.max(np.abs(Pg))
+    assert np.max(np.abs(w - g["si_w"])) <= 1e-10
+    x = om.LowRankIterate(n=n, r=r, V=g["V"][-1], lam=g["lam"][-1], eps=float(g["eps"][-1]))
+    assert abs(oq.dual_gap(inst, x, seed=seed) - float(g["gap_final"])) <= 1e-9 * abs(float(g["gap_final"]))
