@@ -112,3 +112,80 @@ def run(
     x = (LowRankIterate(n, r, v_out, lam_out, eps_out.value, warm_block=ritz[:, : rec.ritz_cols],
                         warm_orth_err=rec.ritz_orth_err) if T > 0 else x0)
     return RunResult(iterate=x, holds=holds.astype(bool), passes=passes, **out)
+
+
+# ---------------------------------------------------------------------------
+# Recovery runs (the paper's experiment): a step loop over the
+# quadratic-measurement objective with the RunRecord rows of SPEC.md's harness
+# (t, f_value, eps_t, eta_t, cheap certificate, lambda_{r+1}, elapsed) and an optional dual gap
+# every k rows, emitted as the spec's CSV.  The full-certificate / Bregman columns need the
+# dense shadow (out of scope) and are left empty, as the spec prescribes for missing fields.
+
+RUN_CSV_HEADER = ("t,f_value,eps_t,eta_t,cert_cheap_lhs,cert_cheap_holds,cert_full_lhs,cert_full_holds,"
+                  "bregman_to_exact,lambda_rsp1,elapsed_ns")
+
+
+@dataclass
+class RecoveryRun:
+    iterate: LowRankIterate
+    rows: list  # dicts keyed by the CSV columns (+ "dual_gap" where computed)
+    summary: dict
+
+
+def run_recovery(objective, x0: LowRankIterate, T: int, *, eta: float, eps_schedule: EpsilonSchedule | None = None,
+                 oracle=None, gap_every: int = 0, svd_subspace: int | None = None, block: int | None = None,
+                 seed: int = 0) -> RecoveryRun:
+    """T MEG steps on a QuadMeasObjective (deterministic, or mini-batch when `oracle` is a
+    QuadMeasStochasticOracle): step t uses eta, eps_{t+1}, svd_seed = t; row t logs f(tau X_{t+1}),
+    the cheap certificate and lambda_{r+1} of the step and its wall time; every `gap_every` rows
+    (and at the end) the dual gap of X_{t+1}."""
+    import time
+
+    from .meg import lowrank_meg_step
+
+    eps_schedule = eps_schedule or EpsilonSchedule.experiment(10.0)
+    rows = []
+    x = x0
+    for t in range(int(T)):
+        t0 = time.perf_counter_ns()
+        g = oracle.grad_operator(x, oracle.sample_batch()) if oracle is not None else objective.grad_operator(x)
+        res = lowrank_meg_step(x, g, float(eta), eps_schedule.eval(t + 1), svd_seed=t, svd_subspace=svd_subspace,
+                               block=block)
+        x = res.iterate
+        row = {"t": t + 1, "f_value": objective.value(x), "eps_t": float(x.eps), "eta_t": float(eta),
+               "cert_cheap_lhs": float(res.cert.lhs_cheap), "cert_cheap_holds": int(res.cert.holds_cheap),
+               "cert_full_lhs": None, "cert_full_holds": None, "bregman_to_exact": None,
+               "lambda_rsp1": float(res.lambda_r_plus_1), "elapsed_ns": time.perf_counter_ns() - t0}
+        if gap_every and ((t + 1) % gap_every == 0 or t + 1 == T):
+            row["dual_gap"] = objective.dual_gap(x, seed=seed)
+        rows.append(row)
+    holds = [r["t"] for r in rows if r["cert_cheap_holds"]]
+    summary = {"T": int(T), "f_final": rows[-1]["f_value"] if rows else objective.value(x0),
+               "first_iter_cert_cheap": holds[0] if holds else -1}
+    gaps = [r["dual_gap"] for r in rows if "dual_gap" in r]
+    if gaps:
+        summary["dual_gap"] = gaps[-1]
+    return RecoveryRun(iterate=x, rows=rows, summary=summary)
+
+
+def emit_metrics(run: RecoveryRun, path: str) -> None:
+    """SPEC.md harness emit_metrics: the exact header row, one row per iteration (17 significant
+    digits, empty cells for absent fields), the summary as trailing `# key = value` comments."""
+    cols = RUN_CSV_HEADER.split(",")
+
+    def fmt(v):
+        if v is None:
+            return ""
+        if isinstance(v, (int, np.integer)):
+            return str(int(v))
+        return repr(float(v)) if np.isfinite(v) else ("-inf" if v < 0 else "inf" if v > 0 else "nan")
+
+    try:
+        with open(path, "w") as fh:
+            fh.write(RUN_CSV_HEADER + "\n")
+            for r in run.rows:
+                fh.write(",".join(fmt(r.get(c)) for c in cols) + "\n")
+            for k, v in run.summary.items():
+                fh.write(f"# {k} = {fmt(v)}\n")
+    except OSError as e:
+        raise OSError(f"{path}: {e}") from e

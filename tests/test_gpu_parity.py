@@ -494,3 +494,35 @@ def test_quad_meas_spectral_init_and_dual_gap(pb, name):
     assert np.max(np.abs(w - g["si_w"])) <= 1e-9
     x = pb.LowRankIterate(n, r, g["V"][-1], g["lam"][-1], float(g["eps"][-1]))
     assert abs(dev.dual_gap(x, seed=seed) - float(g["gap_final"])) <= 1e-9 * abs(float(g["gap_final"]))
+
+
+def test_recovery_run_record_and_csv(pb, tmp_path):
+    """driver.run_recovery (SPEC harness rows) reproduces the reference trajectory's f values and
+    certificates, logs the dual gap, and emit_metrics writes the spec's CSV (exact header, empty
+    dense-shadow cells, summary comments) that parses back to full precision."""
+    import csv
+
+    from oracle import qm as oq
+    from paper_2012_10469_b200 import driver
+    from tests.test_oracle_pins import _qm_eps  # noqa: F401
+
+    g = load_golden("qm_n60_r3")
+    n, r, seed = int(g["n"]), int(g["r"]), int(g["seed"])
+    inst = oq.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=seed)
+    dev = pb.QuadMeasObjective.from_instance(inst)
+    x0 = pb.LowRankIterate(n, r, g["V0"], g["lam0"], float(g["eps0"]))
+    T = len(g["shift"])
+    run = driver.run_recovery(dev, x0, T, eta=float(g["eta"]), gap_every=5, seed=seed)
+    f = np.array([row["f_value"] for row in run.rows])
+    assert np.max(np.abs(f - g["f"]) / np.abs(g["f"])) <= 1e-9
+    lhs = np.array([row["cert_cheap_lhs"] for row in run.rows])
+    assert np.max(np.abs(lhs - g["lhs"]) / np.maximum(1.0, np.abs(g["lhs"]))) <= 1e-9
+    assert abs(run.summary["dual_gap"] - float(g["gap_final"])) <= 1e-9 * abs(float(g["gap_final"]))
+    path = tmp_path / "run.csv"
+    driver.emit_metrics(run, str(path))
+    lines = path.read_text().splitlines()
+    assert lines[0] == driver.RUN_CSV_HEADER
+    body = list(csv.DictReader([ln for ln in lines if not ln.startswith("#")]))
+    assert len(body) == T and body[0]["cert_full_lhs"] == "" and body[0]["bregman_to_exact"] == ""
+    assert np.array_equal(np.array([float(b["f_value"]) for b in body]), f)
+    assert any(ln.startswith("# dual_gap = ") for ln in lines)
