@@ -312,10 +312,11 @@ def run_device_arm(args, world, rank, local):
     lam, eps, warm, werr = x.lam.copy(), x.eps, x.warm_block, x.warm_orth_err
     h2d = w.n * w.r * 8 + w.r * 8
     d2h = w.n * w.r * 8 + (4 * w.r + 3) * 8 + 8 * 8
-    # warm the host-buffer entry point (its device staging is allocated on first use)
+    # the host-buffer entry point through its session object (structs and result buffers made
+    # once; each step is one native call); warmed first (device staging is allocated on first use)
+    stepper = pb.HostStepper(obj, w.n, w.r, svd_subspace=w.subspace, block=w.block)
     for _ in range(max(3, args.warmup)):
-        res = pb.lowrank_meg_step_host(Vh, lam, eps, obj, w.eta(t), w.eps(t + 1), svd_seed=t,
-                                       svd_subspace=w.subspace, block=w.block, warm=warm, warm_orth_err=werr, out=Vn)
+        res = stepper.step(Vh, lam, eps, w.eta(t), w.eps(t + 1), t, warm=warm, warm_orth_err=werr, out=Vn)
         Vh, Vn = Vn, Vh
         lam, eps, warm, werr = res.lam, res.eps, res.warm_block, res.warm_orth_err
         t += 1
@@ -325,8 +326,7 @@ def run_device_arm(args, world, rank, local):
     f0.record()
     for i in range(K2):
         # one reference-facing call with host buffers: upload + validate V, step, read V_next back
-        res = pb.lowrank_meg_step_host(Vh, lam, eps, obj, w.eta(t), w.eps(t + 1), svd_seed=t,
-                                       svd_subspace=w.subspace, block=w.block, warm=warm, warm_orth_err=werr, out=Vn)
+        res = stepper.step(Vh, lam, eps, w.eta(t), w.eps(t + 1), t, warm=warm, warm_orth_err=werr, out=Vn)
         Vh, Vn = Vn, Vh
         lam, eps, warm, werr = res.lam, res.eps, res.warm_block, res.warm_orth_err
         t += 1
@@ -385,7 +385,8 @@ def run_device_arm(args, world, rank, local):
             "host_ms_per_step": 1e3 * host_s / K,
             "timing": "device: native run loop megb200_meg_run (pipelined), one CUDA-event pair around the K steps "
                       "on the solver stream; e2e: per-step lowrank_meg_step_host (C-ABI megb200_lowrank_meg_step_host): "
-                      "V uploaded from pinned host memory, validated, stepped and V_next read back every step",
+                      "V uploaded from pinned host memory, validated, stepped and V_next written back every step "
+                      "(pb.HostStepper: one native call per step)",
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -15,6 +15,7 @@ from .meg import (
     LogmapOperator,
     LowRankIterate,
     HostStepResult,
+    HostStepper,
     LowRankStepResult,
     StepConfig,
     certificate_cheap,
@@ -39,7 +40,7 @@ from .objectives import (
 )
 
 __all__ = [
-    "CertificateRecord", "DenseGradient", "HostStepResult", "EighError", "EpsilonSchedule", "FrobeniusObjective", "GradientOperator",
+    "CertificateRecord", "DenseGradient", "HostStepResult", "HostStepper", "EighError", "EpsilonSchedule", "FrobeniusObjective", "GradientOperator",
     "LanczosError", "LogmapOperator", "QuadMeasObjective", "QuadMeasStochasticOracle", "LowRankIterate", "LowRankStepResult", "ParameterError", "RankDeficiencyError",
     "SampledObjective", "StepConfig", "StochasticFrobeniusObjective", "SymmetricOperator", "TopREigen",
     "ZeroGradient", "certificate_cheap", "certificate_full", "eps_schedule_eval", "lanczos_top_r", "logmap_operator",

@@ -504,3 +504,87 @@ def lowrank_meg_step_host(
     return HostStepResult(V=out, lam=lam_next, eps=float(eps_next), cert=cert, lambda_r_plus_1=o.lambda_r_plus_1,
                           b_r_plus_1=o.b_r_plus_1, shift=o.shift, top_eigenvalues=y, residual_norms=res,
                           passes=int(o.passes), warm_block=ritz[:, : o.ritz_cols], warm_orth_err=o.ritz_orth_err)
+
+
+class HostStepper:
+    """Repeated host-buffer MEG steps on one objective: the per-call part of
+    `lowrank_meg_step_host` without its per-call setup.  The native structs, the result
+    arrays and two alternating device Ritz-block buffers are made once; `step` validates
+    lam/eps like LowRankIterate (meg.py:62-77; V is validated by the native call), fills the
+    changing fields and makes the one native call.
+
+    The returned `warm_block` stays valid until the step after next (double buffered), and the
+    returned arrays are fresh copies.  For objectives whose gradient depends on the step index
+    (the stochastic Frobenius objective) use `lowrank_meg_step_host`."""
+
+    def __init__(self, objective, n: int, r: int, *, svd_tol: float = 1e-10, svd_subspace: int | None = None,
+                 block: int | None = None):
+        from .objectives import StochasticFrobeniusObjective
+
+        if isinstance(objective, StochasticFrobeniusObjective):
+            raise ParameterError("HostStepper needs a step-independent gradient; use lowrank_meg_step_host")
+        g = objective.grad_operator(None, 0) if hasattr(objective, "grad_operator") else objective
+        if not isinstance(g, GradientOperator):
+            raise TypeError("objective must be a device objective or gradient descriptor")
+        self.n, self.r = int(n), int(r)
+        self.s = g.solver()
+        self._hold: list = [g]
+        self.gs = g.struct(self._hold)
+        self.tol = max(svd_tol, g.tol_floor)
+        self.subspace, self.block = svd_subspace, block
+        dev = runtime.device()
+        self.ritz = [torch.empty((self.n, runtime.MAX_BLOCK), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.k = 0
+        self.buf = np.zeros(4 * self.r + 3)
+        self.lam_next = self.buf[: self.r]
+        self.y = self.buf[self.r: 2 * self.r + 1]
+        self.mu = self.buf[2 * self.r + 1: 3 * self.r + 2]
+        self.res = self.buf[3 * self.r + 2:]
+        self.it = _lib.Iterate()
+        self.it.n, self.it.r = self.n, self.r
+        self.lam_in = np.zeros(self.r)
+        self.it.lam = _lib.dptr(self.lam_in)
+        self.o = _lib.StepResult()
+        self.o.lam_next, self.o.y, self.o.mu = _lib.dptr(self.lam_next), _lib.dptr(self.y), _lib.dptr(self.mu)
+        self.o.residual_norms = _lib.dptr(self.res)
+        self.fn = self.s.lib.megb200_lowrank_meg_step_host
+
+    def step(self, V, lam, eps: float, eta: float, eps_next: float, svd_seed: int = 0, *, warm=None,
+             warm_orth_err: float = 1.0, out=None) -> HostStepResult:
+        if not 0 < eps_next <= 0.75:
+            raise ParameterError(f"eps_next must lie in (0, 3/4], got {eps_next}")
+        if not 0 < eps <= 0.75:
+            raise ParameterError(f"eps must lie in (0, 3/4], got {eps}")
+        lam = np.asarray(lam, dtype=np.float64).reshape(-1)
+        if lam.shape != (self.r,):
+            raise ParameterError(f"lam must have {self.r} entries")
+        if abs(lam.sum() - 1.0) > 1e-10:
+            raise ParameterError(f"lam must sum to 1, got {lam.sum()!r}")
+        if np.any(lam[1:] > lam[:-1]) or not lam[-1] > 0:
+            raise ParameterError("lam must be sorted non-increasing and strictly positive")
+        self.lam_in[:] = lam
+        it = self.it
+        it.eps = float(eps)
+        if not (isinstance(V, torch.Tensor) and not V.is_cuda and V.dtype == torch.float64 and V.is_contiguous()
+                and tuple(V.shape) == (self.n, self.r)):
+            raise ParameterError("V must be a contiguous float64 host tensor of shape (n, r)")
+        it.V, it.ldv = V.data_ptr(), self.r
+        if out is None:
+            out = torch.empty((self.n, self.r), dtype=torch.float64).pin_memory()
+        warm_t = warm if isinstance(warm, torch.Tensor) and warm.shape[0] == self.n else None
+        opts = _eig_opts(self.tol, None, svd_seed, self.subspace, 12, self.block, None, warm_t,
+                         warm_orthonormal=warm_t is not None and warm_orth_err <= 1e-13)
+        ritz = self.ritz[self.k]
+        self.k ^= 1
+        o = self.o
+        o.ritz_block, o.ld_ritz = ritz.data_ptr(), ritz.stride(0)
+        rc = self.fn(self.s.handle, C.byref(it), C.byref(self.gs), float(eta), float(eps_next), C.byref(opts),
+                     C.c_void_p(out.data_ptr()), self.r, C.byref(o))
+        if rc:
+            runtime.check(rc, residual_norms=self.res.copy())
+        cert = CertificateRecord(iteration=None, lhs_cheap=o.lhs_cheap, holds_cheap=bool(o.holds_cheap),
+                                 threshold=o.threshold)
+        return HostStepResult(V=out, lam=self.lam_next.copy(), eps=float(eps_next), cert=cert,
+                              lambda_r_plus_1=o.lambda_r_plus_1, b_r_plus_1=o.b_r_plus_1, shift=o.shift,
+                              top_eigenvalues=self.y.copy(), residual_norms=self.res.copy(), passes=int(o.passes),
+                              warm_block=ritz[:, : o.ritz_cols], warm_orth_err=o.ritz_orth_err)

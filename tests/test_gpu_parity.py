@@ -526,3 +526,34 @@ def test_recovery_run_record_and_csv(pb, tmp_path):
     assert len(body) == T and body[0]["cert_full_lhs"] == "" and body[0]["bregman_to_exact"] == ""
     assert np.array_equal(np.array([float(b["f_value"]) for b in body]), f)
     assert any(ln.startswith("# dual_gap = ") for ln in lines)
+
+
+def test_host_stepper_matches_host_step(pb):
+    """HostStepper (structs and buffers made once) gives bit-identical results to
+    lowrank_meg_step_host, rejects invalid lam / V like LowRankIterate (meg.py:62-77)."""
+    import torch
+
+    cfg = inputs.CONFIGS["cfg2"].scaled(1024, 6)
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    dev = pb.FrobeniusObjective(host.m)
+    st = pb.HostStepper(dev, x0.n, x0.r, svd_subspace=64, block=18)
+    Va = torch.from_numpy(np.ascontiguousarray(x0.V)).pin_memory()
+    Vb = Va.clone().pin_memory()
+    la, ea, wa, wea = x0.lam.copy(), x0.eps, None, 1.0
+    lb, eb, wb, web = x0.lam.copy(), x0.eps, None, 1.0
+    for t in range(6):
+        ra = pb.lowrank_meg_step_host(Va, la, ea, dev, 1.0, cfg.eps(t + 1), svd_seed=t, svd_subspace=64, block=18,
+                                      warm=wa, warm_orth_err=wea, out=torch.empty_like(Va).pin_memory())
+        rb = st.step(Vb, lb, eb, 1.0, cfg.eps(t + 1), t, warm=wb, warm_orth_err=web,
+                     out=torch.empty_like(Vb).pin_memory())
+        assert np.array_equal(ra.top_eigenvalues, rb.top_eigenvalues) and np.array_equal(ra.lam, rb.lam)
+        assert np.array_equal(ra.V.numpy(), rb.V.numpy()) and ra.cert.lhs_cheap == rb.cert.lhs_cheap
+        Va, la, ea, wa, wea = ra.V, ra.lam, ra.eps, ra.warm_block, ra.warm_orth_err
+        Vb, lb, eb, wb, web = rb.V, rb.lam, rb.eps, rb.warm_block, rb.warm_orth_err
+    with pytest.raises(pb.ParameterError):
+        st.step(Vb, lb[::-1].copy(), eb, 1.0, 0.01)
+    bad = Vb.clone()
+    bad[:, 0] *= 1.5
+    with pytest.raises(pb.ParameterError):
+        st.step(bad.pin_memory(), lb, eb, 1.0, 0.01)
