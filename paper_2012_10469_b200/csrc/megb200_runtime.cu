@@ -1589,8 +1589,19 @@ int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_ho
     if (!s->host_io) MEG_CUDA(cudaMalloc(&s->host_io, (size_t)2 * n * 64 * sizeof(double)));
     double* Vd = s->host_io;
     double* Vn = s->host_io + n * 64;
-    // contiguous factors move as one block (a pitched copy of 8r-byte rows is n tiny DMA rows)
-    if (x_host->ldv == r)
+    // a contiguous factor in mapped pinned memory is read by the kernels in place (the fused first
+    // pass stages its rows once: no upload on the stream's critical path); otherwise it is
+    // uploaded as one block (a pitched copy of 8r-byte rows is n tiny DMA rows)
+    double* v_mapped = nullptr;
+    if (x_host->ldv == r && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&v_mapped), const_cast<double*>(x_host->V), 0) !=
+            cudaSuccess) {
+      cudaGetLastError();
+      v_mapped = nullptr;
+    }
+    if (v_mapped)
+      Vd = v_mapped;
+    else if (x_host->ldv == r)
       MEG_CUDA(cudaMemcpyAsync(Vd, x_host->V, (size_t)n * r * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     else
       MEG_CUDA(cudaMemcpy2DAsync(Vd, r * sizeof(double), x_host->V, x_host->ldv * sizeof(double), r * sizeof(double),
