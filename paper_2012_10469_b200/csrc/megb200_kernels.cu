@@ -732,13 +732,15 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1)
 // (col, val) pairs with one coalesced access, then walks them two at a time: each
 // half-warp takes one nonzero and reads that U row with consecutive lanes
 // (columns hl and hl + 16), so a gathered row costs ~b*8/32 sectors instead of
-// one sector per column.  Sixteen steps are unrolled so their row loads are in
+// one sector per column.  Groups of UN steps are unrolled so their row loads are in
 // flight together.  Fixed order: nonzeros in index order per half, halves
 // combined at the end (bitwise reproducible).
-__global__ void __launch_bounds__(256) k_csr_apply(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                                                   const double* __restrict__ val, int64_t n,
-                                                   const double* __restrict__ U, int64_t ldu, int b,
-                                                   double* __restrict__ out) {
+template <int UN, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_csr_apply(const int32_t* __restrict__ rowptr,
+                                                      const int32_t* __restrict__ col,
+                                                      const double* __restrict__ val, int64_t n,
+                                                      const double* __restrict__ U, int64_t ldu, int b,
+                                                      double* __restrict__ out) {
   const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= n) return;
@@ -753,20 +755,25 @@ __global__ void __launch_bounds__(256) k_csr_apply(const int32_t* __restrict__ r
       j = __ldg(col + e);
       g = __ldg(val + e);
     }
-    double u0[16], u1[16], gg[16];
+    // the batch's 16 pair-steps in groups of UN: UN row loads per lane in flight, fewer
+    // registers (four CTAs per SM instead of one)
 #pragma unroll
-    for (int s2 = 0; s2 < 16; ++s2) {
-      const int src = 2 * s2 + half;
-      const int jj = __shfl_sync(0xffffffffu, j, src);
-      gg[s2] = __shfl_sync(0xffffffffu, g, src);
-      const double* u = U + (int64_t)jj * ldu;
-      u0[s2] = c0 ? __ldg(u + hl) : 0.0;
-      u1[s2] = c1 ? __ldg(u + hl + 16) : 0.0;
-    }
+    for (int s0 = 0; s0 < 16; s0 += UN) {
+      double u0[UN], u1[UN], gg[UN];
 #pragma unroll
-    for (int s2 = 0; s2 < 16; ++s2) {
-      a0 = fma(gg[s2], u0[s2], a0);
-      a1 = fma(gg[s2], u1[s2], a1);
+      for (int q = 0; q < UN; ++q) {
+        const int src = 2 * (s0 + q) + half;
+        const int jj = __shfl_sync(0xffffffffu, j, src);
+        gg[q] = __shfl_sync(0xffffffffu, g, src);
+        const double* u = U + (int64_t)jj * ldu;
+        u0[q] = c0 ? __ldg(u + hl) : 0.0;
+        u1[q] = c1 ? __ldg(u + hl + 16) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < UN; ++q) {
+        a0 = fma(gg[q], u0[q], a0);
+        a1 = fma(gg[q], u1[q], a1);
+      }
     }
   }
   a0 += __shfl_xor_sync(0xffffffffu, a0, 16);
@@ -1536,7 +1543,9 @@ int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, 
 void csr_apply_partial(const Launch& L, const int32_t* rowptr, const int32_t* col, const double* val, int64_t n,
                        const double* U, int64_t ldu, int b, double* part) {
   if (b > 32) throw Error(MEGB200_ERR_PARAM, "CSR pass supports b <= 32");
-  k_csr_apply<<<cdiv(n, 8), 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
+  // four row loads in flight per lane at four CTAs per SM (cfg3 pass+finish 107 us) beat eight at
+  // three CTAs (112 us) and sixteen at one (139 us): the gathers need warps more than depth
+  k_csr_apply<4, 4><<<cdiv(n, 8), 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
   MEG_LAUNCHED();
   ++*L.counter;
 }
