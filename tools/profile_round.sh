@@ -16,4 +16,5 @@ timeout 900 $G -k regex:k_csr_apply -o $O/prof_csr -f python tools/config_profil
 timeout 900 $G -k regex:k_coop_orth -o $O/prof_orth -f python tools/config_profile.py cfg4 --steps 3 > $O/ncu_orth.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -c 1 -s 2 -k regex:k_rr_wide -o $O/prof_rrwide -f python tools/config_profile.py cfg4 --steps 3 > $O/ncu_rrwide.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -c 1 -s 30 -k regex:k_dense_pass_umma -o $O/prof_umma -f python tools/config_profile.py cfg5 --steps 3 > $O/ncu_umma.log 2>&1
+timeout 600 python tools/qm_bench.py > $O/qm_bench.log 2>&1
 ls -la $O
