@@ -318,6 +318,13 @@ __device__ bool rr_small_neardiag(const double* __restrict__ Hg, int64_t ldh, in
   return true;
 }
 
+// the sweeping Jacobi is a rare fallback here: kept out of line so the fused kernel's hot path
+// stays small in the instruction cache
+__device__ __noinline__ void jacobi_fallback(const double* H, int m, double* theta, double* S, double* sm,
+                                             double* info) {
+  block_jacobi(H, m, m, theta, S, sm, info);
+}
+
 template <int NT, bool CL>
 __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs a) {
   // programmatic dependent launch after the operand pass: nothing is read before it completed
@@ -432,7 +439,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
     stamp(a.stamps, 5);
     if (!rr_small_neardiag<NT>(Hs, b, b, a.theta, a.Sout, jac, thsh, a.info)) {
       __syncthreads();
-      block_jacobi(Hs, b, b, a.theta, a.Sout, jac, a.info);
+      jacobi_fallback(Hs, b, a.theta, a.Sout, jac, a.info);
       __syncthreads();
       for (int c = t; c < b; c += NT) thsh[c] = a.theta[c];
       __syncthreads();
