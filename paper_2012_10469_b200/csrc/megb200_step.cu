@@ -222,7 +222,9 @@ __device__ bool rr_small_neardiag(const double* __restrict__ Hg, int64_t ldh, in
   const double stop2 = fro2 * 1e-30;
   bool done = off2 <= stop2;
   if (!done && !(off2 <= 1e-6 * fro2)) return false;
+  int npre = 0, nns = 0;  // diagnostics: pre-steps and Newton-Schulz steps taken
   for (int pre = 0; pre < 3 && !done; ++pre) {
+    ++npre;
     // Y = I + X
     double xm = 0.0;
     for (int idx = t; idx < mm; idx += NT) {
@@ -244,6 +246,7 @@ __device__ bool rr_small_neardiag(const double* __restrict__ Hg, int64_t ldh, in
     for (int k = 0; k < NT / 32; ++k) xmax = fmax(xmax, wred[64 + k]);
     double* Zp = Y;
     if (xmax >= 1e-8) {
+      ++nns;
       // Newton-Schulz: Tm = (3I - Y^T Y) / 2, Z = Y Tm
       for (int idx = t; idx < mm; idx += NT) {
         const int i = idx / m, j = idx - i * m;
@@ -310,7 +313,7 @@ __device__ bool rr_small_neardiag(const double* __restrict__ Hg, int64_t ldh, in
     Sout[k * m + rk[i]] = V[idx];
   }
   if (t == 0 && info) {
-    info[0] = 0.0;
+    info[0] = -(double)(npre + 10 * nns);  // fast path: -(pre-steps + 10 x Newton-Schulz steps)
     info[1] = sqrt(off2);
     info[2] = sqrt(fro2);
   }
