@@ -493,11 +493,22 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
   const int gw = blockIdx.x * wpb + (t >> 5);
   auto cgs = [&]() {
     const int pq = cols * q;
-    for (int o = t; o < pq; o += kCT) {
-      const int a = o / q, c = o - a * q;
-      double acc = 0.0;
-      for (int r = 0; r < rows; ++r) acc = fma(Qs[r * cols + a], Ws[r * q + c], acc);
-      part[(int64_t)blockIdx.x * pq + o] = acc;
+    // C partial = Qs^T Ws: a thread owns four basis columns a0..a0+3 of one block column c
+    // (four independent row-ordered chains, one Ws load per four FMAs)
+    const int na4 = (cols + 3) / 4;
+    for (int item = t; item < na4 * q; item += kCT) {
+      const int a0 = (item / q) * 4, c = item - (item / q) * q;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int r = 0; r < rows; ++r) {
+        const double wv = Ws[r * q + c];
+        const double* qr = Qs + r * cols + a0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (a0 + u < cols) acc[u] = fma(qr[u], wv, acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (a0 + u < cols) part[(int64_t)blockIdx.x * pq + (a0 + u) * q + c] = acc[u];
     }
     phase_mark(pm++);
     grid.sync();
@@ -509,28 +520,40 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
     phase_mark(pm++);
     for (int o = t; o < pq; o += kCT) Cs[o] = Cws[o];
     __syncthreads();
-    for (int idx = t; idx < rows * q; idx += kCT) {
-      const int r = idx / q, c = idx - r * q;
+    // Ws -= Qs C: a thread owns four block columns c0..c0+3 of one row (one Qs load per four FMAs)
+    const int nc4 = (q + 3) / 4;
+    for (int item = t; item < rows * nc4; item += kCT) {
+      const int r = item / nc4, c0 = (item - r * nc4) * 4;
       const double* qr = Qs + r * cols;
-      double s0 = 0.0, s1 = 0.0;
-      int k = 0;
-      for (; k + 1 < cols; k += 2) {
-        s0 = fma(qr[k], Cs[k * q + c], s0);
-        s1 = fma(qr[k + 1], Cs[(k + 1) * q + c], s1);
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < cols; ++k) {
+        const double qk = qr[k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + u < q) acc[u] = fma(qk, Cs[k * q + c0 + u], acc[u]);
       }
-      if (k < cols) s0 = fma(qr[k], Cs[k * q + c], s0);
-      Ws[idx] -= s0 + s1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c0 + u < q) Ws[r * q + c0 + u] -= acc[u];
     }
     __syncthreads();
     phase_mark(pm++);
   };
   auto cholqr = [&](double thresh, uint64_t bs) {
     const int qq = q * q;
-    for (int o = t; o < qq; o += kCT) {
-      const int a = o / q, c = o - a * q;
-      double acc = 0.0;
-      for (int r = 0; r < rows; ++r) acc = fma(Ws[r * q + a], Ws[r * q + c], acc);
-      part[(int64_t)blockIdx.x * qq + o] = acc;
+    const int nq4 = (q + 3) / 4;
+    for (int item = t; item < nq4 * q; item += kCT) {
+      const int a0 = (item / q) * 4, c = item - (item / q) * q;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int r = 0; r < rows; ++r) {
+        const double wc = Ws[r * q + c];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (a0 + u < q) acc[u] = fma(Ws[r * q + a0 + u], wc, acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (a0 + u < q) part[(int64_t)blockIdx.x * qq + (a0 + u) * q + c] = acc[u];
     }
     phase_mark(pm++);
     grid.sync();
