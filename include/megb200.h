@@ -284,6 +284,12 @@ int megb200_dense_stats(megb200_solver* s, const void* M, int32_t dtype, int64_t
  * lambda_min from the block solver on M - X.  Also returns lambda_min. */
 int megb200_dual_gap(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts, double m_trace,
                      double* gap, double* lambda_min);
+/* The same certificate, also returning the solve's final Ritz block (device, n x *ritz_cols, ld
+ * ld_ritz >= max_block) so the next certificate can start from it (opts->warm): the gradient
+ * moves little between certificates, and a cold solve near the bulk edge takes ~200 passes. */
+int megb200_dual_gap_warm(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts,
+                          double m_trace, double* gap, double* lambda_min, double* ritz_out, int64_t ld_ritz,
+                          int32_t* ritz_cols);
 
 /* Quadratic-measurement objective (the paper's experiment; SURVEY.md 8f row 1,
  * reference objectives.py:111-228): f(tau X) = 1/2 sum_i (a_i^T (tau X) b_i - y_i)^2

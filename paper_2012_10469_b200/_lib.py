@@ -130,6 +130,9 @@ SIGNATURES = [
     ("megb200_dense_stats", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, c_double_p, c_double_p]),
     ("megb200_dual_gap", C.c_int,
      [C.c_void_p, C.POINTER(Gradient), C.POINTER(EigOpts), C.c_double, c_double_p, c_double_p]),
+    ("megb200_dual_gap_warm", C.c_int,
+     [C.c_void_p, C.POINTER(Gradient), C.POINTER(EigOpts), C.c_double, c_double_p, c_double_p, C.c_void_p, C.c_int64,
+      c_int32_p]),
     ("megb200_qm_residuals", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, c_double_p,
       C.c_double, C.c_double, C.c_void_p]),

@@ -1763,9 +1763,29 @@ int megb200_objective_value(megb200_solver* s, const megb200_gradient* g, double
   });
 }
 
+namespace {
+void dual_gap_core(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts, double m_trace,
+                   double* gap, double* lambda_min, double* ritz_out, int64_t ld_ritz, int32_t* ritz_cols);
+}
+
 int megb200_dual_gap(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts, double m_trace,
                      double* gap, double* lambda_min) {
+  return guarded_impl([&] { dual_gap_core(s, g, opts, m_trace, gap, lambda_min, nullptr, 0, nullptr); });
+}
+
+int megb200_dual_gap_warm(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts,
+                          double m_trace, double* gap, double* lambda_min, double* ritz_out, int64_t ld_ritz,
+                          int32_t* ritz_cols) {
   return guarded_impl([&] {
+    if (!ritz_out || !ritz_cols || ld_ritz < s->max_block) throw Error(MEGB200_ERR_PARAM, "Ritz block output missing");
+    dual_gap_core(s, g, opts, m_trace, gap, lambda_min, ritz_out, ld_ritz, ritz_cols);
+  });
+}
+
+namespace {
+void dual_gap_core(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts, double m_trace,
+                   double* gap, double* lambda_min, double* ritz_out, int64_t ld_ritz, int32_t* ritz_cols) {
+  {
     if (!s) throw Error(MEGB200_ERR_PARAM, "solver is NULL");
     check_gradient(s, g);
     if (g->kind != MEGB200_GRAD_FROBENIUS && g->kind != MEGB200_GRAD_STOCHASTIC)
@@ -1790,8 +1810,10 @@ int megb200_dual_gap(megb200_solver* s, const megb200_gradient* g, const megb200
     op.d_dev = s->dvec;
     op.alpha = -tail;
     EigParams P = params_from_opts(opts);
-    EigRun run = top_eigs(s, op, 1, P, nullptr, 0, nullptr, 0, nullptr);
+    int rc_cols = 0;
+    EigRun run = top_eigs(s, op, 1, P, nullptr, 0, ritz_out, ld_ritz, ritz_out ? &rc_cols : nullptr);
     if (!run.converged) throw_lanczos(run, P.tol);
+    if (ritz_cols) *ritz_cols = rc_cols;
     const double lmin = -run.theta[0];
     // Tr(X grad) = ||X||^2 - <X, M>
     if (isnan(m_trace)) {
@@ -1820,8 +1842,9 @@ int megb200_dual_gap(megb200_solver* s, const megb200_gradient* g, const megb200
     }
     if (gap) *gap = (x2 - inner) - lmin;
     if (lambda_min) *lambda_min = lmin;
-  });
+  }
 }
+}  // namespace
 
 int megb200_qm_residuals(megb200_solver* s, const double* a, const double* b, const double* y, int64_t m,
                          const double* V, int64_t ldv, int32_t r, const double* lam_host, double eps, double tau,

@@ -164,12 +164,14 @@ class FrobeniusObjective:
         return v.value
 
     def dual_gap(self, x, tol: float = 1e-10, seed: int = 0, block: int | None = None,
-                 subspace: int | None = None) -> tuple[float, float]:
+                 subspace: int | None = None, warm: bool = True) -> tuple[float, float]:
         """Tr(X grad) - lambda_min(grad), grad = X - M (_dual_gap_core, objectives.py:332-335).
 
         Returns (gap, lambda_min).  lambda_min comes from the block solver on
-        M - X (the top eigenpair of -grad, as the reference computes it).
-        """
+        M - X (the top eigenpair of -grad, as the reference computes it).  With
+        warm=True the solve starts from the Ritz block of this objective's previous
+        certificate (the gradient moves little between certificates); the converged
+        result obeys the same residual rule either way."""
         from .linalg import _eig_opts
 
         g = self.grad_operator(x)
@@ -177,10 +179,15 @@ class FrobeniusObjective:
         keep: list = []
         gs = g.struct(keep)
         tol = max(tol, g.tol_floor)
-        opts = _eig_opts(tol, None, seed, subspace, 12, block)
+        prev = getattr(self, "_gap_warm", None) if warm else None
+        opts = _eig_opts(tol, None, seed, subspace, 12, block, None, prev, warm_orthonormal=False)
         gap, lmin = C.c_double(), C.c_double()
-        runtime.check(s.lib.megb200_dual_gap(s.handle, C.byref(gs), C.byref(opts), self.m_trace, C.byref(gap),
-                                             C.byref(lmin)), residual_norms=[])
+        out = torch.empty((self.n, runtime.MAX_BLOCK), dtype=torch.float64, device=runtime.device())
+        cols = C.c_int32()
+        runtime.check(s.lib.megb200_dual_gap_warm(s.handle, C.byref(gs), C.byref(opts), self.m_trace, C.byref(gap),
+                                                  C.byref(lmin), out.data_ptr(), out.stride(0), C.byref(cols)),
+                      residual_norms=[])
+        self._gap_warm = out[:, : cols.value] if cols.value > 0 else None
         return gap.value, lmin.value
 
 

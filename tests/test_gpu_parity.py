@@ -557,3 +557,24 @@ def test_host_stepper_matches_host_step(pb):
     bad[:, 0] *= 1.5
     with pytest.raises(pb.ParameterError):
         st.step(bad.pin_memory(), lb, eb, 1.0, 0.01)
+
+
+def test_dual_gap_warm_start_matches_cold(pb):
+    """A certificate warm-started from the previous certificate's Ritz block (megb200_dual_gap_warm)
+    converges to the cold one within the residual rule (cfg2 shape at n = 1024)."""
+    cfg = inputs.CONFIGS["cfg2"].scaled(1024, 6)
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    dev = pb.FrobeniusObjective(host.m)
+    x = pb.LowRankIterate(x0.n, x0.r, x0.V, x0.lam, x0.eps)
+    gaps = []
+    for t in range(12):
+        x = pb.lowrank_meg_step(x, dev.grad_operator(x), 1.0, cfg.eps(t + 1), svd_seed=t, svd_subspace=64,
+                                block=18).iterate
+        if t % 4 == 3:
+            warm = dev.dual_gap(x, warm=True)
+            cold = dev.dual_gap(x, warm=False)
+            assert abs(warm[0] - cold[0]) <= 1e-9 * max(1.0, abs(cold[0]))
+            assert abs(warm[1] - cold[1]) <= 1e-9 * max(1.0, abs(cold[1]))
+            gaps.append(warm[0])
+    assert all(g > -1e-9 for g in gaps)
