@@ -548,6 +548,8 @@ class HostStepper:
         self.o.lam_next, self.o.y, self.o.mu = _lib.dptr(self.lam_next), _lib.dptr(self.y), _lib.dptr(self.mu)
         self.o.residual_norms = _lib.dptr(self.res)
         self.fn = self.s.lib.megb200_lowrank_meg_step_host
+        self.opts = _eig_opts(self.tol, None, 0, self.subspace, 12, self.block)
+        self._views: dict = {}  # (buffer, cols) -> warm-block view (the width is fixed per solve shape)
 
     def step(self, V, lam, eps: float, eta: float, eps_next: float, svd_seed: int = 0, *, warm=None,
              warm_orth_err: float = 1.0, out=None) -> HostStepResult:
@@ -555,14 +557,20 @@ class HostStepper:
             raise ParameterError(f"eps_next must lie in (0, 3/4], got {eps_next}")
         if not 0 < eps <= 0.75:
             raise ParameterError(f"eps must lie in (0, 3/4], got {eps}")
-        lam = np.asarray(lam, dtype=np.float64).reshape(-1)
-        if lam.shape != (self.r,):
-            raise ParameterError(f"lam must have {self.r} entries")
-        if abs(lam.sum() - 1.0) > 1e-10:
-            raise ParameterError(f"lam must sum to 1, got {lam.sum()!r}")
-        if np.any(lam[1:] > lam[:-1]) or not lam[-1] > 0:
-            raise ParameterError("lam must be sorted non-increasing and strictly positive")
-        self.lam_in[:] = lam
+        lam_in = self.lam_in
+        try:
+            lam_in[:] = lam
+        except ValueError as e:
+            raise ParameterError(f"lam must have {self.r} entries") from e
+        ssum = 0.0
+        prev = math.inf
+        for v in lam_in.tolist():  # LowRankIterate's lam rules (meg.py:72-77), without array temporaries
+            if not (0.0 < v <= prev):
+                raise ParameterError("lam must be sorted non-increasing and strictly positive")
+            prev = v
+            ssum += v
+        if abs(ssum - 1.0) > 1e-10:
+            raise ParameterError(f"lam must sum to 1, got {ssum!r}")
         it = self.it
         it.eps = float(eps)
         if not (isinstance(V, torch.Tensor) and not V.is_cuda and V.dtype == torch.float64 and V.is_contiguous()
@@ -571,10 +579,15 @@ class HostStepper:
         it.V, it.ldv = V.data_ptr(), self.r
         if out is None:
             out = torch.empty((self.n, self.r), dtype=torch.float64).pin_memory()
-        warm_t = warm if isinstance(warm, torch.Tensor) and warm.shape[0] == self.n else None
-        opts = _eig_opts(self.tol, None, svd_seed, self.subspace, 12, self.block, None, warm_t,
-                         warm_orthonormal=warm_t is not None and warm_orth_err <= 1e-13)
-        ritz = self.ritz[self.k]
+        opts = self.opts
+        opts.seed = int(svd_seed) & 0xFFFFFFFFFFFFFFFF
+        if isinstance(warm, torch.Tensor) and warm.shape[0] == self.n:
+            opts.warm, opts.warm_cols, opts.ld_warm = warm.data_ptr(), warm.shape[1], warm.stride(0)
+            opts.warm_orthonormal = 1 if warm_orth_err <= 1e-13 else 0
+        else:
+            opts.warm, opts.warm_cols, opts.ld_warm, opts.warm_orthonormal = 0, 0, 0, 0
+        kb = self.k
+        ritz = self.ritz[kb]
         self.k ^= 1
         o = self.o
         o.ritz_block, o.ld_ritz = ritz.data_ptr(), ritz.stride(0)
@@ -587,4 +600,10 @@ class HostStepper:
         return HostStepResult(V=out, lam=self.lam_next.copy(), eps=float(eps_next), cert=cert,
                               lambda_r_plus_1=o.lambda_r_plus_1, b_r_plus_1=o.b_r_plus_1, shift=o.shift,
                               top_eigenvalues=self.y.copy(), residual_norms=self.res.copy(), passes=int(o.passes),
-                              warm_block=ritz[:, : o.ritz_cols], warm_orth_err=o.ritz_orth_err)
+                              warm_block=self._view(kb, ritz, o.ritz_cols), warm_orth_err=o.ritz_orth_err)
+
+    def _view(self, kb: int, ritz, cols: int):
+        v = self._views.get((kb, cols))
+        if v is None:
+            v = self._views[(kb, cols)] = ritz[:, :cols]
+        return v
