@@ -202,6 +202,8 @@ struct FusedPassArgs {
   double* vgram = nullptr;  // optional out: Gram of the first nvg columns of L (phase 0 only)
   int nvg = 0;
   bool stage_l = true;  // set by fused_first_pass: L rows staged in shared memory
+  int lam_inline_n = 0;   // > 0: lc's kept weights passed by value (lam_inline), lc.lam not read
+  double lam_inline[64] = {};
 };
 bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count);
 void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count);

@@ -74,6 +74,17 @@ struct megb200_solver {
   unsigned* fsync = nullptr;  // tickets / flags of the fused first-pass kernel (zeroed)
   unsigned epoch = 0;
   int want_vgram = 0;      // host-buffer step: fused phase 0 also reduces the factor Gram (r x r)
+  // kept weights of the current iterate, uploaded lazily: the fused first pass takes them as
+  // kernel arguments, other consumers flush them to dlam first
+  double dlam_host[64] = {};
+  int dlam_n = 0;
+  bool dlam_dirty = false;
+  void flush_dlam() {
+    if (dlam_dirty) {
+      h2d(dlam, dlam_host, dlam_n);
+      dlam_dirty = false;
+    }
+  }
   bool vgram_done = false;
   int64_t pack_vgram = 0;  // its offset in the result pack
   double* qm_part = nullptr;  // quadratic-measurement gradient split-K partials (grown on demand)
@@ -239,6 +250,7 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
               int hp = 0, double* Hout = nullptr) {
   Launch L = s->launch();
   const int S = pass_launch(s, op, U, ldu, k);
+  if (op.lc.lam == s->dlam) s->flush_dlam();
   coop_finish(L, s->n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
               s->sm_count, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap, op.lc, op.Eg, op.ldg);
 }
@@ -480,6 +492,10 @@ int fused_pass(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu,
   a.l = op.L ? op.l : 0;
   a.d = op.d_dev;
   a.lc = op.lc;
+  if (op.lc.lam == s->dlam && s->dlam_dirty) {  // the iterate's weights as kernel arguments
+    std::copy(s->dlam_host, s->dlam_host + s->dlam_n, a.lam_inline);
+    a.lam_inline_n = s->dlam_n;
+  }
   a.Eg = op.Eg;
   a.ldg = op.ldg;
   a.U = U;
@@ -804,7 +820,9 @@ StepOperator build_step_operator(megb200_solver* s, const megb200_iterate* x, co
   StepOperator so;
   if (g->kind == MEGB200_GRAD_FROBENIUS && g->gV == x->V && g->g_r == r && g->g_ldv == x->ldv && g->g_eps == x->eps &&
       r <= 64 && std::equal(x->lam, x->lam + r, g->g_lam)) {
-    s->h2d(s->dlam, x->lam, r);
+    std::copy(x->lam, x->lam + r, s->dlam_host);
+    s->dlam_n = (int)r;
+    s->dlam_dirty = true;  // uploaded only if a consumer other than the fused first pass needs it
     so.op = frob_merged_op(g, x->V, x->ldv, n, (int)r, x->eps, eta, s->dlam);
     return so;
   }

@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
   for (int k = t; k < l; k += NT) {
     double v;
     if (a.lc.lam && k < a.lc.lr) {
-      const double kept = a.lc.c1 * a.lc.lam[k];
+      const double kept = a.lc.c1 * (a.lam_inline_n > 0 ? a.lam_inline[k] : a.lc.lam[k]);
       v = (log(kept) - a.lc.log_tail) + (-a.lc.eta * (kept - a.lc.tail_g));
     } else {
       v = a.d[k];
