@@ -585,9 +585,13 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   uint64_t refill_ctr = 0;
 
   s->mark("begin");
-  // ---- start block: warm columns + seeded random fill
+  // ---- start block: warm columns + seeded random fill.  A verified-orthonormal warm block of
+  // exactly bw columns is read in place by the fused first pass; it is copied into the basis only
+  // if the solve continues past that pass (deferred_warm)
   const int wc = (int)std::min<int64_t>(P.warm_cols, bw);
-  if (wc > 0) copy_block(L, n, wc, P.warm, P.ld_warm, s->Q, s->ldq);
+  bool deferred_warm = wc == bw && P.warm_orthonormal && ((uintptr_t)P.warm % 16) == 0 && (P.ld_warm % 2) == 0 &&
+                       fused_ok(s, op, bw, nreq) && getenv("MEGB200_NO_INPLACE_WARM") == nullptr;
+  if (wc > 0 && !deferred_warm) copy_block(L, n, wc, P.warm, P.ld_warm, s->Q, s->ldq);
   if (bw > wc) fill_gaussian(L, n, bw - wc, key_start, 0, 1.0, false, s->Q + wc, s->ldq);
   if (wc == bw && P.warm_orthonormal) {
     // verified-orthonormal warm Ritz block (its Gram came back with the previous step): use as is
@@ -625,7 +629,8 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       double* v2 = vec_out ? vec_out : (epi ? epi->v_next : nullptr);
       const int64_t ld2 = vec_out ? ld_vec : (epi ? epi->ld_next : 0);
       const int r2 = vec_out ? nreq : (epi ? epi->r : 0);
-      const int gr = fuse ? fused_pass(s, op, s->Q, s->ldq, bw, nreq, epi, ritz_out, ld_ritz, v2, ld2, r2, pk)
+      const int gr = fuse ? fused_pass(s, op, deferred_warm ? P.warm : s->Q, deferred_warm ? P.ld_warm : s->ldq, bw,
+                                       nreq, epi, ritz_out, ld_ritz, v2, ld2, r2, pk)
                           : rr_readback(s, newcols, nreq, bw, epi, pk, ritz_out, ld_ritz, v2, ld2, r2);
       const int rq = std::min(newcols, std::max(nreq, bw));
       // host-buffer step: V_next travels back with the pack (one wait when this RR converges)
@@ -682,6 +687,10 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       if (run.passes >= max_passes) break;
     }
     if (nxt <= 0) break;
+    if (deferred_warm) {  // the solve continues: the first block joins the basis
+      copy_block(L, n, bw, P.warm, P.ld_warm, s->Q, s->ldq);
+      deferred_warm = false;
+    }
     // next Krylov block: the image block orthogonalised against the basis
     if (nxt == cur) {
       copy_block(L, n, cur, s->AQ + cols, s->ldq, s->Q + newcols, s->ldq);
