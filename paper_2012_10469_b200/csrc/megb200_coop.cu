@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
   cg::grid_group grid = cg::this_grid();
   phase_mark(10);
   // small Rayleigh-Ritz problems are solved here by CTA 0; large ones (m > 48)
-  // arrive pre-solved from k_rr_jacobi (1024 threads) -- flagged by info == nullptr
+  // arrive pre-solved from k_rr_wide (megb200_rr.cu, 1024 threads) -- flagged by info == nullptr
   const int cols = m;
   double* Ss = sm;
   double* Qs = sm + cols * rq;    // chunk rows of Q (kRC x cols)

@@ -72,10 +72,6 @@ int dense_pass_umma(const Launch& L, const float* M, int64_t ldm, int64_t n, con
                     double* part, int64_t part_cap_slices, int sm_count, float* uscratch);
 void csr_apply_partial(const Launch& L, const int32_t* rowptr, const int32_t* col, const double* val, int64_t n,
                        const double* U, int64_t ldu, int b, double* part);
-// W = scale * sum_s part[s] + L E + alpha U   (E = l x b, dense ld b, device)
-void apply_finish(const Launch& L, int64_t n, int b, int S, const double* part, double scale, const double* Lf,
-                  int64_t ldl, int l, const double* E, double alpha, const double* U, int64_t ldu, double* W,
-                  int64_t ldw);
 
 // C (p x q, ld ldc) = diag(rowscale) * X^T Y  (+ beta C if accumulate).  rowscale may be null.
 void tn(const Launch& Lc, int64_t n, const double* X, int64_t ldx, int p, const double* Y, int64_t ldy, int q,
@@ -83,31 +79,15 @@ void tn(const Launch& Lc, int64_t n, const double* X, int64_t ldx, int p, const 
 // Y (n x q) = beta * Y + alpha * X C   (X n x p, C p x q dense ld ldc).  Z == Y allowed only if beta path.
 void nn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const double* C, int64_t ldc, int q,
         double alpha, double beta, double* Y, int64_t ldy);
-// Cholesky of the q x q Gram G (ld q); R = chol, Rinv = R^-1 (both q x q ld q);
-// deficient pivots (<= thresh^2) flagged in mask; Rtot = R * Rprev if Rprev.
-void chol(const Launch& L, const double* G, int q, double thresh, double* R, double* Rinv, int* mask,
-          const double* Rprev, double* Rtot, int cols_prev);
-// W (n x q) = W * Rinv (upper triangular), deficient columns refilled with random normals
-void apply_rinv(const Launch& L, int64_t n, double* W, int64_t ldw, int q, const double* Rinv, const int* mask,
-                uint64_t key, uint64_t ctr_base);
-// Rayleigh-Ritz: eigen-decomposition of the symmetric m x m H (upper triangle,
-// ld ldh) by parallel cyclic Jacobi in one CTA.  theta: m non-increasing; S: m x m
-// row-major (column j = eigenvector j).  est[j] = ||Rn * S[m-cur:m, j]|| for j < nreq.
-void rr_jacobi(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, const double* Rn,
-               int rn_rows, int cur, int nreq, double* est, double* info);
 // Wide Rayleigh-Ritz (m <= 112, one CTA): Householder tridiagonalisation + multisection +
 // twisted-factorisation eigenvectors, verified, with a cyclic-Jacobi fallback (megb200_rr.cu)
 // (only the top nvec eigenpairs and the smallest eigenvalue are computed when nvec < m; the
 // other theta entries are reported as the smallest, the other S columns as zero)
 void rr_wide(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info,
              int nvec = 0);
-// explicit residuals  ||AX_j - theta_j X_j||^2 partial sums, reduced into out[j] (sqrt applied)
-void resid_norms(const Launch& L, int64_t n, const double* X, int64_t ldx, const double* AX, int64_t ldax,
-                 int q, const double* theta, double* out, double* part, int64_t part_cap, int sm_count);
 void copy_block(const Launch& L, int64_t n, int q, const double* src, int64_t lds, double* dst, int64_t ldd);
 void fill_gaussian(const Launch& L, int64_t n, int q, uint64_t key, uint64_t base, double scale, bool round_f32,
                    double* dst, int64_t ldd);
-void zero(const Launch& L, double* p, int64_t count);
 // sampled gradient values g_e = X_ij - obs_e from factors; optional partial sum of squares
 void csr_values(const Launch& L, int64_t n, const int32_t* rowptr, const int32_t* col, const double* obs,
                 const double* V, int64_t ldv, int r, const double* coeff, double tail, double* g, double* sq_part,
@@ -115,9 +95,6 @@ void csr_values(const Launch& L, int64_t n, const int32_t* rowptr, const int32_t
 void dense_stats(const Launch& L, const void* M, int dtype, int64_t ld, int64_t n, double* part, int slots);
 void gen_dense_target(const Launch& L, const double* U, int64_t r, const double* lam, double sigma, uint64_t key,
                       void* M, int dtype, int64_t ld, int64_t n);
-// step epilogue on device: mu (nreq) -> out[0..]: y (nreq), lam (r), lam_rp1, b_rp1, shift, lhs, holds,
-// threshold, kept-mass flag
-void step_epilogue(const Launch& L, const double* theta, int r, int64_t n, double eps_next, double* out);
 void reduce_sum(const Launch& L, const double* part, int slots, int width, double* out);
 // H[0:cap, 0:cap] = 0 except H[j][j] = theta[j] for j < k
 void set_diag(const Launch& L, double* H, int cap, int k, const double* theta);

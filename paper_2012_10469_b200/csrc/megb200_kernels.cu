@@ -321,10 +321,6 @@ __device__ __forceinline__ void tma_2d_stream(void* dst, const CUtensorMap* map,
       " [%0], [%1, {%2, %3}], [%4], %5;"
       ::"r"(su32(dst)), "l"(map), "r"(x), "r"(y), "r"(su32(b)), "l"(policy) : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(b)) : "memory");
-}
 }  // namespace pipe
 
 constexpr int kPipeKC = 32;      // k rows per stage
@@ -784,26 +780,6 @@ __global__ void __launch_bounds__(256, MINB) k_csr_apply(const int32_t* __restri
   }
 }
 
-// W = scale * sum_s part[s] + L E + alpha U
-__global__ void k_apply_finish(int64_t n, int b, int S, const double* __restrict__ part, double scale,
-                               const double* __restrict__ Lf, int64_t ldl, int l, const double* __restrict__ E,
-                               double alpha, const double* __restrict__ U, int64_t ldu, double* __restrict__ W,
-                               int64_t ldw) {
-  extern __shared__ double Es[];
-  for (int idx = threadIdx.x; idx < l * b; idx += blockDim.x) Es[idx] = E[idx];
-  __syncthreads();
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n * b) return;
-  const int64_t i = idx / b;
-  const int c = (int)(idx - i * b);
-  double s = 0.0;
-  for (int t = 0; t < S; ++t) s += part[(int64_t)t * n * b + idx];
-  double v = scale * s + alpha * U[i * ldu + c];
-  const double* Lr = Lf + i * ldl;
-  for (int k = 0; k < l; ++k) v = fma(Lr[k], Es[k * b + c], v);
-  W[i * ldw + c] = v;
-}
-
 // ===========================================================================
 // Tall-skinny X^T Y partials: each CTA reduces a contiguous row range into
 // one p x q partial; k_reduce_partials sums the partials in CTA order.
@@ -889,179 +865,6 @@ __global__ void k_nn(int64_t n, const double* __restrict__ X, int64_t ldx, int p
   *y = (beta == 0.0 ? 0.0 : beta * *y) + alpha * s;
 }
 
-// ===========================================================================
-// K4: Cholesky of a q x q Gram matrix (q <= 64) with column equilibration
-// and breakdown detection (linalg.py:193-199 rule: a direction whose norm is
-// <= thresh is replaced by a fresh random one).
-__global__ void __launch_bounds__(256) k_chol(const double* __restrict__ Gin, int q, double thresh, double* __restrict__ Rrel,
-                                              double* __restrict__ Rinv, int* __restrict__ mask,
-                                              const double* __restrict__ Rprev, double* __restrict__ Rtot,
-                                              int cols_prev) {
-  extern __shared__ double chol_sm[];
-  const int ld = q + 1;
-  double* Ab = chol_sm;            // q x (q+1)
-  double* Rb = chol_sm + q * ld;   // q x (q+1)
-  __shared__ double D[64];
-  __shared__ int bad[64];
-  const int t = threadIdx.x;
-#define A(i, j) Ab[(i) * ld + (j)]
-#define R(i, j) Rb[(i) * ld + (j)]
-  for (int idx = t; idx < q * q; idx += blockDim.x) {
-    const int i = idx / q, j = idx - i * q;
-    A(i, j) = Gin[(i <= j) ? i * q + j : j * q + i];
-    R(i, j) = 0.0;
-  }
-  __syncthreads();
-  if (t < q) {
-    const double g = A(t, t);
-    bad[t] = !(g > thresh * thresh);
-    D[t] = bad[t] ? 1.0 : sqrt(g);
-  }
-  __syncthreads();
-  for (int idx = t; idx < q * q; idx += blockDim.x) {
-    const int i = idx / q, j = idx - i * q;
-    A(i, j) = (bad[i] || bad[j]) ? (i == j ? 1.0 : 0.0) : A(i, j) / (D[i] * D[j]);
-  }
-  __syncthreads();
-  for (int j = 0; j < q; ++j) {
-    if (t == 0) {
-      const double d = A(j, j);
-      if (!bad[j] && d > 1e-20) {
-        R(j, j) = sqrt(d);
-      } else {
-        bad[j] = 1;
-        R(j, j) = 1.0;
-      }
-    }
-    __syncthreads();
-    const double rjj = R(j, j);
-    const bool bj = bad[j];
-    for (int k = j + 1 + t; k < q; k += blockDim.x) R(j, k) = bj ? 0.0 : A(j, k) / rjj;
-    __syncthreads();
-    for (int idx = t; idx < (q - j - 1) * (q - j - 1); idx += blockDim.x) {
-      const int k = j + 1 + idx / (q - j - 1), l = j + 1 + idx % (q - j - 1);
-      A(k, l) -= R(j, k) * R(j, l);
-    }
-    __syncthreads();
-  }
-  // de-equilibrate: R_true = Rs D, Rinv = D^-1 Rs^-1
-  if (t < q) {
-    const int c = t;  // column c of Rs^-1 by back substitution
-    double x[64];
-    for (int i = 0; i < 64; ++i) x[i] = 0.0;
-    x[c] = 1.0 / R(c, c);
-    for (int i = c - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int k = i + 1; k <= c; ++k) s += R(i, k) * x[k];
-      x[i] = -s / R(i, i);
-    }
-    for (int i = 0; i < q; ++i) Rinv[i * q + c] = (i <= c) ? x[i] / D[i] : 0.0;
-  }
-  __syncthreads();
-  for (int idx = t; idx < q * q; idx += blockDim.x) {
-    const int i = idx / q, j = idx - i * q;
-    Rrel[idx] = (bad[i] || j < i) ? 0.0 : R(i, j) * D[j];
-  }
-  if (t < q) mask[t] = bad[t];
-  if (Rtot) {
-    __syncthreads();
-    // Rtot (q x cols_prev) = Rrel (q x q) * Rprev (q x cols_prev)
-    for (int idx = t; idx < q * cols_prev; idx += blockDim.x) {
-      const int i = idx / cols_prev, j = idx - i * cols_prev;
-      double s = 0.0;
-      if (!bad[i])
-        for (int k = i; k < q; ++k) s += R(i, k) * D[k] * Rprev[k * cols_prev + j];
-      Rtot[idx] = s;
-    }
-  }
-}
-#undef A
-#undef R
-
-// W = W Rinv, deficient columns replaced by random normals
-__global__ void __launch_bounds__(256) k_apply_rinv(int64_t n, double* __restrict__ W, int64_t ldw, int q,
-                                                    const double* __restrict__ Rinv, const int* __restrict__ mask,
-                                                    uint64_t key, uint64_t base) {
-  extern __shared__ double rinv_sm[];
-  double* Ri = rinv_sm;           // q x q
-  double* Ws = rinv_sm + q * q;   // 32 x q
-  __shared__ int bad[64];
-  for (int idx = threadIdx.x; idx < q * q; idx += blockDim.x) Ri[idx] = Rinv[idx];
-  if (threadIdx.x < q) bad[threadIdx.x] = mask[threadIdx.x];
-  const int64_t r0 = (int64_t)blockIdx.x * 32;
-  const int rows = (int)min((int64_t)32, n - r0);
-  for (int idx = threadIdx.x; idx < rows * q; idx += blockDim.x) {
-    const int r = idx / q, c = idx - r * q;
-    Ws[idx] = W[(r0 + r) * ldw + c];
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < rows * q; idx += blockDim.x) {
-    const int r = idx / q, c = idx - r * q;
-    double v;
-    if (bad[c]) {
-      v = gauss_dev(key, base + (uint64_t)(r0 + r) * q + c);
-    } else {
-      v = 0.0;
-      for (int k = 0; k <= c; ++k) v = fma(Ws[r * q + k], Ri[k * q + c], v);
-    }
-    W[(r0 + r) * ldw + c] = v;
-  }
-}
-
-// ===========================================================================
-// K6: Rayleigh-Ritz by parallel cyclic Jacobi (round-robin ordering) in one
-// CTA; H and the accumulated rotations live in shared memory (m <= 112).
-constexpr int kJacobiThreads = 1024;
-
-__global__ void __launch_bounds__(kJacobiThreads, 1)
-    k_rr_jacobi(const double* __restrict__ Hg, int64_t ldh, int m, double* __restrict__ theta,
-                double* __restrict__ Sout, const double* __restrict__ Rn, int rn_rows, int cur, int nreq,
-                double* __restrict__ est, double* __restrict__ info) {
-  extern __shared__ double sm[];
-  block_jacobi(Hg, ldh, m, theta, Sout, sm, info);
-  __syncthreads();
-  // residual estimates est[j] = || Rn (rn_rows x cur) * S[m-cur:m, j] ||
-  if (Rn && est) {
-    for (int j = threadIdx.x; j < nreq; j += blockDim.x) {
-      double s2 = 0.0;
-      for (int a = 0; a < rn_rows; ++a) {
-        double v = 0.0;
-        for (int c = 0; c < cur; ++c) v = fma(Rn[a * cur + c], Sout[(int64_t)(m - cur + c) * m + j], v);
-        s2 += v * v;
-      }
-      est[j] = sqrt(s2);
-    }
-  }
-}
-
-// partial sums of (AX_j - theta_j X_j)^2 per CTA
-__global__ void __launch_bounds__(256) k_resid_partial(int64_t n, const double* __restrict__ X, int64_t ldx,
-                                                       const double* __restrict__ AX, int64_t ldax, int q,
-                                                       const double* __restrict__ theta, double* __restrict__ part,
-                                                       int64_t rows_per_cta) {
-  __shared__ double red[8][64];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
-  const int64_t r1 = min(n, r0 + rows_per_cta);
-  for (int c = 0; c < q; ++c) {
-    const double th = theta[c];
-    double s = 0.0;
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-      const double d = AX[i * ldax + c] - th * X[i * ldx + c];
-      s = fma(d, d, s);
-    }
-    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) red[warp][c & 63] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tot = 0.0;
-      for (int w = 0; w < 8; ++w) tot += red[w][c & 63];
-      part[(int64_t)blockIdx.x * q + c] = tot;
-    }
-    __syncthreads();
-  }
-}
-
 __global__ void k_copy_block(int64_t n, int q, const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
                              int64_t ldd) {
   // let a programmatically dependent launch (the operand pass) start its prologue now;
@@ -1083,11 +886,6 @@ __global__ void k_fill_gaussian(int64_t n, int q, uint64_t key, uint64_t base, d
   double v = scale * gauss_dev(key, base + (uint64_t)idx);
   if (round_f32) v = (double)__double2float_rn(v);
   dst[i * ldd + c] = v;
-}
-
-__global__ void k_zero(double* p, int64_t count) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < count) p[idx] = 0.0;
 }
 
 // sampled gradient values: one warp per row; optional per-row sum of squares
@@ -1172,47 +970,6 @@ __global__ void __launch_bounds__(256) k_gen_dense_target(const double* __restri
     acc += sigma * ((0.5 / sqrt((double)n)) * g);
   }
   M[i * ld + j] = (T)acc;
-}
-
-__global__ void k_step_epilogue(const double* __restrict__ theta, int r, int64_t n, double eps_next,
-                                double* __restrict__ out) {
-  // out layout: [0, r+1) y; [r+1, 2r+1) lam; then lam_rp1, b_rp1, shift, lhs, holds, threshold, status
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const double shift = theta[0];
-  double y[65];
-  for (int k = 0; k <= r; ++k) y[k] = exp(theta[k] - shift);
-  double kept = 0.0;
-  for (int k = 0; k < r; ++k) kept += y[k];
-  double* o = out;
-  for (int k = 0; k <= r; ++k) o[k] = y[k];
-  double status = 0.0;
-  if (!(kept > 1e-290)) status = 4.0;
-  double lsum = 0.0;
-  for (int k = 0; k < r; ++k) {
-    o[r + 1 + k] = y[k] / kept;
-    lsum += o[r + 1 + k];
-  }
-  for (int k = 0; k < r; ++k) o[r + 1 + k] /= lsum;
-  const double lam_rp1 = y[r];
-  double b = 0.0;
-  for (int k = 0; k <= r; ++k) b += y[k];
-  double lhs;
-  if (!(b > 0.0) || lam_rp1 < 0.0) {
-    status = 1.0;
-    lhs = 0.0;
-  } else if (lam_rp1 == 0.0) {
-    lhs = -INFINITY;
-  } else {
-    lhs = log((double)(n - r) * lam_rp1 / (eps_next * b));
-  }
-  double* tail = o + 2 * r + 1;
-  tail[0] = lam_rp1;
-  tail[1] = b;
-  tail[2] = shift;
-  tail[3] = lhs;
-  tail[4] = (lhs <= 2.0 * eps_next) ? 1.0 : 0.0;
-  tail[5] = 2.0 * eps_next;
-  tail[6] = status;
 }
 
 __global__ void k_set_diag(double* __restrict__ H, int cap, int k, const double* __restrict__ theta) {
@@ -1550,21 +1307,6 @@ void csr_apply_partial(const Launch& L, const int32_t* rowptr, const int32_t* co
   ++*L.counter;
 }
 
-void apply_finish(const Launch& L, int64_t n, int b, int S, const double* part, double scale, const double* Lf,
-                  int64_t ldl, int l, const double* E, double alpha, const double* U, int64_t ldu, double* W,
-                  int64_t ldw) {
-  const size_t smem = (size_t)std::max(1, l * b) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    MEG_CUDA(cudaFuncSetAttribute(k_apply_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
-  k_apply_finish<<<cdiv(n * b, 256), 256, smem, L.stream>>>(n, b, S, part, scale, Lf, ldl, l, E, alpha, U, ldu, W,
-                                                           ldw);
-  MEG_LAUNCHED();
-  ++*L.counter;
-}
-
 void tn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const double* Y, int64_t ldy, int q,
         double* C, int64_t ldc, const double* rowscale, double* part, int64_t part_cap, int sm_count) {
   const int pq = p * q;
@@ -1614,59 +1356,6 @@ void nn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const d
   ++*L.counter;
 }
 
-void chol(const Launch& L, const double* G, int q, double thresh, double* R, double* Rinv, int* mask,
-          const double* Rprev, double* Rtot, int cols_prev) {
-  static bool attr = false;
-  if (!attr) {
-    MEG_CUDA(cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 65 * 8));
-    attr = true;
-  }
-  k_chol<<<1, 256, (size_t)2 * q * (q + 1) * sizeof(double), L.stream>>>(G, q, thresh, R, Rinv, mask, Rprev, Rtot,
-                                                                          cols_prev);
-  MEG_LAUNCHED();
-  ++*L.counter;
-}
-
-void apply_rinv(const Launch& L, int64_t n, double* W, int64_t ldw, int q, const double* Rinv, const int* mask,
-                uint64_t key, uint64_t ctr_base) {
-  static bool attr = false;
-  if (!attr) {
-    MEG_CUDA(cudaFuncSetAttribute(k_apply_rinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 64 + 32 * 64) * 8));
-    attr = true;
-  }
-  k_apply_rinv<<<cdiv(n, 32), 256, (size_t)(q * q + 32 * q) * sizeof(double), L.stream>>>(n, W, ldw, q, Rinv, mask,
-                                                                                          key, ctr_base);
-  MEG_LAUNCHED();
-  ++*L.counter;
-}
-
-void rr_jacobi(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, const double* Rn,
-               int rn_rows, int cur, int nreq, double* est, double* info) {
-  const size_t smem = (size_t)jacobi_smem_doubles(m) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    MEG_CUDA(cudaFuncSetAttribute(k_rr_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 215 * 1024));
-    attr = true;
-  }
-  const int threads = m <= 24 ? 64 : m <= 48 ? 256 : kJacobiThreads;
-  k_rr_jacobi<<<1, threads, smem, L.stream>>>(H, ldh, m, theta, S, Rn, rn_rows, cur, nreq, est, info);
-  MEG_LAUNCHED();
-  ++*L.counter;
-}
-
-void resid_norms(const Launch& L, int64_t n, const double* X, int64_t ldx, const double* AX, int64_t ldax, int q,
-                 const double* theta, double* out, double* part, int64_t part_cap, int sm_count) {
-  int G = std::max(1, std::min(sm_count, cdiv(n, 256)));
-  while ((int64_t)G * q > part_cap && G > 1) G = (G + 1) / 2;
-  const int64_t rows_per = cdiv(n, G);
-  G = cdiv(n, rows_per);
-  k_resid_partial<<<G, 256, 0, L.stream>>>(n, X, ldx, AX, ldax, q, theta, part, rows_per);
-  MEG_LAUNCHED();
-  k_reduce_partials<<<cdiv(q, 256), 256, 0, L.stream>>>(part, G, 1, q, out, q, nullptr, 1);
-  MEG_LAUNCHED();
-  *L.counter += 2;
-}
-
 void copy_block(const Launch& L, int64_t n, int q, const double* src, int64_t lds, double* dst, int64_t ldd) {
   if (n * q == 0) return;
   k_copy_block<<<cdiv(n * q, 256), 256, 0, L.stream>>>(n, q, src, lds, dst, ldd);
@@ -1678,13 +1367,6 @@ void fill_gaussian(const Launch& L, int64_t n, int q, uint64_t key, uint64_t bas
                    double* dst, int64_t ldd) {
   if (n * q == 0) return;
   k_fill_gaussian<<<cdiv(n * q, 256), 256, 0, L.stream>>>(n, q, key, base, scale, round_f32 ? 1 : 0, dst, ldd);
-  MEG_LAUNCHED();
-  ++*L.counter;
-}
-
-void zero(const Launch& L, double* p, int64_t count) {
-  if (count == 0) return;
-  k_zero<<<cdiv(count, 256), 256, 0, L.stream>>>(p, count);
   MEG_LAUNCHED();
   ++*L.counter;
 }
@@ -1713,12 +1395,6 @@ void gen_dense_target(const Launch& L, const double* U, int64_t r, const double*
     k_gen_dense_target<double><<<grid, 256, 0, L.stream>>>(U, (int)r, lam, sigma, key, static_cast<double*>(M), ld, n);
   else
     k_gen_dense_target<float><<<grid, 256, 0, L.stream>>>(U, (int)r, lam, sigma, key, static_cast<float*>(M), ld, n);
-  MEG_LAUNCHED();
-  ++*L.counter;
-}
-
-void step_epilogue(const Launch& L, const double* theta, int r, int64_t n, double eps_next, double* out) {
-  k_step_epilogue<<<1, 32, 0, L.stream>>>(theta, r, n, eps_next, out);
   MEG_LAUNCHED();
   ++*L.counter;
 }
