@@ -38,6 +38,17 @@ WORKLOAD_DESC = ("cfg2: deterministic low-rank MEG, dense 1/2||X-M||_F^2, n=4096
                  "block k=r+8=18, eta=1, eps_t=0.6/(t+11)^2, warm start from the rank-10 projection of M")
 
 
+def workload_desc(name: str) -> str:
+    """The bench line's config.workload for the dense workloads (cfg2 is the headline)."""
+    if name == "cfg2":
+        return WORKLOAD_DESC
+    from paper_2012_10469_b200 import configs
+
+    w = configs.WORKLOADS[name]
+    return (f"{name}: deterministic low-rank MEG, dense 1/2||X-M||_F^2, n={w.n}, r={w.r}, {w.dtype}, block k={w.block}, "
+            f"eta={w.eta0}, eps_t=0.6/(t+11)^2, warm start from the rank-{w.r} projection of M")
+
+
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -201,7 +212,7 @@ def run_reference_arm(args, world, rank):
         "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": done, "warmup": min(warm, 3),
         "ms_per_step": 1e3 * dt / done, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD_DESC, "parallelism": "host cores (single process, BLAS threads)"},
+        "config": {"workload": workload_desc(args.workload), "parallelism": "host cores (single process, BLAS threads)"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
                          "sample": f"{done} consecutive iterations of {args.workload} after {min(warm, 3)} warm-up "
                                    "iterations, oracle/cpu_meg.lowrank_meg_step (restatement of meg.py:327-364 "
@@ -351,7 +362,8 @@ def run_device_arm(args, world, rank, local):
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-        "kernel": "streamed operator pass k_dense_pass_mma (TMA + DMMA/DFMA), every --prof-stride-th (16th) launch of the timed region "
+        "kernel": ("streamed operator pass k_dense_pass_mma (TMA + DMMA/DFMA)" if w.dtype == "f64" else
+                   "streamed operator pass k_dense_pass_umma (TMA + tcgen05 split TF32)") + ", every --prof-stride-th (16th) launch of the timed region "
                   "bracketed by CUDA events on the solver stream (includes its launch latency)",
         "bytes_per_pass": (pb_bytes.value / pc.value) if pc.value else None,
         "pass_ms": (pm.value / pc.value) if pc.value else None, "passes": int(pc.value), "peak_source": peak_src,
@@ -371,9 +383,11 @@ def run_device_arm(args, world, rank, local):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(3, args.warmup),
             "ms_per_step": 1e3 * tmax / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": w.dtype, "data": "synthetic (seeded counter-based generator, device-side)", "impl": "b200",
-            "config": {"workload": WORKLOAD_DESC, "n": w.n, "r": w.r, "block": w.block, "operand_bytes": w.n * w.n * 8,
-                       "l2": "not flushed: operand 134 MB > 126 MB L2, streamed evict-first; ncu --cache-control "
-                             "none shows 135.5 MB DRAM read per pass in the steady loop",
+            "config": {"workload": workload_desc(args.workload), "n": w.n, "r": w.r, "block": w.block,
+                       "operand_bytes": w.n * w.n * (8 if w.dtype == "f64" else 4),
+                       "l2": f"not flushed: operand {w.n * w.n * (8 if w.dtype == 'f64' else 4) / 1e6:.0f} MB > 126 MB L2, "
+                             "streamed evict-first" + ("; ncu --cache-control none shows 135.5 MB DRAM read per pass "
+                                                       "in the steady loop" if args.workload == "cfg2" else ""),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "roofline": roofline,
             "cpu_baseline": cpu,
