@@ -1620,7 +1620,9 @@ int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_ho
     // pass stages its rows once: no upload on the stream's critical path); otherwise it is
     // uploaded as one block (a pitched copy of 8r-byte rows is n tiny DMA rows)
     double* v_mapped = nullptr;
-    if (x_host->ldv == r && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
+    // (small factors only: a large one is not staged by the fused kernel and would be re-read
+    // over the host link)
+    if (x_host->ldv == r && n * r * (int64_t)sizeof(double) <= (2 << 20) && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&v_mapped), const_cast<double*>(x_host->V), 0) !=
             cudaSuccess) {
       cudaGetLastError();
