@@ -185,3 +185,44 @@ def test_qmi_container_matches_reference_bytes(tmp_path):
     cut.write_bytes(open(path, "rb").read()[:-8])
     with pytest.raises(ValueError):
         pin.load_quad_meas(str(cut))
+
+
+def test_quad_meas_instance_generator_matches_oracle():
+    """The product-side instance generator (inputs.quad_meas_instance) draws exactly the oracle's
+    (= the reference's) instance: same numpy draws in the same order."""
+    import numpy as np
+
+    from oracle import qm as oq
+    from paper_2012_10469_b200 import inputs as pin
+
+    for n, r, seed in ((20, 1, 0), (30, 3, 5)):
+        a, b, y, tau = pin.quad_meas_instance(n, r, seed=seed)
+        inst = oq.generate_instance(n, r, seed=seed)
+        assert np.array_equal(a, inst.a) and np.array_equal(b, inst.b) and np.array_equal(y, inst.y)
+        assert tau == inst.tau
+
+
+def test_emit_metrics_csv_format(tmp_path):
+    """SPEC harness emit_metrics: exact header, empty cells for absent fields, 17-digit round trip,
+    summary as trailing comments; an empty record gives header + summary only."""
+    import csv
+
+    import numpy as np
+
+    from paper_2012_10469_b200 import driver
+
+    rows = [{"t": 1, "f_value": 0.1 + 0.2, "eps_t": 1e-3 / 3, "eta_t": 0.5, "cert_cheap_lhs": -np.inf,
+             "cert_cheap_holds": 1, "cert_full_lhs": None, "cert_full_holds": None, "bregman_to_exact": None,
+             "lambda_rsp1": 2.0 / 3.0, "elapsed_ns": 12345}]
+    run = driver.RecoveryRun(iterate=None, rows=rows, summary={"T": 1, "dual_gap": 1.0 / 7.0})
+    path = tmp_path / "r.csv"
+    driver.emit_metrics(run, str(path))
+    lines = path.read_text().splitlines()
+    assert lines[0] == driver.RUN_CSV_HEADER
+    row = next(csv.DictReader(lines[:2]))
+    assert float(row["f_value"]) == 0.1 + 0.2 and float(row["eps_t"]) == 1e-3 / 3
+    assert row["cert_cheap_lhs"] == "-inf" and row["cert_full_lhs"] == "" and row["elapsed_ns"] == "12345"
+    assert lines[2:] == ["# T = 1", f"# dual_gap = {1.0 / 7.0!r}"]
+    empty = tmp_path / "e.csv"
+    driver.emit_metrics(driver.RecoveryRun(iterate=None, rows=[], summary={"T": 0}), str(empty))
+    assert empty.read_text().splitlines() == [driver.RUN_CSV_HEADER, "# T = 0"]
