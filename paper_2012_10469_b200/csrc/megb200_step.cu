@@ -261,11 +261,11 @@ __device__ bool rr_small_neardiag(const double* __restrict__ Hg, int64_t ldh, in
       Zp = Z;
     }
     double* Vn = (Zp == Y) ? Z : Y;
-    // Tm = H Zp, Vn = V Zp
+    // Tm = H Zp, Vn = V Zp (V is still the identity in the first pre-step: Vn = Zp)
     for (int idx = t; idx < mm; idx += NT) {
       const int i = idx / m, j = idx - i * m;
       Tm[idx] = jdot(H, i * m, 1, Zp, j, m, m);
-      Vn[idx] = jdot(V, i * m, 1, Zp, j, m, m);
+      Vn[idx] = pre == 0 ? Zp[idx] : jdot(V, i * m, 1, Zp, j, m, m);
     }
     __syncthreads();
     // H <- Zp^T Tm (upper triangle, mirrored)
