@@ -28,7 +28,7 @@ namespace {
 
 constexpr int kQmTile = 32;    // output tile of the gradient
 constexpr int kQmSub = 64;     // measurement rows staged per sub-block
-constexpr int kQmChunk = 512;  // measurement rows per split-K chunk
+constexpr int kQmChunkMax = 512;  // measurement rows per split-K chunk (fewer when the grid would be small)
 
 template <int RB>
 __global__ void __launch_bounds__(256) k_qm_residuals(const double* __restrict__ a, const double* __restrict__ b,
@@ -78,12 +78,13 @@ __global__ void __launch_bounds__(256) k_qm_residuals(const double* __restrict__
 // rows are the measurements idx[0 .. m) when idx is given (a mini-batch, with repeats), else 0 .. m
 __global__ void __launch_bounds__(256) k_qm_grad_part(const double* __restrict__ a, const double* __restrict__ b,
                                                       const double* __restrict__ res, int64_t m, int64_t n,
-                                                      const int64_t* __restrict__ idx, double* __restrict__ part) {
+                                                      const int64_t* __restrict__ idx, int chunk,
+                                                      double* __restrict__ part) {
   __shared__ double As[kQmSub][kQmTile + 1];
   __shared__ double Bs[kQmSub][kQmTile + 1];
   const int i0 = blockIdx.x * kQmTile, j0 = blockIdx.y * kQmTile;
-  const int64_t l0 = (int64_t)blockIdx.z * kQmChunk;
-  const int64_t l1 = min(m, l0 + kQmChunk);
+  const int64_t l0 = (int64_t)blockIdx.z * chunk;
+  const int64_t l1 = min(m, l0 + chunk);
   const int t = threadIdx.x;
   const int tp = t / 8, tq = (t % 8) * 4;  // outputs (tp, tq .. tq+3)
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -157,13 +158,25 @@ void qm_residuals(const Launch& L, const double* a, const double* b, const doubl
   ++*L.counter;
 }
 
-int64_t qm_grad_part_doubles(int64_t m, int64_t n) { return ((m + kQmChunk - 1) / kQmChunk) * n * n; }
+// split-K chunk: 512 measurements, halved (down to 64) until the grid covers ~2 waves of 148 SMs
+int qm_chunk(int64_t m, int64_t n) {
+  const int64_t tiles = ((n + kQmTile - 1) / kQmTile) * ((n + kQmTile - 1) / kQmTile);
+  int chunk = kQmChunkMax;
+  while (chunk > kQmSub && tiles * ((m + chunk - 1) / chunk) < 296) chunk /= 2;
+  return chunk;
+}
+
+int64_t qm_grad_part_doubles(int64_t m, int64_t n) {
+  const int chunk = qm_chunk(m, n);
+  return ((m + chunk - 1) / chunk) * n * n;
+}
 
 void qm_gradient(const Launch& L, const double* a, const double* b, const double* res, int64_t m, int64_t n,
                  double weight, double* G, int64_t ldg, double* part, const int64_t* idx) {
-  const int chunks = (int)((m + kQmChunk - 1) / kQmChunk);
+  const int chunk = qm_chunk(m, n);
+  const int chunks = (int)((m + chunk - 1) / chunk);
   const dim3 grid((unsigned)((n + kQmTile - 1) / kQmTile), (unsigned)((n + kQmTile - 1) / kQmTile), (unsigned)chunks);
-  k_qm_grad_part<<<grid, 256, 0, L.stream>>>(a, b, res, m, n, idx, part);
+  k_qm_grad_part<<<grid, 256, 0, L.stream>>>(a, b, res, m, n, idx, chunk, part);
   MEG_LAUNCHED();
   k_qm_grad_reduce<<<(unsigned)((n * n + 255) / 256), 256, 0, L.stream>>>(part, chunks, n, weight, G, ldg);
   MEG_LAUNCHED();
