@@ -402,7 +402,11 @@ EigShape eig_shape(const megb200_solver* s, int nreq, const EigParams& P) {
   // small problems (n <= the Rayleigh-Ritz limit): let the basis grow to span R^n instead of
   // restarting -- a full basis converges by the basis.shape[1] >= n rule (linalg.py:215) with one
   // wide Rayleigh-Ritz, where restarted cycles near the bulk edge take tens of passes
-  if (!exhaust && n <= s->max_basis && P.basis <= 0) mmax = (int)n;
+  if (!exhaust && n <= s->max_basis && P.basis <= 0) {
+    mmax = (int)n;
+    // and a wider default block: four passes span R^n (each pass is latency-bound at this size)
+    if (P.block <= 0) bw = std::min<int>(std::max<int>(bw, (int)((n + 3) / 4)), std::min(32, s->max_block));
+  }
   mmax = (int)std::min<int64_t>(mmax, n);
   // even block widths and column offsets keep every block 16-byte aligned for the TMA pass
   if (!exhaust && (bw & 1) && bw < s->max_block && bw + 1 + nreq <= mmax) bw += 1;
