@@ -179,6 +179,7 @@ struct FusedPassArgs {
   double* vgram = nullptr;  // optional out: Gram of the first nvg columns of L (phase 0 only)
   int nvg = 0;
   bool stage_l = true;  // set by fused_first_pass: L rows staged in shared memory
+  bool cooperative = false;  // launch cooperatively (more than one solver handle alive)
   int lam_inline_n = 0;   // > 0: lc's kept weights passed by value (lam_inline), lc.lam not read
   double lam_inline[64] = {};
 };

@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <functional>
@@ -23,6 +24,9 @@ using namespace megb200;
 namespace {
 
 thread_local std::string g_last_error;
+// live solver handles: with more than one, fused first passes launch cooperatively (handles may
+// drive different streams, and concurrent spin-waiting grids must not share the SMs)
+std::atomic<int> g_live_solvers{0};
 
 constexpr int kMaxBlock = 64;
 constexpr int kMaxBasis = 112;  // Jacobi Rayleigh-Ritz keeps H and S in shared memory
@@ -528,6 +532,8 @@ int fused_pass(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu,
   a.part2 = s->red + kFusedPart2;
   a.Ews = s->E;
   a.sync = s->fsync;
+  static const bool coop_env = getenv("MEGB200_COOPERATIVE") != nullptr;
+  a.cooperative = coop_env || g_live_solvers.load() > 1;
   if (++s->epoch == 0) ++s->epoch;
   a.epoch = s->epoch;
   a.pack = s->pack;
@@ -1088,11 +1094,13 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
       throw Error(MEGB200_ERR_CUDA, "sync flag allocation failed");
     }
     *out = s;
+    g_live_solvers.fetch_add(1);
   });
 }
 
 void megb200_solver_destroy(megb200_solver* s) {
   if (!s) return;
+  g_live_solvers.fetch_sub(1);
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   cudaFree(s->arena);

@@ -652,16 +652,23 @@ void launch_fused(const Launch& L, const FusedPassArgs& a, int G, size_t smem) {
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = L.stream;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   int na = 1;
+  if (a.cooperative) {
+    // the driver guarantees that all CTAs are co-resident (the tickets and release flags rely on
+    // it) also against fused kernels of other solver handles that may run on other streams
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
   if (CL) {
-    at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = kGroup;
-    at[1].val.clusterDim.y = 1;
-    at[1].val.clusterDim.z = 1;
-    na = 2;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = kGroup;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
