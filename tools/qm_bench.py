@@ -30,11 +30,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=5.0)
+    ap.add_argument("--sizes", default="100x1,100x5,100x20", help="comma-separated n x r list")
+    ap.add_argument("--split", action="store_true", help="also time gradient and step separately (host clock)")
     args = ap.parse_args()
     from oracle import cpu_meg as om  # CPU comparison leg only
     from oracle import qm as oq
 
-    for n, r in ((100, 1), (100, 5), (100, 20)):
+    for n, r in (tuple(int(v) for v in nr.split("x")) for nr in args.sizes.split(",")):
         a, b, y, tau = inputs.quad_meas_instance(n, r, seed=0)
         obj = pb.QuadMeasObjective(a, b, y, tau)
         eta = 1.0 / pb.QuadMeasObjective.preset_beta(n, r)
@@ -54,6 +56,19 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         gpu = args.steps / (e0.elapsed_time(e1) / 1e3)
+        split = {}
+        if args.split:
+            tg = ts = 0.0
+            for t in range(5 + args.steps, 5 + 2 * args.steps):
+                h0 = time.perf_counter()
+                op = obj.grad_operator(x)
+                torch.cuda.synchronize()
+                h1 = time.perf_counter()
+                x = pb.lowrank_meg_step(x, op, eta, eps(t + 1), svd_seed=t).iterate
+                torch.cuda.synchronize()
+                h2 = time.perf_counter()
+                tg, ts = tg + h1 - h0, ts + h2 - h1
+            split = {"grad_ms": round(1e3 * tg / args.steps, 4), "step_ms": round(1e3 * ts / args.steps, 4)}
         inst = oq.generate_instance(n, r, seed=0)
         ox = om.warm_start_wrap(q, np.full(r, 1.0 / r), eps(0))
         done, t0 = 0, time.perf_counter()
@@ -64,7 +79,7 @@ def main():
         cpu = done / (time.perf_counter() - t0)
         print(json.dumps({"n": n, "r": r, "m": 20 * n * r, "gpu_it_per_s": round(gpu, 1),
                           "passes_per_step": passes / args.steps, "cpu_port_it_per_s": round(cpu, 2),
-                          "cpu_cores": len(os.sched_getaffinity(0))}), flush=True)
+                          "cpu_cores": len(os.sched_getaffinity(0)), **split}), flush=True)
 
 
 if __name__ == "__main__":
