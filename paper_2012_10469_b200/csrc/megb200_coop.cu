@@ -132,21 +132,60 @@ __device__ __forceinline__ double warp_sum_partials(const double* __restrict__ p
   return s;
 }
 
+// Small grids (n <= 16 kRC rows): a thread per output sums the G partials with the xor tree
+// warp_sum_partials applies across lanes (lanes >= G hold zeros), so the sum is the same; a warp
+// per output leaves only G * 8 warps for up to 3.6k outputs there, a chain of dependent
+// global-load round trips (80 us of k_coop_orth's CGS reduction at n = 100)
+constexpr int kThreadSumG = 16;
+
+__device__ __forceinline__ double thread_sum_partials(const double* __restrict__ part, int G, int64_t stride, int o) {
+  double w[kThreadSumG];
+#pragma unroll
+  for (int g = 0; g < kThreadSumG; ++g) w[g] = g < G ? part[(int64_t)g * stride + o] : 0.0;
+#pragma unroll
+  for (int off = kThreadSumG / 2; off >= 1; off >>= 1)
+#pragma unroll
+    for (int i = 0; i < off; ++i) w[i] += w[i + off];
+  return w[0];
+}
+
+struct PartRef {
+  const double* p;
+  int64_t stride;
+  int o;
+};
+
+// emit(o, sum over the grid's partials of output o) for o in [0, nout); ref(o) locates the partials
+template <typename Ref, typename Emit>
+__device__ __forceinline__ void grid_reduce_outputs(int nout, Ref&& ref, Emit&& emit) {
+  const int G = gridDim.x;
+  if (G <= kThreadSumG) {
+    #pragma unroll 1
+    for (int o = blockIdx.x * kCT + threadIdx.x; o < nout; o += G * kCT) {
+      const PartRef r = ref(o);
+      emit(o, thread_sum_partials(r.p, G, r.stride, r.o));
+    }
+  } else {
+    const int wpb = kCT / 32;
+    #pragma unroll 1
+    for (int o = blockIdx.x * wpb + (threadIdx.x >> 5); o < nout; o += G * wpb) {
+      const PartRef r = ref(o);
+      const double v = warp_sum_partials(r.p, G, r.stride, r.o);
+      if ((threadIdx.x & 31) == 0) emit(o, v);
+    }
+  }
+}
+
 __device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int pq, int q,
                                                 double* __restrict__ C, int64_t ldc,
                                                 const double* __restrict__ rowscale, double scale) {
-  const int G = gridDim.x;
-  const int wpb = kCT / 32;
-  const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
-  #pragma unroll 1
-  for (int o = gw; o < pq; o += G * wpb) {
-    double s = warp_sum_partials(part, G, pq, o);
-    if ((threadIdx.x & 31) == 0) {
-      const int a = o / q, c = o - a * q;
-      if (rowscale) s *= rowscale[a];
-      C[(int64_t)a * ldc + c] = scale * s;
-    }
-  }
+  grid_reduce_outputs(
+      pq, [&](int o) { return PartRef{part, pq, o}; },
+      [&](int o, double s) {
+        const int a = o / q, c = o - a * q;
+        if (rowscale) s *= rowscale[a];
+        C[(int64_t)a * ldc + c] = scale * s;
+      });
 }
 
 // ---------------------------------------------------------------------------
@@ -489,8 +528,6 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
   __syncthreads();
   phase_mark(51);
   int pm = 52;
-  const int wpb = kCT / 32;
-  const int gw = blockIdx.x * wpb + (t >> 5);
   auto cgs = [&]() {
     const int pq = cols * q;
     // C partial = Qs^T Ws: a thread owns four basis columns a0..a0+3 of one block column c
@@ -512,10 +549,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
     }
     phase_mark(pm++);
     grid.sync();
-    for (int o = gw; o < pq; o += gridDim.x * wpb) {
-      const double v = warp_sum_partials(part, gridDim.x, pq, o);
-      if ((t & 31) == 0) Cws[o] = v;
-    }
+    grid_reduce_outputs(pq, [&](int o) { return PartRef{part, pq, o}; }, [&](int o, double v) { Cws[o] = v; });
     grid.sync();
     phase_mark(pm++);
     for (int o = t; o < pq; o += kCT) Cs[o] = Cws[o];
@@ -557,10 +591,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
     }
     phase_mark(pm++);
     grid.sync();
-    for (int o = gw; o < qq; o += gridDim.x * wpb) {
-      const double v = warp_sum_partials(part, gridDim.x, qq, o);
-      if ((t & 31) == 0) Gws[o] = v;
-    }
+    grid_reduce_outputs(qq, [&](int o) { return PartRef{part, qq, o}; }, [&](int o, double v) { Gws[o] = v; });
     grid.sync();
     phase_mark(pm++);
     if (blockIdx.x == 0) block_cholesky(Gws, q, thresh, chol_sm, Rrel, Rinv, mask, nullptr, nullptr);
@@ -864,21 +895,16 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
   grid.sync();
   phase_mark(14);
   {
-    // warp-per-output grid reduction of the residual squares and the Gram
-    const int wpb = kCT / 32;
-    const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
-    const int nout = nreq + gr * gr;
-    #pragma unroll 1
-    for (int o = gw; o < nout; o += gridDim.x * wpb) {
-      const double v = o < nreq ? warp_sum_partials(rpart, gridDim.x, nreq, o)
-                                : warp_sum_partials(gpart, gridDim.x, gr * gr, o - nreq);
-      if ((threadIdx.x & 31) == 0) {
-        if (o < nreq)
-          resid[o] = sqrt(v);
-        else
-          Gout[o - nreq] = v;
-      }
-    }
+    // grid reduction of the residual squares and the Gram
+    grid_reduce_outputs(
+        nreq + gr * gr,
+        [&](int o) { return o < nreq ? PartRef{rpart, nreq, o} : PartRef{gpart, gr * gr, o - nreq}; },
+        [&](int o, double v) {
+          if (o < nreq)
+            resid[o] = sqrt(v);
+          else
+            Gout[o - nreq] = v;
+        });
   }
   phase_mark(15);
   if (blockIdx.x == 0 && threadIdx.x < 32 && epi) {

@@ -16,14 +16,27 @@ import config_profile as cp  # noqa: E402
 import paper_2012_10469_b200 as pb  # noqa: E402
 from paper_2012_10469_b200 import configs, driver, inputs, runtime  # noqa: E402
 
-w = configs.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "cfg4"]
-obj, init = cp.objective_for(w)
-tol = 1e-10 if w.dtype == "f64" else pb.objectives.F32_TOL_FLOOR
-x = inputs.initial_iterate(w, init, tol=tol)
-lib = runtime.solver_for(w.n).lib
-lib.megb200_debug_phase_ns.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+which = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 buf = (C.c_ulonglong * 64)()
-r0 = driver.run(x, obj, 3, eta=w.eta0, eta_decay=w.eta_decay, svd_subspace=w.subspace, block=w.block)
+if which.startswith("qm"):  # quadratic measurements, e.g. qm100x5 (n = 100, r = 5)
+    n, r = (int(v) for v in which[2:].split("x"))
+    a, b, y, tau = inputs.quad_meas_instance(n, r, seed=0)
+    obj = pb.QuadMeasObjective(a, b, y, tau)
+    q, _ = np.linalg.qr(np.random.default_rng(1000).standard_normal((n, r)))
+    x = pb.warm_start_wrap(q, np.full(r, 1.0 / r), 0.6 / 121)
+    for t in range(4):
+        x = pb.lowrank_meg_step(x, obj.grad_operator(x), 1.0 / obj.preset_beta(n, r), 0.6 / (t + 12) ** 2,
+                                svd_seed=t).iterate
+    lib = runtime.solver_for(n).lib
+    lib.megb200_debug_phase_ns.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+else:
+    w = configs.WORKLOADS[which]
+    obj, init = cp.objective_for(w)
+    tol = 1e-10 if w.dtype == "f64" else pb.objectives.F32_TOL_FLOOR
+    x = inputs.initial_iterate(w, init, tol=tol)
+    lib = runtime.solver_for(w.n).lib
+    lib.megb200_debug_phase_ns.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+    r0 = driver.run(x, obj, 3, eta=w.eta0, eta_decay=w.eta_decay, svd_subspace=w.subspace, block=w.block)
 lib.megb200_debug_phase_ns(buf, 64)
 v = list(buf)
 pm = int(v[49])
