@@ -8,7 +8,7 @@
 //                    measurement row, coalesced reads of a_i and b_i, fixed
 //                    lane-strided sums + xor trees;
 //   k_qm_grad_part   C_c = a[chunk]^T diag(res[chunk]) b[chunk] per m-chunk and
-//                    32 x 32 output tile (split-K over the measurements, or over a
+//                    64 x 64 output tile (split-K over the measurements, or over a
 //                    mini-batch of measurement indices: StochasticOracle, :235-283);
 //   k_qm_grad_reduce G = weight * (C + C^T) / 2, chunks summed in order
 //                    (tau * _dense_measurement_gradient, objectives.py:155-156,
@@ -26,8 +26,8 @@
 namespace megb200 {
 namespace {
 
-constexpr int kQmTile = 32;    // output tile of the gradient
-constexpr int kQmSub = 64;     // measurement rows staged per sub-block
+constexpr int kQmTile = 64;    // output tile of the gradient
+constexpr int kQmSub = 32;     // measurement rows staged per sub-block
 constexpr int kQmChunkMax = 512;  // measurement rows per split-K chunk (fewer when the grid would be small)
 
 template <int RB>
@@ -75,7 +75,10 @@ __global__ void __launch_bounds__(256) k_qm_residuals(const double* __restrict__
 }
 
 // C_c[p][q] = sum_{l in chunk c} a[l][i0 + p] res[l] b[l][j0 + q]
-// rows are the measurements idx[0 .. m) when idx is given (a mini-batch, with repeats), else 0 .. m
+// rows are the measurements idx[0 .. m) when idx is given (a mini-batch, with repeats), else 0 .. m.
+// 64 x 64 output tile per CTA, a 4 x 4 register tile per thread (rows tp + 16 a, columns tq + 16 u):
+// per staged measurement row a thread reads 4 + 4 shared values for 16 FMAs (conflict-free: the
+// half-warps read the same 16 consecutive B values); each output sums its chunk's rows in order
 __global__ void __launch_bounds__(256) k_qm_grad_part(const double* __restrict__ a, const double* __restrict__ b,
                                                       const double* __restrict__ res, int64_t m, int64_t n,
                                                       const int64_t* __restrict__ idx, int chunk,
@@ -86,8 +89,12 @@ __global__ void __launch_bounds__(256) k_qm_grad_part(const double* __restrict__
   const int64_t l0 = (int64_t)blockIdx.z * chunk;
   const int64_t l1 = min(m, l0 + chunk);
   const int t = threadIdx.x;
-  const int tp = t / 8, tq = (t % 8) * 4;  // outputs (tp, tq .. tq+3)
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int tp = t >> 4, tq = t & 15;
+  double acc[4][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[x][u] = 0.0;
   for (int64_t ls = l0; ls < l1; ls += kQmSub) {
     const int rows = (int)min((int64_t)kQmSub, l1 - ls);
     __syncthreads();
@@ -101,17 +108,26 @@ __global__ void __launch_bounds__(256) k_qm_grad_part(const double* __restrict__
     __syncthreads();
 #pragma unroll 4
     for (int rr = 0; rr < kQmSub; ++rr) {
-      const double x = As[rr][tp];
+      double x[4], z[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fma(x, Bs[rr][tq + u], acc[u]);
+      for (int k = 0; k < 4; ++k) {
+        x[k] = As[rr][tp + 16 * k];
+        z[k] = Bs[rr][tq + 16 * k];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[k][u] = fma(x[k], z[u], acc[k][u]);
     }
   }
   double* out = part + (int64_t)blockIdx.z * n * n;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int p = i0 + tp, q = j0 + tq + u;
-    if (p < n && q < n) out[(int64_t)p * n + q] = acc[u];
-  }
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = i0 + tp + 16 * k, q = j0 + tq + 16 * u;
+      if (p < n && q < n) out[(int64_t)p * n + q] = acc[k][u];
+    }
 }
 
 __global__ void k_qm_grad_reduce(const double* __restrict__ part, int chunks, int64_t n, double weight,
@@ -162,7 +178,7 @@ void qm_residuals(const Launch& L, const double* a, const double* b, const doubl
 int qm_chunk(int64_t m, int64_t n) {
   const int64_t tiles = ((n + kQmTile - 1) / kQmTile) * ((n + kQmTile - 1) / kQmTile);
   int chunk = kQmChunkMax;
-  while (chunk > kQmSub && tiles * ((m + chunk - 1) / chunk) < 296) chunk /= 2;
+  while (chunk > 64 && tiles * ((m + chunk - 1) / chunk) < 296) chunk /= 2;
   return chunk;
 }
 
