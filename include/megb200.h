@@ -239,6 +239,9 @@ typedef struct megb200_schedule {
   double eta0;
   uint64_t minibatch_seed;     /* STOCHASTIC: A_t = N(0,1/n) at stream 5, counter (t n + i) b + j */
   int32_t minibatch_round_f32; /* round A_t through float32 (f32 configs)                         */
+  int32_t cert_every;          /* > 0: dual-gap certificate of X_{t+1} after every step t with      */
+                               /* (t + 1) % cert_every == 0 (_dual_gap_core objectives.py:332-335;  */
+                               /* FROBENIUS only), warm-started from the previous certificate      */
 } megb200_schedule;
 
 typedef struct megb200_run_record { /* host arrays, any may be NULL; row i = step t0 + i */
@@ -257,6 +260,16 @@ typedef struct megb200_run_record { /* host arrays, any may be NULL; row i = ste
   int64_t ritz_cap;
   int64_t ritz_cols;
   double ritz_orth_err;
+  /* optional sub-range timing: when timed_count > 0, CUDA events on the solver stream bracket
+   * steps [timed_from, timed_from + timed_count) inside the loop (the device time of exactly those
+   * steps in the pipelined steady state, the earlier steps being the warm-up);
+   * timed_ms and timed_launches (kernels enqueued for those steps) are written back */
+  int64_t timed_from;
+  int64_t timed_count;
+  double timed_ms;
+  int64_t timed_launches;
+  double* gap;  /* T: dual gap of X_{t+1} at certificate steps, NaN elsewhere (sch->cert_every)       */
+  double* lmin; /* T: lambda_min(grad f(X_{t+1})) at certificate steps, NaN elsewhere                */
 } megb200_run_record;
 
 int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_gradient* g,
@@ -275,6 +288,11 @@ int megb200_certificate_cheap(double lambda_r_plus_1, double b_r_plus_1, double 
  * X is the gradient's (gV, g_lam, g_eps). */
 int megb200_objective_value(megb200_solver* s, const megb200_gradient* g, double m_norm2, double m_trace,
                             double* value);
+
+/* The same value summed entry by entry, 1/2 sum_ij (X_ij - M_ij)^2 with X_ij from the factors
+ * (one pass over M, r FMAs per entry; no cancellation when X -> M, so the value compares
+ * RELATIVELY).  SAMPLED descriptors take the entry sum above.  r <= 64. */
+int megb200_objective_value_direct(megb200_solver* s, const megb200_gradient* g, double* value);
 
 /* ||M||_F^2 and Tr M of a dense symmetric operand. */
 int megb200_dense_stats(megb200_solver* s, const void* M, int32_t dtype, int64_t ld, double* norm2, double* trace);
@@ -314,6 +332,15 @@ int megb200_qm_value(megb200_solver* s, const double* res, int64_t m, double* va
  * allowed; the caller folds tau * m / L into weight). */
 int megb200_qm_gradient_batch(megb200_solver* s, const double* a, const double* b, const double* res,
                               const int64_t* idx, int64_t L, double weight, double* G, int64_t ldg);
+
+/* Synthetic config-3 instance (seeded counter-based twin of oracle/inputs.sampled_instance):
+ * pattern = symmetric Bernoulli(p) over i <= j at counter min*n + max of stream 3, mirrored;
+ * _pattern writes rowptr (n + 1, device int32) and the nonzero count, _values fills col (sorted
+ * per row) and val = (U diag(lam) U^T)_ij + obs_noise N(0,1) (stream 4, same counter). */
+int megb200_gen_sampled_pattern(megb200_solver* s, uint64_t seed, double p, int32_t* rowptr, int64_t* nnz);
+int megb200_gen_sampled_values(megb200_solver* s, uint64_t seed, double p, const double* U, int64_t r,
+                               const double* lam_host, double obs_noise, const int32_t* rowptr, int32_t* col,
+                               double* val);
 
 /* Seeded synthetic inputs (oracle/inputs.py twins):
  *   M_ij = sum_k U_ik lam_k U_jk + sigma (g_ij + g_ji) / (2 sqrt(n)),

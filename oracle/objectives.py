@@ -51,6 +51,26 @@ def frob_value(x, m: np.ndarray, m_norm2: float | None = None, mv: np.ndarray | 
     return 0.5 * (x_norm2 - 2.0 * inner + m_norm2)
 
 
+def x_rows(x, i0: int, i1: int) -> np.ndarray:
+    """Rows i0:i1 of the dense X from its factors (row-chunked densify, meg.py:84-87)."""
+    tail = x.eps / (x.n - x.r)
+    coeff = (1.0 - x.eps) * x.lam - tail
+    rows = (x.V[i0:i1] * coeff) @ x.V.T
+    rows[np.arange(i1 - i0), np.arange(i0, i1)] += tail
+    return rows
+
+
+def frob_value_direct(x, m: np.ndarray, chunk: int = 1024) -> float:
+    """1/2 sum_ij (X_ij - M_ij)^2 summed entry by entry (no cancellation between the
+    1/2(||X||^2 - 2<X,M> + ||M||^2) summands), row chunks of X from the factors."""
+    total = 0.0
+    for i0 in range(0, x.n, chunk):
+        i1 = min(x.n, i0 + chunk)
+        d = x_rows(x, i0, i1) - m[i0:i1]
+        total += float(np.einsum("ij,ij->", d, d))
+    return 0.5 * total
+
+
 class DenseFrobenius:
     """f(X) = 1/2 ||X - M||_F^2; grad f(X) u = X u - M u."""
 
@@ -65,6 +85,9 @@ class DenseFrobenius:
 
     def value(self, x) -> float:
         return frob_value(x, self.m, self.m_norm2)
+
+    def value_direct(self, x) -> float:
+        return frob_value_direct(x, self.m)
 
     def init_apply(self):
         m = self.m
@@ -151,6 +174,8 @@ def run_trajectory(api, cfg: inputs.MegConfig, obj, x0, iters: int, probe_at=(),
     step_kwargs = dict(step_kwargs or {})
     z = probes(cfg.n)
     rec = {k: [] for k in ("shift", "y", "lam", "eps", "lhs", "f")}
+    if hasattr(obj, "value_direct"):
+        rec["f_direct"] = []
     probe = {}
     x = x0
     for t in range(iters):
@@ -165,6 +190,8 @@ def run_trajectory(api, cfg: inputs.MegConfig, obj, x0, iters: int, probe_at=(),
         rec["eps"].append(x.eps)
         rec["lhs"].append(res.cert.lhs_cheap)
         rec["f"].append(obj.value(x))
+        if "f_direct" in rec:
+            rec["f_direct"].append(obj.value_direct(x))
         if t in probe_at:
             probe[t] = x_apply(x, z)
     out = {k: np.asarray(v) for k, v in rec.items()}

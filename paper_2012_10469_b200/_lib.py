@@ -77,6 +77,8 @@ class StepResult(C.Structure):
         ("lhs_cheap", C.c_double), ("holds_cheap", C.c_int32), ("threshold", C.c_double),
         ("gram_err", C.c_double), ("passes", C.c_int32), ("restarts", C.c_int32), ("ritz_cols", C.c_int32),
         ("ritz_orth_err", C.c_double),
+        ("timed_from", C.c_int64), ("timed_count", C.c_int64), ("timed_ms", C.c_double),
+        ("timed_launches", C.c_int64), ("gap", c_double_p), ("lmin", c_double_p),
     ]
 
 
@@ -84,7 +86,7 @@ class Schedule(C.Structure):
     _fields_ = [
         ("eps_kind", C.c_int32), ("eps0_tilde", C.c_double), ("G", C.c_double), ("c", C.c_double),
         ("eta_kind", C.c_int32), ("eta0", C.c_double),
-        ("minibatch_seed", C.c_uint64), ("minibatch_round_f32", C.c_int32),
+        ("minibatch_seed", C.c_uint64), ("minibatch_round_f32", C.c_int32), ("cert_every", C.c_int32),
     ]
 
 
@@ -94,6 +96,8 @@ class RunRecord(C.Structure):
         ("holds", c_int32_p), ("passes", c_int32_p), ("step_ms", c_double_p),
         ("ritz_block", C.c_void_p), ("ld_ritz", C.c_int64), ("ritz_cap", C.c_int64), ("ritz_cols", C.c_int64),
         ("ritz_orth_err", C.c_double),
+        ("timed_from", C.c_int64), ("timed_count", C.c_int64), ("timed_ms", C.c_double),
+        ("timed_launches", C.c_int64), ("gap", c_double_p), ("lmin", c_double_p),
     ]
 
 
@@ -127,6 +131,7 @@ SIGNATURES = [
     ("megb200_certificate_cheap", C.c_int,
      [C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, c_double_p, c_int32_p, c_double_p]),
     ("megb200_objective_value", C.c_int, [C.c_void_p, C.POINTER(Gradient), C.c_double, C.c_double, c_double_p]),
+    ("megb200_objective_value_direct", C.c_int, [C.c_void_p, C.POINTER(Gradient), c_double_p]),
     ("megb200_dense_stats", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, c_double_p, c_double_p]),
     ("megb200_dual_gap", C.c_int,
      [C.c_void_p, C.POINTER(Gradient), C.POINTER(EigOpts), C.c_double, c_double_p, c_double_p]),
@@ -144,6 +149,10 @@ SIGNATURES = [
     ("megb200_gen_dense_target", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_int64, c_double_p, C.c_double, C.c_uint64, C.c_int32, C.c_void_p, C.c_int32,
       C.c_int64]),
+    ("megb200_gen_sampled_pattern", C.c_int, [C.c_void_p, C.c_uint64, C.c_double, C.c_void_p, C.POINTER(C.c_int64)]),
+    ("megb200_gen_sampled_values", C.c_int,
+     [C.c_void_p, C.c_uint64, C.c_double, C.c_void_p, C.c_int64, c_double_p, C.c_double, C.c_void_p, C.c_void_p,
+      C.c_void_p]),
     ("megb200_gen_gaussian", C.c_int,
      [C.c_void_p, C.c_uint64, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int32, C.c_void_p,
       C.c_int64]),

@@ -96,6 +96,13 @@ void dense_stats(const Launch& L, const void* M, int dtype, int64_t ld, int64_t 
 void gen_dense_target(const Launch& L, const double* U, int64_t r, const double* lam, double sigma, uint64_t key,
                       void* M, int dtype, int64_t ld, int64_t n);
 void reduce_sum(const Launch& L, const double* part, int slots, int width, double* out);
+// config-3 synthetic sampled instance (twin of oracle/inputs.sampled_instance)
+void sampled_count(const Launch& L, int64_t n, uint64_t kmask, double p, int32_t* counts);
+void sampled_fill(const Launch& L, int64_t n, uint64_t kmask, uint64_t knoise, double p, const double* U, int r,
+                  const double* lam, double obs_noise, const int32_t* rowptr, int32_t* col, double* val);
+// part[g] (g < slots) = partial sums of (X_ij - M_ij)^2, X from (V, coeff, tail); r <= 64
+void frob_direct(const Launch& L, const void* M, int dtype, int64_t ld, int64_t n, const double* V, int64_t ldv, int r,
+                 const double* coeff, double tail, double* part, int slots);
 // H[0:cap, 0:cap] = 0 except H[j][j] = theta[j] for j < k
 void set_diag(const Launch& L, double* H, int cap, int k, const double* theta);
 

@@ -953,6 +953,103 @@ __global__ void __launch_bounds__(256) k_dense_stats(const T* __restrict__ M, in
   }
 }
 
+// 1/2 ||X - M||_F^2 summed entry by entry (no cancellation between ||X||^2, <X, M>, ||M||^2):
+// X_ij = sum_k (V_ik c_k) V_jk + tail [i == j] from the factors.  A CTA owns row blocks of RB rows
+// (blk = blockIdx.x, + gridDim.x, ...); thread j streams M row entries coalesced and holds the
+// RB values of X's column j in registers.  part[blockIdx.x] = the CTA's sum (fixed order).
+template <typename T, int RB>
+__global__ void __launch_bounds__(256) k_frob_direct(const T* __restrict__ M, int64_t ld, int64_t n,
+                                                     const double* __restrict__ V, int64_t ldv, int r,
+                                                     const double* __restrict__ coeff, double tail,
+                                                     double* __restrict__ part) {
+  __shared__ double vc[RB][64];
+  __shared__ double red[8];
+  double acc = 0.0;
+  const int64_t nblk = (n + RB - 1) / RB;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t i0 = blk * RB;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < RB * r; idx += blockDim.x) {
+      const int ii = idx / r, k = idx - ii * r;
+      vc[ii][k] = i0 + ii < n ? V[(i0 + ii) * ldv + k] * coeff[k] : 0.0;
+    }
+    __syncthreads();
+    const int rows = (int)min((int64_t)RB, n - i0);
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      double x[RB];
+#pragma unroll
+      for (int ii = 0; ii < RB; ++ii) x[ii] = 0.0;
+      for (int k = 0; k < r; ++k) {
+        const double v = V[j * ldv + k];
+#pragma unroll
+        for (int ii = 0; ii < RB; ++ii) x[ii] = fma(vc[ii][k], v, x[ii]);
+      }
+#pragma unroll
+      for (int ii = 0; ii < RB; ++ii) {
+        if (ii < rows) {
+          const double d = (x[ii] + (i0 + ii == j ? tail : 0.0)) - (double)M[(i0 + ii) * ld + j];
+          acc = fma(d, d, acc);
+        }
+      }
+    }
+  }
+  for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int w = 0; w < 8; ++w) a += red[w];
+    part[blockIdx.x] = a;
+  }
+}
+
+__device__ __forceinline__ double uniform_dev(uint64_t key, uint64_t ctr) {
+  return (double)(mix64(key + (ctr + 1) * kGolden) >> 11) * kInv53;
+}
+
+// Config-3 sampling pattern (twin of oracle/inputs.sampled_instance): (i, j) is observed iff
+// U[0,1) at the canonical counter min(i,j) * n + max(i,j) of stream 3 is < p -- a symmetric
+// pattern.  One warp per row; columns ascend, so each CSR row comes out sorted.
+__global__ void __launch_bounds__(256) k_sampled_count(int64_t n, uint64_t kmask, double p,
+                                                       int32_t* __restrict__ counts) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  int c = 0;
+  for (int64_t j0 = 0; j0 < n; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const bool hit = j < n && uniform_dev(kmask, (uint64_t)(min(i, j) * n + max(i, j))) < p;
+    c += __popc(__ballot_sync(0xffffffffu, hit));
+  }
+  if (lane == 0) counts[i] = c;
+}
+
+// observed values (U diag(lam) U^T)_ij + obs_noise * N(0,1) at the same canonical counter (stream 4)
+__global__ void __launch_bounds__(256) k_sampled_fill(int64_t n, uint64_t kmask, uint64_t knoise, double p,
+                                                      const double* __restrict__ U, int r,
+                                                      const double* __restrict__ lam, double obs_noise,
+                                                      const int32_t* __restrict__ rowptr, int32_t* __restrict__ col,
+                                                      double* __restrict__ val) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  int64_t pos = rowptr[i];
+  for (int64_t j0 = 0; j0 < n; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const uint64_t ctr = (uint64_t)(min(i, j) * n + max(i, j));
+    const bool hit = j < n && uniform_dev(kmask, ctr) < p;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (hit) {
+      const int64_t at = pos + __popc(m & ((1u << lane) - 1u));
+      double pl = 0.0;
+      for (int k = 0; k < r; ++k) pl = fma(U[i * r + k] * U[j * r + k], lam[k], pl);
+      col[at] = (int32_t)j;
+      val[at] = pl + obs_noise * gauss_dev(knoise, ctr);
+    }
+    pos += __popc(m);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_gen_dense_target(const double* __restrict__ U, int r,
                                                           const double* __restrict__ lam, double sigma, uint64_t key,
@@ -1384,6 +1481,31 @@ void dense_stats(const Launch& L, const void* M, int dtype, int64_t ld, int64_t 
     k_dense_stats<double><<<slots, 256, 0, L.stream>>>(static_cast<const double*>(M), ld, n, part);
   else
     k_dense_stats<float><<<slots, 256, 0, L.stream>>>(static_cast<const float*>(M), ld, n, part);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void frob_direct(const Launch& L, const void* M, int dtype, int64_t ld, int64_t n, const double* V, int64_t ldv, int r,
+                 const double* coeff, double tail, double* part, int slots) {
+  if (dtype == MEGB200_F64)
+    k_frob_direct<double, 8><<<slots, 256, 0, L.stream>>>(static_cast<const double*>(M), ld, n, V, ldv, r, coeff, tail,
+                                                           part);
+  else
+    k_frob_direct<float, 8><<<slots, 256, 0, L.stream>>>(static_cast<const float*>(M), ld, n, V, ldv, r, coeff, tail,
+                                                          part);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void sampled_count(const Launch& L, int64_t n, uint64_t kmask, double p, int32_t* counts) {
+  k_sampled_count<<<cdiv(n * 32, 256), 256, 0, L.stream>>>(n, kmask, p, counts);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void sampled_fill(const Launch& L, int64_t n, uint64_t kmask, uint64_t knoise, double p, const double* U, int r,
+                  const double* lam, double obs_noise, const int32_t* rowptr, int32_t* col, double* val) {
+  k_sampled_fill<<<cdiv(n * 32, 256), 256, 0, L.stream>>>(n, kmask, knoise, p, U, r, lam, obs_noise, rowptr, col, val);
   MEG_LAUNCHED();
   ++*L.counter;
 }

@@ -1285,6 +1285,11 @@ double eta_eval(const megb200_schedule& sc, int64_t t) {
 }
 }  // namespace
 
+namespace {
+void dual_gap_core(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts, double m_trace,
+                   double* gap, double* lambda_min, double* ritz_out, int64_t ld_ritz, int32_t* ritz_cols);
+}
+
 int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_gradient* g,
                     const megb200_schedule* sch, int64_t t0, int64_t T, const megb200_eig_opts* opts,
                     uint64_t flush_bytes, double* V_out, int64_t ld_out, double* lam_out, double* eps_out,
@@ -1299,7 +1304,12 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
     Launch L = s->launch();
     // three slots of (V, Ritz block): step i reads slot i % 3 and writes slot (i + 1) % 3, so a
     // speculatively enqueued step i + 1 never overwrites the inputs of a step i that must re-run
-    if (!s->run_buf) MEG_CUDA(cudaMalloc(&s->run_buf, (size_t)6 * n * 64 * sizeof(double)));
+    // + two slots for the certificate's warm Ritz block (ping-pong)
+    if (!s->run_buf) MEG_CUDA(cudaMalloc(&s->run_buf, (size_t)8 * n * 64 * sizeof(double)));
+    const int cert_every = sch->cert_every;
+    if (cert_every < 0) throw Error(MEGB200_ERR_PARAM, "cert_every must be >= 0");
+    if (cert_every > 0 && g->kind != MEGB200_GRAD_FROBENIUS)
+      throw Error(MEGB200_ERR_PARAM, "the dual-gap certificate cadence needs a Frobenius gradient");
     if (flush_bytes > s->flush_len) {
       if (s->flush_buf) MEG_CUDA(cudaFree(s->flush_buf));
       MEG_CUDA(cudaMalloc(&s->flush_buf, flush_bytes));
@@ -1353,13 +1363,36 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
     } guard{done};
     double* hspec[2] = {s->h_buf + 2 * s->pack_len, s->h_buf + 3 * s->pack_len};
 
+    // sub-range timing (rec->timed_count > 0): events bracket steps [tf, tl]
+    const int64_t tf = (rec && rec->timed_count > 0) ? rec->timed_from : -1;
+    const int64_t tl = tf >= 0 ? tf + rec->timed_count - 1 : -1;
+    if (tf >= 0 && tl >= T) throw Error(MEGB200_ERR_PARAM, "timed steps outside [0, T)");
+    cudaEvent_t tev[2] = {nullptr, nullptr};
+    int64_t tlaunch0 = 0, tlaunch1 = 0;
+    if (tf >= 0)
+      for (auto& e : tev) MEG_CUDA(cudaEventCreate(&e));
+    struct TevGuard {
+      cudaEvent_t* e;
+      ~TevGuard() {
+        if (e[0]) cudaEventDestroy(e[0]);
+        if (e[1]) cudaEventDestroy(e[1]);
+      }
+    } tguard{tev};
     auto begin_step = [&](int64_t i) {
+      if (i == tf) {
+        MEG_CUDA(cudaEventRecord(tev[0], s->stream));
+        tlaunch0 = s->launches;
+      }
       if (!ev.empty()) MEG_CUDA(cudaEventRecord(evf[i], s->stream));
       if (flush_bytes) MEG_CUDA(cudaMemsetAsync(s->flush_buf, (int)(i & 0xff), flush_bytes, s->stream));
       if (!ev.empty()) MEG_CUDA(cudaEventRecord(ev[i].first, s->stream));
     };
     auto end_step = [&](int64_t i) {
       if (!ev.empty()) MEG_CUDA(cudaEventRecord(ev[i].second, s->stream));
+      if (i == tl) {  // re-recorded if step tl re-runs: the event marks its last completion
+        MEG_CUDA(cudaEventRecord(tev[1], s->stream));
+        tlaunch1 = s->launches;
+      }
     };
     auto result_for = [&](int64_t i, megb200_step_result& out) {
       out = megb200_step_result{};
@@ -1390,6 +1423,44 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
       ld_warm = 64;
       warm_orth = out.ritz_orth_err <= 1e-13;
       last_orth = out.ritz_orth_err;
+    };
+    // dual-gap certificate of X_{i+1} after step i when (t0 + i + 1) % cert_every == 0
+    auto cert_due = [&](int64_t i) { return cert_every > 0 && (t0 + i + 1) % cert_every == 0; };
+    double* gapW[2] = {s->run_buf + (int64_t)6 * n * 64, s->run_buf + (int64_t)7 * n * 64};
+    int gap_slot = 0;
+    int32_t gap_cols = 0;
+    double m_trace = NAN;
+    if (rec && (rec->gap || rec->lmin))
+      for (int64_t k = 0; k < T; ++k) {
+        if (rec->gap) rec->gap[k] = NAN;
+        if (rec->lmin) rec->lmin[k] = NAN;
+      }
+    auto certify = [&](int64_t i) {  // after commit(i): (Vb[(i + 1) % 3], lam, eps) is X_{i+1}
+      if (!cert_due(i)) return;
+      if (isnan(m_trace)) {
+        double a = 0.0;
+        const int rc = megb200_dense_stats(s, g->dense, g->dtype, g->ld, &a, &m_trace);
+        if (rc != MEGB200_OK) throw Error(rc, g_last_error);
+      }
+      megb200_gradient gg = *g;
+      gg.gV = Vb[(i + 1) % 3];
+      gg.g_r = r;
+      gg.g_ldv = r;
+      gg.g_lam = lam.data();
+      gg.g_eps = eps;
+      megb200_eig_opts go = o;
+      go.seed = 0;
+      go.warm = gap_cols > 0 ? gapW[gap_slot] : nullptr;
+      go.warm_cols = gap_cols;
+      go.ld_warm = 64;
+      go.warm_orthonormal = 0;
+      double gap = NAN, lmin = NAN;
+      int32_t cols = 0;
+      dual_gap_core(s, &gg, &go, m_trace, &gap, &lmin, gapW[gap_slot ^ 1], 64, &cols);
+      gap_slot ^= 1;
+      gap_cols = cols;
+      if (rec && rec->gap) rec->gap[i] = gap;
+      if (rec && rec->lmin) rec->lmin[i] = lmin;
     };
     auto gradient_for = [&](int64_t i, const double* V) {
       megb200_gradient gg = *g;
@@ -1425,6 +1496,7 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
       step_core(s, &it, &gg, eta, eps_next, &so, &out);
       end_step(i);
       commit(i, out, eps_next);
+      certify(i);
     };
     auto fast_ok = [&]() { return pipe && warm && warm_cols == sh.bw && warm_orth; };
     FastStep fs[2];
@@ -1454,7 +1526,9 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
       }
       // speculate step i + 1 on step i's device outputs (V, Ritz block, kept weights in the pack)
       bool spec = false;
-      if (i + 1 < T) {
+      // no speculation across a certificate: the certificate's solve reuses the solver workspace
+      // (and the device pack the next step's coefficients come from)
+      if (i + 1 < T && !cert_due(i)) {
         const int64_t t1 = t0 + i + 1;
         const double eps1 = eps_eval(*sch, t0 + i + 1);  // eps of iterate i + 1 = eps_next of step i
         const auto h0 = std::chrono::steady_clock::now();
@@ -1480,6 +1554,7 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
       host_wait += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h1).count();
       if (conf) {
         commit(i, out, eps_next);
+        certify(i);
         ++i;
         bool lam_pos = true;
         for (double v : lam) lam_pos = lam_pos && v > 0.0;
@@ -1508,6 +1583,12 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
     if (lam_out) std::copy(lam.begin(), lam.end(), lam_out);
     if (eps_out) *eps_out = eps;
     s->sync();
+    if (tf >= 0) {
+      float ms = 0.f;
+      MEG_CUDA(cudaEventElapsedTime(&ms, tev[0], tev[1]));
+      rec->timed_ms = ms;
+      rec->timed_launches = tlaunch1 - tlaunch0;
+    }
     for (int64_t k = 0; k < (int64_t)ev.size(); ++k) {
       float ms = 0.f, fl = 0.f;
       if (k == 0) {
@@ -1804,6 +1885,34 @@ int megb200_objective_value(megb200_solver* s, const megb200_gradient* g, double
   });
 }
 
+int megb200_objective_value_direct(megb200_solver* s, const megb200_gradient* g, double* value) {
+  return guarded_impl([&] {
+    if (!s || !value) throw Error(MEGB200_ERR_PARAM, "solver/value is NULL");
+    check_gradient(s, g);
+    if (g->kind == MEGB200_GRAD_SAMPLED) {  // the sampled value is already an entry-by-entry sum
+      const int rc = megb200_objective_value(s, g, NAN, NAN, value);
+      if (rc != MEGB200_OK) throw Error(rc, g_last_error);
+      return;
+    }
+    if (g->kind != MEGB200_GRAD_FROBENIUS && g->kind != MEGB200_GRAD_STOCHASTIC)
+      throw Error(MEGB200_ERR_PARAM, "objective value needs a Frobenius or sampled gradient descriptor");
+    const int64_t n = s->n, r = g->g_r;
+    if (r > 64) throw Error(MEGB200_ERR_PARAM, "direct objective value supports r <= 64");
+    Launch L = s->launch();
+    std::vector<double> c;
+    double tail = 0.0;
+    x_coeffs(n, r, g->g_lam, g->g_eps, c, tail);
+    s->h2d(s->small, c.data(), r);
+    const int slots = std::min<int>(s->sm_count * 4, 1024);
+    frob_direct(L, g->dense, g->dtype, g->ld, n, g->gV, g->g_ldv, (int)r, s->small, tail, s->red, slots);
+    reduce_sum(L, s->red, slots, 1, s->small + 64);
+    double h = 0.0;
+    s->d2h(&h, s->small + 64, 1);
+    s->sync();
+    *value = 0.5 * h;
+  });
+}
+
 namespace {
 void dual_gap_core(megb200_solver* s, const megb200_gradient* g, const megb200_eig_opts* opts, double m_trace,
                    double* gap, double* lambda_min, double* ritz_out, int64_t ld_ritz, int32_t* ritz_cols);
@@ -1949,6 +2058,40 @@ int megb200_qm_value(megb200_solver* s, const double* res, int64_t m, double* va
     s->d2h(s->h_buf, s->small, 1);
     s->sync();
     *value = s->h_buf[0];
+  });
+}
+
+int megb200_gen_sampled_pattern(megb200_solver* s, uint64_t seed, double p, int32_t* rowptr, int64_t* nnz) {
+  return guarded_impl([&] {
+    if (!s || !rowptr || !nnz) throw Error(MEGB200_ERR_PARAM, "null argument");
+    if (!(p > 0.0 && p <= 1.0)) throw Error(MEGB200_ERR_PARAM, "sampling probability must lie in (0, 1]");
+    const int64_t n = s->n;
+    sampled_count(s->launch(), n, stream_key(seed, 3), p, rowptr + 1);
+    std::vector<int32_t> c((size_t)n + 1, 0);
+    MEG_CUDA(cudaMemcpyAsync(c.data() + 1, rowptr + 1, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+    s->sync();
+    int64_t acc = 0;
+    for (int64_t i = 0; i <= n; ++i) {
+      acc += c[(size_t)i];
+      if (acc > INT32_MAX) throw Error(MEGB200_ERR_PARAM, "sampled pattern exceeds int32 indices");
+      c[(size_t)i] = (int32_t)acc;
+    }
+    MEG_CUDA(cudaMemcpyAsync(rowptr, c.data(), ((size_t)n + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s->stream));
+    s->sync();
+    *nnz = acc;
+  });
+}
+
+int megb200_gen_sampled_values(megb200_solver* s, uint64_t seed, double p, const double* U, int64_t r,
+                               const double* lam_host, double obs_noise, const int32_t* rowptr, int32_t* col,
+                               double* val) {
+  return guarded_impl([&] {
+    if (!s || !U || !lam_host || !rowptr || !col || !val) throw Error(MEGB200_ERR_PARAM, "null argument");
+    if (r < 0 || r > 64) throw Error(MEGB200_ERR_PARAM, "r must be in [0, 64]");
+    s->h2d(s->small, lam_host, r);
+    sampled_fill(s->launch(), s->n, stream_key(seed, 3), stream_key(seed, 4), p, U, (int)r, s->small, obs_noise, rowptr,
+                 col, val);
+    s->sync();
   });
 }
 

@@ -35,6 +35,10 @@ class RunResult:
     holds: np.ndarray  # (T,) bool
     passes: np.ndarray  # (T,) operand passes per step
     step_ms: np.ndarray  # (T,) device time per step (flush excluded)
+    timed_ms: float = 0.0  # device time of steps [timed_from, timed_from + timed_count) (CUDA events, in loop)
+    timed_launches: int = 0  # kernels enqueued for those steps
+    gap: np.ndarray | None = None  # (T,) dual gap of X_{t+1} at certificate steps, NaN elsewhere
+    lmin: np.ndarray | None = None  # (T,) lambda_min(grad f(X_{t+1})) at certificate steps
 
 
 def _schedule(eps_schedule: EpsilonSchedule, eta, eta_decay: bool, objective) -> _lib.Schedule:
@@ -68,10 +72,19 @@ def run(
     block: int | None = None,
     flush_bytes: int = 0,
     timing: bool = True,
+    timed_from: int = 0,
+    timed_count: int = 0,
+    cert_every: int = 0,
 ) -> RunResult:
     """Run T MEG steps from x0 on `objective` (Frobenius, sampled or stochastic).
 
-    timing=False skips the per-step CUDA events (step_ms is then all zeros)."""
+    timing=False skips the per-step CUDA events (step_ms is then all zeros).  timed_count > 0
+    brackets steps [timed_from, timed_from + timed_count) with CUDA events on the solver stream
+    inside the loop (RunResult.timed_ms): the device time of exactly those steps, the steps
+    before them serving as warm-up of the same pipelined loop.  cert_every > 0 (Frobenius
+    objectives) computes the dual-gap certificate (_dual_gap_core, objectives.py:332-335) of
+    X_{t+1} after every step t with (t + 1) % cert_every == 0, inside the native loop, each
+    solve warm-started from the previous certificate's Ritz block (RunResult.gap / .lmin)."""
     if not isinstance(objective, (FrobeniusObjective, SampledObjective)):
         raise TypeError("run() needs a device objective (FrobeniusObjective, StochasticFrobeniusObjective, "
                         "SampledObjective)")
@@ -85,6 +98,9 @@ def run(
     opts = _eig_opts(max(svd_tol, g.tol_floor), None, 0, svd_subspace, 12, block, None, warm,
                      warm_orthonormal=warm is not None and x0.warm_orth_err <= 1e-13)
     sc = _schedule(eps_schedule, eta, eta_decay, objective)
+    if cert_every < 0:
+        raise ParameterError("cert_every must be >= 0")
+    sc.cert_every = int(cert_every)
     T = int(T)
     out = {k: np.zeros(T) for k in ("shift", "eps", "lhs", "step_ms")}
     out["y"] = np.zeros((T, r + 1))
@@ -96,6 +112,10 @@ def run(
         if k == "step_ms" and not timing:
             continue
         setattr(rec, k, _lib.dptr(out[k]))
+    gap = np.full(T, np.nan)
+    lmin = np.full(T, np.nan)
+    if cert_every:
+        rec.gap, rec.lmin = _lib.dptr(gap), _lib.dptr(lmin)
     rec.holds = holds.ctypes.data_as(_lib.c_int32_p)
     rec.passes = passes.ctypes.data_as(_lib.c_int32_p)
     v_out = torch.empty((n, r), dtype=torch.float64, device=runtime.device())
@@ -103,6 +123,10 @@ def run(
     rec.ritz_block = ritz.data_ptr()
     rec.ld_ritz = ritz.stride(0)
     rec.ritz_cap = ritz.shape[1]
+    if timed_count > 0:
+        if timed_from < 0 or timed_from + timed_count > T:
+            raise ParameterError("timed steps must lie inside [0, T)")
+        rec.timed_from, rec.timed_count = int(timed_from), int(timed_count)
     lam_out = np.zeros(r)
     eps_out = C.c_double()
     runtime.check(s.lib.megb200_meg_run(s.handle, C.byref(xs), C.byref(gs), C.byref(sc), int(t0), T, C.byref(opts),
@@ -111,7 +135,9 @@ def run(
     # the final iterate carries the warm Ritz block, so a later run or step continues warm
     x = (LowRankIterate(n, r, v_out, lam_out, eps_out.value, warm_block=ritz[:, : rec.ritz_cols],
                         warm_orth_err=rec.ritz_orth_err) if T > 0 else x0)
-    return RunResult(iterate=x, holds=holds.astype(bool), passes=passes, **out)
+    return RunResult(iterate=x, holds=holds.astype(bool), passes=passes, timed_ms=rec.timed_ms,
+                     timed_launches=rec.timed_launches, gap=gap if cert_every else None,
+                     lmin=lmin if cert_every else None, **out)
 
 
 # ---------------------------------------------------------------------------

@@ -40,14 +40,40 @@ def dense_target(w: Workload, U: np.ndarray | None = None) -> torch.Tensor:
     return m
 
 
-def initial_iterate(w: Workload, op_dense: torch.Tensor, tol: float = 1e-10):
-    """Warm start of SURVEY.md 8d step 4: top-r eigenpairs of M (device solver, basis 64),
-    simplex-projected weights floored at 1e-12, warm_start_wrap with eps0 = schedule(0)."""
+def sampled_instance(w: Workload, U: np.ndarray | None = None):
+    """Config 3 in HBM (twin of oracle/inputs.sampled_instance): the symmetric Bernoulli(p)
+    pattern over i <= j (stream 3, canonical counter min(i,j) n + max(i,j)), mirrored, and the
+    observed values (U Lambda U^T)_ij + obs_noise N(0,1) (stream 4).  Returns device tensors
+    (rowptr int32 (n+1), col int32 (nnz) sorted per row, obs f64 (nnz))."""
+    U = planted_factor(w) if U is None else U
+    s = runtime.solver_for(w.n)
+    dev = runtime.device()
+    rowptr = torch.empty(w.n + 1, dtype=torch.int32, device=dev)
+    nnz = C.c_int64()
+    runtime.check(s.lib.megb200_gen_sampled_pattern(s.handle, w.seed, float(w.sample_p), rowptr.data_ptr(),
+                                                    C.byref(nnz)))
+    col = torch.empty(nnz.value, dtype=torch.int32, device=dev)
+    obs = torch.empty(nnz.value, dtype=torch.float64, device=dev)
+    ud = runtime.as_device_f64(U)
+    lam = np.ascontiguousarray(np.asarray(w.spectrum, dtype=np.float64))
+    runtime.check(s.lib.megb200_gen_sampled_values(s.handle, w.seed, float(w.sample_p), ud.data_ptr(), w.r,
+                                                   _lib.dptr(lam), float(w.obs_noise), rowptr.data_ptr(),
+                                                   col.data_ptr(), obs.data_ptr()))
+    return rowptr, col, obs
+
+
+def initial_iterate(w: Workload, op_dense: torch.Tensor | None = None, tol: float = 1e-10, csr=None):
+    """Warm start of SURVEY.md 8d step 4: top-r eigenpairs of M (device solver, basis 64) -- or of
+    (1/p) P_Omega(Mobs) for the sampled config (csr = (rowptr, col, obs)) -- simplex-projected
+    weights floored at 1e-12, warm_start_wrap with eps0 = schedule(0)."""
     from .linalg import SymmetricOperator, lanczos_top_r, project_simplex
     from .meg import warm_start_wrap
 
-    top = lanczos_top_r(SymmetricOperator(w.n, dense=op_dense), w.r, tol=tol, seed=w.seed, subspace=64,
-                        return_device=True)
+    if csr is not None:
+        op = SymmetricOperator(w.n, csr=tuple(csr), scale=1.0 / w.sample_p)
+    else:
+        op = SymmetricOperator(w.n, dense=op_dense)
+    top = lanczos_top_r(op, w.r, tol=tol, seed=w.seed, subspace=64, return_device=True)
     lam = project_simplex(top.eigenvalues, 1.0)
     lam = lam / lam.sum()
     lam = np.maximum(lam, 1e-12)

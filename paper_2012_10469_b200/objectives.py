@@ -154,7 +154,20 @@ class FrobeniusObjective:
         return GradientOperator(_lib.GRAD_FROBENIUS, self.n, dense=self.m, x=x, owner=self)
 
     def value(self, x) -> float:
-        """1/2 ||X - M||_F^2 from the factors: one pass M V."""
+        """1/2 ||X - M||_F^2 summed entry by entry over M with X_ij from the factors
+        (megb200_objective_value_direct): no cancellation as X -> M, so it is exact to
+        rounding RELATIVE to f itself.  One pass over M with r FMAs per entry."""
+        g = self.grad_operator(x)
+        s = g.solver()
+        keep: list = []
+        gs = g.struct(keep)
+        v = C.c_double()
+        runtime.check(s.lib.megb200_objective_value_direct(s.handle, C.byref(gs), C.byref(v)))
+        return v.value
+
+    def value_factored(self, x) -> float:
+        """1/2 (||X||^2 - 2<X, M> + ||M||^2) from the factors: one pass M V.
+        Cheaper (a block pass), but pure cancellation once X -> M (accurate to ~1e-16 ||M||^2)."""
         g = self.grad_operator(x)
         s = g.solver()
         keep: list = []
@@ -197,9 +210,15 @@ class SampledObjective:
     def __init__(self, n: int, rowptr, col, obs):
         dev = runtime.device()
         self.n = int(n)
-        self.rowptr = torch.as_tensor(np.asarray(rowptr, dtype=np.int32)).to(dev)
-        self.col = torch.as_tensor(np.asarray(col, dtype=np.int32)).to(dev)
-        self.obs = runtime.as_device_f64(obs)
+
+        def idx(a):
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                return a.to(torch.int32).contiguous()
+            return torch.as_tensor(np.asarray(a, dtype=np.int32)).to(dev)
+
+        self.rowptr, self.col = idx(rowptr), idx(col)
+        self.obs = (obs.to(torch.float64).contiguous() if isinstance(obs, torch.Tensor) and obs.is_cuda
+                    else runtime.as_device_f64(obs))
         if self.rowptr.numel() != self.n + 1 or self.col.numel() != self.obs.numel():
             raise ParameterError("inconsistent CSR arrays")
 

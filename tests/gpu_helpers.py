@@ -26,6 +26,8 @@ class GpuObjective:
                                                        dtype=cfg.dtype)
         else:
             raise ValueError(cfg.kind)
+        if cfg.kind != "sampled":
+            self.value_direct = self.dev.value  # the device value is the entry-by-entry sum
 
     def grad_apply(self, x, t: int = 0):
         return self.dev.grad_operator(x, t)

@@ -178,8 +178,9 @@ def test_oracle_reproduces_reference_trajectory(name, cfg_name, n):
     assert np.max(np.abs(objectives.x_apply(x0, z) - ref["x0_probe"])) <= 1e-12
     probe_at = [int(k.split("_")[1]) for k in ref if k.startswith("probe_")]
     got, _ = objectives.run_trajectory(om, cfg, obj, x0, iters, probe_at=probe_at)
-    # converged-quantity parity between two valid solvers: <= ~1e-11
-    compare_trajectory(got, ref, tol=1e-10, f_scale=f_scale(obj))
+    # converged-quantity parity between two valid solvers: <= ~1e-11.  f itself (entry
+    # sums) amplifies iterate differences by ~||X|| / ||X - M|| (3e3 on cfg4, where X -> M)
+    compare_trajectory(got, ref, tol=1e-10, f_scale=f_scale(obj), f_direct_tol=1e-9)
 
 
 def test_generator_is_counter_based():
