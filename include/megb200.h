@@ -148,7 +148,10 @@ typedef struct megb200_eig_result {
   int32_t ritz_cols;      /* out: columns written to ritz_block (<= 64)              */
 } megb200_eig_result;
 
-/* Result of one MEG step (LowRankStepResult, meg.py:310-324). */
+/* Result of one MEG step (LowRankStepResult, meg.py:310-324).
+ * Aliasing: V_next and ritz_block may overlap the iterate's V, the gradient's factor or the
+ * warm block (opts->warm) -- the step then writes them only after the solve has converged
+ * (through solver scratch), never while an operand is still being read. */
 typedef struct megb200_step_result {
   double* V_next;         /* (device) n x r, ld = ld_next (caller-allocated)        */
   int64_t ld_next;

@@ -34,9 +34,28 @@ def up_to_date() -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
+    """Each translation unit compiles in parallel (-c), then one shared link; the translation units
+    share no device code, so no device link step is needed."""
     if not force and up_to_date():
         return TARGET
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", TARGET + ".tmp", *SOURCES]
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
+        cmd = [nvcc(), *cflags, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", "-o",
+           TARGET + ".tmp", *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -681,8 +681,8 @@ void coop_tn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, co
   const int J = pick_j(p * q);
 #define MEG_TN(jj)                                                                                      \
   {                                                                                                     \
-    static bool a = false;                                                                              \
-    if (!a) { raise_smem(k_coop_tn<jj>, kCoopSmem); a = true; }                                         \
+    static char a = 0;                                                                              \
+    if (first_on_device(&a)) raise_smem(k_coop_tn<jj>, kCoopSmem);                                         \
     coop_launch(L, k_coop_tn<jj>, G, smem, n, X, ldx, p, Y, ldy, q, C, ldc, rowscale, scale, part);     \
   }
   MEG_J_DISPATCH(J, MEG_TN)
@@ -696,8 +696,8 @@ void coop_cgs(const Launch& L, int64_t n, const double* Q, int64_t ldq, int cols
   const int J = pick_j(cols * q);
 #define MEG_CGS(jj)                                                                              \
   {                                                                                              \
-    static bool a = false;                                                                       \
-    if (!a) { raise_smem(k_coop_cgs<jj>, kCoopSmem); a = true; }                                 \
+    static char a = 0;                                                                       \
+    if (first_on_device(&a)) raise_smem(k_coop_cgs<jj>, kCoopSmem);                                 \
     coop_launch(L, k_coop_cgs<jj>, G, smem, n, Q, ldq, cols, W, ldw, q, Cws, part);              \
   }
   MEG_J_DISPATCH(J, MEG_CGS)
@@ -714,8 +714,8 @@ void coop_cholqr(const Launch& L, int64_t n, const double* Wsrc, int64_t lds, do
   const int J = pick_j(q * q);
 #define MEG_CQR(jj)                                                                                          \
   {                                                                                                          \
-    static bool a = false;                                                                                   \
-    if (!a) { raise_smem(k_coop_cholqr<jj>, kCoopSmem); a = true; }                                          \
+    static char a = 0;                                                                                   \
+    if (first_on_device(&a)) raise_smem(k_coop_cholqr<jj>, kCoopSmem);                                          \
     coop_launch(L, k_coop_cholqr<jj>, G, smem, n, Wsrc, lds, W, ldw, q, thresh, Gws, Rrel, Rinv, mask, Rprev, Rtot, key, \
                 base, part);                                                                                 \
   }
@@ -734,10 +734,9 @@ bool coop_orth(const Launch& L, int64_t n, const double* Q, int64_t ldq, int col
   const size_t smem =
       ((size_t)R * cols + 2 * (size_t)R * q + (size_t)std::max(cols * q, q * q) + 32 + chol_smem) * sizeof(double);
   if (off || q > 32 || q < 1 || smem > 200 * 1024) return false;
-  static bool a = false;
-  if (!a) {
+  static char a = 0;
+  if (first_on_device(&a)) {
     raise_smem(k_coop_orth, 200 * 1024);
-    a = true;
   }
   coop_launch(L, k_coop_orth, G, smem, n, Q, ldq, cols, W, ldw, q, thresh1, key, base, part, Cws, Gws, Rinv, mask,
               Rrel, cgs_rounds);
@@ -756,8 +755,8 @@ void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, 
   const int J2 = Hout ? pick_j(hp * b) : 1;
 #define MEG_FIN2(jj, j2)                                                                                        \
   {                                                                                                             \
-    static bool a = false;                                                                                      \
-    if (!a) { raise_smem(k_coop_finish<jj, j2>, kCoopSmem); a = true; }                                         \
+    static char a = 0;                                                                                      \
+    if (first_on_device(&a)) raise_smem(k_coop_finish<jj, j2>, kCoopSmem);                                         \
     coop_launch(L, k_coop_finish<jj, j2>, G, smem, n, b, S, spart, scale, Lf, ldl, l, d, alpha, U, ldu, W, ldw,  \
                 Ews, part, Qh, ldq, hp, Hout, ldh, lc, Eg, ldg);                                                \
   }
@@ -939,9 +938,10 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
 #pragma unroll
     for (int h = 0; h < 2; ++h)
       if (lane + 32 * h < r) epi[r + 1 + lane + 32 * h] = lam[h] / lsum;
+    // y_{r+1} from the lane that owns pair r (register shuffle: no read of another lane's store)
+    const double lam_rp1 = __shfl_sync(0xffffffffu, (r >> 5) ? y[1] : y[0], r & 31);
     if (lane == 0) {
       double status = !(kept > 1e-290) ? 4.0 : 0.0;
-      const double lam_rp1 = epi[r];
       double lhs;
       if (!(b > 0.0) || lam_rp1 < 0.0) {
         status = 1.0;
@@ -978,8 +978,8 @@ void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta
   const int JG = pick_j(std::max(1, gr * gr));
 #define MEG_RR(jj)                                                                                              \
   {                                                                                                             \
-    static bool a = false;                                                                                      \
-    if (!a) { raise_smem(k_coop_rr<jj>, 215 * 1024); a = true; }                                                \
+    static char a = 0;                                                                                      \
+    if (first_on_device(&a)) raise_smem(k_coop_rr<jj>, 215 * 1024);                                                \
     coop_launch(L, k_coop_rr<jj>, G, smem, H, ldh, m, theta, S, info_arg, n, Q, AQ, ldq, rq, nreq, T, ldt, resid, \
                 part, gr, Gout, eps_next, epi, V2, ld2, r2);                                                    \
   }

@@ -54,6 +54,11 @@ constexpr int kStreamRefill = 12;  // breakdown replacement directions
 // launch wrappers (megb200_kernels.cu).  All tall-skinny arrays are float64
 // row-major with explicit leading dimensions.
 
+// True the first time it is called for (current device, tag), thread-safe: per-device one-time
+// setup such as cudaFuncSetAttribute(MaxDynamicSharedMemorySize), which is a per-device function
+// attribute (a process-wide flag would skip it on a second device).
+bool first_on_device(const void* tag);
+
 struct Launch {
   cudaStream_t stream;
   int64_t* counter;  // kernels launched (telemetry for bench.py)
@@ -160,6 +165,8 @@ struct FusedPassArgs {
   LamCoef lc;
   const double* Eg = nullptr;  // precomputed L^T U (l x b, ld ldg) or null
   int64_t ldg = 0;
+  const double* Gu = nullptr;  // U^T U (b x b, ld ldgu): k_dense_step_mma forms H = U^T W from it
+  int64_t ldgu = 0;
   const double* U = nullptr;
   int64_t ldu = 0;
   double* W = nullptr;
@@ -192,6 +199,18 @@ struct FusedPassArgs {
 };
 bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count);
 void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count);
+
+// The float64 dense pass and the step tail above in ONE cooperative launch (megb200_kernels.cu,
+// k_dense_step_mma); needs a.Eg when a.l > 0, a.rq == b, a.gr <= b, no vgram, a.sync with >= 512
+// zeroed words.  part: the pass's partial slots (part_cap_slices x n x b).
+bool dense_step_mma_supported(const void* M, int dtype, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                              int l, int64_t part_cap_slices, int sm_count);
+void dense_step_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                    double* part, int64_t part_cap_slices, int sm_count, const FusedPassArgs& a);
+// E = L^T U (l x b, ld b), vgram = L^T L (nvg x nvg) and Gu = U^T U (b x b) over 128-row tiles, the
+// step tail's Gram product order; part: tiles x kFusedStride doubles; ticket: one zeroed word
+void tile_gram(const Launch& L, int64_t n, const double* Lm, int64_t ldl, int l, const double* U, int64_t ldu, int b,
+               int nvg, double* part, unsigned* ticket, double* E, double* vgram, double* Gu);
 
 // quadratic-measurement objective (megb200_qm.cu)
 struct QmCoef {

@@ -19,6 +19,7 @@
 
 #include "megb200_internal.h"
 #include "megb200_jacobi.cuh"
+#include "megb200_tail.cuh"
 
 namespace megb200 {
 namespace {
@@ -508,16 +509,41 @@ constexpr size_t mma_smem_bytes() {
 // so k = 18 costs 2 DMMA n-tiles + 2 DFMA columns instead of 3 padded n-tiles.
 // CW consumer warps: 8 (warp w owns rows [16w, 16w+16), two m-tiles) or 16 (warp w owns one
 // 8-row m-tile: rows [8w, 8w+8); twice the warps per SMSP to hide fragment-load latency)
-template <int NT, int TAIL, int CW>
-__global__ void __launch_bounds__(32 * (CW + 1), 1)
-    k_dense_pass_mma(const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmU, int64_t n,
-                     int b, double* __restrict__ part, int tiles, int kch, int smax) {
-  // Stream-K: the (row tile, 32-row k chunk) space, tile-major, is cut into
-  // gridDim.x contiguous ranges of equal length (+-1 chunk), so every CTA
-  // streams the same number of operand bytes.  A CTA flushes one partial per
-  // tile segment it covers, into slot (its index - the index of the first CTA
-  // on that tile); the CTA that closes a tile zero-fills the tile's unused
-  // slots, so the epilogue sums exactly smax slots per row.
+//
+// Stream-K: the (row tile, 32-row k chunk) space, tile-major, is cut into
+// gridDim.x contiguous ranges of equal length (+-1 chunk), so every CTA
+// streams the same number of operand bytes.  A CTA flushes one partial per
+// tile segment it covers, into slot (its index - the index of the first CTA
+// on that tile).  Pass only (STEP = false): the CTA that closes a tile zero-fills
+// the tile's unused slots, so the consumer of `part` sums exactly smax slots per row.
+// Fused step (STEP = true): every contributor bumps the tile's counter after its
+// partial is visible; the last one records the tile in `fixlist` (it finishes the
+// tile after its own range, k_dense_step_mma).  The producer warp falls through
+// instead of returning when STEP, so the whole CTA can run the step tail.
+__host__ __device__ __forceinline__ int sk_cfirst(int64_t x, int G, int64_t utot) {
+  // the first CTA whose range contains unit x: the largest c with c * utot / G <= x
+  return (int)(((x + 1) * G + utot - 1) / utot) - 1;
+}
+
+// STEP extras after the ring: U rows of the current tile (prefetched with cp.async when a tile
+// segment starts) and the segment's W rows, for the segment's H partial U_tile^T W_segment
+template <int NT, int TAIL>
+__host__ __device__ constexpr size_t mma_step_extra_offset() {
+  // the ring (operand + U stages) and its mbarriers, rounded up
+  return (((size_t)kPipeStages * kPipeKC * kMmaRows * 8 + (size_t)kPipeStages * kPipeKC * mma_bnp<NT, TAIL>() * 8 +
+           2 * kPipeStages * 8 + 127) / 128) * 128;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(pipe::su32(dst)), "l"(src) : "memory");
+}
+
+template <int NT, int TAIL, int CW, bool STEP>
+__device__ __forceinline__ void dense_mma_body(const CUtensorMap* tmM, const CUtensorMap* tmU, int64_t n, int b,
+                                               double* __restrict__ part, int tiles, int kch, int smax,
+                                               unsigned char* base, unsigned* tilecnt, int* fixlist, int* nfix,
+                                               const double* __restrict__ Ug = nullptr, int64_t ldu = 0,
+                                               double* __restrict__ hpart = nullptr) {
   const int64_t utot = (int64_t)tiles * kch;
   const int64_t ua = (int64_t)blockIdx.x * utot / gridDim.x, ub = (int64_t)(blockIdx.x + 1) * utot / gridDim.x;
   // Operand stage = 8 TMA boxes of 16 (i) x 32 (k) doubles with the 128-byte
@@ -528,8 +554,6 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1)
   // disjoint bank quarters (B) -- both fragment loads at the 2-wavefront minimum.
   constexpr int BNP = mma_bnp<NT, TAIL>();
   constexpr int TL = TAIL > 0 ? TAIL : 1;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* base = smem + ((1024 - ((uintptr_t)smem & 1023)) & 1023);
   double* Ms = reinterpret_cast<double*>(base);                      // stages x 8 boxes x 512 doubles
   double* Us = Ms + (size_t)kPipeStages * kPipeKC * kMmaRows;         // stages x KC x BNP
   uint64_t* full = reinterpret_cast<uint64_t*>(Us + (size_t)kPipeStages * kPipeKC * BNP);
@@ -541,8 +565,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1)
       pipe::bar_init(empty + st, CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmM) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmM) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmU) : "memory");
   }
   __syncthreads();
   // launched programmatically dependent on the previous kernel: everything above
@@ -563,8 +587,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1)
           double* mst = Ms + (size_t)st * kPipeKC * kMmaRows;
 #pragma unroll
           for (int bx = 0; bx < kMmaRows / 16; ++bx)
-            pipe::tma_2d_stream(mst + bx * 16 * kPipeKC, &tmM, tile * kMmaRows + 16 * bx, (int)kc, full + st, pol);
-          pipe::tma_2d(Us + (size_t)st * kPipeKC * BNP, &tmU, 0, (int)kc, full + st);
+            pipe::tma_2d_stream(mst + bx * 16 * kPipeKC, tmM, tile * kMmaRows + 16 * bx, (int)kc, full + st, pol);
+          pipe::tma_2d(Us + (size_t)st * kPipeKC * BNP, tmU, 0, (int)kc, full + st);
           if (++st == kPipeStages) {
             st = 0;
             ph ^= 1u;
@@ -572,12 +596,15 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1)
         }
       }
     }
-    return;
+    return;  // STEP: the caller's tail starts with a CTA barrier the producer warp joins
   }
   constexpr int MT = 16 / (CW / 8) / 8;  // m-tiles per warp: 2 (CW = 8) or 1 (CW = 16)
   const int mrow0 = (CW == 16) ? 8 * (warp & 1) : 0;  // first row of this warp within its box
   const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
   const int kperm = 2 * tq;  // {0,2,4,6}; +1 for the second MMA of a k group
+  double* Usm = reinterpret_cast<double*>(base + mma_step_extra_offset<NT, TAIL>());  // 128 x b (STEP)
+  double* Wsm = Usm + kMmaRows * b;                                                 // 128 x b (STEP)
+  double hc[2] = {0.0, 0.0};  // STEP: this thread's entries o = tid, tid + 256 of sum_seg U_tile^T W_seg
   int st = 0;
   uint32_t ph = 0;
   for (int64_t u = ua; u < ub;) {
@@ -585,10 +612,18 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1)
     const int64_t i0 = (int64_t)tile * kMmaRows;
     const int64_t uend = min(ub, (int64_t)(tile + 1) * kch);
     const bool closes = uend == (int64_t)(tile + 1) * kch;
-    // first CTA on this tile: the largest c with c * utot / G <= tile * kch
-    const int64_t x = (int64_t)tile * kch;
-    const int cfirst = (int)(((x + 1) * gridDim.x + utot - 1) / utot) - 1;
+    const int cfirst = sk_cfirst((int64_t)tile * kch, gridDim.x, utot);
     const int slot = (int)blockIdx.x - cfirst;
+    const int trows = (int)min((int64_t)kMmaRows, n - i0);
+    if constexpr (STEP) {
+      // the tile's U rows, in flight while the segment streams (16-byte chunks)
+      const int hb = b / 2;
+      for (int q = threadIdx.x; q < trows * hb; q += 32 * CW) {
+        const int rr = q / hb, cc = 2 * (q - rr * hb);
+        cp_async16(Usm + rr * b + cc, Ug + (i0 + rr) * ldu + cc);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     // two accumulator sets (even / odd k steps): dependent DMMAs on one accumulator
     // are 2 * 2 * NT instructions apart, which covers the DMMA latency
     double acc[2][MT][NT][2];
@@ -710,7 +745,53 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1)
         if (tq == 0 && row < n) out[row * b + 8 * NT + tc] = v;
       }
     }
-    if (closes) {
+    if constexpr (STEP) {
+      // the segment's W rows (pass part) to shared memory, next to the prefetched U rows
+      const int rb = (CW == 16) ? warp * 8 : warp * 16;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int rr = rb + mt * 8 + g;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = nt * 8 + 2 * tq;
+          if (c < b) Wsm[rr * b + c] = acc[0][mt][nt][0] + acc[1][mt][nt][0];
+          if (c + 1 < b) Wsm[rr * b + c + 1] = acc[0][mt][nt][1] + acc[1][mt][nt][1];
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+        for (int tc = 0; tc < TAIL; ++tc) {
+          double v = tl[mt][tc];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          if (tq == 0) Wsm[(rb + mt * 8 + g) * b + 8 * NT + tc] = v;
+        }
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      // the partial's global stores visible before the tile counter moves
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * CW) : "memory");
+      // H partial of the segment: U_tile^T W_segment (upper triangle), accumulated in segment order
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int o = threadIdx.x + j * 32 * CW;
+        if (o < b * b) {
+          const int ia = o / b, c = o - ia * b;
+          if (ia <= c) hc[j] += tile_dot(Usm, b, ia, Wsm, b, c, trows);
+        }
+      }
+      if (threadIdx.x == 0) {
+        // tile counter: the contributor that completes it finishes the tile (after its own range)
+        const int clast = sk_cfirst((int64_t)(tile + 1) * kch - 1, gridDim.x, utot);
+        const unsigned cnt = (unsigned)(clast - cfirst + 1);
+        if (atomicAdd(tilecnt + tile, 1u) == cnt - 1) {
+          atomicExch(tilecnt + tile, 0u);
+          fixlist[(*nfix)++] = tile;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * CW) : "memory");  // Usm / Wsm free for the next segment
+    } else if (closes) {
       // zero the tile's slots no CTA covers (rows of this warp)
       for (int sl = slot + 1; sl < smax; ++sl) {
         double* z = part + (int64_t)sl * n * b;
@@ -720,6 +801,395 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1)
         }
       }
     }
+  }
+  if constexpr (STEP) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int o = threadIdx.x + j * 32 * CW;
+      if (o < b * b) hpart[(int64_t)blockIdx.x * kFusedStride + o] = hc[j];
+    }
+  }
+}
+
+template <int NT, int TAIL, int CW>
+__global__ void __launch_bounds__(32 * (CW + 1), 1)
+    k_dense_pass_mma(const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmU, int64_t n,
+                     int b, double* __restrict__ part, int tiles, int kch, int smax) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* base = smem + ((1024 - ((uintptr_t)smem & 1023)) & 1023);
+  dense_mma_body<NT, TAIL, CW, false>(&tmM, &tmU, n, b, part, tiles, kch, smax, base, nullptr, nullptr, nullptr);
+}
+
+// ===========================================================================
+// K1 + step tail in ONE launch (float64 dense operand, block b <= 32): the operand
+// pass above, and -- as the tiles complete -- the whole first-pass finish of the MEG
+// step (what k_fused_first_pass does after a separate pass):
+//   fix-up (the last contributor of each 128-row tile): W = scale * sum_slots part +
+//       L E + alpha U (E = diag(d) Eg, Eg = L^T U given), H_tile = U^T W (upper)
+//   Rayleigh-Ritz (the CTA that fixes the last tile): H = sum over tiles in tile order,
+//       near-diagonal / Jacobi solve (linalg.py:205-211), theta and S released by a flag;
+//       the step epilogue (meg.py:347-356) after the release
+//   phase 2 (CTA c takes tiles c, c + G, ...): Ritz block T = U S and V_next,
+//       residuals ||W s_j - theta_j T_j|| (linalg.py:212-216), Gram of T, per tile
+//   the last phase-2 arrival sums the tile partials in tile order and writes the
+//       result pack (device + mapped host slot).
+// Launched cooperatively (the flag spin needs every CTA resident).  Every reduction runs
+// in a fixed order, so the result is bitwise reproducible; the Gram's tile partials use the
+// same products as k_tile_gram, so L^T U of the next step taken from this Gram equals
+// reducing it again.
+namespace stepsync {  // word offsets in FusedPassArgs::sync
+constexpr int kTileCnt = 256;  // per-tile contributor counters (<= kStepMaxTiles)
+constexpr int kTicketA = 416;  // tiles finished (H partials ready)
+constexpr int kTicketB = 417;  // phase-2 tiles done (+1 from the Rayleigh-Ritz CTA)
+constexpr int kFlag = 418;     // theta / S released (epoch)
+}  // namespace stepsync
+constexpr int kStepMaxTiles = 148;
+constexpr int kStepMaxFix = 16;
+constexpr int kStepMaxTileSlots = 2;  // completed tiles whose U / W rows stay in shared memory
+constexpr int kStepThreads = 32 * 9;
+
+__device__ __forceinline__ void step_publish(unsigned* flag, unsigned epoch) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release_u32(flag, epoch);
+}
+
+__device__ __forceinline__ void step_wait(const unsigned* flag, unsigned epoch) {
+  if (threadIdx.x == 0)
+    while (ld_acquire_u32(flag) != epoch) __nanosleep(32);
+  __syncthreads();
+}
+
+// dA[r * wA + c] = sA[(r0 + r) * ldA + c] (and the same for B, wB = 0 for none), r < rows: eight
+// loads of each source in flight per thread before the stores
+__device__ __forceinline__ void step_stage2(double* dA, const double* __restrict__ sA, int64_t ldA, int wA, double* dB,
+                                            const double* __restrict__ sB, int64_t ldB, int wB, int64_t r0,
+                                            int rows) {
+  const int ta = rows * wA, tb = rows * wB, nt = blockDim.x;
+  for (int base = threadIdx.x; base < max(ta, tb); base += 8 * nt) {
+    double va[8], vb[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int idx = base + j * nt;
+      const int ra = idx / max(wA, 1), ca = idx - ra * max(wA, 1);
+      const int rb = idx / max(wB, 1), cb = idx - rb * max(wB, 1);
+      va[j] = idx < ta ? __ldcg(sA + (r0 + ra) * ldA + ca) : 0.0;
+      vb[j] = idx < tb ? __ldcg(sB + (r0 + rb) * ldB + cb) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int idx = base + j * nt;
+      if (idx < ta) dA[idx] = va[j];
+      if (idx < tb) dB[idx] = vb[j];
+    }
+  }
+}
+
+__device__ __forceinline__ void step_stage(double* dst, const double* __restrict__ src, int64_t ld, int64_t r0,
+                                           int rows, int w) {
+  step_stage2(dst, src, ld, w, nullptr, nullptr, 0, 0, r0, rows);
+}
+
+// diagnostics (MEGB200_FUSED_STAMPS): %globaltimer maxima over CTAs at the tail's phase boundaries
+__device__ __forceinline__ void step_stamp(unsigned long long* st, int slot) {
+  if (st && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    atomicMax(st + slot, v);
+  }
+}
+
+// the last arrival of phase 2: tile partials summed in tile order, result pack out
+__device__ void step_finish_pack(const FusedPassArgs& a, int tiles) {
+  step_stamp(a.stamps, 6);
+  const int pw = a.nreq + a.gr * a.gr;
+  for (int o = threadIdx.x; o < pw; o += blockDim.x) {
+    const double s = tile_ordered_sum<32>(a.part2, tiles, kFusedStride, o);
+    if (o < a.nreq)
+      a.resid[o] = sqrt(s);
+    else
+      a.gram[o - a.nreq] = s;
+  }
+  __threadfence_block();
+  __syncthreads();
+  if (a.host_pack)
+    for (int idx = threadIdx.x; idx < a.pack_count; idx += blockDim.x) a.host_pack[idx] = __ldcg(a.pack + idx);
+  step_stamp(a.stamps, 7);
+}
+
+template <int NT, int TAIL>
+__global__ void __launch_bounds__(kStepThreads, 1)
+    k_dense_step_mma(const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmU, int64_t n,
+                     int b, double* __restrict__ part, int tiles, int kch, int smax,
+                     const __grid_constant__ FusedPassArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* base = smem + ((1024 - ((uintptr_t)smem & 1023)) & 1023);
+  __shared__ int s_fix[kStepMaxFix];
+  __shared__ int s_nfix, s_flag;
+  __shared__ double dsh[kFusedMaxL];
+  __shared__ double thsh[64];
+  if (threadIdx.x == 0) s_nfix = 0;  // ordered before the body's first CTA barrier
+  dense_mma_body<NT, TAIL, 8, true>(&tmM, &tmU, n, b, part, tiles, kch, smax, base, a.sync + stepsync::kTileCnt,
+                                    s_fix, &s_nfix, a.U, a.ldu, a.part1);
+  step_stamp(a.stamps, 0);  // (per CTA) main loop and H partial done
+  const int t = threadIdx.x, NTH = kStepThreads, l = a.l, rq = a.rq, G = gridDim.x;
+  const int64_t utot = (int64_t)tiles * kch;
+  // every CTA's H partial (sum over its segments of U_tile^T W_segment) is in a.part1: the last
+  // CTA to get here forms H and solves the Rayleigh-Ritz problem while the others finish tiles
+  __threadfence();
+  __syncthreads();  // the ring is drained: its shared memory is reused below (the mbarriers are not touched)
+  if (t == 0) {
+    const unsigned old = atomicAdd(a.sync + stepsync::kTicketA, 1u);
+    s_flag = old == (unsigned)G - 1;
+    if (s_flag) atomicExch(a.sync + stepsync::kTicketA, 0u);
+  }
+  const int nfix = s_nfix;  // tiles this CTA completed (<= kStepMaxTileSlots)
+  const bool rr_cta = s_flag != 0;  // (read after the barrier below)
+  for (int k = t; k < l; k += NTH) {  // log-map coefficients: device kept weights (lc) or as given
+    double v;
+    if (a.lc.lam && k < a.lc.lr) {
+      const double kept = a.lc.c1 * (a.lam_inline_n > 0 ? a.lam_inline[k] : __ldcg(a.lc.lam + k));
+      v = (log(kept) - a.lc.log_tail) + (-a.lc.eta * (kept - a.lc.tail_g));
+    } else {
+      v = __ldcg(a.d + k);
+    }
+    dsh[k] = v;
+  }
+  __syncthreads();
+  const bool is_rr = s_flag != 0;
+  (void)rr_cta;
+  if (nfix == 0 && !is_rr) return;
+  const int lb = max(l, b);
+  // shared memory: per completed tile its U and W rows (kept for phase 2), then L | T rows, E, S,
+  // warp partials, H, Rayleigh-Ritz scratch (step_mma_tail_doubles)
+  double* sm = reinterpret_cast<double*>(base);
+  double* Ls = sm + 2 * (size_t)kStepMaxTileSlots * kMmaRows * b;  // 128 x l (fix-up) | T rows 128 x rq (phase 2)
+  double* Ts = Ls;
+  double* Es = Ls + kMmaRows * lb;     // l x b
+  double* Ss = Es + max(l, 1) * b;     // b x rq
+  double* red = Ss + b * rq;           // NTH
+  double* Hs = red + NTH;              // b x b
+  double* jac = Hs + b * b;            // Rayleigh-Ritz scratch
+  auto Uf = [&](int f) { return sm + (size_t)f * 2 * kMmaRows * b; };
+  auto Wf = [&](int f) { return sm + (size_t)f * 2 * kMmaRows * b + kMmaRows * b; };
+
+  if (is_rr) {
+    // ---- Rayleigh-Ritz: H = U^T W = scale sum_CTA H_partial + Eg^T diag(d) Eg + alpha U^T U
+    // (W = scale M U + L diag(d) L^T U + alpha U), CTA partials in CTA order
+    __threadfence();
+    step_stamp(a.stamps, 2);
+    for (int o = t; o < b * b; o += NTH) {
+      const int ia = o / b, c = o - ia * b;
+      double h = 0.0;
+      if (ia <= c) {
+        const double hm = tile_ordered_sum<32>(a.part1, G, kFusedStride, o);
+        double lr = 0.0;
+        for (int k = 0; k < l; ++k) lr = fma(__ldcg(a.Eg + k * a.ldg + ia) * dsh[k], __ldcg(a.Eg + k * a.ldg + c), lr);
+        h = (a.scale * hm + lr) + a.alpha * __ldcg(a.Gu + ia * a.ldgu + c);
+      }
+      Hs[o] = h;
+    }
+    __syncthreads();
+    if (!rr_small_neardiag<kStepThreads>(Hs, b, b, a.theta, a.Sout, jac, thsh, a.info)) {
+      __syncthreads();
+      jacobi_fallback(Hs, b, a.theta, a.Sout, jac, a.info);
+      __syncthreads();
+      for (int c = t; c < b; c += NTH) thsh[c] = a.theta[c];
+      __syncthreads();
+    }
+    step_stamp(a.stamps, 3);
+    step_publish(a.sync + stepsync::kFlag, a.epoch);
+    for (int o = t; o < b * b; o += NTH) {  // H for a continued solve (read after the launch)
+      const int ia = o / b, c = o - ia * b;
+      if (ia <= c) a.H[ia * a.ldh + c] = Hs[o];
+    }
+    if (a.epi && t < 32) step_epilogue_warp(thsh, a.nreq, n, a.eps_next, a.epi);
+    __threadfence();
+    __syncthreads();
+    if (t == 0) {
+      const unsigned old = atomicAdd(a.sync + stepsync::kTicketB, 1u);
+      s_flag = old == (unsigned)tiles;
+      if (s_flag) atomicExch(a.sync + stepsync::kTicketB, 0u);
+    }
+    __syncthreads();
+    if (s_flag) {
+      __threadfence();
+      step_finish_pack(a, tiles);
+    }
+    if (nfix == 0) return;
+  }
+
+  // ---- fix-up: the W rows of each tile this CTA completed (kept in shared memory for phase 2)
+  for (int idx = t; idx < l * b; idx += NTH) {
+    const int k = idx / b, c = idx - k * b;
+    Es[idx] = dsh[k] * __ldcg(a.Eg + k * a.ldg + c);
+  }
+  const int64_t slice = n * b;
+  for (int f = 0; f < nfix; ++f) {
+    const int tile = s_fix[f];
+    const int64_t i0 = (int64_t)tile * kMmaRows;
+    const int rows = (int)min((int64_t)kMmaRows, n - i0);
+    double* Us = Uf(f);
+    double* Ws = Wf(f);
+    step_stage2(Us, a.U, a.ldu, b, Ls, a.L, a.ldl, l, i0, rows);
+    __syncthreads();
+    const int cf = sk_cfirst((int64_t)tile * kch, G, utot);
+    const int cnt = sk_cfirst((int64_t)(tile + 1) * kch - 1, G, utot) - cf + 1;
+    const int total = rows * b;
+    // four outputs per thread per round, every slot load of the four in flight at once
+    for (int base0 = t; base0 < total; base0 += 4 * NTH) {
+      double pv[4][16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int idx = base0 + q * NTH;
+        const bool ok = idx < total;
+        const double* pp = part + i0 * b + (ok ? idx : 0);
+#pragma unroll
+        for (int s2 = 0; s2 < 16; ++s2) pv[q][s2] = (ok && s2 < cnt) ? __ldcg(pp + s2 * slice) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int idx = base0 + q * NTH;
+        if (idx < total) {
+          const int rr = idx / b, c = idx - rr * b;
+          double sum = 0.0;
+#pragma unroll
+          for (int s2 = 0; s2 < 16; ++s2) sum += pv[q][s2];  // slot order
+          const double* Lr = Ls + rr * l;
+          double v0 = a.scale * sum + a.alpha * Us[idx], v1 = 0.0;
+          int k = 0;
+          for (; k + 1 < l; k += 2) {
+            v0 = fma(Lr[k], Es[k * b + c], v0);
+            v1 = fma(Lr[k + 1], Es[(k + 1) * b + c], v1);
+          }
+          if (k < l) v0 = fma(Lr[k], Es[k * b + c], v0);
+          const double wv = v0 + v1;
+          Ws[idx] = wv;
+          a.W[(i0 + rr) * a.ldw + c] = wv;
+        }
+      }
+    }
+    __syncthreads();  // Ls is restaged by the next tile
+  }
+  step_stamp(a.stamps, 1);  // fix-ups done
+
+  // ---- phase 2 on the tiles this CTA completed (their U and W rows are still in shared memory):
+  // Ritz block rows, residual and Gram partials
+  step_wait(a.sync + stepsync::kFlag, a.epoch);
+  step_stamp(a.stamps, 4);  // released (max over phase-2 CTAs)
+  for (int idx = t; idx < b * rq; idx += NTH) {
+    const int k = idx / rq, c = idx - k * rq;
+    Ss[idx] = __ldcg(a.Sout + k * b + c);
+  }
+  for (int c = t; c < rq; c += NTH) thsh[c] = __ldcg(a.theta + c);
+  __syncthreads();
+  const int rpt = NTH / rq;  // rows in flight per column
+  const int c = t % rq;
+  const int rofs = t / rq;
+  for (int f = 0; f < nfix; ++f) {
+    const int tile = s_fix[f];
+    const int64_t i0 = (int64_t)tile * kMmaRows;
+    const int rows = (int)min((int64_t)kMmaRows, n - i0);
+    const double* Us = Uf(f);
+    const double* Ws = Wf(f);
+    double sq = 0.0;
+    if (rofs < rpt) {
+      const double th = c < a.nreq ? thsh[c] : 0.0;
+      const bool res = c < a.nreq;
+      // four rows per round: independent chains x_q = U_row S_c, y_q = W_row S_c
+      for (int r0 = rofs; r0 < rows; r0 += 4 * rpt) {
+        double x[4] = {0.0, 0.0, 0.0, 0.0}, y[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = 0; k < b; ++k) {
+          const double sk = Ss[k * rq + c];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int rr = min(r0 + q * rpt, rows - 1);
+            x[q] = fma(Us[rr * b + k], sk, x[q]);
+            if (res) y[q] = fma(Ws[rr * b + k], sk, y[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int rr = r0 + q * rpt;
+          if (rr < rows) {
+            const int64_t i = i0 + rr;
+            a.T[i * a.ldt + c] = x[q];
+            Ts[rr * rq + c] = x[q];
+            if (c < a.r2) a.V2[i * a.ld2 + c] = x[q];
+            if (res) {
+              const double d = y[q] - th * x[q];
+              sq = fma(d, d, sq);
+            }
+          }
+        }
+      }
+    }
+    red[t] = sq;
+    __syncthreads();  // also publishes Ts
+    step_stamp(a.stamps, 5);  // Ritz rows written
+    double* p2 = a.part2 + (int64_t)tile * kFusedStride;
+    if (t < a.nreq) {
+      double s2 = 0.0;
+      for (int j = t; j < rpt * rq; j += rq) s2 += red[j];
+      p2[t] = s2;
+    }
+    for (int o = t; o < a.gr * a.gr; o += NTH) {
+      const int ia = o / a.gr, cc = o - ia * a.gr;
+      p2[a.nreq + o] = tile_dot(Ts, rq, ia, Ts, rq, cc, rows);
+    }
+    __threadfence();
+    __syncthreads();
+    if (t == 0) {
+      const unsigned old = atomicAdd(a.sync + stepsync::kTicketB, 1u);
+      s_flag = old == (unsigned)tiles;
+      if (s_flag) atomicExch(a.sync + stepsync::kTicketB, 0u);
+    }
+    __syncthreads();
+    if (s_flag) {
+      __threadfence();
+      step_finish_pack(a, tiles);
+    }
+    __syncthreads();  // Ts and red are reused by the next tile
+  }
+}
+
+// L^T U (l x b) and optionally L^T L (nvg x nvg) over 128-row tiles with the step tail's Gram
+// products (tile_dot), the tile partials summed in tile order by the last CTA: the start of a
+// step whose E is not carried over from the previous step's Ritz-block Gram (bit-identical to it).
+__global__ void __launch_bounds__(256) k_tile_gram(int64_t n, const double* __restrict__ L, int64_t ldl, int l,
+                                                   const double* __restrict__ U, int64_t ldu, int b, int nvg,
+                                                   double* __restrict__ part, unsigned* ticket, double* __restrict__ E,
+                                                   double* __restrict__ vgram, double* __restrict__ Gu) {
+  extern __shared__ __align__(16) double gsm[];
+  __shared__ int s_last;
+  double* Ls = gsm;                  // 128 x l
+  double* Us = Ls + kMmaRows * l;    // 128 x b
+  const int tile = blockIdx.x, tiles = gridDim.x, t = threadIdx.x;
+  const int64_t i0 = (int64_t)tile * kMmaRows;
+  const int rows = (int)min((int64_t)kMmaRows, n - i0);
+  step_stage2(Ls, L, ldl, l, Us, U, ldu, b, i0, rows);
+  __syncthreads();
+  double* p = part + (int64_t)tile * kFusedStride;
+  for (int o = t; o < l * b; o += blockDim.x) p[o] = tile_dot(Ls, l, o / b, Us, b, o % b, rows);
+  for (int o = t; o < nvg * nvg; o += blockDim.x) p[l * b + o] = tile_dot(Ls, l, o / nvg, Ls, l, o % nvg, rows);
+  for (int o = t; o < b * b; o += blockDim.x) p[l * b + nvg * nvg + o] = tile_dot(Us, b, o / b, Us, b, o % b, rows);
+  __threadfence();
+  __syncthreads();
+  if (t == 0) {
+    s_last = atomicAdd(ticket, 1u) == (unsigned)tiles - 1;
+    if (s_last) atomicExch(ticket, 0u);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int o = t; o < l * b + nvg * nvg + b * b; o += blockDim.x) {
+    const double s = tile_ordered_sum<32>(part, tiles, kFusedStride, o);
+    if (o < l * b)
+      E[o] = s;
+    else if (o < l * b + nvg * nvg)
+      vgram[o - l * b] = s;
+    else
+      Gu[o - l * b - nvg * nvg] = s;
   }
 }
 
@@ -1090,17 +1560,15 @@ void launch_dense_f64(const Launch& L, const double* M, int64_t ldm, int64_t n, 
   const size_t smem = (size_t)(KC * BN + 4 * BN * 64) * sizeof(double);
   dim3 grid(cdiv(n, 64), S);
   if (vec) {
-    static bool attr = false;
-    if (!attr) {
+    static char attr = 0;
+    if (first_on_device(&attr)) {
       MEG_CUDA(cudaFuncSetAttribute(k_dense_apply_f64<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
     }
     k_dense_apply_f64<BN, true><<<grid, kApplyThreads, smem, L.stream>>>(M, ldm, n, U, ldu, b, part, kslice);
   } else {
-    static bool attr = false;
-    if (!attr) {
+    static char attr = 0;
+    if (first_on_device(&attr)) {
       MEG_CUDA(cudaFuncSetAttribute(k_dense_apply_f64<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
     }
     k_dense_apply_f64<BN, false><<<grid, kApplyThreads, smem, L.stream>>>(M, ldm, n, U, ldu, b, part, kslice);
   }
@@ -1114,17 +1582,15 @@ void launch_dense_f32(const Launch& L, const float* M, int64_t ldm, int64_t n, c
   const size_t smem = (size_t)((KC * BN + 1) / 2 + 4 * BN * 128) * sizeof(double);
   dim3 grid(cdiv(n, 128), S);
   if (vec) {
-    static bool attr = false;
-    if (!attr) {
+    static char attr = 0;
+    if (first_on_device(&attr)) {
       MEG_CUDA(cudaFuncSetAttribute(k_dense_apply_f32<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
     }
     k_dense_apply_f32<BN, true><<<grid, kApplyThreads, smem, L.stream>>>(M, ldm, n, U, ldu, b, part, kslice);
   } else {
-    static bool attr = false;
-    if (!attr) {
+    static char attr = 0;
+    if (first_on_device(&attr)) {
       MEG_CUDA(cudaFuncSetAttribute(k_dense_apply_f32<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
     }
     k_dense_apply_f32<BN, false><<<grid, kApplyThreads, smem, L.stream>>>(M, ldm, n, U, ldu, b, part, kslice);
   }
@@ -1200,10 +1666,9 @@ template <typename T, int BN>
 void launch_pipe(const Launch& L, const T* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
                  double* part, int tiles, int64_t kslice, int items, int grid) {
   constexpr size_t smem = pipe_smem_bytes<T, BN>();
-  static bool attr = false;
-  if (!attr) {
+  static char attr = 0;
+  if (first_on_device(&attr)) {
     MEG_CUDA(cudaFuncSetAttribute(k_dense_pass<T, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
   }
   const CUtensorMap tmM = make_map(M, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                                    sizeof(T), n, n, ldm, PipeShape<T>::BM, kPipeKC);
@@ -1245,13 +1710,12 @@ void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, c
                      double* part, int tiles, int kch, int smax, int grid) {
   constexpr size_t smem = mma_smem_bytes<NT, TAIL>();
   const int cw = mma_consumer_warps();
-  static bool attr = false;
-  if (!attr) {
+  static char attr = 0;
+  if (first_on_device(&attr)) {
     MEG_CUDA(cudaFuncSetAttribute(k_dense_pass_mma<NT, TAIL, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     MEG_CUDA(cudaFuncSetAttribute(k_dense_pass_mma<NT, TAIL, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-    attr = true;
   }
   const CUtensorMap tmM =
       make_map(M, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, n, n, ldm, 16, kPipeKC, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1273,6 +1737,59 @@ void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, c
     MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL, 16>, tmM, tmU, n, b, part, tiles, kch, smax));
   else
     MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL, 8>, tmM, tmU, n, b, part, tiles, kch, smax));
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+// Stream-K grid of the DMMA pass over (128-row tile, 32-row k chunk) units: one CTA per SM,
+// shrunk until every tile is covered by at most min(cap, 16) CTAs (its partial slots).
+void stream_k_grid(int64_t n, int sm_count, int64_t part_cap_slices, int* grid_out, int* smax_out) {
+  const int tiles = cdiv(n, kMmaRows);
+  const int kch = cdiv(n, kPipeKC);
+  const int64_t utot = (int64_t)tiles * kch;
+  const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(part_cap_slices, 16));
+  int grid = (int)std::min<int64_t>(sm_count, utot);
+  int smax = 1;
+  for (;;) {
+    smax = 1;
+    for (int t = 0; t < tiles; ++t)
+      smax = std::max(smax, sk_cfirst((int64_t)(t + 1) * kch - 1, grid, utot) - sk_cfirst((int64_t)t * kch, grid, utot) + 1);
+    if (smax <= cap || grid == 1) break;
+    grid = std::max(1, grid * cap / (smax + 1));
+  }
+  *grid_out = grid;
+  *smax_out = smax;
+}
+
+template <int NT, int TAIL>
+void launch_step_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                     double* part, int tiles, int kch, int smax, int grid, const FusedPassArgs& a) {
+  constexpr size_t smem_ring = mma_smem_bytes<NT, TAIL>();
+  const size_t smem = 1024 + mma_step_extra_offset<NT, TAIL>() + 2 * (size_t)kMmaRows * b * sizeof(double);
+  (void)smem_ring;
+  static char attr = 0;
+  if (first_on_device(&attr))
+    MEG_CUDA(cudaFuncSetAttribute(k_dense_step_mma<NT, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(1024 + mma_step_extra_offset<NT, TAIL>() +
+                                        2 * kMmaRows * (8 * NT + TAIL) * sizeof(double))));
+  const CUtensorMap tmM =
+      make_map(M, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, n, n, ldm, 16, kPipeKC, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap tmU =
+      make_map(U, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, b, n, ldu, (uint32_t)mma_bnp<NT, TAIL>(), kPipeKC);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kStepThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = L.stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  // the release flag needs every CTA resident: cooperative launch (driver-guaranteed co-residency)
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_step_mma<NT, TAIL>, tmM, tmU, n, b, part, tiles, kch, smax, a));
   MEG_LAUNCHED();
   ++*L.counter;
 }
@@ -1309,18 +1826,8 @@ int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, 
       // shrinks until every tile is covered by at most part_cap_slices CTAs
       const int tiles = cdiv(n, kMmaRows);
       const int kch = cdiv(n, kPipeKC);
-      const int64_t utot = (int64_t)tiles * kch;
-      const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(part_cap_slices, 16));
-      int grid = (int)std::min<int64_t>(sm_count, utot);
-      int smax = 1;
-      for (;;) {
-        auto cfirst = [&](int64_t x) { return (int)(((x + 1) * grid + utot - 1) / utot) - 1; };
-        smax = 1;
-        for (int t = 0; t < tiles; ++t)
-          smax = std::max(smax, cfirst((int64_t)(t + 1) * kch - 1) - cfirst((int64_t)t * kch) + 1);
-        if (smax <= cap || grid == 1) break;
-        grid = std::max(1, grid * cap / (smax + 1));
-      }
+      int grid = 0, smax = 0;
+      stream_k_grid(n, sm_count, part_cap_slices, &grid, &smax);
       const double* m = static_cast<const double*>(M);
       // DMMA n-tiles for the multiple-of-8 head of the block, DFMA for the (even) rest
 #define MEG_MMA(nt, tail) launch_pipe_mma<nt, tail>(L, m, ldm, n, U, ldu, b, part, tiles, kch, smax, grid)
@@ -1413,14 +1920,13 @@ void tn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const d
   G = cdiv(n, rows_per);
   const size_t smem = (size_t)kTnRows * (p + q) * sizeof(double);
   const int J = cdiv(pq, kTnThreads);
-  static bool attr = false;
-  if (!attr) {
+  static char attr = 0;
+  if (first_on_device(&attr)) {
     MEG_CUDA(cudaFuncSetAttribute(k_tn_partial<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     MEG_CUDA(cudaFuncSetAttribute(k_tn_partial<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     MEG_CUDA(cudaFuncSetAttribute(k_tn_partial<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     MEG_CUDA(cudaFuncSetAttribute(k_tn_partial<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     MEG_CUDA(cudaFuncSetAttribute(k_tn_partial<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    attr = true;
   }
   if (J <= 1)
     k_tn_partial<1><<<G, kTnThreads, smem, L.stream>>>(n, X, ldx, p, Y, ldy, q, part, rows_per);
@@ -1443,12 +1949,78 @@ void tn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const d
 void nn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const double* C, int64_t ldc, int q,
         double alpha, double beta, double* Y, int64_t ldy) {
   const size_t smem = (size_t)std::max(1, p * q) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static char attr = 0;
+  if (first_on_device(&attr)) {
     MEG_CUDA(cudaFuncSetAttribute(k_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
   }
   k_nn<<<cdiv(n * q, 256), 256, smem, L.stream>>>(n, X, ldx, p, C, ldc, q, alpha, beta, Y, ldy);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+size_t step_mma_tail_doubles(int b, int l) {
+  const size_t jac = std::max((size_t)jacobi_smem_doubles(b), (size_t)5 * b * b + 128);
+  return 2 * (size_t)kStepMaxTileSlots * kMmaRows * b + (size_t)kMmaRows * std::max(l, b) +
+         (size_t)std::max(l, 1) * b + 2 * (size_t)b * b + kStepThreads + jac;
+}
+
+bool dense_step_mma_supported(const void* M, int dtype, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                              int l, int64_t part_cap_slices, int sm_count) {
+  // opt-in (MEGB200_STEP_MMA=1) until its tail beats the separate pass + k_fused_first_pass
+  static const bool on = getenv("MEGB200_STEP_MMA") != nullptr && getenv("MEGB200_STEP_MMA")[0] == '1';
+  if (!on) return false;
+  if (dtype != MEGB200_F64 || b < 8 || b > 32 || b % 2 != 0 || l < 0 || l > kFusedMaxL) return false;
+  if (!(ldu % 2 == 0 && ((uintptr_t)U % 16 == 0) && (ldm * 8) % 16 == 0 && ((uintptr_t)M % 16 == 0) && (n * 8) % 16 == 0))
+    return false;
+  const int tiles = cdiv(n, kMmaRows);
+  if (tiles > kStepMaxTiles || b * b > kFusedStride || l * b > kFusedStride) return false;
+  int grid = 0, smax = 0;
+  stream_k_grid(n, sm_count, part_cap_slices, &grid, &smax);
+  const int64_t units_per_cta = cdiv((int64_t)tiles * cdiv(n, kPipeKC), grid);
+  // a CTA completes at most kStepMaxTileSlots tiles (its range spans <= 2 tiles when tiles <= grid)
+  if (tiles > grid || cdiv(units_per_cta, cdiv(n, kPipeKC)) + 1 > kStepMaxTileSlots) return false;
+  // the tail's shared memory stays below the operand ring (the mbarriers after it are not reused);
+  // ring + the U / W segment rows fit one SM (b <= 18 with the 5-stage ring)
+  if (b * b > 2 * 32 * 8) return false;  // two H entries per consumer thread
+  const int bnp = ((b - 2 + 7) / 8) * 8 + 2;  // mma_bnp<b / 8, b % 8>()
+  const size_t dyn = 1024 + (size_t)kPipeStages * kPipeKC * kMmaRows * 8 + 2 * (size_t)kMmaRows * b * 8 + 256 +
+                     (size_t)kPipeStages * kPipeKC * bnp * 8;
+  return dyn + 2048 <= 227 * 1024 &&
+         step_mma_tail_doubles(b, l) * sizeof(double) <= (size_t)kPipeStages * kPipeKC * kMmaRows * 8;
+}
+
+void dense_step_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
+                    double* part, int64_t part_cap_slices, int sm_count, const FusedPassArgs& a) {
+  const int tiles = cdiv(n, kMmaRows);
+  const int kch = cdiv(n, kPipeKC);
+  int grid = 0, smax = 0;
+  stream_k_grid(n, sm_count, part_cap_slices, &grid, &smax);
+#define MEG_STEP(nt, tail) launch_step_mma<nt, tail>(L, M, ldm, n, U, ldu, b, part, tiles, kch, smax, grid, a)
+  switch (b) {
+    case 8: MEG_STEP(1, 0); break;
+    case 10: MEG_STEP(1, 2); break;
+    case 12: MEG_STEP(1, 4); break;
+    case 14: MEG_STEP(1, 6); break;
+    case 16: MEG_STEP(2, 0); break;
+    case 18: MEG_STEP(2, 2); break;
+    case 20: MEG_STEP(2, 4); break;
+    case 22: MEG_STEP(2, 6); break;
+    case 24: MEG_STEP(3, 0); break;
+    case 26: MEG_STEP(3, 2); break;
+    case 28: MEG_STEP(3, 4); break;
+    case 30: MEG_STEP(3, 6); break;
+    default: MEG_STEP(4, 0); break;
+  }
+#undef MEG_STEP
+}
+
+void tile_gram(const Launch& L, int64_t n, const double* Lm, int64_t ldl, int l, const double* U, int64_t ldu, int b,
+               int nvg, double* part, unsigned* ticket, double* E, double* vgram, double* Gu) {
+  const size_t smem = (size_t)kMmaRows * (l + b) * sizeof(double);
+  static char attr = 0;
+  if (first_on_device(&attr))
+    MEG_CUDA(cudaFuncSetAttribute(k_tile_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  k_tile_gram<<<cdiv(n, kMmaRows), 256, smem, L.stream>>>(n, Lm, ldl, l, U, ldu, b, nvg, part, ticket, E, vgram, Gu);
   MEG_LAUNCHED();
   ++*L.counter;
 }

@@ -542,10 +542,9 @@ void rr_wide(const Launch& L, const double* H, int64_t ldh, int m, double* theta
   static const bool force_env = getenv("MEGB200_RR_JACOBI") != nullptr;  // diagnostics: cyclic Jacobi only
   const bool force = force_env || getenv("MEGB200_RR_JACOBI_ONCE") != nullptr;
   const size_t smem = rr_wide_smem(m);
-  static bool attr = false;
-  if (!attr) {
+  static char attr = 0;
+  if (first_on_device(&attr)) {
     MEG_CUDA(cudaFuncSetAttribute(k_rr_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
   }
   if (smem > 227 * 1024) throw Error(MEGB200_ERR_PARAM, "wide Rayleigh-Ritz: basis too large");
   k_rr_wide<<<1, kRT, smem, L.stream>>>(H, ldh, m, theta, S, info, nvec, force ? 1 : 0);

@@ -19,13 +19,26 @@
 
 #include "megb200_internal.h"
 
+#include <mutex>
+#include <set>
+
+namespace megb200 {
+bool first_on_device(const void* tag) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  MEG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  return done.insert({dev, tag}).second;
+}
+}  // namespace megb200
+
 using namespace megb200;
 
 namespace {
 
 thread_local std::string g_last_error;
-// live solver handles: with more than one, fused first passes launch cooperatively (handles may
-// drive different streams, and concurrent spin-waiting grids must not share the SMs)
+// live solver handles (telemetry)
 std::atomic<int> g_live_solvers{0};
 
 constexpr int kMaxBlock = 64;
@@ -215,7 +228,33 @@ struct OpDev {
   double alpha = 0.0;
   const double* Eg = nullptr;     // device L^T U when the caller already has it (else reduced per pass)
   int64_t ldg = 0;
+  const double* Gu = nullptr;     // device U^T U when the caller already has it (with Eg)
+  int64_t ldgu = 0;
 };
+
+// Live pass profiling (megb200_profile_enable): every prof-th streamed pass kernel is bracketed
+// by events on the solver stream; prof_end books its algorithmic bytes (operand as stored + the
+// n x k float64 block read and written).
+int prof_begin(megb200_solver* s) {
+  if (!(s->prof > 0 && (s->prof_seen++ % s->prof) == 0)) return -1;
+  const int ev0 = s->ev_next;
+  MEG_CUDA(cudaEventRecord(s->next_event(), s->stream));
+  return ev0;
+}
+
+void prof_end(megb200_solver* s, int ev0, const OpDev& op, int k) {
+  if (ev0 < 0) return;
+  const int64_t n = s->n;
+  const int ev1 = s->ev_next;
+  MEG_CUDA(cudaEventRecord(s->next_event(), s->stream));
+  s->ev_pending.emplace_back(ev0, ev1);
+  const double es = op.kind == MEGB200_OP_DENSE ? (op.dtype == MEGB200_F64 ? 8.0 : 4.0) : 0.0;
+  double b = 2.0 * (double)n * k * 8.0;  // read U, write W (float64)
+  if (op.kind == MEGB200_OP_DENSE) b += (double)n * (double)n * es;
+  if (op.kind == MEGB200_OP_CSR) b += (double)op.nnz * 12.0 + (double)(n + 1) * 4.0;
+  s->prof_bytes += b;
+  s->prof_passes++;
+}
 
 // Streamed operand pass alone: partial slices of Op U into s->part; returns the slice count.
 int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k) {
@@ -224,11 +263,7 @@ int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu
   int S = 0;
   const bool streamed = (op.kind == MEGB200_OP_DENSE || op.kind == MEGB200_OP_CSR) && op.scale != 0.0;
   // live profiling brackets the streamed operand kernel only (the roofline's dominant kernel)
-  int ev0 = -1;
-  if (s->prof > 0 && streamed && (s->prof_seen++ % s->prof) == 0) {
-    ev0 = s->ev_next;
-    MEG_CUDA(cudaEventRecord(s->next_event(), s->stream));
-  }
+  const int ev0 = streamed ? prof_begin(s) : -1;
   if (op.kind == MEGB200_OP_DENSE && op.scale != 0.0) {
     S = dense_apply_partial(L, op.dense, op.dtype, op.ld, n, U, ldu, k, s->part, s->part_slices, s->sm_count,
                             reinterpret_cast<float*>(s->uT));
@@ -236,17 +271,7 @@ int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu
     csr_apply_partial(L, op.rowptr, op.col, op.val, n, U, ldu, k, s->part);
     S = 1;
   }
-  if (ev0 >= 0) {
-    const int ev1 = s->ev_next;
-    MEG_CUDA(cudaEventRecord(s->next_event(), s->stream));
-    s->ev_pending.emplace_back(ev0, ev1);
-    const double es = op.kind == MEGB200_OP_DENSE ? (op.dtype == MEGB200_F64 ? 8.0 : 4.0) : 0.0;
-    double b = 2.0 * (double)n * k * 8.0;  // read U, write W (float64)
-    if (op.kind == MEGB200_OP_DENSE) b += (double)n * (double)n * es;
-    if (op.kind == MEGB200_OP_CSR) b += (double)op.nnz * 12.0 + (double)(n + 1) * 4.0;
-    s->prof_bytes += b;
-    s->prof_passes++;
-  }
+  prof_end(s, ev0, op, k);
   return S;
 }
 
@@ -474,6 +499,7 @@ int rr_readback(megb200_solver* s, int newcols, int nreq, int bw, const EpiSpec*
 // launch whose result pack lands in dst (pinned; written by the kernel itself when
 // the staging buffer is mapped).  Same outputs as block_pass + rr_readback.
 // per reduction: G partials + ceil(G / 8) group partials + the result, kFusedStride doubles each
+constexpr int kTileGramTicket = 420;  // word of s->fsync (k_dense_step_mma uses words 256..418)
 constexpr int64_t kFusedPart1 = (148 + 19 + 1) * (int64_t)kFusedStride;  // offsets in s->red
 constexpr int64_t kFusedPart2 = 2 * kFusedPart1;
 constexpr int64_t kFusedRed = 3 * kFusedPart1;
@@ -484,10 +510,18 @@ bool fused_ok(const megb200_solver* s, const OpDev& op, int bw, int nreq) {
          nreq <= bw && fused_pass_supported(s->n, bw, op.l, nreq, s->sm_count);
 }
 
+// the pass + step tail in one launch applies (float64 dense operand, b <= 32, ...)
+bool step_mma_ok(const megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int bw) {
+  return op.kind == MEGB200_OP_DENSE && op.scale != 0.0 &&
+         dense_step_mma_supported(op.dense, op.dtype, op.ld, s->n, U, ldu, bw, op.L ? op.l : 0, s->part_slices,
+                                  s->sm_count);
+}
+
 int fused_pass(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int bw, int nreq, const EpiSpec* epi,
                double* tdst, int64_t ldt, double* v2, int64_t ld2, int r2, double* dst) {
   Launch L = s->launch();
-  const int S = pass_launch(s, op, U, ldu, bw);
+  const bool one_launch = step_mma_ok(s, op, U, ldu, bw);
+  const int S = one_launch ? 0 : pass_launch(s, op, U, ldu, bw);
   FusedPassArgs a;
   a.n = s->n;
   a.b = bw;
@@ -532,21 +566,60 @@ int fused_pass(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu,
   a.part2 = s->red + kFusedPart2;
   a.Ews = s->E;
   a.sync = s->fsync;
-  static const bool coop_env = getenv("MEGB200_COOPERATIVE") != nullptr;
-  a.cooperative = coop_env || g_live_solvers.load() > 1;
+  // always a cooperative launch: the release flags and last-CTA tickets need every CTA resident,
+  // which only the driver's cooperative-launch guarantee provides against concurrent work (other
+  // solver handles or streams, NCCL, MPS neighbours)
+  a.cooperative = true;
   if (++s->epoch == 0) ++s->epoch;
   a.epoch = s->epoch;
   a.pack = s->pack;
   a.pack_count = (int)(s->pack_gram + (int64_t)a.gr * a.gr);
-  if (s->want_vgram > 0 && !op.Eg && a.L && a.l >= s->want_vgram && s->want_vgram <= 32 &&
+  if (!one_launch && s->want_vgram > 0 && !op.Eg && a.L && a.l >= s->want_vgram && s->want_vgram <= 32 &&
       a.l * bw + s->want_vgram * s->want_vgram <= kFusedStride) {
     a.vgram = s->pack + s->pack_vgram;
     a.nvg = s->want_vgram;
     a.pack_count = (int)(s->pack_vgram + (int64_t)a.nvg * a.nvg);
     s->vgram_done = true;
   }
-  s->want_vgram = 0;
+  if (!one_launch) s->want_vgram = 0;
   a.host_pack = s->h_buf_dev ? s->h_buf_dev + (dst - s->h_buf) : nullptr;
+  if (one_launch) {
+    // E = diag(d) L^T U needs L^T U before the launch: carried over from the previous step's
+    // Ritz-block Gram (op.Eg), else reduced here with the same products (k_tile_gram), which also
+    // yields the Gram of the iterate's factor when the host-buffer step asked for it
+    a.vgram = nullptr;
+    a.pack_count = (int)(s->pack_gram + (int64_t)a.gr * a.gr);
+    // H = U^T W is formed from U^T U too: the previous step's Ritz-block Gram when carried over
+    // (pipelined: Eg is its first rows), else reduced with L^T U
+    if (a.Eg && op.Gu) {
+      a.Gu = op.Gu;
+      a.ldgu = op.ldgu;
+    } else {
+      const int nvg = (s->want_vgram > 0 && s->want_vgram <= a.l && s->want_vgram <= 32) ? s->want_vgram : 0;
+      tile_gram(L, s->n, a.L, a.ldl, a.l, U, ldu, bw, nvg, s->red, s->fsync + kTileGramTicket, s->E,
+                nvg ? s->pack + s->pack_vgram : nullptr, s->E + (int64_t)a.l * bw);
+      if (nvg) {
+        a.pack_count = (int)(s->pack_vgram + (int64_t)nvg * nvg);
+        s->vgram_done = true;
+      }
+      a.Eg = s->E;
+      a.ldg = bw;
+      a.Gu = s->E + (int64_t)a.l * bw;
+      a.ldgu = bw;
+    }
+    s->want_vgram = 0;
+    static const bool step_stamps = getenv("MEGB200_FUSED_STAMPS") != nullptr;
+    if (step_stamps) {  // diagnostics: phase timestamps (maxima over CTAs), reset per launch
+      a.stamps = reinterpret_cast<unsigned long long*>(s->fsync + 128);
+      MEG_CUDA(cudaMemsetAsync(a.stamps, 0, 16 * sizeof(unsigned long long), s->stream));
+    }
+    const int ev0 = prof_begin(s);
+    dense_step_mma(L, static_cast<const double*>(op.dense), op.ld, s->n, U, ldu, bw, s->part, s->part_slices,
+                   s->sm_count, a);
+    prof_end(s, ev0, op, bw);
+    if (!a.host_pack) s->d2h(dst, s->pack, a.pack_count);
+    return a.gr;
+  }
   static const bool stamps = getenv("MEGB200_FUSED_STAMPS") != nullptr;
   if (stamps) a.stamps = reinterpret_cast<unsigned long long*>(s->fsync + 128);
   fused_first_pass(L, a, s->sm_count);
@@ -1085,8 +1158,10 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
     if (cudaHostGetDevicePointer(&hd, s->h_buf, 0) == cudaSuccess && getenv("MEGB200_NO_ZEROCOPY") == nullptr)
       s->h_buf_dev = static_cast<double*>(hd);
     cudaGetLastError();
-    e = cudaMalloc(&s->fsync, 128 * sizeof(unsigned) + 64 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemset(s->fsync, 0, 128 * sizeof(unsigned) + 64 * sizeof(unsigned long long));
+    // words 0..127 tickets / flags of k_fused_first_pass, 128..255 its stamps (64 x u64),
+    // 256..418 k_dense_step_mma (tile counters, tickets, flag), 420 the k_tile_gram ticket
+    e = cudaMalloc(&s->fsync, 1024 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(s->fsync, 0, 1024 * sizeof(unsigned));
     if (e != cudaSuccess) {
       cudaFree(s->arena);
       cudaFreeHost(s->h_buf);
@@ -1539,6 +1614,8 @@ int megb200_meg_run(megb200_solver* s, const megb200_iterate* x0, const megb200_
         // Rayleigh-Ritz launch just reduced (same rows, same order: bit-identical to reducing it again)
         op1.Eg = s->pack + s->pack_gram;
         op1.ldg = sh.bw;
+        op1.Gu = s->pack + s->pack_gram;  // U^T U: the whole Ritz-block Gram
+        op1.ldgu = sh.bw;
         fast_step_enqueue(s, op1, r, sh, P0.tol, Wb[(i + 1) % 3], 64, eps_eval(*sch, t1 + 1), Wb[(i + 2) % 3], 64,
                           Vb[(i + 2) % 3], r, hspec[(i + 1) & 1], done[(i + 1) & 1], fs[(i + 1) & 1]);
         end_step(i + 1);
@@ -1661,9 +1738,14 @@ void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradie
   const bool v_alias = overlaps(out->V_next, out->ld_next, r, x->V, x->ldv, r) ||
                        overlaps(out->V_next, out->ld_next, r, g->gV, g->g_ldv, (int)g->g_r);
   const int ritz_cap = std::max(nreq, (int)s->max_block);
+  // the warm block is an operand too: the fused first pass reads it in place (deferred warm) while
+  // it writes the Ritz block, and a continued solve copies it into the basis afterwards
   const bool w_alias = overlaps(out->ritz_block, out->ld_ritz, ritz_cap, x->V, x->ldv, r) ||
-                       overlaps(out->ritz_block, out->ld_ritz, ritz_cap, g->gV, g->g_ldv, (int)g->g_r);
-  if (!v_alias) {
+                       overlaps(out->ritz_block, out->ld_ritz, ritz_cap, g->gV, g->g_ldv, (int)g->g_r) ||
+                       overlaps(out->ritz_block, out->ld_ritz, ritz_cap, P.warm, P.ld_warm, (int)P.warm_cols);
+  // V_next must not overwrite the warm block before the solve has read it either
+  const bool v_warm_alias = overlaps(out->V_next, out->ld_next, r, P.warm, P.ld_warm, (int)P.warm_cols);
+  if (!v_alias && !v_warm_alias) {
     epi.v_next = out->V_next;
     epi.ld_next = out->ld_next;
     epi.v_host = v_host;
@@ -1680,7 +1762,7 @@ void step_core(megb200_solver* s, const megb200_iterate* x, const megb200_gradie
   if (!run.converged) throw_lanczos(run, P.tol);
   // next iterate: V = top r Ritz vectors (written by top_eigs unless aliased); lam / certificate
   // came from the fused epilogue
-  if (v_alias) copy_block(L, n, r, s->T, s->ldq, out->V_next, out->ld_next);
+  if (v_alias || v_warm_alias) copy_block(L, n, r, s->T, s->ldq, out->V_next, out->ld_next);
   if (v_host_done) *v_host_done = epi.v_host_done;
   if (w_alias && out->ritz_block) copy_block(L, n, out->ritz_cols, s->W, s->max_block, out->ritz_block, out->ld_ritz);
   fill_step_result(epi.host.data(), epi.host.data() + 2 * r + 8, epi.gr, r, run.theta.data(), out);
@@ -1713,9 +1795,16 @@ int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_ho
     // pass stages its rows once: no upload on the stream's critical path); otherwise it is
     // uploaded as one block (a pitched copy of 8r-byte rows is n tiny DMA rows)
     double* v_mapped = nullptr;
+    // an output that overlaps the input factor in host memory disables zero-copy for both: the
+    // factor is uploaded and validated from the device copy, never from memory the step writes
+    const char* vh0 = reinterpret_cast<const char*>(x_host->V);
+    const char* vh1 = reinterpret_cast<const char*>(x_host->V + (n - 1) * x_host->ldv + r);
+    const char* oh0 = reinterpret_cast<const char*>(V_next_host);
+    const char* oh1 = reinterpret_cast<const char*>(V_next_host + (n - 1) * ld_next_host + r);
+    const bool io_overlap = vh0 < oh1 && oh0 < vh1;
     // (small factors only: a large one is not staged by the fused kernel and would be re-read
     // over the host link)
-    if (x_host->ldv == r && n * r * (int64_t)sizeof(double) <= (2 << 20) && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
+    if (!io_overlap && x_host->ldv == r && n * r * (int64_t)sizeof(double) <= (2 << 20) && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&v_mapped), const_cast<double*>(x_host->V), 0) !=
             cudaSuccess) {
       cudaGetLastError();
@@ -1772,7 +1861,7 @@ int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_ho
     bool v_done = false;
     // a mapped pinned destination takes V_next straight from the kernels (no read-back copy)
     double* vn_mapped = nullptr;
-    if (ld_next_host == r && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
+    if (!io_overlap && ld_next_host == r && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&vn_mapped), V_next_host, 0) != cudaSuccess) {
       cudaGetLastError();
       vn_mapped = nullptr;

@@ -36,11 +36,10 @@ int dense_pass_umma(const Launch& L, const float* M, int64_t ldm, int64_t n, con
   umma::k_split_u<<<(unsigned)((n + 31) / 32), 256, 0, L.stream>>>(n, b, U, ldu, uscratch, n);
   MEG_LAUNCHED();
   ++*L.counter;
-  static bool attr = false;
-  if (!attr) {
+  static char attr = 0;
+  if (first_on_device(&attr)) {
     MEG_CUDA(cudaFuncSetAttribute(umma::k_dense_pass_umma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)umma::smem_bytes()));
-    attr = true;
   }
   const CUtensorMap tmM = make_map(M, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, n, n, ldm, umma::kKC, umma::kRows,
                                    CU_TENSOR_MAP_SWIZZLE_128B);
