@@ -41,7 +41,8 @@ enum {
   MEGB200_ERR_LANCZOS = 2,   /* -> specmeg.linalg.LanczosError   (linalg.py:43-52)     */
   MEGB200_ERR_CUDA = 3,      /* CUDA runtime / launch failure                           */
   MEGB200_ERR_KEPT_MASS = 4, /* -> AssertionError "kept mass vanished" (meg.py:350)     */
-  MEGB200_ERR_NO_DEVICE = 5  /* no sm_100 device visible                                */
+  MEGB200_ERR_NO_DEVICE = 5, /* no sm_100 device visible                                */
+  MEGB200_ERR_CALLBACK = 6   /* a caller-supplied apply callback returned non-zero      */
 };
 
 enum { MEGB200_F64 = 0, MEGB200_F32 = 1 };
@@ -51,7 +52,15 @@ enum { MEGB200_F64 = 0, MEGB200_F32 = 1 };
  * Op is a dense symmetric matrix, a CSR matrix with float64 values, or
  * absent.  This is the device form of specmeg.linalg.SymmetricOperator
  * (linalg.py:81-103) for the operators the hot path builds. */
-enum { MEGB200_OP_NONE = 0, MEGB200_OP_DENSE = 1, MEGB200_OP_CSR = 2 };
+enum { MEGB200_OP_NONE = 0, MEGB200_OP_DENSE = 1, MEGB200_OP_CSR = 2, MEGB200_OP_CALLBACK = 3 };
+
+/* Caller-supplied block application W = Op U: the C form of the reference's Python callables
+ * (SymmetricOperator(dim, apply_fn), linalg.py:81-94; grad_apply, meg.py:327-335).  U (n x k, ld
+ * ldu) and W (n x k, ld ldw) are device pointers; the callback must enqueue its work on `stream`
+ * (or finish it before returning) and return 0, non-zero on failure (-> MEGB200_ERR_CALLBACK).
+ * The solver calls it once per block pass from the calling thread, k <= 64 columns at a time. */
+typedef int (*megb200_apply_fn)(void* ctx, const double* U, int64_t ldu, int32_t k, double* W, int64_t ldw,
+                                void* stream);
 
 typedef struct megb200_operator {
   int32_t kind;          /* MEGB200_OP_*                                      */
@@ -69,6 +78,8 @@ typedef struct megb200_operator {
   int64_t ldl;
   const double* d;       /* (host) l coefficients                             */
   double alpha;
+  megb200_apply_fn apply; /* CALLBACK: Op U (scaled by `scale`)               */
+  void* apply_ctx;
 } megb200_operator;
 
 /* The gradient a step consumes: the device form of the reference's
@@ -84,7 +95,8 @@ enum {
   MEGB200_GRAD_DENSE = 1,
   MEGB200_GRAD_FROBENIUS = 2,
   MEGB200_GRAD_SAMPLED = 3,
-  MEGB200_GRAD_STOCHASTIC = 4
+  MEGB200_GRAD_STOCHASTIC = 4,
+  MEGB200_GRAD_CALLBACK = 5 /* grad u computed by `apply` (the reference's callable grad_apply) */
 };
 
 typedef struct megb200_gradient {
@@ -106,6 +118,8 @@ typedef struct megb200_gradient {
   int64_t bsz;
   int64_t lda;
   double sigma;
+  megb200_apply_fn apply; /* CALLBACK */
+  void* apply_ctx;
 } megb200_gradient;
 
 /* Structured iterate (meg.py:47-92): V (device) n x r, lam (host) r, eps. */
@@ -200,6 +214,11 @@ int megb200_operator_apply(megb200_solver* s, const megb200_operator* op, const 
  * The low-rank factors are gathered into the handle's workspace. */
 int megb200_logmap_apply(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta,
                          const double* U, int64_t ldu, int32_t k, double* W, int64_t ldw);
+
+/* grad f(X_g) U for any gradient descriptor (the device form of calling the reference's
+ * grad_apply(u), meg.py:327-335): W (n x k, ld ldw) = G U.  Makes the descriptors callables. */
+int megb200_gradient_apply(megb200_solver* s, const megb200_gradient* g, const double* U, int64_t ldu, int32_t k,
+                           double* W, int64_t ldw);
 
 /* lanczos_top_r (linalg.py:130-241): the r algebraically largest eigenpairs. */
 int megb200_top_r(megb200_solver* s, const megb200_operator* op, int32_t r, const megb200_eig_opts* opts,

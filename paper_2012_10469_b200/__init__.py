@@ -28,7 +28,9 @@ from .meg import (
     step_eval,
     warm_start_wrap,
 )
+from .callbacks import device_callable
 from .objectives import (
+    CallbackGradient,
     DenseGradient,
     FrobeniusObjective,
     GradientOperator,
@@ -40,7 +42,7 @@ from .objectives import (
 )
 
 __all__ = [
-    "CertificateRecord", "DenseGradient", "HostStepResult", "HostStepper", "EighError", "EpsilonSchedule", "FrobeniusObjective", "GradientOperator",
+    "CallbackGradient", "CertificateRecord", "DenseGradient", "device_callable", "HostStepResult", "HostStepper", "EighError", "EpsilonSchedule", "FrobeniusObjective", "GradientOperator",
     "LanczosError", "LogmapOperator", "QuadMeasObjective", "QuadMeasStochasticOracle", "LowRankIterate", "LowRankStepResult", "ParameterError", "RankDeficiencyError",
     "SampledObjective", "StepConfig", "StochasticFrobeniusObjective", "SymmetricOperator", "TopREigen",
     "ZeroGradient", "certificate_cheap", "certificate_full", "eps_schedule_eval", "lanczos_top_r", "logmap_operator",

@@ -13,13 +13,17 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmegb200.so")
 
-OK, ERR_PARAM, ERR_LANCZOS, ERR_CUDA, ERR_KEPT_MASS, ERR_NO_DEVICE = range(6)
+OK, ERR_PARAM, ERR_LANCZOS, ERR_CUDA, ERR_KEPT_MASS, ERR_NO_DEVICE, ERR_CALLBACK = range(7)
 F64, F32 = 0, 1
-OP_NONE, OP_DENSE, OP_CSR = 0, 1, 2
-GRAD_ZERO, GRAD_DENSE, GRAD_FROBENIUS, GRAD_SAMPLED, GRAD_STOCHASTIC = range(5)
+OP_NONE, OP_DENSE, OP_CSR, OP_CALLBACK = 0, 1, 2, 3
+GRAD_ZERO, GRAD_DENSE, GRAD_FROBENIUS, GRAD_SAMPLED, GRAD_STOCHASTIC, GRAD_CALLBACK = range(6)
 
 c_double_p = C.POINTER(C.c_double)
 c_int32_p = C.POINTER(C.c_int32)
+
+
+# int apply(void* ctx, const double* U, int64_t ldu, int32_t k, double* W, int64_t ldw, void* stream)
+APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p)
 
 
 class Operator(C.Structure):
@@ -29,7 +33,7 @@ class Operator(C.Structure):
         ("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p), ("nnz", C.c_int64),
         ("scale", C.c_double),
         ("L", C.c_void_p), ("l", C.c_int64), ("ldl", C.c_int64), ("d", c_double_p),
-        ("alpha", C.c_double),
+        ("alpha", C.c_double), ("apply", APPLY_FN), ("apply_ctx", C.c_void_p),
     ]
 
 
@@ -40,6 +44,7 @@ class Gradient(C.Structure):
         ("rowptr", C.c_void_p), ("col", C.c_void_p), ("obs", C.c_void_p), ("nnz", C.c_int64),
         ("gV", C.c_void_p), ("g_r", C.c_int64), ("g_ldv", C.c_int64), ("g_lam", c_double_p), ("g_eps", C.c_double),
         ("A", C.c_void_p), ("bsz", C.c_int64), ("lda", C.c_int64), ("sigma", C.c_double),
+        ("apply", APPLY_FN), ("apply_ctx", C.c_void_p),
     ]
 
 
@@ -132,6 +137,8 @@ SIGNATURES = [
      [C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, c_double_p, c_int32_p, c_double_p]),
     ("megb200_objective_value", C.c_int, [C.c_void_p, C.POINTER(Gradient), C.c_double, C.c_double, c_double_p]),
     ("megb200_objective_value_direct", C.c_int, [C.c_void_p, C.POINTER(Gradient), c_double_p]),
+    ("megb200_gradient_apply", C.c_int,
+     [C.c_void_p, C.POINTER(Gradient), C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64]),
     ("megb200_dense_stats", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, c_double_p, c_double_p]),
     ("megb200_dual_gap", C.c_int,
      [C.c_void_p, C.POINTER(Gradient), C.POINTER(EigOpts), C.c_double, c_double_p, c_double_p]),

@@ -230,6 +230,8 @@ struct OpDev {
   int64_t ldg = 0;
   const double* Gu = nullptr;     // device U^T U when the caller already has it (with Eg)
   int64_t ldgu = 0;
+  megb200_apply_fn apply = nullptr;  // CALLBACK: the caller's block application
+  void* apply_ctx = nullptr;
 };
 
 // Live pass profiling (megb200_profile_enable): every prof-th streamed pass kernel is bracketed
@@ -262,6 +264,15 @@ int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu
   const int64_t n = s->n;
   int S = 0;
   const bool streamed = (op.kind == MEGB200_OP_DENSE || op.kind == MEGB200_OP_CSR) && op.scale != 0.0;
+  if (op.kind == MEGB200_OP_CALLBACK && op.scale != 0.0) {
+    // the caller's application writes the one partial slice (n x k, ld k) on the solver stream
+    const int rc = op.apply(op.apply_ctx, U, ldu, k, s->part, k, (void*)s->stream);
+    if (rc != 0) throw Error(MEGB200_ERR_CALLBACK, "apply callback failed (returned " + std::to_string(rc) + ")");
+    // the callback's last stream operation may be a copy: the programmatically dependent launches
+    // that follow only order against kernels, so its completion is waited for here
+    s->sync();
+    return 1;
+  }
   // live profiling brackets the streamed operand kernel only (the roofline's dominant kernel)
   const int ev0 = streamed ? prof_begin(s) : -1;
   if (op.kind == MEGB200_OP_DENSE && op.scale != 0.0) {
@@ -307,6 +318,9 @@ OpDev op_from_public(megb200_solver* s, const megb200_operator* op) {
   o.nnz = op->nnz;
   o.scale = op->scale;
   o.alpha = op->alpha;
+  o.apply = op->apply;
+  o.apply_ctx = op->apply_ctx;
+  if (o.kind == MEGB200_OP_CALLBACK && !o.apply) throw Error(MEGB200_ERR_PARAM, "callback operator without apply");
   if (o.kind == MEGB200_OP_DENSE && (!o.dense || o.ld < s->n)) throw Error(MEGB200_ERR_PARAM, "dense operand missing");
   if (o.kind == MEGB200_OP_CSR && (!o.rowptr || !o.col || !o.val)) throw Error(MEGB200_ERR_PARAM, "CSR operand missing");
   if (op->l > 0) {
@@ -747,6 +761,10 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
         }
       }
       const RRDecision dec = rr_decide(s, pk, newcols, nreq, tol);
+      static const bool dbg_rr = getenv("MEGB200_DEBUG_RR") != nullptr;  // diagnostics
+      if (dbg_rr)
+        fprintf(stderr, "rr pass %d cols %d newcols %d full %d rmax %.3e theta0 %.6f scale %.3f\n", run.passes, cols,
+                newcols, (int)full, dec.rmax, pk[0], dec.scale);
       scale = dec.scale;
       double best_max = 0.0;
       for (double v : best) best_max = std::max(best_max, v);
@@ -855,6 +873,9 @@ void check_gradient(megb200_solver* s, const megb200_gradient* g) {
       if (g->kind == MEGB200_GRAD_STOCHASTIC && (!g->A || g->bsz < 1))
         throw Error(MEGB200_ERR_PARAM, "stochastic minibatch missing");
       break;
+    case MEGB200_GRAD_CALLBACK:
+      if (!g->apply) throw Error(MEGB200_ERR_PARAM, "callback gradient without apply");
+      break;
     case MEGB200_GRAD_SAMPLED:
       if (!g->rowptr || !g->col || !g->obs) throw Error(MEGB200_ERR_PARAM, "sampled pattern missing");
       if (g->nnz > s->max_nnz) throw Error(MEGB200_ERR_PARAM, "nnz exceeds the solver's max_nnz");
@@ -863,7 +884,8 @@ void check_gradient(megb200_solver* s, const megb200_gradient* g) {
     default:
       throw Error(MEGB200_ERR_PARAM, "unknown gradient kind");
   }
-  if (g->gV && (g->g_r >= g->n || !(g->g_eps > 0.0)) && g->kind != MEGB200_GRAD_ZERO && g->kind != MEGB200_GRAD_DENSE)
+  if (g->gV && (g->g_r >= g->n || !(g->g_eps > 0.0)) && g->kind != MEGB200_GRAD_ZERO && g->kind != MEGB200_GRAD_DENSE &&
+      g->kind != MEGB200_GRAD_CALLBACK)
     throw Error(MEGB200_ERR_PARAM, "invalid gradient iterate");
 }
 
@@ -939,6 +961,12 @@ StepOperator build_step_operator(megb200_solver* s, const megb200_iterate* x, co
       op.dtype = g->dtype;
       op.dense = g->dense;
       op.ld = g->ld;
+      op.scale = -eta;
+      break;
+    case MEGB200_GRAD_CALLBACK:
+      op.kind = MEGB200_OP_CALLBACK;
+      op.apply = g->apply;
+      op.apply_ctx = g->apply_ctx;
       op.scale = -eta;
       break;
     case MEGB200_GRAD_FROBENIUS:
@@ -1219,6 +1247,82 @@ int megb200_logmap_apply(megb200_solver* s, const megb200_iterate* x, const megb
     if (!U || !W || k < 1) throw Error(MEGB200_ERR_PARAM, "invalid block");
     StepOperator so = build_step_operator(s, x, g, eta);
     apply_op_wide(s, so.op, U, ldu, k, W, ldw);
+  });
+}
+
+int megb200_gradient_apply(megb200_solver* s, const megb200_gradient* g, const double* U, int64_t ldu, int32_t k,
+                           double* W, int64_t ldw) {
+  return guarded_impl([&] {
+    if (!s) throw Error(MEGB200_ERR_PARAM, "solver is NULL");
+    check_gradient(s, g);
+    if (!U || !W || k < 1) throw Error(MEGB200_ERR_PARAM, "invalid block");
+    Launch L = s->launch();
+    const int64_t n = s->n;
+    // grad u as a device operator: scale * Op u + L diag(d) L^T u + alpha u
+    OpDev op;
+    std::vector<double> d;
+    std::vector<double> cg;
+    double tail_g = 0.0;
+    if (g->kind == MEGB200_GRAD_FROBENIUS || g->kind == MEGB200_GRAD_STOCHASTIC || g->kind == MEGB200_GRAD_SAMPLED)
+      x_coeffs(n, g->g_r, g->g_lam, g->g_eps, cg, tail_g);
+    switch (g->kind) {
+      case MEGB200_GRAD_ZERO:
+        op.kind = MEGB200_OP_NONE;
+        break;
+      case MEGB200_GRAD_DENSE:
+        op.kind = MEGB200_OP_DENSE;
+        op.dtype = g->dtype;
+        op.dense = g->dense;
+        op.ld = g->ld;
+        op.scale = 1.0;
+        break;
+      case MEGB200_GRAD_CALLBACK:
+        op.kind = MEGB200_OP_CALLBACK;
+        op.apply = g->apply;
+        op.apply_ctx = g->apply_ctx;
+        op.scale = 1.0;
+        break;
+      case MEGB200_GRAD_FROBENIUS:
+      case MEGB200_GRAD_STOCHASTIC: {
+        // X_g - M (+ sigma ((1/b) A A^T - I/n)): -M streamed, the rest low-rank
+        op.kind = MEGB200_OP_DENSE;
+        op.dtype = g->dtype;
+        op.dense = g->dense;
+        op.ld = g->ld;
+        op.scale = -1.0;
+        op.alpha = tail_g;
+        d = cg;
+        const bool stoch = g->kind == MEGB200_GRAD_STOCHASTIC;
+        const int64_t l = g->g_r + (stoch ? g->bsz : 0);
+        if (l > s->max_lowrank) throw Error(MEGB200_ERR_PARAM, "low-rank width exceeds the solver's max_lowrank");
+        copy_block(L, n, (int)g->g_r, g->gV, g->g_ldv, s->L, s->max_lowrank);
+        if (stoch) {
+          copy_block(L, n, (int)g->bsz, g->A, g->lda, s->L + g->g_r, s->max_lowrank);
+          for (int64_t j = 0; j < g->bsz; ++j) d.push_back(g->sigma / (double)g->bsz);
+          op.alpha -= g->sigma / (double)n;
+        }
+        op.L = s->L;
+        op.ldl = s->max_lowrank;
+        op.l = (int)l;
+        break;
+      }
+      case MEGB200_GRAD_SAMPLED:
+        s->h2d(s->small, cg.data(), (int64_t)cg.size());
+        csr_values(L, n, g->rowptr, g->col, g->obs, g->gV, g->g_ldv, (int)g->g_r, s->small, tail_g, s->csr_g, nullptr,
+                   0);
+        op.kind = MEGB200_OP_CSR;
+        op.rowptr = g->rowptr;
+        op.col = g->col;
+        op.val = s->csr_g;
+        op.nnz = g->nnz;
+        op.scale = 1.0;
+        break;
+    }
+    if (op.l > 0) {
+      s->h2d(s->dvec, d.data(), op.l);
+      op.d_dev = s->dvec;
+    }
+    apply_op_wide(s, op, U, ldu, k, W, ldw);
   });
 }
 

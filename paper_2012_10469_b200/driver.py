@@ -20,7 +20,7 @@ import torch
 from . import _lib, runtime
 from .errors import ParameterError
 from .linalg import _eig_opts
-from .meg import EpsilonSchedule, LowRankIterate, StepConfig
+from .meg import EpsilonSchedule, LowRankIterate, StepConfig, effective_settings
 from .objectives import FrobeniusObjective, SampledObjective, StochasticFrobeniusObjective
 
 
@@ -95,7 +95,8 @@ def run(
     hold: list = []
     xs, gs = x0.struct(hold), g.struct(hold)
     warm = x0.warm_block if isinstance(x0.warm_block, torch.Tensor) and x0.warm_block.shape[0] == n else None
-    opts = _eig_opts(max(svd_tol, g.tol_floor), None, 0, svd_subspace, 12, block, None, warm,
+    tol_eff, sub_eff = effective_settings(svd_tol, svd_subspace, g)
+    opts = _eig_opts(tol_eff, None, 0, sub_eff, 12, block, None, warm,
                      warm_orthonormal=warm is not None and x0.warm_orth_err <= 1e-13)
     sc = _schedule(eps_schedule, eta, eta_decay, objective)
     if cert_every < 0:

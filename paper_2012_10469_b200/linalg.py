@@ -10,9 +10,11 @@ Jacobi Rayleigh-Ritz, same convergence rule (every residual <= tol *
 max(1, max|theta|), linalg.py:214-215) and the same failure contract
 (LanczosError carrying the best residuals).
 
-Python callables cannot run inside the device solver; operators must be
-built from device data (`from_dense`, `from_csr`, or the descriptors in
-`meg` / `objectives`).
+Operators built from device data (`from_dense`, `from_csr`, or the descriptors
+in `meg` / `objectives`) stream from HBM inside the pass kernels.  The
+reference's form `SymmetricOperator(dim, apply_fn)` with a Python callable is
+accepted too: the native solver calls it once per block pass through the C
+ABI's callback operator (callbacks.py).
 """
 
 from __future__ import annotations
@@ -24,6 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib, runtime
+from .callbacks import checked
 from .errors import EighError, LanczosError, ParameterError, RankDeficiencyError  # noqa: F401  (re-export)
 
 
@@ -50,6 +53,7 @@ class TopREigen:
     residual_norms: np.ndarray  # (r,)
     passes: int = 0
     restarts: int = 0
+    subspace_effective: int | None = None  # basis bound as applied (<= runtime.MAX_BASIS)
 
 
 class SymmetricOperator:
@@ -57,12 +61,14 @@ class SymmetricOperator:
 
     def __init__(self, dim: int, apply_fn=None, *, dense=None, csr=None, scale: float = 1.0, L=None, d=None,
                  alpha: float = 0.0):
-        if apply_fn is not None:
-            raise TypeError(
-                "the B200 solver cannot call back into Python per application; build the operator from device "
-                "data (SymmetricOperator.from_dense / from_csr or the meg/objectives descriptors)"
-            )
+        """`SymmetricOperator(dim, apply_fn)` is the reference's form (linalg.py:89-94): apply_fn
+        takes a numpy (n, k) block (or torch CUDA tensors when marked with
+        callbacks.device_callable) and is called once per block pass through the C ABI's callback
+        operator.  Device data (dense / csr / low-rank) is the fast path."""
+        from .callbacks import ApplyCallback
+
         self.dim = int(dim)
+        self.callback = ApplyCallback(apply_fn, self.dim) if apply_fn is not None else None
         self.dense = dense  # torch (n, n) f64/f32 contiguous, symmetric
         self.csr = csr  # (rowptr int32, col int32, val f64) torch tensors
         self.scale = float(scale)
@@ -102,6 +108,9 @@ class SymmetricOperator:
             op.kind = _lib.OP_CSR
             op.rowptr, op.col, op.val = rp.data_ptr(), cl.data_ptr(), vl.data_ptr()
             op.nnz = cl.numel()
+        elif self.callback is not None:
+            op.kind = _lib.OP_CALLBACK
+            op.apply = self.callback.c_fn
         else:
             op.kind = _lib.OP_NONE
         if self.L is not None and self.L.shape[1] > 0:
@@ -131,8 +140,8 @@ class SymmetricOperator:
         s = self._solver()
         keep: list = []
         op = self._struct(keep)
-        runtime.check(s.lib.megb200_operator_apply(s.handle, C.byref(op), ut.data_ptr(), ut.stride(0), k,
-                                                   w.data_ptr(), w.stride(0)))
+        checked(s.lib.megb200_operator_apply(s.handle, C.byref(op), ut.data_ptr(), ut.stride(0), k,
+                                             w.data_ptr(), w.stride(0)), [self.callback])
         if vec:
             w = w.reshape(-1)
         return w.cpu().numpy() if is_np else w
@@ -180,13 +189,24 @@ def lanczos_top_r(
     best residual norms when the tolerance is not reached.
     """
     if not isinstance(op, SymmetricOperator):
-        raise TypeError("lanczos_top_r needs a device SymmetricOperator")
+        if hasattr(op, "dim") and hasattr(op, "apply"):  # any object with the reference's operator interface
+            op = SymmetricOperator(op.dim, op.apply)
+        else:
+            raise TypeError("lanczos_top_r needs a SymmetricOperator (or an object with .dim and .apply)")
     n = op.dim
     if not 1 <= r < n:
         raise ParameterError(f"need 1 <= r < n, got r={r}, n={n}")
     s = op._solver()
     keep: list = []
     ops = op._struct(keep)
+    if subspace is not None and subspace > runtime.MAX_BASIS:
+        import warnings
+
+        from .meg import SolverSettingWarning
+
+        warnings.warn(f"subspace={subspace} bounded by the device Rayleigh-Ritz limit {runtime.MAX_BASIS}",
+                      SolverSettingWarning, stacklevel=2)
+        subspace = runtime.MAX_BASIS
     opts = _eig_opts(tol, max_iter, seed, subspace, restarts, block)
     vals = np.zeros(r)
     res = np.zeros(r)
@@ -197,7 +217,7 @@ def lanczos_top_r(
     out.eigenvectors = vecs.data_ptr()
     out.ld_vec = r
     rc = s.lib.megb200_top_r(s.handle, C.byref(ops), int(r), C.byref(opts), C.byref(out))
-    runtime.check(rc, residual_norms=res.copy())
+    checked(rc, [op.callback], residual_norms=res.copy())
     return TopREigen(
         r=r,
         eigenvalues=vals,
@@ -205,6 +225,7 @@ def lanczos_top_r(
         residual_norms=res,
         passes=int(out.passes),
         restarts=int(out.restarts),
+        subspace_effective=subspace,
     )
 
 

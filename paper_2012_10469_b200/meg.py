@@ -27,6 +27,7 @@ import numpy as np
 import torch
 
 from . import _lib, runtime
+from .callbacks import checked
 from .errors import ParameterError
 from .linalg import SymmetricOperator, _eig_opts, symmetrize  # noqa: F401
 from .objectives import GradientOperator
@@ -259,14 +260,18 @@ def merge_certificates(cheap: CertificateRecord, full: CertificateRecord) -> Cer
 
 
 def _as_gradient(x: LowRankIterate, grad_apply) -> GradientOperator:
+    """A device descriptor as is; any other callable through the callback operator (the
+    reference's `grad_apply` contract, meg.py:327-335: numpy blocks in and out, or torch CUDA
+    tensors when marked with callbacks.device_callable)."""
     if isinstance(grad_apply, GradientOperator):
         if grad_apply.n != x.n:
             raise ParameterError(f"gradient dimension {grad_apply.n} does not match n={x.n}")
         return grad_apply
-    raise TypeError(
-        "grad_apply must be a device gradient descriptor (objectives.DenseGradient, FrobeniusObjective(...)"
-        ".grad_operator(x), ...): the B200 step cannot call a Python callable per Krylov application"
-    )
+    if callable(grad_apply):
+        from .objectives import CallbackGradient
+
+        return CallbackGradient(x.n, grad_apply)
+    raise TypeError("grad_apply must be a device gradient descriptor or a callable u -> grad f(X) u")
 
 
 class LogmapOperator:
@@ -286,8 +291,8 @@ class LogmapOperator:
         s = self.grad.solver()
         keep: list = []
         xs, gs = self.x.struct(keep), self.grad.struct(keep)
-        runtime.check(s.lib.megb200_logmap_apply(s.handle, C.byref(xs), C.byref(gs), self.eta, ut.data_ptr(),
-                                                 ut.stride(0), ut.shape[1], w.data_ptr(), w.stride(0)))
+        checked(s.lib.megb200_logmap_apply(s.handle, C.byref(xs), C.byref(gs), self.eta, ut.data_ptr(),
+                                           ut.stride(0), ut.shape[1], w.data_ptr(), w.stride(0)), [self.grad.callback])
         if vec:
             w = w.reshape(-1)
         return w.cpu().numpy() if is_np else w
@@ -319,6 +324,31 @@ class LowRankStepResult:
     residual_norms: np.ndarray | None = field(repr=False, default=None)
     passes: int = 0
     restarts: int = 0
+    svd_tol_effective: float = 0.0  # the residual rule's tol as applied (float32 operands: >= F32_TOL_FLOOR)
+    svd_subspace_effective: int | None = None  # the Krylov basis bound as applied (<= runtime.MAX_BASIS)
+
+
+class SolverSettingWarning(UserWarning):
+    """A solver setting was applied in a modified form (reported in the step result as well)."""
+
+
+def effective_settings(svd_tol: float, svd_subspace: int | None, g) -> tuple[float, int | None]:
+    """(tol, basis bound) the device solver applies: float32 operands raise the residual rule's tol
+    to objectives.F32_TOL_FLOOR (their product noise sits above 1e-10); the basis is bounded by the
+    shared-memory Rayleigh-Ritz limit runtime.MAX_BASIS (the block solver then restarts: the same
+    rule linalg.py:214-216, more passes).  Either change is reported once per call site."""
+    import warnings
+
+    tol = max(float(svd_tol), g.tol_floor)
+    if tol > svd_tol:
+        warnings.warn(f"svd_tol={svd_tol:g} raised to {tol:g} for a float32 operand", SolverSettingWarning,
+                      stacklevel=3)
+    sub = svd_subspace
+    if sub is not None and sub > runtime.MAX_BASIS:
+        warnings.warn(f"svd_subspace={sub} bounded by the device Rayleigh-Ritz limit {runtime.MAX_BASIS}",
+                      SolverSettingWarning, stacklevel=3)
+        sub = runtime.MAX_BASIS
+    return tol, sub
 
 
 def lowrank_meg_step(
@@ -354,7 +384,8 @@ def lowrank_meg_step(
     hold: list = []
     xs, gs = x.struct(hold), g.struct(hold)
     warm = x.warm_block if isinstance(x.warm_block, torch.Tensor) and x.warm_block.shape[0] == n else None
-    opts = _eig_opts(max(svd_tol, g.tol_floor), max_passes, svd_seed, svd_subspace, 12, block, keep, warm,
+    tol_eff, sub_eff = effective_settings(svd_tol, svd_subspace, g)
+    opts = _eig_opts(tol_eff, max_passes, svd_seed, sub_eff, 12, block, keep, warm,
                      warm_orthonormal=warm is not None and x.warm_orth_err <= 1e-13)
     v_next = torch.empty((n, r), dtype=torch.float64, device=dev)
     ritz = torch.empty((n, runtime.MAX_BLOCK), dtype=torch.float64, device=dev)
@@ -373,7 +404,7 @@ def lowrank_meg_step(
     out.ld_ritz = ritz.stride(0)
     rc = s.lib.megb200_lowrank_meg_step(s.handle, C.byref(xs), C.byref(gs), float(eta), float(eps_next),
                                         C.byref(opts), C.byref(out))
-    runtime.check(rc, residual_norms=res.copy())
+    checked(rc, [g.callback], residual_norms=res.copy())
     nxt = LowRankIterate(n, r, v_next, lam, eps_next, warm_block=ritz[:, : out.ritz_cols],
                          warm_orth_err=out.ritz_orth_err, _gram_err=out.gram_err)
     cert = CertificateRecord(iteration=None, lhs_cheap=out.lhs_cheap, holds_cheap=bool(out.holds_cheap),
@@ -389,6 +420,8 @@ def lowrank_meg_step(
         residual_norms=res,
         passes=int(out.passes),
         restarts=int(out.restarts),
+        svd_tol_effective=tol_eff,
+        svd_subspace_effective=sub_eff,
     )
 
 
@@ -488,7 +521,8 @@ def lowrank_meg_step_host(
     out_ptr = out.data_ptr() if isinstance(out, torch.Tensor) else out.ctypes.data
     ld_out = out.stride(0) if isinstance(out, torch.Tensor) else out.strides[0] // 8
     warm_t = warm if isinstance(warm, torch.Tensor) and warm.shape[0] == n else None
-    opts = _eig_opts(max(svd_tol, g.tol_floor), None, svd_seed, svd_subspace, 12, block, None, warm_t,
+    tol_eff, sub_eff = effective_settings(svd_tol, svd_subspace, g)
+    opts = _eig_opts(tol_eff, None, svd_seed, sub_eff, 12, block, None, warm_t,
                      warm_orthonormal=warm_t is not None and warm_orth_err <= 1e-13)
     ritz = torch.empty((n, runtime.MAX_BLOCK), dtype=torch.float64, device=runtime.device())
     lam_next, y, mu, res = np.zeros(r), np.zeros(r + 1), np.zeros(r + 1), np.zeros(r + 1)
@@ -498,7 +532,7 @@ def lowrank_meg_step_host(
     o.ld_ritz = ritz.stride(0)
     rc = s.lib.megb200_lowrank_meg_step_host(s.handle, C.byref(it), C.byref(gs), float(eta), float(eps_next),
                                              C.byref(opts), C.c_void_p(out_ptr), int(ld_out), C.byref(o))
-    runtime.check(rc, residual_norms=res.copy())
+    checked(rc, [getattr(g, "callback", None)], residual_norms=res.copy())
     cert = CertificateRecord(iteration=None, lhs_cheap=o.lhs_cheap, holds_cheap=bool(o.holds_cheap),
                              threshold=o.threshold)
     return HostStepResult(V=out, lam=lam_next, eps=float(eps_next), cert=cert, lambda_r_plus_1=o.lambda_r_plus_1,
@@ -530,8 +564,8 @@ class HostStepper:
         self.s = g.solver()
         self._hold: list = [g]
         self.gs = g.struct(self._hold)
-        self.tol = max(svd_tol, g.tol_floor)
-        self.subspace, self.block = svd_subspace, block
+        self.tol, self.subspace = effective_settings(svd_tol, svd_subspace, g)
+        self.block = block
         dev = runtime.device()
         self.ritz = [torch.empty((self.n, runtime.MAX_BLOCK), dtype=torch.float64, device=dev) for _ in range(2)]
         self.k = 0
@@ -594,7 +628,7 @@ class HostStepper:
         rc = self.fn(self.s.handle, C.byref(it), C.byref(self.gs), float(eta), float(eps_next), C.byref(opts),
                      C.c_void_p(out.data_ptr()), self.r, C.byref(o))
         if rc:
-            runtime.check(rc, residual_norms=self.res.copy())
+            checked(rc, [getattr(self._hold[0], "callback", None)], residual_norms=self.res.copy())
         cert = CertificateRecord(iteration=None, lhs_cheap=o.lhs_cheap, holds_cheap=bool(o.holds_cheap),
                                  threshold=o.threshold)
         return HostStepResult(V=out, lam=self.lam_next.copy(), eps=float(eps_next), cert=cert,

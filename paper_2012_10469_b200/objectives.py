@@ -35,8 +35,9 @@ class GradientOperator:
     """A gradient evaluated at a bound iterate (device descriptor, see module doc)."""
 
     def __init__(self, kind: int, n: int, *, dense=None, csr=None, obs=None, x=None, A=None, sigma: float = 0.0,
-                 owner=None):
+                 owner=None, callback=None):
         self.kind = kind
+        self.callback = callback  # callbacks.ApplyCallback (GRAD_CALLBACK)
         self.n = int(n)
         self.dense = dense
         self.csr = csr
@@ -91,14 +92,48 @@ class GradientOperator:
             g.bsz = self.A.shape[1]
             g.lda = self.A.stride(0)
             g.sigma = self.sigma
+        if self.callback is not None:
+            g.apply = self.callback.c_fn
         return g
 
     def solver(self):
         return runtime.solver_for(self.n, max_nnz=self.nnz,
                                   max_lowrank=max(runtime.MAX_LOWRANK, 2 * self.lowrank_width + 8))
 
-    def __call__(self, u):  # pragma: no cover - guard against reference-style use
-        raise TypeError("device gradient descriptors are consumed by lowrank_meg_step; they are not host callables")
+    def __call__(self, u):
+        """grad f(X_g) u, u of shape (n,) or (n, k): the descriptor is also the reference's
+        `grad_apply` callable (meg.py:327-335), evaluated on the device (megb200_gradient_apply);
+        numpy in -> numpy out, torch in -> torch out."""
+        from .callbacks import checked
+
+        is_np = not isinstance(u, torch.Tensor)
+        vec = u.ndim == 1
+        ut = runtime.as_device_f64(u)
+        if vec:
+            ut = ut.reshape(-1, 1).contiguous()
+        if ut.shape[0] != self.n:
+            raise ParameterError(f"expected {self.n} rows, got {ut.shape[0]}")
+        w = torch.empty_like(ut)
+        s = self.solver()
+        keep: list = []
+        gs = self.struct(keep)
+        checked(s.lib.megb200_gradient_apply(s.handle, C.byref(gs), ut.data_ptr(), ut.stride(0), ut.shape[1],
+                                             w.data_ptr(), w.stride(0)), [self.callback])
+        if vec:
+            w = w.reshape(-1)
+        return w.cpu().numpy() if is_np else w
+
+
+class CallbackGradient(GradientOperator):
+    """grad u = fn(u) for a caller-supplied callable: the reference's `grad_apply` contract
+    (meg.py:327-335; e.g. `lambda u: g @ u`, test_meg.py:153).  fn takes and returns numpy
+    blocks (n, k) unless marked with callbacks.device_callable (torch CUDA tensors on the
+    solver stream).  Called once per block pass by the native solver (callbacks.py)."""
+
+    def __init__(self, n: int, fn, device: bool | None = None):
+        from .callbacks import ApplyCallback
+
+        super().__init__(_lib.GRAD_CALLBACK, n, callback=ApplyCallback(fn, n, device))
 
 
 class ZeroGradient(GradientOperator):

@@ -96,6 +96,10 @@ def check(rc: int, residual_norms=None) -> None:
         raise AssertionError("kept mass vanished despite max-shift")
     if rc == _lib.ERR_NO_DEVICE:
         raise _lib.NativeLibraryError(msg)
+    if rc == _lib.ERR_CALLBACK:
+        from .callbacks import CallbackError
+
+        raise CallbackError(msg)
     raise RuntimeError(f"megb200 CUDA error: {msg}")
 
 

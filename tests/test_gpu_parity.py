@@ -113,7 +113,7 @@ def test_eps_next_validation(pb):
     with pytest.raises(pb.ParameterError):
         pb.lowrank_meg_step(x, pb.ZeroGradient(8), eta=1.0, eps_next=0.8)
     with pytest.raises(TypeError):
-        pb.lowrank_meg_step(x, lambda u: u, eta=1.0, eps_next=0.1)
+        pb.lowrank_meg_step(x, 5, eta=1.0, eps_next=0.1)
 
 
 def test_iterate_validation(pb):
@@ -698,3 +698,80 @@ def test_full_size_prefix_run_loop_matches_reference(pb, name, cfg_name):
 
     dev = GpuObjective(cfg, host).dev
     _run_loop_vs_golden(pb, dev, _golden_x0(pb, ref), ref, cfg, TOL[cfg.dtype])
+
+
+# ---------------------------------------------------------------------------
+# the reference's callable contract (linalg.py:81-94, meg.py:327-335) through the callback operator
+
+
+def test_callable_operator_matches_dense(pb):
+    """SymmetricOperator(dim, apply_fn) with a numpy callable (test_linalg.py's usage) and with a
+    device (torch) callable give the dense operator's eigenpairs."""
+    import torch
+
+    from paper_2012_10469_b200.callbacks import device_callable
+
+    a = random_symmetric(300, np.random.default_rng(21))
+    ref = pb.lanczos_top_r(pb.SymmetricOperator.from_dense(a), r=4, seed=3)
+    got = pb.lanczos_top_r(pb.SymmetricOperator(300, lambda u: a @ u), r=4, seed=3)
+    at = torch.as_tensor(a, device="cuda")
+    dev = pb.lanczos_top_r(pb.SymmetricOperator(300, device_callable(lambda u: at @ u)), r=4, seed=3)
+    scale = np.abs(np.linalg.eigvalsh(a)).max()
+    for t in (got, dev):
+        assert np.max(np.abs(t.eigenvalues - ref.eigenvalues)) <= 1e-12 * scale
+        assert np.max(np.abs(np.abs(t.eigenvectors.T @ ref.eigenvectors) - np.eye(4))) <= 1e-8
+    assert np.allclose(pb.SymmetricOperator(300, lambda u: a @ u).apply(np.eye(300)[:, :3]), a[:, :3], atol=1e-14)
+
+
+def test_callable_grad_apply_matches_descriptor(pb):
+    """lowrank_meg_step with the reference-style `lambda u: g @ u` (test_meg.py:153) equals the
+    DenseGradient descriptor step, and the descriptors are themselves callables."""
+    rng = np.random.default_rng(9)
+    n, r = 120, 4
+    q, lam, eps = random_lowrank_iterate_np(n, r, rng)
+    g = om.symmetrize(rng.standard_normal((n, n))) * 0.2
+    x = pb.LowRankIterate(n, r, q, lam, eps)
+    ref = pb.lowrank_meg_step(x, pb.DenseGradient(g), eta=0.7, eps_next=0.05, svd_seed=2)
+    got = pb.lowrank_meg_step(x, lambda u: g @ u, eta=0.7, eps_next=0.05, svd_seed=2)
+    assert np.max(np.abs(got.top_eigenvalues - ref.top_eigenvalues) / ref.top_eigenvalues) <= 1e-12
+    assert np.max(np.abs(got.iterate.densify() - ref.iterate.densify())) <= 1e-12
+    assert abs(got.cert.lhs_cheap - ref.cert.lhs_cheap) <= 1e-12 * max(1.0, abs(ref.cert.lhs_cheap))
+    u = rng.standard_normal((n, 3))
+    m = om.symmetrize(rng.standard_normal((n, n)))
+    dev = pb.FrobeniusObjective(m).grad_operator(x)
+    assert normwise(dev(u), x.densify() @ u - m @ u) <= 1e-13
+    assert normwise(dev(u[:, 0]), x.densify() @ u[:, 0] - m @ u[:, 0]) <= 1e-13
+    assert normwise(pb.DenseGradient(g)(u), g @ u) <= 1e-14
+
+
+def test_callable_errors_propagate(pb):
+    rng = np.random.default_rng(3)
+    q, lam, eps = random_lowrank_iterate_np(50, 3, rng)
+    x = pb.LowRankIterate(50, 3, q, lam, eps)
+
+    def bad(u):
+        raise ValueError("user gradient failed")
+
+    with pytest.raises(ValueError, match="user gradient failed"):
+        pb.lowrank_meg_step(x, bad, eta=1.0, eps_next=0.1)
+    with pytest.raises(ValueError):
+        pb.lanczos_top_r(pb.SymmetricOperator(50, bad), r=2)
+
+
+def test_solver_settings_reported(pb):
+    """svd_subspace beyond the device basis limit and the float32 tolerance floor are applied
+    visibly: a SolverSettingWarning and the effective values in the result."""
+    from paper_2012_10469_b200.meg import SolverSettingWarning
+
+    rng = np.random.default_rng(4)
+    n, r = 400, 3
+    q, lam, eps = random_lowrank_iterate_np(n, r, rng)
+    m = om.symmetrize(rng.standard_normal((n, n))) * 0.01
+    x = pb.LowRankIterate(n, r, q, lam, eps)
+    with pytest.warns(SolverSettingWarning):
+        res = pb.lowrank_meg_step(x, pb.FrobeniusObjective(m).grad_operator(x), 1.0, 0.05, svd_subspace=200)
+    assert res.svd_subspace_effective == pb.runtime.MAX_BASIS
+    with pytest.warns(SolverSettingWarning):
+        res32 = pb.lowrank_meg_step(x, pb.FrobeniusObjective(m, dtype="f32").grad_operator(x), 1.0, 0.05)
+    assert res32.svd_tol_effective == pb.objectives.F32_TOL_FLOOR
+    assert res.svd_tol_effective == 1e-10
