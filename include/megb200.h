@@ -215,6 +215,13 @@ int megb200_operator_apply(megb200_solver* s, const megb200_operator* op, const 
 int megb200_logmap_apply(megb200_solver* s, const megb200_iterate* x, const megb200_gradient* g, double eta,
                          const double* U, int64_t ldu, int32_t k, double* W, int64_t ldw);
 
+/* All eigenpairs of a small dense symmetric matrix A (m <= 112, device, row-major, ld lda):
+ * w (device, m) non-increasing, V (device, m x m row-major, column j = eigenvector j).  The
+ * Rayleigh-Ritz solver of the block Krylov method (tridiagonalisation + multisection + twisted
+ * factorisation, verified to 1e-12 ||A||_F, Jacobi fallback) used directly; the dense-shadow
+ * diagnostics (exact MEG, meg.py:269-284; Bregman distances, entropy.py:76-96) call it. */
+int megb200_sym_eigh(megb200_solver* s, const double* A, int64_t lda, int32_t m, double* w, double* V);
+
 /* grad f(X_g) U for any gradient descriptor (the device form of calling the reference's
  * grad_apply(u), meg.py:327-335): W (n x k, ld ldw) = G U.  Makes the descriptors callables. */
 int megb200_gradient_apply(megb200_solver* s, const megb200_gradient* g, const double* U, int64_t ldu, int32_t k,

@@ -469,3 +469,68 @@ def dual_gap_core(grad: np.ndarray, trace_term: float, tau: float = 1.0, seed: i
     top = lanczos_top_r(SymmetricOperator.from_dense(-grad), 1, seed=seed)
     v = top.eigenvectors[:, 0]
     return trace_term - tau * float(v @ grad @ v)
+
+
+# ---------------------------------------------------------------------------
+# dense-shadow diagnostics -- test oracle only
+
+
+def exact_meg_step(z, grad, eta):
+    """exp(log Z - eta grad) / trace (meg.py:269-284)."""
+    w, v = full_eigh(z)
+    if w[-1] <= 0:
+        raise ParameterError(f"iterate must be positive definite, min eigenvalue {w[-1]:.3e}")
+    log_z = (v * np.log(w)) @ v.T
+    mu, ev = full_eigh(symmetrize(log_z - eta * np.asarray(grad, dtype=float)))
+    y = np.exp(mu - mu[0])
+    y /= y.sum()
+    return symmetrize((ev * y) @ ev.T)
+
+
+EIG_CLAMP = 1e-300  # entropy.py:21
+MASS_TOL = 1e-14  # entropy.py:22
+
+
+def entropy_sum(w):
+    """sum lambda log lambda, 0 log 0 = 0 (entropy.py:54-58)."""
+    w = np.maximum(w, 0.0)
+    m = w > EIG_CLAMP
+    return float(np.sum(w[m] * np.log(w[m])))
+
+
+def bregman(x, y):
+    """(value, finite, clamped) of Tr(X log X - X log Y) (entropy.py:76-96)."""
+    x, y = symmetrize(x), symmetrize(y)
+    wx, _ = full_eigh(x)
+    wy, vy = full_eigh(y)
+    mass = np.einsum("ij,ji->i", vy.T @ x, vy)
+    heavy = mass > MASS_TOL
+    if np.any(heavy & (wy <= 0.0)):
+        return math.inf, False, True
+    clamped = bool(np.any(heavy & (wy <= EIG_CLAMP)))
+    cross = float(np.sum(mass * np.log(np.maximum(wy, EIG_CLAMP))))
+    return entropy_sum(wx) - cross, True, clamped
+
+
+def structured_log_trace(x, y):
+    """Tr(X log Y), Y structured; X dense or structured (entropy.py:108-125)."""
+    log_kept = np.log((1.0 - y.eps) * y.lam)
+    log_tail = math.log(y.eps / (y.n - y.r))
+    if isinstance(x, np.ndarray):
+        mass = np.einsum("ij,ij->j", y.V, x @ y.V)
+        trace_x = float(np.trace(x))
+    else:
+        sq = (x.V.T @ y.V) ** 2
+        mass = (1.0 - x.eps) * (x.lam @ sq) + (x.eps / (x.n - x.r)) * (1.0 - sq.sum(axis=0))
+        trace_x = 1.0
+    return float(np.sum(mass * (log_kept - log_tail))) + log_tail * trace_x
+
+
+def bregman_structured(x, y):
+    """Tr(X log X - X log Y), Y structured (entropy.py:128-142)."""
+    if isinstance(x, np.ndarray):
+        own = entropy_sum(full_eigh(symmetrize(x))[0])
+    else:
+        kept = (1.0 - x.eps) * x.lam
+        own = entropy_sum(kept) + x.eps * math.log(x.eps / (x.n - x.r))
+    return own - structured_log_trace(x, y)

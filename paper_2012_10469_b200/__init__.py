@@ -29,6 +29,7 @@ from .meg import (
     warm_start_wrap,
 )
 from .callbacks import device_callable
+from .shadow import BregmanValue, bregman, bregman_structured, exact_meg_step, shadow_lowrank_step
 from .objectives import (
     CallbackGradient,
     DenseGradient,
@@ -42,6 +43,7 @@ from .objectives import (
 )
 
 __all__ = [
+    "BregmanValue", "bregman", "bregman_structured", "exact_meg_step", "shadow_lowrank_step",
     "CallbackGradient", "CertificateRecord", "DenseGradient", "device_callable", "HostStepResult", "HostStepper", "EighError", "EpsilonSchedule", "FrobeniusObjective", "GradientOperator",
     "LanczosError", "LogmapOperator", "QuadMeasObjective", "QuadMeasStochasticOracle", "LowRankIterate", "LowRankStepResult", "ParameterError", "RankDeficiencyError",
     "SampledObjective", "StepConfig", "StochasticFrobeniusObjective", "SymmetricOperator", "TopREigen",

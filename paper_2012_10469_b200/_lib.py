@@ -137,6 +137,7 @@ SIGNATURES = [
      [C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64, c_double_p, c_int32_p, c_double_p]),
     ("megb200_objective_value", C.c_int, [C.c_void_p, C.POINTER(Gradient), C.c_double, C.c_double, c_double_p]),
     ("megb200_objective_value_direct", C.c_int, [C.c_void_p, C.POINTER(Gradient), c_double_p]),
+    ("megb200_sym_eigh", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     ("megb200_gradient_apply", C.c_int,
      [C.c_void_p, C.POINTER(Gradient), C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64]),
     ("megb200_dense_stats", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, c_double_p, c_double_p]),

@@ -1250,6 +1250,15 @@ int megb200_logmap_apply(megb200_solver* s, const megb200_iterate* x, const megb
   });
 }
 
+int megb200_sym_eigh(megb200_solver* s, const double* A, int64_t lda, int32_t m, double* w, double* V) {
+  return guarded_impl([&] {
+    if (!s || !A || !w || !V) throw Error(MEGB200_ERR_PARAM, "null argument");
+    if (m < 1 || m > kMaxBasis || lda < m) throw Error(MEGB200_ERR_PARAM, "sym_eigh needs 1 <= m <= 112, lda >= m");
+    Launch L = s->launch();
+    rr_wide(L, A, lda, m, w, V, s->info, 0);
+  });
+}
+
 int megb200_gradient_apply(megb200_solver* s, const megb200_gradient* g, const double* U, int64_t ldu, int32_t k,
                            double* W, int64_t ldw) {
   return guarded_impl([&] {

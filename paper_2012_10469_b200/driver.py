@@ -161,34 +161,60 @@ class RecoveryRun:
 
 def run_recovery(objective, x0: LowRankIterate, T: int, *, eta: float, eps_schedule: EpsilonSchedule | None = None,
                  oracle=None, gap_every: int = 0, svd_subspace: int | None = None, block: int | None = None,
-                 seed: int = 0) -> RecoveryRun:
+                 seed: int = 0, shadow: bool = False, dense_cap: int = 400) -> RecoveryRun:
     """T MEG steps on a QuadMeasObjective (deterministic, or mini-batch when `oracle` is a
     QuadMeasStochasticOracle): step t uses eta, eps_{t+1}, svd_seed = t; row t logs f(tau X_{t+1}),
     the cheap certificate and lambda_{r+1} of the step and its wall time; every `gap_every` rows
-    (and at the end) the dual gap of X_{t+1}."""
+    (and at the end) the dual gap of X_{t+1}.
+
+    shadow=True is the spec's lockstep / dense-shadow mode (n <= dense_cap): the
+    full certificate from the whole spectrum of log X_t - eta grad (shadow_lowrank_step +
+    certificate_full, meg.py:240-262, 367-385) and B(W_{t+1}, X_{t+1}) against the exact MEG
+    sequence W_{t+1} = exact_meg_step(W_t, grad(W_t), eta) from W_0 = X_0 (Fig. 1-2; entropy.py:128-142);
+    the elapsed time then covers only the low-rank step."""
     import time
 
-    from .meg import lowrank_meg_step
+    from .meg import certificate_full, lowrank_meg_step
 
+    if shadow:
+        from . import shadow as sh
+
+        if x0.n > dense_cap:
+            raise ParameterError(f"dense shadow allowed only for n <= {dense_cap}, got n={x0.n}")
+        if oracle is not None:
+            raise ParameterError("the lockstep shadow follows the deterministic gradient (oracle must be None)")
+        W = x0.densify() if hasattr(x0, "densify") else None
     eps_schedule = eps_schedule or EpsilonSchedule.experiment(10.0)
     rows = []
     x = x0
     for t in range(int(T)):
         t0 = time.perf_counter_ns()
         g = oracle.grad_operator(x, oracle.sample_batch()) if oracle is not None else objective.grad_operator(x)
-        res = lowrank_meg_step(x, g, float(eta), eps_schedule.eval(t + 1), svd_seed=t, svd_subspace=svd_subspace,
+        eps_next = eps_schedule.eval(t + 1)
+        res = lowrank_meg_step(x, g, float(eta), eps_next, svd_seed=t, svd_subspace=svd_subspace,
                                block=block)
+        elapsed = time.perf_counter_ns() - t0
+        row = {"t": t + 1, "f_value": objective.value(res.iterate), "eps_t": float(res.iterate.eps),
+               "eta_t": float(eta), "cert_cheap_lhs": float(res.cert.lhs_cheap),
+               "cert_cheap_holds": int(res.cert.holds_cheap), "cert_full_lhs": None, "cert_full_holds": None,
+               "bregman_to_exact": None, "lambda_rsp1": float(res.lambda_r_plus_1), "elapsed_ns": elapsed}
+        if shadow:
+            _, _, yfull = sh.shadow_lowrank_step(x.densify(), g.dense, float(eta), eps_next, x.r)
+            cf = certificate_full(yfull.cpu().numpy(), eps_next, x.n, x.r, iteration=t)
+            W = sh.exact_meg_step(W, objective.gradient_dense(W), float(eta))
+            row["cert_full_lhs"] = float(cf.lhs_full)
+            row["cert_full_holds"] = int(cf.holds_full)
+            row["bregman_to_exact"] = float(sh.bregman_structured(W, res.iterate))
         x = res.iterate
-        row = {"t": t + 1, "f_value": objective.value(x), "eps_t": float(x.eps), "eta_t": float(eta),
-               "cert_cheap_lhs": float(res.cert.lhs_cheap), "cert_cheap_holds": int(res.cert.holds_cheap),
-               "cert_full_lhs": None, "cert_full_holds": None, "bregman_to_exact": None,
-               "lambda_rsp1": float(res.lambda_r_plus_1), "elapsed_ns": time.perf_counter_ns() - t0}
         if gap_every and ((t + 1) % gap_every == 0 or t + 1 == T):
             row["dual_gap"] = objective.dual_gap(x, seed=seed)
         rows.append(row)
     holds = [r["t"] for r in rows if r["cert_cheap_holds"]]
     summary = {"T": int(T), "f_final": rows[-1]["f_value"] if rows else objective.value(x0),
                "first_iter_cert_cheap": holds[0] if holds else -1}
+    if shadow:
+        holds_full = [r["t"] for r in rows if r["cert_full_holds"]]
+        summary["first_iter_cert_full"] = holds_full[0] if holds_full else -1
     gaps = [r["dual_gap"] for r in rows if "dual_gap" in r]
     if gaps:
         summary["dual_gap"] = gaps[-1]

@@ -418,6 +418,14 @@ class QuadMeasObjective:
                                                 self.m, w, G.data_ptr(), G.stride(0)))
         return G
 
+    def gradient_dense(self, X) -> torch.Tensor:
+        """tau * grad f(tau X) at a DENSE trace-1 matrix X (the dense-shadow / exact-MEG mode,
+        SPEC.md:320 grad_dense): residuals a_i^T (tau X) b_i - y_i by a dense product (cuBLAS --
+        a diagnostic off the step path), then the device gradient kernel."""
+        Xd = runtime.as_device_f64(X)
+        res = self.tau * torch.sum((self.a @ Xd) * self.b, dim=1) - self.y
+        return self.gradient_matrix(res.contiguous())
+
     def grad_operator(self, x, t: int = 0) -> GradientOperator:
         """tau * grad f(tau X) at x, materialised on the device (RecoveryObjective.grad_operator)."""
         G = self.gradient_matrix(self.residuals(x))

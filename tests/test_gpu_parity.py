@@ -775,3 +775,92 @@ def test_solver_settings_reported(pb):
         res32 = pb.lowrank_meg_step(x, pb.FrobeniusObjective(m, dtype="f32").grad_operator(x), 1.0, 0.05)
     assert res32.svd_tol_effective == pb.objectives.F32_TOL_FLOOR
     assert res.svd_tol_effective == 1e-10
+
+
+# ---------------------------------------------------------------------------
+# dense shadow / lockstep: exact MEG, shadow step, full certificate, Bregman
+
+
+def test_shadow_lockstep_matches_reference(pb):
+    """The device dense-shadow diagnostics against the unmodified reference's lockstep run
+    (tests/golden/make_golden_shadow.py): exact_meg_step (meg.py:269-284), shadow_lowrank_step
+    (meg.py:367-385) + certificate_full, bregman (entropy.py:76-96), bregman_structured
+    (entropy.py:128-142); the low-rank steps themselves through lowrank_meg_step."""
+    from paper_2012_10469_b200 import shadow as sh
+
+    g0 = load_golden("shadow_n40_r3")
+    n, r, eta = int(g0["n"]), int(g0["r"]), float(g0["eta"])
+    d = g0["D"]
+    x = pb.LowRankIterate(n, r, g0["V0"], g0["lam0"], float(g0["eps0"]))
+    w = x.densify()
+    for t in range(len(g0["bregman"])):
+        eps_next = 0.6 / (t + 11) ** 2
+        g = om.symmetrize(x.densify() - d)
+        res = pb.lowrank_meg_step(x, pb.DenseGradient(g), eta, eps_next, svd_seed=t)
+        assert abs(res.cert.lhs_cheap - g0["lhs_cheap"][t]) <= 1e-9 * max(1.0, abs(g0["lhs_cheap"][t]))
+        low, _, y = sh.shadow_lowrank_step(x.densify(), g, eta, eps_next, r)
+        y = y.cpu().numpy()
+        assert np.max(np.abs(y - g0["y"][t])) <= 1e-11 * np.abs(g0["y"][t]).max()
+        cert = pb.certificate_full(y, eps_next, n, r)
+        assert abs(cert.lhs_full - g0["lhs_full"][t]) <= 1e-9 * max(1.0, abs(g0["lhs_full"][t]))
+        w = sh.exact_meg_step(w, om.symmetrize(w - d), eta).cpu().numpy()
+        x = res.iterate
+        assert np.max(np.abs(low.cpu().numpy() - x.densify())) <= 1e-7  # test_meg.py:144-156's bar
+        b = sh.bregman(w, x.densify())
+        assert b.finite and abs(b.value - g0["bregman"][t]) <= 1e-9 * abs(g0["bregman"][t])
+        bs = sh.bregman_structured(w, x)
+        assert abs(bs.value - g0["bregman_structured"][t]) <= 1e-9 * abs(g0["bregman"][t])
+    assert np.max(np.abs(w - g0["W_final"])) <= 1e-10
+
+
+def test_shadow_eigh_paths_and_entropy_identities(pb):
+    """full_eigh on the native small solver (n <= 112) and on cuSOLVER (n > 112) agree with
+    numpy; bregman(X, X) = 0 and the structured form equals the dense one (test_entropy.py)."""
+    from paper_2012_10469_b200 import shadow as sh
+
+    rng = np.random.default_rng(12)
+    for n in (30, 112, 150):
+        a = random_symmetric(n, rng)
+        w, v = sh.full_eigh(a)
+        ref = np.sort(np.linalg.eigvalsh(a))[::-1]
+        assert np.max(np.abs(w.cpu().numpy() - ref)) <= 1e-12 * np.abs(ref).max()
+        vv = v.cpu().numpy()
+        assert np.max(np.abs(a @ vv - vv * w.cpu().numpy())) <= 1e-11 * np.abs(ref).max()
+    q, lam, eps = random_lowrank_iterate_np(50, 4, rng)
+    x = pb.LowRankIterate(50, 4, q, lam, eps)
+    assert abs(sh.bregman(x.densify(), x.densify()).value) <= 1e-12
+    z = om.symmetrize(rng.standard_normal((50, 50)))
+    z = z @ z.T + np.eye(50)
+    z /= np.trace(z)
+    assert abs(sh.bregman_structured(z, x).value - sh.bregman(z, x.densify()).value) <= 1e-10
+
+
+def test_recovery_lockstep_columns(pb):
+    """driver.run_recovery(shadow=True) fills the spec's dense-shadow columns (cert_full_lhs,
+    cert_full_holds, bregman_to_exact) exactly as the oracle computes them."""
+    from oracle import qm as oq
+    from paper_2012_10469_b200 import driver
+
+    g = load_golden("qm_n60_r3")
+    n, r, seed = int(g["n"]), int(g["r"]), int(g["seed"])
+    inst = oq.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=seed)
+    dev = pb.QuadMeasObjective.from_instance(inst)
+    x0 = pb.LowRankIterate(n, r, g["V0"], g["lam0"], float(g["eps0"]))
+    eta = 0.02 * float(g["eta"])  # the exact MEG sequence stays positive definite over the 5 steps
+    run = driver.run_recovery(dev, x0, 5, eta=eta, shadow=True)
+    ox = om.LowRankIterate(n=n, r=r, V=g["V0"], lam=g["lam0"], eps=float(g["eps0"]))
+    w = ox.densify()
+    from tests.test_oracle_pins import _qm_eps
+
+    for t, row in enumerate(run.rows):
+        eps_next = _qm_eps(t + 1)
+        G = oq.dense_gradient(inst, oq.residuals(inst, ox), inst.tau)
+        _, _, y = om.shadow_lowrank_step(ox.densify(), G, eta, eps_next, r)
+        cf = om.certificate_full(y, eps_next, n, r)
+        assert abs(row["cert_full_lhs"] - cf.lhs_full) <= 1e-8 * max(1.0, abs(cf.lhs_full))
+        assert row["cert_full_holds"] == int(cf.holds_full)
+        res_w = inst.tau * np.einsum("ij,ij->i", inst.a @ w, inst.b) - inst.y
+        w = om.exact_meg_step(w, oq.dense_gradient(inst, res_w, inst.tau), eta)
+        ox = om.lowrank_meg_step(ox, lambda u, G=G: G @ u, eta, eps_next, svd_seed=t).iterate
+        assert abs(row["bregman_to_exact"] - om.bregman_structured(w, ox)) <= 1e-8 * max(1.0, abs(row["bregman_to_exact"]))
+    assert "first_iter_cert_full" in run.summary

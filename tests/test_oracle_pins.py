@@ -282,3 +282,28 @@ def test_qm_spectral_init_and_dual_gap_oracle(name):
     assert np.max(np.abs(w - g["si_w"])) <= 1e-10
     x = om.LowRankIterate(n=n, r=r, V=g["V"][-1], lam=g["lam"][-1], eps=float(g["eps"][-1]))
     assert abs(oq.dual_gap(inst, x, seed=seed) - float(g["gap_final"])) <= 1e-9 * abs(float(g["gap_final"]))
+
+
+def test_oracle_shadow_lockstep_matches_reference():
+    """Dense-shadow diagnostics of the oracle (exact_meg_step, shadow_lowrank_step,
+    certificate_full, bregman, bregman_structured) reproduce the unmodified reference's lockstep
+    run (tests/golden/make_golden_shadow.py)."""
+    g0 = load_golden("shadow_n40_r3")
+    n, r, eta = int(g0["n"]), int(g0["r"]), float(g0["eta"])
+    d = g0["D"]
+    x = om.LowRankIterate(n=n, r=r, V=g0["V0"], lam=g0["lam0"], eps=float(g0["eps0"]))
+    w = x.densify()
+    for t in range(len(g0["bregman"])):
+        eps_next = 0.6 / (t + 11) ** 2
+        g = om.symmetrize(x.densify() - d)
+        res = om.lowrank_meg_step(x, lambda u, g=g: g @ u, eta, eps_next, svd_seed=t)
+        low, _, y = om.shadow_lowrank_step(x.densify(), g, eta, eps_next, r)
+        assert np.max(np.abs(y - g0["y"][t]) / np.abs(g0["y"][t]).max()) <= 1e-11
+        cert = om.certificate_full(y, eps_next, n, r)
+        assert abs(cert.lhs_full - g0["lhs_full"][t]) <= 1e-10 * max(1.0, abs(g0["lhs_full"][t]))
+        w = om.exact_meg_step(w, om.symmetrize(w - d), eta)
+        x = res.iterate
+        assert np.max(np.abs(low - x.densify())) <= 1e-7
+        assert abs(om.bregman(w, x.densify())[0] - g0["bregman"][t]) <= 1e-9 * abs(g0["bregman"][t])
+        assert abs(om.bregman_structured(w, x) - g0["bregman_structured"][t]) <= 1e-9 * abs(g0["bregman"][t])
+    assert np.max(np.abs(w - g0["W_final"])) <= 1e-10
