@@ -62,6 +62,10 @@ bool first_on_device(const void* tag);
 struct Launch {
   cudaStream_t stream;
   int64_t* counter;  // kernels launched (telemetry for bench.py)
+  // float64 DMMA pass only: wait until *wait_ctr >= wait_target instead of for the preceding grid's
+  // completion (the preceding k_fused_first_pass released its Ritz rows early, see FusedPassArgs)
+  const unsigned long long* wait_ctr = nullptr;
+  unsigned long long wait_target = 0;
 };
 
 // Streamed operator product: part[s] (S x n x b, dense row-major ld b) =
@@ -196,9 +200,17 @@ struct FusedPassArgs {
   bool cooperative = false;  // launch cooperatively (more than one solver handle alive)
   int lam_inline_n = 0;   // > 0: lc's kept weights passed by value (lam_inline), lc.lam not read
   double lam_inline[64] = {};
+  // overlap with the next step's operand pass: every CTA bumps rows_ctr once its Ritz rows are
+  // written and lets the dependent launch start (the pass waits on the counter, not on this grid's
+  // completion); the CTA that writes the result pack then stores `epoch` into done_flag (and into
+  // host_pack[pack_count], the host's completion marker).  A launch first waits until done_flag
+  // holds prev_epoch (the previous launch's reduction buffers are free); prev_epoch 0: no wait.
+  unsigned long long* rows_ctr = nullptr;
+  unsigned* done_flag = nullptr;
+  unsigned prev_epoch = 0;
 };
 bool fused_pass_supported(int64_t n, int b, int l, int nreq, int sm_count);
-void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count);
+int fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count);  // returns the grid size
 
 // The float64 dense pass and the step tail above in ONE cooperative launch (megb200_kernels.cu,
 // k_dense_step_mma); needs a.Eg when a.l > 0, a.rq == b, a.gr <= b, no vgram, a.sync with >= 512

@@ -543,7 +543,9 @@ __device__ __forceinline__ void dense_mma_body(const CUtensorMap* tmM, const CUt
                                                double* __restrict__ part, int tiles, int kch, int smax,
                                                unsigned char* base, unsigned* tilecnt, int* fixlist, int* nfix,
                                                const double* __restrict__ Ug = nullptr, int64_t ldu = 0,
-                                               double* __restrict__ hpart = nullptr) {
+                                               double* __restrict__ hpart = nullptr,
+                                               const unsigned long long* wait_ctr = nullptr,
+                                               unsigned long long wait_target = 0) {
   const int64_t utot = (int64_t)tiles * kch;
   const int64_t ua = (int64_t)blockIdx.x * utot / gridDim.x, ub = (int64_t)(blockIdx.x + 1) * utot / gridDim.x;
   // Operand stage = 8 TMA boxes of 16 (i) x 32 (k) doubles with the 128-byte
@@ -568,10 +570,24 @@ __device__ __forceinline__ void dense_mma_body(const CUtensorMap* tmM, const CUt
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmM) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmU) : "memory");
   }
-  __syncthreads();
   // launched programmatically dependent on the previous kernel: everything above
-  // overlapped its tail; U and the partial buffer are touched only after it completed
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // overlapped its tail; U and the partial buffer are touched only after it completed -- or,
+  // after a k_fused_first_pass that released its Ritz rows early, once all of its CTAs counted
+  // theirs (its last CTA may still be reducing residuals, in buffers this pass does not touch)
+  if (wait_ctr) {
+    if (threadIdx.x == 0) {
+      unsigned long long v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(wait_ctr) : "memory");
+        if (v >= wait_target) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  } else {
+    __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (warp == CW) {
     if (lane == 0) {
       const uint32_t stage_bytes = (uint32_t)(kPipeKC * kMmaRows * 8 + kPipeKC * BNP * 8);
@@ -814,10 +830,12 @@ __device__ __forceinline__ void dense_mma_body(const CUtensorMap* tmM, const CUt
 template <int NT, int TAIL, int CW>
 __global__ void __launch_bounds__(32 * (CW + 1), 1)
     k_dense_pass_mma(const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmU, int64_t n,
-                     int b, double* __restrict__ part, int tiles, int kch, int smax) {
+                     int b, double* __restrict__ part, int tiles, int kch, int smax,
+                     const unsigned long long* wait_ctr, unsigned long long wait_target) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* base = smem + ((1024 - ((uintptr_t)smem & 1023)) & 1023);
-  dense_mma_body<NT, TAIL, CW, false>(&tmM, &tmU, n, b, part, tiles, kch, smax, base, nullptr, nullptr, nullptr);
+  dense_mma_body<NT, TAIL, CW, false>(&tmM, &tmU, n, b, part, tiles, kch, smax, base, nullptr, nullptr, nullptr,
+                                      nullptr, 0, nullptr, wait_ctr, wait_target);
 }
 
 // ===========================================================================
@@ -1734,9 +1752,11 @@ void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, c
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
   if (cw == 16)
-    MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL, 16>, tmM, tmU, n, b, part, tiles, kch, smax));
+    MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL, 16>, tmM, tmU, n, b, part, tiles, kch, smax,
+                                L.wait_ctr, L.wait_target));
   else
-    MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL, 8>, tmM, tmU, n, b, part, tiles, kch, smax));
+    MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL, 8>, tmM, tmU, n, b, part, tiles, kch, smax,
+                                L.wait_ctr, L.wait_target));
   MEG_LAUNCHED();
   ++*L.counter;
 }
@@ -1827,7 +1847,9 @@ int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, 
       const int tiles = cdiv(n, kMmaRows);
       const int kch = cdiv(n, kPipeKC);
       int grid = 0, smax = 0;
-      stream_k_grid(n, sm_count, part_cap_slices, &grid, &smax);
+      // after an early-released fused first pass, one SM stays with its last CTA (the residual
+      // reduction): the pass takes the others, so none of its CTAs queues behind that one
+      stream_k_grid(n, L.wait_ctr ? sm_count - 1 : sm_count, part_cap_slices, &grid, &smax);
       const double* m = static_cast<const double*>(M);
       // DMMA n-tiles for the multiple-of-8 head of the block, DFMA for the (even) rest
 #define MEG_MMA(nt, tail) launch_pipe_mma<nt, tail>(L, m, ldm, n, U, ldu, b, part, tiles, kch, smax, grid)

@@ -90,6 +90,14 @@ struct megb200_solver {
   int64_t h_buf_len = 0;
   unsigned* fsync = nullptr;  // tickets / flags of the fused first-pass kernel (zeroed)
   unsigned epoch = 0;
+  // early release of a fused first pass's Ritz rows to the next operand pass (FusedPassArgs):
+  // cumulative count of fused CTAs launched, the last fused launch's epoch, and the launch counter
+  // right after it (a pass launched with nothing in between waits on the counter)
+  unsigned long long rows_target = 0;
+  unsigned last_fused_epoch = 0;
+  int64_t launches_after_fused = -1;
+  int last_pack_count = 0;
+  bool last_pack_host = false;
   int want_vgram = 0;      // host-buffer step: fused phase 0 also reduces the factor Gram (r x r)
   // kept weights of the current iterate, uploaded lazily: the fused first pass takes them as
   // kernel arguments, other consumers flush them to dlam first
@@ -234,6 +242,9 @@ struct OpDev {
   void* apply_ctx = nullptr;
 };
 
+constexpr int kRowsCtrWord = 512;     // u64 at words 512..513: fused CTAs whose Ritz rows are final
+constexpr int kDoneFlagWord = 520;    // epoch of the last fused launch whose result pack is written
+
 // Live pass profiling (megb200_profile_enable): every prof-th streamed pass kernel is bracketed
 // by events on the solver stream; prof_end books its algorithmic bytes (operand as stored + the
 // n x k float64 block read and written).
@@ -261,6 +272,11 @@ void prof_end(megb200_solver* s, int ev0, const OpDev& op, int k) {
 // Streamed operand pass alone: partial slices of Op U into s->part; returns the slice count.
 int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k) {
   Launch L = s->launch();
+  if (s->launches == s->launches_after_fused) {
+    // directly after a fused first pass: wait for its Ritz rows, not for its residual reduction
+    L.wait_ctr = reinterpret_cast<const unsigned long long*>(s->fsync + kRowsCtrWord);
+    L.wait_target = s->rows_target;
+  }
   const int64_t n = s->n;
   int S = 0;
   const bool streamed = (op.kind == MEGB200_OP_DENSE || op.kind == MEGB200_OP_CSR) && op.scale != 0.0;
@@ -636,7 +652,20 @@ int fused_pass(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu,
   }
   static const bool stamps = getenv("MEGB200_FUSED_STAMPS") != nullptr;
   if (stamps) a.stamps = reinterpret_cast<unsigned long long*>(s->fsync + 128);
-  fused_first_pass(L, a, s->sm_count);
+  static const bool no_release = getenv("MEGB200_NO_EARLY_RELEASE") != nullptr;  // diagnostics
+  if (!no_release) {
+    a.rows_ctr = reinterpret_cast<unsigned long long*>(s->fsync + kRowsCtrWord);
+    a.done_flag = s->fsync + kDoneFlagWord;
+    a.prev_epoch = s->last_fused_epoch;
+  }
+  const int G = fused_first_pass(L, a, s->sm_count);
+  if (!no_release) {
+    s->rows_target += (unsigned long long)G;
+    s->last_fused_epoch = a.epoch;
+    s->launches_after_fused = s->launches;
+  }
+  s->last_pack_count = a.pack_count;
+  s->last_pack_host = a.host_pack != nullptr && !no_release;
   if (!a.host_pack) s->d2h(dst, s->pack, a.pack_count);
   return a.gr;
 }
@@ -1409,6 +1438,10 @@ struct FastStep {
   double tol = 0.0;
   double* dst = nullptr;  // pinned read-back slot
   cudaEvent_t done = nullptr;
+  // completion by the kernel's marker in the mapped slot (no event between this step's fused kernel
+  // and the next step's pass, whose programmatic launch it would serialise)
+  const volatile double* marker = nullptr;
+  double marker_value = 0.0;
 };
 
 void fast_step_enqueue(megb200_solver* s, const OpDev& op, int r, const EigShape& sh, double tol, const double* warm,
@@ -1425,9 +1458,15 @@ void fast_step_enqueue(megb200_solver* s, const OpDev& op, int r, const EigShape
   EpiSpec epi;
   epi.r = r;
   epi.eps_next = eps_next;
+  fs.marker = nullptr;
   if (fused_ok(s, op, sh.bw, fs.nreq)) {
     // the fused first pass reads the warm block in place (no copy into the basis)
     fs.gr = fused_pass(s, op, warm, ld_warm, sh.bw, fs.nreq, &epi, ritz_out, ld_ritz, V_next, ld_next, r, dst);
+    if (s->last_pack_host) {
+      fs.marker = dst + s->last_pack_count;
+      fs.marker_value = (double)s->last_fused_epoch;
+      return;
+    }
   } else {
     copy_block(L, n, sh.bw, warm, ld_warm, s->Q, s->ldq);
     block_pass(s, op, 0, sh.bw);
@@ -1437,7 +1476,21 @@ void fast_step_enqueue(megb200_solver* s, const OpDev& op, int r, const EigShape
 }
 
 bool fast_step_confirm(megb200_solver* s, const FastStep& fs, megb200_step_result* out) {
-  MEG_CUDA(cudaEventSynchronize(fs.done));
+  if (fs.marker) {
+    // the kernel stores the marker after the whole pack (system-scope fence); a stuck marker falls
+    // back to draining the stream, which surfaces any device error
+    const auto t0 = std::chrono::steady_clock::now();
+    while (*fs.marker != fs.marker_value) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(5)) {
+        s->sync();
+        if (*fs.marker != fs.marker_value) throw Error(MEGB200_ERR_CUDA, "fused step did not complete");
+        break;
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+  } else {
+    MEG_CUDA(cudaEventSynchronize(fs.done));
+  }
   const double* pk = fs.dst;
   const RRDecision dec = rr_decide(s, pk, fs.bw, fs.nreq, fs.tol);
   if (!dec.ok) return false;

@@ -167,6 +167,12 @@ template <int NT, bool CL>
 __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs a) {
   // programmatic dependent launch after the operand pass: nothing is read before it completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (a.prev_epoch && a.done_flag) {
+    // the previous launch's last CTA may still be reducing into the buffers reused below
+    if (threadIdx.x == 0)
+      while (ld_acquire_u32(a.done_flag) != a.prev_epoch) __nanosleep(32);
+    __syncthreads();
+  }
   unsigned long long* st0 = blockIdx.x == 0 ? a.stamps : nullptr;
   stamp(st0, 0);
   extern __shared__ __align__(16) double sm[];
@@ -355,6 +361,13 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
     }
   }
   stamp(st0, 9);
+  if (a.rows_ctr) {
+    // this CTA's Ritz rows (T, V_next) are final: count them and let the next operand pass launch
+    __threadfence();
+    __syncthreads();
+    if (t == 0) atomicAdd(a.rows_ctr, 1ull);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   double* res2 = a.part2 + (int64_t)(G + (G + kGroup - 1) / kGroup) * kFusedStride;
   if (tree_reduce<NT, CL>(a.part2, a.part2 + (int64_t)G * kFusedStride, res2, pw, kFusedStride, a.sync + 64, &s_flag)) {
     stamp(a.stamps, 10);
@@ -373,6 +386,15 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
       for (int idx = t; idx < a.pack_count; idx += NT) a.host_pack[idx] = __ldcg(a.pack + idx);
     }
     stamp(a.stamps, 12);
+    if (a.done_flag) {
+      __threadfence_system();
+      __syncthreads();
+      if (t == 0) {
+        if (a.host_pack) *reinterpret_cast<volatile double*>(a.host_pack + a.pack_count) = (double)a.epoch;
+        __threadfence_system();
+        st_release_u32(a.done_flag, a.epoch);
+      }
+    }
   }
 }
 
@@ -486,7 +508,7 @@ bool cluster_fits(int G, size_t smem) {
   return G % kGroup == 0 && G / kGroup <= max_clusters;
 }
 
-void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count) {
+int fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count) {
   // clusters of 8 replace the group tickets with the hardware cluster barrier; measured ~1.5 us
   // faster per step but with sporadic 2x slow runs (cluster placement under the pass's tail), so
   // they are a diagnostics option (MEGB200_CLUSTER=1), not the default
@@ -508,6 +530,7 @@ void fused_first_pass(const Launch& L, FusedPassArgs a, int sm_count) {
     case 512: cl ? launch_fused<512, true>(L, a, G, smem) : launch_fused<512, false>(L, a, G, smem); break;
     default: cl ? launch_fused<256, true>(L, a, G, smem) : launch_fused<256, false>(L, a, G, smem); break;
   }
+  return G;
 }
 
 }  // namespace megb200
