@@ -340,7 +340,9 @@ def measure_workload(name: str, W: int, K: int, world: int, dev, peak: float, sa
         time.sleep(0.3)  # let nvidia-smi attach before the timed region
     barrier(world)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push(f"timed_{name}")  # ncu --nvtx-include timed_cfg2/ (launch lists in profiles/)
     rr = driver.run(x, obj, W + K, t0=0, timed_from=W, timed_count=K, **run_kw)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     barrier(world)
     clocks = sampler.stop() if sampler else None
