@@ -112,6 +112,8 @@ void sampled_fill(const Launch& L, int64_t n, uint64_t kmask, uint64_t knoise, d
 // part[g] (g < slots) = partial sums of (X_ij - M_ij)^2, X from (V, coeff, tail); r <= 64
 void frob_direct(const Launch& L, const void* M, int dtype, int64_t ld, int64_t n, const double* V, int64_t ldv, int r,
                  const double* coeff, double tail, double* part, int slots);
+// Q[0:n, 0:n] = I (leading dimension ldq)
+void set_identity(const Launch& L, int64_t n, double* Q, int64_t ldq);
 // H[0:cap, 0:cap] = 0 except H[j][j] = theta[j] for j < k
 void set_diag(const Launch& L, double* H, int cap, int k, const double* theta);
 

@@ -1557,6 +1557,13 @@ __global__ void __launch_bounds__(256) k_gen_dense_target(const double* __restri
   M[i * ld + j] = (T)acc;
 }
 
+__global__ void k_set_identity(int64_t n, double* __restrict__ Q, int64_t ldq) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * n) return;
+  const int64_t i = idx / n, j = idx - i * n;
+  Q[i * ldq + j] = i == j ? 1.0 : 0.0;
+}
+
 __global__ void k_set_diag(double* __restrict__ H, int cap, int k, const double* __restrict__ theta) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= cap * cap) return;
@@ -1848,8 +1855,10 @@ int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, 
       const int kch = cdiv(n, kPipeKC);
       int grid = 0, smax = 0;
       // after an early-released fused first pass, one SM stays with its last CTA (the residual
-      // reduction): the pass takes the others, so none of its CTAs queues behind that one
-      stream_k_grid(n, L.wait_ctr ? sm_count - 1 : sm_count, part_cap_slices, &grid, &smax);
+      // reduction): the pass takes the others, so none of its CTAs queues behind that one.  Always
+      // one SM less, whether or not this launch follows a fused pass: the stream-K partition (hence
+      // every bit of the result) must not depend on what ran before
+      stream_k_grid(n, std::max(1, sm_count - 1), part_cap_slices, &grid, &smax);
       const double* m = static_cast<const double*>(M);
       // DMMA n-tiles for the multiple-of-8 head of the block, DFMA for the (even) rest
 #define MEG_MMA(nt, tail) launch_pipe_mma<nt, tail>(L, m, ldm, n, U, ldu, b, part, tiles, kch, smax, grid)
@@ -2111,6 +2120,12 @@ void gen_dense_target(const Launch& L, const double* U, int64_t r, const double*
     k_gen_dense_target<double><<<grid, 256, 0, L.stream>>>(U, (int)r, lam, sigma, key, static_cast<double*>(M), ld, n);
   else
     k_gen_dense_target<float><<<grid, 256, 0, L.stream>>>(U, (int)r, lam, sigma, key, static_cast<float*>(M), ld, n);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void set_identity(const Launch& L, int64_t n, double* Q, int64_t ldq) {
+  k_set_identity<<<cdiv(n * n, 256), 256, 0, L.stream>>>(n, Q, ldq);
   MEG_LAUNCHED();
   ++*L.counter;
 }

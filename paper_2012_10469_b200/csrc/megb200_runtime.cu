@@ -272,7 +272,8 @@ void prof_end(megb200_solver* s, int ev0, const OpDev& op, int k) {
 // Streamed operand pass alone: partial slices of Op U into s->part; returns the slice count.
 int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k) {
   Launch L = s->launch();
-  if (s->launches == s->launches_after_fused) {
+  static const bool no_rows_wait = getenv("MEGB200_NO_ROWS_WAIT") != nullptr;  // diagnostics
+  if (!no_rows_wait && s->launches == s->launches_after_fused) {
     // directly after a fused first pass: wait for its Ritz rows, not for its residual reduction
     L.wait_ctr = reinterpret_cast<const unsigned long long*>(s->fsync + kRowsCtrWord);
     L.wait_target = s->rows_target;
@@ -434,6 +435,10 @@ struct EpiSpec {
 struct EigShape {
   int bw = 1, mmax = 1, keep = 1, max_passes = 1;
   bool exhaust = false;
+  // n <= the Rayleigh-Ritz limit with a basis allowed to span R^n: the basis IS the identity (no
+  // start block, no orthonormalisation), A I in passes of <= 32 columns, one Rayleigh-Ritz on all of
+  // A returning only the Ritz pairs the step needs (linalg.py:215's basis.shape[1] >= n exit)
+  bool identity = false;
 };
 
 EigShape eig_shape(const megb200_solver* s, int nreq, const EigParams& P) {
@@ -481,6 +486,14 @@ EigShape eig_shape(const megb200_solver* s, int nreq, const EigParams& P) {
   if (!exhaust && (keep & 1) && (bw & 1) == 0) keep = (keep + 1 <= mmax - bw) ? keep + 1 : (keep - 1 >= nreq ? keep - 1 : keep);
   if (!exhaust && keep < nreq) throw Error(MEGB200_ERR_PARAM, "basis too small for the requested eigenpairs");
   EigShape sh;
+  static const bool no_identity = getenv("MEGB200_NO_IDENTITY_BASIS") != nullptr;  // diagnostics
+  sh.identity = !no_identity && n <= s->max_basis && n <= s->cap && (P.basis <= 0 || P.basis >= n);
+  if (sh.identity) {
+    exhaust = true;
+    mmax = (int)n;
+    bw = (int)std::min<int64_t>(std::max(bw, std::min(nreq, 32)), std::min<int64_t>(32, n));
+    keep = std::min(keep, mmax);
+  }
   sh.bw = bw;
   sh.mmax = mmax;
   sh.keep = keep;
@@ -700,7 +713,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   const EigShape sh = eig_shape(s, nreq, P);
   const int bw = sh.bw, mmax = sh.mmax, keep = sh.keep, max_passes = sh.max_passes;
   // a wide Rayleigh-Ritz needs the Ritz pairs a thick restart keeps (and the Ritz block)
-  s->rr_nvec = sh.exhaust ? 0 : std::max(keep, nreq);
+  s->rr_nvec = sh.identity ? std::min<int>((int)n, std::max(nreq, bw)) : sh.exhaust ? 0 : std::max(keep, nreq);
   struct NvecReset {
     megb200_solver* s;
     ~NvecReset() { s->rr_nvec = 0; }
@@ -714,12 +727,19 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   // ---- start block: warm columns + seeded random fill.  A verified-orthonormal warm block of
   // exactly bw columns is read in place by the fused first pass; it is copied into the basis only
   // if the solve continues past that pass (deferred_warm)
-  const int wc = (int)std::min<int64_t>(P.warm_cols, bw);
-  bool deferred_warm = wc == bw && P.warm_orthonormal && ((uintptr_t)P.warm % 16) == 0 && (P.ld_warm % 2) == 0 &&
-                       fused_ok(s, op, bw, nreq) && getenv("MEGB200_NO_INPLACE_WARM") == nullptr;
+  const int wc = sh.identity ? 0 : (int)std::min<int64_t>(P.warm_cols, bw);
+  bool deferred_warm = !sh.identity && wc == bw && P.warm_orthonormal && ((uintptr_t)P.warm % 16) == 0 &&
+                       (P.ld_warm % 2) == 0 && fused_ok(s, op, bw, nreq) &&
+                       getenv("MEGB200_NO_INPLACE_WARM") == nullptr;
   if (wc > 0 && !deferred_warm) copy_block(L, n, wc, P.warm, P.ld_warm, s->Q, s->ldq);
-  if (bw > wc) fill_gaussian(L, n, bw - wc, key_start, 0, 1.0, false, s->Q + wc, s->ldq);
-  if (wc == bw && P.warm_orthonormal) {
+  if (sh.identity) {
+    set_identity(L, n, s->Q, s->ldq);
+  } else if (bw > wc) {
+    fill_gaussian(L, n, bw - wc, key_start, 0, 1.0, false, s->Q + wc, s->ldq);
+  }
+  if (sh.identity) {
+    // the identity is orthonormal
+  } else if (wc == bw && P.warm_orthonormal) {
     // verified-orthonormal warm Ritz block (its Gram came back with the previous step): use as is
   } else if (wc == bw) {
     // a warm Ritz block needs one CholQR round
@@ -738,7 +758,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   for (;;) {
     // operator pass on the current block, then its column of H = Q^T A Q; the first pass
     // of a solve runs fused with its Rayleigh-Ritz (one launch after the pass)
-    const bool fuse = cols == 0 && cur == bw && fused_ok(s, op, bw, nreq);
+    const bool fuse = !sh.identity && cols == 0 && cur == bw && fused_ok(s, op, bw, nreq);
     if (!fuse) block_pass(s, op, cols, cur);
     run.passes++;
     s->mark("pass+finish");
@@ -747,7 +767,8 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
     const bool full = (nxt <= 0) || (newcols + nxt > mmax);
     // Rayleigh-Ritz only where its result is used: the first pass of a solve
     // (warm-started steps converge there), a full basis (restart), the budget end
-    const bool do_rr = (cols == 0) || full || (run.passes >= max_passes);
+    const bool do_rr = sh.identity ? (nxt <= 0 || run.passes >= max_passes)
+                                   : ((cols == 0) || full || (run.passes >= max_passes));
     if (do_rr) {
       double* pk = s->h_buf;
       // outputs written by the Rayleigh-Ritz launch itself, before the wait: if it
@@ -817,6 +838,11 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       if (run.passes >= max_passes) break;
     }
     if (nxt <= 0) break;
+    if (sh.identity) {  // the next identity columns are already in place
+      cols = newcols;
+      cur = nxt;
+      continue;
+    }
     if (deferred_warm) {  // the solve continues: the first block joins the basis
       copy_block(L, n, bw, P.warm, P.ld_warm, s->Q, s->ldq);
       deferred_warm = false;
@@ -1462,7 +1488,8 @@ void fast_step_enqueue(megb200_solver* s, const OpDev& op, int r, const EigShape
   if (fused_ok(s, op, sh.bw, fs.nreq)) {
     // the fused first pass reads the warm block in place (no copy into the basis)
     fs.gr = fused_pass(s, op, warm, ld_warm, sh.bw, fs.nreq, &epi, ritz_out, ld_ritz, V_next, ld_next, r, dst);
-    if (s->last_pack_host) {
+    static const bool no_marker = getenv("MEGB200_NO_MARKER") != nullptr;  // diagnostics
+    if (s->last_pack_host && !no_marker) {
       fs.marker = dst + s->last_pack_count;
       fs.marker_value = (double)s->last_fused_epoch;
       return;
@@ -2033,10 +2060,21 @@ int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_ho
       vn_mapped = nullptr;
     }
     if (vn_mapped) o.V_next = vn_mapped;
+    static const bool htime = getenv("MEGB200_HOST_TIMING") != nullptr;  // diagnostics
+    static double acc[4] = {0, 0, 0, 0};
+    static int64_t nacc = 0;
+    const auto h0 = std::chrono::steady_clock::now();
     try {
       step_core(s, &it, &gg, eta, eps_next, opts, &o, (ld_next_host == r && !vn_mapped) ? V_next_host : nullptr, r,
                 &v_done);
       if (vn_mapped) v_done = true;
+      if (htime) {
+        const auto h1 = std::chrono::steady_clock::now();
+        acc[0] += std::chrono::duration<double, std::micro>(h1 - h0).count();
+        if (++nacc % 200 == 0) {
+          fprintf(stderr, "host step: step_core %.1f us avg over %lld calls\n", acc[0] / nacc, (long long)nacc);
+        }
+      }
     } catch (const Error&) {
       s->want_vgram = 0;
       s->sync();
