@@ -121,15 +121,7 @@ __device__ __forceinline__ void wait_published(const unsigned* flag, unsigned ep
 // same order)
 __device__ __forceinline__ double rows_dot(const double* X, int ldx, int a, const double* Y, int ldy, int c,
                                            int rows) {
-  double e = 0.0, o = 0.0;
-  int r = 0;
-#pragma unroll 2
-  for (; r + 1 < rows; r += 2) {
-    e = fma(X[r * ldx + a], Y[r * ldy + c], e);
-    o = fma(X[(r + 1) * ldx + a], Y[(r + 1) * ldy + c], o);
-  }
-  if (r < rows) e = fma(X[r * ldx + a], Y[r * ldy + c], e);
-  return e + o;
+  return tile_dot(X, ldx, a, Y, ldy, c, rows);  // four chains (rows mod 4): megb200_tail.cuh
 }
 
 // diagnostics: %globaltimer at phase boundaries (a.stamps, MEGB200_FUSED_STAMPS=1)
@@ -247,30 +239,48 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
   // ---- phase 1: W rows, H = U^T W
   {
     const int64_t slice = a.n * b;
-    for (int idx = t; idx < rows * b; idx += NT) {
-      const int rr = idx / b, c = idx - rr * b;
-      const int64_t i = r0 + rr;
-      const double* pp = a.part + i * b + c;
-      double pv[16];  // all slices' loads in flight before the (ordered) sum
+    const int nw = rows * b;
+    // four W elements per thread per round (large row ranges, e.g. cfg5's 256 rows): the first
+    // eight slices of all four in flight together; per element the same slice-ordered sum and
+    // the same two-chain L E product as one element at a time
+    for (int base = t; base < nw; base += 4 * NT) {
+      double pv[4][8];
 #pragma unroll
-      for (int tt = 0; tt < 16; ++tt) pv[tt] = tt < a.S ? pp[tt * slice] : 0.0;
-      double s = 0.0;
+      for (int q = 0; q < 4; ++q) {
+        const int idx = base + q * NT;
+        const bool ok = idx < nw;
+        const double* pp = a.part + r0 * b + (ok ? idx : 0);
 #pragma unroll
-      for (int tt = 0; tt < 16; ++tt) s += pv[tt];
-      for (int tt = 16; tt < a.S; ++tt) s += pp[tt * slice];
-      const double* Lr = Lb + rr * ldL;
-      double v0 = a.scale * s + a.alpha * Us[idx], v1 = 0.0;
-      int k = 0;
-      for (; k + 1 < l; k += 2) {
-        v0 = fma(Lr[k], Es[k * b + c], v0);
-        v1 = fma(Lr[k + 1], Es[(k + 1) * b + c], v1);
+        for (int tt = 0; tt < 8; ++tt) pv[q][tt] = (ok && tt < a.S) ? pp[tt * slice] : 0.0;
       }
-      if (k < l) v0 = fma(Lr[k], Es[k * b + c], v0);
-      const double wv = v0 + v1;
-      Ws[idx] = wv;
-      a.W[i * a.ldw + c] = wv;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int idx = base + q * NT;
+        if (idx >= nw) break;
+        const int rr = idx / b, c = idx - rr * b;
+        const int64_t i = r0 + rr;
+        const double* pp = a.part + i * b + c;
+        double s = 0.0;
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt) s += pv[q][tt];
+#pragma unroll
+        for (int tt = 8; tt < 16; ++tt) s += tt < a.S ? pp[tt * slice] : 0.0;
+        for (int tt = 16; tt < a.S; ++tt) s += pp[tt * slice];
+        const double* Lr = Lb + rr * ldL;
+        double v0 = a.scale * s + a.alpha * Us[idx], v1 = 0.0;
+        int k = 0;
+        for (; k + 1 < l; k += 2) {
+          v0 = fma(Lr[k], Es[k * b + c], v0);
+          v1 = fma(Lr[k + 1], Es[(k + 1) * b + c], v1);
+        }
+        if (k < l) v0 = fma(Lr[k], Es[k * b + c], v0);
+        const double wv = v0 + v1;
+        Ws[idx] = wv;
+        a.W[i * a.ldw + c] = wv;
+      }
     }
     __syncthreads();
+    stamp(st0, 15);
     double* p1 = a.part1 + (int64_t)g * kFusedStride;
     for (int o = t; o < b * b; o += NT) {
       const int ia = o / b, c = o - ia * b;
@@ -310,42 +320,63 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
   }
   for (int c = t; c < rq; c += NT) thsh[c] = __ldcg(a.theta + c);
   __syncthreads();
+  stamp(st0, 13);
   const int rpt = NT / rq;
   const int c = t % rq;
   const int rofs = t / rq;
   double sq = 0.0;
   if (rofs < rpt) {
     const double th = c < a.nreq ? thsh[c] : 0.0;
-    for (int rr = rofs; rr < rows; rr += rpt) {
-      const double* ur = Us + rr * b;
-      double x0 = 0.0, x1 = 0.0;
+    const bool res = c < a.nreq;
+    // four rows per round (independent chains; the S entry is loaded once for the four), each
+    // row's products in the same two-chain order as one row at a time; residual squares in row order
+    for (int rb = rofs; rb < rows; rb += 4 * rpt) {
+      double x0[4], x1[4], y0[4], y1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x0[q] = x1[q] = y0[q] = y1[q] = 0.0;
       int k = 0;
       for (; k + 1 < b; k += 2) {
-        x0 = fma(ur[k], Ss[k * rq + c], x0);
-        x1 = fma(ur[k + 1], Ss[(k + 1) * rq + c], x1);
-      }
-      if (k < b) x0 = fma(ur[k], Ss[k * rq + c], x0);
-      const double x = x0 + x1;
-      const int64_t i = r0 + rr;
-      a.T[i * a.ldt + c] = x;
-      Ts[rr * rq + c] = x;
-      if (c < a.r2) a.V2[i * a.ld2 + c] = x;
-      if (c < a.nreq) {
-        const double* wr = Ws + rr * b;
-        double y0 = 0.0, y1 = 0.0;
-        k = 0;
-        for (; k + 1 < b; k += 2) {
-          y0 = fma(wr[k], Ss[k * rq + c], y0);
-          y1 = fma(wr[k + 1], Ss[(k + 1) * rq + c], y1);
+        const double s0 = Ss[k * rq + c], s1 = Ss[(k + 1) * rq + c];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int rr = min(rb + q * rpt, rows - 1);
+          x0[q] = fma(Us[rr * b + k], s0, x0[q]);
+          x1[q] = fma(Us[rr * b + k + 1], s1, x1[q]);
+          if (res) {
+            y0[q] = fma(Ws[rr * b + k], s0, y0[q]);
+            y1[q] = fma(Ws[rr * b + k + 1], s1, y1[q]);
+          }
         }
-        if (k < b) y0 = fma(wr[k], Ss[k * rq + c], y0);
-        const double d = (y0 + y1) - th * x;
-        sq = fma(d, d, sq);
+      }
+      if (k < b) {
+        const double s0 = Ss[k * rq + c];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int rr = min(rb + q * rpt, rows - 1);
+          x0[q] = fma(Us[rr * b + k], s0, x0[q]);
+          if (res) y0[q] = fma(Ws[rr * b + k], s0, y0[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int rr = rb + q * rpt;
+        if (rr < rows) {
+          const double x = x0[q] + x1[q];
+          const int64_t i = r0 + rr;
+          a.T[i * a.ldt + c] = x;
+          Ts[rr * rq + c] = x;
+          if (c < a.r2) a.V2[i * a.ld2 + c] = x;
+          if (res) {
+            const double d = (y0[q] + y1[q]) - th * x;
+            sq = fma(d, d, sq);
+          }
+        }
       }
     }
   }
   red[t] = sq;
   __syncthreads();  // also publishes Ts
+  stamp(st0, 14);
   const int pw = a.nreq + a.gr * a.gr;
   double* p2 = a.part2 + (int64_t)g * kFusedStride;
   if (t < a.nreq) {
@@ -421,7 +452,9 @@ int fused_pass_rows(int64_t n, int sm_count) {
   return (int)((n + G - 1) / G);
 }
 
-constexpr size_t kFusedSmemMax = 200 * 1024;
+// dynamic shared memory of the fused kernel: up to 224 KiB (its static arrays take ~1 KiB of the
+// 227 KiB per CTA), so cfg5-sized row ranges (R = 256, b = 32, l = 20) still stage their L rows
+constexpr size_t kFusedSmemMax = 224 * 1024;
 
 // shared memory of the fused kernel; L rows are staged when they fit (stage_l), else read from global
 size_t fused_pass_smem(int64_t n, int b, int l, int rq, int sm_count, bool* stage_l = nullptr) {
@@ -445,7 +478,7 @@ void launch_fused(const Launch& L, const FusedPassArgs& a, int G, size_t smem) {
   static char attr = 0;
   if (first_on_device(&attr)) {
     MEG_CUDA(cudaFuncSetAttribute(k_fused_first_pass<NT, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024));
+                                  (int)kFusedSmemMax));
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G);
@@ -487,11 +520,11 @@ bool cluster_fits(int G, size_t smem) {
   int& max_clusters = max_clusters_dev[dev & 63];
   if (first_on_device(max_clusters_dev)) {
     MEG_CUDA(cudaFuncSetAttribute(k_fused_first_pass<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024));
+                                  (int)kFusedSmemMax));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = 200 * 1024;  // worst case of the supported shapes
+    cfg.dynamicSmemBytes = kFusedSmemMax;  // worst case of the supported shapes
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = kGroup;

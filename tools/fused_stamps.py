@@ -21,7 +21,8 @@ from paper_2012_10469_b200 import configs, inputs, runtime  # noqa: E402
 NAMES = {1: "stage U, L rows (CTA 0)", 2: "phase 0 (E)", 3: "phase 1 W rows + H partial (CTA 0)",
          4: "-> last CTA arrives (ticket)", 5: "last: reduce H", 6: "last: Jacobi", 7: "last: epilogue+publish",
          8: "CTA 0: released", 9: "phase 2 rows + partials (CTA 0)", 10: "-> last CTA arrives", 11: "last: reduce",
-         12: "last: host pack"}
+         12: "last: host pack", 13: "(CTA 0 S, theta loaded after release)", 14: "(CTA 0 Ritz rows + residual rows done)",
+         15: "(CTA 0 W rows done, before the H partial)"}
 
 
 def main():
@@ -49,6 +50,9 @@ def main():
         if t >= 10 and res.passes == 1:
             v = np.array(list(buf), dtype=np.float64)
             acc[1:13] += (v[1:13] - v[0:12]) / 1e3
+            acc[13] += (v[13] - v[8]) / 1e3
+            acc[14] += (v[14] - v[13]) / 1e3
+            acc[15] += (v[15] - v[2]) / 1e3
             k += 1
     print(f"{args.name}: {k} warm steps")
     for i, nm in NAMES.items():
