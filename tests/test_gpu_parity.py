@@ -864,3 +864,92 @@ def test_recovery_lockstep_columns(pb):
         ox = om.lowrank_meg_step(ox, lambda u, G=G: G @ u, eta, eps_next, svd_seed=t).iterate
         assert abs(row["bregman_to_exact"] - om.bregman_structured(w, ox)) <= 1e-8 * max(1.0, abs(row["bregman_to_exact"]))
     assert "first_iter_cert_full" in run.summary
+
+
+# ---------------------------------------------------------------------------
+# round-2 plumbing: device generators, direct objective, run-loop certificate cadence and timed window
+
+
+def test_device_sampled_instance_matches_oracle(pb):
+    """The device generator of cfg3's instance (k_sampled_count / k_sampled_fill) reproduces
+    oracle/inputs.sampled_instance: same symmetric pattern (exact) and observed values."""
+    from paper_2012_10469_b200 import configs
+    from paper_2012_10469_b200 import inputs as dinputs
+
+    cfg = inputs.CONFIGS["cfg3"].scaled(1024)
+    w = configs.Workload(**{k: getattr(cfg, k) for k in configs.Workload.__dataclass_fields__})
+    ref = inputs.sampled_instance(cfg, keep_planted=False)
+    rp, col, obs = dinputs.sampled_instance(w)
+    assert np.array_equal(rp.cpu().numpy(), ref.rowptr)
+    assert np.array_equal(col.cpu().numpy(), ref.col)
+    assert np.max(np.abs(obs.cpu().numpy() - ref.obs)) <= 1e-15
+
+
+def test_direct_objective_value(pb):
+    """megb200_objective_value_direct (entry-by-entry 1/2 ||X - M||^2) against the oracle's direct
+    sum, relatively, in float64 and float32 operands."""
+    rng = np.random.default_rng(31)
+    n, r = 700, 6
+    q, lam, eps = random_lowrank_iterate_np(n, r, rng)
+    m = om.symmetrize(rng.standard_normal((n, n))) * 0.01 + q[:, :r] @ np.diag(lam) @ q[:, :r].T
+    xo = om.LowRankIterate(n=n, r=r, V=q, lam=lam, eps=eps)
+    x = pb.LowRankIterate(n, r, q, lam, eps)
+    ref = objectives.frob_value_direct(xo, m)
+    assert abs(pb.FrobeniusObjective(m).value(x) - ref) <= 1e-12 * ref
+    m32 = m.astype(np.float32).astype(np.float64)
+    ref32 = objectives.frob_value_direct(xo, m32)
+    assert abs(pb.FrobeniusObjective(m, dtype="f32").value(x) - ref32) <= 1e-12 * ref32
+
+
+def test_run_loop_certificate_cadence_and_timed_window(pb):
+    """driver.run(cert_every=k) computes the dual gap of X_{t+1} after every step t with
+    (t+1) % k == 0, equal to FrobeniusObjective.dual_gap on the same iterate; the timed window
+    brackets exactly the requested steps."""
+    from paper_2012_10469_b200 import driver
+
+    cfg = inputs.CONFIGS["cfg2"].scaled(1024, 12)
+    host = objectives.make_objective(cfg)
+    x0 = objectives.initial_iterate(om, cfg, host)
+    dev = pb.FrobeniusObjective(host.m)
+    x = pb.LowRankIterate(x0.n, x0.r, x0.V, x0.lam, x0.eps)
+    res = driver.run(x, dev, 12, svd_subspace=64, block=18, cert_every=4, timed_from=2, timed_count=8)
+    cert_steps = [i for i in range(12) if np.isfinite(res.gap[i])]
+    assert cert_steps == [3, 7, 11]
+    assert res.timed_ms > 0 and res.timed_launches > 0
+    # the same trajectory step by step, certificates from the public dual_gap (cold, same rule)
+    xs = pb.LowRankIterate(x0.n, x0.r, x0.V, x0.lam, x0.eps)
+    for t in range(12):
+        xs = pb.lowrank_meg_step(xs, dev.grad_operator(xs), 1.0, cfg.eps(t + 1), svd_seed=t, svd_subspace=64,
+                                 block=18).iterate
+        if t in cert_steps:
+            gap, lmin = dev.dual_gap(xs, warm=False)
+            assert abs(gap - res.gap[t]) <= 1e-9 * max(1.0, abs(gap))
+            assert abs(lmin - res.lmin[t]) <= 1e-9 * max(1.0, abs(lmin))
+
+
+def test_one_launch_step_kernel_parity():
+    """The opt-in one-launch pass + step tail (k_dense_step_mma, MEGB200_STEP_MMA=1)
+    stays parity-green: a cfg2-shaped trajectory (n = 1024, 30 steps) against the reference golden,
+    in a subprocess (the switch is read once per process)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np\n"
+        "from oracle import cpu_meg as om, inputs, objectives\n"
+        "from tests.gpu_helpers import run_gpu, f_scale\n"
+        "from tests.parity import TOL, compare_trajectory, load_golden\n"
+        "ref = load_golden('cfg2_n1024')\n"
+        "cfg = inputs.CONFIGS['cfg2'].scaled(1024, int(ref['iters']))\n"
+        "host = objectives.make_objective(cfg)\n"
+        "x0 = objectives.initial_iterate(om, cfg, host)\n"
+        "got, _, _ = run_gpu(cfg, host, x0, int(ref['iters']), probe_at=[0, 29], block=cfg.block)\n"
+        "compare_trajectory(got, ref, tol=TOL['f64'], f_scale=f_scale(host))\n"
+        "print('ok')\n"
+    )
+    import os
+
+    env = dict(os.environ, MEGB200_STEP_MMA="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
