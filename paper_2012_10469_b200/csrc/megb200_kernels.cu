@@ -1862,7 +1862,8 @@ int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, 
       const double* m = static_cast<const double*>(M);
       // DMMA n-tiles for the multiple-of-8 head of the block, DFMA for the (even) rest
 #define MEG_MMA(nt, tail) launch_pipe_mma<nt, tail>(L, m, ldm, n, U, ldu, b, part, tiles, kch, smax, grid)
-      switch (b < 8 ? 0 : b) {
+      static const bool pad = getenv("MEGB200_MMA_PAD") != nullptr;  // diagnostics: DMMA-only (padded) n-tiles
+      switch (b < 8 ? 0 : (pad && b % 8 ? (b + 7) / 8 * 8 : b)) {
         case 0: MEG_MMA(1, 0); break;
         case 8: MEG_MMA(1, 0); break;
         case 10: MEG_MMA(1, 2); break;
