@@ -52,7 +52,26 @@ enum { MEGB200_F64 = 0, MEGB200_F32 = 1 };
  * Op is a dense symmetric matrix, a CSR matrix with float64 values, or
  * absent.  This is the device form of specmeg.linalg.SymmetricOperator
  * (linalg.py:81-103) for the operators the hot path builds. */
-enum { MEGB200_OP_NONE = 0, MEGB200_OP_DENSE = 1, MEGB200_OP_CSR = 2, MEGB200_OP_CALLBACK = 3 };
+enum { MEGB200_OP_NONE = 0, MEGB200_OP_DENSE = 1, MEGB200_OP_CSR = 2, MEGB200_OP_CALLBACK = 3,
+       MEGB200_OP_QUADMEAS = 4 };
+
+/* Matrix-free quadratic-measurement gradient: Op U = weight / 2 (a^T diag(res) (b U) + b^T diag(res)
+ * (a U)) over m measurement pairs -- the reference's _apply_measurement_gradient (objectives.py:152-158),
+ * the operator RecoveryObjective builds above dense_cap (objectives.py:214-221).  a, b (m x n row-major,
+ * ld n), res (one per measurement) and scratch are device pointers; scratch holds at least
+ * megb200_qm_apply_scratch(s, m, 32) doubles.  Passed through `apply_ctx` of an operator / gradient of
+ * kind QUADMEAS (`apply` unused). */
+typedef struct megb200_qm_data {
+  const double* a;
+  const double* b;
+  const double* res;
+  int64_t m;          /* rows applied: the measurements, or the mini-batch length when idx is given */
+  const int64_t* idx; /* (device, optional) mini-batch of measurement indices, repeats allowed
+                         (StochasticOracle.grad_operator, objectives.py:255-269; weight carries tau m / L) */
+  double weight;
+  double* scratch;
+  int64_t scratch_len;
+} megb200_qm_data;
 
 /* Caller-supplied block application W = Op U: the C form of the reference's Python callables
  * (SymmetricOperator(dim, apply_fn), linalg.py:81-94; grad_apply, meg.py:327-335).  U (n x k, ld
@@ -96,7 +115,8 @@ enum {
   MEGB200_GRAD_FROBENIUS = 2,
   MEGB200_GRAD_SAMPLED = 3,
   MEGB200_GRAD_STOCHASTIC = 4,
-  MEGB200_GRAD_CALLBACK = 5 /* grad u computed by `apply` (the reference's callable grad_apply) */
+  MEGB200_GRAD_CALLBACK = 5, /* grad u computed by `apply` (the reference's callable grad_apply) */
+  MEGB200_GRAD_QUADMEAS = 6  /* grad u = matrix-free quadratic-measurement gradient, apply_ctx -> megb200_qm_data */
 };
 
 typedef struct megb200_gradient {
@@ -361,6 +381,12 @@ int megb200_qm_value(megb200_solver* s, const double* res, int64_t m, double* va
  * allowed; the caller folds tau * m / L into weight). */
 int megb200_qm_gradient_batch(megb200_solver* s, const double* a, const double* b, const double* res,
                               const int64_t* idx, int64_t L, double weight, double* G, int64_t ldg);
+
+/* Matrix-free block application of the measurement gradient (k <= 32): W (n x k, ld ldw) = Op U for the
+ * QUADMEAS operator above; and the scratch it needs, in doubles. */
+int64_t megb200_qm_apply_scratch(megb200_solver* s, int64_t m, int32_t k);
+int megb200_qm_apply(megb200_solver* s, const megb200_qm_data* q, const double* U, int64_t ldu, int32_t k,
+                     double* W, int64_t ldw);
 
 /* Synthetic config-3 instance (seeded counter-based twin of oracle/inputs.sampled_instance):
  * pattern = symmetric Bernoulli(p) over i <= j at counter min*n + max of stream 3, mirrored;

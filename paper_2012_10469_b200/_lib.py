@@ -15,8 +15,8 @@ LIB_PATH = os.path.join(_HERE, "libmegb200.so")
 
 OK, ERR_PARAM, ERR_LANCZOS, ERR_CUDA, ERR_KEPT_MASS, ERR_NO_DEVICE, ERR_CALLBACK = range(7)
 F64, F32 = 0, 1
-OP_NONE, OP_DENSE, OP_CSR, OP_CALLBACK = 0, 1, 2, 3
-GRAD_ZERO, GRAD_DENSE, GRAD_FROBENIUS, GRAD_SAMPLED, GRAD_STOCHASTIC, GRAD_CALLBACK = range(6)
+OP_NONE, OP_DENSE, OP_CSR, OP_CALLBACK, OP_QUADMEAS = 0, 1, 2, 3, 4
+GRAD_ZERO, GRAD_DENSE, GRAD_FROBENIUS, GRAD_SAMPLED, GRAD_STOCHASTIC, GRAD_CALLBACK, GRAD_QUADMEAS = range(7)
 
 c_double_p = C.POINTER(C.c_double)
 c_int32_p = C.POINTER(C.c_int32)
@@ -24,6 +24,15 @@ c_int32_p = C.POINTER(C.c_int32)
 
 # int apply(void* ctx, const double* U, int64_t ldu, int32_t k, double* W, int64_t ldw, void* stream)
 APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p)
+
+
+class QmData(C.Structure):
+    """megb200_qm_data: the matrix-free quadratic-measurement operator's device arrays."""
+
+    _fields_ = [
+        ("a", C.c_void_p), ("b", C.c_void_p), ("res", C.c_void_p), ("m", C.c_int64), ("idx", C.c_void_p), ("weight", C.c_double),
+        ("scratch", C.c_void_p), ("scratch_len", C.c_int64),
+    ]
 
 
 class Operator(C.Structure):
@@ -152,6 +161,8 @@ SIGNATURES = [
     ("megb200_qm_gradient", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_int64]),
     ("megb200_qm_value", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, c_double_p]),
+    ("megb200_qm_apply_scratch", C.c_int64, [C.c_void_p, C.c_int64, C.c_int32]),
+    ("megb200_qm_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64]),
     ("megb200_qm_gradient_batch", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_int64]),
     ("megb200_gen_dense_target", C.c_int,

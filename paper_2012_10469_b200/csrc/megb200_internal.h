@@ -237,5 +237,9 @@ int64_t qm_grad_part_doubles(int64_t m, int64_t n);
 void qm_gradient(const Launch& L, const double* a, const double* b, const double* res, int64_t m, int64_t n,
                  double weight, double* G, int64_t ldg, double* part, const int64_t* idx = nullptr);
 void qm_sumsq(const Launch& L, const double* res, int64_t m, double* out);
+// matrix-free block application W = weight / 2 (a^T diag(res) b + b^T diag(res) a) U  (n x k, ld k)
+int64_t qm_apply_scratch_doubles(int64_t m, int64_t n, int k, int sm_count);
+void qm_apply(const Launch& L, const double* a, const double* b, const double* res, const int64_t* idx, int64_t m,
+              int64_t n, double weight, const double* U, int64_t ldu, int k, double* W, double* scratch, int sm_count);
 
 }  // namespace megb200

@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "megb200_internal.h"
 
 namespace megb200 {
@@ -158,7 +160,188 @@ __global__ void __launch_bounds__(1024) k_qm_sumsq(const double* __restrict__ re
   }
 }
 
+// ---------------------------------------------------------------------------
+// Matrix-free block application (reference _apply_measurement_gradient,
+// objectives.py:152-158, the path RecoveryObjective takes above dense_cap, :214-221):
+//     W = weight / 2 (a^T diag(res) (b U) + b^T diag(res) (a U)),  U n x k, k <= 32
+// in two streaming passes over a and b (4 m n 8 bytes per application, like the
+// reference's four products), never forming the n x n gradient:
+//   k_qm_fwd   PQ[i] = res_i [b_i U | a_i U]  (m x 2 KB): a warp per MW measurements, lanes
+//              stride the coalesced rows a_i, b_i; each lane's U row (KB doubles, L1/L2
+//              resident) feeds 4 MW FMAs per load; fixed xor trees
+//   k_qm_bwd   W_c[j] = sum_{i in chunk c} a_i[j] PQ[i][0:KB] + b_i[j] PQ[i][KB:2KB]: a thread
+//              per two columns j (coalesced rows again), the chunk's PQ rows staged in shared
+//              memory, split over (column block, measurement chunk)
+//   k_qm_bwd_reduce  W = weight / 2 * sum_c W_c in chunk order (bitwise reproducible).
+constexpr int kQmBwdRows = 64;    // measurements staged per round of k_qm_bwd
+constexpr int kQmBwdCols = 512;   // columns per CTA of k_qm_bwd (two per thread)
+
+template <int KB, int MW>
+__global__ void __launch_bounds__(256) k_qm_fwd(const double* __restrict__ a, const double* __restrict__ b,
+                                                const double* __restrict__ res, const int64_t* __restrict__ idx,
+                                                int64_t m, int64_t n, const double* __restrict__ U, int64_t ldu,
+                                                int k, double* __restrict__ PQ) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * MW;
+  if (i0 >= m) return;
+  double p[MW][KB], q[MW][KB];
+#pragma unroll
+  for (int w = 0; w < MW; ++w)
+#pragma unroll
+    for (int c = 0; c < KB; ++c) p[w][c] = q[w][c] = 0.0;
+  const double* ar[MW];
+  const double* br[MW];
+  int64_t li[MW];  // measurement of batch position i0 + w
+#pragma unroll
+  for (int w = 0; w < MW; ++w) {
+    const int64_t i = min(i0 + w, m - 1);
+    li[w] = idx ? idx[i] : i;
+    ar[w] = a + li[w] * n;
+    br[w] = b + li[w] * n;
+  }
+  for (int64_t j = lane; j < n; j += 32) {
+    double x[MW], z[MW];
+#pragma unroll
+    for (int w = 0; w < MW; ++w) {
+      x[w] = __ldcs(ar[w] + j);  // streamed once per pass
+      z[w] = __ldcs(br[w] + j);
+    }
+    const double* uj = U + j * ldu;
+#pragma unroll
+    for (int c = 0; c < KB; ++c) {
+      if (c < k) {
+        const double u = __ldg(uj + c);
+#pragma unroll
+        for (int w = 0; w < MW; ++w) {
+          p[w][c] = fma(z[w], u, p[w][c]);  // b_i U
+          q[w][c] = fma(x[w], u, q[w][c]);  // a_i U
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < MW; ++w) {
+    if (i0 + w < m) {
+      const double rs = res[li[w]];
+      double* out = PQ + (i0 + w) * (2 * KB);
+#pragma unroll
+      for (int c = 0; c < KB; ++c) {
+        double pv = p[w][c], qv = q[w][c];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+          pv += __shfl_xor_sync(0xffffffffu, pv, off);
+          qv += __shfl_xor_sync(0xffffffffu, qv, off);
+        }
+        if (lane == 0) {
+          out[c] = c < k ? rs * pv : 0.0;
+          out[KB + c] = c < k ? rs * qv : 0.0;
+        }
+      }
+    }
+  }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(256) k_qm_bwd(const double* __restrict__ a, const double* __restrict__ b,
+                                                const double* __restrict__ PQ, const int64_t* __restrict__ idx,
+                                                int64_t m, int64_t n, int chunk, int k,
+                                                double* __restrict__ part) {
+  __shared__ double pq[kQmBwdRows][2 * KB];
+  __shared__ int64_t lrow[kQmBwdRows];
+  const int64_t j0 = (int64_t)blockIdx.x * kQmBwdCols + threadIdx.x;
+  const int64_t j1 = j0 + 256;
+  const int64_t l0 = (int64_t)blockIdx.y * chunk;
+  const int64_t l1 = min(m, l0 + chunk);
+  double w0[KB], w1[KB];
+#pragma unroll
+  for (int c = 0; c < KB; ++c) w0[c] = w1[c] = 0.0;
+  const bool ok0 = j0 < n, ok1 = j1 < n;
+  for (int64_t ls = l0; ls < l1; ls += kQmBwdRows) {
+    const int rows = (int)min((int64_t)kQmBwdRows, l1 - ls);
+    __syncthreads();
+    for (int e = threadIdx.x; e < rows * 2 * KB; e += 256) (&pq[0][0])[e] = PQ[ls * (2 * KB) + e];
+    if (threadIdx.x < rows) lrow[threadIdx.x] = idx ? idx[ls + threadIdx.x] : ls + threadIdx.x;
+    __syncthreads();
+#pragma unroll 2
+    for (int rr = 0; rr < rows; ++rr) {
+      const int64_t i = lrow[rr];
+      const double x0 = ok0 ? __ldcs(a + i * n + j0) : 0.0, z0 = ok0 ? __ldcs(b + i * n + j0) : 0.0;
+      const double x1 = ok1 ? __ldcs(a + i * n + j1) : 0.0, z1 = ok1 ? __ldcs(b + i * n + j1) : 0.0;
+#pragma unroll
+      for (int c = 0; c < KB; ++c) {
+        const double pv = pq[rr][c], qv = pq[rr][KB + c];
+        w0[c] = fma(x0, pv, w0[c]);
+        w0[c] = fma(z0, qv, w0[c]);
+        w1[c] = fma(x1, pv, w1[c]);
+        w1[c] = fma(z1, qv, w1[c]);
+      }
+    }
+  }
+  double* out = part + (int64_t)blockIdx.y * n * k;
+#pragma unroll
+  for (int c = 0; c < KB; ++c) {
+    if (c < k) {
+      if (ok0) out[j0 * k + c] = w0[c];
+      if (ok1) out[j1 * k + c] = w1[c];
+    }
+  }
+}
+
+__global__ void k_qm_bwd_reduce(const double* __restrict__ part, int chunks, int64_t nk, double weight,
+                                double* __restrict__ W) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nk) return;
+  double s = 0.0;
+  for (int c = 0; c < chunks; ++c) s += part[(int64_t)c * nk + idx];
+  W[idx] = 0.5 * weight * s;
+}
+
 }  // namespace
+
+// split of the backward pass: measurement chunks so that (column blocks x chunks) covers ~2 waves
+int qm_apply_chunk(int64_t m, int64_t n, int sm_count) {
+  const int64_t cb = (n + kQmBwdCols - 1) / kQmBwdCols;
+  int64_t chunks = std::max<int64_t>(1, (2 * (int64_t)sm_count + cb - 1) / cb);
+  int64_t chunk = (m + chunks - 1) / chunks;
+  chunk = ((chunk + kQmBwdRows - 1) / kQmBwdRows) * kQmBwdRows;
+  return (int)std::max<int64_t>(kQmBwdRows, chunk);
+}
+
+int qm_apply_kb(int k) { return k <= 8 ? 8 : (k <= 16 ? 16 : 32); }
+
+// scratch: PQ (m x 2 KB) followed by the chunk partials (chunks x n x k)
+int64_t qm_apply_scratch_doubles(int64_t m, int64_t n, int k, int sm_count) {
+  const int chunk = qm_apply_chunk(m, n, sm_count);
+  return m * 2 * qm_apply_kb(k) + ((m + chunk - 1) / chunk) * n * k;
+}
+
+void qm_apply(const Launch& L, const double* a, const double* b, const double* res, const int64_t* idx, int64_t m,
+              int64_t n, double weight, const double* U, int64_t ldu, int k, double* W, double* scratch, int sm_count) {
+  if (k < 1 || k > 32) throw Error(MEGB200_ERR_PARAM, "quadratic-measurement block application supports 1 <= k <= 32");
+  const int KB = qm_apply_kb(k);
+  double* PQ = scratch;
+  double* part = scratch + m * 2 * KB;
+  const int chunk = qm_apply_chunk(m, n, sm_count);
+  const int chunks = (int)((m + chunk - 1) / chunk);
+  const dim3 gb((unsigned)((n + kQmBwdCols - 1) / kQmBwdCols), (unsigned)chunks);
+  if (KB == 8) {
+    k_qm_fwd<8, 2><<<(unsigned)((m + 15) / 16), 256, 0, L.stream>>>(a, b, res, idx, m, n, U, ldu, k, PQ);
+    MEG_LAUNCHED();
+    k_qm_bwd<8><<<gb, 256, 0, L.stream>>>(a, b, PQ, idx, m, n, chunk, k, part);
+  } else if (KB == 16) {
+    k_qm_fwd<16, 2><<<(unsigned)((m + 15) / 16), 256, 0, L.stream>>>(a, b, res, idx, m, n, U, ldu, k, PQ);
+    MEG_LAUNCHED();
+    k_qm_bwd<16><<<gb, 256, 0, L.stream>>>(a, b, PQ, idx, m, n, chunk, k, part);
+  } else {
+    k_qm_fwd<32, 1><<<(unsigned)((m + 7) / 8), 256, 0, L.stream>>>(a, b, res, idx, m, n, U, ldu, k, PQ);
+    MEG_LAUNCHED();
+    k_qm_bwd<32><<<gb, 256, 0, L.stream>>>(a, b, PQ, idx, m, n, chunk, k, part);
+  }
+  MEG_LAUNCHED();
+  k_qm_bwd_reduce<<<(unsigned)((n * k + 255) / 256), 256, 0, L.stream>>>(part, chunks, n * k, weight, W);
+  MEG_LAUNCHED();
+  *L.counter += 3;
+}
 
 void qm_residuals(const Launch& L, const double* a, const double* b, const double* y, int64_t m, int64_t n,
                   const double* V, int64_t ldv, int r, const QmCoef& qc, double* res) {

@@ -269,6 +269,11 @@ void prof_end(megb200_solver* s, int ev0, const OpDev& op, int k) {
   s->prof_passes++;
 }
 
+void check_qm_data(const megb200_qm_data* q) {
+  if (!q || !q->a || !q->b || !q->res || q->m < 1 || !q->scratch)
+    throw Error(MEGB200_ERR_PARAM, "quadratic-measurement operator data missing");
+}
+
 // Streamed operand pass alone: partial slices of Op U into s->part; returns the slice count.
 int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k) {
   Launch L = s->launch();
@@ -288,6 +293,14 @@ int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu
     // the callback's last stream operation may be a copy: the programmatically dependent launches
     // that follow only order against kernels, so its completion is waited for here
     s->sync();
+    return 1;
+  }
+  if (op.kind == MEGB200_OP_QUADMEAS && op.scale != 0.0) {
+    // matrix-free quadratic-measurement gradient: two streaming passes over a and b write the one slice
+    const megb200_qm_data* q = static_cast<const megb200_qm_data*>(op.apply_ctx);
+    if (q->scratch_len < qm_apply_scratch_doubles(q->m, n, k, s->sm_count))
+      throw Error(MEGB200_ERR_PARAM, "quadratic-measurement scratch too small (megb200_qm_apply_scratch)");
+    qm_apply(L, q->a, q->b, q->res, q->idx, q->m, n, q->weight, U, ldu, k, s->part, q->scratch, s->sm_count);
     return 1;
   }
   // live profiling brackets the streamed operand kernel only (the roofline's dominant kernel)
@@ -338,6 +351,7 @@ OpDev op_from_public(megb200_solver* s, const megb200_operator* op) {
   o.apply = op->apply;
   o.apply_ctx = op->apply_ctx;
   if (o.kind == MEGB200_OP_CALLBACK && !o.apply) throw Error(MEGB200_ERR_PARAM, "callback operator without apply");
+  if (o.kind == MEGB200_OP_QUADMEAS) check_qm_data(static_cast<const megb200_qm_data*>(o.apply_ctx));
   if (o.kind == MEGB200_OP_DENSE && (!o.dense || o.ld < s->n)) throw Error(MEGB200_ERR_PARAM, "dense operand missing");
   if (o.kind == MEGB200_OP_CSR && (!o.rowptr || !o.col || !o.val)) throw Error(MEGB200_ERR_PARAM, "CSR operand missing");
   if (op->l > 0) {
@@ -931,6 +945,9 @@ void check_gradient(megb200_solver* s, const megb200_gradient* g) {
     case MEGB200_GRAD_CALLBACK:
       if (!g->apply) throw Error(MEGB200_ERR_PARAM, "callback gradient without apply");
       break;
+    case MEGB200_GRAD_QUADMEAS:
+      check_qm_data(static_cast<const megb200_qm_data*>(g->apply_ctx));
+      break;
     case MEGB200_GRAD_SAMPLED:
       if (!g->rowptr || !g->col || !g->obs) throw Error(MEGB200_ERR_PARAM, "sampled pattern missing");
       if (g->nnz > s->max_nnz) throw Error(MEGB200_ERR_PARAM, "nnz exceeds the solver's max_nnz");
@@ -940,7 +957,7 @@ void check_gradient(megb200_solver* s, const megb200_gradient* g) {
       throw Error(MEGB200_ERR_PARAM, "unknown gradient kind");
   }
   if (g->gV && (g->g_r >= g->n || !(g->g_eps > 0.0)) && g->kind != MEGB200_GRAD_ZERO && g->kind != MEGB200_GRAD_DENSE &&
-      g->kind != MEGB200_GRAD_CALLBACK)
+      g->kind != MEGB200_GRAD_CALLBACK && g->kind != MEGB200_GRAD_QUADMEAS)
     throw Error(MEGB200_ERR_PARAM, "invalid gradient iterate");
 }
 
@@ -1021,6 +1038,11 @@ StepOperator build_step_operator(megb200_solver* s, const megb200_iterate* x, co
     case MEGB200_GRAD_CALLBACK:
       op.kind = MEGB200_OP_CALLBACK;
       op.apply = g->apply;
+      op.apply_ctx = g->apply_ctx;
+      op.scale = -eta;
+      break;
+    case MEGB200_GRAD_QUADMEAS:
+      op.kind = MEGB200_OP_QUADMEAS;
       op.apply_ctx = g->apply_ctx;
       op.scale = -eta;
       break;
@@ -1343,6 +1365,11 @@ int megb200_gradient_apply(megb200_solver* s, const megb200_gradient* g, const d
       case MEGB200_GRAD_CALLBACK:
         op.kind = MEGB200_OP_CALLBACK;
         op.apply = g->apply;
+        op.apply_ctx = g->apply_ctx;
+        op.scale = 1.0;
+        break;
+      case MEGB200_GRAD_QUADMEAS:
+        op.kind = MEGB200_OP_QUADMEAS;
         op.apply_ctx = g->apply_ctx;
         op.scale = 1.0;
         break;
@@ -2351,6 +2378,24 @@ int megb200_qm_value(megb200_solver* s, const double* res, int64_t m, double* va
     s->d2h(s->h_buf, s->small, 1);
     s->sync();
     *value = s->h_buf[0];
+  });
+}
+
+int64_t megb200_qm_apply_scratch(megb200_solver* s, int64_t m, int32_t k) {
+  if (!s || m < 1 || k < 1 || k > 32) return -1;
+  return qm_apply_scratch_doubles(m, s->n, k, s->sm_count);
+}
+
+int megb200_qm_apply(megb200_solver* s, const megb200_qm_data* q, const double* U, int64_t ldu, int32_t k,
+                     double* W, int64_t ldw) {
+  return guarded_impl([&] {
+    if (!s || !U || !W || k < 1 || ldu < k || ldw < k) throw Error(MEGB200_ERR_PARAM, "invalid block");
+    check_qm_data(q);
+    OpDev op;
+    op.kind = MEGB200_OP_QUADMEAS;
+    op.apply_ctx = const_cast<megb200_qm_data*>(q);
+    op.scale = 1.0;
+    apply_op_wide(s, op, U, ldu, k, W, ldw);
   });
 }
 

@@ -60,7 +60,7 @@ class SymmetricOperator:
     """Device symmetric operator  u -> scale * Op u + L diag(d) L^T u + alpha u."""
 
     def __init__(self, dim: int, apply_fn=None, *, dense=None, csr=None, scale: float = 1.0, L=None, d=None,
-                 alpha: float = 0.0):
+                 alpha: float = 0.0, qm=None):
         """`SymmetricOperator(dim, apply_fn)` is the reference's form (linalg.py:89-94): apply_fn
         takes a numpy (n, k) block (or torch CUDA tensors when marked with
         callbacks.device_callable) and is called once per block pass through the C ABI's callback
@@ -71,6 +71,7 @@ class SymmetricOperator:
         self.callback = ApplyCallback(apply_fn, self.dim) if apply_fn is not None else None
         self.dense = dense  # torch (n, n) f64/f32 contiguous, symmetric
         self.csr = csr  # (rowptr int32, col int32, val f64) torch tensors
+        self.qm = qm  # objectives.QuadMeasOperand: matrix-free measurement gradient (OP_QUADMEAS)
         self.scale = float(scale)
         self.L = L  # torch (n, l) f64 or None
         self.d = None if d is None else runtime.host_f64(d)
@@ -108,6 +109,9 @@ class SymmetricOperator:
             op.kind = _lib.OP_CSR
             op.rowptr, op.col, op.val = rp.data_ptr(), cl.data_ptr(), vl.data_ptr()
             op.nnz = cl.numel()
+        elif self.qm is not None:
+            op.kind = _lib.OP_QUADMEAS
+            op.apply_ctx = self.qm.ctx(keep)
         elif self.callback is not None:
             op.kind = _lib.OP_CALLBACK
             op.apply = self.callback.c_fn

@@ -35,9 +35,10 @@ class GradientOperator:
     """A gradient evaluated at a bound iterate (device descriptor, see module doc)."""
 
     def __init__(self, kind: int, n: int, *, dense=None, csr=None, obs=None, x=None, A=None, sigma: float = 0.0,
-                 owner=None, callback=None):
+                 owner=None, callback=None, qm=None):
         self.kind = kind
         self.callback = callback  # callbacks.ApplyCallback (GRAD_CALLBACK)
+        self.qm = qm  # QuadMeasOperand (GRAD_QUADMEAS)
         self.n = int(n)
         self.dense = dense
         self.csr = csr
@@ -94,6 +95,8 @@ class GradientOperator:
             g.sigma = self.sigma
         if self.callback is not None:
             g.apply = self.callback.c_fn
+        if self.qm is not None:
+            g.apply_ctx = self.qm.ctx(keep)
         return g
 
     def solver(self):
@@ -309,6 +312,28 @@ class StochasticFrobeniusObjective(FrobeniusObjective):
                                 sigma=self.sigma, owner=self)
 
 
+class QuadMeasOperand:
+    """Device arrays of the matrix-free measurement gradient weight * sym(a^T diag(res) b) (the C
+    ABI's megb200_qm_data): a, b, the residuals it is evaluated at and the pass scratch."""
+
+    def __init__(self, objective: "QuadMeasObjective", res: torch.Tensor, weight: float, idx: torch.Tensor | None = None):
+        self.objective = objective
+        self.res = res
+        self.weight = float(weight)
+        self.idx = idx  # device int64 mini-batch indices, or None for every measurement
+
+    def ctx(self, keep: list) -> int:
+        o = self.objective
+        scratch = o._apply_scratch()
+        d = _lib.QmData(a=o.a.data_ptr(), b=o.b.data_ptr(), res=self.res.data_ptr(),
+                        m=o.m if self.idx is None else int(self.idx.numel()),
+                        idx=None if self.idx is None else self.idx.data_ptr(), weight=self.weight,
+                        scratch=scratch.data_ptr(), scratch_len=scratch.numel())
+        keep.append(d)
+        keep.append(self)
+        return C.addressof(d)
+
+
 class QuadMeasObjective:
     """The paper's recovery experiment (reference RecoveryObjective,
     objectives.py:174-228): g(X) = f(tau X) on the unit-trace cone,
@@ -318,9 +343,14 @@ class QuadMeasObjective:
     residuals of x from its factors on the device (k_qm_residuals, the structured
     measurement of objectives.py:111-118) and materialises tau * grad f(tau X) =
     tau * sym(a^T diag(res) b) (k_qm_grad_part / k_qm_grad_reduce; the reference's own dense
-    path, objectives.py:211-216), which the step consumes as its dense gradient."""
+    path, objectives.py:211-216), which the step consumes as its dense gradient.  Above `dense_cap`
+    (default 1024, the reference's) the gradient is never formed: the operator is matrix-free,
+    two streaming passes over a and b per block application (k_qm_fwd / k_qm_bwd; the reference's
+    _apply_measurement_gradient, objectives.py:152-158 and :218-221)."""
 
-    def __init__(self, a, b, y, tau: float):
+    def __init__(self, a, b, y, tau: float, dense_cap: int = 1024):
+        self.dense_cap = int(dense_cap)
+        self._scratch = None
         self.a = runtime.as_device_f64(a).contiguous()
         self.b = runtime.as_device_f64(b).contiguous()
         self.y = runtime.as_device_f64(np.asarray(y, dtype=np.float64).ravel() if not isinstance(y, torch.Tensor)
@@ -352,6 +382,42 @@ class QuadMeasObjective:
     def _solver(self):
         return runtime.solver_for(self.n)
 
+    @property
+    def matrix_free(self) -> bool:
+        return self.n > self.dense_cap
+
+    def _apply_scratch(self) -> torch.Tensor:
+        if self._scratch is None:
+            s = self._solver()
+            need = int(s.lib.megb200_qm_apply_scratch(s.handle, self.m, 32))
+            self._scratch = torch.empty(need, dtype=torch.float64, device=runtime.device())
+        return self._scratch
+
+    def _operator(self, res: torch.Tensor, weight: float, scale: float = 1.0):
+        """weight * sym(a^T diag(res) b) as a device operator (_operator_from_residuals,
+        objectives.py:214-221): materialised up to dense_cap, matrix-free above it."""
+        from .linalg import SymmetricOperator
+
+        if self.matrix_free:
+            return SymmetricOperator(self.n, qm=QuadMeasOperand(self, res, weight), scale=scale)
+        return SymmetricOperator(self.n, dense=self.gradient_matrix(res, weight=weight), scale=scale)
+
+    def apply_gradient(self, res: torch.Tensor, u, weight: float | None = None) -> torch.Tensor:
+        """weight / 2 (a^T (res * (b u)) + b^T (res * (a u))) for a device block u (n x k, k <= 32)
+        without forming the gradient (_apply_measurement_gradient, objectives.py:152-158)."""
+        s = self._solver()
+        ut = runtime.as_device_f64(u)
+        vec = ut.dim() == 1
+        if vec:
+            ut = ut.reshape(-1, 1)
+        ut = ut.contiguous()
+        w = torch.empty_like(ut)
+        keep: list = []
+        q = QuadMeasOperand(self, res, self.tau if weight is None else weight)
+        runtime.check(s.lib.megb200_qm_apply(s.handle, q.ctx(keep), ut.data_ptr(), ut.stride(0), int(ut.shape[1]),
+                                             w.data_ptr(), w.stride(0)))
+        return w.reshape(-1) if vec else w
+
     def residuals(self, x) -> torch.Tensor:
         """a_i^T (tau X) b_i - y_i for a factored iterate (device tensor of length m)."""
         if x.n != self.n:
@@ -381,8 +447,7 @@ class QuadMeasObjective:
         u = rng.standard_normal((self.n, r))
         u /= np.linalg.norm(u)
         res = self._residuals(u, np.ones(r), 0.0)
-        G = self.gradient_matrix(res, weight=1.0)
-        top = lanczos_top_r(SymmetricOperator(self.n, dense=G, scale=-1.0), r, tol=tol, seed=seed)
+        top = lanczos_top_r(self._operator(res, 1.0, scale=-1.0), r, tol=tol, seed=seed)
         w = project_simplex(-np.asarray(top.eigenvalues, dtype=float), self.tau)
         w = w / w.sum()
         w = np.maximum(w, 1e-12)
@@ -395,8 +460,7 @@ class QuadMeasObjective:
         from .linalg import SymmetricOperator, lanczos_top_r
 
         res = self.residuals(x)
-        G = self.gradient_matrix(res, weight=1.0)
-        top = lanczos_top_r(SymmetricOperator(self.n, dense=G, scale=-1.0), 1, tol=tol, seed=seed)
+        top = lanczos_top_r(self._operator(res, 1.0, scale=-1.0), 1, tol=tol, seed=seed)
         r_h = res.cpu().numpy()
         trace_term = float(r_h @ (r_h + self.y.cpu().numpy()))
         return trace_term + self.tau * float(top.eigenvalues[0])
@@ -427,8 +491,12 @@ class QuadMeasObjective:
         return self.gradient_matrix(res.contiguous())
 
     def grad_operator(self, x, t: int = 0) -> GradientOperator:
-        """tau * grad f(tau X) at x, materialised on the device (RecoveryObjective.grad_operator)."""
-        G = self.gradient_matrix(self.residuals(x))
+        """tau * grad f(tau X) at x (RecoveryObjective.grad_operator, objectives.py:211-221):
+        materialised on the device up to dense_cap, matrix-free above it."""
+        res = self.residuals(x)
+        if self.matrix_free:
+            return GradientOperator(_lib.GRAD_QUADMEAS, self.n, qm=QuadMeasOperand(self, res, self.tau), owner=self)
+        G = self.gradient_matrix(res)
         return GradientOperator(_lib.GRAD_DENSE, self.n, dense=G, owner=self)
 
 
@@ -458,8 +526,10 @@ class QuadMeasStochasticOracle:
         if idx.numel() < 1:
             raise ParameterError("batch must contain at least one index")
         s = obj._solver()
-        G = torch.empty((obj.n, obj.n), dtype=torch.float64, device=runtime.device())
         w = obj.tau * obj.m / idx.numel()
+        if obj.matrix_free and idx.numel() <= obj.m:  # objectives.py:266-269 (the scratch is sized for m rows)
+            return GradientOperator(_lib.GRAD_QUADMEAS, obj.n, qm=QuadMeasOperand(obj, res, w, idx), owner=(obj, idx))
+        G = torch.empty((obj.n, obj.n), dtype=torch.float64, device=runtime.device())
         runtime.check(s.lib.megb200_qm_gradient_batch(s.handle, obj.a.data_ptr(), obj.b.data_ptr(), res.data_ptr(),
                                                       idx.data_ptr(), idx.numel(), w, G.data_ptr(), G.stride(0)))
         return GradientOperator(_lib.GRAD_DENSE, obj.n, dense=G, owner=(obj, idx))

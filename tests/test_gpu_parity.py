@@ -478,6 +478,74 @@ def test_quad_meas_stochastic_matches_reference_golden(pb, name):
     compare_trajectory({k: np.array(v) for k, v in got.items()}, g, TOL["f64"])
 
 
+@pytest.mark.parametrize("n,r,ks", [(100, 5, (1, 5, 13, 20, 32, 40)), (1100, 1, (1, 9, 18))])
+def test_quad_meas_matrix_free_apply(pb, n, r, ks):
+    """The matrix-free block application of the measurement gradient (k_qm_fwd / k_qm_bwd,
+    reference _apply_measurement_gradient objectives.py:152-158) against the oracle restatement
+    and against the materialised gradient, over all measurements and over a mini-batch with
+    repeats, for block widths on both sides of the kernels' 8 / 16 / 32 register tiles (1e-12)."""
+    from oracle import qm as oq
+    from paper_2012_10469_b200 import _lib as _plib
+
+    inst = oq.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=3)
+    dev = pb.QuadMeasObjective.from_instance(inst)
+    ox = oq.start_iterate(n, r, 3, 0.6 / 121)
+    x = pb.LowRankIterate(n, r, ox.V, ox.lam, ox.eps)
+    res_o = oq.residuals(inst, ox)
+    res_d = dev.residuals(x)
+    rng = np.random.default_rng(17)
+    batch = rng.integers(0, inst.m, size=max(1, inst.m // 7))
+    for k in ks:
+        u = rng.standard_normal((n, k))
+        want = inst.tau * oq.apply_measurement_gradient(inst.a, inst.b, res_o, u)
+        got = dev.apply_gradient(res_d, u).cpu().numpy()
+        assert normwise(got, want) <= 1e-12
+    u = rng.standard_normal((n, 7))
+    w = inst.tau * inst.m / batch.size
+    want = w * oq.apply_measurement_gradient(inst.a[batch], inst.b[batch], res_o[batch], u)
+    sto = pb.QuadMeasStochasticOracle(dev, batch.size, seed=0)
+    dev.dense_cap = 0  # matrix-free at any n
+    op = sto.grad_operator(x, batch)
+    assert op.kind == _plib.GRAD_QUADMEAS
+    assert normwise(op(u), want) <= 1e-12
+    dev.dense_cap = 10 ** 9
+    assert normwise(sto.grad_operator(x, batch)(u), want) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["qm_n100_r5", "qm_n60_r3"])
+def test_quad_meas_matrix_free_matches_reference_golden(pb, name):
+    """The MEG trajectory with the matrix-free operator (dense_cap = 0: what RecoveryObjective
+    does above dense_cap, objectives.py:218-221) against the unmodified reference's golden run
+    (1e-9), plus spectral_init and the dual gap through the same operator."""
+    from oracle import qm as oq
+    from paper_2012_10469_b200 import _lib as _plib
+    from tests.test_oracle_pins import _qm_eps, qm_projector_err
+
+    g = load_golden(name)
+    n, r, seed = int(g["n"]), int(g["r"]), int(g["seed"])
+    inst = oq.generate_instance(n, r, kappa=0.5, tau_fraction=0.5, seed=seed)
+    dev = pb.QuadMeasObjective(inst.a, inst.b, inst.y, inst.tau, dense_cap=0)
+    assert dev.matrix_free
+    x = pb.LowRankIterate(n, r, g["V0"], g["lam0"], float(g["eps0"]))
+    eta = float(g["eta"])
+    got = {k: [] for k in ("shift", "y", "lam", "lhs", "f")}
+    for t in range(len(g["shift"])):
+        gop = dev.grad_operator(x)
+        assert gop.kind == _plib.GRAD_QUADMEAS
+        res = pb.lowrank_meg_step(x, gop, eta, _qm_eps(t + 1), svd_seed=t)
+        x = res.iterate
+        for k, v in (("shift", res.shift), ("y", res.top_eigenvalues), ("lam", x.lam), ("lhs", res.cert.lhs_cheap),
+                     ("f", dev.value(x))):
+            got[k].append(v)
+        assert qm_projector_err(x.V, x.lam, x.eps, g["V"][t], g["lam"][t], float(g["eps"][t])) <= 1e-9
+    compare_trajectory({k: np.array(v) for k, v in got.items()}, g, TOL["f64"])
+    V, w = dev.spectral_init(r, seed=seed)
+    P, Pg = (V * w) @ V.T, (g["si_V"] * g["si_w"]) @ g["si_V"].T
+    assert np.max(np.abs(P - Pg)) <= 1e-9 * np.max(np.abs(Pg))
+    xg = pb.LowRankIterate(n, r, g["V"][-1], g["lam"][-1], float(g["eps"][-1]))
+    assert abs(dev.dual_gap(xg, seed=seed) - float(g["gap_final"])) <= 1e-9 * abs(float(g["gap_final"]))
+
+
 @pytest.mark.parametrize("name", ["qm_n100_r1", "qm_n60_r3", "qm_n100_r5"])
 def test_quad_meas_spectral_init_and_dual_gap(pb, name):
     """QuadMeasObjective.spectral_init (probe residuals with eps = 0, gradient, block solver on

@@ -307,3 +307,18 @@ def test_oracle_shadow_lockstep_matches_reference():
         assert abs(om.bregman(w, x.densify())[0] - g0["bregman"][t]) <= 1e-9 * abs(g0["bregman"][t])
         assert abs(om.bregman_structured(w, x) - g0["bregman_structured"][t]) <= 1e-9 * abs(g0["bregman"][t])
     assert np.max(np.abs(w - g0["W_final"])) <= 1e-10
+
+
+def test_qm_matrix_free_apply_oracle():
+    """oracle.qm.apply_measurement_gradient (objectives.py:152-158) equals the materialised
+    gradient's product (objectives.py:155-156) -- the identity the reference's dense_cap switch
+    relies on (objectives.py:214-221) -- for a vector and for a block."""
+    from oracle import qm as oq
+
+    inst = oq.generate_instance(40, 2, kappa=0.5, tau_fraction=0.5, seed=4)
+    rng = np.random.default_rng(0)
+    res = rng.standard_normal(inst.m)
+    G = oq.dense_gradient(inst, res, 1.0)
+    for u in (rng.standard_normal(40), rng.standard_normal((40, 6))):
+        got = oq.apply_measurement_gradient(inst.a, inst.b, res, u)
+        assert np.max(np.abs(got - G @ u)) <= 1e-13 * np.max(np.abs(G @ u))
