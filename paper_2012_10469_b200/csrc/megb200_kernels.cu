@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -315,6 +317,11 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void tma_2d_stream(void* dst, const CUtensorMap* map, int x, int y, uint64_t* b,
                                               uint64_t policy) {
   asm volatile(
@@ -538,6 +545,17 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(pipe::su32(dst)), "l"(src) : "memory");
 }
 
+// diagnostics (MEGB200_PASS_STAMPS): %globaltimer per CTA at the pass's phase boundaries
+// (0 CTA start, 1 dependency wait over, 2 first stage landed, 3 last stage consumed, 4 partials stored)
+__device__ unsigned long long g_pass_ns[160 * 8];
+__device__ __forceinline__ void pass_stamp(int on, int slot) {
+  if (on) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    g_pass_ns[blockIdx.x * 8 + slot] = v;
+  }
+}
+
 template <int NT, int TAIL, int CW, bool STEP>
 __device__ __forceinline__ void dense_mma_body(const CUtensorMap* tmM, const CUtensorMap* tmU, int64_t n, int b,
                                                double* __restrict__ part, int tiles, int kch, int smax,
@@ -545,7 +563,9 @@ __device__ __forceinline__ void dense_mma_body(const CUtensorMap* tmM, const CUt
                                                const double* __restrict__ Ug = nullptr, int64_t ldu = 0,
                                                double* __restrict__ hpart = nullptr,
                                                const unsigned long long* wait_ctr = nullptr,
-                                               unsigned long long wait_target = 0) {
+                                               unsigned long long wait_target = 0, int keep_q = 0, int keep_p = 1,
+                                               int stamps = 0) {
+  if (threadIdx.x == 0) pass_stamp(stamps, 0);
   const int64_t utot = (int64_t)tiles * kch;
   const int64_t ua = (int64_t)blockIdx.x * utot / gridDim.x, ub = (int64_t)(blockIdx.x + 1) * utot / gridDim.x;
   // Operand stage = 8 TMA boxes of 16 (i) x 32 (k) doubles with the 128-byte
@@ -588,15 +608,21 @@ __device__ __forceinline__ void dense_mma_body(const CUtensorMap* tmM, const CUt
     __syncthreads();
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
+  if (threadIdx.x == 0) pass_stamp(stamps, 1);
   if (warp == CW) {
     if (lane == 0) {
       const uint32_t stage_bytes = (uint32_t)(kPipeKC * kMmaRows * 8 + kPipeKC * BNP * 8);
-      const uint64_t pol = pipe::evict_first_policy();
+      // L2 residency: keep_q of every keep_p consecutive units are loaded evict-last (they stay in the
+      // 126 MB L2 from pass to pass when the operand is not much larger than it), the rest evict-first;
+      // interleaved by unit so every CTA's range holds the same mix
+      const uint64_t pol_first = pipe::evict_first_policy();
+      const uint64_t pol_last = keep_q > 0 ? pipe::evict_last_policy() : pol_first;
       int st = 0;
       uint32_t ph = 0;
       for (int64_t u = ua; u < ub; ++u) {
         const int tile = (int)(u / kch);
         const int64_t kc = (u - (int64_t)tile * kch) * kPipeKC;
+        const uint64_t pol = (int)(u % keep_p) < keep_q ? pol_last : pol_first;
         {
           pipe::bar_wait(empty + st, ph ^ 1u);
           pipe::bar_arrive_tx(full + st, stage_bytes);
@@ -658,6 +684,7 @@ __device__ __forceinline__ void dense_mma_body(const CUtensorMap* tmM, const CUt
       const int64_t kc = (u - (int64_t)tile * kch) * kPipeKC;
       const int nk = (int)min((int64_t)kPipeKC, n - kc);  // the last chunk of a row may be short
       pipe::bar_wait(full + st, ph);
+      if (threadIdx.x == 0 && u == ua) pass_stamp(stamps, 2);
       const char* box = reinterpret_cast<const char*>(Ms + (size_t)st * kPipeKC * kMmaRows) + (warp / (CW / 8)) * 4096;
       const double* us = Us + (size_t)st * kPipeKC * BNP;
       auto mma_k = [&](int k, double (&ac)[MT][NT][2]) {  // one m8n8k4 step over k rows {k + kperm}
@@ -734,6 +761,7 @@ __device__ __forceinline__ void dense_mma_body(const CUtensorMap* tmM, const CUt
         ph ^= 1u;
       }
     }
+    if (threadIdx.x == 0 && u == ub) pass_stamp(stamps, 3);
     // C fragment: row g, columns 2*tq, 2*tq+1 of each 8x8 tile
     double* out = part + (int64_t)slot * n * b;
     const int rbase = (CW == 16) ? warp * 8 : warp * 16;
@@ -825,17 +853,19 @@ __device__ __forceinline__ void dense_mma_body(const CUtensorMap* tmM, const CUt
       if (o < b * b) hpart[(int64_t)blockIdx.x * kFusedStride + o] = hc[j];
     }
   }
+  if (threadIdx.x == 0) pass_stamp(stamps, 4);
 }
 
 template <int NT, int TAIL, int CW>
 __global__ void __launch_bounds__(32 * (CW + 1), 1)
     k_dense_pass_mma(const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmU, int64_t n,
                      int b, double* __restrict__ part, int tiles, int kch, int smax,
-                     const unsigned long long* wait_ctr, unsigned long long wait_target) {
+                     const unsigned long long* wait_ctr, unsigned long long wait_target, int keep_q, int keep_p,
+                     int stamps) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* base = smem + ((1024 - ((uintptr_t)smem & 1023)) & 1023);
   dense_mma_body<NT, TAIL, CW, false>(&tmM, &tmU, n, b, part, tiles, kch, smax, base, nullptr, nullptr, nullptr,
-                                      nullptr, 0, nullptr, wait_ctr, wait_target);
+                                      nullptr, 0, nullptr, wait_ctr, wait_target, keep_q, keep_p, stamps);
 }
 
 // ===========================================================================
@@ -1730,6 +1760,27 @@ int mma_consumer_warps() {
   return cw;
 }
 
+// Share of the operand's units loaded evict-last (L2-resident from pass to pass): none by default;
+// MEGB200_L2_KEEP="q/p" (diagnostics) sets it
+void l2_keep_fraction(int64_t operand_bytes, int* q, int* p) {
+  static const int env_q = [] {
+    const char* e = getenv("MEGB200_L2_KEEP");
+    return e ? atoi(e) : -1;
+  }();
+  static const int env_p = [] {
+    const char* e = getenv("MEGB200_L2_KEEP");
+    const char* s = e ? strchr(e, '/') : nullptr;
+    return s ? std::max(1, atoi(s + 1)) : 8;
+  }();
+  (void)operand_bytes;
+  *q = 0;
+  *p = 1;
+  if (env_q >= 0) {
+    *q = env_q;
+    *p = env_p;
+  }
+}
+
 template <int NT, int TAIL>
 void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
                      double* part, int tiles, int kch, int smax, int grid) {
@@ -1758,12 +1809,15 @@ void launch_pipe_mma(const Launch& L, const double* M, int64_t ldm, int64_t n, c
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
+  int keep_q = 0, keep_p = 1;
+  l2_keep_fraction((int64_t)n * n * 8, &keep_q, &keep_p);
+  static const int stamps = getenv("MEGB200_PASS_STAMPS") != nullptr;
   if (cw == 16)
     MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL, 16>, tmM, tmU, n, b, part, tiles, kch, smax,
-                                L.wait_ctr, L.wait_target));
+                                L.wait_ctr, L.wait_target, keep_q, keep_p, stamps));
   else
     MEG_CUDA(cudaLaunchKernelEx(&cfg, k_dense_pass_mma<NT, TAIL, 8>, tmM, tmU, n, b, part, tiles, kch, smax,
-                                L.wait_ctr, L.wait_target));
+                                L.wait_ctr, L.wait_target, keep_q, keep_p, stamps));
   MEG_LAUNCHED();
   ++*L.counter;
 }
@@ -2144,3 +2198,11 @@ void reduce_sum(const Launch& L, const double* part, int slots, int width, doubl
 }
 
 }  // namespace megb200
+
+// Diagnostics: per-CTA phase timestamps of the last float64 DMMA pass (MEGB200_PASS_STAMPS=1)
+extern "C" int megb200_debug_pass_ns(unsigned long long* out, int count) {
+  if (!out || count < 1 || count > 160 * 8) return MEGB200_ERR_PARAM;
+  return cudaMemcpyFromSymbol(out, megb200::g_pass_ns, sizeof(unsigned long long) * count) == cudaSuccess
+             ? MEGB200_OK
+             : MEGB200_ERR_CUDA;
+}
