@@ -116,6 +116,12 @@ __device__ __forceinline__ void store_partial(double* __restrict__ part, int pq,
 // g = lane, lane + 32, ... in parallel (independent L2 loads) and combine with a
 // fixed xor-shuffle tree, so the result is reproducible and the latency is one
 // round trip instead of G dependent ones.
+__device__ __forceinline__ double warp_min_f64(double v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
+  return v;
+}
+
 __device__ __forceinline__ double warp_sum_partials(const double* __restrict__ part, int G, int64_t stride, int o) {
   const int lane = threadIdx.x & 31;
   double v[5];
@@ -196,9 +202,11 @@ __device__ __forceinline__ void reduce_partials(const double* __restrict__ part,
 // only), mask; optionally Rtot = Rrel * Rprev.
 __device__ void block_cholesky(const double* __restrict__ Gg, int q, double thresh, double* sm,
                                double* __restrict__ Rrel, double* __restrict__ Rinv, int* __restrict__ mask,
-                               const double* __restrict__ Rprev, double* __restrict__ Rtot) {
+                               const double* __restrict__ Rprev, double* __restrict__ Rtot,
+                               double* pivot_min = nullptr) {
   const int t = threadIdx.x, nth = blockDim.x;
   const int ld = q + 1;
+  double pmin = 1.0;  // smallest equilibrated pivot (every thread tracks it from shared memory)
   double* A = sm;             // q x ld   (factorised in place: upper triangle -> Rs)
   double* X = sm + q * ld;    // q x ld   (Rs^-1)
   double* D = X + q * ld;     // q
@@ -221,49 +229,50 @@ __device__ void block_cholesky(const double* __restrict__ Gg, int q, double thre
     A[i * ld + j] = (bad[i] || bad[j]) ? (i == j ? 1.0 : 0.0) : A[i * ld + j] / (D[i] * D[j]);
   }
   __syncthreads();
-  // right-looking factorisation: column j pivot by thread 0, row scale + trailing update in parallel
-  for (int j = 0; j < q; ++j) {
-    if (t == 0) {
+  // right-looking factorisation and R^-1 by ONE warp with warp barriers only (q <= 64 columns: a
+  // column step is a few hundred cycles, which CTA-wide barriers and a one-thread pivot dominated --
+  // 22 us at q = 18).  Every lane forms the pivot (reciprocal square root, r = d * rsqrt(d)); lane l
+  // owns column l of the trailing update and of R^-1 (no barrier inside a column's back substitution).
+  if (t < 32) {
+    const int lane = t;
+    for (int j = 0; j < q; ++j) {
       const double d = A[j * ld + j];
       const bool bj = bad[j] || !(d > 1e-20);
-      bad[j] = bj;
-      const double r = bj ? 1.0 : sqrt(d);
-      A[j * ld + j] = r;
-      rd[j] = 1.0 / r;
+      const double ir = bj ? 1.0 : rsqrt(d);
+      const double r = bj ? 1.0 : d * ir;
+      for (int k = j + 1 + lane; k < q; k += 32) A[j * ld + k] = bj ? 0.0 : A[j * ld + k] * ir;
+      __syncwarp();
+      if (lane == 0) {
+        bad[j] = bj;
+        A[j * ld + j] = r;
+        rd[j] = ir;
+      }
+      for (int l = j + 1 + lane; l < q; l += 32) {
+        const double ajl = A[j * ld + l];
+        for (int k = j + 1; k <= l; ++k) A[k * ld + l] -= A[j * ld + k] * ajl;
+      }
+      __syncwarp();
     }
-    __syncthreads();
-    const double ir = rd[j];
-    const bool bj = bad[j];
-    for (int k = j + 1 + t; k < q; k += nth) A[j * ld + k] = bj ? 0.0 : A[j * ld + k] * ir;
-    __syncthreads();
-    const int m = q - j - 1;
-    for (int idx = t; idx < m * m; idx += nth) {
-      const int k = j + 1 + idx / m, l = j + 1 + idx % m;
-      if (l >= k) A[k * ld + l] -= A[j * ld + k] * A[j * ld + l];
-    }
-    __syncthreads();
-  }
-  // Rs^-1 by rows from the bottom: X[i][c] = -rd_i * sum_{k=i+1..c} Rs[i][k] X[k][c], X[i][i] = rd_i
-  for (int i = q - 1; i >= 0; --i) {
-    for (int c = i + t; c < q; c += nth) {
-      double v;
-      if (c == i) {
-        v = rd[i];
-      } else {
+    // Rs^-1 by columns: X[i][c] = -rd_i * sum_{k=i+1..c} Rs[i][k] X[k][c], X[c][c] = rd_c
+    for (int c = lane; c < q; c += 32) {
+      X[c * ld + c] = rd[c];
+      for (int i = c - 1; i >= 0; --i) {
         double s = 0.0;
         for (int k = i + 1; k <= c; ++k) s = fma(A[i * ld + k], X[k * ld + c], s);
-        v = -s * rd[i];
+        X[i * ld + c] = -s * rd[i];
       }
-      X[i * ld + c] = v;
     }
-    __syncthreads();
   }
+  __syncthreads();
+  pmin = 1.0;
+  for (int j = 0; j < q; ++j) pmin = bad[j] ? 0.0 : fmin(pmin, 1.0 / (rd[j] * rd[j]));
   for (int idx = t; idx < q * q; idx += nth) {
     const int i = idx / q, j = idx - i * q;
     Rinv[idx] = (i <= j) ? X[i * ld + j] / D[i] : 0.0;
     Rrel[idx] = (bad[i] || j < i) ? 0.0 : A[i * ld + j] * D[j];
   }
   for (int i = t; i < q; i += nth) mask[i] = bad[i];
+  if (pivot_min) *pivot_min = pmin;
   if (Rtot) {
     for (int idx = t; idx < q * q; idx += nth) {
       const int i = idx / q, j = idx - i * q;
@@ -502,7 +511,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
                                                      uint64_t key, uint64_t base, double* __restrict__ part,
                                                      double* __restrict__ Cws, double* __restrict__ Gws,
                                                      double* __restrict__ Rinv, int* __restrict__ mask,
-                                                     double* __restrict__ Rrel, int cgs_rounds) {
+                                                     double* __restrict__ Rrel, int cgs_rounds, int pip) {
   extern __shared__ double sm[];
   phase_mark(50);
   cg::grid_group grid = cg::this_grid();
@@ -618,10 +627,149 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
     __syncthreads();
     phase_mark(pm++);
   };
-  for (int round = 0; round < cgs_rounds && cols > 0; ++round) cgs();
-  cholqr(thresh1, base);
-  if (cols > 0) cgs();
-  cholqr(0.0, base + (uint64_t)n * q);
+  // ---- fast path: two rounds of block Gram-Schmidt with the Pythagorean inner product (BCGS-PIP2).
+  // One grid reduction per round yields C = Q^T W and G = W^T W together; the Gram of the projected
+  // block is G' = G - C^T C, factorised redundantly by every CTA (no broadcast barrier), and
+  // W <- (W - Q C) R^-1 in one sweep: 4 grid barriers instead of 12.  G' is formed by subtraction, so
+  // a round is only taken when (kept share of each column's squared norm) x (smallest equilibrated
+  // pivot) >= 1e-12 (the round's error ~ eps / that <= 1e-4, which the second round removes);
+  // otherwise -- near-breakdown blocks, refills -- the five-phase sequence below runs from the same W.
+  double* Gs = chol_sm + (2 * q * (q + 1) + 2 * q + 1) + 64;  // q x q: G, then G'
+  double* Rinv_s = Gs + q * q;                                // q x q
+  double* Rrel_s = Rinv_s + q * q;                            // q x q (unused factor output)
+  int* mask_s = reinterpret_cast<int*>(Rrel_s + q * q);       // q
+  auto pip_round = [&](double thresh) -> bool {
+    const int pq = cols * q, qq = q * q, tot = pq + qq;
+    const int na4 = (cols + 3) / 4, nq4 = (q + 3) / 4;
+    double* mypart = part + (int64_t)blockIdx.x * tot;
+    for (int item = t; item < (na4 + nq4) * q; item += kCT) {
+      const int grp4 = item / q, c = item - grp4 * q;
+      const bool isq = grp4 < na4;
+      const int a0 = (isq ? grp4 : grp4 - na4) * 4;
+      const int lim = isq ? cols : q;
+      const double* X = isq ? Qs : Ws;
+      const int ldx = isq ? cols : q;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int r = 0; r < rows; ++r) {
+        const double wv = Ws[r * q + c];
+        const double* xr = X + r * ldx + a0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (a0 + u < lim) acc[u] = fma(xr[u], wv, acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (a0 + u < lim) mypart[(isq ? 0 : pq) + (a0 + u) * q + c] = acc[u];
+    }
+    phase_mark(pm++);
+    grid.sync();
+    grid_reduce_outputs(tot, [&](int o) { return PartRef{part, tot, o}; },
+                        [&](int o, double v) {
+                          if (o < pq) Cws[o] = v;
+                          else Gws[o - pq] = v;
+                        });
+    grid.sync();
+    phase_mark(pm++);
+    for (int o = t; o < pq; o += kCT) Cs[o] = __ldcg(Cws + o);
+    for (int o = t; o < qq; o += kCT) Gs[o] = __ldcg(Gws + o);
+    __syncthreads();
+    // G' = G - C^T C (upper triangle; the lower is mirrored by block_cholesky) and the kept share of
+    // every column's squared norm
+    double keep_min = 1.0;
+    for (int o = t; o < qq; o += kCT) {
+      const int i = o / q, j = o - i * q;
+      if (i <= j) {
+        double s0 = 0.0, s1 = 0.0;
+        int k = 0;
+        for (; k + 1 < cols; k += 2) {
+          s0 = fma(Cs[k * q + i], Cs[k * q + j], s0);
+          s1 = fma(Cs[(k + 1) * q + i], Cs[(k + 1) * q + j], s1);
+        }
+        if (k < cols) s0 = fma(Cs[k * q + i], Cs[k * q + j], s0);
+        const double g = Gs[o];
+        const double gp = g - (s0 + s1);
+        if (i == j) keep_min = (g > 0.0 && gp > thresh * thresh) ? fmin(keep_min, gp / g) : 0.0;
+        Rrel_s[o] = gp;
+      }
+    }
+    __syncthreads();
+    for (int o = t; o < qq; o += kCT) {
+      const int i = o / q, j = o - i * q;
+      if (i <= j) Gs[o] = Rrel_s[o];
+    }
+    // CTA-wide minimum of keep_min (bad[0..] as scratch is not enough: use the warp partials in Rrel_s tail)
+    keep_min = warp_min_f64(keep_min);
+    __syncthreads();
+    if ((t & 31) == 0) Rinv_s[t >> 5] = keep_min;
+    __syncthreads();
+    double km = 1.0;
+    for (int wv = 0; wv < kCT / 32; ++wv) km = fmin(km, Rinv_s[wv]);
+    __syncthreads();
+    if (!(km >= 1e-11)) return false;  // uniform: every CTA reduced the same G and C
+    double pmin = 1.0;
+    block_cholesky(Gs, q, thresh, chol_sm, Rrel_s, Rinv_s, mask_s, nullptr, nullptr, &pmin);
+    __syncthreads();
+    bool okc = km * pmin >= 1e-12;  // error of the round ~ eps / (kept share x smallest pivot) <= 1e-4
+    for (int c = 0; c < q; ++c) okc = okc && !mask_s[c];
+    if (!okc) return false;  // uniform
+    // W <- (W - Q C) R^-1: the projection into W2, then the triangular solve back into Ws
+    const int nc4 = (q + 3) / 4;
+    for (int item = t; item < rows * nc4; item += kCT) {
+      const int r = item / nc4, c0 = (item - r * nc4) * 4;
+      const double* qr = Qs + r * cols;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < cols; ++k) {
+        const double qk = qr[k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + u < q) acc[u] = fma(qk, Cs[k * q + c0 + u], acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c0 + u < q) W2[r * q + c0 + u] = Ws[r * q + c0 + u] - acc[u];
+    }
+    __syncthreads();
+    for (int idx = t; idx < rows * q; idx += kCT) {
+      const int r = idx / q, c = idx - r * q;
+      double v = 0.0;
+      for (int k = 0; k <= c; ++k) v = fma(W2[r * q + k], Rinv_s[k * q + c], v);
+      Ws[idx] = v;
+    }
+    __syncthreads();
+    phase_mark(pm++);
+    return true;
+  };
+  bool done = false;
+  if (pip && cols > 0 && cgs_rounds == 2) {
+    if (pip_round(thresh1)) {
+      done = pip_round(0.0);
+    } else {
+      // the round's C = Q^T W is the first CGS projection: apply it (Cs holds it), no second reduction
+      const int nc4 = (q + 3) / 4;
+      for (int item = t; item < rows * nc4; item += kCT) {
+        const int r = item / nc4, c0 = (item - r * nc4) * 4;
+        const double* qr = Qs + r * cols;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = 0; k < cols; ++k) {
+          const double qk = qr[k];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c0 + u < q) acc[u] = fma(qk, Cs[k * q + c0 + u], acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c0 + u < q) Ws[r * q + c0 + u] -= acc[u];
+      }
+      __syncthreads();
+    }
+    if (!done) cgs_rounds = 1;  // W is projected once: one more CGS before the CholQR rounds
+  }
+  if (!done) {
+    for (int round = 0; round < cgs_rounds && cols > 0; ++round) cgs();
+    cholqr(thresh1, base);
+    if (cols > 0) cgs();
+    cholqr(0.0, base + (uint64_t)n * q);
+  }
   for (int idx = t; idx < rows * q; idx += kCT) {
     const int r = idx / q, c = idx - r * q;
     W[(r0 + r) * ldw + c] = Ws[idx];
@@ -731,15 +879,17 @@ bool coop_orth(const Launch& L, int64_t n, const double* Q, int64_t ldq, int col
   const int G = coop_grid(n, sm_count);
   const int R = (int)((n + G - 1) / G);
   const size_t chol_smem = (size_t)(2 * q * (q + 1) + 2 * q + 1) + 64;
-  const size_t smem =
-      ((size_t)R * cols + 2 * (size_t)R * q + (size_t)std::max(cols * q, q * q) + 32 + chol_smem) * sizeof(double);
+  const size_t pip_smem = 3 * (size_t)q * q + 64;  // G / G', R^-1, factor scratch, mask of the PIP rounds
+  const size_t smem = ((size_t)R * cols + 2 * (size_t)R * q + (size_t)std::max(cols * q, q * q) + 32 + chol_smem +
+                       pip_smem) * sizeof(double);
   if (off || q > 32 || q < 1 || smem > 200 * 1024) return false;
+  static const int pip = getenv("MEGB200_NO_ORTH_PIP") == nullptr;  // diagnostics: the five-phase sequence only
   static char a = 0;
   if (first_on_device(&a)) {
     raise_smem(k_coop_orth, 200 * 1024);
   }
   coop_launch(L, k_coop_orth, G, smem, n, Q, ldq, cols, W, ldw, q, thresh1, key, base, part, Cws, Gws, Rinv, mask,
-              Rrel, cgs_rounds);
+              Rrel, cgs_rounds, pip);
   return true;
 }
 
@@ -966,12 +1116,14 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_rr(const double* __restrict__ H
 void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,
              const double* Q, const double* AQ, int64_t ldq, int rq, int nreq, double* T, int64_t ldt, double* resid,
              double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi, double* V2, int64_t ld2,
-             int r2, int nvec) {
+             int r2, int nvec, bool presolved) {
   if (!V2) r2 = 0;
   if (nreq > 64 || rq > 64) throw Error(MEGB200_ERR_PARAM, "rr: at most 64 Ritz vectors");
   const int G = coop_grid(n, sm_count);
   const bool fused = m <= 48;
-  if (!fused) rr_wide(L, H, ldh, m, theta, S, info, nvec > 0 ? std::max(nvec, rq) : 0);
+  // presolved: the caller already ran the wide solver (on its side stream, overlapped)
+  if (presolved && fused) throw Error(MEGB200_ERR_PARAM, "rr: presolved needs the wide solver (m > 48)");
+  if (!fused && !presolved) rr_wide(L, H, ldh, m, theta, S, info, nvec > 0 ? std::max(nvec, rq) : 0);
   const size_t smem = std::max(fused ? (size_t)jacobi_smem_doubles(m) : (size_t)0,
                                (size_t)(m * rq + 2 * kRC * m + kCT + kRC * 2 * std::max(gr, 1))) * sizeof(double);
   double* info_arg = fused ? info : nullptr;

@@ -79,8 +79,15 @@ CUtensorMap make_map(const void* base, CUtensorMapDataType dt, size_t es, int64_
 bool umma_pass_supported(int64_t n, int b, int64_t ldm, const void* M);
 int dense_pass_umma(const Launch& L, const float* M, int64_t ldm, int64_t n, const double* U, int64_t ldu, int b,
                     double* part, int64_t part_cap_slices, int sm_count, float* uscratch);
-void csr_apply_partial(const Launch& L, const int32_t* rowptr, const int32_t* col, const double* val, int64_t n,
-                       const double* U, int64_t ldu, int b, double* part);
+// Sampled-entry (CSR) pass.  With a panel-pointer scratch (pp: n x (P + 1) int32, P <= 16 column panels)
+// and enough partial slices the panel-tiled kernel runs: CTA (row group, column panel) stages the
+// panel's rows of U in shared memory and gathers from there; slice p holds panel p's contribution.
+// pp_valid: the scratch already holds this pattern's panel pointers (set on return).  Returns the
+// number of slices written (1 for the warp-per-row kernel that gathers U rows through L2).
+int csr_apply_partial(const Launch& L, const int32_t* rowptr, const int32_t* col, const double* val, int64_t n,
+                      const double* U, int64_t ldu, int b, double* part, int64_t part_cap_slices = 1,
+                      int32_t* pp = nullptr, bool* pp_valid = nullptr, int sm_count = 148);
+constexpr int kCsrMaxPanels = 16;
 
 // C (p x q, ld ldc) = diag(rowscale) * X^T Y  (+ beta C if accumulate).  rowscale may be null.
 void tn(const Launch& Lc, int64_t n, const double* X, int64_t ldx, int p, const double* Y, int64_t ldy, int q,
@@ -116,6 +123,10 @@ void frob_direct(const Launch& L, const void* M, int dtype, int64_t ld, int64_t 
 void set_identity(const Launch& L, int64_t n, double* Q, int64_t ldq);
 // H[0:cap, 0:cap] = 0 except H[j][j] = theta[j] for j < k
 void set_diag(const Launch& L, double* H, int cap, int k, const double* theta);
+// Thick restart of H when the next block's column block H[0:m+q, m:m+q] is already there (the overlapped
+// Rayleigh-Ritz of top_eigs): H <- [diag(theta[0:keep]), S[:, 0:keep]^T H[0:m, m:m+q]; ., H[m:m+q, m:m+q]]
+// (upper triangle), everything else zero.  S is m x m row-major (column k = Ritz vector k).
+void restart_h(const Launch& L, double* H, int cap, const double* S, int m, int keep, int q, const double* theta);
 
 // cooperative tall-skinny kernels (megb200_coop.cu): one launch each
 void coop_tn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const double* Y, int64_t ldy, int q,
@@ -149,7 +160,7 @@ void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, 
 void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,
              const double* Q, const double* AQ, int64_t ldq, int rq, int nreq, double* T, int64_t ldt, double* resid,
              double* part, int sm_count, int gr, double* Gout, double eps_next, double* epi, double* V2 = nullptr,
-             int64_t ld2 = 0, int r2 = 0, int nvec = 0);
+             int64_t ld2 = 0, int r2 = 0, int nvec = 0, bool presolved = false);
 
 // First pass of a solve fused with its finish and Rayleigh-Ritz (megb200_step.cu):
 // W = scale * sum_s part[s] + L E + alpha U, H = U^T W, Jacobi RR, Ritz block T,

@@ -1298,6 +1298,165 @@ __global__ void __launch_bounds__(256, MINB) k_csr_apply(const int32_t* __restri
   }
 }
 
+// ---------------------------------------------------------------------------
+// Panel-tiled CSR pass (cfg3): the n columns are cut into P panels of pw columns whose U rows
+// (pw x b doubles, <= ~200 KiB) fit shared memory.  CTA (row group g, panel p) stages panel p's rows
+// of U once, then a warp per row walks that row's nonzeros inside the panel (pp: per-row panel
+// pointers, columns are sorted within a row): the (column offset, value) pairs of 32 nonzeros are
+// staged per warp in shared memory, each half-warp takes one nonzero per step (lane hl: block
+// columns hl and hl + 16) with a broadcast read of the pair and a conflict-free read of the U row.
+// Slice p of `out` (S = P slices, summed in order by the finish) holds panel p's contribution.
+__global__ void __launch_bounds__(256) k_csr_panel_ptr(const int32_t* __restrict__ rowptr,
+                                                       const int32_t* __restrict__ col, int64_t n, int P, int pw,
+                                                       int32_t* __restrict__ pp) {
+  const int64_t idx = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (idx >= n * (P + 1)) return;
+  const int64_t row = idx / (P + 1);
+  const int p = (int)(idx - row * (P + 1));
+  int lo = rowptr[row], hi = rowptr[row + 1];
+  if (p == 0) {
+    hi = lo;
+  } else if (p < P) {
+    const int target = p * pw;  // first nonzero with column >= target
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(col + mid) < target) lo = mid + 1;
+      else hi = mid;
+    }
+  } else {
+    lo = hi;
+  }
+  pp[idx] = p == 0 ? hi : lo;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(32 * NW, 1) k_csr_apply_panel(const int32_t* __restrict__ rowptr,
+                                                              const int32_t* __restrict__ col,
+                                                              const double* __restrict__ val, int64_t n,
+                                                              const double* __restrict__ U, int64_t ldu, int b,
+                                                              double* __restrict__ out,
+                                                              const int32_t* __restrict__ pp, int P, int pw,
+                                                              int rpg) {
+  extern __shared__ __align__(16) double csm[];
+  struct Meta {
+    int off, pad;
+    double g;
+  };
+  constexpr int KB = 3;  // batches of 32 nonzeros prefetched per row (a longer panel row loops on)
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, half = lane >> 4, hl = lane & 15;
+  const int p = blockIdx.x % P, grp = blockIdx.x / P;
+  const int64_t c0 = (int64_t)p * pw;
+  const int prow = (int)min((int64_t)pw, n - c0);
+  Meta* meta = reinterpret_cast<Meta*>(csm) + warp * 32;
+  double* Us = csm + (size_t)NW * 32 * 2;
+  // stage the panel's rows of U: 16-byte asynchronous copies when the block is aligned (all in flight)
+  if ((b & 1) == 0 && (ldu & 1) == 0 && (reinterpret_cast<uintptr_t>(U) & 15) == 0) {
+    const int hb = b >> 1, total = prow * hb;
+    for (int idx = t; idx < total; idx += 32 * NW) {
+      const int r = idx / hb, c = 2 * (idx - r * hb);
+      cp_async16(Us + r * b + c, U + (c0 + r) * ldu + c);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  } else {
+    const int total = prow * b;
+    for (int idx = t; idx < total; idx += 32 * NW) {
+      const int r = idx / b, c = idx - r * b;
+      Us[idx] = __ldg(U + (c0 + r) * ldu + c);
+    }
+  }
+  const bool ok0 = hl < b, ok1 = hl + 16 < b;
+  const int64_t rbeg = (int64_t)grp * rpg, rend = min(n, (int64_t)(grp + 1) * rpg);
+  const int nrw = rbeg + warp < rend ? (int)((rend - rbeg - warp + NW - 1) / NW) : 0;  // rows of this warp
+  double* outp = out + (int64_t)p * n * b;
+  auto load_row = [&](int e0, int e1, int (&jj)[KB], double (&gg)[KB]) {
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const int e = e0 + lane + 32 * k;
+      const bool in = e < e1;
+      jj[k] = in ? (__ldg(col + e) - (int)c0) * b : 0;
+      gg[k] = in ? __ldg(val + e) : 0.0;
+    }
+  };
+  // panel pointers of up to 32 of the warp's rows at a time (lane i: the chunk's i-th row), then per
+  // row the first KB batches of (column, value) are prefetched while the previous row is multiplied
+  int my_e0 = 0, my_e1 = 0;
+  if (lane < min(nrw, 32)) {
+    const int64_t r = rbeg + warp + (int64_t)NW * lane;
+    my_e0 = __ldg(pp + r * (P + 1) + p);
+    my_e1 = __ldg(pp + r * (P + 1) + p + 1);
+  }
+  int nj[KB];
+  double ng[KB];
+  int ne0 = __shfl_sync(0xffffffffu, my_e0, 0), ne1 = __shfl_sync(0xffffffffu, my_e1, 0);
+  load_row(ne0, ne1, nj, ng);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  for (int i0 = 0; i0 < nrw; i0 += 32) {
+    const int cnt = min(32, nrw - i0);
+    if (i0 > 0) {
+      my_e0 = my_e1 = 0;
+      if (lane < cnt) {
+        const int64_t r = rbeg + warp + (int64_t)NW * (i0 + lane);
+        my_e0 = __ldg(pp + r * (P + 1) + p);
+        my_e1 = __ldg(pp + r * (P + 1) + p + 1);
+      }
+      ne0 = __shfl_sync(0xffffffffu, my_e0, 0);
+      ne1 = __shfl_sync(0xffffffffu, my_e1, 0);
+      load_row(ne0, ne1, nj, ng);
+    }
+    for (int ii = 0; ii < cnt; ++ii) {
+      const int e0 = ne0, e1 = ne1;
+      int cj[KB];
+      double cgv[KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        cj[k] = nj[k];
+        cgv[k] = ng[k];
+      }
+      if (ii + 1 < cnt) {
+        ne0 = __shfl_sync(0xffffffffu, my_e0, ii + 1);
+        ne1 = __shfl_sync(0xffffffffu, my_e1, ii + 1);
+        load_row(ne0, ne1, nj, ng);
+      }
+      const int64_t row = rbeg + warp + (int64_t)NW * (i0 + ii);
+      double a0 = 0.0, a1 = 0.0;
+      auto batch = [&](int off, double g, int left) {
+        Meta m;
+        m.off = off;
+        m.pad = 0;
+        m.g = g;
+        __syncwarp();
+        meta[lane] = m;
+        __syncwarp();
+        const int steps = (min(32, left) + 1) >> 1;
+#pragma unroll 4
+        for (int q = 0; q < steps; ++q) {
+          const Meta mm = meta[2 * q + half];
+          const double* u = Us + mm.off;
+          const double u0 = ok0 ? u[hl] : 0.0;
+          const double u1 = ok1 ? u[hl + 16] : 0.0;
+          a0 = fma(mm.g, u0, a0);
+          a1 = fma(mm.g, u1, a1);
+        }
+      };
+#pragma unroll
+      for (int k = 0; k < KB; ++k)
+        if (e0 + 32 * k < e1) batch(cj[k], cgv[k], e1 - (e0 + 32 * k));
+      for (int base = e0 + 32 * KB; base < e1; base += 32) {  // long panel rows
+        const int e = base + lane;
+        const bool in = e < e1;
+        batch(in ? (__ldg(col + e) - (int)c0) * b : 0, in ? __ldg(val + e) : 0.0, e1 - base);
+      }
+      a0 += __shfl_xor_sync(0xffffffffu, a0, 16);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 16);
+      if (half == 0) {
+        if (ok0) outp[row * b + hl] = a0;
+        if (ok1) outp[row * b + hl + 16] = a1;
+      }
+    }
+  }
+}
+
 // ===========================================================================
 // Tall-skinny X^T Y partials: each CTA reduces a contiguous row range into
 // one p x q partial; k_reduce_partials sums the partials in CTA order.
@@ -1599,6 +1758,37 @@ __global__ void k_set_diag(double* __restrict__ H, int cap, int k, const double*
   if (idx >= cap * cap) return;
   const int i = idx / cap, j = idx - i * cap;
   H[idx] = (i == j && i < k) ? theta[i] : 0.0;
+}
+
+// one CTA: the new block's column block B = H[0:m+q, m:m+q] is staged in shared memory, H is
+// cleared, then diag(theta), S_keep^T B[0:m] and the block's own diagonal block are written
+__global__ void __launch_bounds__(256) k_restart_h(double* __restrict__ H, int cap, const double* __restrict__ S, int m,
+                                                   int keep, int q, const double* __restrict__ theta) {
+  extern __shared__ double bs[];  // (m + q) x q
+  const int t = threadIdx.x;
+  for (int idx = t; idx < (m + q) * q; idx += 256) {
+    const int i = idx / q, j = idx - i * q;
+    bs[idx] = H[(int64_t)i * cap + m + j];
+  }
+  __syncthreads();
+  for (int idx = t; idx < cap * cap; idx += 256) H[idx] = 0.0;
+  __syncthreads();
+  for (int i = t; i < keep; i += 256) H[(int64_t)i * cap + i] = theta[i];
+  for (int idx = t; idx < keep * q; idx += 256) {
+    const int i = idx / q, j = idx - i * q;
+    double a0 = 0.0, a1 = 0.0;
+    int k = 0;
+    for (; k + 1 < m; k += 2) {
+      a0 = fma(S[(int64_t)k * m + i], bs[k * q + j], a0);
+      a1 = fma(S[(int64_t)(k + 1) * m + i], bs[(k + 1) * q + j], a1);
+    }
+    if (k < m) a0 = fma(S[(int64_t)k * m + i], bs[k * q + j], a0);
+    H[(int64_t)i * cap + keep + j] = a0 + a1;
+  }
+  for (int idx = t; idx < q * q; idx += 256) {
+    const int i = idx / q, j = idx - i * q;
+    if (i <= j) H[(int64_t)(keep + i) * cap + keep + j] = bs[(m + i) * q + j];
+  }
 }
 
 __global__ void k_reduce_sum(const double* __restrict__ part, int slots, int width, double* __restrict__ out) {
@@ -1987,14 +2177,47 @@ int dense_apply_partial(const Launch& L, const void* M, int dtype, int64_t ldm, 
   return S;
 }
 
-void csr_apply_partial(const Launch& L, const int32_t* rowptr, const int32_t* col, const double* val, int64_t n,
-                       const double* U, int64_t ldu, int b, double* part) {
+// panel geometry of the tiled CSR pass: the widest panel whose U rows (pw x b doubles) fit ~200 KiB
+constexpr size_t kCsrPanelSmem = 200 * 1024;
+constexpr int kCsrPanelWarps = 16;
+
+int csr_apply_partial(const Launch& L, const int32_t* rowptr, const int32_t* col, const double* val, int64_t n,
+                      const double* U, int64_t ldu, int b, double* part, int64_t part_cap_slices, int32_t* pp,
+                      bool* pp_valid, int sm_count) {
   if (b > 32) throw Error(MEGB200_ERR_PARAM, "CSR pass supports b <= 32");
+  static const bool no_panel = getenv("MEGB200_NO_CSR_PANEL") != nullptr;  // diagnostics: the L2-gather kernel
+  const size_t meta = (size_t)kCsrPanelWarps * 32 * 16;
+  const int64_t cap_rows = (int64_t)((kCsrPanelSmem - meta) / ((size_t)b * 8));
+  const int P = (int)cdiv(n, cap_rows);
+  if (!no_panel && pp && pp_valid && P <= kCsrMaxPanels && P <= part_cap_slices && n >= 1024) {
+    const int pw = (int)cdiv(n, P);
+    if (!*pp_valid) {
+      k_csr_panel_ptr<<<cdiv(n * (P + 1), 256), 256, 0, L.stream>>>(rowptr, col, n, P, pw, pp);
+      MEG_LAUNCHED();
+      ++*L.counter;
+      *pp_valid = true;
+    }
+    // row groups: the grid covers the SMs about once (one CTA per SM: the panel takes the shared memory)
+    const int RG = std::max(1, sm_count / P);
+    const int rpg = (int)cdiv(n, RG);
+    const int rgs = (int)cdiv(n, rpg);
+    const size_t smem = (size_t)pw * b * 8 + meta;
+    static char attr = 0;
+    if (first_on_device(&attr))
+      MEG_CUDA(cudaFuncSetAttribute(k_csr_apply_panel<kCsrPanelWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kCsrPanelSmem));
+    k_csr_apply_panel<kCsrPanelWarps><<<P * rgs, 32 * kCsrPanelWarps, smem, L.stream>>>(rowptr, col, val, n, U, ldu, b,
+                                                                                       part, pp, P, pw, rpg);
+    MEG_LAUNCHED();
+    ++*L.counter;
+    return P;
+  }
   // four row loads in flight per lane at four CTAs per SM (cfg3 pass+finish 107 us) beat eight at
   // three CTAs (112 us) and sixteen at one (139 us): the gathers need warps more than depth
   k_csr_apply<4, 4><<<cdiv(n, 8), 256, 0, L.stream>>>(rowptr, col, val, n, U, ldu, b, part);
   MEG_LAUNCHED();
   ++*L.counter;
+  return 1;
 }
 
 void tn(const Launch& L, int64_t n, const double* X, int64_t ldx, int p, const double* Y, int64_t ldy, int q,
@@ -2187,6 +2410,14 @@ void set_identity(const Launch& L, int64_t n, double* Q, int64_t ldq) {
 
 void set_diag(const Launch& L, double* H, int cap, int k, const double* theta) {
   k_set_diag<<<cdiv((int64_t)cap * cap, 256), 256, 0, L.stream>>>(H, cap, k, theta);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void restart_h(const Launch& L, double* H, int cap, const double* S, int m, int keep, int q, const double* theta) {
+  const size_t smem = (size_t)(m + q) * q * sizeof(double);
+  if (keep + q > m || m + q > cap || smem > 48 * 1024) throw Error(MEGB200_ERR_PARAM, "restart_h: shape out of range");
+  k_restart_h<<<1, 256, smem, L.stream>>>(H, cap, S, m, keep, q, theta);
   MEG_LAUNCHED();
   ++*L.counter;
 }

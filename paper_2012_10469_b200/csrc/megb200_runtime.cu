@@ -53,8 +53,19 @@ struct megb200_solver {
   int max_block = 0, max_basis = 0, cap = 0;
   int64_t max_lowrank = 0, max_nnz = 0;
   int sm_count = 148;
+  // grid limit of the multi-pass solver's cooperative kernels: sm_count, or sm_count - 1 while a solve
+  // overlaps its wide Rayleigh-Ritz (one CTA on the side stream) with the next block's work
+  int coop_sm = 148;
   cudaStream_t stream = nullptr;
+  // side stream of the overlapped wide Rayleigh-Ritz (top_eigs), forked / joined with events
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t launches = 0;
+  // panel pointers of the tiled CSR pass (n x 17 int32, allocated on first use) and their key
+  int32_t* csr_pp = nullptr;
+  bool csr_pp_valid = false, in_solve = false;
+  const int32_t *csr_pp_rowptr = nullptr, *csr_pp_col = nullptr;
+  int csr_pp_b = 0;
 
   char* arena = nullptr;
   int64_t arena_bytes = 0;
@@ -309,8 +320,21 @@ int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu
     S = dense_apply_partial(L, op.dense, op.dtype, op.ld, n, U, ldu, k, s->part, s->part_slices, s->sm_count,
                             reinterpret_cast<float*>(s->uT));
   } else if (op.kind == MEGB200_OP_CSR && op.scale != 0.0) {
-    csr_apply_partial(L, op.rowptr, op.col, op.val, n, U, ldu, k, s->part);
-    S = 1;
+    // panel pointers are computed once per solve (the pattern cannot change inside top_eigs), per
+    // pass outside one
+    const bool same = s->in_solve && s->csr_pp_rowptr == op.rowptr && s->csr_pp_col == op.col && s->csr_pp_b == k;
+    if (!same) s->csr_pp_valid = false;
+    if (!s->csr_pp) {
+      if (cudaMalloc(&s->csr_pp, (size_t)n * (kCsrMaxPanels + 1) * sizeof(int32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        s->csr_pp = nullptr;
+      }
+    }
+    S = csr_apply_partial(L, op.rowptr, op.col, op.val, n, U, ldu, k, s->part, s->part_slices, s->csr_pp,
+                          &s->csr_pp_valid, s->sm_count);
+    s->csr_pp_rowptr = op.rowptr;
+    s->csr_pp_col = op.col;
+    s->csr_pp_b = k;
   }
   prof_end(s, ev0, op, k);
   return S;
@@ -322,7 +346,7 @@ void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, 
   const int S = pass_launch(s, op, U, ldu, k);
   if (op.lc.lam == s->dlam) s->flush_dlam();
   coop_finish(L, s->n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
-              s->sm_count, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap, op.lc, op.Eg, op.ldg);
+              s->coop_sm, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap, op.lc, op.Eg, op.ldg);
 }
 
 // columns k > 64 are applied in chunks (re-streams the operand; not used by the configs)
@@ -377,18 +401,18 @@ void orthonormalize(megb200_solver* s, double* W, int64_t ldw, int q, int cols, 
   Launch L = s->launch();
   const int64_t n = s->n;
   if (!want_relation && coop_orth(L, n, s->Q, s->ldq, cols, W, ldw, q, 1e-13 * scale, key, refill_ctr, s->red, s->C2,
-                                  s->G, s->Rinv, s->mask, s->Rtmp, s->sm_count, cgs_rounds)) {
+                                  s->G, s->Rinv, s->mask, s->Rtmp, s->coop_sm, cgs_rounds)) {
     refill_ctr += 2 * (uint64_t)n * q;
     return;
   }
   for (int round = 0; round < cgs_rounds && cols > 0; ++round)
-    coop_cgs(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, s->red, s->sm_count);
+    coop_cgs(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, s->red, s->coop_sm);
   coop_cholqr(L, n, W, ldw, W, ldw, q, 1e-13 * scale, s->G, s->R1, s->Rinv, s->mask, nullptr, nullptr, key,
-              refill_ctr, s->red, s->sm_count);
+              refill_ctr, s->red, s->coop_sm);
   refill_ctr += (uint64_t)n * q;
-  if (cols > 0) coop_cgs(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, s->red, s->sm_count);
+  if (cols > 0) coop_cgs(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, s->red, s->coop_sm);
   coop_cholqr(L, n, W, ldw, W, ldw, q, 0.0, s->G, s->R2, s->Rinv, s->mask, want_relation ? s->R1 : nullptr,
-              want_relation ? s->Rn : nullptr, key, refill_ctr, s->red, s->sm_count);
+              want_relation ? s->Rn : nullptr, key, refill_ctr, s->red, s->coop_sm);
   refill_ctr += (uint64_t)n * q;
 }
 
@@ -525,7 +549,7 @@ void block_pass(megb200_solver* s, const OpDev& op, int cols, int cur) {
   } else {
     apply_op_wide(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq);
     coop_tn(L, s->n, s->Q, s->ldq, cols + cur, s->AQ + cols, s->ldq, cur, s->H + cols, s->cap, nullptr, 1.0, s->red,
-            s->sm_count);
+            s->coop_sm);
   }
 }
 
@@ -534,7 +558,8 @@ void block_pass(megb200_solver* s, const OpDev& op, int cols, int cur) {
 // the Ritz-block Gram) in one launch, then one asynchronous read-back of the
 // pack [theta | resid | epilogue | Gram] into dst (pinned).  Returns the Gram order.
 int rr_readback(megb200_solver* s, int newcols, int nreq, int bw, const EpiSpec* epi, double* dst,
-                double* tdst = nullptr, int64_t ldt = 0, double* v2 = nullptr, int64_t ld2 = 0, int r2 = 0) {
+                double* tdst = nullptr, int64_t ldt = 0, double* v2 = nullptr, int64_t ld2 = 0, int r2 = 0,
+                bool presolved = false) {
   Launch L = s->launch();
   const int rq = std::min(newcols, std::max(nreq, bw));
   const int gr = epi ? rq : 0;  // Gram of the whole Ritz block (V_next = its first r columns)
@@ -545,8 +570,8 @@ int rr_readback(megb200_solver* s, int newcols, int nreq, int bw, const EpiSpec*
   static const bool twice = getenv("MEGB200_DEBUG_RR_TWICE") != nullptr;  // diagnostics: warm i-cache timing
   for (int rep = 0; rep < (twice ? 2 : 1); ++rep)
     coop_rr(L, s->H, s->cap, newcols, s->theta, s->S, s->info, s->n, s->Q, s->AQ, s->ldq, rq, nreq, tdst, ldt,
-            s->resid, s->red, s->sm_count, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
-            epi ? s->pack + s->pack_epi : nullptr, v2, ld2, r2, s->rr_nvec);
+            s->resid, s->red, s->coop_sm, gr, s->pack + s->pack_gram, epi ? epi->eps_next : 0.0,
+            epi ? s->pack + s->pack_epi : nullptr, v2, ld2, r2, s->rr_nvec, presolved);
   s->d2h(dst, s->pack, s->pack_gram + (int64_t)gr * gr);
   return gr;
 }
@@ -732,6 +757,23 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
     megb200_solver* s;
     ~NvecReset() { s->rr_nvec = 0; }
   } nvec_reset{s};
+  // Overlapped restarts: at a full basis the wide Rayleigh-Ritz (one CTA, ~0.5 ms) runs on the side
+  // stream while the solver stream orthonormalises the next Krylov block against the full basis and
+  // runs its operator pass (neither depends on the Ritz pairs); the restart then carries that block's
+  // image and its column of H over (restart_h).  Same subspaces as the serial order.  The cooperative
+  // kernels of such a solve leave one SM to the Rayleigh-Ritz CTA.
+  static const bool no_overlap = getenv("MEGB200_NO_RR_OVERLAP") != nullptr;  // diagnostics
+  const bool overlap = !no_overlap && s->side && !sh.identity && !sh.exhaust && mmax > 48 && s->sm_count > 8;
+  struct CoopSmReset {
+    megb200_solver* s;
+    ~CoopSmReset() {
+      s->coop_sm = s->sm_count;
+      s->in_solve = false;
+    }
+  } coop_reset{s};
+  s->in_solve = true;  // the operator is fixed for the solve: per-pattern scratch (CSR panel pointers) is reused
+  s->csr_pp_valid = false;
+  if (overlap) s->coop_sm = s->sm_count - 1;
   const double tol = P.tol;
   const uint64_t key_start = stream_key(P.seed, kStreamStart);
   const uint64_t key_refill = stream_key(P.seed, kStreamRefill);
@@ -769,13 +811,17 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   std::vector<double> best(nreq, INFINITY);
   int cols = 0, cur = bw;
   double scale = 1.0;
+  bool pass_done = false;  // the current block's pass already ran (overlapped with the last Rayleigh-Ritz)
   for (;;) {
     // operator pass on the current block, then its column of H = Q^T A Q; the first pass
     // of a solve runs fused with its Rayleigh-Ritz (one launch after the pass)
     const bool fuse = !sh.identity && cols == 0 && cur == bw && fused_ok(s, op, bw, nreq);
-    if (!fuse) block_pass(s, op, cols, cur);
-    run.passes++;
-    s->mark("pass+finish");
+    if (!pass_done) {
+      if (!fuse) block_pass(s, op, cols, cur);
+      run.passes++;
+      s->mark("pass+finish");
+    }
+    pass_done = false;
     const int newcols = cols + cur;
     const int nxt = (int)std::min<int64_t>(bw, n - newcols);
     const bool full = (nxt <= 0) || (newcols + nxt > mmax);
@@ -790,9 +836,28 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       double* v2 = vec_out ? vec_out : (epi ? epi->v_next : nullptr);
       const int64_t ld2 = vec_out ? ld_vec : (epi ? epi->ld_next : 0);
       const int r2 = vec_out ? nreq : (epi ? epi->r : 0);
+      // overlapped restart: the wide solve on the side stream, the next block's orthonormalisation
+      // and pass on the solver stream, joined before the Ritz block / residual launch
+      // (from the second full basis of a solve on: a solve that converges at its first one -- cfg4's
+      // six-pass steps -- would only pay for the speculation)
+      const bool spec = overlap && !fuse && full && cols > 0 && run.restarts >= 1 && nxt == cur && nxt > 0 &&
+                        newcols > 48 && run.passes < max_passes && newcols + nxt <= s->cap && keep + nxt <= newcols;
+      if (spec) {
+        MEG_CUDA(cudaEventRecord(s->ev_fork, s->stream));
+        MEG_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+        Launch Ls{s->side, &s->launches};
+        const int rq_ = std::min(newcols, std::max(nreq, bw));
+        rr_wide(Ls, s->H, s->cap, newcols, s->theta, s->S, s->info, s->rr_nvec > 0 ? std::max(s->rr_nvec, rq_) : 0);
+        MEG_CUDA(cudaEventRecord(s->ev_join, s->side));
+        copy_block(L, n, cur, s->AQ + cols, s->ldq, s->Q + newcols, s->ldq);
+        orthonormalize(s, s->Q + newcols, s->ldq, nxt, newcols, scale, key_refill, refill_ctr, false);
+        block_pass(s, op, newcols, nxt);
+        s->mark("spec orth+pass");
+        MEG_CUDA(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
+      }
       const int gr = fuse ? fused_pass(s, op, deferred_warm ? P.warm : s->Q, deferred_warm ? P.ld_warm : s->ldq, bw,
                                        nreq, epi, ritz_out, ld_ritz, v2, ld2, r2, pk)
-                          : rr_readback(s, newcols, nreq, bw, epi, pk, ritz_out, ld_ritz, v2, ld2, r2);
+                          : rr_readback(s, newcols, nreq, bw, epi, pk, ritz_out, ld_ritz, v2, ld2, r2, spec);
       const int rq = std::min(newcols, std::max(nreq, bw));
       // host-buffer step: V_next travels back with the pack (one wait when this RR converges)
       if (epi && epi->v_host && epi->v_next && epi->ld_next == epi->r && epi->ld_host == epi->r)
@@ -850,6 +915,24 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
         return run;
       }
       if (run.passes >= max_passes) break;
+      if (spec) {
+        // not converged: the speculative pass is the next block's pass.  Thick restart keeping the
+        // leading `keep` Ritz pairs, the new block (orthogonal to all of Q) and its image behind them
+        run.passes++;
+        nn(L, n, s->Q, s->ldq, newcols, s->S, newcols, keep, 1.0, 0.0, s->T, s->ldq);
+        copy_block(L, n, keep, s->T, s->ldq, s->Q, s->ldq);
+        nn(L, n, s->AQ, s->ldq, newcols, s->S, newcols, keep, 1.0, 0.0, s->T, s->ldq);
+        copy_block(L, n, keep, s->T, s->ldq, s->AQ, s->ldq);
+        copy_block(L, n, nxt, s->Q + newcols, s->ldq, s->Q + keep, s->ldq);
+        copy_block(L, n, nxt, s->AQ + newcols, s->ldq, s->AQ + keep, s->ldq);
+        restart_h(L, s->H, s->cap, s->S, newcols, keep, nxt, s->theta);
+        s->mark("restart");
+        run.restarts++;
+        cols = keep;
+        cur = nxt;
+        pass_done = true;
+        continue;
+      }
     }
     if (nxt <= 0) break;
     if (sh.identity) {  // the next identity columns are already in place
@@ -1180,6 +1263,7 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
     s->max_lowrank = std::max<int64_t>(1, max_lowrank);
     s->max_nnz = std::max<int64_t>(0, max_nnz);
     s->sm_count = sm;
+    s->coop_sm = sm;
     s->ldq = s->cap;
     // apply partial slices: up to 16 (wave balancing of the persistent pass), <= 256 MiB
     s->part_slices = std::max<int64_t>(1, std::min<int64_t>(16, (256ll << 20) / (n * (int64_t)max_block * 8)));
@@ -1273,6 +1357,12 @@ int megb200_solver_create(int64_t n, int32_t max_block, int32_t max_basis, int64
       delete s;
       throw Error(MEGB200_ERR_CUDA, "sync flag allocation failed");
     }
+    if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      s->side = nullptr;  // no overlap: the wide Rayleigh-Ritz stays on the solver stream
+    }
     *out = s;
     g_live_solvers.fetch_add(1);
   });
@@ -1282,6 +1372,12 @@ void megb200_solver_destroy(megb200_solver* s) {
   if (!s) return;
   g_live_solvers.fetch_sub(1);
   if (s->stream) cudaStreamSynchronize(s->stream);
+  if (s->side) {
+    cudaStreamSynchronize(s->side);
+    cudaStreamDestroy(s->side);
+  }
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   cudaFree(s->arena);
   if (s->run_buf) cudaFree(s->run_buf);
@@ -1291,6 +1387,7 @@ void megb200_solver_destroy(megb200_solver* s) {
   cudaFreeHost(s->h_up);
   if (s->fsync) cudaFree(s->fsync);
   if (s->qm_part) cudaFree(s->qm_part);
+  if (s->csr_pp) cudaFree(s->csr_pp);
   delete s;
 }
 

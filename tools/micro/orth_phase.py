@@ -10,7 +10,8 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 from paper_2012_10469_b200 import build  # noqa: E402
 
-subprocess.run([build.nvcc(), *build.NVCC_FLAGS, "-DMEG_PHASE_TIMING", "-o", build.TARGET, *build.SOURCES], check=True)
+if not os.environ.get("ORTH_PHASE_SKIP_BUILD"):
+    subprocess.run([build.nvcc(), *build.NVCC_FLAGS, "-DMEG_PHASE_TIMING", "-o", build.TARGET, *build.SOURCES], check=True)
 import numpy as np  # noqa: E402
 import config_profile as cp  # noqa: E402
 import paper_2012_10469_b200 as pb  # noqa: E402
@@ -33,7 +34,14 @@ else:
     w = configs.WORKLOADS[which]
     obj, init = cp.objective_for(w)
     tol = 1e-10 if w.dtype == "f64" else pb.objectives.F32_TOL_FLOOR
-    x = inputs.initial_iterate(w, init, tol=tol)
+    import torch
+    if isinstance(init, torch.Tensor):
+        x = inputs.initial_iterate(w, init, tol=tol)
+    else:
+        top = pb.lanczos_top_r(init, w.r, tol=tol, seed=w.seed, subspace=64, return_device=True)
+        lam = pb.project_simplex(top.eigenvalues, 1.0)
+        lam = np.maximum(lam / lam.sum(), 1e-12)
+        x = pb.warm_start_wrap(top.eigenvectors, lam / lam.sum(), w.eps(0))
     lib = runtime.solver_for(w.n).lib
     lib.megb200_debug_phase_ns.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
     r0 = driver.run(x, obj, 3, eta=w.eta0, eta_decay=w.eta_decay, svd_subspace=w.subspace, block=w.block)
