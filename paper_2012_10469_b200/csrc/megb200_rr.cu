@@ -28,6 +28,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "megb200_internal.h"
 
@@ -75,14 +76,30 @@ __device__ __forceinline__ double fast_rcp(double q) {
   return fma(r, e, r);
 }
 
+// Division-free form: the leading principal minors p_i(x) = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}
+// (the ratios q_i = p_i / p_{i-1} above are negative exactly where consecutive minors change sign).
+// One fused multiply-add on the dependent chain per row instead of a reciprocal and its Newton
+// steps (~4x shorter: the multisection rounds are latency-bound on this chain); both minors are
+// rescaled by a power of two every eight rows, a vanishing minor takes the sign opposite to its
+// predecessor (the pivmin convention: counted as negative).
 __device__ __forceinline__ int sturm_count(const double* d, const double* e2, int m, double x, double pivmin) {
-  double q = d[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  int c = q < 0.0;
+  double pm2 = 1.0, pm1 = d[0] - x;
+  if (fabs(pm1) < pivmin) pm1 = -pivmin;
+  int c = pm1 < 0.0;
+#pragma unroll 8
   for (int i = 1; i < m; ++i) {
-    q = (d[i] - x) - e2[i - 1] * fast_rcp(q);
-    if (fabs(q) < pivmin) q = -pivmin;
-    c += q < 0.0;
+    double pi = fma(d[i] - x, pm1, -(e2[i - 1] * pm2));
+    if (pi == 0.0) pi = -copysign(1e-300, pm1);
+    c += (__double2hiint(pi) ^ __double2hiint(pm1)) < 0;
+    pm2 = pm1;
+    pm1 = pi;
+    if ((i & 7) == 7) {
+      // 2^-exponent(pm1): |pm1| back to [1, 2), pm2 by the same factor
+      const int ex = (__double2hiint(pm1) >> 20) & 0x7ff;
+      const double sc = __hiloint2double((2046 - ex) << 20, 0);
+      pm1 *= sc;
+      pm2 *= sc;
+    }
   }
   return c;
 }
@@ -120,6 +137,38 @@ __device__ __forceinline__ void gemm_t4(const double* A, int ai, int ak, const d
   }
 }
 
+// Multisection on Sturm counts: group k of LPE lanes owns the k-th largest eigenvalue (the group
+// after the top nvec owns the smallest); per round the lanes probe LPE interior points of the
+// group's interval and the interval shrinks to the sub-interval that holds the eigenvalue.
+template <int LPE, int ROUNDS>
+__device__ __forceinline__ void multisect(const double* d, const double* e2, int m, int nvec, int neig, double glo,
+                                          double ghi, double pivmin, double* lam) {
+  const int t = threadIdx.x, lane = t & 31;
+  const int grp = t / LPE, sub = t % LPE;
+  const int ngrp = kRT / LPE;
+  for (int k0 = 0; k0 < neig; k0 += ngrp) {
+    const int kk = k0 + grp;
+    const bool act = kk < neig;
+    const int k = (act && kk == nvec && nvec < m) ? m - 1 : kk;  // the extra group: the smallest
+    const int idx = m - 1 - (act ? k : 0);
+    double lo = glo, hi = ghi;
+    for (int round = 0; round < ROUNDS; ++round) {
+      const double x = lo + (hi - lo) * (double)(sub + 1) / (double)(LPE + 1);
+      const int c = act ? sturm_count(d, e2, m, x, pivmin) : 0;
+      const unsigned below = __ballot_sync(0xffffffffu, c <= idx);
+      const unsigned gmask = LPE == 32 ? 0xffffffffu : ((1u << LPE) - 1u);
+      const unsigned mine = (below >> ((lane / LPE) * LPE)) & gmask;
+      const int ones = __popc(mine);  // counts are monotone in x: lanes 0..ones-1 are below
+      const double step = (hi - lo) / (double)(LPE + 1);
+      const double nlo = ones > 0 ? lo + step * ones : lo;
+      const double nhi = ones < LPE ? lo + step * (ones + 1) : hi;
+      lo = nlo;
+      hi = nhi;
+    }
+    if (act && sub == 0) lam[k] = 0.5 * (lo + hi);
+  }
+}
+
 // Returns true with theta (non-increasing) and S (m x m row-major, column k =
 // eigenvector k) written; false (nothing written) when the verification fails.
 __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, int nvec, double* __restrict__ theta_g,
@@ -151,27 +200,46 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
   double fro2 = 0.0;
   for (int k = 0; k < kNW; ++k) fro2 += wp[k];
   rr_mark(0);
-  // ---- 1. tridiagonalisation
+  // ---- 1. tridiagonalisation, three CTA barriers per column and few warp shuffles (one SM issues
+  //      about one shuffle per cycle, and a float64 warp sum is ten of them: a warp-per-row matvec
+  //      spends ~1000 shuffle slots per column):
+  //      warp 0 forms the Householder vector (one warp sum); eight threads per row form
+  //      p = tau A22 v (three shuffle levels per row group) and the row groups' share of p^T v;
+  //      every thread sums the 32 warp shares for K = tau p^T v / 2; the rank-2 update
+  //      A22 -= v w^T + w v^T (w = p - K v on the fly) runs eight threads per row.
   for (int j = 0; j < m - 2; ++j) {
     const int L = m - j - 1;
     if (w == 0) {
+      double xr[4];
       double s = 0.0;
-      for (int i = lane + 1; i < L; i += 32) {
-        const double x = A[(j + 1 + i) * la + j];
-        s += x * x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        xr[q] = i < L ? A[(j + 1 + i) * la + j] : 0.0;
+        if (i > 0) s = fma(xr[q], xr[q], s);
       }
       s = wsum(s);
-      const double alpha = A[(j + 1) * la + j];
+      const double alpha = __shfl_sync(0xffffffffu, xr[0], 0);
+      // beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta = 1 + |alpha| / ||x||, scale = 1 / (alpha - beta):
+      // one reciprocal square root and one Newton-refined reciprocal instead of a square root and two
+      // divisions (each a ~40-instruction dependent float64 sequence on this serial section)
       double tj = 0.0, beta = alpha, scale = 0.0;
       if (s > 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + s), alpha);
-        tj = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
+        const double n2 = fma(alpha, alpha, s);
+        const double ri = rsqrt(n2);
+        const double nrm = n2 * ri;
+        beta = -copysign(nrm, alpha);
+        tj = fma(fabs(alpha), ri, 1.0);
+        scale = fast_rcp(alpha - beta);
       }
-      for (int i = lane; i < L; i += 32) {
-        const double vi = i == 0 ? 1.0 : A[(j + 1 + i) * la + j] * scale;
-        v[i] = vi;
-        if (i > 0) A[(j + 1 + i) * la + j] = vi;  // reflector kept for the back-transform
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        if (i < L) {
+          const double vi = i == 0 ? 1.0 : xr[q] * scale;
+          v[i] = vi;
+          if (i > 0) A[(j + 1 + i) * la + j] = vi;  // reflector kept for the back-transform
+        }
       }
       if (lane == 0) {
         tau[j] = tj;
@@ -186,30 +254,63 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
       __syncthreads();
       continue;
     }
-    // p = tau A22 v (warp per row), partial p^T v
-    double pv = 0.0;
-    for (int i = w; i < L; i += kNW) {
-      const double* row = A + (j + 1 + i) * la + (j + 1);
-      double s = 0.0;
-      for (int k = lane; k < L; k += 32) s = fma(row[k], v[k], s);
-      s = wsum(s);
-      const double pi = tj * s;
-      if (lane == 0) p[i] = pi;
-      pv = fma(pi, v[i], pv);
+    // p = tau A22 v and the shares of p^T v: eight threads per row (128 rows per sweep)
+    {
+      const int rr = t >> 3, k0 = t & 7;
+      double acc = 0.0;
+      if (rr < L) {
+        const double* row = A + (j + 1 + rr) * la + (j + 1);
+        // fixed trip count (m <= 112: at most 14 entries per thread), fully unrolled so the
+        // shared-memory loads of all entries are in flight together
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int it = 0; it < 7; ++it) {
+          const int k = k0 + 16 * it;
+          const double x0 = k < L ? row[k] : 0.0, y0 = k < L ? v[k] : 0.0;
+          const double x1 = k + 8 < L ? row[k + 8] : 0.0, y1 = k + 8 < L ? v[k + 8] : 0.0;
+          a0 = fma(x0, y0, a0);
+          a1 = fma(x1, y1, a1);
+        }
+        acc = a0 + a1;
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      double pvs = 0.0;
+      if (rr < L && k0 == 0) {
+        const double pi = tj * acc;
+        p[rr] = pi;
+        pvs = pi * v[rr];
+      }
+      pvs += __shfl_xor_sync(0xffffffffu, pvs, 8);
+      pvs += __shfl_xor_sync(0xffffffffu, pvs, 16);
+      if (lane == 0) wp[w] = pvs;
     }
-    if (lane == 0) wp[w] = pv;
     __syncthreads();
     double K = 0.0;
+#pragma unroll 8
     for (int k = 0; k < kNW; ++k) K += wp[k];
     K *= 0.5 * tj;
-    // w = p - K v (in place over p)
-    for (int i = t; i < L; i += kRT) p[i] = p[i] - K * v[i];
-    __syncthreads();
-    // A22 -= v w^T + w v^T: eight threads per row, each row's (v_i, w_i) held in registers
-    for (int rr = t >> 3; rr < L; rr += kRT >> 3) {
-      const double vi = v[rr], wi = p[rr];
-      double* row = A + (j + 1 + rr) * la + (j + 1);
-      for (int k = t & 7; k < L; k += 8) row[k] -= fma(vi, p[k], wi * v[k]);
+    // A22 -= v w^T + w v^T with w = p - K v: eight threads per row
+    {
+      const int rr = t >> 3, k0 = t & 7;
+      if (rr < L) {
+        const double vi = v[rr], wi = p[rr] - K * vi;
+        double* row = A + (j + 1 + rr) * la + (j + 1);
+        double nv[14];
+#pragma unroll
+        for (int it = 0; it < 14; ++it) {
+          const int k = k0 + 8 * it;
+          const bool in = k < L;
+          const double vk = in ? v[k] : 0.0, pk = in ? p[k] : 0.0, ak = in ? row[k] : 0.0;
+          nv[it] = ak - fma(vi, pk - K * vk, wi * vk);
+        }
+#pragma unroll
+        for (int it = 0; it < 14; ++it) {
+          const int k = k0 + 8 * it;
+          if (k < L) row[k] = nv[it];
+        }
+      }
     }
     __syncthreads();
   }
@@ -248,32 +349,13 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
   __syncthreads();
   const double pivmin = sc[3];
   // ---- 2. eigenvalues by multisection: group k owns the k-th largest (index m-1-k ascending),
-  //      the eight lanes of a group split its interval nine ways per round; only the top nvec
-  //      and the smallest are computed (the Ritz values a restart keeps, and the norm estimate)
+  //      the LPE lanes of a group split its interval LPE + 1 ways per round; only the top nvec
+  //      and the smallest are computed (the Ritz values a restart keeps, and the norm estimate).
   {
-    const int grp = t / kLanesPerEig, sub = t % kLanesPerEig;
-    const int ngrp = kRT / kLanesPerEig;
     const int neig = nvec < m ? nvec + 1 : m;
-    for (int k0 = 0; k0 < neig; k0 += ngrp) {
-      const int kk = k0 + grp;
-      const bool act = kk < neig;
-      const int k = (act && kk == nvec && nvec < m) ? m - 1 : kk;  // the extra group: the smallest
-      const int idx = m - 1 - (act ? k : 0);
-      double lo = sc[1], hi = sc[2];
-      for (int round = 0; round < kBisectRounds; ++round) {
-        const double x = lo + (hi - lo) * (double)(sub + 1) / (double)(kLanesPerEig + 1);
-        const int c = act ? sturm_count(d, e2, m, x, pivmin) : 0;
-        const unsigned below = __ballot_sync(0xffffffffu, c <= idx);
-        const unsigned mine = (below >> ((lane / kLanesPerEig) * kLanesPerEig)) & ((1u << kLanesPerEig) - 1u);
-        const int ones = __popc(mine);  // counts are monotone in x: lanes 0..ones-1 are below
-        const double step = (hi - lo) / (double)(kLanesPerEig + 1);
-        const double nlo = ones > 0 ? lo + step * ones : lo;
-        const double nhi = ones < kLanesPerEig ? lo + step * (ones + 1) : hi;
-        lo = nlo;
-        hi = nhi;
-      }
-      if (act && sub == 0) lam[k] = 0.5 * (lo + hi);
-    }
+    // (sixteen lanes / 14 rounds measured slower, 164 vs 116 us at m = 108: the Sturm recurrences
+    // share one SM's float64 pipe, so fewer evaluations beat fewer rounds)
+    multisect<kLanesPerEig, kBisectRounds>(d, e2, m, nvec, neig, sc[1], sc[2], pivmin, lam);
   }
   __syncthreads();
   // Ritz values not computed (between the top nvec and the smallest) are reported as the smallest
@@ -342,11 +424,11 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
   //      I - V T V^T, T upper triangular from tau and V^T V): per block one pass of dots
   //      W1 = V^T Z (a warp per column, lanes over rows, shuffle trees), T and W2 = T W1, one
   //      rank-P update -- four barriers per block instead of three per reflector
-  {
-    constexpr int kWY = 8;
-    double* W1 = sc + 8;   // kWY x nvec (<= 8 x 112)
-    double* Gv = wp;       // kWY x kWY Gram of the block's reflectors
-    double* Tm = wp + 64;  // kWY x kWY
+  auto back_transform = [&](auto kwy_c) {
+    constexpr int kWY = decltype(kwy_c)::value;
+    double* W1 = sc + 8;               // kWY x nvec (8 x 112 or 16 x 64 doubles)
+    double* Gv = W1 + 1024;            // kWY x kWY Gram of the block's reflectors
+    double* Tm = Gv + kWY * kWY;       // kWY x kWY
     const int nr = m - 2;  // reflectors 0 .. m-3
     for (int j1 = nr; j1 > 0; j1 -= kWY) {
       const int j0 = j1 - kWY > 0 ? j1 - kWY : 0;
@@ -443,7 +525,9 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
       }
       __syncthreads();
     }
-  }
+  };
+  // (blocks of sixteen reflectors measured no faster than eight: 159 vs 146 us at m = 108, top 56)
+  back_transform(std::integral_constant<int, 8>{});
   rr_mark(4);
   // ---- 5. Newton-Schulz: G = S^T S in A (reflectors no longer needed), S <- S (3I - G) / 2 by rows
   double delta = 0.0;
@@ -533,7 +617,7 @@ __global__ void __launch_bounds__(kRT, 1) k_rr_wide(const double* __restrict__ H
 }  // namespace
 
 size_t rr_wide_smem(int m) {
-  const size_t tri = (size_t)m * (m + 1) + (size_t)m * m + 8 * (size_t)m + 8 * kNW + 8 + 8 * 112;
+  const size_t tri = (size_t)m * (m + 1) + (size_t)m * m + 8 * (size_t)m + 8 * kNW + 8 + 1024 + 512;
   return std::max(tri, (size_t)jacobi_smem_doubles(m)) * sizeof(double);
 }
 

@@ -774,6 +774,10 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   s->in_solve = true;  // the operator is fixed for the solve: per-pattern scratch (CSR panel pointers) is reused
   s->csr_pp_valid = false;
   if (overlap) s->coop_sm = s->sm_count - 1;
+  static const int rr_lag = [] {  // blocks run ahead of an overlapped Rayleigh-Ritz (diagnostics override)
+    const char* e = getenv("MEGB200_RR_LAG");
+    return e ? std::max(1, std::min(4, atoi(e))) : 1;
+  }();
   const double tol = P.tol;
   const uint64_t key_start = stream_key(P.seed, kStreamStart);
   const uint64_t key_refill = stream_key(P.seed, kStreamRefill);
@@ -836,12 +840,19 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       double* v2 = vec_out ? vec_out : (epi ? epi->v_next : nullptr);
       const int64_t ld2 = vec_out ? ld_vec : (epi ? epi->ld_next : 0);
       const int r2 = vec_out ? nreq : (epi ? epi->r : 0);
-      // overlapped restart: the wide solve on the side stream, the next block's orthonormalisation
-      // and pass on the solver stream, joined before the Ritz block / residual launch
+      // overlapped restart: the wide solve on the side stream, the next `lag` blocks' orthonormalisation
+      // and passes on the solver stream, joined before the Ritz block / residual launch
       // (from the second full basis of a solve on: a solve that converges at its first one -- cfg4's
       // six-pass steps -- would only pay for the speculation)
-      const bool spec = overlap && !fuse && full && cols > 0 && run.restarts >= 1 && nxt == cur && nxt > 0 &&
-                        newcols > 48 && run.passes < max_passes && newcols + nxt <= s->cap && keep + nxt <= newcols;
+      int lag = 0;
+      if (overlap && !fuse && full && cols > 0 && run.restarts >= 1 && nxt == cur && cur == bw && newcols > 48) {
+        lag = rr_lag;
+        while (lag > 0 && !(run.passes + lag <= max_passes && newcols + lag * bw <= std::min<int64_t>(s->cap, n) &&
+                            keep + lag * bw <= newcols &&
+                            (size_t)(newcols + lag * bw) * (lag * bw) * sizeof(double) <= 48 * 1024))
+          --lag;
+      }
+      const bool spec = lag > 0;
       if (spec) {
         MEG_CUDA(cudaEventRecord(s->ev_fork, s->stream));
         MEG_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
@@ -849,10 +860,42 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
         const int rq_ = std::min(newcols, std::max(nreq, bw));
         rr_wide(Ls, s->H, s->cap, newcols, s->theta, s->S, s->info, s->rr_nvec > 0 ? std::max(s->rr_nvec, rq_) : 0);
         MEG_CUDA(cudaEventRecord(s->ev_join, s->side));
-        copy_block(L, n, cur, s->AQ + cols, s->ldq, s->Q + newcols, s->ldq);
-        orthonormalize(s, s->Q + newcols, s->ldq, nxt, newcols, scale, key_refill, refill_ctr, false);
-        block_pass(s, op, newcols, nxt);
+        for (int l = 0; l < lag; ++l) {
+          const int cl = cols + l * bw;  // the block whose image seeds the next one
+          copy_block(L, n, bw, s->AQ + cl, s->ldq, s->Q + cl + bw, s->ldq);
+          orthonormalize(s, s->Q + cl + bw, s->ldq, bw, cl + bw, scale, key_refill, refill_ctr, false);
+          block_pass(s, op, cl + bw, bw);
+        }
         s->mark("spec orth+pass");
+        static const bool dbg_basis = getenv("MEGB200_DEBUG_BASIS") != nullptr;  // diagnostics: basis consistency
+        if (dbg_basis) {
+          const int nc = newcols + lag * bw;
+          std::vector<double> g((size_t)nc * s->cap), hc((size_t)nc * s->cap), hh((size_t)nc * s->cap);
+          for (int c0 = 0; c0 < nc; c0 += 32) {
+            const int w = std::min(32, nc - c0);
+            coop_tn(L, n, s->Q, s->ldq, nc, s->Q + c0, s->ldq, w, s->G + c0, s->cap, nullptr, 1.0, s->red, s->coop_sm);
+          }
+          s->sync();
+          MEG_CUDA(cudaMemcpy(g.data(), s->G, g.size() * sizeof(double), cudaMemcpyDeviceToHost));
+          for (int c0 = 0; c0 < nc; c0 += 32) {
+            const int w = std::min(32, nc - c0);
+            coop_tn(L, n, s->Q, s->ldq, nc, s->AQ + c0, s->ldq, w, s->G + c0, s->cap, nullptr, 1.0, s->red, s->coop_sm);
+          }
+          s->sync();
+          MEG_CUDA(cudaMemcpy(hc.data(), s->G, hc.size() * sizeof(double), cudaMemcpyDeviceToHost));
+          MEG_CUDA(cudaMemcpy(hh.data(), s->H, hh.size() * sizeof(double), cudaMemcpyDeviceToHost));
+          double eg = 0.0, eh = 0.0;
+          int gi = 0, gj = 0, hi = 0, hj = 0;
+          for (int i = 0; i < nc; ++i)
+            for (int j = i; j < nc; ++j) {
+              const double dg = fabs(g[(size_t)i * s->cap + j] - (i == j ? 1.0 : 0.0));
+              const double dh = fabs(hc[(size_t)i * s->cap + j] - hh[(size_t)i * s->cap + j]);
+              if (dg > eg) { eg = dg; gi = i; gj = j; }
+              if (dh > eh) { eh = dh; hi = i; hj = j; }
+            }
+          fprintf(stderr, "basis check nc %d: |Q^T Q - I| %.2e at (%d,%d), |Q^T AQ - H| %.2e at (%d,%d)\n", nc, eg, gi, gj,
+                  eh, hi, hj);
+        }
         MEG_CUDA(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
       }
       const int gr = fuse ? fused_pass(s, op, deferred_warm ? P.warm : s->Q, deferred_warm ? P.ld_warm : s->ldq, bw,
@@ -916,20 +959,21 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       }
       if (run.passes >= max_passes) break;
       if (spec) {
-        // not converged: the speculative pass is the next block's pass.  Thick restart keeping the
-        // leading `keep` Ritz pairs, the new block (orthogonal to all of Q) and its image behind them
-        run.passes++;
+        // not converged: the speculative passes are the next blocks' passes.  Thick restart keeping the
+        // leading `keep` Ritz pairs, the new blocks (orthogonal to all of Q) and their images behind them
+        const int tq = lag * bw;
+        run.passes += lag;
         nn(L, n, s->Q, s->ldq, newcols, s->S, newcols, keep, 1.0, 0.0, s->T, s->ldq);
         copy_block(L, n, keep, s->T, s->ldq, s->Q, s->ldq);
         nn(L, n, s->AQ, s->ldq, newcols, s->S, newcols, keep, 1.0, 0.0, s->T, s->ldq);
         copy_block(L, n, keep, s->T, s->ldq, s->AQ, s->ldq);
-        copy_block(L, n, nxt, s->Q + newcols, s->ldq, s->Q + keep, s->ldq);
-        copy_block(L, n, nxt, s->AQ + newcols, s->ldq, s->AQ + keep, s->ldq);
-        restart_h(L, s->H, s->cap, s->S, newcols, keep, nxt, s->theta);
+        copy_block(L, n, tq, s->Q + newcols, s->ldq, s->Q + keep, s->ldq);
+        copy_block(L, n, tq, s->AQ + newcols, s->ldq, s->AQ + keep, s->ldq);
+        restart_h(L, s->H, s->cap, s->S, newcols, keep, tq, s->theta);
         s->mark("restart");
         run.restarts++;
-        cols = keep;
-        cur = nxt;
+        cols = keep + tq - bw;  // the last carried block is the current one, its pass done
+        cur = bw;
         pass_done = true;
         continue;
       }
