@@ -126,6 +126,10 @@ void set_diag(const Launch& L, double* H, int cap, int k, const double* theta);
 // Thick restart of H when the next block's column block H[0:m+q, m:m+q] is already there (the overlapped
 // Rayleigh-Ritz of top_eigs): H <- [diag(theta[0:keep]), S[:, 0:keep]^T H[0:m, m:m+q]; ., H[m:m+q, m:m+q]]
 // (upper triangle), everything else zero.  S is m x m row-major (column k = Ritz vector k).
+// Thick restart of the basis, in place, in one launch: Q[:, 0:keep] = Q[:, 0:m] S[:, 0:keep], the same for
+// AQ, and the tq columns [m, m + tq) of both moved to [keep, keep + tq) (keep + tq <= m)
+void restart_basis(const Launch& L, int64_t n, double* Q, double* AQ, int64_t ldq, const double* S, int m, int keep,
+                   int tq, int sm_count);
 void restart_h(const Launch& L, double* H, int cap, const double* S, int m, int keep, int q, const double* theta);
 
 // cooperative tall-skinny kernels (megb200_coop.cu): one launch each

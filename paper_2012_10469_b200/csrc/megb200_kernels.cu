@@ -1760,32 +1760,85 @@ __global__ void k_set_diag(double* __restrict__ H, int cap, int k, const double*
   H[idx] = (i == j && i < k) ? theta[i] : 0.0;
 }
 
+// Thick restart of the basis in ONE launch, in place: Q[:, 0:keep] = Q[:, 0:m] S_keep, the same for
+// the images AQ, and the tq carried columns [m, m + tq) of both moved to [keep, keep + tq).  A CTA
+// stages 32 rows of both arrays (m + tq columns) in shared memory next to S_keep (m x keep), so the
+// rows are read once and written once (the seven launches this replaces re-read S per 256 outputs).
+constexpr int kRestartRows = 32;
+__global__ void __launch_bounds__(256) k_restart_basis(int64_t n, double* __restrict__ Q, double* __restrict__ AQ,
+                                                       int64_t ldq, const double* __restrict__ S, int m, int keep,
+                                                       int tq) {
+  extern __shared__ double rsm[];
+  const int W = m + tq, t = threadIdx.x;
+  double* Ss = rsm;              // m x keep
+  double* Xs = Ss + m * keep;    // 2 x kRestartRows x W
+  for (int idx = t; idx < m * keep; idx += 256) {
+    const int k = idx / keep, c = idx - k * keep;
+    Ss[idx] = S[(int64_t)k * m + c];
+  }
+  const int64_t rows_per = ((n + gridDim.x - 1) / gridDim.x + kRestartRows - 1) / kRestartRows * kRestartRows;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(n, r0 + rows_per);
+  for (int64_t rc = r0; rc < r1; rc += kRestartRows) {
+    const int rows = (int)min((int64_t)kRestartRows, r1 - rc);
+    __syncthreads();
+    for (int idx = t; idx < rows * W; idx += 256) {
+      const int r = idx / W, k = idx - r * W;
+      Xs[idx] = Q[(rc + r) * ldq + k];
+      Xs[kRestartRows * W + idx] = AQ[(rc + r) * ldq + k];
+    }
+    __syncthreads();
+    for (int o = t; o < 2 * rows * keep; o += 256) {
+      const int mat = o / (rows * keep), rem = o - mat * rows * keep;
+      const int r = rem / keep, c = rem - r * keep;
+      const double* x = Xs + mat * kRestartRows * W + r * W;
+      double a0 = 0.0, a1 = 0.0;
+      int k = 0;
+      for (; k + 1 < m; k += 2) {
+        a0 = fma(x[k], Ss[k * keep + c], a0);
+        a1 = fma(x[k + 1], Ss[(k + 1) * keep + c], a1);
+      }
+      if (k < m) a0 = fma(x[k], Ss[k * keep + c], a0);
+      (mat ? AQ : Q)[(rc + r) * ldq + c] = a0 + a1;
+    }
+    for (int o = t; o < 2 * rows * tq; o += 256) {
+      const int mat = o / (rows * tq), rem = o - mat * rows * tq;
+      const int r = rem / tq, j = rem - r * tq;
+      (mat ? AQ : Q)[(rc + r) * ldq + keep + j] = Xs[mat * kRestartRows * W + r * W + m + j];
+    }
+  }
+}
+
 // one CTA: the new block's column block B = H[0:m+q, m:m+q] is staged in shared memory, H is
 // cleared, then diag(theta), S_keep^T B[0:m] and the block's own diagonal block are written
-__global__ void __launch_bounds__(256) k_restart_h(double* __restrict__ H, int cap, const double* __restrict__ S, int m,
-                                                   int keep, int q, const double* __restrict__ theta) {
-  extern __shared__ double bs[];  // (m + q) x q
-  const int t = threadIdx.x;
-  for (int idx = t; idx < (m + q) * q; idx += 256) {
+__global__ void __launch_bounds__(1024) k_restart_h(double* __restrict__ H, int cap, const double* __restrict__ S, int m,
+                                                    int keep, int q, const double* __restrict__ theta) {
+  extern __shared__ double bs[];  // (m + q) x q, then S_keep (m x keep)
+  double* Ss = bs + (m + q) * q;
+  const int t = threadIdx.x, NT = blockDim.x;
+  for (int idx = t; idx < (m + q) * q; idx += NT) {
     const int i = idx / q, j = idx - i * q;
     bs[idx] = H[(int64_t)i * cap + m + j];
   }
+  for (int idx = t; idx < m * keep; idx += NT) {
+    const int k = idx / keep, c = idx - k * keep;
+    Ss[idx] = S[(int64_t)k * m + c];
+  }
   __syncthreads();
-  for (int idx = t; idx < cap * cap; idx += 256) H[idx] = 0.0;
+  for (int idx = t; idx < cap * cap; idx += NT) H[idx] = 0.0;
   __syncthreads();
-  for (int i = t; i < keep; i += 256) H[(int64_t)i * cap + i] = theta[i];
-  for (int idx = t; idx < keep * q; idx += 256) {
+  for (int i = t; i < keep; i += NT) H[(int64_t)i * cap + i] = theta[i];
+  for (int idx = t; idx < keep * q; idx += NT) {
     const int i = idx / q, j = idx - i * q;
     double a0 = 0.0, a1 = 0.0;
     int k = 0;
     for (; k + 1 < m; k += 2) {
-      a0 = fma(S[(int64_t)k * m + i], bs[k * q + j], a0);
-      a1 = fma(S[(int64_t)(k + 1) * m + i], bs[(k + 1) * q + j], a1);
+      a0 = fma(Ss[k * keep + i], bs[k * q + j], a0);
+      a1 = fma(Ss[(k + 1) * keep + i], bs[(k + 1) * q + j], a1);
     }
-    if (k < m) a0 = fma(S[(int64_t)k * m + i], bs[k * q + j], a0);
+    if (k < m) a0 = fma(Ss[k * keep + i], bs[k * q + j], a0);
     H[(int64_t)i * cap + keep + j] = a0 + a1;
   }
-  for (int idx = t; idx < q * q; idx += 256) {
+  for (int idx = t; idx < q * q; idx += NT) {
     const int i = idx / q, j = idx - i * q;
     if (i <= j) H[(int64_t)(keep + i) * cap + keep + j] = bs[(m + i) * q + j];
   }
@@ -2414,10 +2467,26 @@ void set_diag(const Launch& L, double* H, int cap, int k, const double* theta) {
   ++*L.counter;
 }
 
+void restart_basis(const Launch& L, int64_t n, double* Q, double* AQ, int64_t ldq, const double* S, int m, int keep,
+                   int tq, int sm_count) {
+  const size_t smem = ((size_t)m * keep + 2 * (size_t)kRestartRows * (m + tq)) * sizeof(double);
+  if (keep + tq > m || smem > 200 * 1024) throw Error(MEGB200_ERR_PARAM, "restart_basis: shape out of range");
+  static char attr = 0;
+  if (first_on_device(&attr))
+    MEG_CUDA(cudaFuncSetAttribute(k_restart_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count, cdiv(n, kRestartRows)));
+  k_restart_basis<<<grid, 256, smem, L.stream>>>(n, Q, AQ, ldq, S, m, keep, tq);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
 void restart_h(const Launch& L, double* H, int cap, const double* S, int m, int keep, int q, const double* theta) {
-  const size_t smem = (size_t)(m + q) * q * sizeof(double);
-  if (keep + q > m || m + q > cap || smem > 48 * 1024) throw Error(MEGB200_ERR_PARAM, "restart_h: shape out of range");
-  k_restart_h<<<1, 256, smem, L.stream>>>(H, cap, S, m, keep, q, theta);
+  const size_t smem = ((size_t)(m + q) * q + (size_t)m * keep) * sizeof(double);
+  if (keep + q > m || m + q > cap || smem > 160 * 1024) throw Error(MEGB200_ERR_PARAM, "restart_h: shape out of range");
+  static char attr = 0;
+  if (first_on_device(&attr))
+    MEG_CUDA(cudaFuncSetAttribute(k_restart_h, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  k_restart_h<<<1, 1024, smem, L.stream>>>(H, cap, S, m, keep, q, theta);
   MEG_LAUNCHED();
   ++*L.counter;
 }

@@ -849,7 +849,8 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
         lag = rr_lag;
         while (lag > 0 && !(run.passes + lag <= max_passes && newcols + lag * bw <= std::min<int64_t>(s->cap, n) &&
                             keep + lag * bw <= newcols &&
-                            (size_t)(newcols + lag * bw) * (lag * bw) * sizeof(double) <= 48 * 1024))
+                            ((size_t)(newcols + lag * bw) * (lag * bw) + (size_t)newcols * keep) * sizeof(double) <=
+                                160 * 1024))
           --lag;
       }
       const bool spec = lag > 0;
@@ -963,12 +964,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
         // leading `keep` Ritz pairs, the new blocks (orthogonal to all of Q) and their images behind them
         const int tq = lag * bw;
         run.passes += lag;
-        nn(L, n, s->Q, s->ldq, newcols, s->S, newcols, keep, 1.0, 0.0, s->T, s->ldq);
-        copy_block(L, n, keep, s->T, s->ldq, s->Q, s->ldq);
-        nn(L, n, s->AQ, s->ldq, newcols, s->S, newcols, keep, 1.0, 0.0, s->T, s->ldq);
-        copy_block(L, n, keep, s->T, s->ldq, s->AQ, s->ldq);
-        copy_block(L, n, tq, s->Q + newcols, s->ldq, s->Q + keep, s->ldq);
-        copy_block(L, n, tq, s->AQ + newcols, s->ldq, s->AQ + keep, s->ldq);
+        restart_basis(L, n, s->Q, s->AQ, s->ldq, s->S, newcols, keep, tq, s->sm_count);
         restart_h(L, s->H, s->cap, s->S, newcols, keep, tq, s->theta);
         s->mark("restart");
         run.restarts++;
@@ -1000,11 +996,16 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
     cols = newcols;
     if (full) {
       // thick restart: keep the leading `keep` Ritz pairs, continue from the next block
-      nn(L, n, s->Q, s->ldq, cols, s->S, cols, keep, 1.0, 0.0, s->T, s->ldq);
-      copy_block(L, n, keep, s->T, s->ldq, s->Q, s->ldq);
-      nn(L, n, s->AQ, s->ldq, cols, s->S, cols, keep, 1.0, 0.0, s->T, s->ldq);
-      copy_block(L, n, keep, s->T, s->ldq, s->AQ, s->ldq);
-      copy_block(L, n, nxt, s->Q + cols, s->ldq, s->Q + keep, s->ldq);
+      if (keep + nxt <= cols && cols + nxt <= s->cap) {
+        // one launch (the carried AQ columns are not images yet: the next pass overwrites them)
+        restart_basis(L, n, s->Q, s->AQ, s->ldq, s->S, cols, keep, nxt, s->sm_count);
+      } else {
+        nn(L, n, s->Q, s->ldq, cols, s->S, cols, keep, 1.0, 0.0, s->T, s->ldq);
+        copy_block(L, n, keep, s->T, s->ldq, s->Q, s->ldq);
+        nn(L, n, s->AQ, s->ldq, cols, s->S, cols, keep, 1.0, 0.0, s->T, s->ldq);
+        copy_block(L, n, keep, s->T, s->ldq, s->AQ, s->ldq);
+        copy_block(L, n, nxt, s->Q + cols, s->ldq, s->Q + keep, s->ldq);
+      }
       set_diag(L, s->H, s->cap, keep, s->theta);  // H = diag(theta_keep); couplings arrive with the next pass
       s->mark("restart");
       cols = keep;

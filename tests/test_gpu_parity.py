@@ -96,6 +96,63 @@ def test_operator_apply_f32_and_csr(pb):
     assert normwise(op.apply(u), -0.5 * (g @ u)) <= 1e-14
 
 
+@pytest.mark.parametrize("n,b,density", [(3000, 18, 0.04), (2500, 32, 0.02), (4096, 7, 0.05), (1500, 16, 0.001)])
+def test_csr_panel_pass_ragged(pb, n, b, density):
+    """The panel-tiled CSR pass (n >= 1024: U panels in shared memory, per-row panel pointers) against
+    scipy on ragged patterns: empty rows, one dense row longer than the prefetched batches, odd and
+    even block widths (the 16-byte staged copy and its plain fallback), a nearly empty matrix."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(n + b)
+    mask = rng.random((n, n)) < density
+    mask[5, :] = True         # a row with n entries in every panel
+    mask[17:40, :] = False    # empty rows
+    mask = np.triu(mask) | np.triu(mask).T
+    vals = om.symmetrize(rng.standard_normal((n, n)))
+    g = sp.csr_matrix(np.where(mask, vals, 0.0))
+    g.sort_indices()
+    u = rng.standard_normal((n, b))
+    op = pb.SymmetricOperator.from_csr(n, g.indptr.astype(np.int32), g.indices.astype(np.int32), g.data, scale=1.5)
+    want = 1.5 * (g @ u)
+    assert normwise(op.apply(u), want) <= 1e-14
+    assert normwise(op.apply(u), want) <= 1e-14  # a second pass (panel pointers rebuilt outside a solve)
+
+
+def test_overlapped_restart_matches_serial_order():
+    """top_r through restarts with the wide Rayleigh-Ritz overlapped (side stream, carried block) and with
+    the serial order (MEGB200_NO_RR_OVERLAP=1, its own process: the switch is read once) agree to the
+    solver's accuracy and take the same number of passes."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json, numpy as np, paper_2012_10469_b200 as pb\n"
+        "from oracle import cpu_meg as om\n"
+        "rng = np.random.default_rng(11)\n"
+        "n = 1536\n"
+        "q, _ = np.linalg.qr(rng.standard_normal((n, n)))\n"
+        "ev = np.concatenate([3.0 - 0.2 * np.arange(6), 1.0 - 0.9 * rng.random(n - 6) ** 0.5])\n"
+        "a = (q * ev) @ q.T\n"
+        "a = (a + a.T) / 2\n"
+        "top = pb.lanczos_top_r(pb.SymmetricOperator.from_dense(a), r=6, tol=1e-10, seed=3, subspace=64, block=14)\n"
+        "print(json.dumps({'ev': top.eigenvalues.tolist(), 'passes': int(top.passes),\n"
+        "                  'res': float(np.abs(a @ top.eigenvectors - top.eigenvectors * top.eigenvalues).max())}))\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for extra in ({}, {"MEGB200_NO_RR_OVERLAP": "1"}):
+        env = dict(os.environ, PYTHONPATH=root, **extra)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    a, b = outs
+    assert a["passes"] > 8 and a["passes"] == b["passes"]  # restarts happened; same subspaces
+    assert np.max(np.abs(np.array(a["ev"]) - np.array(b["ev"]))) <= 1e-10
+    assert a["res"] <= 1e-9 and b["res"] <= 1e-9
+
+
 # ---------------------------------------------------------------------------
 # step, operator, certificates (test_meg.py)
 
