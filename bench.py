@@ -204,8 +204,9 @@ def operand_bytes(w) -> int:
 
 def l2_note(w) -> str:
     if w.kind == "sampled":
-        return ("not flushed: CSR operand (~40 MB) + factor gathers are re-streamed every pass; the pass is "
-                "L2-gather bound (profiles/)")
+        return ("not flushed: the CSR operand (~40 MB) is smaller than the 126 MB L2 and is re-read by every one of "
+                "the ~27 passes of a step, so it can stay L2-resident between passes; the panel pass is bound by "
+                "shared-memory wavefronts, not by HBM (profiles/)")
     mb = operand_bytes(w) / 1e6
     return f"not flushed: operand {mb:.0f} MB > 126 MB L2, streamed evict-first every pass"
 
@@ -369,7 +370,7 @@ def measure_workload(name: str, W: int, K: int, world: int, dev, peak: float, sa
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak if achieved else None, "traffic": None,
         "kernel": {"f64": "k_dense_pass_mma (TMA + DMMA/DFMA)", "f32": "k_dense_pass_umma (TMA + tcgen05 split TF32)",
-                   "csr": "k_csr_apply (warp per row, gathered factor rows)"}["csr" if w.kind == "sampled" else w.dtype],
+                   "csr": "k_csr_apply_panel (U panels in shared memory, warp per row)"}["csr" if w.kind == "sampled" else w.dtype],
         "bytes_per_pass": bytes_per_pass, "pass_ms": pass_ms, "passes_measured": int(pc.value),
         "share_of_step": (pass_ms * float(np.mean(passes)) / ms_per_step) if pass_ms else None,
     }

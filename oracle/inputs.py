@@ -110,7 +110,7 @@ def _geom(r, ratio):
 CONFIGS = {
     "cfg1": MegConfig("cfg1", 500, 5, (0.4, 0.25, 0.15, 0.12, 0.08), 0.01, 200, "f64", 13, "dense", subspace=None),
     "cfg2": MegConfig("cfg2", 4096, 10, _geom(10, 0.7), 0.01, 300, "f64", 18, "dense"),
-    "cfg3": MegConfig("cfg3", 8192, 10, _geom(10, 0.7), 0.0, 300, "f64", 16, "sampled"),
+    "cfg3": MegConfig("cfg3", 8192, 10, _geom(10, 0.7), 0.0, 300, "f64", 14, "sampled", subspace=98),
     "cfg4": MegConfig(
         "cfg4", 16384, 8, (0.3, 0.2, 0.15, 0.1, 0.1, 0.05, 0.05, 0.05), 0.0, 1000, "f32", 16, "stochastic",
         eta_decay=True,

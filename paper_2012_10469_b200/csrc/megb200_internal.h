@@ -154,6 +154,10 @@ struct LamCoef {
   int lr = 0;
   double c1 = 0.0, log_tail = 0.0, eta = 0.0, tail_g = 0.0;
 };
+// The operator itself into AQ (n x n, ld ldq) and H (ld ldh): A = scale * M + L diag(d) L^T + alpha I (identity-basis
+// solves of small problems; M float64 symmetric, may be null with scale 0)
+void form_operator(const Launch& L, int64_t n, const double* M, int64_t ldm, double scale, const double* Lf, int64_t ldl,
+                   int l, const double* d, LamCoef lc, double alpha, double* AQ, int64_t ldq, double* H, int64_t ldh);
 void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, double scale, const double* Lf,
                  int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
                  int64_t ldw, double* Ews, double* part, int sm_count, const double* Qh = nullptr, int64_t ldq = 0,

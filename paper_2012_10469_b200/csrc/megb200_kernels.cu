@@ -1760,6 +1760,46 @@ __global__ void k_set_diag(double* __restrict__ H, int cap, int k, const double*
   H[idx] = (i == j && i < k) ? theta[i] : 0.0;
 }
 
+// Small problems solved on the identity basis (n <= the Rayleigh-Ritz limit): the operator itself,
+// A = scale * M + L diag(d) L^T + alpha I, formed entry by entry into H (the Rayleigh-Ritz matrix) and
+// AQ (the images A I) in one launch -- instead of n / 32 block passes over identity columns.
+constexpr int kFormMaxLowrank = 160;
+__global__ void __launch_bounds__(128) k_form_operator(int64_t n, const double* __restrict__ M, int64_t ldm, double scale,
+                                                       const double* __restrict__ Lf, int64_t ldl, int l,
+                                                       const double* __restrict__ d, LamCoef lc, double alpha,
+                                                       double* __restrict__ AQ, int64_t ldq, double* __restrict__ H,
+                                                       int64_t ldh) {
+  __shared__ double dsh[kFormMaxLowrank];
+  __shared__ double li[kFormMaxLowrank];
+  const int i = blockIdx.x;
+  for (int k = threadIdx.x; k < l; k += 128) {
+    double v;
+    if (lc.lam && k < lc.lr) {
+      const double kept = lc.c1 * lc.lam[k];
+      v = (log(kept) - lc.log_tail) + (-lc.eta * (kept - lc.tail_g));
+    } else {
+      v = d[k];
+    }
+    dsh[k] = v;
+    li[k] = Lf[(int64_t)i * ldl + k] * v;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += 128) {
+    double a0 = 0.0, a1 = 0.0;
+    const double* lj = Lf + (int64_t)j * ldl;
+    int k = 0;
+    for (; k + 1 < l; k += 2) {
+      a0 = fma(li[k], lj[k], a0);
+      a1 = fma(li[k + 1], lj[k + 1], a1);
+    }
+    if (k < l) a0 = fma(li[k], lj[k], a0);
+    // the pass reads rows of M where the product needs columns (M symmetric): M[j, i]
+    const double v = (scale != 0.0 ? scale * M[(int64_t)j * ldm + i] : 0.0) + (a0 + a1) + (i == j ? alpha : 0.0);
+    AQ[(int64_t)i * ldq + j] = v;
+    H[(int64_t)i * ldh + j] = v;
+  }
+}
+
 // Thick restart of the basis in ONE launch, in place: Q[:, 0:keep] = Q[:, 0:m] S_keep, the same for
 // the images AQ, and the tq carried columns [m, m + tq) of both moved to [keep, keep + tq).  A CTA
 // stages 32 rows of both arrays (m + tq columns) in shared memory next to S_keep (m x keep), so the
@@ -2463,6 +2503,14 @@ void set_identity(const Launch& L, int64_t n, double* Q, int64_t ldq) {
 
 void set_diag(const Launch& L, double* H, int cap, int k, const double* theta) {
   k_set_diag<<<cdiv((int64_t)cap * cap, 256), 256, 0, L.stream>>>(H, cap, k, theta);
+  MEG_LAUNCHED();
+  ++*L.counter;
+}
+
+void form_operator(const Launch& L, int64_t n, const double* M, int64_t ldm, double scale, const double* Lf, int64_t ldl,
+                   int l, const double* d, LamCoef lc, double alpha, double* AQ, int64_t ldq, double* H, int64_t ldh) {
+  if (l > kFormMaxLowrank) throw Error(MEGB200_ERR_PARAM, "form_operator: low-rank width out of range");
+  k_form_operator<<<(unsigned)n, 128, 0, L.stream>>>(n, M, ldm, scale, Lf, ldl, l, d, lc, alpha, AQ, ldq, H, ldh);
   MEG_LAUNCHED();
   ++*L.counter;
 }

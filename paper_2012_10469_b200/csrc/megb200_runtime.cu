@@ -752,7 +752,11 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   const EigShape sh = eig_shape(s, nreq, P);
   const int bw = sh.bw, mmax = sh.mmax, keep = sh.keep, max_passes = sh.max_passes;
   // a wide Rayleigh-Ritz needs the Ritz pairs a thick restart keeps (and the Ritz block)
-  s->rr_nvec = sh.identity ? std::min<int>((int)n, std::max(nreq, bw)) : sh.exhaust ? 0 : std::max(keep, nreq);
+  // identity basis: no later pass uses a Ritz block (no warm start, no restart), so only the nreq
+  // wanted Ritz pairs are formed (eigenvectors, back-transform and Newton-Schulz of the wide solver
+  // scale with that count) and the Ritz block returned is nreq wide
+  const int rbw = sh.identity ? std::min(bw, nreq) : bw;
+  s->rr_nvec = sh.identity ? nreq : sh.exhaust ? 0 : std::max(keep, nreq);
   struct NvecReset {
     megb200_solver* s;
     ~NvecReset() { s->rr_nvec = 0; }
@@ -816,6 +820,21 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
   int cols = 0, cur = bw;
   double scale = 1.0;
   bool pass_done = false;  // the current block's pass already ran (overlapped with the last Rayleigh-Ritz)
+  double first_ratio = 0.0;  // worst residual / tolerance after the first pass
+  // identity basis with a float64 dense (or no) streamed operand: A I is the operator itself, formed
+  // entry by entry in one launch (H and the images) instead of ceil(n / 32) block passes
+  static const bool no_form = getenv("MEGB200_NO_FORM_OPERATOR") != nullptr;  // diagnostics
+  if (sh.identity && !no_form && op.l <= 160 && (op.l == 0 || op.L) &&
+      ((op.kind == MEGB200_OP_DENSE && op.dtype == MEGB200_F64) || op.scale == 0.0 || op.kind == MEGB200_OP_NONE)) {
+    if (op.lc.lam == s->dlam) s->flush_dlam();
+    const bool dense = op.kind == MEGB200_OP_DENSE && op.scale != 0.0;
+    form_operator(L, n, dense ? static_cast<const double*>(op.dense) : nullptr, op.ld, dense ? op.scale : 0.0, op.L,
+                  op.ldl, op.L ? op.l : 0, op.d_dev, op.lc, op.alpha, s->AQ, s->ldq, s->H, s->cap);
+    run.passes = 1;
+    cur = (int)n;
+    pass_done = true;
+    s->mark("pass+finish");
+  }
   for (;;) {
     // operator pass on the current block, then its column of H = Q^T A Q; the first pass
     // of a solve runs fused with its Rayleigh-Ritz (one launch after the pass)
@@ -842,10 +861,12 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       const int r2 = vec_out ? nreq : (epi ? epi->r : 0);
       // overlapped restart: the wide solve on the side stream, the next `lag` blocks' orthonormalisation
       // and passes on the solver stream, joined before the Ritz block / residual launch
-      // (from the second full basis of a solve on: a solve that converges at its first one -- cfg4's
-      // six-pass steps -- would only pay for the speculation)
+      // (from the second full basis of a solve on, or from the first when the first pass left the
+      // residuals more than 1e5 x the tolerance away: a solve that converges at its first full basis --
+      // cfg4's six-pass steps, ~1e4 x after the first pass -- would only pay for the speculation)
       int lag = 0;
-      if (overlap && !fuse && full && cols > 0 && run.restarts >= 1 && nxt == cur && cur == bw && newcols > 48) {
+      if (overlap && !fuse && full && cols > 0 && (run.restarts >= 1 || first_ratio > 1e5) && nxt == cur && cur == bw &&
+          newcols > 48) {
         lag = rr_lag;
         while (lag > 0 && !(run.passes + lag <= max_passes && newcols + lag * bw <= std::min<int64_t>(s->cap, n) &&
                             keep + lag * bw <= newcols &&
@@ -901,8 +922,8 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
       }
       const int gr = fuse ? fused_pass(s, op, deferred_warm ? P.warm : s->Q, deferred_warm ? P.ld_warm : s->ldq, bw,
                                        nreq, epi, ritz_out, ld_ritz, v2, ld2, r2, pk)
-                          : rr_readback(s, newcols, nreq, bw, epi, pk, ritz_out, ld_ritz, v2, ld2, r2, spec);
-      const int rq = std::min(newcols, std::max(nreq, bw));
+                          : rr_readback(s, newcols, nreq, rbw, epi, pk, ritz_out, ld_ritz, v2, ld2, r2, spec);
+      const int rq = std::min(newcols, std::max(nreq, rbw));
       // host-buffer step: V_next travels back with the pack (one wait when this RR converges)
       if (epi && epi->v_host && epi->v_next && epi->ld_next == epi->r && epi->ld_host == epi->r)
         MEG_CUDA(cudaMemcpyAsync(epi->v_host, epi->v_next, (size_t)n * epi->r * sizeof(double),
@@ -934,6 +955,7 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
         }
       }
       const RRDecision dec = rr_decide(s, pk, newcols, nreq, tol);
+      if (cols == 0) first_ratio = dec.rmax / (tol * dec.scale);
       static const bool dbg_rr = getenv("MEGB200_DEBUG_RR") != nullptr;  // diagnostics
       if (dbg_rr)
         fprintf(stderr, "rr pass %d cols %d newcols %d full %d rmax %.3e theta0 %.6f scale %.3f\n", run.passes, cols,

@@ -13,6 +13,11 @@ KEYS = [
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe active %"),
     ("SM_C.TriageCompute.smsp__pipe_tensor_subpipe_dmma_cycles_active.avg", "DMMA subpipe active cycles / SMSP"),
     ("TPC.TriageCompute.sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg", "HMMA (tf32) subpipe active cycles / SM"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % of peak"),
+    ("lts__t_bytes.sum", "L2 bytes"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "L1/shared-memory throughput % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts"),
+    ("smsp__inst_executed.sum", "warp instructions executed"),
     ("sm__cycles_active.avg", "SM active cycles (avg)"),
     ("sm__cycles_active.max", "SM active cycles (max)"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared-memory bank conflicts"),
