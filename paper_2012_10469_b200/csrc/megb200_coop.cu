@@ -68,10 +68,11 @@ __device__ __forceinline__ void cta_rows(int64_t n, int64_t& r0, int64_t& r1) {
 template <int J>
 __device__ __forceinline__ void xty_rows(int64_t r0, int64_t r1, const double* __restrict__ X, int64_t ldx, int p,
                                          const double* __restrict__ Y, int64_t ldy, int q, double* sm,
-                                         double (&acc)[J]) {
+                                         double (&acc)[J], bool gram = false) {
+  // gram: the output has q more rows, Y^T Y, after the p rows of X^T Y (the staged Y rows serve as both)
   double* Xs = sm;
   double* Ys = sm + kRC * p;
-  const int pq = p * q;
+  const int pq = (gram ? p + q : p) * q;
   int oa[J], oc[J];
 #pragma unroll
   for (int j = 0; j < J; ++j) {
@@ -97,11 +98,13 @@ __device__ __forceinline__ void xty_rows(int64_t r0, int64_t r1, const double* _
     #pragma unroll 1
     for (int r = 0; r < rows; ++r) {
 #pragma unroll
-      for (int j = 0; j < J; ++j) acc[j] = fma(Xs[r * p + oa[j]], Ys[r * q + oc[j]], acc[j]);
+      for (int j = 0; j < J; ++j) {
+        const double xv = oa[j] < p ? Xs[r * p + oa[j]] : Ys[r * q + (oa[j] - p)];
+        acc[j] = fma(xv, Ys[r * q + oc[j]], acc[j]);
+      }
     }
   }
 }
-
 template <int J>
 __device__ __forceinline__ void store_partial(double* __restrict__ part, int pq, const double (&acc)[J]) {
   double* out = part + (int64_t)blockIdx.x * pq;
@@ -406,7 +409,8 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
                                                       double* __restrict__ W, int64_t ldw, double* __restrict__ Ews,
                                                       double* __restrict__ part, const double* __restrict__ Qh,
                                                       int64_t ldq, int hp, double* __restrict__ Hout, int64_t ldh,
-                                                      LamCoef lc, const double* __restrict__ Eg, int64_t ldg) {
+                                                      LamCoef lc, const double* __restrict__ Eg, int64_t ldg,
+                                                      double* __restrict__ Gout) {
   extern __shared__ double sm[];
   __shared__ double dsh[kMaxLowrank];
   phase_mark(20);
@@ -483,14 +487,23 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
   if (Hout) {
     // H[0:hp, :] = Q[:, 0:hp]^T W over this CTA's rows (W just written), reduced across the grid
     __syncthreads();
+    // (Gout: W^T W rides along as b more rows of the same reduction -- with H's rows, which are
+    // Q^T W, it is what the first Pythagorean round of the next block's orthonormalisation needs)
     double acc2[J2];
-    xty_rows<J2>(r0, r1, Qh, ldq, hp, W, ldw, b, sm, acc2);
-    store_partial<J2>(part, hp * b, acc2);  // E partials were consumed before the previous grid.sync
+    const int hpe = Gout ? hp + b : hp;
+    xty_rows<J2>(r0, r1, Qh, ldq, hp, W, ldw, b, sm, acc2, Gout != nullptr);
+    store_partial<J2>(part, hpe * b, acc2);  // E partials were consumed before the previous grid.sync
     cg::grid_group grid = cg::this_grid();
     phase_mark(24);
     grid.sync();
     phase_mark(25);
-    reduce_partials(part, hp * b, b, Hout, ldh, nullptr, 1.0);
+    grid_reduce_outputs(
+        hpe * b, [&](int o) { return PartRef{part, hpe * b, o}; },
+        [&](int o, double v) {
+          const int a = o / b, c = o - a * b;
+          if (a < hp) Hout[(int64_t)a * ldh + c] = v;
+          else Gout[(a - hp) * b + c] = v;
+        });
   }
   phase_mark(26);
 }
@@ -507,11 +520,14 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
 // flagged and refilled with the seeded normals of the same counters.
 
 __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* __restrict__ Q, int64_t ldq, int cols,
-                                                     double* __restrict__ W, int64_t ldw, int q, double thresh1,
+                                                     const double* Wsrc, int64_t lds, double* W, int64_t ldw, int q,
+                                                     double thresh1,
                                                      uint64_t key, uint64_t base, double* __restrict__ part,
                                                      double* __restrict__ Cws, double* __restrict__ Gws,
                                                      double* __restrict__ Rinv, int* __restrict__ mask,
-                                                     double* __restrict__ Rrel, int cgs_rounds, int pip) {
+                                                     double* __restrict__ Rrel, int cgs_rounds, int pip,
+                                                     const double* __restrict__ Cpre, int64_t ldcp,
+                                                     const double* __restrict__ Gpre) {
   extern __shared__ double sm[];
   phase_mark(50);
   cg::grid_group grid = cg::this_grid();
@@ -530,9 +546,11 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
     const int r = idx / cols, k = idx - r * cols;
     Qs[idx] = Q[(r0 + r) * ldq + k];
   }
+  // the block is read from Wsrc (the image block A Q_j of the previous pass) and the orthonormal
+  // block is written to W (its place in the basis): no copy launch in between
   for (int idx = t; idx < rows * q; idx += kCT) {
     const int r = idx / q, c = idx - r * q;
-    Ws[idx] = W[(r0 + r) * ldw + c];
+    Ws[idx] = Wsrc[(r0 + r) * lds + c];
   }
   __syncthreads();
   phase_mark(51);
@@ -638,10 +656,16 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
   double* Rinv_s = Gs + q * q;                                // q x q
   double* Rrel_s = Rinv_s + q * q;                            // q x q (unused factor output)
   int* mask_s = reinterpret_cast<int*>(Rrel_s + q * q);       // q
-  auto pip_round = [&](double thresh) -> bool {
+  auto pip_round = [&](double thresh, bool pre) -> bool {
     const int pq = cols * q, qq = q * q, tot = pq + qq;
     const int na4 = (cols + 3) / 4, nq4 = (q + 3) / 4;
     double* mypart = part + (int64_t)blockIdx.x * tot;
+    // pre: C = Q^T W and G = W^T W were already reduced (by the finish of the pass that produced W)
+    if (pre) {
+      for (int o = t; o < pq; o += kCT) Cs[o] = __ldcg(Cpre + (int64_t)(o / q) * ldcp + (o - (o / q) * q));
+      for (int o = t; o < qq; o += kCT) Gs[o] = __ldcg(Gpre + o);
+      pm += 2;
+    } else {
     for (int item = t; item < (na4 + nq4) * q; item += kCT) {
       const int grp4 = item / q, c = item - grp4 * q;
       const bool isq = grp4 < na4;
@@ -672,6 +696,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
     phase_mark(pm++);
     for (int o = t; o < pq; o += kCT) Cs[o] = __ldcg(Cws + o);
     for (int o = t; o < qq; o += kCT) Gs[o] = __ldcg(Gws + o);
+    }
     __syncthreads();
     // G' = G - C^T C (upper triangle; the lower is mirrored by block_cholesky) and the kept share of
     // every column's squared norm
@@ -741,8 +766,8 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
   };
   bool done = false;
   if (pip && cols > 0 && cgs_rounds == 2) {
-    if (pip_round(thresh1)) {
-      done = pip_round(0.0);
+    if (pip_round(thresh1, Cpre != nullptr && Gpre != nullptr)) {
+      done = pip_round(0.0, false);
     } else {
       // the round's C = Q^T W is the first CGS projection: apply it (Cs holds it), no second reduction
       const int nc4 = (q + 3) / 4;
@@ -874,7 +899,12 @@ void coop_cholqr(const Launch& L, int64_t n, const double* Wsrc, int64_t lds, do
 
 bool coop_orth(const Launch& L, int64_t n, const double* Q, int64_t ldq, int cols, double* W, int64_t ldw, int q,
                double thresh1, uint64_t key, uint64_t base, double* part, double* Cws, double* Gws, double* Rinv,
-               int* mask, double* Rrel, int sm_count, int cgs_rounds) {
+               int* mask, double* Rrel, int sm_count, int cgs_rounds, const double* Wsrc, int64_t lds,
+               const double* Cpre, int64_t ldcp, const double* Gpre) {
+  if (!Wsrc) {
+    Wsrc = W;
+    lds = ldw;
+  }
   static const bool off = getenv("MEGB200_NO_ORTH_FUSED") != nullptr;  // diagnostics: the five-launch path
   const int G = coop_grid(n, sm_count);
   const int R = (int)((n + G - 1) / G);
@@ -888,27 +918,28 @@ bool coop_orth(const Launch& L, int64_t n, const double* Q, int64_t ldq, int col
   if (first_on_device(&a)) {
     raise_smem(k_coop_orth, 200 * 1024);
   }
-  coop_launch(L, k_coop_orth, G, smem, n, Q, ldq, cols, W, ldw, q, thresh1, key, base, part, Cws, Gws, Rinv, mask,
-              Rrel, cgs_rounds, pip);
+  coop_launch(L, k_coop_orth, G, smem, n, Q, ldq, cols, Wsrc, lds, W, ldw, q, thresh1, key, base, part, Cws, Gws, Rinv,
+              mask, Rrel, cgs_rounds, pip, Cpre, ldcp, Gpre);
   return true;
 }
 
 void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, double scale, const double* Lf,
                  int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
                  int64_t ldw, double* Ews, double* part, int sm_count, const double* Qh, int64_t ldq, int hp,
-                 double* Hout, int64_t ldh, LamCoef lc, const double* Eg, int64_t ldg) {
+                 double* Hout, int64_t ldh, LamCoef lc, const double* Eg, int64_t ldg, double* Gout) {
+  if (!Hout) Gout = nullptr;
   if (lc.lam && (l > kMaxLowrank || lc.lr > l)) throw Error(MEGB200_ERR_PARAM, "finish: coefficient width out of range");
   const int G = coop_grid(n, sm_count);
   const size_t smem = std::max({(size_t)kRC * (l + b), (size_t)std::max(1, l * b) + (size_t)kRC * l,
                                 (size_t)kRC * (hp + b)}) * sizeof(double);
   const int J = pick_j(std::max(1, l * b));
-  const int J2 = Hout ? pick_j(hp * b) : 1;
+  const int J2 = Hout ? pick_j((hp + (Gout ? b : 0)) * b) : 1;
 #define MEG_FIN2(jj, j2)                                                                                        \
   {                                                                                                             \
     static char a = 0;                                                                                      \
     if (first_on_device(&a)) raise_smem(k_coop_finish<jj, j2>, kCoopSmem);                                         \
     coop_launch(L, k_coop_finish<jj, j2>, G, smem, n, b, S, spart, scale, Lf, ldl, l, d, alpha, U, ldu, W, ldw,  \
-                Ews, part, Qh, ldq, hp, Hout, ldh, lc, Eg, ldg);                                                \
+                Ews, part, Qh, ldq, hp, Hout, ldh, lc, Eg, ldg, Gout);                                          \
   }
 #define MEG_FIN(jj)                                            \
   switch (J2) {                                                \

@@ -145,7 +145,8 @@ void coop_cholqr(const Launch& L, int64_t n, const double* Wsrc, int64_t lds, do
 // (q > 32 or the staged rows exceed shared memory): the caller then runs the separate launches.
 bool coop_orth(const Launch& L, int64_t n, const double* Q, int64_t ldq, int cols, double* W, int64_t ldw, int q,
                double thresh1, uint64_t key, uint64_t base, double* part, double* Cws, double* Gws, double* Rinv,
-               int* mask, double* Rrel, int sm_count, int cgs_rounds);
+               int* mask, double* Rrel, int sm_count, int cgs_rounds, const double* Wsrc = nullptr, int64_t lds = 0,
+               const double* Cpre = nullptr, int64_t ldcp = 0, const double* Gpre = nullptr);
 // Log-map coefficients of a factored iterate computed on the device (so a step
 // can consume the kept weights lam another launch left in device memory):
 // d[k] = log(c1 lam[k]) - log_tail - eta (c1 lam[k] - tail_g) for k < lr.
@@ -162,7 +163,8 @@ void coop_finish(const Launch& L, int64_t n, int b, int S, const double* spart, 
                  int64_t ldl, int l, const double* d, double alpha, const double* U, int64_t ldu, double* W,
                  int64_t ldw, double* Ews, double* part, int sm_count, const double* Qh = nullptr, int64_t ldq = 0,
                  int hp = 0, double* Hout = nullptr, int64_t ldh = 0, LamCoef lc = LamCoef(),
-                 const double* Eg = nullptr, int64_t ldg = 0);  // Eg: precomputed L^T U (skips its reduction)
+                 const double* Eg = nullptr, int64_t ldg = 0,  // Eg: precomputed L^T U (skips its reduction)
+                 double* Gout = nullptr);  // with Hout: also W^T W (b x b, ld b), in the same reduction
 // Jacobi RR + Ritz block + residuals (+ Gram of the first gr Ritz vectors, + MEG epilogue into epi);
 // the first r2 Ritz vectors are also written to V2
 void coop_rr(const Launch& L, const double* H, int64_t ldh, int m, double* theta, double* S, double* info, int64_t n,

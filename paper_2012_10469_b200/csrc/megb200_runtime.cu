@@ -56,6 +56,11 @@ struct megb200_solver {
   // grid limit of the multi-pass solver's cooperative kernels: sm_count, or sm_count - 1 while a solve
   // overlaps its wide Rayleigh-Ritz (one CTA on the side stream) with the next block's work
   int coop_sm = 148;
+  // Q^T W (a column block of H) and W^T W left by the finish of the last block pass, for the
+  // orthonormalisation of W as the next Krylov block (block_pass / orthonormalize)
+  bool pre_valid = false;
+  const double *pre_src = nullptr, *pre_c = nullptr, *pre_g = nullptr;
+  int pre_cols = 0, pre_q = 0;
   cudaStream_t stream = nullptr;
   // side stream of the overlapped wide Rayleigh-Ritz (top_eigs), forked / joined with events
   cudaStream_t side = nullptr;
@@ -341,12 +346,12 @@ int pass_launch(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu
 }
 
 void apply_op(megb200_solver* s, const OpDev& op, const double* U, int64_t ldu, int k, double* W, int64_t ldw,
-              int hp = 0, double* Hout = nullptr) {
+              int hp = 0, double* Hout = nullptr, double* Gout = nullptr) {
   Launch L = s->launch();
   const int S = pass_launch(s, op, U, ldu, k);
   if (op.lc.lam == s->dlam) s->flush_dlam();
   coop_finish(L, s->n, k, S, s->part, op.scale, op.L, op.ldl, op.l, op.d_dev, op.alpha, U, ldu, W, ldw, s->E, s->red,
-              s->coop_sm, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap, op.lc, op.Eg, op.ldg);
+              s->coop_sm, Hout ? s->Q : nullptr, s->ldq, hp, Hout, s->cap, op.lc, op.Eg, op.ldg, Gout);
 }
 
 // columns k > 64 are applied in chunks (re-streams the operand; not used by the configs)
@@ -397,14 +402,22 @@ OpDev op_from_public(megb200_solver* s, const megb200_operator* op) {
 // the relation factor Rn = R2 R1 (W_in - Q C = W_out Rn) is formed.
 
 void orthonormalize(megb200_solver* s, double* W, int64_t ldw, int q, int cols, double scale, uint64_t key,
-                    uint64_t& refill_ctr, bool want_relation, int cgs_rounds = 2) {
+                    uint64_t& refill_ctr, bool want_relation, int cgs_rounds = 2, const double* src = nullptr,
+                    int64_t lds = 0) {
   Launch L = s->launch();
   const int64_t n = s->n;
+  // src: the block to orthonormalise lives elsewhere (the image block of the previous pass); the fused
+  // kernel reads it there and writes W, the fallback copies it first
+  // the finish of the pass that produced src already reduced Q^T src and src^T src (block_pass)
+  const bool pre = s->pre_valid && src && src == s->pre_src && cols == s->pre_cols && q == s->pre_q && lds == s->ldq;
+  s->pre_valid = false;
   if (!want_relation && coop_orth(L, n, s->Q, s->ldq, cols, W, ldw, q, 1e-13 * scale, key, refill_ctr, s->red, s->C2,
-                                  s->G, s->Rinv, s->mask, s->Rtmp, s->coop_sm, cgs_rounds)) {
+                                  s->G, s->Rinv, s->mask, s->Rtmp, s->coop_sm, cgs_rounds, src, lds,
+                                  pre ? s->pre_c : nullptr, s->cap, pre ? s->pre_g : nullptr)) {
     refill_ctr += 2 * (uint64_t)n * q;
     return;
   }
+  if (src) copy_block(L, n, q, src, lds, W, ldw);
   for (int round = 0; round < cgs_rounds && cols > 0; ++round)
     coop_cgs(L, n, s->Q, s->ldq, cols, W, ldw, q, s->C2, s->red, s->coop_sm);
   coop_cholqr(L, n, W, ldw, W, ldw, q, 1e-13 * scale, s->G, s->R1, s->Rinv, s->mask, nullptr, nullptr, key,
@@ -543,9 +556,19 @@ EigShape eig_shape(const megb200_solver* s, int nreq, const EigParams& P) {
 // One operator pass on the block Q[:, cols:cols+cur] into AQ, and its column of H = Q^T A Q.
 void block_pass(megb200_solver* s, const OpDev& op, int cols, int cur) {
   Launch L = s->launch();
+  s->pre_valid = false;
   if (cur <= 32) {
-    // pass + epilogue; the epilogue launch also reduces the H column Q^T (A Q_j)
-    apply_op(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq, cols + cur, s->H + cols);
+    // pass + epilogue; the epilogue launch also reduces the H column Q^T (A Q_j) and, in the same
+    // reduction, the image block's Gram: together the first Pythagorean round of the orthonormalisation
+    // of the next Krylov block (which is this image block) needs no reduction of its own
+    double* gpre = s->small + 2048;  // 32 x 32
+    apply_op(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq, cols + cur, s->H + cols, gpre);
+    s->pre_valid = true;
+    s->pre_src = s->AQ + cols;
+    s->pre_c = s->H + cols;
+    s->pre_g = gpre;
+    s->pre_cols = cols + cur;
+    s->pre_q = cur;
   } else {
     apply_op_wide(s, op, s->Q + cols, s->ldq, cur, s->AQ + cols, s->ldq);
     coop_tn(L, s->n, s->Q, s->ldq, cols + cur, s->AQ + cols, s->ldq, cur, s->H + cols, s->cap, nullptr, 1.0, s->red,
@@ -884,8 +907,8 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
         MEG_CUDA(cudaEventRecord(s->ev_join, s->side));
         for (int l = 0; l < lag; ++l) {
           const int cl = cols + l * bw;  // the block whose image seeds the next one
-          copy_block(L, n, bw, s->AQ + cl, s->ldq, s->Q + cl + bw, s->ldq);
-          orthonormalize(s, s->Q + cl + bw, s->ldq, bw, cl + bw, scale, key_refill, refill_ctr, false);
+          orthonormalize(s, s->Q + cl + bw, s->ldq, bw, cl + bw, scale, key_refill, refill_ctr, false, 2, s->AQ + cl,
+                         s->ldq);
           block_pass(s, op, cl + bw, bw);
         }
         s->mark("spec orth+pass");
@@ -1008,12 +1031,14 @@ EigRun top_eigs(megb200_solver* s, const OpDev& op, int nreq, const EigParams& P
     }
     // next Krylov block: the image block orthogonalised against the basis
     if (nxt == cur) {
-      copy_block(L, n, cur, s->AQ + cols, s->ldq, s->Q + newcols, s->ldq);
+      // the image block, read in place by the orthonormalisation kernel
+      orthonormalize(s, s->Q + newcols, s->ldq, nxt, newcols, scale, key_refill, refill_ctr, false, 2, s->AQ + cols,
+                     s->ldq);
     } else {
       fill_gaussian(L, n, nxt, key_refill, refill_ctr, 1.0, false, s->Q + newcols, s->ldq);
       refill_ctr += (uint64_t)n * nxt;
+      orthonormalize(s, s->Q + newcols, s->ldq, nxt, newcols, scale, key_refill, refill_ctr, false);
     }
-    orthonormalize(s, s->Q + newcols, s->ldq, nxt, newcols, scale, key_refill, refill_ctr, false);
     s->mark("orth_next");
     cols = newcols;
     if (full) {
