@@ -1,5 +1,6 @@
 // Wide Rayleigh-Ritz (m = 49..112, the restarted block Krylov basis of the
-// multi-pass solves, linalg.py:205-211) by one CTA of 1024 threads:
+// multi-pass solves, linalg.py:205-211) by one CTA of 512 threads (1024 measured 11 % slower: the
+// phases are latency chains, more warps only add barrier and issue contention):
 //
 //   1. Householder tridiagonalisation H = Q T Q^T (LAPACK dsytd2 'L' scheme:
 //      per column one norm, one symmetric matvec, one rank-2 update);
@@ -38,7 +39,10 @@
 namespace megb200 {
 namespace {
 
-constexpr int kRT = 1024;           // threads
+#ifndef MEG_RR_THREADS
+#define MEG_RR_THREADS 512
+#endif
+constexpr int kRT = MEG_RR_THREADS;  // threads
 constexpr int kNW = kRT / 32;       // warps
 constexpr int kLanesPerEig = 8;     // multisection lanes per eigenvalue
 constexpr int kBisectRounds = 18;   // 9^18 > 1e17
@@ -255,8 +259,9 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
       continue;
     }
     // p = tau A22 v and the shares of p^T v: eight threads per row (128 rows per sweep)
-    {
-      const int rr = t >> 3, k0 = t & 7;
+    double pvs = 0.0;
+    for (int rr0 = 0; rr0 < L; rr0 += kRT >> 3) {
+      const int rr = rr0 + (t >> 3), k0 = t & 7;
       double acc = 0.0;
       if (rr < L) {
         const double* row = A + (j + 1 + rr) * la + (j + 1);
@@ -276,24 +281,23 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
       acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      double pvs = 0.0;
       if (rr < L && k0 == 0) {
         const double pi = tj * acc;
         p[rr] = pi;
-        pvs = pi * v[rr];
+        pvs = fma(pi, v[rr], pvs);
       }
-      pvs += __shfl_xor_sync(0xffffffffu, pvs, 8);
-      pvs += __shfl_xor_sync(0xffffffffu, pvs, 16);
-      if (lane == 0) wp[w] = pvs;
     }
+    pvs += __shfl_xor_sync(0xffffffffu, pvs, 8);
+    pvs += __shfl_xor_sync(0xffffffffu, pvs, 16);
+    if (lane == 0) wp[w] = pvs;
     __syncthreads();
     double K = 0.0;
 #pragma unroll 8
     for (int k = 0; k < kNW; ++k) K += wp[k];
     K *= 0.5 * tj;
     // A22 -= v w^T + w v^T with w = p - K v: eight threads per row
-    {
-      const int rr = t >> 3, k0 = t & 7;
+    for (int rr0 = 0; rr0 < L; rr0 += kRT >> 3) {
+      const int rr = rr0 + (t >> 3), k0 = t & 7;
       if (rr < L) {
         const double vi = v[rr], wi = p[rr] - K * vi;
         double* row = A + (j + 1 + rr) * la + (j + 1);
