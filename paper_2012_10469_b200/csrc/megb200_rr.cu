@@ -213,6 +213,12 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
   //      A22 -= v w^T + w v^T (w = p - K v on the fly) runs eight threads per row.
   for (int j = 0; j < m - 2; ++j) {
     const int L = m - j - 1;
+#ifdef MEG_RR_CLOCKS
+#define RRCLK(s_) if (j == 10 && t == 0) g_rr_ns[8 + s_] = clock64();
+#else
+#define RRCLK(s_)
+#endif
+    RRCLK(0)
     if (w == 0) {
       double xr[4];
       double s = 0.0;
@@ -252,71 +258,95 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
         sc[0] = tj;
       }
     }
+    RRCLK(1)
     __syncthreads();
+    RRCLK(2)
     const double tj = sc[0];
     if (tj == 0.0) {  // uniform; the barrier keeps warp 0's next write of sc[0] behind every read
       __syncthreads();
       continue;
     }
-    // p = tau A22 v and the shares of p^T v: eight threads per row (128 rows per sweep)
+    // p = tau A22 v and the shares of p^T v: sixteen threads per row -- a warp reads two rows of 16
+    // consecutive doubles (two conflict-free wavefronts) -- with the thread's seven entries of v held
+    // in registers for all of its rows (the loads of the row entries are the only shared-memory
+    // traffic: this phase and the update are bound by shared-memory wavefronts, not by latency)
+    constexpr int kTPR = 16, kEnt = 7;  // threads per row, entries per thread (16 * 7 = 112 >= m)
+    const int k0 = t & (kTPR - 1);
+    double vk[kEnt];
+#pragma unroll
+    for (int it = 0; it < kEnt; ++it) {
+      const int k = k0 + kTPR * it;
+      vk[it] = k < L ? v[k] : 0.0;
+    }
     double pvs = 0.0;
-    for (int rr0 = 0; rr0 < L; rr0 += kRT >> 3) {
-      const int rr = rr0 + (t >> 3), k0 = t & 7;
+    constexpr int kSweeps = (112 * kTPR + kRT - 1) / kRT;  // row sweeps, unrolled: their loads and shuffles overlap
+#pragma unroll
+    for (int sw = 0; sw < kSweeps; ++sw) {
+      const int rr = sw * (kRT / kTPR) + t / kTPR;
+      if (sw * (kRT / kTPR) >= L) break;  // uniform
       double acc = 0.0;
       if (rr < L) {
         const double* row = A + (j + 1 + rr) * la + (j + 1);
-        // fixed trip count (m <= 112: at most 14 entries per thread), fully unrolled so the
-        // shared-memory loads of all entries are in flight together
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-        for (int it = 0; it < 7; ++it) {
-          const int k = k0 + 16 * it;
-          const double x0 = k < L ? row[k] : 0.0, y0 = k < L ? v[k] : 0.0;
-          const double x1 = k + 8 < L ? row[k + 8] : 0.0, y1 = k + 8 < L ? v[k + 8] : 0.0;
-          a0 = fma(x0, y0, a0);
-          a1 = fma(x1, y1, a1);
+        for (int it = 0; it < kEnt; ++it) {
+          const int k = k0 + kTPR * it;
+          const double x = k < L ? row[k] : 0.0;
+          if (it & 1) a1 = fma(x, vk[it], a1);
+          else a0 = fma(x, vk[it], a0);
         }
         acc = a0 + a1;
       }
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
       acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 8);
       if (rr < L && k0 == 0) {
         const double pi = tj * acc;
         p[rr] = pi;
         pvs = fma(pi, v[rr], pvs);
       }
     }
-    pvs += __shfl_xor_sync(0xffffffffu, pvs, 8);
     pvs += __shfl_xor_sync(0xffffffffu, pvs, 16);
     if (lane == 0) wp[w] = pvs;
+    RRCLK(3)
     __syncthreads();
+    RRCLK(4)
     double K = 0.0;
 #pragma unroll 8
     for (int k = 0; k < kNW; ++k) K += wp[k];
     K *= 0.5 * tj;
-    // A22 -= v w^T + w v^T with w = p - K v: eight threads per row
-    for (int rr0 = 0; rr0 < L; rr0 += kRT >> 3) {
-      const int rr = rr0 + (t >> 3), k0 = t & 7;
+    RRCLK(5)
+    // A22 -= v w^T + w v^T with w = p - K v: sixteen threads per row, the thread's entries of v and w
+    // in registers (one load and one store per matrix entry)
+    double wk[kEnt];
+#pragma unroll
+    for (int it = 0; it < kEnt; ++it) {
+      const int k = k0 + kTPR * it;
+      wk[it] = k < L ? p[k] - K * vk[it] : 0.0;
+    }
+#pragma unroll 1
+    for (int sw = 0; sw < kSweeps; ++sw) {
+      const int rr = sw * (kRT / kTPR) + t / kTPR;
       if (rr < L) {
         const double vi = v[rr], wi = p[rr] - K * vi;
         double* row = A + (j + 1 + rr) * la + (j + 1);
-        double nv[14];
+        double nv[kEnt];
 #pragma unroll
-        for (int it = 0; it < 14; ++it) {
-          const int k = k0 + 8 * it;
-          const bool in = k < L;
-          const double vk = in ? v[k] : 0.0, pk = in ? p[k] : 0.0, ak = in ? row[k] : 0.0;
-          nv[it] = ak - fma(vi, pk - K * vk, wi * vk);
+        for (int it = 0; it < kEnt; ++it) {
+          const int k = k0 + kTPR * it;
+          nv[it] = (k < L ? row[k] : 0.0) - fma(vi, wk[it], wi * vk[it]);
         }
 #pragma unroll
-        for (int it = 0; it < 14; ++it) {
-          const int k = k0 + 8 * it;
+        for (int it = 0; it < kEnt; ++it) {
+          const int k = k0 + kTPR * it;
           if (k < L) row[k] = nv[it];
         }
       }
     }
+    RRCLK(6)
     __syncthreads();
+    RRCLK(7)
   }
   if (t == 0) {
     if (m >= 2) {
@@ -442,22 +472,22 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
       auto vat = [&](int row, int q) -> double {
         return row < q ? 0.0 : (row == q ? 1.0 : A[(j0 + 1 + row) * la + j0 + q]);
       };
-      // W1[q][c] = sum_rows V[row][q] Z[j0+1+row][c]: warp per column c
-      for (int c = w; c < nvec; c += kNW) {
-        double acc[kWY];
-#pragma unroll
-        for (int q = 0; q < kWY; ++q) acc[q] = 0.0;
-        for (int row = lane; row < L0; row += 32) {
-          const double z = Z[(j0 + 1 + row) * m + c];
-#pragma unroll
-          for (int q = 0; q < kWY; ++q)
-            if (q < P) acc[q] = fma(vat(row, q), z, acc[q]);
+      // W1[q][c] = sum_rows V[row][q] Z[j0+1+row][c]: a thread per (q, c) runs down the rows in four
+      // independent chains (neighbouring threads take neighbouring c: conflict-free Z rows, broadcast V
+      // entries) -- no warp reductions (a warp per column spent 80 shuffles per column and block, and one
+      // SM issues about one shuffle per cycle)
+      for (int o = t; o < P * nvec; o += kRT) {
+        const int q = o / nvec, c = o - q * nvec;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int row = q;  // V[row][q] = 0 above the reflector's unit entry
+        for (; row + 3 < L0; row += 4) {
+          a0 = fma(vat(row, q), Z[(j0 + 1 + row) * m + c], a0);
+          a1 = fma(vat(row + 1, q), Z[(j0 + 2 + row) * m + c], a1);
+          a2 = fma(vat(row + 2, q), Z[(j0 + 3 + row) * m + c], a2);
+          a3 = fma(vat(row + 3, q), Z[(j0 + 4 + row) * m + c], a3);
         }
-#pragma unroll
-        for (int q = 0; q < kWY; ++q) {
-          const double v = wsum(acc[q]);
-          if (lane == 0 && q < P) W1[q * nvec + c] = v;
-        }
+        for (; row < L0; ++row) a0 = fma(vat(row, q), Z[(j0 + 1 + row) * m + c], a0);
+        W1[q * nvec + c] = (a0 + a1) + (a2 + a3);
       }
       // Gv = V^T V: warp q' < P computes row q' (lanes over rows)
       if (w < P) {
