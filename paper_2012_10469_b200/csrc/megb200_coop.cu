@@ -24,6 +24,11 @@ namespace megb200 {
 // Optional phase timestamps (compile with -DMEG_PHASE_TIMING): CTA 0 thread 0
 // records %globaltimer at phase boundaries of the cooperative kernels.
 __device__ unsigned long long g_phase_ns[64];
+#ifdef MEG_PHASE_TIMING
+#define PIPCLK(i_) if (blockIdx.x == 0 && threadIdx.x == 0) g_phase_ns[32 + (i_)] = clock64();
+#else
+#define PIPCLK(i_)
+#endif
 __device__ __forceinline__ void phase_mark(int slot) {
 #ifdef MEG_PHASE_TIMING
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -209,6 +214,7 @@ __device__ void block_cholesky(const double* __restrict__ Gg, int q, double thre
                                double* pivot_min = nullptr) {
   const int t = threadIdx.x, nth = blockDim.x;
   const int ld = q + 1;
+  PIPCLK(8)
   double pmin = 1.0;  // smallest equilibrated pivot (every thread tracks it from shared memory)
   double* A = sm;             // q x ld   (factorised in place: upper triangle -> Rs)
   double* X = sm + q * ld;    // q x ld   (Rs^-1)
@@ -225,6 +231,7 @@ __device__ void block_cholesky(const double* __restrict__ Gg, int q, double thre
     const double g = A[i * ld + i];
     bad[i] = !(g > thresh * thresh);
     D[i] = bad[i] ? 1.0 : sqrt(g);
+    X[i * ld + q] = 1.0 / D[i];  // padding column of X: used for R^-1's row scaling at the end
   }
   __syncthreads();
   for (int idx = t; idx < q * q; idx += nth) {
@@ -236,45 +243,81 @@ __device__ void block_cholesky(const double* __restrict__ Gg, int q, double thre
   // column step is a few hundred cycles, which CTA-wide barriers and a one-thread pivot dominated --
   // 22 us at q = 18).  Every lane forms the pivot (reciprocal square root, r = d * rsqrt(d)); lane l
   // owns column l of the trailing update and of R^-1 (no barrier inside a column's back substitution).
+  PIPCLK(9)
   if (t < 32) {
     const int lane = t;
-    for (int j = 0; j < q; ++j) {
-      const double d = A[j * ld + j];
-      const bool bj = bad[j] || !(d > 1e-20);
+    // left-looking by rows of R: in step k every lane l >= k forms s_l = A[k][l] - sum_{i<k} R[i][k] R[i][l]
+    // (a dot product over finished entries: its loads pipeline, nothing is read back after a store
+    // inside the loop -- the right-looking update's read-modify-write chains cost ~2000 cycles per
+    // column), the pivot s_k is broadcast, R[k][l] = s_l / sqrt(s_k).  Same subtraction order per entry
+    // as the right-looking form.  One warp barrier per step.
+    double pm = 1.0;
+    for (int k = 0; k < q; ++k) {
+      double sv[2] = {0.0, 0.0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int l = lane + 32 * h;
+        if (l >= k && l < q) {
+          // two chains (even / odd i): the float64 multiply-add latency, not its rate, bounds this loop
+          double s0 = A[k * ld + l], s1 = 0.0;
+          int i = 0;
+#pragma unroll 4
+          for (; i + 1 < k; i += 2) {
+            s0 = fma(-A[i * ld + k], A[i * ld + l], s0);
+            s1 = fma(-A[(i + 1) * ld + k], A[(i + 1) * ld + l], s1);
+          }
+          if (i < k) s0 = fma(-A[i * ld + k], A[i * ld + l], s0);
+          sv[h] = s0 + s1;
+        }
+      }
+      const double d = __shfl_sync(0xffffffffu, (k >> 5) ? sv[1] : sv[0], k & 31);
+      const bool bj = bad[k] || !(d > 1e-20);
+      pm = bj ? 0.0 : fmin(pm, d);
+      // (the step is a ~800-cycle chain of dependent float64 operations -- dot, broadcast, reciprocal
+      // square root, scale, store -- whichever reciprocal square root is used)
       const double ir = bj ? 1.0 : rsqrt(d);
       const double r = bj ? 1.0 : d * ir;
-      for (int k = j + 1 + lane; k < q; k += 32) A[j * ld + k] = bj ? 0.0 : A[j * ld + k] * ir;
-      __syncwarp();
-      if (lane == 0) {
-        bad[j] = bj;
-        A[j * ld + j] = r;
-        rd[j] = ir;
-      }
-      for (int l = j + 1 + lane; l < q; l += 32) {
-        const double ajl = A[j * ld + l];
-        for (int k = j + 1; k <= l; ++k) A[k * ld + l] -= A[j * ld + k] * ajl;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int l = lane + 32 * h;
+        if (l == k) {
+          A[k * ld + k] = r;
+          rd[k] = ir;
+          bad[k] = bj;
+        } else if (l > k && l < q) {
+          A[k * ld + l] = bj ? 0.0 : sv[h] * ir;
+        }
       }
       __syncwarp();
     }
+    if (lane == 0) A[q] = pm;  // smallest pivot, in the padding column of row 0
+    PIPCLK(10)
     // Rs^-1 by columns: X[i][c] = -rd_i * sum_{k=i+1..c} Rs[i][k] X[k][c], X[c][c] = rd_c
     for (int c = lane; c < q; c += 32) {
       X[c * ld + c] = rd[c];
       for (int i = c - 1; i >= 0; --i) {
-        double s = 0.0;
-        for (int k = i + 1; k <= c; ++k) s = fma(A[i * ld + k], X[k * ld + c], s);
-        X[i * ld + c] = -s * rd[i];
+        double s0 = 0.0, s1 = 0.0;
+        int k = i + 1;
+#pragma unroll 4
+        for (; k + 1 <= c; k += 2) {
+          s0 = fma(A[i * ld + k], X[k * ld + c], s0);
+          s1 = fma(A[i * ld + k + 1], X[(k + 1) * ld + c], s1);
+        }
+        if (k <= c) s0 = fma(A[i * ld + k], X[k * ld + c], s0);
+        X[i * ld + c] = -(s0 + s1) * rd[i];
       }
     }
   }
+  PIPCLK(11)
   __syncthreads();
-  pmin = 1.0;
-  for (int j = 0; j < q; ++j) pmin = bad[j] ? 0.0 : fmin(pmin, 1.0 / (rd[j] * rd[j]));
+  pmin = A[q];
   for (int idx = t; idx < q * q; idx += nth) {
     const int i = idx / q, j = idx - i * q;
-    Rinv[idx] = (i <= j) ? X[i * ld + j] / D[i] : 0.0;
+    Rinv[idx] = (i <= j) ? X[i * ld + j] * X[i * ld + q] : 0.0;  // 1 / D_i from the padding column
     Rrel[idx] = (bad[i] || j < i) ? 0.0 : A[i * ld + j] * D[j];
   }
   for (int i = t; i < q; i += nth) mask[i] = bad[i];
+  PIPCLK(12)
   if (pivot_min) *pivot_min = pmin;
   if (Rtot) {
     for (int idx = t; idx < q * q; idx += nth) {
@@ -698,6 +741,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
     for (int o = t; o < qq; o += kCT) Gs[o] = __ldcg(Gws + o);
     }
     __syncthreads();
+    PIPCLK(0)
     // G' = G - C^T C (upper triangle; the lower is mirrored by block_cholesky) and the kept share of
     // every column's squared norm
     double keep_min = 1.0;
@@ -718,6 +762,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
       }
     }
     __syncthreads();
+    PIPCLK(1)
     for (int o = t; o < qq; o += kCT) {
       const int i = o / q, j = o - i * q;
       if (i <= j) Gs[o] = Rrel_s[o];
@@ -731,9 +776,11 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
     for (int wv = 0; wv < kCT / 32; ++wv) km = fmin(km, Rinv_s[wv]);
     __syncthreads();
     if (!(km >= 1e-11)) return false;  // uniform: every CTA reduced the same G and C
+    PIPCLK(2)
     double pmin = 1.0;
     block_cholesky(Gs, q, thresh, chol_sm, Rrel_s, Rinv_s, mask_s, nullptr, nullptr, &pmin);
     __syncthreads();
+    PIPCLK(3)
     bool okc = km * pmin >= 1e-12;  // error of the round ~ eps / (kept share x smallest pivot) <= 1e-4
     for (int c = 0; c < q; ++c) okc = okc && !mask_s[c];
     if (!okc) return false;  // uniform
@@ -754,6 +801,7 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
         if (c0 + u < q) W2[r * q + c0 + u] = Ws[r * q + c0 + u] - acc[u];
     }
     __syncthreads();
+    PIPCLK(4)
     for (int idx = t; idx < rows * q; idx += kCT) {
       const int r = idx / q, c = idx - r * q;
       double v = 0.0;

@@ -52,3 +52,8 @@ print("phases (last orth of the run), us:")
 for k in range(51, min(pm, 64)):
     print(f"  slot {k}: {(v[k] - v[k - 1]) / 1e3:8.2f}")
 print(f"  total 50 -> {pm}: {(v[min(pm, 63)] - v[50]) / 1e3:8.2f}")
+print("last Pythagorean round, CTA 0 thread 0, cycles: G' " + str(v[33] - v[32]) + ", kept-share min " + str(v[34] - v[33]) +
+      ", Cholesky + R^-1 " + str(v[35] - v[34]) + ", projection " + str(v[36] - v[35]) + ", (solve follows)")
+print("block_cholesky (last call), cycles: load + equilibrate " + str(v[41] - v[40]) + ", factorisation " + str(v[42] - v[41]) +
+      ", R^-1 " + str(v[43] - v[42]) + ", outputs " + str(v[44] - v[43]))
+
