@@ -56,4 +56,8 @@ print("last Pythagorean round, CTA 0 thread 0, cycles: G' " + str(v[33] - v[32])
       ", Cholesky + R^-1 " + str(v[35] - v[34]) + ", projection " + str(v[36] - v[35]) + ", (solve follows)")
 print("block_cholesky (last call), cycles: load + equilibrate " + str(v[41] - v[40]) + ", factorisation " + str(v[42] - v[41]) +
       ", R^-1 " + str(v[43] - v[42]) + ", outputs " + str(v[44] - v[43]))
+print("k_coop_finish (last launch), us: coefficients + L^T U partial " + f"{(v[21] - v[20]) / 1e3:.2f}" + ", reduce E " +
+      f"{(v[22] - v[21]) / 1e3:.2f}" + ", W rows " + f"{(v[23] - v[22]) / 1e3:.2f}" + ", H partial " +
+      f"{(v[24] - v[23]) / 1e3:.2f}" + ", grid barrier " + f"{(v[25] - v[24]) / 1e3:.2f}" + ", reduce H " +
+      f"{(v[26] - v[25]) / 1e3:.2f}")
 
