@@ -110,6 +110,78 @@ __device__ __forceinline__ void xty_rows(int64_t r0, int64_t r1, const double* _
     }
   }
 }
+// Register-tiled X^T Y over a CTA's rows (optionally with the q rows Y^T Y after the p rows of X^T Y):
+// a thread owns NT tiles of TA output rows x 4 consecutive output columns, so a staged row costs
+// TA + 4 shared-memory loads per 4 TA multiply-adds (the one-output-per-slot form above loads two
+// operands per multiply-add and is bound by shared-memory wavefronts: 30 us for cfg4's L^T U).
+// The partials land at their linear index a * q + c, as store_partial would put them.
+template <int TA, int NT>
+__device__ __forceinline__ void xty_rows_tiled_store(int64_t r0, int64_t r1, const double* __restrict__ X, int64_t ldx,
+                                                     int p, const double* __restrict__ Y, int64_t ldy, int q,
+                                                     double* sm, bool gram, double* __restrict__ part) {
+  double* Xs = sm;
+  double* Ys = sm + kRC * p;
+  const int pe = gram ? p + q : p;
+  const int ncg = (q + 3) / 4, nag = (pe + TA - 1) / TA, tiles = nag * ncg;
+  int ta[NT], tc[NT];
+  double acc[NT][TA][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const int tt = threadIdx.x + i * kCT;
+    ta[i] = tt < tiles ? (tt / ncg) * TA : -1;
+    tc[i] = tt < tiles ? (tt - (tt / ncg) * ncg) * 4 : 0;
+#pragma unroll
+    for (int v = 0; v < TA; ++v)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[i][v][u] = 0.0;
+  }
+  for (int64_t rc = r0; rc < r1; rc += kRC) {
+    const int rows = (int)min((int64_t)kRC, r1 - rc);
+    __syncthreads();
+    #pragma unroll 1
+    for (int idx = threadIdx.x; idx < rows * p; idx += kCT) {
+      const int r = idx / p, a = idx - r * p;
+      Xs[idx] = X[(rc + r) * ldx + a];
+    }
+    #pragma unroll 1
+    for (int idx = threadIdx.x; idx < rows * q; idx += kCT) {
+      const int r = idx / q, c = idx - r * q;
+      Ys[idx] = Y[(rc + r) * ldy + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      if (ta[i] < 0) continue;
+      #pragma unroll 2
+      for (int r = 0; r < rows; ++r) {
+        double y[4], xv[TA];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) y[u] = tc[i] + u < q ? Ys[r * q + tc[i] + u] : 0.0;
+#pragma unroll
+        for (int v = 0; v < TA; ++v) {
+          const int a = ta[i] + v;
+          xv[v] = a < p ? Xs[r * p + a] : (a < pe ? Ys[r * q + (a - p)] : 0.0);
+        }
+#pragma unroll
+        for (int v = 0; v < TA; ++v)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[i][v][u] = fma(xv[v], y[u], acc[i][v][u]);
+      }
+    }
+  }
+  double* out = part + (int64_t)blockIdx.x * pe * q;
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    if (ta[i] < 0) continue;
+#pragma unroll
+    for (int v = 0; v < TA; ++v)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int a = ta[i] + v, c = tc[i] + u;
+        if (a < pe && c < q) out[a * q + c] = acc[i][v][u];
+      }
+  }
+}
 template <int J>
 __device__ __forceinline__ void store_partial(double* __restrict__ part, int pq, const double (&acc)[J]) {
   double* out = part + (int64_t)blockIdx.x * pq;
@@ -477,9 +549,8 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
   if (Eg) {
     __syncthreads();  // E = diag(d) L^T U from the caller's L^T U (no grid reduction)
   } else if (l > 0) {
-    double acc[J];
-    xty_rows<J>(r0, r1, Lf, ldl, l, U, ldu, b, sm, acc);
-    store_partial<J>(part, l * b, acc);
+    if constexpr (J > 16) xty_rows_tiled_store<4, 2>(r0, r1, Lf, ldl, l, U, ldu, b, sm, false, part);
+    else xty_rows_tiled_store<2, 2>(r0, r1, Lf, ldl, l, U, ldu, b, sm, false, part);
     cg::grid_group grid = cg::this_grid();
     grid.sync();
     phase_mark(21);
@@ -532,10 +603,10 @@ __global__ void __launch_bounds__(kCT) k_coop_finish(int64_t n, int b, int S, co
     __syncthreads();
     // (Gout: W^T W rides along as b more rows of the same reduction -- with H's rows, which are
     // Q^T W, it is what the first Pythagorean round of the next block's orthonormalisation needs)
-    double acc2[J2];
     const int hpe = Gout ? hp + b : hp;
-    xty_rows<J2>(r0, r1, Qh, ldq, hp, W, ldw, b, sm, acc2, Gout != nullptr);
-    store_partial<J2>(part, hpe * b, acc2);  // E partials were consumed before the previous grid.sync
+    // (E partials were consumed before the previous grid.sync)
+    if constexpr (J2 > 16) xty_rows_tiled_store<4, 2>(r0, r1, Qh, ldq, hp, W, ldw, b, sm, Gout != nullptr, part);
+    else xty_rows_tiled_store<2, 2>(r0, r1, Qh, ldq, hp, W, ldw, b, sm, Gout != nullptr, part);
     cg::grid_group grid = cg::this_grid();
     phase_mark(24);
     grid.sync();
