@@ -2213,7 +2213,13 @@ int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_ho
     const bool io_overlap = vh0 < oh1 && oh0 < vh1;
     // (small factors only: a large one is not staged by the fused kernel and would be re-read
     // over the host link)
-    if (!io_overlap && x_host->ldv == r && n * r * (int64_t)sizeof(double) <= (2 << 20) && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
+    // and only for the gradients whose warm steps take ONE pass (dense targets): the sampled and
+    // stochastic gradients solve in 6-30 passes, each of which -- and the per-step sampled values --
+    // would re-read the factor over the host link (cfg3: 10.4 -> 6.5 ms per host-buffer step)
+    const bool one_pass_kind = g->kind == MEGB200_GRAD_ZERO || g->kind == MEGB200_GRAD_DENSE ||
+                               g->kind == MEGB200_GRAD_FROBENIUS;
+    if (!io_overlap && one_pass_kind && x_host->ldv == r && n * r * (int64_t)sizeof(double) <= (2 << 20) &&
+        getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&v_mapped), const_cast<double*>(x_host->V), 0) !=
             cudaSuccess) {
       cudaGetLastError();
@@ -2270,7 +2276,8 @@ int megb200_lowrank_meg_step_host(megb200_solver* s, const megb200_iterate* x_ho
     bool v_done = false;
     // a mapped pinned destination takes V_next straight from the kernels (no read-back copy)
     double* vn_mapped = nullptr;
-    if (!io_overlap && ld_next_host == r && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
+    // (one-pass gradients only: a multi-pass solve writes its Ritz vectors at every Rayleigh-Ritz)
+    if (!io_overlap && one_pass_kind && ld_next_host == r && getenv("MEGB200_NO_ZEROCOPY") == nullptr &&
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&vn_mapped), V_next_host, 0) != cudaSuccess) {
       cudaGetLastError();
       vn_mapped = nullptr;
