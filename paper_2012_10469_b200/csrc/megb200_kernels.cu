@@ -1827,18 +1827,33 @@ __global__ void __launch_bounds__(256) k_restart_basis(int64_t n, double* __rest
       Xs[kRestartRows * W + idx] = AQ[(rc + r) * ldq + k];
     }
     __syncthreads();
-    for (int o = t; o < 2 * rows * keep; o += 256) {
-      const int mat = o / (rows * keep), rem = o - mat * rows * keep;
-      const int r = rem / keep, c = rem - r * keep;
-      const double* x = Xs + mat * kRestartRows * W + r * W;
-      double a0 = 0.0, a1 = 0.0;
-      int k = 0;
-      for (; k + 1 < m; k += 2) {
-        a0 = fma(x[k], Ss[k * keep + c], a0);
-        a1 = fma(x[k + 1], Ss[(k + 1) * keep + c], a1);
+    // 2 rows x 4 columns per thread: six shared-memory loads per eight multiply-adds (one output per
+    // thread loads two operands per multiply-add and is bound by shared-memory wavefronts)
+    const int ncg = (keep + 3) / 4, nrg = (rows + 1) / 2;
+    for (int o = t; o < 2 * nrg * ncg; o += 256) {
+      const int mat = o / (nrg * ncg), rem = o - mat * nrg * ncg;
+      const int r = 2 * (rem / ncg), c = 4 * (rem - (rem / ncg) * ncg);
+      const double* x0 = Xs + mat * kRestartRows * W + r * W;
+      const double* x1 = x0 + (r + 1 < rows ? W : 0);
+      double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+      for (int k = 0; k < m; ++k) {
+        const double xa = x0[k], xb = x1[k];
+        const double* sk = Ss + k * keep + c;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double sv = c + u < keep ? sk[u] : 0.0;
+          acc[0][u] = fma(xa, sv, acc[0][u]);
+          acc[1][u] = fma(xb, sv, acc[1][u]);
+        }
       }
-      if (k < m) a0 = fma(x[k], Ss[k * keep + c], a0);
-      (mat ? AQ : Q)[(rc + r) * ldq + c] = a0 + a1;
+      double* dst = mat ? AQ : Q;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (c + u < keep) {
+          dst[(rc + r) * ldq + c + u] = acc[0][u];
+          if (r + 1 < rows) dst[(rc + r + 1) * ldq + c + u] = acc[1][u];
+        }
+      }
     }
     for (int o = t; o < 2 * rows * tq; o += 256) {
       const int mat = o / (rows * tq), rem = o - mat * rows * tq;
