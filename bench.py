@@ -374,6 +374,13 @@ def measure_workload(name: str, W: int, K: int, world: int, dev, peak: float, sa
         "bytes_per_pass": bytes_per_pass, "pass_ms": pass_ms, "passes_measured": int(pc.value),
         "share_of_step": (pass_ms * float(np.mean(passes)) / ms_per_step) if pass_ms else None,
     }
+    if w.kind != "sampled" and w.dtype == "f64" and pass_ms:
+        # the float64 pass against the FP64 tensor-core (DMMA) rate as well: 2 n^2 b flops per pass; 40 TFLOP/s
+        # is the nominal B200 figure (DMMA.8x8x4 measured at 16 cycles per SMSP: profiles/r02b_ncu_pass.md)
+        fl = 2.0 * w.n * w.n * w.block
+        roofline["fp64_tensor"] = {"flops_per_pass": fl, "achieved_tflops": fl / (pass_ms * 1e-3) / 1e12,
+                                   "peak_tflops": 40.0, "peak_source": "nominal",
+                                   "frac": fl / (pass_ms * 1e-3) / 1e12 / 40.0}
 
     # ---- e2e through the host-buffer entry point (pinned host V in, V_next out every step)
     Vh = torch.empty((w.n, w.r), dtype=torch.float64).pin_memory()
