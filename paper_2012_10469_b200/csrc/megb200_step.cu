@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
     }
   }
   stamp(st0, 3);
+  bool rr_cta = false;  // this CTA solved the Rayleigh-Ritz problem (its H write and epilogue are deferred)
   if (tree_reduce<NT, CL>(a.part1, a.part1 + (int64_t)G * kFusedStride, Hs, b * b, kFusedStride, a.sync + 32, &s_flag)) {
     stamp(a.stamps, 4);
     stamp(a.stamps, 5);
@@ -299,14 +300,11 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
       __syncthreads();
     }
     stamp(a.stamps, 6);
-    // the other CTAs need theta and S only; H (for a continued solve) and the step
-    // epilogue are written after the release, off the critical path
+    // the other CTAs need theta and S only; H (for a continued solve) and the step epilogue are
+    // written after this CTA's own Ritz rows are out (rr_cta below): the next operand pass waits for
+    // the Ritz rows of ALL CTAs, so anything this CTA does before them delays it
     publish(a.sync + kFusedFlags + 1, a.epoch);
-    for (int o = t; o < b * b; o += NT) {
-      const int ia = o / b, c = o - ia * b;
-      if (ia <= c) a.H[ia * a.ldh + c] = Hs[o];
-    }
-    if (a.epi && t < 32) step_epilogue_warp(thsh, a.nreq, a.n, a.eps_next, a.epi);
+    rr_cta = true;
     stamp(a.stamps, 7);
   } else {
     wait_published(a.sync + kFusedFlags + 1, a.epoch);
@@ -398,6 +396,15 @@ __global__ void __launch_bounds__(NT, 1) k_fused_first_pass(const FusedPassArgs 
     __syncthreads();
     if (t == 0) atomicAdd(a.rows_ctr, 1ull);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
+  if (rr_cta) {
+    // (Hs and the theta copy in thsh are untouched by phase 2; the epilogue lands in the pack before
+    // this CTA's ticket below, whose fence publishes it to the CTA that writes the pack out)
+    for (int o = t; o < b * b; o += NT) {
+      const int ia = o / b, cc = o - ia * b;
+      if (ia <= cc) a.H[ia * a.ldh + cc] = Hs[o];
+    }
+    if (a.epi && t < 32) step_epilogue_warp(thsh, a.nreq, a.n, a.eps_next, a.epi);
   }
   double* res2 = a.part2 + (int64_t)(G + (G + kGroup - 1) / kGroup) * kFusedStride;
   if (tree_reduce<NT, CL>(a.part2, a.part2 + (int64_t)G * kFusedStride, res2, pw, kFusedStride, a.sync + 64, &s_flag)) {
