@@ -12,7 +12,7 @@
 //      U- D- U-^T (twist at the smallest |gamma_k|, the MRRR "getvec" step), one
 //      thread per eigenvalue, O(m) each;
 //   4. S = Q Y by the stored reflectors, applied in reverse;
-//   5. one to three Newton-Schulz steps S <- S (3I - S^T S) / 2 (clustered
+//   5. one to six Newton-Schulz steps S <- S (3I - S^T S) / 2 (clustered
 //      eigenvalues leave the twisted vectors slightly non-orthogonal), row-wise in
 //      place;
 //   6. verification against the original H: every column residual
@@ -565,7 +565,9 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
   rr_mark(4);
   // ---- 5. Newton-Schulz: G = S^T S in A (reflectors no longer needed), S <- S (3I - G) / 2 by rows
   double delta = 0.0;
-  for (int it = 0; it < 3; ++it) {
+  // (up to six: delta is measured before each update and squares with it -- a start near 0.2 needs five;
+  // with three, cfg4's later steps failed the final delta < 1e-10 test on the stale 5e-6 and paid the 3 ms Jacobi)
+  for (int it = 0; it < 6; ++it) {
     double gm = 0.0;
     gemm_t4(Z, 1, m, Z, m, 1, nvec, nvec, m, [&](int i, int c, double g) {
       A[i * la + c] = g;
@@ -577,7 +579,14 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
     delta = 0.0;
     for (int k = 0; k < kNW; ++k) delta = fmax(delta, wp[k]);
     __syncthreads();
-    if (!(delta < 0.25)) return false;  // uniform: twisted vectors too far from orthogonal
+    if (!(delta < 0.25)) {  // uniform: twisted vectors too far from orthogonal
+      if (t == 0) {  // diagnostics: why the tridiagonal path gave up (megb200_debug_rr_ns slots 12-14)
+        g_rr_ns[12] = 1 + it;
+        g_rr_ns[13] = (unsigned long long)(delta * 1e6);
+        g_rr_ns[14] += 1;
+      }
+      return false;
+    }
     if (delta <= 1e-15) break;
     // M = (3I - G) / 2 in place, then S <- S M by rows: four rows per warp, in place
     for (int idx = t; idx < nvec * nvec; idx += kRT) {
@@ -627,7 +636,15 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
   double res = 0.0;
   for (int k = 0; k < kNW; ++k) res = fmax(res, wp[k]);
   const double hn = sqrt(fro2);
-  if (!(res <= 1e-12 * fmax(hn, 1e-300) && delta < 1e-10)) return false;
+  if (!(res <= 1e-12 * fmax(hn, 1e-300) && delta < 1e-10)) {
+    if (t == 0) {
+      g_rr_ns[12] = 10;
+      g_rr_ns[13] = (unsigned long long)(res / fmax(hn, 1e-300) * 1e18);
+      g_rr_ns[14] += 1;
+      g_rr_ns[11] = (unsigned long long)(delta * 1e18);
+    }
+    return false;
+  }
   rr_mark(6);
   for (int k = t; k < m; k += kRT) theta_g[k] = lam[k];
   for (int idx = t; idx < m * m; idx += kRT) Sout[idx] = (idx % m) < nvec ? Z[idx] : 0.0;
