@@ -846,7 +846,13 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
     double km = 1.0;
     for (int wv = 0; wv < kCT / 32; ++wv) km = fmin(km, Rinv_s[wv]);
     __syncthreads();
-    if (!(km >= 1e-11)) return false;  // uniform: every CTA reduced the same G and C
+    if (!(km >= 1e-11)) {  // uniform: every CTA reduced the same G and C
+      if (blockIdx.x == 0 && t == 0) {  // diagnostics: rejected rounds and why (megb200_debug_phase_ns 56-59)
+        g_phase_ns[56] += 1;
+        g_phase_ns[58] = (unsigned long long)(km * 1e18);
+      }
+      return false;
+    }
     PIPCLK(2)
     double pmin = 1.0;
     block_cholesky(Gs, q, thresh, chol_sm, Rrel_s, Rinv_s, mask_s, nullptr, nullptr, &pmin);
@@ -854,6 +860,13 @@ __global__ void __launch_bounds__(kCT, 1) k_coop_orth(int64_t n, const double* _
     PIPCLK(3)
     bool okc = km * pmin >= 1e-12;  // error of the round ~ eps / (kept share x smallest pivot) <= 1e-4
     for (int c = 0; c < q; ++c) okc = okc && !mask_s[c];
+    if (blockIdx.x == 0 && t == 0) {
+      if (okc) g_phase_ns[55] += 1;
+      else {
+        g_phase_ns[57] += 1;
+        g_phase_ns[59] = (unsigned long long)(km * pmin * 1e18);
+      }
+    }
     if (!okc) return false;  // uniform
     // W <- (W - Q C) R^-1: the projection into W2, then the triangular solve back into Ws
     const int nc4 = (q + 3) / 4;
