@@ -387,9 +387,14 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
   //      and the smallest are computed (the Ritz values a restart keeps, and the norm estimate).
   {
     const int neig = nvec < m ? nvec + 1 : m;
-    // (sixteen lanes / 14 rounds measured slower, 164 vs 116 us at m = 108: the Sturm recurrences
-    // share one SM's float64 pipe, so fewer evaluations beat fewer rounds)
-    multisect<kLanesPerEig, kBisectRounds>(d, e2, m, nvec, neig, sc[1], sc[2], pivmin, lam);
+    // (sixteen lanes / 14 rounds measured slower with 37-57 eigenvalues, 164 vs 116 us at m = 108: the
+    // Sturm recurrences share one SM's float64 pipe, so fewer evaluations beat fewer rounds.  With at
+    // most 16 wanted -- identity-basis solves keep r + 1 -- a whole warp per eigenvalue keeps the same
+    // number of threads busy and needs 12 rounds instead of 18)
+    if (neig * 32 <= kRT)
+      multisect<32, 12>(d, e2, m, nvec, neig, sc[1], sc[2], pivmin, lam);
+    else
+      multisect<kLanesPerEig, kBisectRounds>(d, e2, m, nvec, neig, sc[1], sc[2], pivmin, lam);
   }
   __syncthreads();
   // Ritz values not computed (between the top nvec and the smallest) are reported as the smallest
