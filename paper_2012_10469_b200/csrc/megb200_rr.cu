@@ -401,6 +401,7 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
   for (int k = nvec + t; k < m - 1; k += kRT) lam[k] = lam[m - 1];
   __syncthreads();
   rr_mark(2);
+  // (reciprocals by the MUFU seed + two Newton steps, fast_rcp: the chains below are one division per row)
   // ---- 3. eigenvectors of T by twisted factorisations (thread k <-> eigenvalue k, column k of Z)
   for (int k = t; k < nvec; k += kRT) {
     const double lk = lam[k];
@@ -409,7 +410,7 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
     for (int i = 0; i < m - 1; ++i) {
       if (fabs(dp) < pivmin) dp = -pivmin;
       Z[i * m + k] = dp;
-      dp = (d[i + 1] - lk) - e2[i] / dp;
+      dp = (d[i + 1] - lk) - e2[i] * fast_rcp(dp);
     }
     if (fabs(dp) < pivmin) dp = -pivmin;
     Z[(m - 1) * m + k] = dp;
@@ -419,20 +420,22 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
     int r = m - 1;
     double gbest = fabs(Z[(m - 1) * m + k]);
     for (int i = m - 2; i >= 0; --i) {
-      const double g = Z[i * m + k] - e2[i] / dm;
+      const double rdm = fast_rcp(dm);
+      const double g = Z[i * m + k] - e2[i] * rdm;
       if (fabs(g) < gbest) {
         gbest = fabs(g);
         r = i;
       }
-      dm = (d[i] - lk) - e2[i] / dm;
+      dm = (d[i] - lk) - e2[i] * rdm;
       if (fabs(dm) < pivmin) dm = -pivmin;
     }
     // U-_i = e_i / D-_{i+1} for i >= r, stored over D+_i (i >= r no longer needed)
     dm = d[m - 1] - lk;
     if (fabs(dm) < pivmin) dm = -pivmin;
     for (int i = m - 2; i >= r; --i) {
-      Z[i * m + k] = e[i] / dm;
-      dm = (d[i] - lk) - e2[i] / dm;
+      const double rdm = fast_rcp(dm);
+      Z[i * m + k] = e[i] * rdm;
+      dm = (d[i] - lk) - e2[i] * rdm;
       if (fabs(dm) < pivmin) dm = -pivmin;
     }
     // z_r = 1; upward z_{i+1} = -U-_i z_i; downward z_i = -(e_i / D+_i) z_{i+1}
@@ -449,7 +452,7 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
     }
     cur = 1.0;
     for (int i = r - 1; i >= 0; --i) {
-      const double nxt = -(e[i] / Z[i * m + k]) * cur;
+      const double nxt = -(e[i] * fast_rcp(Z[i * m + k])) * cur;
       Z[i * m + k] = nxt;
       nrm = fma(nxt, nxt, nrm);
       cur = nxt;
