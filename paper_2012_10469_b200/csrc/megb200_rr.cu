@@ -266,56 +266,52 @@ __device__ bool rr_tridiag(const double* __restrict__ Hg, int64_t ldh, int m, in
       __syncthreads();
       continue;
     }
-    // p = tau A22 v and the shares of p^T v: sixteen threads per row -- a warp reads two rows of 16
-    // consecutive doubles (two conflict-free wavefronts) -- with the thread's seven entries of v held
-    // in registers for all of its rows (the loads of the row entries are the only shared-memory
-    // traffic: this phase and the update are bound by shared-memory wavefronts, not by latency)
-    constexpr int kTPR = 16, kEnt = 7;  // threads per row, entries per thread (16 * 7 = 112 >= m)
+    // p = tau A22 v: thread (column i = t mod 128, quarter g = t / 128) runs down its quarter of the rows
+    // of column i -- A22 is symmetric, and consecutive lanes read consecutive doubles of a row
+    // (conflict-free) with v as a broadcast -- no warp reductions: the four quarters meet in shared
+    // memory (the sixteen-threads-per-row form spent 26 shuffles per warp and column)
+    static_assert(kRT == 512, "the tridiagonalisation's matvec maps 4 x 128 threads");
+    constexpr int kTPR = 16, kEnt = 7;  // update: threads per row, entries per thread (16 * 7 = 112 >= m)
     const int k0 = t & (kTPR - 1);
+    double* red4 = sc + 8;  // 4 x 128 (the back-transform's W1 buffer, idle here)
+    {
+      const int i = t & 127, g = t >> 7;
+      const int Lq = (L + 3) >> 2, kb = g * Lq, ke = min(L, kb + Lq);
+      double a0 = 0.0, a1 = 0.0;
+      if (i < L) {
+        const double* col = A + (j + 1) * la + (j + 1) + i;
+        int k = kb;
+#pragma unroll 4
+        for (; k + 1 < ke; k += 2) {
+          a0 = fma(col[k * la], v[k], a0);
+          a1 = fma(col[(k + 1) * la], v[k + 1], a1);
+        }
+        if (k < ke) a0 = fma(col[k * la], v[k], a0);
+      }
+      red4[t] = a0 + a1;
+    }
+    __syncthreads();
+    if (t < 128) {
+      double pvs = 0.0;
+      if (t < L) {
+        const double pi = tj * ((red4[t] + red4[128 + t]) + (red4[256 + t] + red4[384 + t]));
+        p[t] = pi;
+        pvs = pi * v[t];
+      }
+      pvs = wsum(pvs);
+      if (lane == 0) wp[w] = pvs;
+    }
+    RRCLK(3)
+    __syncthreads();
+    RRCLK(4)
     double vk[kEnt];
 #pragma unroll
     for (int it = 0; it < kEnt; ++it) {
       const int k = k0 + kTPR * it;
       vk[it] = k < L ? v[k] : 0.0;
     }
-    double pvs = 0.0;
-    constexpr int kSweeps = (112 * kTPR + kRT - 1) / kRT;  // row sweeps, unrolled: their loads and shuffles overlap
-#pragma unroll
-    for (int sw = 0; sw < kSweeps; ++sw) {
-      const int rr = sw * (kRT / kTPR) + t / kTPR;
-      if (sw * (kRT / kTPR) >= L) break;  // uniform
-      double acc = 0.0;
-      if (rr < L) {
-        const double* row = A + (j + 1 + rr) * la + (j + 1);
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-        for (int it = 0; it < kEnt; ++it) {
-          const int k = k0 + kTPR * it;
-          const double x = k < L ? row[k] : 0.0;
-          if (it & 1) a1 = fma(x, vk[it], a1);
-          else a0 = fma(x, vk[it], a0);
-        }
-        acc = a0 + a1;
-      }
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 8);
-      if (rr < L && k0 == 0) {
-        const double pi = tj * acc;
-        p[rr] = pi;
-        pvs = fma(pi, v[rr], pvs);
-      }
-    }
-    pvs += __shfl_xor_sync(0xffffffffu, pvs, 16);
-    if (lane == 0) wp[w] = pvs;
-    RRCLK(3)
-    __syncthreads();
-    RRCLK(4)
-    double K = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < kNW; ++k) K += wp[k];
-    K *= 0.5 * tj;
+    constexpr int kSweeps = (112 * kTPR + kRT - 1) / kRT;
+    const double K = 0.5 * tj * ((wp[0] + wp[1]) + (wp[2] + wp[3]));
     RRCLK(5)
     // A22 -= v w^T + w v^T with w = p - K v: sixteen threads per row, the thread's entries of v and w
     // in registers (one load and one store per matrix entry)
